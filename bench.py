@@ -1,0 +1,398 @@
+"""Benchmark: BASELINE config 5a -- batched incremental-SVD streams on B200.
+
+Workload (BASELINE.json configs[4] part a, the config the headline metric
+"iSVD updates/sec (k=32)" is quoted on): 4096 independent streams, each a
+1024 x 256 rank-32 Gaussian product plus N(0, 0.05^2) noise, k = 32; 1024
+events per stream alternating row append and rank-1 update (delta ~
+N(0, 0.01)).  One step = one tick = one event applied to every stream.
+Streams are sharded across ranks (strong scaling: the 4096 streams are split
+over N GPUs, no data-path collective).
+
+`value`   updates/s with inputs resident in HBM (device-event timing on the
+          engine's stream, max over ranks).
+`e2e`     the same through the public API with pinned HOST event buffers:
+          host validation + H2D copy + kernels + D2H read of the step's
+          result (per-stream sq_norm, residual and input norm) every step.
+`roofline` dominant kernel (the factor rotation K3/K4): algorithmic bytes /
+          its measured average duration (CUDA events on the engine stream).
+
+`--impl reference` times the reference algorithm's CPU implementation (the
+numpy restatement in oracle/, all host cores) on a bounded sample of the
+same workload, printing the same JSON line with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+M0, N0, RANK, K = 1024, 256, 32, 32
+TOTAL_STREAMS = 4096
+EVENTS = 1024
+METRIC = "iSVD updates/sec (k=32)"
+UNIT = "updates/s"
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------ reference arm
+def _ref_worker(args):
+    """One CPU worker: its streams through the oracle engine (numpy/LAPACK),
+    single BLAS thread; returns (updates, seconds excluding init)."""
+    seed, streams, n_events = args
+    os.environ["OMP_NUM_THREADS"] = "1"
+    from oracle import OracleEngine
+    from paper_2605_24514_b200 import workloads
+
+    engines, evs = [], []
+    for b in streams:
+        a0, ev = workloads.cfg5a_stream(seed, b, n_events=n_events)
+        engines.append(OracleEngine(a0, K))
+        evs.append(ev)
+    t0 = time.perf_counter()
+    for t in range(n_events):
+        for e, ev in zip(engines, evs):
+            x = ev[t]
+            if x[0] == "row":
+                e.row_append(x[1])
+            else:
+                e.rank_one_update(x[1], x[2], x[3])
+    return len(streams) * n_events, time.perf_counter() - t0
+
+
+def cpu_reference(n_streams: int, n_events: int, seed: int = 0):
+    """Aggregate updates/s of the CPU reference implementation over all host
+    cores (multiprocessing, one BLAS thread per worker)."""
+    import multiprocessing as mp
+
+    cores = len(os.sched_getaffinity(0))
+    workers = min(cores, n_streams)
+    chunks = [list(range(w, n_streams, workers)) for w in range(workers)]
+    env_before = os.environ.get("OMP_NUM_THREADS")
+    os.environ["OMP_NUM_THREADS"] = "1"
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(workers) as pool:
+        res = pool.map(_ref_worker, [(seed, c, n_events) for c in chunks])
+    if env_before is None:
+        os.environ.pop("OMP_NUM_THREADS", None)
+    else:
+        os.environ["OMP_NUM_THREADS"] = env_before
+    updates = sum(r[0] for r in res)
+    secs = max(r[1] for r in res)
+    return updates / secs, workers, updates, secs
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    # bounded sample: 64 streams; each "step" = one event on every sampled stream
+    n_streams = 64
+    steps = max(1, args.steps)
+    value, cores, updates, secs = cpu_reference(n_streams, steps + args.warmup)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * secs / (steps + args.warmup), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg5a_batched_streams", "streams_sampled": n_streams,
+                   "m0": M0, "n": N0, "k": K, "events_per_stream": steps + args.warmup},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{n_streams} cfg5a streams x {steps + args.warmup} events "
+                                   f"(oracle/ numpy restatement, LAPACK core SVD, 1 BLAS thread "
+                                   f"per worker, init excluded)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+class ClockSampler:
+    def __init__(self, path):
+        self.path = path
+        self.proc = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv",
+                                          "-lms", "100"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+            self.f.close()
+
+    def summary(self, gpu_index=0):
+        try:
+            lines = Path(self.path).read_text().strip().splitlines()[1:]
+        except Exception:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9 or parts[0] != str(gpu_index):
+                continue
+            try:
+                sm.append(float(parts[1].split()[0]))
+                mx = float(parts[2].split()[0])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_inputs(torch, dev, streams, seed=0, n_events=EVENTS):
+    """Seeded device-side synthetic inputs for the local streams (torch
+    Philox per stream id, so shards are independent of the world size)."""
+    B = len(streams)
+    a0 = torch.empty((B, M0, N0), dtype=torch.float64, device=dev)
+    ys = torch.empty((B, N0, RANK), dtype=torch.float64, device=dev)
+    g = torch.Generator(device=dev)
+    for i, b in enumerate(streams):
+        g.manual_seed(1_000_003 * seed + b)
+        x = torch.randn((M0, RANK), dtype=torch.float64, device=dev, generator=g)
+        y = torch.randn((N0, RANK), dtype=torch.float64, device=dev, generator=g)
+        a0[i] = x @ y.T + 0.05 * torch.randn((M0, N0), dtype=torch.float64, device=dev, generator=g)
+        ys[i] = y
+    g.manual_seed(7_777_777 + seed * 131 + streams[0])
+    nrow = (n_events + 1) // 2
+    nr1 = n_events // 2
+    rows = torch.empty((nrow, B, N0), dtype=torch.float64, device=dev)
+    for t in range(nrow):
+        l = torch.randn((B, RANK, 1), dtype=torch.float64, device=dev, generator=g)
+        rows[t] = torch.bmm(ys, l).squeeze(-1) + 0.05 * torch.randn((B, N0), dtype=torch.float64,
+                                                                    device=dev, generator=g)
+    ii = torch.empty((nr1, B), dtype=torch.int64, device=dev)
+    for t in range(nr1):
+        m_now = M0 + t + 1  # rows appended before rank-1 tick 2t+1
+        ii[t] = torch.randint(0, m_now, (B,), device=dev, generator=g)
+    jj = torch.randint(0, N0, (nr1, B), device=dev, generator=g)
+    dd = 0.01 * torch.randn((nr1, B), dtype=torch.float64, device=dev, generator=g)
+    return a0, rows, ii, jj, dd
+
+
+def rotation_bytes(B, m, n, r, keep, row_tick):
+    """Algorithmic HBM bytes of one rotation launch (K3+K4 over B streams):
+    U read m x r + written (m [+1]) x keep, V read n x r + written n x keep,
+    plus the injected residual z (n) on row appends."""
+    if row_tick:
+        return 8 * B * (m * r + (m + 1) * keep + n * r + n * keep + n)
+    return 8 * B * (m * r + m * keep + n * r + n * keep)
+
+
+def tick_bytes(B, m, n, w, row_tick):
+    """SURVEY.md 8(d) algorithmic bytes per update (whole tick)."""
+    if row_tick:
+        return 8 * B * (2 * m * w + 2 * n * w + 2 * n)
+    return 8 * B * (2 * m * w + 2 * n * w + 2 * w + 2)
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2605_24514_b200 import BatchedSvdEngine, _lib
+
+    total = args.streams
+    per = total // world
+    streams = list(range(rank * per, (rank + 1) * per))
+    B = len(streams)
+    steps, warm = args.steps, args.warmup
+    n_events = max(steps, warm)
+    a0, rows, ii, jj, dd = make_inputs(torch, dev, streams, n_events=n_events)
+    m_cap = M0 + (n_events + 1) // 2 + 1
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def run_ticks(eng, nt, host=None):
+        """nt ticks; device-resident inputs unless host=(rows, ii, jj, dd)."""
+        results = []
+        for t in range(nt):
+            if t % 2 == 0:
+                if host is None:
+                    eng.row_append(rows[t // 2])
+                else:
+                    eng.row_append(host[0][t // 2])
+            else:
+                if host is None:
+                    eng.rank_one_update(ii[t // 2], jj[t // 2], dd[t // 2])
+                else:
+                    eng.rank_one_update(host[1][t // 2], host[2][t // 2], host[3][t // 2])
+            if host is not None:
+                results.append(eng.scalars())  # D2H read of the step's result
+        return results
+
+    # ---------------- device-resident timing (value)
+    eng = BatchedSvdEngine(a0, K, m_cap=m_cap, k_cap=K)
+    run_ticks(eng, warm)
+    del eng
+    torch.cuda.empty_cache()
+    eng = BatchedSvdEngine(a0, K, m_cap=m_cap, k_cap=K)
+    stream = torch.cuda.ExternalStream(eng.cuda_stream, device=dev)
+    lib = _lib.load()
+    _lib.check(lib.isvd_engine_set_timing(eng._h.h, 1))
+    barrier()
+    l0 = _lib.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(str(ROOT / "gpurun_out" / f"clocks_r{rank}.csv")) as clk:
+        e0.record(stream)
+        run_ticks(eng, steps)
+        e1.record(stream)
+        barrier()
+    launches = _lib.launch_count() - l0
+    dev_ms = e0.elapsed_time(e1)
+    phase = np.zeros(4)
+    nt = np.zeros(1, dtype=np.int64)
+    _lib.check(lib.isvd_engine_phase_times(eng._h.h, _lib.dptr(phase), nt.ctypes.data_as(
+        __import__("ctypes").POINTER(__import__("ctypes").c_int64))))
+    # algorithmic bytes of the timed ticks (dominant kernel = rotation)
+    rot_bytes = 0
+    all_bytes = 0
+    m = M0
+    for t in range(steps):
+        row = t % 2 == 0
+        rot_bytes += rotation_bytes(B, m, N0, K, K, row)
+        all_bytes += tick_bytes(B, m, N0, K, row)
+        if row:
+            m += 1
+    t_max = dev_ms
+    if world > 1:
+        tt = torch.tensor([dev_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    value = total * steps / (t_max / 1e3)
+    clock = clk.summary(local)
+    # sanity: spectrum of stream 0 is finite and sorted
+    f0 = eng.factors(0)
+    assert np.all(np.isfinite(f0.s)) and np.all(np.diff(f0.s) <= 0)
+    del eng
+    torch.cuda.empty_cache()
+
+    # ---------------- end-to-end through the public API with host buffers
+    e2e_steps = min(steps, args.e2e_steps)
+    nrow = (e2e_steps + 1) // 2
+    nr1 = e2e_steps // 2
+    h_rows = torch.empty((nrow, B, N0), dtype=torch.float64, pin_memory=True)
+    h_rows.copy_(rows[:nrow])
+    h_ii = torch.empty((nr1, B), dtype=torch.int64, pin_memory=True)
+    h_jj = torch.empty((nr1, B), dtype=torch.int64, pin_memory=True)
+    h_dd = torch.empty((nr1, B), dtype=torch.float64, pin_memory=True)
+    h_ii.copy_(ii[:nr1]); h_jj.copy_(jj[:nr1]); h_dd.copy_(dd[:nr1])
+    host = (h_rows.numpy(), h_ii.numpy(), h_jj.numpy(), h_dd.numpy())
+    eng = BatchedSvdEngine(a0, K, m_cap=m_cap, k_cap=K)
+    barrier()
+    t0 = time.perf_counter()
+    run_ticks(eng, e2e_steps, host=host)
+    barrier()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        tt = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    e2e_value = total * e2e_steps / e2e_s
+    h2d = (nrow * B * N0 * 8 + nr1 * B * 24) / max(1, e2e_steps)
+    d2h = 3 * B * 8
+    del eng
+
+    if rank == 0:
+        peak, peak_kind = _peaks()
+        rot_ms = phase[2] / max(1, int(nt[0]))
+        achieved = rot_bytes / max(1, steps) / (rot_ms / 1e3) / 1e9
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+            "warmup": warm, "ms_per_step": t_max / steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "cfg5a_batched_streams", "streams": total,
+                       "streams_per_gpu": B, "m0": M0, "n": N0, "rank": RANK, "k": K,
+                       "events": steps, "event_mix": "alternating row append / rank-1",
+                       "l2": "inputs larger than L2 (state ~2 GB/GPU touched per step)",
+                       "parallelism": f"streams sharded over {world} GPU(s)"},
+            "clocks": clock,
+            "gpu_launches": int(launches),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "steps": e2e_steps},
+            "roofline": {"kernel": "rotate_kernel (K3/K4, FP64 DMMA)", "bound": "hbm",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_kind": peak_kind, "traffic": None,
+                         "bytes_per_launch": rot_bytes / max(1, steps)},
+            "phase_ms_per_step": {"project": phase[0] / max(1, nt[0]),
+                                  "core_svd": phase[1] / max(1, nt[0]),
+                                  "rotate": phase[2] / max(1, nt[0]),
+                                  "install": phase[3] / max(1, nt[0])},
+            "tick_effective_gbs": all_bytes / (t_max / 1e3) / 1e9,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            v, cores, updates, secs = cpu_reference(args.cpu_streams, args.cpu_events)
+            line["cpu_baseline"] = {
+                "value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                "sample": f"{args.cpu_streams} cfg5a streams x {args.cpu_events} events on "
+                          f"{cores} processes (oracle/ numpy restatement, 1 BLAS thread each, "
+                          f"init excluded)"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=EVENTS)
+    ap.add_argument("--warmup", type=int, default=8)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--streams", type=int, default=TOTAL_STREAMS)
+    ap.add_argument("--e2e-steps", type=int, default=128)
+    ap.add_argument("--cpu-streams", type=int, default=64)
+    ap.add_argument("--cpu-events", type=int, default=128)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    (ROOT / "gpurun_out").mkdir(exist_ok=True)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

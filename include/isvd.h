@@ -1,0 +1,175 @@
+/*
+ * isvd.h -- C ABI of libisvd, the B200-native incremental-SVD engine.
+ *
+ * This is the drop-in boundary for the reference `svdstream` per-tick update
+ * path (arxiv/paper_2605_24514).  All citations are relative to
+ * /root/reference/pkg/src/svdstream/.
+ *
+ * Two layers, mirroring the reference's two boundaries:
+ *
+ *  1. Functional kernel entry points -- the `svdstream.backend` contract
+ *     (backend.py:54-63): core_svd, row_append, rank_one.  Inputs are read,
+ *     outputs are written to caller buffers; nothing is retained.
+ *
+ *  2. An engine handle -- the `SvdEngine` state machine (engine.py:73-217),
+ *     holding B independent streams of identical shape ("batch") whose
+ *     factors, tracked matrix and squared norm live in HBM.  B = 1 is the
+ *     reference's single engine; B > 1 is the batched-stream workload.
+ *
+ * Conventions
+ *  - Every entry point returns 0 on success, nonzero on failure; the message
+ *    is available from isvd_last_error() (thread-local).  Argument errors the
+ *    reference raises as ValueError return ISVD_EINVAL *before* any state is
+ *    touched, so a rejected event leaves the engine unchanged
+ *    (tests/test_engine.py:88-95).
+ *  - Matrices are row-major float64.  `on_device` flags say whether a
+ *    pointer is a device pointer (1) or host memory (0).
+ *  - `stream` arguments are cudaStream_t passed as void*; 0 = legacy stream.
+ *  - No CPU fallback exists: without a CUDA device every compute call fails
+ *    with ISVD_ENODEV.
+ */
+#ifndef ISVD_H_
+#define ISVD_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ISVD_OK 0
+#define ISVD_EINVAL 1   /* invalid argument (reference: ValueError)        */
+#define ISVD_ENODEV 2   /* no CUDA device / CUDA runtime failure            */
+#define ISVD_ENOMEM 3   /* device allocation failed                         */
+#define ISVD_ESTATE 4   /* operation not valid in the current engine state  */
+
+/* Library / error reporting ------------------------------------------------ */
+const char* isvd_last_error(void);
+int isvd_version(void);
+/* Number of kernel launches issued by this process so far (evidence counter
+ * reported by bench.py as `gpu_launches`). */
+int64_t isvd_launch_count(void);
+
+/* 1. Functional kernels (backend.py:54-63) ---------------------------------- */
+
+/* core_svd: batched full SVD of `batch` square s x s cores (row-major,
+ * contiguous, stride s*s).  One-sided Jacobi + stable descending sort + snap
+ * below 1e-12*s[0] + dead-column completion, as _kernels.pyx:82-109.
+ * Outputs u (s x s), sv (s), vt (s x s) per core.  Device pointers. */
+int isvd_core_svd(int batch, int s, const double* core, double* u, double* sv,
+                  double* vt, void* stream);
+
+/* row_append (_kernels_py.py:22-49, _kernels.pyx:112-187): u (m x r),
+ * s (r), vt (r x n), x (n) -> u_out ((m+1) x keep), s_out (keep),
+ * vt_out (keep x n), *rho.  Host pointers; synchronous. */
+int isvd_row_append(int m, int r, int n, const double* u, const double* s,
+                    const double* vt, const double* x, double tol, int keep,
+                    double* u_out, double* s_out, double* vt_out, double* rho);
+
+/* rank_one (_kernels_py.py:52-58, _kernels.pyx:190-237): projection rule
+ * K = diag(s) + delta U[i,:]^T Vt[:,j]^T.  Host pointers; synchronous. */
+int isvd_rank_one(int m, int r, int n, const double* u, const double* s,
+                  const double* vt, int64_t i, int64_t j, double delta, int keep,
+                  double* u_out, double* s_out, double* vt_out);
+
+/* 2. Engine handle (engine.py:73-217) --------------------------------------- */
+
+typedef struct isvd_engine isvd_engine;
+
+/* Create B streams of shape m x n with work rank k (engine.py:76-94).
+ * Capacities (rows, cols, rank) are hints; the engine grows by doubling.
+ * Returns ISVD_EINVAL for k < 1, tol <= 0, empty shape. */
+int isvd_engine_create(isvd_engine** out, int batch, int m, int n, int k,
+                       double tol, int reortho_guard, int m_cap, int n_cap,
+                       int k_cap, void* stream);
+int isvd_engine_destroy(isvd_engine* e);
+
+/* Initialise from a0 (B x m x n, row-major per stream): copies the tracked
+ * matrix, N0 = sum a0^2, factors = truncated_svd(a0, k) on the device
+ * (engine.py:87-89, linalg.py:84-109).  Non-finite entries -> ISVD_EINVAL. */
+int isvd_engine_init(isvd_engine* e, const double* a0, int on_device);
+
+/* Events.  x: B x n (row append, engine.py:117-129); y: B x m (column
+ * append, engine.py:131-147); i, j, delta: B each (rank-1 update,
+ * engine.py:149-167).  Host inputs are validated (finite, in bounds) before
+ * any device work; device inputs are trusted. */
+int isvd_engine_row_append(isvd_engine* e, const double* x, int on_device);
+int isvd_engine_col_append(isvd_engine* e, const double* y, int on_device);
+int isvd_engine_rank_one(isvd_engine* e, const int64_t* i, const int64_t* j,
+                         const double* delta, int on_device);
+
+/* Maintenance: refresh (engine.py:171-176), set_reference (:178-180),
+ * set_rank (:182-198). */
+int isvd_engine_refresh(isvd_engine* e, int store_reference);
+int isvd_engine_set_reference(isvd_engine* e);
+int isvd_engine_set_rank(isvd_engine* e, int k_new);
+
+/* Shape / scalar state. */
+int isvd_engine_shape(const isvd_engine* e, int* batch, int* m, int* n,
+                      int* rank, int* work_rank, int64_t* step);
+int isvd_engine_has_reference(const isvd_engine* e, int* has_ref, int* ref_m,
+                              int* ref_r);
+
+/* Host copies (synchronous).  Factors are returned in canonical sign form
+ * (linalg.py:63-75).  b = stream index.  u: m x r, s: r, v: n x r (V, i.e.
+ * the transpose of the reference's vt; the host shim exposes vt = v.T). */
+int isvd_engine_get_factors(isvd_engine* e, int b, double* u, double* s, double* v);
+int isvd_engine_get_tracked(isvd_engine* e, int b, double* a);
+int isvd_engine_get_reference(isvd_engine* e, int b, double* ref);
+/* sq_norm: B values; last_residual / last_input_norm: B values each. */
+int isvd_engine_get_scalars(isvd_engine* e, double* sq_norm, double* last_residual,
+                            double* last_input_norm);
+/* Overwrite the factors / reference of stream b from host memory (test and
+ * checkpoint hook; the reference tests mutate factors in place). */
+int isvd_engine_set_factors(isvd_engine* e, int b, int r, const double* u,
+                            const double* s, const double* v);
+int isvd_engine_put_reference(isvd_engine* e, int b, int ref_m, int ref_r,
+                              const double* ref);
+
+/* Device views (no copy).  Pointers stay valid until the next event that
+ * grows a capacity.  Leading dimensions are in elements.  U_dev and V_dev
+ * hold stream b at offset b*stride.  NOTE: signs are lazy -- call
+ * isvd_engine_canonicalize() first when the canonical form is required. */
+int isvd_engine_device_views(isvd_engine* e, double** u, int64_t* u_stride, int* ldu,
+                             double** v, int64_t* v_stride, int* ldv, double** s,
+                             int* lds, double** a, int64_t* a_stride, int* lda);
+int isvd_engine_canonicalize(isvd_engine* e);
+/* The cudaStream_t (as void*) every launch of this engine goes to. */
+void* isvd_engine_stream(isvd_engine* e);
+int isvd_engine_synchronize(isvd_engine* e);
+/* Per-phase device timing (CUDA events on the engine stream around each
+ * phase of every event): phase 0 = projection / rank-1 gather (K1/K6),
+ * 1 = core SVD (K2), 2 = factor rotation (K3/K4), 3 = install.  phase_times
+ * returns the summed milliseconds of the ticks recorded since the last call
+ * and resets the record. */
+int isvd_engine_set_timing(isvd_engine* e, int on);
+int isvd_engine_phase_times(isvd_engine* e, double* ms4, int64_t* ticks);
+
+/* 3. Metrics (metrics.py:56-145, linalg.py:126-153) ------------------------- */
+
+/* Per-stream frob_error = ||A - U diag(s) Vt||_F without materialising the
+ * product (metrics.py:74-76).  out: B doubles (host). */
+int isvd_engine_frob_error(isvd_engine* e, double* out);
+/* Orthonormality defects ||U^T U - I||_F and ||V^T V - I||_F (linalg.py:126-130). */
+int isvd_engine_ortho_defect(isvd_engine* e, double* du, double* dv);
+/* Largest principal angle arccos(sigma_min(U^T Q)) against the stored
+ * reference (which = 0) or an explicit basis q (B x m x r, host or device;
+ * which = 1), linalg.py:133-153.  Returns -1 in out[b] when undefined
+ * (no reference / shape mismatch -> reference returns None).  Raises
+ * ISVD_EINVAL when either basis has defect > 1e-6 (linalg.py:148-150). */
+int isvd_engine_angle(isvd_engine* e, int which, const double* q, int q_cols,
+                      int on_device, double* out);
+
+/* Dense thin SVD of B matrices (m x n each) on the device, in canonical
+ * form (linalg.py:84-92).  Outputs: s (B x min(m,n)); u (B x m x w) and
+ * vt (B x w x n) for the leading w = min(w_keep, min(m,n)) triplets; u/vt
+ * may be NULL.  All pointers host; synchronous.  Used by compute_oracle. */
+int isvd_dense_svd(int batch, int m, int n, const double* a, int w_keep, double* s,
+                   double* u, double* vt);
+/* Same, from the engine's tracked matrices (no host copy of A). */
+int isvd_engine_oracle(isvd_engine* e, int w_keep, double* s, double* u);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ISVD_H_ */

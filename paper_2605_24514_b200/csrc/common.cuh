@@ -1,0 +1,80 @@
+// Shared device helpers for libisvd (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+
+namespace isvd {
+
+// Relative snap cutoff (linalg.py:18, _kernels.pyx:15).
+constexpr double kZeroSvRtol = 1e-12;
+// Jacobi orthogonality target and sweep cap (_kernels.pyx:17-19).
+constexpr double kOrthoEps = 1e-14;
+constexpr int kMaxSweeps = 64;
+
+void set_error(const std::string& msg);
+void count_launch(int n = 1);
+
+#define ISVD_CUDA(call)                                                        \
+  do {                                                                         \
+    cudaError_t _e = (call);                                                   \
+    if (_e != cudaSuccess) {                                                   \
+      ::isvd::set_error(std::string(#call) + ": " + cudaGetErrorString(_e));   \
+      return ISVD_ENODEV;                                                      \
+    }                                                                          \
+  } while (0)
+
+#define ISVD_LAUNCHED()                                                        \
+  do {                                                                         \
+    ::isvd::count_launch();                                                    \
+    cudaError_t _e = cudaGetLastError();                                       \
+    if (_e != cudaSuccess) {                                                   \
+      ::isvd::set_error(std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+      return ISVD_ENODEV;                                                      \
+    }                                                                          \
+  } while (0)
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Block-wide sum; `red` must hold >= 32 doubles of shared memory.  Result is
+// returned to every thread.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = (threadIdx.x < nw) ? red[threadIdx.x] : 0.0;
+  if (warp == 0) t = warp_sum(t);
+  if (threadIdx.x == 0) red[0] = t;
+  __syncthreads();
+  double r = red[0];
+  __syncthreads();
+  return r;
+}
+
+// D(8x8) += A(8x4, row) * B(4x8, col), FP64 tensor path (DMMA.8x8x4).
+// Fragment layout (verified on B200, profiles/r01_fp64_peaks.txt):
+//   a = A[lane>>2][lane&3], b = B[lane&3][lane>>2],
+//   d0,d1 = D[lane>>2][2*(lane&3) + {0,1}].
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+inline int round_up(int a, int b) { return (a + b - 1) / b * b; }
+
+}  // namespace isvd

@@ -1,0 +1,21 @@
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace isvd {
+
+constexpr int kCoreMaxS = 160;   // largest core: k_max + 1 (k <= 159)
+constexpr int kSmemMaxS = 112;   // G and V both in shared memory up to here
+
+size_t core_svd_smem_bytes(int s, bool v_in_smem);
+
+// Batched core SVD.  core[b] is s x s row-major at core + b*core_stride with
+// row pitch ldcore.  Outputs uk[b], vk[b] (row-major s x s, pitch ldo, the
+// columns are the singular vectors), sv[b] (s values).  `active` (optional)
+// skips streams whose flag is 0.  vscratch: batch * s * (s|1) doubles, needed
+// when s > kSmemMaxS.
+int launch_core_svd(int batch, int s, const double* core, int64_t core_stride, int ldcore,
+                    double* uk, double* vk, int64_t out_stride, int ldo, double* sv,
+                    int64_t sv_stride, double* vscratch, const int* active, cudaStream_t st);
+
+}  // namespace isvd

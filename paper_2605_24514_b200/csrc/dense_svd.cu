@@ -1,0 +1,360 @@
+// K7 -- dense thin SVD on the device (init, refresh, oracle).
+//
+// Reference semantics: linalg.py:84-109 (np.linalg.svd -> LAPACK gesdd,
+// snapped below 1e-12 s0, sign-canonical), used by SvdEngine.__init__
+// (engine.py:89), refresh (engine.py:173) and compute_oracle (metrics.py:56-64).
+//
+// Algorithm: blocked one-sided Jacobi (Hestenes) on the columns of
+// X = A (m >= n) or X = A^T (m < n).  Columns are grouped into blocks of 16;
+// a round-robin tournament pairs blocks; for each block pair the 32 x 32 Gram
+// matrix is formed on the FP64 tensor path (DMMA.8x8x4), diagonalised by a
+// parallel two-sided Jacobi in shared memory (same rotation formulas as
+// _kernels.pyx:38-44), and the resulting 32 x 32 rotation is applied to the
+// 32 long columns and to the accumulated right rotation, again with DMMA.
+// Convergence: a sweep in which no block pair's fresh Gram has an
+// off-diagonal above tol * sqrt(M_pp M_qq).  sigma = column norms, so the
+// result has one-sided-Jacobi (high relative) accuracy.
+#include <algorithm>
+#include <vector>
+#include "common.cuh"
+#include "dense_svd.cuh"
+#include "../../include/isvd.h"
+
+namespace isvd {
+
+namespace {
+
+constexpr int BW = 16;
+constexpr int PW = 2 * BW;
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ int tslot(int j, int round, int ne) {
+  return j == 0 ? 0 : 1 + (j - 1 + round) % (ne - 1);
+}
+
+__global__ void dsvd_prep_kernel(int m, int n, int ldx, int ncp, const double* __restrict__ a,
+                                 int64_t a_stride, int lda, double* __restrict__ X,
+                                 int64_t x_stride, double* __restrict__ Jm, int64_t j_stride) {
+  const int b = blockIdx.y;
+  const double* ab = a + b * a_stride;
+  double* xb = X + b * x_stride;
+  double* jb = Jm + b * j_stride;
+  const bool tall = m >= n;
+  const int64_t total = (int64_t)ncp * ldx;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int j = (int)(idx / ldx), i = (int)(idx % ldx);
+    double v = 0.0;
+    if (tall) {
+      if (i < m && j < n) v = ab[(int64_t)i * lda + j];
+    } else {
+      if (j < m && i < n) v = ab[(int64_t)j * lda + i];
+    }
+    xb[idx] = v;
+  }
+  const int64_t jt = (int64_t)ncp * ncp;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < jt;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int j = (int)(idx / ncp), i = (int)(idx % ncp);
+    jb[idx] = (i == j) ? 1.0 : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) dsvd_round_kernel(int ldx, int ncp, int nbe, int round,
+                                                               double* __restrict__ X,
+                                                               int64_t x_stride,
+                                                               double* __restrict__ Jm,
+                                                               int64_t j_stride, int* flags,
+                                                               double tol) {
+  __shared__ double M[PW][PW + 1];
+  __shared__ double Q[PW][PW + 1];
+  __shared__ double rc[PW / 2], rs[PW / 2];
+  __shared__ int rp[PW / 2], rq[PW / 2];
+  __shared__ int any, rot;
+  const int b = blockIdx.y;
+  if (flags[b] & 2) return;  // stream already converged
+  const int pi = blockIdx.x;
+  const int I = tslot(pi, round, nbe), Jb = tslot(nbe - 1 - pi, round, nbe);
+  double* xb = X + b * x_stride;
+  double* jb = Jm + b * j_stride;
+  auto col = [&](int c) { return c < BW ? I * BW + c : Jb * BW + (c - BW); };
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kThreads / 32;
+  const int g = lane >> 2, q = lane & 3;
+  for (int idx = tid; idx < PW * (PW + 1); idx += kThreads) {
+    (&M[0][0])[idx] = 0.0;
+    (&Q[0][0])[idx] = 0.0;
+  }
+  __syncthreads();
+
+  // ---- Gram of the 32 selected columns (DMMA)
+  {
+    double acc[10][2];
+#pragma unroll
+    for (int t = 0; t < 10; ++t) acc[t][0] = acc[t][1] = 0.0;
+    const double* cp[4];
+#pragma unroll
+    for (int cg = 0; cg < 4; ++cg) cp[cg] = xb + (int64_t)col(cg * 8 + g) * ldx + q;
+    for (int k0 = warp * 4; k0 < ldx; k0 += nw * 4) {
+      double a[4];
+#pragma unroll
+      for (int cg = 0; cg < 4; ++cg) a[cg] = cp[cg][k0];
+      int t = 0;
+#pragma unroll
+      for (int c1 = 0; c1 < 4; ++c1)
+#pragma unroll
+        for (int c2 = c1; c2 < 4; ++c2) {
+          dmma_8x8x4(acc[t][0], acc[t][1], a[c1], a[c2]);
+          ++t;
+        }
+    }
+    // warps add their partial Grams in a fixed order (bit-reproducible runs)
+    for (int w = 0; w < nw; ++w) {
+      if (warp == w) {
+        int t = 0;
+#pragma unroll
+        for (int c1 = 0; c1 < 4; ++c1)
+#pragma unroll
+          for (int c2 = c1; c2 < 4; ++c2) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              int row = c1 * 8 + g, cc = c2 * 8 + 2 * q + e;
+              M[row][cc] += acc[t][e];
+              if (c1 != c2) M[cc][row] += acc[t][e];
+            }
+            ++t;
+          }
+      }
+      __syncthreads();
+    }
+  }
+  if (tid == 0) any = 0;
+  __syncthreads();
+  for (int idx = tid; idx < PW * PW; idx += kThreads) {
+    int p = idx / PW, qq = idx % PW;
+    if (p < qq && fabs(M[p][qq]) > tol * sqrt(M[p][p] * M[qq][qq])) any = 1;
+  }
+  __syncthreads();
+  if (!any) return;
+  if (tid == 0) atomicOr(&flags[b], 1);
+  for (int i = tid; i < PW; i += kThreads) Q[i][i] = 1.0;
+  __syncthreads();
+
+  // ---- parallel two-sided Jacobi on M (symmetric PSD), Q accumulates
+  for (int sweep = 0; sweep < 12; ++sweep) {
+    if (tid == 0) rot = 0;
+    __syncthreads();
+    for (int r2 = 0; r2 < PW - 1; ++r2) {
+      if (tid < PW / 2) {
+        int a0 = tslot(tid, r2, PW), a1 = tslot(PW - 1 - tid, r2, PW);
+        int p = min(a0, a1), qq = max(a0, a1);
+        double app = M[p][p], aqq = M[qq][qq], apq = M[p][qq];
+        double c = 1.0, s = 0.0;
+        if (fabs(apq) > tol * sqrt(app * aqq) && apq != 0.0) {
+          double zeta = (aqq - app) / (2.0 * apq);
+          double t = zeta >= 0.0 ? 1.0 / (zeta + sqrt(1.0 + zeta * zeta))
+                                 : -1.0 / (-zeta + sqrt(1.0 + zeta * zeta));
+          c = 1.0 / sqrt(1.0 + t * t);
+          s = t * c;
+          rot = 1;
+        }
+        rp[tid] = p;
+        rq[tid] = qq;
+        rc[tid] = c;
+        rs[tid] = s;
+      }
+      __syncthreads();
+      for (int task = tid; task < (PW / 2) * PW; task += kThreads) {
+        int pr = task / PW, i = task % PW;
+        double s = rs[pr];
+        if (s == 0.0) continue;
+        double c = rc[pr];
+        int p = rp[pr], qq = rq[pr];
+        double mp = M[i][p], mq = M[i][qq];
+        M[i][p] = c * mp - s * mq;
+        M[i][qq] = s * mp + c * mq;
+        double qp = Q[i][p], qv = Q[i][qq];
+        Q[i][p] = c * qp - s * qv;
+        Q[i][qq] = s * qp + c * qv;
+      }
+      __syncthreads();
+      for (int task = tid; task < (PW / 2) * PW; task += kThreads) {
+        int pr = task / PW, i = task % PW;
+        double s = rs[pr];
+        if (s == 0.0) continue;
+        double c = rc[pr];
+        int p = rp[pr], qq = rq[pr];
+        double mp = M[p][i], mq = M[qq][i];
+        M[p][i] = c * mp - s * mq;
+        M[qq][i] = s * mp + c * mq;
+      }
+      __syncthreads();
+    }
+    if (!rot) break;
+  }
+
+  // ---- apply X[:, cols] <- X[:, cols] Q and J[:, cols] <- J[:, cols] Q (DMMA)
+  double bq[8][4];
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk)
+#pragma unroll
+    for (int nn = 0; nn < 4; ++nn) bq[kk][nn] = Q[kk * 4 + q][nn * 8 + g];
+  for (int target = 0; target < 2; ++target) {
+    double* T = target == 0 ? xb : jb;
+    const int ld = target == 0 ? ldx : ncp;
+    for (int r0 = warp * 8; r0 < ld; r0 += nw * 8) {
+      double a[8];
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) a[kk] = T[(int64_t)col(kk * 4 + q) * ld + r0 + g];
+#pragma unroll
+      for (int nn = 0; nn < 4; ++nn) {
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) dmma_8x8x4(d0, d1, a[kk], bq[kk][nn]);
+        T[(int64_t)col(nn * 8 + 2 * q) * ld + r0 + g] = d0;
+        T[(int64_t)col(nn * 8 + 2 * q + 1) * ld + r0 + g] = d1;
+      }
+    }
+  }
+}
+
+__global__ void dsvd_finalize_kernel(int m, int n, int nc, int ldx, int ncp,
+                                     const double* __restrict__ X, int64_t x_stride,
+                                     const double* __restrict__ Jm, int64_t j_stride, int w, Mat U,
+                                     Mat V, double* s_w, int64_t s_w_stride, double* s_all,
+                                     int64_t s_all_stride) {
+  extern __shared__ double dsm[];
+  double* raw = dsm;
+  int* order = reinterpret_cast<int*>(dsm + nc);
+  const int b = blockIdx.x;
+  const double* xb = X + b * x_stride;
+  const double* jb = Jm + b * j_stride;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = warp; j < nc; j += nw) {
+    const double* c = xb + (int64_t)j * ldx;
+    double acc = 0.0;
+    for (int i = lane; i < ldx; i += 32) acc = fma(c[i], c[i], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) raw[j] = sqrt(acc);
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < nc; j += blockDim.x) {
+    double rj = raw[j];
+    int rank = 0;
+    for (int i = 0; i < nc; ++i) {
+      double ri = raw[i];
+      rank += (ri > rj) || (ri == rj && i < j);
+    }
+    order[rank] = j;
+  }
+  __syncthreads();
+  const double s0 = raw[order[0]];
+  auto snapped = [&](int t) {
+    double r = raw[order[t]];
+    return (s0 > 0.0 && r < kZeroSvRtol * s0) ? 0.0 : r;
+  };
+  if (s_all)
+    for (int t = threadIdx.x; t < nc; t += blockDim.x) s_all[b * s_all_stride + t] = snapped(t);
+  if (s_w)
+    for (int t = threadIdx.x; t < w; t += blockDim.x) s_w[b * s_w_stride + t] = snapped(t);
+  const bool tall = m >= n;
+  const int len = tall ? m : n;
+  // normalized side (len rows) and rotation side (nc rows)
+  double* Nb = tall ? (U.p ? U.p + b * U.stride : nullptr) : (V.p ? V.p + b * V.stride : nullptr);
+  const int ldn = tall ? U.ld : V.ld;
+  double* Rb = tall ? (V.p ? V.p + b * V.stride : nullptr) : (U.p ? U.p + b * U.stride : nullptr);
+  const int ldr = tall ? V.ld : U.ld;
+  for (int t = warp; t < w; t += nw) {
+    const int j = order[t];
+    const double r = raw[j];
+    const bool live = snapped(t) > 0.0;
+    const double inv = live ? 1.0 / r : 0.0;
+    if (Nb) {
+      const double* c = xb + (int64_t)j * ldx;
+      for (int i = lane; i < len; i += 32) Nb[(int64_t)i * ldn + t] = live ? c[i] * inv : 0.0;
+    }
+    if (Rb) {
+      const double* c = jb + (int64_t)j * ncp;
+      for (int i = lane; i < nc; i += 32) Rb[(int64_t)i * ldr + t] = c[i];
+    }
+  }
+}
+
+}  // namespace
+
+DenseSvdPlan dense_svd_plan(int m, int n) {
+  DenseSvdPlan p;
+  p.m = m;
+  p.n = n;
+  p.nc = std::min(m, n);
+  p.len = std::max(m, n);
+  int nb = ceil_div(p.nc, BW);
+  if (nb % 2) ++nb;
+  p.nb = nb;
+  p.ncp = nb * BW;
+  p.ldx = round_up(p.len, 8);
+  return p;
+}
+
+int dense_svd_run(int batch, int m, int n, const double* a, int64_t a_stride, int lda, int w,
+                  Mat u, Mat v, double* s_w, int64_t s_w_stride, double* s_all,
+                  int64_t s_all_stride, double* x, double* jac, int* flags, int* flags_host,
+                  cudaStream_t st, int* sweeps_out) {
+  if (batch == 0) return ISVD_OK;
+  DenseSvdPlan P = dense_svd_plan(m, n);
+  const int64_t xs = P.x_elems(), js = P.j_elems();
+  {
+    int64_t total = std::max(xs, js);
+    int gx = (int)std::min<int64_t>((total + 255) / 256, 2048);
+    dsvd_prep_kernel<<<dim3(gx, batch), 256, 0, st>>>(m, n, P.ldx, P.ncp, a, a_stride, lda, x, xs,
+                                                      jac, js);
+    ISVD_LAUNCHED();
+  }
+  ISVD_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * batch, st));
+  const double eps = 2.220446049250313e-16;
+  const double tol = std::max(1e-14, 4.0 * std::sqrt((double)P.len) * eps);
+  std::vector<int> fl(batch, 0);
+  int sweep = 0;
+  const int kMaxOuter = 40;
+  for (; sweep < kMaxOuter; ++sweep) {
+    for (int round = 0; round < P.nb - 1; ++round) {
+      dsvd_round_kernel<<<dim3(P.nb / 2, batch), kThreads, 0, st>>>(P.ldx, P.ncp, P.nb, round, x,
+                                                                    xs, jac, js, flags, tol);
+      ISVD_LAUNCHED();
+    }
+    ISVD_CUDA(cudaMemcpyAsync(flags_host, flags, sizeof(int) * batch, cudaMemcpyDeviceToHost, st));
+    ISVD_CUDA(cudaStreamSynchronize(st));
+    bool all_done = true;
+    for (int b = 0; b < batch; ++b) {
+      int f = flags_host[b];
+      if (f & 2) continue;
+      if (f & 1)
+        all_done = false, f = 0;
+      else
+        f = 2;
+      flags_host[b] = f;
+    }
+    if (all_done) break;
+    ISVD_CUDA(cudaMemcpyAsync(flags, flags_host, sizeof(int) * batch, cudaMemcpyHostToDevice, st));
+  }
+  if (sweeps_out) *sweeps_out = sweep + 1;
+  {
+    size_t smem = sizeof(double) * P.nc + sizeof(int) * P.nc;
+    static bool attr = false;
+    if (!attr) {
+      ISVD_CUDA(cudaFuncSetAttribute(dsvd_finalize_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+    if (smem > 200 * 1024) {
+      set_error("dense_svd: min(m, n) too large for the finalize kernel");
+      return ISVD_EINVAL;
+    }
+    dsvd_finalize_kernel<<<batch, 256, smem, st>>>(m, n, P.nc, P.ldx, P.ncp, x, xs, jac, js, w, u,
+                                                   v, s_w, s_w_stride, s_all, s_all_stride);
+    ISVD_LAUNCHED();
+  }
+  return ISVD_OK;
+}
+
+}  // namespace isvd

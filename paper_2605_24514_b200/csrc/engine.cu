@@ -1,0 +1,987 @@
+// libisvd C ABI: functional kernels + engine handle (include/isvd.h).
+//
+// The engine mirrors SvdEngine (engine.py:73-217).  Device state per stream
+// b (B streams of identical shape):
+//   U  [m_cap x ld]  row-major, columns 0..r-1 live (ld = padded rank cap)
+//   V  [n_cap x ld]  row-major (V = Vt^T, so U and V rotate with one kernel
+//                    and the column-append transpose trick is a pointer swap)
+//   s  [ld], A [m_cap x n_cap] (tracked matrix, lda = n_cap), N (||A||^2)
+// Per-tick sequence (row append, engine.py:117-129):
+//   K1 project_append  -> p, z, rho, ||x||, core, A row write, N += x.x
+//   K2 core_svd        -> Uk, s', Vk (Jacobi, sort, snap, complete)
+//   K3/K4 rotate       -> U <- [U 0; 0 1] Uk[:, :keep], V <- V Vk[:r] + z^ Vk[r]
+//   install            -> s <- s'[:keep]; zero-sigma completion (engine.py:59-70)
+// Sign canonicalisation (engine.py:207) is deferred to observation: the
+// update is exactly sign-equivariant (flipping a U column and V column pair
+// flips the core by a +-1 diagonal similarity, the Jacobi rotations by the
+// same similarity, and the rotated factors come out bit-identical), so the
+// canonical form is produced whenever factors are read.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+#include "common.cuh"
+#include "core_svd.cuh"
+#include "dense_svd.cuh"
+#include "metrics.cuh"
+#include "tick.cuh"
+#include "../../include/isvd.h"
+
+namespace isvd {
+
+static thread_local std::string g_err;
+static int64_t g_launches = 0;
+void set_error(const std::string& msg) { g_err = msg; }
+void count_launch(int n) { __atomic_add_fetch(&g_launches, n, __ATOMIC_RELAXED); }
+
+template <typename T>
+static int dalloc(T** p, size_t n) {
+  *p = nullptr;
+  if (n == 0) return ISVD_OK;
+  cudaError_t e = cudaMalloc((void**)p, n * sizeof(T));
+  if (e != cudaSuccess) {
+    set_error(std::string("cudaMalloc(") + std::to_string(n * sizeof(T)) + "): " +
+              cudaGetErrorString(e));
+    cudaGetLastError();
+    *p = nullptr;
+    return e == cudaErrorMemoryAllocation ? ISVD_ENOMEM : ISVD_ENODEV;
+  }
+  return ISVD_OK;
+}
+template <typename T>
+static void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+#define ISVD_TRY(x)              \
+  do {                           \
+    int _rc = (x);               \
+    if (_rc != ISVD_OK) return _rc; \
+  } while (0)
+
+static int check_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    set_error("no CUDA device available (libisvd has no CPU fallback)");
+    return ISVD_ENODEV;
+  }
+  return ISVD_OK;
+}
+
+static bool all_finite(const double* p, size_t n) {
+  for (size_t i = 0; i < n; ++i)
+    if (!std::isfinite(p[i])) return false;
+  return true;
+}
+
+}  // namespace isvd
+
+using namespace isvd;
+
+struct isvd_engine {
+  int B = 0, m = 0, n = 0, r = 0, k = 0;
+  int64_t step = 0;
+  double tol = 1e-10;
+  bool guard = false;
+  int m_cap = 0, n_cap = 0, ld = 0;
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  bool canonical = true;
+  bool initialized = false;
+  double *U = nullptr, *V = nullptr, *s = nullptr, *A = nullptr, *N = nullptr;
+  double *core = nullptr, *uk = nullptr, *vk = nullptr, *sv = nullptr, *vscr = nullptr;
+  double *z = nullptr, *inj = nullptr, *rho = nullptr, *xnorm = nullptr, *ev = nullptr;
+  int64_t *ei = nullptr, *ej = nullptr;
+  double* ed = nullptr;
+  int* dflag = nullptr;
+  double* ref = nullptr;
+  int ref_m = 0, ref_r = 0, ref_cap = 0;
+  bool has_ref = false;
+  // dense-SVD / metrics workspace
+  double *wx = nullptr, *wj = nullptr, *wpart = nullptr, *wout = nullptr;
+  int64_t wx_n = 0, wj_n = 0, wpart_n = 0, wout_n = 0;
+  int* wflags = nullptr;
+  std::vector<int> hflags;
+  // optional per-phase timing (CUDA events on the engine stream):
+  // phase 0 = K1/K6 project+build, 1 = K2 core SVD, 2 = K3/K4 rotation,
+  // 3 = install (s copy + zero-sigma completion)
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<cudaEvent_t> ev_marks;  // 5 per recorded tick
+  int64_t timed_ticks = 0;
+
+  void mark() {
+    if (!timing) return;
+    cudaEvent_t ev;
+    if (ev_pool.empty()) {
+      cudaEventCreate(&ev);
+    } else {
+      ev = ev_pool.back();
+      ev_pool.pop_back();
+    }
+    cudaEventRecord(ev, st);
+    ev_marks.push_back(ev);
+  }
+
+  int S() const { return ld + 1; }
+  int64_t ustride() const { return (int64_t)m_cap * ld; }
+  int64_t vstride() const { return (int64_t)n_cap * ld; }
+  int64_t astride() const { return (int64_t)m_cap * n_cap; }
+  int64_t cstride() const { return (int64_t)S() * S(); }
+  int zlen() const { return std::max(m_cap, n_cap) + 8; }
+  Mat Um() const { return Mat{U, ustride(), ld}; }
+  Mat Vm() const { return Mat{V, vstride(), ld}; }
+
+  int alloc_core_bufs() {
+    dfree(core); dfree(uk); dfree(vk); dfree(sv); dfree(vscr);
+    size_t cs = (size_t)B * cstride();
+    ISVD_TRY(dalloc(&core, cs));
+    ISVD_TRY(dalloc(&uk, cs));
+    ISVD_TRY(dalloc(&vk, cs));
+    ISVD_TRY(dalloc(&sv, (size_t)B * S()));
+    if (S() > kSmemMaxS) ISVD_TRY(dalloc(&vscr, (size_t)B * S() * (S() | 1)));
+    return ISVD_OK;
+  }
+
+  int alloc_vec_bufs() {
+    dfree(z); dfree(ev);
+    ISVD_TRY(dalloc(&z, (size_t)B * zlen()));
+    ISVD_TRY(dalloc(&ev, (size_t)B * zlen()));
+    return ISVD_OK;
+  }
+
+  int ensure_work(int64_t x_n, int64_t j_n, int64_t part_n, int64_t out_n) {
+    if (x_n > wx_n) { dfree(wx); ISVD_TRY(dalloc(&wx, x_n)); wx_n = x_n; }
+    if (j_n > wj_n) { dfree(wj); ISVD_TRY(dalloc(&wj, j_n)); wj_n = j_n; }
+    if (part_n > wpart_n) { dfree(wpart); ISVD_TRY(dalloc(&wpart, part_n)); wpart_n = part_n; }
+    if (out_n > wout_n) { dfree(wout); ISVD_TRY(dalloc(&wout, out_n)); wout_n = out_n; }
+    if (!wflags) ISVD_TRY(dalloc(&wflags, (size_t)B));
+    hflags.resize(B);
+    return ISVD_OK;
+  }
+
+  // grow U (rows) and A (rows) to hold at least rows_needed rows
+  int grow_rows(int rows_needed) {
+    if (rows_needed <= m_cap) return ISVD_OK;
+    int nc = std::max(rows_needed, m_cap * 2);
+    double *U2, *A2;
+    ISVD_TRY(dalloc(&U2, (size_t)B * nc * ld));
+    ISVD_CUDA(cudaMemsetAsync(U2, 0, sizeof(double) * B * nc * ld, st));
+    ISVD_TRY(launch_copy_rows(B, m, ld, U, ustride(), ld, U2, (int64_t)nc * ld, ld, st));
+    ISVD_TRY(dalloc(&A2, (size_t)B * nc * n_cap));
+    ISVD_TRY(launch_copy_rows(B, m, n, A, astride(), n_cap, A2, (int64_t)nc * n_cap, n_cap, st));
+    ISVD_CUDA(cudaStreamSynchronize(st));
+    dfree(U); dfree(A);
+    U = U2; A = A2;
+    m_cap = nc;
+    return alloc_vec_bufs();
+  }
+
+  int grow_cols(int cols_needed) {
+    if (cols_needed <= n_cap) return ISVD_OK;
+    int nc = std::max(cols_needed, n_cap * 2);
+    double *V2, *A2;
+    ISVD_TRY(dalloc(&V2, (size_t)B * nc * ld));
+    ISVD_CUDA(cudaMemsetAsync(V2, 0, sizeof(double) * B * nc * ld, st));
+    ISVD_TRY(launch_copy_rows(B, n, ld, V, vstride(), ld, V2, (int64_t)nc * ld, ld, st));
+    ISVD_TRY(dalloc(&A2, (size_t)B * m_cap * nc));
+    ISVD_TRY(launch_copy_rows(B, m, n, A, astride(), n_cap, A2, (int64_t)m_cap * nc, nc, st));
+    ISVD_CUDA(cudaStreamSynchronize(st));
+    dfree(V); dfree(A);
+    V = V2; A = A2;
+    n_cap = nc;
+    return alloc_vec_bufs();
+  }
+
+  int grow_rank(int k_needed) {
+    int nld = round_up(std::max(k_needed, 1), 8);
+    if (nld <= ld) return ISVD_OK;
+    if (nld + 1 > kCoreMaxS) {
+      set_error("work rank exceeds the supported maximum (" + std::to_string(kCoreMaxS - 1) + ")");
+      return ISVD_EINVAL;
+    }
+    double *U2, *V2, *s2;
+    ISVD_TRY(dalloc(&U2, (size_t)B * m_cap * nld));
+    ISVD_TRY(dalloc(&V2, (size_t)B * n_cap * nld));
+    ISVD_TRY(dalloc(&s2, (size_t)B * nld));
+    ISVD_CUDA(cudaMemsetAsync(U2, 0, sizeof(double) * B * m_cap * nld, st));
+    ISVD_CUDA(cudaMemsetAsync(V2, 0, sizeof(double) * B * n_cap * nld, st));
+    ISVD_CUDA(cudaMemsetAsync(s2, 0, sizeof(double) * B * nld, st));
+    if (U) {
+      ISVD_TRY(launch_copy_rows(B, m, ld, U, ustride(), ld, U2, (int64_t)m_cap * nld, nld, st));
+      ISVD_TRY(launch_copy_rows(B, n, ld, V, vstride(), ld, V2, (int64_t)n_cap * nld, nld, st));
+      ISVD_TRY(launch_copy_rows(B, 1, ld, s, ld, ld, s2, nld, nld, st));
+    }
+    double* ref2 = nullptr;
+    if (ref) {
+      ISVD_TRY(dalloc(&ref2, (size_t)B * ref_cap * nld));
+      ISVD_TRY(launch_copy_rows(B, ref_m, ld, ref, (int64_t)ref_cap * ld, ld, ref2,
+                                (int64_t)ref_cap * nld, nld, st));
+    }
+    ISVD_CUDA(cudaStreamSynchronize(st));
+    dfree(U); dfree(V); dfree(s);
+    U = U2; V = V2; s = s2;
+    if (ref) { dfree(ref); ref = ref2; }
+    ld = nld;
+    return alloc_core_bufs();
+  }
+
+  int canonicalize() {
+    if (canonical) return ISVD_OK;
+    ISVD_TRY(launch_canonicalize(B, r, Um(), m, Vm(), n, st));
+    canonical = true;
+    return ISVD_OK;
+  }
+
+  int install_from_core(int keep) {
+    // s <- sv[:, :keep]
+    if (keep > 0)
+      ISVD_CUDA(cudaMemcpy2DAsync(s, sizeof(double) * ld, sv, sizeof(double) * S(),
+                                  sizeof(double) * keep, B, cudaMemcpyDeviceToDevice, st));
+    return ISVD_OK;
+  }
+
+  // dense thin SVD of the tracked matrix into U, V, s (engine init/refresh)
+  int factor_tracked() {
+    DenseSvdPlan P = dense_svd_plan(m, n);
+    ISVD_TRY(ensure_work((int64_t)B * P.x_elems(), (int64_t)B * P.j_elems(), 0, 0));
+    int w = std::min(k, std::min(m, n));
+    int sweeps = 0;
+    ISVD_TRY(dense_svd_run(B, m, n, A, astride(), n_cap, w, Um(), Vm(), s, ld, nullptr, 0, wx, wj,
+                           wflags, hflags.data(), st, &sweeps));
+    r = w;
+    ISVD_TRY(launch_complete_zero(B, r, s, ld, Um(), m, Vm(), n, st));
+    canonical = false;
+    ISVD_TRY(canonicalize());
+    return ISVD_OK;
+  }
+
+  ~isvd_engine() {
+    dfree(U); dfree(V); dfree(s); dfree(A); dfree(N);
+    dfree(core); dfree(uk); dfree(vk); dfree(sv); dfree(vscr);
+    dfree(z); dfree(inj); dfree(rho); dfree(xnorm); dfree(ev);
+    dfree(ei); dfree(ej); dfree(ed); dfree(dflag); dfree(ref);
+    dfree(wx); dfree(wj); dfree(wpart); dfree(wout); dfree(wflags);
+    for (auto ev : ev_marks) cudaEventDestroy(ev);
+    for (auto ev : ev_pool) cudaEventDestroy(ev);
+    if (own_stream && st) cudaStreamDestroy(st);
+  }
+};
+
+extern "C" {
+
+const char* isvd_last_error(void) { return g_err.c_str(); }
+int isvd_version(void) { return 1; }
+int64_t isvd_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
+
+int isvd_engine_create(isvd_engine** out, int batch, int m, int n, int k, double tol,
+                       int reortho_guard, int m_cap, int n_cap, int k_cap, void* stream) {
+  if (!out) { set_error("out is null"); return ISVD_EINVAL; }
+  *out = nullptr;
+  if (batch < 1) { set_error("batch must be >= 1"); return ISVD_EINVAL; }
+  if (m < 1 || n < 1) { set_error("initial matrix must be nonempty"); return ISVD_EINVAL; }
+  if (k < 1) { set_error("work rank must be >= 1, got " + std::to_string(k)); return ISVD_EINVAL; }
+  if (!(tol > 0.0)) { set_error("tol must be positive"); return ISVD_EINVAL; }
+  ISVD_TRY(check_device());
+  auto* e = new isvd_engine();
+  e->B = batch; e->m = m; e->n = n; e->k = k; e->tol = tol; e->guard = reortho_guard != 0;
+  e->m_cap = std::max(m_cap, m + 1);
+  e->n_cap = std::max(n_cap, n);
+  int kc = std::max(std::max(k_cap, k), 1);
+  e->ld = round_up(kc, 8);
+  if (e->ld + 1 > kCoreMaxS) {
+    delete e;
+    set_error("work rank exceeds the supported maximum");
+    return ISVD_EINVAL;
+  }
+  if (stream) {
+    e->st = (cudaStream_t)stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&e->st, cudaStreamNonBlocking) != cudaSuccess) {
+      delete e;
+      set_error("cudaStreamCreate failed");
+      return ISVD_ENODEV;
+    }
+    e->own_stream = true;
+  }
+  int rc = ISVD_OK;
+  auto A = [&](int x) { if (rc == ISVD_OK) rc = x; };
+  A(dalloc(&e->U, (size_t)batch * e->m_cap * e->ld));
+  A(dalloc(&e->V, (size_t)batch * e->n_cap * e->ld));
+  A(dalloc(&e->s, (size_t)batch * e->ld));
+  A(dalloc(&e->A, (size_t)batch * e->m_cap * e->n_cap));
+  A(dalloc(&e->N, (size_t)batch));
+  A(dalloc(&e->inj, (size_t)batch));
+  A(dalloc(&e->rho, (size_t)batch));
+  A(dalloc(&e->xnorm, (size_t)batch));
+  A(dalloc(&e->ei, (size_t)batch));
+  A(dalloc(&e->ej, (size_t)batch));
+  A(dalloc(&e->ed, (size_t)batch));
+  A(dalloc(&e->dflag, 4));
+  if (rc == ISVD_OK) rc = e->alloc_core_bufs();
+  if (rc == ISVD_OK) rc = e->alloc_vec_bufs();
+  if (rc == ISVD_OK) {
+    cudaMemsetAsync(e->U, 0, sizeof(double) * batch * e->m_cap * e->ld, e->st);
+    cudaMemsetAsync(e->V, 0, sizeof(double) * batch * e->n_cap * e->ld, e->st);
+    cudaMemsetAsync(e->s, 0, sizeof(double) * batch * e->ld, e->st);
+    std::vector<double> nanv(batch, std::nan(""));
+    cudaMemcpyAsync(e->rho, nanv.data(), sizeof(double) * batch, cudaMemcpyHostToDevice, e->st);
+    cudaMemcpyAsync(e->xnorm, nanv.data(), sizeof(double) * batch, cudaMemcpyHostToDevice, e->st);
+    if (cudaStreamSynchronize(e->st) != cudaSuccess) {
+      set_error("initialisation failed");
+      rc = ISVD_ENODEV;
+    }
+  }
+  if (rc != ISVD_OK) {
+    delete e;
+    return rc;
+  }
+  *out = e;
+  return ISVD_OK;
+}
+
+int isvd_engine_destroy(isvd_engine* e) {
+  if (e) {
+    if (e->st) cudaStreamSynchronize(e->st);
+    delete e;
+  }
+  return ISVD_OK;
+}
+
+void* isvd_engine_stream(isvd_engine* e) { return e ? (void*)e->st : nullptr; }
+
+int isvd_engine_init(isvd_engine* e, const double* a0, int on_device) {
+  if (!e || !a0) { set_error("null argument"); return ISVD_EINVAL; }
+  const size_t cnt = (size_t)e->B * e->m * e->n;
+  if (!on_device) {
+    if (!all_finite(a0, cnt)) { set_error("initial matrix contains non-finite entries"); return ISVD_EINVAL; }
+    // stage per stream (row-major m x n) into the pitched tracked matrix
+    for (int b = 0; b < e->B; ++b)
+      ISVD_CUDA(cudaMemcpy2DAsync(e->A + b * e->astride(), sizeof(double) * e->n_cap,
+                                  a0 + (size_t)b * e->m * e->n, sizeof(double) * e->n,
+                                  sizeof(double) * e->n, e->m, cudaMemcpyHostToDevice, e->st));
+  } else {
+    ISVD_CUDA(cudaMemsetAsync(e->dflag, 0, sizeof(int), e->st));
+    ISVD_TRY(launch_check_finite(cnt, a0, e->dflag, e->st));
+    int hf = 0;
+    ISVD_CUDA(cudaMemcpyAsync(&hf, e->dflag, sizeof(int), cudaMemcpyDeviceToHost, e->st));
+    ISVD_CUDA(cudaStreamSynchronize(e->st));
+    if (hf) { set_error("initial matrix contains non-finite entries"); return ISVD_EINVAL; }
+    ISVD_TRY(launch_copy_rows(e->B, e->m, e->n, a0, (int64_t)e->m * e->n, e->n, e->A, e->astride(),
+                              e->n_cap, e->st));
+  }
+  ISVD_TRY(launch_sumsq(e->B, e->m, e->n, e->A, e->astride(), e->n_cap, e->N, e->st));
+  ISVD_TRY(e->factor_tracked());
+  e->step = 0;
+  e->has_ref = false;
+  e->initialized = true;
+  std::vector<double> nanv(e->B, std::nan(""));
+  ISVD_CUDA(cudaMemcpyAsync(e->rho, nanv.data(), sizeof(double) * e->B, cudaMemcpyHostToDevice, e->st));
+  ISVD_CUDA(cudaMemcpyAsync(e->xnorm, nanv.data(), sizeof(double) * e->B, cudaMemcpyHostToDevice, e->st));
+  ISVD_CUDA(cudaStreamSynchronize(e->st));
+  return ISVD_OK;
+}
+
+static int append_common(isvd_engine* e, const double* x, int on_device, bool is_row) {
+  if (!e || !x) { set_error("null argument"); return ISVD_EINVAL; }
+  if (!e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
+  const int len = is_row ? e->n : e->m;
+  if (!on_device && !all_finite(x, (size_t)e->B * len)) {
+    set_error(std::string(is_row ? "appended row" : "appended column") + " contains non-finite entries");
+    return ISVD_EINVAL;
+  }
+  // keep = min(r+1, k, m+1, n) (row) | min(r+1, k, m, n+1) (col): engine.py:122,136
+  const int keep = is_row ? std::min(std::min(e->r + 1, e->k), std::min(e->m + 1, e->n))
+                          : std::min(std::min(e->r + 1, e->k), std::min(e->m, e->n + 1));
+  ISVD_TRY(is_row ? e->grow_rows(e->m + 1) : e->grow_cols(e->n + 1));
+  const double* xd = x;
+  if (!on_device) {
+    ISVD_CUDA(cudaMemcpyAsync(e->ev, x, sizeof(double) * e->B * len, cudaMemcpyHostToDevice, e->st));
+    xd = e->ev;
+  }
+  const int r = e->r;
+  Mat F = is_row ? e->Vm() : e->Um();
+  int64_t a_off = is_row ? (int64_t)e->m * e->n_cap : (int64_t)e->n;
+  int64_t a_step = is_row ? 1 : e->n_cap;
+  e->mark();
+  ISVD_TRY(launch_project_append(e->B, len, r, F, xd, len, e->s, e->ld, e->tol, e->core,
+                                 e->cstride(), e->S(), e->z, e->zlen(), e->inj, e->rho, e->xnorm,
+                                 e->A, e->astride(), a_off, a_step, e->N, e->st));
+  e->mark();
+  ISVD_TRY(launch_core_svd(e->B, r + 1, e->core, e->cstride(), e->S(), e->uk, e->vk, e->cstride(),
+                           e->S(), e->sv, e->S(), e->vscr, nullptr, e->st));
+  e->mark();
+  // row: U <- [U 0; 0 1] Uk, V <- V Vk[:r] + z^ Vk[r] ; col: the same with U<->V
+  RotJob grow{is_row ? e->Um() : e->Vm(), is_row ? e->m : e->n, e->uk, e->cstride(), e->S(),
+              nullptr, 0, nullptr, 1};
+  RotJob inj{is_row ? e->Vm() : e->Um(), is_row ? e->n : e->m, e->vk, e->cstride(), e->S(),
+             e->z, e->zlen(), e->inj, 0};
+  ISVD_TRY(launch_rotate(e->B, r, keep, grow, &inj, e->st));
+  e->mark();
+  ISVD_TRY(e->install_from_core(keep));
+  if (is_row) e->m += 1; else e->n += 1;
+  e->r = keep;
+  ISVD_TRY(launch_complete_zero(e->B, e->r, e->s, e->ld, e->Um(), e->m, e->Vm(), e->n, e->st));
+  e->mark();
+  if (e->timing) e->timed_ticks += 1;
+  e->canonical = false;
+  e->step += 1;
+  return ISVD_OK;
+}
+
+int isvd_engine_row_append(isvd_engine* e, const double* x, int on_device) {
+  return append_common(e, x, on_device, true);
+}
+
+int isvd_engine_col_append(isvd_engine* e, const double* y, int on_device) {
+  return append_common(e, y, on_device, false);
+}
+
+int isvd_engine_rank_one(isvd_engine* e, const int64_t* i, const int64_t* j, const double* delta,
+                         int on_device) {
+  if (!e || !i || !j || !delta) { set_error("null argument"); return ISVD_EINVAL; }
+  if (!e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
+  const int64_t *di = i, *dj = j;
+  const double* dd = delta;
+  if (!on_device) {
+    for (int b = 0; b < e->B; ++b) {
+      if (!(0 <= i[b] && i[b] < e->m && 0 <= j[b] && j[b] < e->n)) {
+        set_error("index (" + std::to_string(i[b]) + ", " + std::to_string(j[b]) +
+                  ") out of bounds for shape (" + std::to_string(e->m) + ", " +
+                  std::to_string(e->n) + ")");
+        return ISVD_EINVAL;
+      }
+      if (!std::isfinite(delta[b])) { set_error("delta must be finite"); return ISVD_EINVAL; }
+    }
+    ISVD_CUDA(cudaMemcpyAsync(e->ei, i, sizeof(int64_t) * e->B, cudaMemcpyHostToDevice, e->st));
+    ISVD_CUDA(cudaMemcpyAsync(e->ej, j, sizeof(int64_t) * e->B, cudaMemcpyHostToDevice, e->st));
+    ISVD_CUDA(cudaMemcpyAsync(e->ed, delta, sizeof(double) * e->B, cudaMemcpyHostToDevice, e->st));
+    di = e->ei; dj = e->ej; dd = e->ed;
+  }
+  const int r = e->r;
+  e->mark();
+  ISVD_TRY(launch_rank1_build(e->B, r, e->Um(), e->Vm(), e->s, e->ld, di, dj, dd, e->core,
+                              e->cstride(), e->S(), e->A, e->astride(), e->n_cap, e->N, e->st));
+  e->mark();
+  ISVD_TRY(launch_core_svd(e->B, r, e->core, e->cstride(), e->S(), e->uk, e->vk, e->cstride(),
+                           e->S(), e->sv, e->S(), e->vscr, nullptr, e->st));
+  e->mark();
+  RotJob ju{e->Um(), e->m, e->uk, e->cstride(), e->S(), nullptr, 0, nullptr, 0};
+  RotJob jv{e->Vm(), e->n, e->vk, e->cstride(), e->S(), nullptr, 0, nullptr, 0};
+  ISVD_TRY(launch_rotate(e->B, r, r, ju, &jv, e->st));
+  e->mark();
+  ISVD_TRY(e->install_from_core(r));
+  ISVD_TRY(launch_complete_zero(e->B, e->r, e->s, e->ld, e->Um(), e->m, e->Vm(), e->n, e->st));
+  e->mark();
+  if (e->timing) e->timed_ticks += 1;
+  e->canonical = false;
+  e->step += 1;
+  return ISVD_OK;
+}
+
+static int copy_reference(isvd_engine* e) {
+  ISVD_TRY(e->canonicalize());
+  if (!e->ref || e->ref_cap < e->m) {
+    dfree(e->ref);
+    e->ref_cap = e->m_cap;
+    ISVD_TRY(dalloc(&e->ref, (size_t)e->B * e->ref_cap * e->ld));
+  }
+  ISVD_TRY(launch_copy_rows(e->B, e->m, e->r, e->U, e->ustride(), e->ld, e->ref,
+                            (int64_t)e->ref_cap * e->ld, e->ld, e->st));
+  e->ref_m = e->m;
+  e->ref_r = e->r;
+  e->has_ref = true;
+  return ISVD_OK;
+}
+
+int isvd_engine_refresh(isvd_engine* e, int store_reference) {
+  if (!e || !e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
+  ISVD_TRY(e->grow_rank(e->k));
+  ISVD_TRY(e->factor_tracked());
+  ISVD_TRY(launch_sumsq(e->B, e->m, e->n, e->A, e->astride(), e->n_cap, e->N, e->st));
+  if (store_reference) ISVD_TRY(copy_reference(e));
+  ISVD_CUDA(cudaStreamSynchronize(e->st));
+  return ISVD_OK;
+}
+
+int isvd_engine_set_reference(isvd_engine* e) {
+  if (!e || !e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
+  ISVD_TRY(copy_reference(e));
+  return ISVD_OK;
+}
+
+int isvd_engine_set_rank(isvd_engine* e, int k_new) {
+  if (!e) { set_error("null engine"); return ISVD_EINVAL; }
+  if (k_new < 1) { set_error("work rank must be >= 1, got " + std::to_string(k_new)); return ISVD_EINVAL; }
+  ISVD_TRY(e->grow_rank(k_new));
+  e->k = k_new;
+  if (e->r > k_new) e->r = k_new;
+  return ISVD_OK;
+}
+
+int isvd_engine_shape(const isvd_engine* e, int* batch, int* m, int* n, int* rank, int* work_rank,
+                      int64_t* step) {
+  if (!e) { set_error("null engine"); return ISVD_EINVAL; }
+  if (batch) *batch = e->B;
+  if (m) *m = e->m;
+  if (n) *n = e->n;
+  if (rank) *rank = e->r;
+  if (work_rank) *work_rank = e->k;
+  if (step) *step = e->step;
+  return ISVD_OK;
+}
+
+int isvd_engine_has_reference(const isvd_engine* e, int* has_ref, int* ref_m, int* ref_r) {
+  if (!e) { set_error("null engine"); return ISVD_EINVAL; }
+  *has_ref = e->has_ref;
+  *ref_m = e->ref_m;
+  *ref_r = e->ref_r;
+  return ISVD_OK;
+}
+
+int isvd_engine_get_factors(isvd_engine* e, int b, double* u, double* sv, double* v) {
+  if (!e || b < 0 || b >= e->B) { set_error("bad stream index"); return ISVD_EINVAL; }
+  ISVD_TRY(e->canonicalize());
+  const int r = e->r;
+  if (r > 0) {
+    if (u)
+      ISVD_CUDA(cudaMemcpy2DAsync(u, sizeof(double) * r, e->U + b * e->ustride(), sizeof(double) * e->ld,
+                                  sizeof(double) * r, e->m, cudaMemcpyDeviceToHost, e->st));
+    if (v)
+      ISVD_CUDA(cudaMemcpy2DAsync(v, sizeof(double) * r, e->V + b * e->vstride(), sizeof(double) * e->ld,
+                                  sizeof(double) * r, e->n, cudaMemcpyDeviceToHost, e->st));
+    if (sv)
+      ISVD_CUDA(cudaMemcpyAsync(sv, e->s + (int64_t)b * e->ld, sizeof(double) * r,
+                                cudaMemcpyDeviceToHost, e->st));
+  }
+  ISVD_CUDA(cudaStreamSynchronize(e->st));
+  return ISVD_OK;
+}
+
+int isvd_engine_get_tracked(isvd_engine* e, int b, double* a) {
+  if (!e || b < 0 || b >= e->B || !a) { set_error("bad argument"); return ISVD_EINVAL; }
+  ISVD_CUDA(cudaMemcpy2DAsync(a, sizeof(double) * e->n, e->A + b * e->astride(),
+                              sizeof(double) * e->n_cap, sizeof(double) * e->n, e->m,
+                              cudaMemcpyDeviceToHost, e->st));
+  ISVD_CUDA(cudaStreamSynchronize(e->st));
+  return ISVD_OK;
+}
+
+int isvd_engine_get_reference(isvd_engine* e, int b, double* out) {
+  if (!e || b < 0 || b >= e->B || !out) { set_error("bad argument"); return ISVD_EINVAL; }
+  if (!e->has_ref) { set_error("no reference stored"); return ISVD_ESTATE; }
+  ISVD_CUDA(cudaMemcpy2DAsync(out, sizeof(double) * e->ref_r, e->ref + (int64_t)b * e->ref_cap * e->ld,
+                              sizeof(double) * e->ld, sizeof(double) * e->ref_r, e->ref_m,
+                              cudaMemcpyDeviceToHost, e->st));
+  ISVD_CUDA(cudaStreamSynchronize(e->st));
+  return ISVD_OK;
+}
+
+int isvd_engine_get_scalars(isvd_engine* e, double* sq_norm, double* last_residual,
+                            double* last_input_norm) {
+  if (!e) { set_error("null engine"); return ISVD_EINVAL; }
+  if (sq_norm) ISVD_CUDA(cudaMemcpyAsync(sq_norm, e->N, sizeof(double) * e->B, cudaMemcpyDeviceToHost, e->st));
+  if (last_residual) ISVD_CUDA(cudaMemcpyAsync(last_residual, e->rho, sizeof(double) * e->B, cudaMemcpyDeviceToHost, e->st));
+  if (last_input_norm) ISVD_CUDA(cudaMemcpyAsync(last_input_norm, e->xnorm, sizeof(double) * e->B, cudaMemcpyDeviceToHost, e->st));
+  ISVD_CUDA(cudaStreamSynchronize(e->st));
+  return ISVD_OK;
+}
+
+int isvd_engine_set_factors(isvd_engine* e, int b, int r, const double* u, const double* sv,
+                            const double* v) {
+  if (!e || b < 0 || b >= e->B) { set_error("bad stream index"); return ISVD_EINVAL; }
+  if (r != e->r) { set_error("set_factors: rank must match the current factor width"); return ISVD_EINVAL; }
+  ISVD_TRY(e->canonicalize());
+  ISVD_CUDA(cudaMemcpy2DAsync(e->U + b * e->ustride(), sizeof(double) * e->ld, u, sizeof(double) * r,
+                              sizeof(double) * r, e->m, cudaMemcpyHostToDevice, e->st));
+  ISVD_CUDA(cudaMemcpy2DAsync(e->V + b * e->vstride(), sizeof(double) * e->ld, v, sizeof(double) * r,
+                              sizeof(double) * r, e->n, cudaMemcpyHostToDevice, e->st));
+  ISVD_CUDA(cudaMemcpyAsync(e->s + (int64_t)b * e->ld, sv, sizeof(double) * r, cudaMemcpyHostToDevice, e->st));
+  ISVD_CUDA(cudaStreamSynchronize(e->st));
+  e->canonical = true;  // the caller's factors are taken verbatim
+  return ISVD_OK;
+}
+
+int isvd_engine_put_reference(isvd_engine* e, int b, int ref_m, int ref_r, const double* refh) {
+  if (!e || b < 0 || b >= e->B || ref_r < 0 || ref_m < 0) { set_error("bad argument"); return ISVD_EINVAL; }
+  if (!refh) { e->has_ref = false; return ISVD_OK; }
+  if (ref_r > e->ld) { set_error("reference wider than the rank capacity"); return ISVD_EINVAL; }
+  if (!e->ref || e->ref_cap < ref_m) {
+    dfree(e->ref);
+    e->ref_cap = std::max(ref_m, e->m_cap);
+    ISVD_TRY(dalloc(&e->ref, (size_t)e->B * e->ref_cap * e->ld));
+  }
+  ISVD_CUDA(cudaMemcpy2DAsync(e->ref + (int64_t)b * e->ref_cap * e->ld, sizeof(double) * e->ld, refh,
+                              sizeof(double) * ref_r, sizeof(double) * ref_r, ref_m,
+                              cudaMemcpyHostToDevice, e->st));
+  ISVD_CUDA(cudaStreamSynchronize(e->st));
+  e->ref_m = ref_m;
+  e->ref_r = ref_r;
+  e->has_ref = true;
+  return ISVD_OK;
+}
+
+int isvd_engine_device_views(isvd_engine* e, double** u, int64_t* u_stride, int* ldu, double** v,
+                             int64_t* v_stride, int* ldv, double** s, int* lds, double** a,
+                             int64_t* a_stride, int* lda) {
+  if (!e) { set_error("null engine"); return ISVD_EINVAL; }
+  if (u) *u = e->U;
+  if (u_stride) *u_stride = e->ustride();
+  if (ldu) *ldu = e->ld;
+  if (v) *v = e->V;
+  if (v_stride) *v_stride = e->vstride();
+  if (ldv) *ldv = e->ld;
+  if (s) *s = e->s;
+  if (lds) *lds = e->ld;
+  if (a) *a = e->A;
+  if (a_stride) *a_stride = e->astride();
+  if (lda) *lda = e->n_cap;
+  return ISVD_OK;
+}
+
+int isvd_engine_set_timing(isvd_engine* e, int on) {
+  if (!e) { set_error("null engine"); return ISVD_EINVAL; }
+  e->timing = on != 0;
+  return ISVD_OK;
+}
+
+int isvd_engine_phase_times(isvd_engine* e, double* ms, int64_t* ticks) {
+  if (!e || !ms) { set_error("bad argument"); return ISVD_EINVAL; }
+  ISVD_CUDA(cudaStreamSynchronize(e->st));
+  for (int p = 0; p < 4; ++p) ms[p] = 0.0;
+  const size_t nt = e->ev_marks.size() / 5;
+  for (size_t t = 0; t < nt; ++t)
+    for (int p = 0; p < 4; ++p) {
+      float f = 0.f;
+      ISVD_CUDA(cudaEventElapsedTime(&f, e->ev_marks[t * 5 + p], e->ev_marks[t * 5 + p + 1]));
+      ms[p] += f;
+    }
+  if (ticks) *ticks = e->timed_ticks;
+  for (auto ev : e->ev_marks) e->ev_pool.push_back(ev);
+  e->ev_marks.clear();
+  e->timed_ticks = 0;
+  return ISVD_OK;
+}
+
+int isvd_engine_canonicalize(isvd_engine* e) {
+  if (!e) { set_error("null engine"); return ISVD_EINVAL; }
+  return e->canonicalize();
+}
+
+int isvd_engine_synchronize(isvd_engine* e) {
+  if (!e) { set_error("null engine"); return ISVD_EINVAL; }
+  ISVD_CUDA(cudaStreamSynchronize(e->st));
+  return ISVD_OK;
+}
+
+// ------------------------------------------------------------------ metrics
+
+int isvd_engine_frob_error(isvd_engine* e, double* out) {
+  if (!e || !e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
+  ISVD_TRY(e->ensure_work(0, 0, (int64_t)e->B * frob_nblk(e->m), e->B));
+  ISVD_TRY(launch_frob_error_sq(e->B, e->m, e->n, e->r, e->A, e->astride(), e->n_cap, e->Um(), e->s,
+                                e->ld, e->Vm(), e->wpart, e->wout, e->st));
+  ISVD_CUDA(cudaMemcpyAsync(out, e->wout, sizeof(double) * e->B, cudaMemcpyDeviceToHost, e->st));
+  ISVD_CUDA(cudaStreamSynchronize(e->st));
+  for (int b = 0; b < e->B; ++b) out[b] = std::sqrt(out[b]);
+  return ISVD_OK;
+}
+
+static int gram_defect(isvd_engine* e, Mat X, int rows, int w, double* host_out) {
+  ISVD_TRY(e->ensure_work(0, 0, (int64_t)e->B * gram_nblk(rows) * w * w, (int64_t)e->B * w * w + e->B));
+  ISVD_TRY(launch_gram(e->B, rows, w, w, X, X, e->wpart, e->wout, e->st));
+  ISVD_TRY(launch_defect(e->B, w, e->wout, e->wout + (int64_t)e->B * w * w, e->st));
+  ISVD_CUDA(cudaMemcpyAsync(host_out, e->wout + (int64_t)e->B * w * w, sizeof(double) * e->B,
+                            cudaMemcpyDeviceToHost, e->st));
+  ISVD_CUDA(cudaStreamSynchronize(e->st));
+  return ISVD_OK;
+}
+
+int isvd_engine_ortho_defect(isvd_engine* e, double* du, double* dv) {
+  if (!e || !e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
+  if (du) ISVD_TRY(gram_defect(e, e->Um(), e->m, e->r, du));
+  if (dv) ISVD_TRY(gram_defect(e, e->Vm(), e->n, e->r, dv));
+  return ISVD_OK;
+}
+
+int isvd_engine_angle(isvd_engine* e, int which, const double* q, int q_cols, int on_device,
+                      double* out) {
+  if (!e || !e->initialized || !out) { set_error("engine not initialised"); return ISVD_ESTATE; }
+  const int B = e->B, m = e->m, r = e->r;
+  Mat Qm;
+  double* qbuf = nullptr;
+  if (which == 0) {
+    if (!e->has_ref || e->ref_m != m || e->ref_r != r) {
+      for (int b = 0; b < B; ++b) out[b] = -1.0;
+      return ISVD_OK;
+    }
+    Qm = Mat{e->ref, (int64_t)e->ref_cap * e->ld, e->ld};
+  } else {
+    if (!q) { set_error("basis is null"); return ISVD_EINVAL; }
+    if (q_cols != r) {
+      set_error("column counts differ: " + std::to_string(r) + " vs " + std::to_string(q_cols));
+      return ISVD_EINVAL;
+    }
+    if (r == 0) { set_error("subspaces must have at least one column"); return ISVD_EINVAL; }
+    if (on_device) {
+      Qm = Mat{const_cast<double*>(q), (int64_t)m * q_cols, q_cols};
+    } else {
+      ISVD_TRY(dalloc(&qbuf, (size_t)B * m * q_cols));
+      cudaMemcpyAsync(qbuf, q, sizeof(double) * B * m * q_cols, cudaMemcpyHostToDevice, e->st);
+      Qm = Mat{qbuf, (int64_t)m * q_cols, q_cols};
+    }
+  }
+  int rc = ISVD_OK;
+  std::vector<double> d1(B), d2(B);
+  rc = gram_defect(e, e->Um(), m, r, d1.data());
+  if (rc == ISVD_OK) rc = gram_defect(e, Qm, m, r, d2.data());
+  if (rc == ISVD_OK) {
+    for (int b = 0; b < B; ++b)
+      if (d1[b] > 1e-6 || d2[b] > 1e-6) {
+        set_error(std::string(d1[b] > 1e-6 ? "q1" : "q2") + " is not orthonormal (defect > 1e-6)");
+        rc = ISVD_EINVAL;
+        break;
+      }
+  }
+  if (rc == ISVD_OK) {
+    // C = U^T Q (r x r) -> sigma_min via the core SVD kernel
+    int S = e->S();
+    rc = e->ensure_work(0, 0, (int64_t)B * gram_nblk(m) * r * r, (int64_t)B * r * r + B);
+    if (rc == ISVD_OK) rc = launch_gram(B, m, r, r, e->Um(), Qm, e->wpart, e->wout, e->st);
+    if (rc == ISVD_OK)
+      rc = launch_core_svd(B, r, e->wout, (int64_t)r * r, r, e->uk, e->vk, e->cstride(), S, e->sv,
+                           S, e->vscr, nullptr, e->st);
+    if (rc == ISVD_OK) {
+      std::vector<double> svh((size_t)B * S);
+      cudaMemcpyAsync(svh.data(), e->sv, sizeof(double) * B * S, cudaMemcpyDeviceToHost, e->st);
+      if (cudaStreamSynchronize(e->st) != cudaSuccess) {
+        set_error("angle: device failure");
+        rc = ISVD_ENODEV;
+      } else {
+        for (int b = 0; b < B; ++b) {
+          double cmin = svh[(size_t)b * S + r - 1];
+          out[b] = std::acos(std::min(1.0, std::max(0.0, cmin)));
+        }
+      }
+    }
+  }
+  if (qbuf) {
+    cudaStreamSynchronize(e->st);
+    cudaFree(qbuf);
+  }
+  return rc;
+}
+
+static int oracle_common(int B, int m, int n, const double* a_dev, int64_t a_stride, int lda,
+                         int w_keep, double* s_host, double* u_host, double* vt_host,
+                         cudaStream_t st) {
+  DenseSvdPlan P = dense_svd_plan(m, n);
+  const int nc = P.nc;
+  const int w = std::max(0, std::min(w_keep, nc));
+  const int ldw = round_up(std::max(w, 1), 8);
+  double *x = nullptr, *jac = nullptr, *U = nullptr, *V = nullptr, *sa = nullptr, *sw = nullptr;
+  int* fl = nullptr;
+  std::vector<int> hf(B);
+  int rc = ISVD_OK;
+  auto T = [&](int v) { if (rc == ISVD_OK) rc = v; };
+  T(dalloc(&x, (size_t)B * P.x_elems()));
+  T(dalloc(&jac, (size_t)B * P.j_elems()));
+  T(dalloc(&U, (size_t)B * m * ldw));
+  T(dalloc(&V, (size_t)B * n * ldw));
+  T(dalloc(&sa, (size_t)B * nc));
+  T(dalloc(&sw, (size_t)B * ldw));
+  T(dalloc(&fl, (size_t)B));
+  if (rc == ISVD_OK) {
+    Mat Um{U, (int64_t)m * ldw, ldw}, Vm{V, (int64_t)n * ldw, ldw};
+    T(dense_svd_run(B, m, n, a_dev, a_stride, lda, w, Um, Vm, sw, ldw, sa, nc, x, jac, fl, hf.data(),
+                    st, nullptr));
+    if (w > 0) {
+      T(launch_complete_zero(B, w, sw, ldw, Um, m, Vm, n, st));
+      T(launch_canonicalize(B, w, Um, m, Vm, n, st));
+    }
+    if (rc == ISVD_OK && s_host)
+      T(cudaMemcpyAsync(s_host, sa, sizeof(double) * B * nc, cudaMemcpyDeviceToHost, st) == cudaSuccess
+            ? ISVD_OK : ISVD_ENODEV);
+    if (rc == ISVD_OK && u_host && w > 0)
+      for (int b = 0; b < B && rc == ISVD_OK; ++b)
+        T(cudaMemcpy2DAsync(u_host + (size_t)b * m * w, sizeof(double) * w, U + (size_t)b * m * ldw,
+                            sizeof(double) * ldw, sizeof(double) * w, m, cudaMemcpyDeviceToHost,
+                            st) == cudaSuccess ? ISVD_OK : ISVD_ENODEV);
+    if (rc == ISVD_OK && vt_host && w > 0) {
+      // V (n x w) -> vt (w x n) on the host after download
+      std::vector<double> vh((size_t)n * w);
+      for (int b = 0; b < B && rc == ISVD_OK; ++b) {
+        T(cudaMemcpy2DAsync(vh.data(), sizeof(double) * w, V + (size_t)b * n * ldw, sizeof(double) * ldw,
+                            sizeof(double) * w, n, cudaMemcpyDeviceToHost, st) == cudaSuccess
+              ? ISVD_OK : ISVD_ENODEV);
+        if (cudaStreamSynchronize(st) != cudaSuccess) T(ISVD_ENODEV);
+        for (int t = 0; t < w; ++t)
+          for (int i = 0; i < n; ++i) vt_host[(size_t)b * w * n + (size_t)t * n + i] = vh[(size_t)i * w + t];
+      }
+    }
+    if (cudaStreamSynchronize(st) != cudaSuccess) T(ISVD_ENODEV);
+  }
+  cudaError_t last = cudaStreamSynchronize(st);
+  dfree(x); dfree(jac); dfree(U); dfree(V); dfree(sa); dfree(sw); dfree(fl);
+  if (rc == ISVD_ENODEV && g_err.empty())
+    set_error(std::string("oracle: device failure: ") + cudaGetErrorString(last));
+  return rc;
+}
+
+int isvd_dense_svd(int batch, int m, int n, const double* a, int w_keep, double* s, double* u,
+                   double* vt) {
+  if (batch < 1 || m < 1 || n < 1 || !a) { set_error("bad argument"); return ISVD_EINVAL; }
+  if (!all_finite(a, (size_t)batch * m * n)) { set_error("matrix contains non-finite entries"); return ISVD_EINVAL; }
+  ISVD_TRY(check_device());
+  double* ad = nullptr;
+  ISVD_TRY(dalloc(&ad, (size_t)batch * m * n));
+  cudaStream_t st = 0;
+  int rc = cudaMemcpy(ad, a, sizeof(double) * batch * m * n, cudaMemcpyHostToDevice) == cudaSuccess
+               ? ISVD_OK : ISVD_ENODEV;
+  if (rc == ISVD_OK) rc = oracle_common(batch, m, n, ad, (int64_t)m * n, n, w_keep, s, u, vt, st);
+  cudaDeviceSynchronize();
+  dfree(ad);
+  return rc;
+}
+
+int isvd_engine_oracle(isvd_engine* e, int w_keep, double* s, double* u) {
+  if (!e || !e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
+  return oracle_common(e->B, e->m, e->n, e->A, e->astride(), e->n_cap, w_keep, s, u, nullptr, e->st);
+}
+
+// --------------------------------------------------------- functional kernels
+
+int isvd_core_svd(int batch, int s, const double* core, double* u, double* sv, double* vt,
+                  void* stream) {
+  if (batch < 0 || s < 1 || !core || !u || !sv || !vt) { set_error("bad argument"); return ISVD_EINVAL; }
+  if (s > kCoreMaxS) { set_error("core too large"); return ISVD_EINVAL; }
+  ISVD_TRY(check_device());
+  cudaStream_t st = (cudaStream_t)stream;
+  double* vscr = nullptr;
+  double* vk = nullptr;
+  if (s > kSmemMaxS) ISVD_TRY(dalloc(&vscr, (size_t)batch * s * (s | 1)));
+  ISVD_TRY(dalloc(&vk, (size_t)batch * s * s));
+  int rc = launch_core_svd(batch, s, core, (int64_t)s * s, s, u, vk, (int64_t)s * s, s, sv, s, vscr,
+                           nullptr, st);
+  // vt = V^T
+  if (rc == ISVD_OK) {
+    std::vector<double> h((size_t)batch * s * s);
+    if (cudaMemcpyAsync(h.data(), vk, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess) {
+      set_error("core_svd: device failure");
+      rc = ISVD_ENODEV;
+    } else {
+      std::vector<double> t(h.size());
+      for (int b = 0; b < batch; ++b)
+        for (int i = 0; i < s; ++i)
+          for (int j = 0; j < s; ++j) t[(size_t)b * s * s + j * s + i] = h[(size_t)b * s * s + i * s + j];
+      if (cudaMemcpy(vt, t.data(), sizeof(double) * t.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+        set_error("core_svd: device failure");
+        rc = ISVD_ENODEV;
+      }
+    }
+  }
+  dfree(vscr);
+  dfree(vk);
+  return rc;
+}
+
+// Functional row_append / rank_one: the reference's kernel contract
+// (_kernels_py.py:22-58): raw factors in, raw factors out (no _install).
+static int functional_common(bool is_row, int m, int r, int n, const double* u, const double* s,
+                             const double* vt, const double* x, double tol, int64_t i, int64_t j,
+                             double delta, int keep, double* u_out, double* s_out, double* vt_out,
+                             double* rho) {
+  if (m < 1 || n < 1 || r < 1 || keep < 1 || keep > (is_row ? r + 1 : r) || !u || !s || !vt ||
+      !u_out || !s_out || !vt_out) {
+    set_error("bad argument");
+    return ISVD_EINVAL;
+  }
+  if (!is_row && !(0 <= i && i < m && 0 <= j && j < n)) { set_error("index out of bounds"); return ISVD_EINVAL; }
+  ISVD_TRY(check_device());
+  const int ld = round_up(std::max(r + 1, keep), 8);
+  const int S = ld + 1;
+  if (S > kCoreMaxS) { set_error("rank too large"); return ISVD_EINVAL; }
+  const int mo = is_row ? m + 1 : m;
+  std::vector<double> Uh((size_t)(mo) * ld, 0.0), Vh((size_t)n * ld, 0.0), sh(ld, 0.0);
+  for (int a = 0; a < m; ++a)
+    for (int c = 0; c < r; ++c) Uh[(size_t)a * ld + c] = u[(size_t)a * r + c];
+  for (int c = 0; c < r; ++c)
+    for (int a = 0; a < n; ++a) Vh[(size_t)a * ld + c] = vt[(size_t)c * n + a];
+  for (int c = 0; c < r; ++c) sh[c] = s[c];
+  double *U = nullptr, *V = nullptr, *sd = nullptr, *core = nullptr, *uk = nullptr, *vk = nullptr,
+         *sv = nullptr, *z = nullptr, *inj = nullptr, *rd = nullptr, *xn = nullptr, *xd = nullptr,
+         *N = nullptr, *vscr = nullptr, *dd = nullptr;
+  int64_t *di = nullptr, *dj = nullptr;
+  int rc = ISVD_OK;
+  auto T = [&](int v) { if (rc == ISVD_OK) rc = v; };
+  T(dalloc(&U, Uh.size())); T(dalloc(&V, Vh.size())); T(dalloc(&sd, ld));
+  T(dalloc(&core, (size_t)S * S)); T(dalloc(&uk, (size_t)S * S)); T(dalloc(&vk, (size_t)S * S));
+  T(dalloc(&sv, S)); T(dalloc(&z, n + 8)); T(dalloc(&inj, 1)); T(dalloc(&rd, 1)); T(dalloc(&xn, 1));
+  T(dalloc(&xd, n + 8)); T(dalloc(&N, 1)); T(dalloc(&dd, 1)); T(dalloc(&di, 1)); T(dalloc(&dj, 1));
+  if (S > kSmemMaxS) T(dalloc(&vscr, (size_t)S * (S | 1)));
+  cudaStream_t st = 0;
+  if (rc == ISVD_OK) {
+    cudaMemcpy(U, Uh.data(), sizeof(double) * Uh.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(V, Vh.data(), sizeof(double) * Vh.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(sd, sh.data(), sizeof(double) * ld, cudaMemcpyHostToDevice);
+    cudaMemset(N, 0, sizeof(double));
+    Mat Um{U, 0, ld}, Vm{V, 0, ld};
+    if (is_row) {
+      cudaMemcpy(xd, x, sizeof(double) * n, cudaMemcpyHostToDevice);
+      T(launch_project_append(1, n, r, Vm, xd, n, sd, ld, tol, core, 0, S, z, 0, inj, rd, xn,
+                              nullptr, 0, 0, 0, N, st));
+      T(launch_core_svd(1, r + 1, core, 0, S, uk, vk, 0, S, sv, 0, vscr, nullptr, st));
+      RotJob grow{Um, m, uk, 0, S, nullptr, 0, nullptr, 1};
+      RotJob injj{Vm, n, vk, 0, S, z, 0, inj, 0};
+      T(launch_rotate(1, r, keep, grow, &injj, st));
+    } else {
+      cudaMemcpy(di, &i, sizeof(int64_t), cudaMemcpyHostToDevice);
+      cudaMemcpy(dj, &j, sizeof(int64_t), cudaMemcpyHostToDevice);
+      cudaMemcpy(dd, &delta, sizeof(double), cudaMemcpyHostToDevice);
+      T(launch_rank1_build(1, r, Um, Vm, sd, ld, di, dj, dd, core, 0, S, nullptr, 0, 0, N, st));
+      T(launch_core_svd(1, r, core, 0, S, uk, vk, 0, S, sv, 0, vscr, nullptr, st));
+      RotJob ju{Um, m, uk, 0, S, nullptr, 0, nullptr, 0};
+      RotJob jv{Vm, n, vk, 0, S, nullptr, 0, nullptr, 0};
+      T(launch_rotate(1, r, keep, ju, &jv, st));
+    }
+    if (cudaDeviceSynchronize() != cudaSuccess) {
+      set_error(std::string("functional kernel: ") + cudaGetErrorString(cudaGetLastError()));
+      T(ISVD_ENODEV);
+    }
+  }
+  if (rc == ISVD_OK) {
+    cudaMemcpy(Uh.data(), U, sizeof(double) * (size_t)mo * ld, cudaMemcpyDeviceToHost);
+    cudaMemcpy(Vh.data(), V, sizeof(double) * Vh.size(), cudaMemcpyDeviceToHost);
+    std::vector<double> svh(S);
+    cudaMemcpy(svh.data(), sv, sizeof(double) * S, cudaMemcpyDeviceToHost);
+    for (int a = 0; a < mo; ++a)
+      for (int c = 0; c < keep; ++c) u_out[(size_t)a * keep + c] = Uh[(size_t)a * ld + c];
+    for (int c = 0; c < keep; ++c)
+      for (int a = 0; a < n; ++a) vt_out[(size_t)c * n + a] = Vh[(size_t)a * ld + c];
+    for (int c = 0; c < keep; ++c) s_out[c] = svh[c];
+    if (is_row && rho) cudaMemcpy(rho, rd, sizeof(double), cudaMemcpyDeviceToHost);
+  }
+  dfree(U); dfree(V); dfree(sd); dfree(core); dfree(uk); dfree(vk); dfree(sv); dfree(z); dfree(inj);
+  dfree(rd); dfree(xn); dfree(xd); dfree(N); dfree(dd); dfree(di); dfree(dj); dfree(vscr);
+  return rc;
+}
+
+int isvd_row_append(int m, int r, int n, const double* u, const double* s, const double* vt,
+                    const double* x, double tol, int keep, double* u_out, double* s_out,
+                    double* vt_out, double* rho) {
+  if (!x) { set_error("x is null"); return ISVD_EINVAL; }
+  return functional_common(true, m, r, n, u, s, vt, x, tol, 0, 0, 0.0, keep, u_out, s_out, vt_out, rho);
+}
+
+int isvd_rank_one(int m, int r, int n, const double* u, const double* s, const double* vt, int64_t i,
+                  int64_t j, double delta, int keep, double* u_out, double* s_out, double* vt_out) {
+  return functional_common(false, m, r, n, u, s, vt, nullptr, 0.0, i, j, delta, keep, u_out, s_out,
+                           vt_out, nullptr);
+}
+
+}  // extern "C"

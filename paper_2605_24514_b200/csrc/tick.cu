@@ -1,0 +1,565 @@
+// Per-tick kernels of the incremental update (kernels K1, K3-K6, K9).
+#include "common.cuh"
+#include "core_svd.cuh"
+#include "tick.cuh"
+#include "../../include/isvd.h"
+
+namespace isvd {
+
+namespace {
+
+constexpr int kRMax = kCoreMaxS;  // max factor width handled by the tick kernels
+
+// ---------------------------------------------------------------- K1 + K9
+// One CTA per stream.  Pass 1: p = F^T x (lanes over factor columns, warps
+// over rows, coalesced row reads) fused with the tracked-matrix write and
+// ||x||^2.  Pass 2: z = x - F p (warp per row), rho = ||z||.  Then the
+// (r+1) x (r+1) Brand core [[diag s, 0], [p, rho]] (_kernels.pyx:149-157).
+__global__ void __launch_bounds__(256) project_append_kernel(
+    int rows, int r, Mat F, const double* __restrict__ x, int64_t x_stride,
+    const double* __restrict__ s, int lds, double tol, double* __restrict__ core,
+    int64_t core_stride, int ldcore, double* __restrict__ z, int64_t z_stride,
+    double* __restrict__ inj_scale, double* __restrict__ rho_out, double* __restrict__ xnorm_out,
+    double* __restrict__ A, int64_t a_stride, int64_t a_off, int64_t a_step,
+    double* __restrict__ N) {
+  __shared__ double part[8][kRMax];
+  __shared__ double p[kRMax];
+  __shared__ double red[32];
+  const int b = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const double* Fb = F.p + b * F.stride;
+  const double* xb = x + b * x_stride;
+  double* Ab = A ? A + b * a_stride + a_off : nullptr;
+
+  double acc[(kRMax + 31) / 32];
+#pragma unroll
+  for (int t = 0; t < (kRMax + 31) / 32; ++t) acc[t] = 0.0;
+  double xx = 0.0;
+  for (int c = warp; c < rows; c += nw) {
+    double xc = xb[c];
+    const double* fr = Fb + (int64_t)c * F.ld;
+#pragma unroll
+    for (int t = 0; t < (kRMax + 31) / 32; ++t) {
+      int l = lane + 32 * t;
+      if (l < r) acc[t] = fma(fr[l], xc, acc[t]);
+    }
+    if (lane == 0) {
+      xx = fma(xc, xc, xx);
+      if (Ab) Ab[(int64_t)c * a_step] = xc;
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < (kRMax + 31) / 32; ++t) {
+    int l = lane + 32 * t;
+    if (l < r) part[warp][l] = acc[t];
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < r; l += blockDim.x) {
+    double v = 0.0;
+    for (int w = 0; w < nw; ++w) v += part[w][l];
+    p[l] = v;
+  }
+  double xnorm2 = block_sum(xx, red);  // contains __syncthreads, p visible after
+
+  double zz = 0.0;
+  double* zb = z + b * z_stride;
+  for (int c = warp; c < rows; c += nw) {
+    const double* fr = Fb + (int64_t)c * F.ld;
+    double v = 0.0;
+    for (int l = lane; l < r; l += 32) v = fma(fr[l], p[l], v);
+    v = warp_sum(v);
+    double zc = xb[c] - v;
+    if (lane == 0) {
+      zb[c] = zc;
+      zz = fma(zc, zc, zz);
+    }
+  }
+  double rho = sqrt(block_sum(zz, red));
+  const bool fresh = rho > tol;
+  const int P = r + 1;
+  double* Kb = core + b * core_stride;
+  const double* sb = s + (int64_t)b * lds;
+  for (int idx = threadIdx.x; idx < P * P; idx += blockDim.x) {
+    int i = idx / P, j = idx % P;
+    double v = 0.0;
+    if (i < r) {
+      if (i == j) v = sb[i];
+    } else {
+      v = (j < r) ? p[j] : (fresh ? rho : 0.0);
+    }
+    Kb[i * ldcore + j] = v;
+  }
+  if (threadIdx.x == 0) {
+    inj_scale[b] = fresh ? 1.0 / rho : 0.0;
+    rho_out[b] = rho;
+    xnorm_out[b] = sqrt(xnorm2);
+    N[b] += xnorm2;
+  }
+}
+
+// -------------------------------------------------------------------- K6
+__global__ void rank1_build_kernel(int r, Mat U, Mat V, const double* __restrict__ s, int lds,
+                                   const int64_t* __restrict__ ii, const int64_t* __restrict__ jj,
+                                   const double* __restrict__ delta, double* __restrict__ core,
+                                   int64_t core_stride, int ldcore, double* __restrict__ A,
+                                   int64_t a_stride, int lda, double* __restrict__ N) {
+  __shared__ double a[kRMax], bb[kRMax];
+  const int b = blockIdx.x;
+  const int64_t i = ii[b], j = jj[b];
+  const double d = delta[b];
+  const double* ur = U.p + b * U.stride + i * U.ld;
+  const double* vr = V.p + b * V.stride + j * V.ld;
+  for (int l = threadIdx.x; l < r; l += blockDim.x) {
+    a[l] = ur[l];
+    bb[l] = vr[l];
+  }
+  __syncthreads();
+  double* Kb = core + b * core_stride;
+  const double* sb = s + (int64_t)b * lds;
+  for (int idx = threadIdx.x; idx < r * r; idx += blockDim.x) {
+    int p = idx / r, q = idx % r;
+    double v = d * a[p] * bb[q];  // _kernels.pyx:209-213
+    if (p == q) v += sb[p];
+    Kb[p * ldcore + q] = v;
+  }
+  if (threadIdx.x == 0 && A) {
+    double* e = A + b * a_stride + i * lda + j;
+    double old = *e;
+    *e = old + d;
+    N[b] += 2.0 * d * old + d * d;  // engine.py:164-166
+  }
+}
+
+// ------------------------------------------------------------------ K3/K4
+// X[0:rows, 0:NP) <- X[0:rows, 0:KP) . Qp, DMMA.8x8x4 FP64.
+// k-index permutation: lane (g, q) feeds A[g][q] for k-step kk from input
+// column q*(KP/4)+kk, so each lane reads KP/4 contiguous doubles of its row.
+// B fragments are pre-permuted into shared memory in lane order (one
+// conflict-free LDS.64 per DMMA).
+constexpr int kRotWarps = 8;
+constexpr int kRotRowsPerBlock = 512;
+
+template <int KP>
+__global__ void __launch_bounds__(kRotWarps * 32, 2)
+    rotate_kernel(int r, int keep, int NP, RotJob j0, RotJob j1, int nblk0) {
+  extern __shared__ double smem[];
+  constexpr int KQ = KP / 4;
+  const int NT = NP / 8;
+  double* Qf = smem;             // [KQ][NT][32]
+  double* Qr = smem + KQ * NT * 32;  // [NP] last core row (inject / new row)
+  const bool second = blockIdx.x >= nblk0;
+  const RotJob& J = second ? j1 : j0;
+  const int blk = second ? blockIdx.x - nblk0 : blockIdx.x;
+  const int b = blockIdx.y;
+  const double* Q = J.Q + b * J.q_stride;
+  const bool has_last = (J.z != nullptr) || J.new_row;
+
+  for (int idx = threadIdx.x; idx < KQ * NT * 32; idx += blockDim.x) {
+    int ln = idx & 31, nn = (idx >> 5) % NT, kk = (idx >> 5) / NT;
+    int g = ln >> 2, q = ln & 3;
+    int l = q * KQ + kk, c = nn * 8 + g;
+    Qf[idx] = (l < r && c < keep) ? Q[l * J.ldq + c] : 0.0;
+  }
+  for (int c = threadIdx.x; c < NP; c += blockDim.x)
+    Qr[c] = (has_last && c < keep) ? Q[r * J.ldq + c] : 0.0;
+  __syncthreads();
+
+  double* X = J.X.p + b * J.X.stride;
+  const int ld = J.X.ld;
+  if (J.new_row && blk == 0) {
+    double* nr = X + (int64_t)J.rows * ld;
+    for (int c = threadIdx.x; c < ld; c += blockDim.x) nr[c] = c < NP ? Qr[c] : 0.0;
+  }
+  const double zscale = J.z ? J.inj_scale[b] : 0.0;
+  const double* zb = J.z ? J.z + b * J.z_stride : nullptr;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int row_begin = blk * kRotRowsPerBlock;
+  const int row_end = min(J.rows, row_begin + kRotRowsPerBlock);
+  const double* qf = Qf + lane;
+
+  int row0 = row_begin + warp * 8;
+  double a[KQ];
+  auto load = [&](int r0, double* dst) {
+    int row = r0 + g;
+    if (row < row_end) {
+      const double* src = X + (int64_t)row * ld + q * KQ;
+      if constexpr (KQ % 2 == 0) {
+#pragma unroll
+        for (int kk = 0; kk < KQ; kk += 2) {
+          double2 v = *reinterpret_cast<const double2*>(src + kk);
+          dst[kk] = v.x;
+          dst[kk + 1] = v.y;
+        }
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < KQ; ++kk) dst[kk] = src[kk];
+      }
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < KQ; ++kk) dst[kk] = 0.0;
+    }
+  };
+  if (row0 < row_end) load(row0, a);
+  for (; row0 < row_end; row0 += kRotWarps * 8) {
+    double an[KQ];
+    const int nxt = row0 + kRotWarps * 8;
+    if (nxt < row_end) load(nxt, an);
+    const int row = row0 + g;
+    const double zr = (zb && row < row_end) ? zb[row] * zscale : 0.0;
+    for (int nn = 0; nn < NT; ++nn) {
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < KQ; ++kk) dmma_8x8x4(d0, d1, a[kk], qf[(kk * NT + nn) * 32]);
+      const int c0 = nn * 8 + 2 * q;
+      if (zb) {
+        d0 = fma(zr, Qr[c0], d0);
+        d1 = fma(zr, Qr[c0 + 1], d1);
+      }
+      if (row < row_end)
+        *reinterpret_cast<double2*>(X + (int64_t)row * ld + c0) = make_double2(d0, d1);
+    }
+    if (nxt < row_end) {
+#pragma unroll
+      for (int kk = 0; kk < KQ; ++kk) a[kk] = an[kk];
+    }
+  }
+}
+
+// ----------------------------------------------------- completion (_install)
+__device__ void complete_column(double* X, int64_t ld, int rows, int w, int t, double* coef,
+                                double* red) {
+  // engine.py:33-56: first the existing direction projected off the others,
+  // then e_0, e_1, ... until the residual norm exceeds 0.5.
+  // coef[c] = <X[:, c], X[:, t]> with a fixed-order block reduction
+  for (int c = 0; c < w; ++c) {
+    double acc = 0.0;
+    if (c != t)
+      for (int i = threadIdx.x; i < rows; i += blockDim.x) acc = fma(X[i * ld + c], X[i * ld + t], acc);
+    double v = block_sum(acc, red);
+    if (threadIdx.x == 0) coef[c] = (c != t) ? v : 0.0;
+  }
+  __syncthreads();
+  double nn = 0.0;
+  for (int i = threadIdx.x; i < rows; i += blockDim.x) {
+    double v = X[i * ld + t];
+    for (int c = 0; c < w; ++c)
+      if (c != t) v -= X[i * ld + c] * coef[c];
+    nn = fma(v, v, nn);
+  }
+  double nrm = sqrt(block_sum(nn, red));
+  if (nrm > 0.5) {
+    for (int i = threadIdx.x; i < rows; i += blockDim.x) {
+      double v = X[i * ld + t];
+      for (int c = 0; c < w; ++c)
+        if (c != t) v -= X[i * ld + c] * coef[c];
+      X[i * ld + t] = v / nrm;
+    }
+    __syncthreads();
+    return;
+  }
+  for (int axis = 0; axis < rows; ++axis) {
+    // cand = e_axis - sum_{c != t} X[:, c] X[axis, c]
+    double cn = 0.0;
+    for (int i = threadIdx.x; i < rows; i += blockDim.x) {
+      double v = (i == axis) ? 1.0 : 0.0;
+      for (int c = 0; c < w; ++c)
+        if (c != t) v -= X[i * ld + c] * X[axis * ld + c];
+      cn = fma(v, v, cn);
+    }
+    double cnrm = sqrt(block_sum(cn, red));
+    if (cnrm > 0.5) {
+      // stage the axis row first: column t of row `axis` is overwritten below
+      for (int c = threadIdx.x; c < w; c += blockDim.x) coef[c] = X[axis * ld + c];
+      __syncthreads();
+      for (int i = threadIdx.x; i < rows; i += blockDim.x) {
+        double v = (i == axis) ? 1.0 : 0.0;
+        for (int c = 0; c < w; ++c)
+          if (c != t) v -= X[i * ld + c] * coef[c];
+        X[i * ld + t] = v / cnrm;
+      }
+      __syncthreads();
+      return;
+    }
+  }
+}
+
+__global__ void complete_zero_kernel(int w, const double* __restrict__ s, int lds, Mat U, int m,
+                                     Mat V, int n) {
+  extern __shared__ double coef[];  // [w]
+  __shared__ double red[32];
+  const int b = blockIdx.x;
+  const double* sb = s + (int64_t)b * lds;
+  for (int t = 0; t < w; ++t) {
+    if (sb[t] != 0.0) continue;
+    for (int side = 0; side < 2; ++side) {
+      double* X = side == 0 ? U.p + b * U.stride : V.p + b * V.stride;
+      int64_t ld = side == 0 ? U.ld : V.ld;
+      int rows = side == 0 ? m : n;
+      double nn = 0.0;
+      for (int i = threadIdx.x; i < rows; i += blockDim.x) nn = fma(X[i * ld + t], X[i * ld + t], nn);
+      double nsq = block_sum(nn, red);
+      if (fabs(nsq - 1.0) > 1e-6) complete_column(X, ld, rows, w, t, coef, red);
+    }
+  }
+}
+
+// ------------------------------------------------------------------- K5
+// Column chunks of kCanonCols so any width works.
+constexpr int kCanonCols = 64;
+__global__ void canonicalize_kernel(int w, Mat U, int m, Mat V, int n) {
+  __shared__ double bestv[8][kCanonCols];
+  __shared__ int besti[8][kCanonCols];
+  __shared__ int flip[kCanonCols];
+  const int b = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double* Ub = U.p + b * U.stride;
+  double* Vb = V.p + b * V.stride;
+  constexpr int T = kCanonCols / 32;
+  for (int c0 = 0; c0 < w; c0 += kCanonCols) {
+    double bv[T];
+    int bi[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      bv[t] = -1.0;
+      bi[t] = 0;
+    }
+    for (int i = warp; i < m; i += nw) {
+      const double* row = Ub + (int64_t)i * U.ld + c0;
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        int c = lane + 32 * t;
+        if (c0 + c < w) {
+          double v = fabs(row[c]);
+          if (v > bv[t]) {
+            bv[t] = v;
+            bi[t] = i;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      int c = lane + 32 * t;
+      bestv[warp][c] = bv[t];
+      besti[warp][c] = bi[t];
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < kCanonCols; c += blockDim.x) {
+      double v = -1.0;
+      int idx = 0;
+      for (int k = 0; k < nw; ++k) {
+        double vk = bestv[k][c];
+        int ik = besti[k][c];
+        if (vk > v || (vk == v && ik < idx)) {
+          v = vk;
+          idx = ik;
+        }
+      }
+      flip[c] = (c0 + c < w) && Ub[(int64_t)idx * U.ld + c0 + c] < 0.0;
+    }
+    __syncthreads();
+    for (int i = warp; i < m; i += nw) {
+      double* row = Ub + (int64_t)i * U.ld + c0;
+      for (int c = lane; c < kCanonCols; c += 32)
+        if (flip[c]) row[c] = -row[c];
+    }
+    for (int i = warp; i < n; i += nw) {
+      double* row = Vb + (int64_t)i * V.ld + c0;
+      for (int c = lane; c < kCanonCols; c += 32)
+        if (flip[c]) row[c] = -row[c];
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- helpers
+__global__ void copy_rows_kernel(int rows, int cols, const double* __restrict__ src,
+                                 int64_t src_stride, int ld_src, double* __restrict__ dst,
+                                 int64_t dst_stride, int ld_dst) {
+  const int b = blockIdx.y;
+  const double* sb = src + b * src_stride;
+  double* db = dst + b * dst_stride;
+  int64_t total = (int64_t)rows * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = idx / cols, j = idx % cols;
+    db[i * ld_dst + j] = sb[i * ld_src + j];
+  }
+}
+
+__global__ void zero_kernel(double* p, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    p[i] = 0.0;
+}
+
+__global__ void sumsq_kernel(int rows, int cols, const double* __restrict__ a, int64_t a_stride,
+                             int lda, double* __restrict__ out) {
+  __shared__ double red[32];
+  const int b = blockIdx.x;
+  const double* ab = a + b * a_stride;
+  double acc = 0.0;
+  for (int i = threadIdx.x >> 5; i < rows; i += blockDim.x >> 5)
+    for (int j = threadIdx.x & 31; j < cols; j += 32) {
+      double v = ab[(int64_t)i * lda + j];
+      acc = fma(v, v, acc);
+    }
+  double t = block_sum(acc, red);
+  if (threadIdx.x == 0) out[b] = t;
+}
+
+__global__ void check_finite_kernel(size_t n, const double* __restrict__ p, int* flag) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    if (!isfinite(p[i])) *flag = 1;
+}
+
+}  // namespace
+
+int launch_project_append(int batch, int rows, int r, Mat F, const double* x, int64_t x_stride,
+                          const double* s, int lds, double tol, double* core, int64_t core_stride,
+                          int ldcore, double* z, int64_t z_stride, double* inj_scale,
+                          double* rho_out, double* xnorm_out, double* A, int64_t a_stride,
+                          int64_t a_off, int64_t a_step, double* N, cudaStream_t st) {
+  if (r > kRMax) {
+    set_error("factor width exceeds kernel limit");
+    return ISVD_EINVAL;
+  }
+  project_append_kernel<<<batch, 256, 0, st>>>(rows, r, F, x, x_stride, s, lds, tol, core,
+                                               core_stride, ldcore, z, z_stride, inj_scale, rho_out,
+                                               xnorm_out, A, a_stride, a_off, a_step, N);
+  ISVD_LAUNCHED();
+  return ISVD_OK;
+}
+
+int launch_rank1_build(int batch, int r, Mat U, Mat V, const double* s, int lds,
+                       const int64_t* ii, const int64_t* jj, const double* delta, double* core,
+                       int64_t core_stride, int ldcore, double* A, int64_t a_stride, int lda,
+                       double* N, cudaStream_t st) {
+  rank1_build_kernel<<<batch, 128, 0, st>>>(r, U, V, s, lds, ii, jj, delta, core, core_stride,
+                                            ldcore, A, a_stride, lda, N);
+  ISVD_LAUNCHED();
+  return ISVD_OK;
+}
+
+template <int KP>
+static int rotate_dispatch(int batch, int r, int keep, const RotJob& j0, const RotJob* j1,
+                           cudaStream_t st) {
+  const int NP = round_up(keep, 8);
+  const int KQ = KP / 4, NT = NP / 8;
+  size_t smem = sizeof(double) * ((size_t)KQ * NT * 32 + NP);
+  static bool attr = false;
+  if (!attr) {
+    ISVD_CUDA(cudaFuncSetAttribute(rotate_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   160 * 1024));
+    attr = true;
+  }
+  int nb0 = ceil_div(j0.rows, kRotRowsPerBlock);
+  if (j0.new_row && nb0 == 0) nb0 = 1;
+  int nb1 = 0;
+  if (j1) {
+    nb1 = ceil_div(j1->rows, kRotRowsPerBlock);
+    if (j1->new_row && nb1 == 0) nb1 = 1;
+  }
+  if (nb0 + nb1 == 0) return ISVD_OK;
+  dim3 grid(nb0 + nb1, batch);
+  rotate_kernel<KP><<<grid, kRotWarps * 32, smem, st>>>(r, keep, NP, j0, j1 ? *j1 : j0, nb0);
+  ISVD_LAUNCHED();
+  return ISVD_OK;
+}
+
+int launch_rotate(int batch, int r, int keep, const RotJob& j0, const RotJob* j1, cudaStream_t st) {
+  if (batch == 0) return ISVD_OK;
+  int KP = round_up(r < 1 ? 1 : r, 8);
+  if (KP > kRMax || round_up(keep, 8) > j0.X.ld || (j1 && round_up(keep, 8) > j1->X.ld)) {
+    set_error("rotation width exceeds kernel limit / leading dimension");
+    return ISVD_EINVAL;
+  }
+  switch (KP) {
+#define ISVD_ROT_CASE(K) \
+  case K:                \
+    return rotate_dispatch<K>(batch, r, keep, j0, j1, st);
+    ISVD_ROT_CASE(8)
+    ISVD_ROT_CASE(16)
+    ISVD_ROT_CASE(24)
+    ISVD_ROT_CASE(32)
+    ISVD_ROT_CASE(40)
+    ISVD_ROT_CASE(48)
+    ISVD_ROT_CASE(56)
+    ISVD_ROT_CASE(64)
+    ISVD_ROT_CASE(72)
+    ISVD_ROT_CASE(80)
+    ISVD_ROT_CASE(88)
+    ISVD_ROT_CASE(96)
+    ISVD_ROT_CASE(104)
+    ISVD_ROT_CASE(112)
+    ISVD_ROT_CASE(120)
+    ISVD_ROT_CASE(128)
+    ISVD_ROT_CASE(136)
+    ISVD_ROT_CASE(144)
+    ISVD_ROT_CASE(152)
+    ISVD_ROT_CASE(160)
+#undef ISVD_ROT_CASE
+    default:
+      set_error("unsupported rotation width");
+      return ISVD_EINVAL;
+  }
+}
+
+int launch_complete_zero(int batch, int w, const double* s, int lds, Mat U, int m, Mat V, int n,
+                         cudaStream_t st) {
+  if (batch == 0 || w == 0) return ISVD_OK;
+  size_t smem = sizeof(double) * w;
+  if (smem > 48 * 1024) {
+    set_error("complete_zero: width too large");
+    return ISVD_EINVAL;
+  }
+  complete_zero_kernel<<<batch, 256, smem, st>>>(w, s, lds, U, m, V, n);
+  ISVD_LAUNCHED();
+  return ISVD_OK;
+}
+
+int launch_canonicalize(int batch, int w, Mat U, int m, Mat V, int n, cudaStream_t st) {
+  if (batch == 0 || w == 0) return ISVD_OK;
+  canonicalize_kernel<<<batch, 256, 0, st>>>(w, U, m, V, n);
+  ISVD_LAUNCHED();
+  return ISVD_OK;
+}
+
+int launch_copy_rows(int batch, int rows, int cols, const double* src, int64_t src_stride,
+                     int ld_src, double* dst, int64_t dst_stride, int ld_dst, cudaStream_t st) {
+  if (batch == 0 || rows == 0 || cols == 0) return ISVD_OK;
+  int64_t total = (int64_t)rows * cols;
+  int gx = (int)std::min<int64_t>((total + 255) / 256, 4096);
+  copy_rows_kernel<<<dim3(gx, batch), 256, 0, st>>>(rows, cols, src, src_stride, ld_src, dst,
+                                                    dst_stride, ld_dst);
+  ISVD_LAUNCHED();
+  return ISVD_OK;
+}
+
+int launch_zero(double* p, size_t n, cudaStream_t st) {
+  if (n == 0) return ISVD_OK;
+  int g = (int)std::min<size_t>((n + 255) / 256, 8192);
+  zero_kernel<<<g, 256, 0, st>>>(p, n);
+  ISVD_LAUNCHED();
+  return ISVD_OK;
+}
+
+int launch_sumsq(int batch, int rows, int cols, const double* a, int64_t a_stride, int lda,
+                 double* out, cudaStream_t st) {
+  sumsq_kernel<<<batch, 512, 0, st>>>(rows, cols, a, a_stride, lda, out);
+  ISVD_LAUNCHED();
+  return ISVD_OK;
+}
+
+int launch_check_finite(size_t n, const double* p, int* flag, cudaStream_t st) {
+  if (n == 0) return ISVD_OK;
+  int g = (int)std::min<size_t>((n + 255) / 256, 4096);
+  check_finite_kernel<<<g, 256, 0, st>>>(n, p, flag);
+  ISVD_LAUNCHED();
+  return ISVD_OK;
+}
+
+}  // namespace isvd

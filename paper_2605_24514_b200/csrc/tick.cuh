@@ -1,0 +1,66 @@
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace isvd {
+
+// Strided view of B per-stream matrices: X[b] = base + b*stride, row pitch ld.
+struct Mat {
+  double* p;
+  int64_t stride;
+  int ld;
+};
+
+// K1 (+ core build, K9 tracked-matrix write, N update) for appends.
+// F[b] (rows x r, row-major pitch F.ld) is the factor whose row space the
+// appended vector x[b] (length rows) is projected on: V for a row append,
+// U for a column append (engine.py:137-139 transpose trick).
+int launch_project_append(int batch, int rows, int r, Mat F, const double* x, int64_t x_stride,
+                          const double* s, int lds, double tol, double* core, int64_t core_stride,
+                          int ldcore, double* z, int64_t z_stride, double* inj_scale,
+                          double* rho_out, double* xnorm_out, double* A, int64_t a_stride,
+                          int64_t a_off, int64_t a_step, double* N, cudaStream_t st);
+
+// K6: rank-1 core K = diag(s) + delta U[i,:]^T V[j,:] plus the tracked entry
+// update A[i,j] += delta and N += 2 delta a_old + delta^2 (engine.py:162-166).
+int launch_rank1_build(int batch, int r, Mat U, Mat V, const double* s, int lds,
+                       const int64_t* ii, const int64_t* jj, const double* delta, double* core,
+                       int64_t core_stride, int ldcore, double* A, int64_t a_stride, int lda,
+                       double* N, cudaStream_t st);
+
+// One rotation job: X[b][0:rows, 0:keep] = X[b][0:rows, 0:r] . Q[b][0:r, 0:keep]
+//   (+ z[b][i] * inj_scale[b] * Q[b][r, c])      if z != nullptr
+//   and X[b][rows, 0:keep] = Q[b][r, 0:keep]       if new_row
+// in place (each output row depends only on the same input row).
+struct RotJob {
+  Mat X;
+  int rows;
+  const double* Q;
+  int64_t q_stride;
+  int ldq;
+  const double* z;
+  int64_t z_stride;
+  const double* inj_scale;
+  int new_row;
+};
+
+// K3/K4: both factor rotations of a tick in one launch (FP64 DMMA).
+int launch_rotate(int batch, int r, int keep, const RotJob& j0, const RotJob* j1, cudaStream_t st);
+
+// engine.py:59-70 -- repair factor columns paired with exact-zero singular
+// values (no-op launch when none are zero).
+int launch_complete_zero(int batch, int w, const double* s, int lds, Mat U, int m, Mat V, int n,
+                         cudaStream_t st);
+
+// linalg.py:63-75 -- sign canonicalisation of (U, V) per stream.
+int launch_canonicalize(int batch, int w, Mat U, int m, Mat V, int n, cudaStream_t st);
+
+// Copy helpers.
+int launch_copy_rows(int batch, int rows, int cols, const double* src, int64_t src_stride,
+                     int ld_src, double* dst, int64_t dst_stride, int ld_dst, cudaStream_t st);
+int launch_zero(double* p, size_t n, cudaStream_t st);
+int launch_sumsq(int batch, int rows, int cols, const double* a, int64_t a_stride, int lda,
+                 double* out, cudaStream_t st);
+int launch_check_finite(size_t n, const double* p, int* flag, cudaStream_t st);
+
+}  // namespace isvd

@@ -1,0 +1,269 @@
+"""Parity of the CUDA path against the reference: golden trajectories (made
+by the real reference), the CPU oracle on seeded BASELINE-shaped inputs, and
+size-independent properties at the full BASELINE sizes.
+
+Tolerances (BASELINE.json north_star): singular values 1e-9 relative;
+subspace principal angles < 1e-6 rad (sine-based, SURVEY.md 7 hard part 4);
+metric trajectories (error ratio, EVR) 1e-8 relative."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from conftest import rel_err, sine_angle
+from oracle import OracleEngine, kernel_rank_one, kernel_row_append, core_svd_jacobi
+from paper_2605_24514_b200 import BatchedSvdEngine, SvdEngine, _lib, workloads
+from paper_2605_24514_b200.metrics import (angle_to_opt, collect, compute_oracle, error_ratio,
+                                           frob_error)
+
+pytestmark = pytest.mark.gpu
+
+SIGMA_RTOL = 1e-9
+ANGLE_TOL = 1e-6
+TRAJ_RTOL = 1e-8
+
+
+# ------------------------------------------------------- functional kernels
+@pytest.mark.parametrize("s", [1, 2, 5, 9, 16, 33, 64, 65, 129])
+def test_core_svd_contract(s):
+    import torch
+
+    rng = np.random.default_rng(s)
+    cores = rng.standard_normal((3, s, s))
+    cores[2, -1, :] = 0.0  # a dead direction (_kernels.pyx:62-79 completion)
+    d = torch.tensor(cores, device="cuda")
+    u, vt = torch.empty_like(d), torch.empty_like(d)
+    sv = torch.empty((3, s), dtype=torch.float64, device="cuda")
+    lib = _lib.load()
+    _lib.check(lib.isvd_core_svd(3, s, d.data_ptr(), u.data_ptr(), sv.data_ptr(), vt.data_ptr(),
+                                 None))
+    torch.cuda.synchronize()
+    u, sv, vt = u.cpu().numpy(), sv.cpu().numpy(), vt.cpu().numpy()
+    for b in range(3):
+        ref = np.linalg.svd(cores[b], compute_uv=False)
+        np.testing.assert_allclose((u[b] * sv[b]) @ vt[b], cores[b], atol=1e-12 * max(1, s))
+        assert np.all(np.diff(sv[b]) <= 0)
+        assert np.linalg.norm(u[b].T @ u[b] - np.eye(s)) <= 1e-12 * max(1, s)
+        assert np.linalg.norm(vt[b] @ vt[b].T - np.eye(s)) <= 1e-12 * max(1, s)
+        live = ref > 1e-12 * ref[0]
+        assert rel_err(sv[b][live], ref[live]) < 1e-10
+    assert sv[2][-1] == 0.0
+
+
+def _functional_row_append(u, s, vt, x, tol, keep):
+    lib = _lib.load()
+    m, r = u.shape
+    n = vt.shape[1]
+    uo, so, vto = np.empty((m + 1, keep)), np.empty(keep), np.empty((keep, n))
+    rho = C.c_double()
+    _lib.check(lib.isvd_row_append(m, r, n, _lib.dptr(np.ascontiguousarray(u)), _lib.dptr(s),
+                                   _lib.dptr(np.ascontiguousarray(vt)), _lib.dptr(x), tol, keep,
+                                   _lib.dptr(uo), _lib.dptr(so), _lib.dptr(vto), C.byref(rho)))
+    return uo, so, vto, rho.value
+
+
+def _functional_rank_one(u, s, vt, i, j, d, keep):
+    lib = _lib.load()
+    m, r = u.shape
+    n = vt.shape[1]
+    uo, so, vto = np.empty((m, keep)), np.empty(keep), np.empty((keep, n))
+    _lib.check(lib.isvd_rank_one(m, r, n, _lib.dptr(np.ascontiguousarray(u)), _lib.dptr(s),
+                                 _lib.dptr(np.ascontiguousarray(vt)), i, j, d, keep, _lib.dptr(uo),
+                                 _lib.dptr(so), _lib.dptr(vto)))
+    return uo, so, vto
+
+
+def test_functional_kernels_match_reference_golden(golden):
+    u, s, vt, x = (golden[k] for k in ("ra_in_u", "ra_in_s", "ra_in_vt", "ra_in_x"))
+    u2, s2, vt2, rho = _functional_row_append(u, s, vt, x, 1e-10, 5)
+    for flavour in ("compiled", "python"):
+        np.testing.assert_allclose(s2, golden[f"ra_{flavour}_s"], rtol=SIGMA_RTOL)
+        np.testing.assert_allclose((u2 * s2) @ vt2, golden[f"ra_{flavour}_recon"], atol=1e-11)
+        assert abs(rho - float(golden[f"ra_{flavour}_rho"])) <= 1e-12
+    u3, s3, vt3 = _functional_rank_one(u, s, vt, 3, 6, 0.25, 4)
+    for flavour in ("compiled", "python"):
+        np.testing.assert_allclose(s3, golden[f"r1_{flavour}_s"], rtol=SIGMA_RTOL)
+        np.testing.assert_allclose((u3 * s3) @ vt3, golden[f"r1_{flavour}_recon"], atol=1e-11)
+
+
+def test_functional_row_append_contracts():
+    rng = np.random.default_rng(1)
+    a = rng.standard_normal((6, 5))
+    f = np.linalg.svd(a, full_matrices=False)
+    x = rng.standard_normal(5)
+    u, s, vt, rho = _functional_row_append(f[0], f[1], f[2], x, 1e-10, 5)
+    stacked = np.vstack([a, x[None, :]])
+    assert rho > 0.0
+    assert np.allclose((u * s) @ vt, stacked, atol=1e-9)
+    # in-span row -> rho <= tol branch, exactly one zero sigma
+    g = np.random.default_rng(4)
+    b = g.standard_normal((7, 3)) @ g.standard_normal((3, 6))
+    uu, ss, vv = np.linalg.svd(b, full_matrices=False)
+    uu, ss, vv = uu[:, :3], ss[:3], vv[:3]
+    x = np.array([0.4, -1.1, 0.3]) @ vv
+    u2, s2, vt2, rho = _functional_row_append(uu, ss, vv, x, 1e-10, 4)
+    assert rho <= 1e-10 and s2[-1] == 0.0 and np.count_nonzero(s2) == 3
+
+
+def test_functional_rank_one_projection():
+    rng = np.random.default_rng(2)
+    b = rng.standard_normal((8, 3)) @ rng.standard_normal((3, 6))
+    uu, ss, vv = np.linalg.svd(b, full_matrices=False)
+    u, s, vt = uu[:, :3], ss[:3], vv[:3]
+    u2, s2, vt2 = _functional_rank_one(u, s, vt, 5, 2, 0.7, 3)
+    bump = np.zeros((8, 6))
+    bump[5, 2] = 0.7
+    proj = (u @ u.T) @ ((u * s) @ vt + bump) @ (vt.T @ vt)
+    assert np.allclose((u2 * s2) @ vt2, proj, atol=1e-10)
+
+
+@pytest.mark.parametrize("keep", [3, 4])
+def test_functional_matches_oracle_kernels(keep):
+    rng = np.random.default_rng(keep)
+    b = rng.standard_normal((50, 3)) @ rng.standard_normal((3, 40)) + 0.1 * rng.standard_normal((50, 40))
+    uu, ss, vv = np.linalg.svd(b, full_matrices=False)
+    u, s, vt = uu[:, :3].copy(), ss[:3].copy(), vv[:3].copy()
+    x = rng.standard_normal(40)
+    g = _functional_row_append(u, s, vt, x, 1e-10, keep)
+    o = kernel_row_append(u, s, vt, x, 1e-10, keep, core_svd_jacobi)
+    assert rel_err(g[1], o[1]) < SIGMA_RTOL
+    np.testing.assert_allclose((g[0] * g[1]) @ g[2], (o[0] * o[1]) @ o[2], atol=1e-11)
+
+
+# ------------------------------------------------------- golden trajectories
+def _run_traj(a0, events, k, kind=None, period=None, gamma=None, theta=None):
+    eng = SvdEngine(a0, k)
+    eng.set_reference()
+    recs = []
+    for t, ev in enumerate(events, start=1):
+        if ev[0] == "row":
+            eng.row_append(ev[1])
+        elif ev[0] == "col":
+            eng.col_append(ev[1])
+        else:
+            eng.rank_one_update(ev[1], ev[2], ev[3])
+        orc = compute_oracle(eng, eng.work_rank)
+        fire = False
+        if kind == "periodic":
+            fire = t % period == 0
+        elif kind == "error":
+            r = error_ratio(frob_error(eng), orc.frob_opt)
+            fire = (not np.isnan(r)) and r > gamma
+        elif kind == "angle":
+            fire = angle_to_opt(eng, orc.basis) > theta
+        if fire:
+            eng.refresh(store_reference=True)
+        rec = collect(eng, 0.0, fire, orc)
+        recs.append([rec.frob_error, rec.evr, rec.rank, float(rec.refreshed), rec.frob_opt,
+                     rec.frob_ratio if rec.frob_ratio is not None else np.nan, rec.angle_opt])
+    return np.array(recs), eng
+
+
+def _check(golden, tag, recs, eng):
+    ref = golden[f"traj_{tag}_records"]
+    np.testing.assert_array_equal(recs[:, 2:4], ref[:, 2:4])
+    np.testing.assert_allclose(recs[:, [0, 1, 4]], ref[:, [0, 1, 4]], rtol=TRAJ_RTOL, atol=1e-12)
+    ok = ~np.isnan(ref[:, 5])
+    np.testing.assert_array_equal(np.isnan(recs[:, 5]), ~ok)
+    np.testing.assert_allclose(recs[ok, 5], ref[ok, 5], rtol=TRAJ_RTOL)
+    f = eng.factors
+    np.testing.assert_allclose(f.s, golden[f"traj_{tag}_s"], rtol=SIGMA_RTOL)
+    assert sine_angle(f.u, golden[f"traj_{tag}_u"]) < ANGLE_TOL
+    assert sine_angle(f.vt.T, golden[f"traj_{tag}_vt"].T) < ANGLE_TOL
+    np.testing.assert_allclose(f.u, golden[f"traj_{tag}_u"], atol=1e-7)  # canonical signs
+    assert abs(eng.sq_norm - float(golden[f"traj_{tag}_sq_norm"])) <= 1e-12 * eng.sq_norm
+
+
+def test_golden_cfg1(golden):
+    a0, ev, _ = workloads.cfg1(0, n_events=120)
+    recs, eng = _run_traj(a0, ev, 10, "periodic", period=100)
+    _check(golden, "cfg1", recs, eng)
+
+
+def test_golden_cfg2(golden):
+    a0, ev, _ = workloads.cfg2(0, n_events=60)
+    recs, eng = _run_traj(a0, ev, 20, "error", gamma=1.05)
+    _check(golden, "cfg2", recs, eng)
+
+
+def test_golden_cfg3(golden):
+    a0, ev, _ = workloads.cfg3(0, t_total=352)
+    recs, eng = _run_traj(a0, ev, 5, "angle", theta=float(np.deg2rad(5.0)))
+    _check(golden, "cfg3", recs, eng)
+
+
+def test_golden_mixed(golden):
+    from test_oracle_golden import _mixed_events
+
+    recs, eng = _run_traj(golden["traj_mixed_a0"], _mixed_events(golden), 6)
+    _check(golden, "mixed", recs, eng)
+
+
+# ------------------------------------------------------------- batched 5a
+def test_cfg5a_batched_matches_oracle(golden):
+    """8 sampled streams, 64 interleaved events each, through the batched
+    engine vs one oracle engine per stream; streams 0 and 1 also against the
+    reference's own golden output."""
+    B, T = 8, 64
+    a0, ticks, streams = workloads.cfg5a_batch(0, B, n_events=T)
+    eng = BatchedSvdEngine(a0, 32, m_cap=1024 + T)
+    for tk in ticks:
+        if tk[0] == "row":
+            eng.row_append(tk[1])
+        else:
+            eng.rank_one_update(tk[1], tk[2], tk[3])
+    for b in range(B):
+        oe = OracleEngine(streams[b][0], 32)
+        for e in streams[b][1]:
+            if e[0] == "row":
+                oe.row_append(e[1])
+            else:
+                oe.rank_one_update(e[1], e[2], e[3])
+        f = eng.factors(b)
+        assert rel_err(f.s, oe.factors.s) < SIGMA_RTOL
+        assert sine_angle(f.u, oe.factors.u) < ANGLE_TOL
+        assert sine_angle(f.vt.T, oe.factors.vt.T) < ANGLE_TOL
+        assert np.array_equal(eng.tracked(b), oe.tracked)
+        if b < 2:
+            assert rel_err(f.s, golden[f"s5a_{b}_s"]) < SIGMA_RTOL
+            np.testing.assert_allclose(f.u[:64], golden[f"s5a_{b}_u"], atol=1e-8)
+    sq, rho, xn = eng.scalars()
+    for b in range(B):
+        assert abs(sq[b] - float(np.sum(eng.tracked(b) ** 2))) <= 1e-12 * sq[b]
+
+
+def test_cfg5a_full_length_properties():
+    """Full 1024-event streams (BASELINE config 5a shape) on a 16-stream
+    batch: size-independent properties (orthonormality, N_t identity,
+    optimality of the truncation error) plus oracle parity on two streams."""
+    B, T = 16, 1024
+    a0, ticks, streams = workloads.cfg5a_batch(1, B, n_events=T)
+    eng = BatchedSvdEngine(a0, 32, m_cap=1024 + T // 2)
+    for tk in ticks:
+        if tk[0] == "row":
+            eng.row_append(tk[1])
+        else:
+            eng.rank_one_update(tk[1], tk[2], tk[3])
+    assert eng.shape == (1536, 256)
+    du, dv = eng.ortho_defect()
+    assert np.all(du <= 1e-8) and np.all(dv <= 1e-8)
+    sq, _, _ = eng.scalars()
+    err = eng.frob_error()
+    s_all, _ = eng.oracle(32)
+    opt = np.sqrt(np.sum(s_all[:, 32:] ** 2, axis=1))
+    for b in range(B):
+        direct = float(np.sum(eng.tracked(b) ** 2))
+        assert abs(sq[b] - direct) <= 1e-9 * direct
+        assert err[b] >= opt[b] - 1e-9
+        assert err[b] / opt[b] < 1.2
+    for b in (0, B - 1):
+        oe = OracleEngine(streams[b][0], 32)
+        for e in streams[b][1]:
+            if e[0] == "row":
+                oe.row_append(e[1])
+            else:
+                oe.rank_one_update(e[1], e[2], e[3])
+        f = eng.factors(b)
+        assert rel_err(f.s, oe.factors.s) < SIGMA_RTOL
+        assert sine_angle(f.u, oe.factors.u) < ANGLE_TOL
