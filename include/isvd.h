@@ -143,6 +143,11 @@ int isvd_engine_synchronize(isvd_engine* e);
  * returns the summed milliseconds of the ticks recorded since the last call
  * and resets the record. */
 int isvd_engine_set_timing(isvd_engine* e, int on);
+/* Verification hook: 1 = factor append cores with the generic one-sided
+ * Jacobi kernel (the reference's compiled algorithm), 0 (default) = the
+ * secular-equation kernel for the broken-arrow core.  Both are exact SVDs;
+ * the parity tests run both. */
+int isvd_engine_set_append_solver(isvd_engine* e, int jacobi);
 int isvd_engine_phase_times(isvd_engine* e, double* ms4, int64_t* ticks);
 
 /* 3. Metrics (metrics.py:56-145, linalg.py:126-153) ------------------------- */

@@ -1,0 +1,394 @@
+// K2a -- SVD of the Brand append core by the secular equation (O(s^2)).
+//
+// The append core of _kernels.pyx:149-157 / _kernels_py.py:36-42 is a
+// "broken arrow":   K = [[diag(d), 0], [p^T, rho]]   (s = r + 1).
+// Its squared singular values are the eigenvalues of K^T K =
+// diag(d^2, 0) + z z^T with z = (p, rho), i.e. the roots of the secular
+// equation  f(sigma) = 1 + sum_j z_j^2 / (delta_j^2 - sigma^2) = 0  with poles
+// delta = (d, 0).  The reference obtains the same factorisation with a
+// cyclic Jacobi sweep (O(s^3) per core, _kernels.pyx:22-59) or LAPACK gesdd;
+// this kernel returns the same singular triplets (to rounding) with:
+//   1. deflation: |z_j| <= tol -> sigma = delta_j with unit vectors; poles
+//      closer than tol merged by a Givens rotation; all poles <= tol form one
+//      zero pole (their z mass rotated into one slot);
+//   2. one thread per root: bracketing by the interval midpoint, origin at the
+//      nearer pole (sigma^2 = delta_o^2 + mu, differences formed without
+//      cancellation), iteration on a two-pole rational model of f with
+//      bisection safeguard;
+//   3. Gu-Eisenstat: z is recomputed from the computed roots (Loewner
+//      formula) so the singular vectors are orthogonal to working precision;
+//   4. v_i ~ zhat_j / (delta_j^2 - sigma_i^2),  u_i ~ (delta_j zhat_j /
+//      (delta_j^2 - sigma_i^2), -1 in the z row), normalised;
+//   5. the reference's output conventions (_kernels.pyx:94-109): descending
+//      sort, snap below 1e-12 sigma_0, dead left columns completed over
+//      e_0, e_1, ... in order.
+#include "common.cuh"
+#include "core_svd.cuh"
+#include "../../include/isvd.h"
+
+namespace isvd {
+
+namespace {
+
+constexpr int kN = kCoreMaxS;  // max core size
+
+struct ArrowSmem {
+  double delta[kN];   // pole value per original column (zero group forced to 0)
+  double z[kN];       // z per original column, updated by the deflation rotations
+  double kd[kN];      // kept poles, ascending
+  double kz[kN];      // their z
+  double zhat[kN];    // Loewner-corrected z
+  double mu[kN];      // root i: sigma_i^2 = kd[org[i]]^2 + mu[i]
+  double sig[kN];     // all n singular values (kept roots then deflated)
+  double rc[kN], rs[kN];
+  int ra[kN], rb[kN], rboth[kN];  // rotation list
+  int kcol[kN];       // kept slot -> original column
+  int org[kN];        // root -> origin index into kd
+  int dcol[kN];       // deflated -> original column
+  int dzero[kN];      // deflated with a zero left direction (completion)
+  int pos[kN];        // triple -> output column (sorted)
+  int order[kN];      // ascending pole order of the original columns
+  int nkept, ndefl, nrot;
+  double scale;
+};
+
+__device__ __forceinline__ void apply_rots(double* col, int64_t stride, const ArrowSmem& S,
+                                           bool left) {
+  // x_orig = G_1 G_2 ... G_k x : apply the last rotation first
+  for (int k = S.nrot - 1; k >= 0; --k) {
+    if (left && !S.rboth[k]) continue;
+    const int a = S.ra[k], b = S.rb[k];
+    const double c = S.rc[k], s = S.rs[k];
+    double xa = col[a * stride], xb = col[b * stride];
+    col[a * stride] = c * xa - s * xb;
+    col[b * stride] = s * xa + c * xb;
+  }
+}
+
+__global__ void __launch_bounds__(kN) arrow_svd_kernel(int n, const double* __restrict__ core,
+                                                       int64_t core_stride, int ldcore,
+                                                       double* __restrict__ uk,
+                                                       double* __restrict__ vk, int64_t out_stride,
+                                                       int ldo, double* __restrict__ sv,
+                                                       int64_t sv_stride) {
+  __shared__ ArrowSmem S;
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int r = n - 1;
+  const double* K = core + b * core_stride;
+  double* U = uk + b * out_stride;
+  double* V = vk + b * out_stride;
+  double* SV = sv + b * sv_stride;
+  const double eps = 2.220446049250313e-16;
+
+  // ---- load, scale
+  for (int c = tid; c < n; c += blockDim.x) {
+    S.delta[c] = c < r ? fabs(K[c * ldcore + c]) : 0.0;
+    S.z[c] = K[r * ldcore + c];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double mx = 0.0;
+    for (int c = 0; c < n; ++c) mx = fmax(mx, fmax(S.delta[c], fabs(S.z[c])));
+    S.scale = mx > 0.0 ? mx : 1.0;
+  }
+  __syncthreads();
+  const double scale = S.scale;
+  for (int c = tid; c < n; c += blockDim.x) {
+    S.delta[c] /= scale;
+    S.z[c] /= scale;
+  }
+  __syncthreads();
+  // ascending order of poles; ties: higher column first (the rho column r
+  // leads the zero group)
+  for (int c = tid; c < n; c += blockDim.x) {
+    double dc = S.delta[c];
+    int rank = 0;
+    for (int e = 0; e < n; ++e) {
+      double de = S.delta[e];
+      rank += (de < dc) || (de == dc && e > c);
+    }
+    S.order[rank] = c;
+  }
+  __syncthreads();
+
+  // ---- deflation (sequential; O(n))
+  if (tid == 0) {
+    const double tol = 8.0 * eps;  // all values scaled to <= 1
+    int nk = 0, nd = 0, nr = 0;
+    // zero group: poles <= tol, combined into the first one (column r)
+    int first = -1;
+    int p = 0;
+    for (; p < n; ++p) {
+      const int c = S.order[p];
+      if (S.delta[c] > tol) break;
+      S.delta[c] = 0.0;
+      if (first < 0) {
+        first = c;
+        continue;
+      }
+      const double z1 = S.z[first], z2 = S.z[c];
+      const double t = hypot(z1, z2);
+      if (t > 0.0) {
+        S.ra[nr] = first; S.rb[nr] = c; S.rc[nr] = z1 / t; S.rs[nr] = z2 / t; S.rboth[nr] = 0;
+        ++nr;
+        S.z[first] = t;
+        S.z[c] = 0.0;
+      }
+      S.dcol[nd] = c; S.dzero[nd] = 1; S.sig[nd] = 0.0;  // sig filled in later slots
+      ++nd;
+    }
+    if (first >= 0) {
+      if (fabs(S.z[first]) <= tol) {
+        S.dcol[nd] = first; S.dzero[nd] = 1; ++nd;
+      } else {
+        S.kcol[nk] = first; S.kd[nk] = 0.0; S.kz[nk] = S.z[first]; ++nk;
+      }
+    }
+    // regular poles, ascending
+    for (; p < n; ++p) {
+      const int c = S.order[p];
+      if (fabs(S.z[c]) <= tol) {
+        S.dcol[nd] = c; S.dzero[nd] = 0; ++nd;
+        continue;
+      }
+      if (nk > 0 && S.kd[nk - 1] > 0.0 && S.delta[c] - S.kd[nk - 1] <= tol) {
+        // merge the previous kept pole into c: zero its z, deflate it
+        const int l = S.kcol[nk - 1];
+        const double zl = S.kz[nk - 1], zc = S.z[c];
+        const double t = hypot(zl, zc);
+        S.ra[nr] = c; S.rb[nr] = l; S.rc[nr] = zc / t; S.rs[nr] = zl / t; S.rboth[nr] = 1;
+        ++nr;
+        S.z[c] = t;
+        S.z[l] = 0.0;
+        --nk;
+        S.dcol[nd] = l; S.dzero[nd] = 0; ++nd;
+      }
+      S.kcol[nk] = c; S.kd[nk] = S.delta[c]; S.kz[nk] = S.z[c]; ++nk;
+    }
+    S.nkept = nk;
+    S.ndefl = nd;
+    S.nrot = nr;
+  }
+  __syncthreads();
+  const int N = S.nkept, ND = S.ndefl;
+
+  // ---- roots: thread i solves for sigma_i in (kd[i], kd[i+1])
+  for (int i = tid; i < N; i += blockDim.x) {
+    int o;
+    double lo, hi;
+    const double di = S.kd[i];
+    if (i < N - 1) {
+      const double dn = S.kd[i + 1];
+      const double sm = 0.5 * (di + dn);
+      const double mum = (sm - di) * (sm + di);
+      double f = 1.0;
+      for (int j = 0; j < N; ++j) {
+        const double dj = S.kd[j];
+        f += S.kz[j] * S.kz[j] / ((dj - di) * (dj + di) - mum);
+      }
+      if (f > 0.0) {
+        o = i; lo = 0.0; hi = mum;
+      } else {
+        o = i + 1; lo = (sm - dn) * (sm + dn); hi = 0.0;
+      }
+    } else {
+      o = i;
+      double zz = 0.0;
+      for (int j = 0; j < N; ++j) zz += S.kz[j] * S.kz[j];
+      lo = 0.0;
+      hi = zz;
+    }
+    const double dorg = S.kd[o];
+    const double Di = (di - dorg) * (di + dorg);
+    const double Dn = (i < N - 1) ? (S.kd[i + 1] - dorg) * (S.kd[i + 1] + dorg) : 0.0;
+    double x = 0.5 * (lo + hi);
+    for (int it = 0; it < 80; ++it) {
+      double psi = 0.0, dpsi = 0.0, phi = 0.0, dphi = 0.0, aps = 0.0;
+      for (int j = 0; j < N; ++j) {
+        const double dj = S.kd[j];
+        const double t = 1.0 / ((dj - dorg) * (dj + dorg) - x);
+        const double w = S.kz[j] * S.kz[j] * t;
+        if (j <= i) {
+          psi += w;
+          dpsi += w * t;
+        } else {
+          phi += w;
+          dphi += w * t;
+        }
+        aps += fabs(w);
+      }
+      const double g = 1.0 + psi + phi;
+      if (g < 0.0) lo = x; else hi = x;
+      if (fabs(g) <= 4.0 * eps * (1.0 + aps) * N || !(g == g)) break;
+      // two-pole rational model through (psi, dpsi) and (phi, dphi)
+      const double pi_ = Di - x;
+      const double b1 = dpsi * pi_ * pi_;
+      const double a1 = psi - b1 / pi_;
+      double xn;
+      if (i < N - 1) {
+        const double qn = Dn - x;
+        const double b2 = dphi * qn * qn;
+        const double a2 = phi - b2 / qn;
+        const double A = 1.0 + a1 + a2;
+        const double Dl = Dn - Di;
+        // A p^2 + (A Dl + b1 + b2) p + b1 Dl = 0 with p = Di - x'
+        const double B = A * Dl + b1 + b2, C = b1 * Dl;
+        const double disc = B * B - 4.0 * A * C;
+        xn = 0.5 * (lo + hi);
+        if (disc >= 0.0) {
+          const double q = -0.5 * (B + copysign(sqrt(disc), B));
+          const double p1 = (A != 0.0) ? q / A : -1e300;
+          const double p2 = (q != 0.0) ? C / q : -1e300;
+          const double x1 = Di - p1, x2 = Di - p2;
+          if (x1 > lo && x1 < hi) xn = x1;
+          else if (x2 > lo && x2 < hi) xn = x2;
+        }
+      } else {
+        const double A = 1.0 + a1 + phi;
+        xn = (A > 0.0) ? Di + b1 / A : 0.5 * (lo + hi);
+        if (!(xn > lo && xn < hi)) xn = 0.5 * (lo + hi);
+      }
+      if (fabs(xn - x) <= 2.0 * eps * fmax(fabs(xn), 1e-300) || hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi))) {
+        x = xn;
+        break;
+      }
+      x = xn;
+    }
+    S.org[i] = o;
+    S.mu[i] = x;
+    S.sig[ND + i] = sqrt(dorg * dorg + x);
+  }
+  // deflated singular values (unscaled positions 0..ND-1)
+  for (int k = tid; k < ND; k += blockDim.x) S.sig[k] = S.dzero[k] ? 0.0 : S.delta[S.dcol[k]];
+  __syncthreads();
+
+  // ---- Loewner: zhat_j^2 = prod_k (sigma_k^2 - d_j^2) / prod_{k != j} (d_k^2 - d_j^2)
+  for (int j = tid; j < N; j += blockDim.x) {
+    const double dj = S.kd[j];
+    auto sdiff = [&](int k) {  // sigma_k^2 - d_j^2, accurate
+      const double dk = S.kd[S.org[k]];
+      return S.mu[k] - (dj - dk) * (dj + dk);
+    };
+    double acc = sdiff(N - 1);
+    for (int k = 0; k < j; ++k) acc *= sdiff(k) / ((S.kd[k] - dj) * (S.kd[k] + dj));
+    for (int k = j; k < N - 1; ++k) acc *= sdiff(k) / ((S.kd[k + 1] - dj) * (S.kd[k + 1] + dj));
+    S.zhat[j] = copysign(sqrt(fmax(acc, 0.0)), S.kz[j]);
+  }
+  // ---- sorted output positions: descending sigma, ties by triple index
+  for (int t = tid; t < n; t += blockDim.x) {
+    const double st = S.sig[t];
+    int rank = 0;
+    for (int e = 0; e < n; ++e) {
+      const double se = S.sig[e];
+      rank += (se > st) || (se == st && e < t);
+    }
+    S.pos[t] = rank;
+  }
+  __syncthreads();
+  const double s0 = S.sig[0] > 0.0 ? 0.0 : 0.0;  // placeholder (max computed below)
+  (void)s0;
+  double smax = 0.0;
+  for (int t = 0; t < n; ++t) smax = fmax(smax, S.sig[t]);
+
+  // ---- vectors, written straight into their sorted columns
+  for (int t = tid; t < n; t += blockDim.x) {
+    const int pc = S.pos[t];
+    double* vcol = V + pc;
+    double* ucol = U + pc;
+    for (int l = 0; l < n; ++l) {
+      vcol[l * ldo] = 0.0;
+      ucol[l * ldo] = 0.0;
+    }
+    const double sg = S.sig[t];
+    const bool dead = !(sg > 0.0) || sg < kZeroSvRtol * smax;
+    if (t < ND) {
+      const int c = S.dcol[t];
+      vcol[c * ldo] = 1.0;
+      apply_rots(vcol, ldo, S, false);
+      if (!S.dzero[t] && !dead) {
+        ucol[c * ldo] = 1.0;
+        apply_rots(ucol, ldo, S, true);
+      }
+    } else {
+      const int i = t - ND;
+      const double dorg = S.kd[S.org[i]];
+      double nv = 0.0, nu = 1.0;  // the z-row entry of u is -1
+      for (int j = 0; j < N; ++j) {
+        const double dj = S.kd[j];
+        const double inv = 1.0 / ((dj - dorg) * (dj + dorg) - S.mu[i]);
+        const double vj = S.zhat[j] * inv;
+        const double uj = dj * vj;
+        nv = fma(vj, vj, nv);
+        nu = fma(uj, uj, nu);
+        vcol[S.kcol[j] * ldo] = vj;
+        if (dj > 0.0) ucol[S.kcol[j] * ldo] = uj;
+      }
+      const double iv = 1.0 / sqrt(nv), iu = 1.0 / sqrt(nu);
+      for (int j = 0; j < N; ++j) {
+        vcol[S.kcol[j] * ldo] *= iv;
+        if (S.kd[j] > 0.0) ucol[S.kcol[j] * ldo] *= iu;
+      }
+      ucol[r * ldo] = -iu;
+      apply_rots(vcol, ldo, S, false);
+      apply_rots(ucol, ldo, S, true);
+      if (dead)
+        for (int l = 0; l < n; ++l) ucol[l * ldo] = 0.0;
+    }
+    SV[pc] = dead ? 0.0 : sg * scale;
+  }
+  __syncthreads();
+
+  // ---- dead-column completion over e_0, e_1, ... (_kernels.pyx:62-79)
+  if (tid < 32) {
+    const int lane = tid;
+    for (int t = 0; t < n; ++t) {
+      if (SV[t] > 0.0) continue;
+      for (int axis = 0; axis < n; ++axis) {
+        double nrm2 = 0.0;
+        for (int i = lane; i < n; i += 32) {
+          double v = (i == axis) ? 1.0 : 0.0;
+          for (int c = 0; c < n; ++c)
+            if (c != t) v -= U[i * ldo + c] * U[axis * ldo + c];
+          nrm2 = fma(v, v, nrm2);
+        }
+        nrm2 = warp_sum(nrm2);
+        const double nrm = sqrt(nrm2);
+        if (nrm > 0.5) {
+          double vals[(kN + 31) / 32];
+          int cnt = 0;
+          for (int i = lane; i < n; i += 32) {
+            double v = (i == axis) ? 1.0 : 0.0;
+            for (int c = 0; c < n; ++c)
+              if (c != t) v -= U[i * ldo + c] * U[axis * ldo + c];
+            vals[cnt++] = v / nrm;
+          }
+          __syncwarp();
+          cnt = 0;
+          for (int i = lane; i < n; i += 32) U[i * ldo + t] = vals[cnt++];
+          __syncwarp();
+          break;
+        }
+      }
+    }
+  }
+}
+
+}  // namespace
+
+int launch_arrow_svd(int batch, int s, const double* core, int64_t core_stride, int ldcore,
+                     double* uk, double* vk, int64_t out_stride, int ldo, double* sv,
+                     int64_t sv_stride, cudaStream_t st) {
+  if (s < 1 || s > kN) {
+    set_error("arrow core size out of range");
+    return ISVD_EINVAL;
+  }
+  if (batch == 0) return ISVD_OK;
+  const int threads = round_up(s, 32);
+  arrow_svd_kernel<<<batch, threads, 0, st>>>(s, core, core_stride, ldcore, uk, vk, out_stride, ldo,
+                                              sv, sv_stride);
+  ISVD_LAUNCHED();
+  return ISVD_OK;
+}
+
+}  // namespace isvd

@@ -19,3 +19,11 @@ int launch_core_svd(int batch, int s, const double* core, int64_t core_stride, i
                     int64_t sv_stride, double* vscratch, const int* active, cudaStream_t st);
 
 }  // namespace isvd
+
+namespace isvd {
+// Secular-equation SVD of the Brand append core [[diag d, 0], [p, rho]]
+// (arrow_svd.cu).  Same outputs and conventions as launch_core_svd.
+int launch_arrow_svd(int batch, int s, const double* core, int64_t core_stride, int ldcore,
+                     double* uk, double* vk, int64_t out_stride, int ldo, double* sv,
+                     int64_t sv_stride, cudaStream_t st);
+}  // namespace isvd

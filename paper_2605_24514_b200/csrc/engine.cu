@@ -110,6 +110,9 @@ struct isvd_engine {
   // phase 0 = K1/K6 project+build, 1 = K2 core SVD, 2 = K3/K4 rotation,
   // 3 = install (s copy + zero-sigma completion)
   bool timing = false;
+  // verification hook: solve append cores with the generic Jacobi kernel
+  // instead of the secular-equation kernel (both are exact SVDs)
+  bool append_jacobi = false;
   std::vector<cudaEvent_t> ev_pool;
   std::vector<cudaEvent_t> ev_marks;  // 5 per recorded tick
   int64_t timed_ticks = 0;
@@ -412,8 +415,12 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
                                  e->cstride(), e->S(), e->z, e->zlen(), e->inj, e->rho, e->xnorm,
                                  e->A, e->astride(), a_off, a_step, e->N, e->st));
   e->mark();
-  ISVD_TRY(launch_core_svd(e->B, r + 1, e->core, e->cstride(), e->S(), e->uk, e->vk, e->cstride(),
-                           e->S(), e->sv, e->S(), e->vscr, nullptr, e->st));
+  if (e->append_jacobi)
+    ISVD_TRY(launch_core_svd(e->B, r + 1, e->core, e->cstride(), e->S(), e->uk, e->vk,
+                             e->cstride(), e->S(), e->sv, e->S(), e->vscr, nullptr, e->st));
+  else
+    ISVD_TRY(launch_arrow_svd(e->B, r + 1, e->core, e->cstride(), e->S(), e->uk, e->vk,
+                              e->cstride(), e->S(), e->sv, e->S(), e->st));
   e->mark();
   // row: U <- [U 0; 0 1] Uk, V <- V Vk[:r] + z^ Vk[r] ; col: the same with U<->V
   RotJob grow{is_row ? e->Um() : e->Vm(), is_row ? e->m : e->n, e->uk, e->cstride(), e->S(),
@@ -640,6 +647,12 @@ int isvd_engine_device_views(isvd_engine* e, double** u, int64_t* u_stride, int*
   if (a) *a = e->A;
   if (a_stride) *a_stride = e->astride();
   if (lda) *lda = e->n_cap;
+  return ISVD_OK;
+}
+
+int isvd_engine_set_append_solver(isvd_engine* e, int jacobi) {
+  if (!e) { set_error("null engine"); return ISVD_EINVAL; }
+  e->append_jacobi = jacobi != 0;
   return ISVD_OK;
 }
 
@@ -935,7 +948,7 @@ static int functional_common(bool is_row, int m, int r, int n, const double* u, 
       cudaMemcpy(xd, x, sizeof(double) * n, cudaMemcpyHostToDevice);
       T(launch_project_append(1, n, r, Vm, xd, n, sd, ld, tol, core, 0, S, z, 0, inj, rd, xn,
                               nullptr, 0, 0, 0, N, st));
-      T(launch_core_svd(1, r + 1, core, 0, S, uk, vk, 0, S, sv, 0, vscr, nullptr, st));
+      T(launch_arrow_svd(1, r + 1, core, 0, S, uk, vk, 0, S, sv, 0, st));
       RotJob grow{Um, m, uk, 0, S, nullptr, 0, nullptr, 1};
       RotJob injj{Vm, n, vk, 0, S, z, 0, inj, 0};
       T(launch_rotate(1, r, keep, grow, &injj, st));

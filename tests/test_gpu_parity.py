@@ -267,3 +267,66 @@ def test_cfg5a_full_length_properties():
         f = eng.factors(b)
         assert rel_err(f.s, oe.factors.s) < SIGMA_RTOL
         assert sine_angle(f.u, oe.factors.u) < ANGLE_TOL
+
+
+# ------------------------------------------- append-core solver cross-checks
+def _solver(eng, jacobi: bool):
+    _lib.check(eng._h.lib.isvd_engine_set_append_solver(eng._h.h, int(jacobi)))
+    return eng
+
+
+HARD_CASES = [
+    ("identity_equal_poles", np.eye(3), 3, [np.array([1.0, 2.0, 3.0])]),
+    ("zero_sigma_present", np.diag([5.0, 0.0]), 2, [np.array([0.3, -0.7])]),
+    ("pythagorean", np.array([[3.0, 0.0], [0.0, 0.0]]), 2, [np.array([4.0, 0.0])]),
+    ("zero_row", np.diag([3.0, 2.0, 1.0]), 3, [np.zeros(3)]),
+    ("rank_deficient_many_zeros", np.outer(np.arange(1.0, 7.0), np.ones(5)), 5,
+     [np.arange(5.0), np.ones(5), np.zeros(5)]),
+    ("repeated_sigma_block", np.kron(np.eye(3), np.ones((2, 2))), 4,
+     [np.linspace(-1, 1, 6), np.full(6, 0.5)]),
+    ("tiny_and_huge", np.diag([1e8, 1.0, 1e-6, 1e-9]), 4, [np.array([1e-3, 2.0, -1e-7, 5.0])]),
+]
+
+
+@pytest.mark.parametrize("name, a0, k, rows", HARD_CASES, ids=[c[0] for c in HARD_CASES])
+def test_append_solver_hard_cases(name, a0, k, rows):
+    """Secular-equation append solver vs the generic Jacobi solver vs the
+    oracle on deflation-heavy cores (equal poles, zero poles, zero z)."""
+    gs = SvdEngine(a0, k)
+    gj = _solver(SvdEngine(a0, k), True)
+    oc = OracleEngine(a0, k)
+    for x in rows:
+        x = np.resize(x, gs.shape[1])
+        gs.row_append(x)
+        gj.row_append(x)
+        oc.row_append(x)
+        yc = np.linspace(0.2, -0.4, gs.shape[0])
+        gs.col_append(yc)
+        gj.col_append(yc)
+        oc.col_append(yc)
+    for g in (gs, gj):
+        f = g.factors
+        fo = oc.factors
+        np.testing.assert_allclose(f.s, fo.s, rtol=1e-9, atol=1e-12 * fo.s[0])
+        np.testing.assert_allclose((f.u * f.s) @ f.vt, (fo.u * fo.s) @ fo.vt,
+                                   atol=1e-10 * max(1.0, fo.s[0]))
+        du, dv = g.ortho_defects()
+        assert du <= 1e-10 and dv <= 1e-10
+
+
+def test_append_solvers_agree_on_streams():
+    rng = np.random.default_rng(77)
+    a0 = rng.standard_normal((80, 40)) @ np.diag(np.logspace(0, -3, 40)) @ rng.standard_normal((40, 40))
+    gs = SvdEngine(a0, 12)
+    gj = _solver(SvdEngine(a0, 12), True)
+    for t in range(200):
+        if t % 2:
+            x = rng.standard_normal(gs.shape[1])
+            gs.row_append(x); gj.row_append(x)
+        else:
+            y = rng.standard_normal(gs.shape[0])
+            gs.col_append(y); gj.col_append(y)
+    fs, fj = gs.factors, gj.factors
+    assert rel_err(fs.s, fj.s) < 1e-11
+    assert sine_angle(fs.u, fj.u) < 1e-9
+    np.testing.assert_allclose(fs.u, fj.u, atol=1e-9)
