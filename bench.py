@@ -281,10 +281,16 @@ def run_gpu(args):
         barrier()
     launches = _lib.launch_count() - l0
     dev_ms = e0.elapsed_time(e1)
-    phase = np.zeros(4)
-    nt = np.zeros(1, dtype=np.int64)
-    _lib.check(lib.isvd_engine_phase_times(eng._h.h, _lib.dptr(phase), nt.ctypes.data_as(
+    ph8 = np.zeros(8)
+    nt2 = np.zeros(2, dtype=np.int64)
+    _lib.check(lib.isvd_engine_phase_times(eng._h.h, _lib.dptr(ph8), nt2.ctypes.data_as(
         __import__("ctypes").POINTER(__import__("ctypes").c_int64))))
+    phase = ph8[:4] + ph8[4:]
+    nt = np.array([nt2.sum()])
+    phase_by_kind = {
+        kind: {name: float(ph8[4 * i + j] / max(1, nt2[i]))
+               for j, name in enumerate(("project", "core_svd", "rotate", "install"))}
+        for i, kind in enumerate(("row_append", "rank_one"))}
     # algorithmic bytes of the timed ticks (dominant kernel = rotation)
     rot_bytes = 0
     all_bytes = 0
@@ -359,6 +365,7 @@ def run_gpu(args):
                                   "core_svd": phase[1] / max(1, nt[0]),
                                   "rotate": phase[2] / max(1, nt[0]),
                                   "install": phase[3] / max(1, nt[0])},
+            "phase_ms_by_event": phase_by_kind,
             "tick_effective_gbs": all_bytes / (t_max / 1e3) / 1e9,
         }
         if world == 1 and not args.no_cpu_baseline:

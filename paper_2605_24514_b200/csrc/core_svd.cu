@@ -179,6 +179,203 @@ __global__ void jacobi_core_kernel(int s, const double* __restrict__ core, int64
   }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-per-core variant for s <= 32 (the rank-1 core of a k <= 32 stream).
+// Lane l holds row l of G and of V in registers.  Ordering: odd-even
+// transposition -- rounds alternate pairs (2k, 2k+1) and (2k+1, 2k+2) and
+// every rotated pair swaps places, so each pair of columns meets exactly once
+// per sweep of 32 rounds and all register indices are compile-time; after a
+// sweep the column order is reversed (tracked for the stable sort).  The 16
+// pair Grams (a_pp, a_qq, a_pq) of a round are reduce-scattered across the
+// warp with shuffles (lane l ends with pair l/2); the rotation (same formulas
+// and threshold as _kernels.pyx:38-57) is computed there and broadcast
+// through shared memory.
+constexpr int kJ32Warps = 4;
+
+template <bool ODD>
+__device__ __forceinline__ void j32_pair_products(const double (&g)[32], int k, double& pp,
+                                                  double& qq, double& pq) {
+  const int p = ODD ? 2 * k + 1 : 2 * k;
+  if (ODD && k == 15) {
+    pp = qq = pq = 0.0;
+    return;
+  }
+  const double x = g[p], y = g[p + 1];
+  pp = x * x;
+  qq = y * y;
+  pq = x * y;
+}
+
+__device__ __forceinline__ void halve(double& keep, double lo, double hi, bool upper, int off) {
+  const double mine = upper ? hi : lo;
+  const double other = upper ? lo : hi;
+  keep = mine + __shfl_xor_sync(0xffffffffu, other, off);
+}
+
+template <bool ODD>
+__device__ __forceinline__ bool j32_round(double (&g)[32], double (&v)[32], int lane,
+                                          double2* cs_sm) {
+  // reduce-scatter of 16 pairs x (pp, qq, pq): lane l ends with pair l >> 1
+  double P[8], Q[8], W[8];
+  const bool b4 = lane & 16;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    double pa, qa, wa, pb, qb, wb;
+    j32_pair_products<ODD>(g, i, pa, qa, wa);
+    j32_pair_products<ODD>(g, i + 8, pb, qb, wb);
+    halve(P[i], pa, pb, b4, 16);
+    halve(Q[i], qa, qb, b4, 16);
+    halve(W[i], wa, wb, b4, 16);
+  }
+  const bool b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    halve(P[i], P[i], P[i + 4], b3, 8);
+    halve(Q[i], Q[i], Q[i + 4], b3, 8);
+    halve(W[i], W[i], W[i + 4], b3, 8);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    halve(P[i], P[i], P[i + 2], b2, 4);
+    halve(Q[i], Q[i], Q[i + 2], b2, 4);
+    halve(W[i], W[i], W[i + 2], b2, 4);
+  }
+  halve(P[0], P[0], P[1], b1, 2);
+  halve(Q[0], Q[0], Q[1], b1, 2);
+  halve(W[0], W[0], W[1], b1, 2);
+  const double app = P[0] + __shfl_xor_sync(0xffffffffu, P[0], 1);
+  const double aqq = Q[0] + __shfl_xor_sync(0xffffffffu, Q[0], 1);
+  const double apq = W[0] + __shfl_xor_sync(0xffffffffu, W[0], 1);
+  double c = 1.0, s = 0.0;
+  const bool rot = fabs(apq) > kOrthoEps * sqrt(app * aqq);
+  if (rot) {
+    const double zeta = (aqq - app) / (2.0 * apq);
+    const double t = zeta >= 0.0 ? 1.0 / (zeta + sqrt(1.0 + zeta * zeta))
+                                 : -1.0 / (-zeta + sqrt(1.0 + zeta * zeta));
+    c = 1.0 / sqrt(1.0 + t * t);
+    s = t * c;
+  }
+  if ((lane & 1) == 0) cs_sm[lane >> 1] = make_double2(c, s);
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    if (ODD && k == 15) break;
+    const int p = ODD ? 2 * k + 1 : 2 * k;
+    const double2 r = cs_sm[k];
+    const double gp = g[p], gq = g[p + 1];
+    g[p] = r.y * gp + r.x * gq;  // columns swap places after meeting
+    g[p + 1] = r.x * gp - r.y * gq;
+    const double vp = v[p], vq = v[p + 1];
+    v[p] = r.y * vp + r.x * vq;
+    v[p + 1] = r.x * vp - r.y * vq;
+  }
+  __syncwarp();
+  return __any_sync(0xffffffffu, rot);
+}
+
+__global__ void __launch_bounds__(kJ32Warps * 32) jacobi32_kernel(
+    int s, const double* __restrict__ core, int64_t core_stride, int ldcore, double* __restrict__ uk,
+    double* __restrict__ vk, int64_t out_stride, int ldo, double* __restrict__ sv,
+    int64_t sv_stride, int batch) {
+  __shared__ double2 cs_all[kJ32Warps][16];
+  __shared__ double nrm_all[kJ32Warps][32];
+  __shared__ int pos_all[kJ32Warps][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int b = blockIdx.x * kJ32Warps + warp;
+  if (b >= batch) return;
+  double2* cs_sm = cs_all[warp];
+  double* nrm = nrm_all[warp];
+  int* pos = pos_all[warp];
+  const double* K = core + b * core_stride;
+  double g[32], v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    g[j] = (lane < s && j < s) ? K[lane * ldcore + j] : 0.0;
+    v[j] = (lane == j && lane < s) ? 1.0 : 0.0;
+  }
+  int sweeps = 0;
+  for (; sweeps < kMaxSweeps;) {
+    bool any = false;
+    for (int rr = 0; rr < 16; ++rr) {
+      any |= j32_round<false>(g, v, lane, cs_sm);
+      any |= j32_round<true>(g, v, lane, cs_sm);
+    }
+    ++sweeps;
+    if (!any) break;
+  }
+  // column norms: reduce-scatter 32 sums, lane l ends with position l
+  double R[16];
+  {
+    const bool b4 = lane & 16;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) halve(R[i], g[i] * g[i], g[i + 16] * g[i + 16], b4, 16);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) halve(R[i], R[i], R[i + 8], lane & 8, 8);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) halve(R[i], R[i], R[i + 4], lane & 4, 4);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) halve(R[i], R[i], R[i + 2], lane & 2, 2);
+    halve(R[0], R[0], R[1], lane & 1, 1);
+  }
+  // position l holds original column id(l): a sweep reverses the order
+  const bool rev = sweeps & 1;
+  auto id_of = [&](int p) { return rev ? 31 - p : p; };
+  nrm[lane] = sqrt(R[0]);
+  __syncwarp();
+  {
+    const double mine = nrm[lane];
+    const int myid = id_of(lane);
+    int rank = 0;
+    for (int p = 0; p < 32; ++p) {
+      const double o = nrm[p];
+      const int oid = id_of(p);
+      rank += (o > mine) || (o == mine && oid < myid);
+    }
+    pos[lane] = rank;
+  }
+  __syncwarp();
+  double s0 = 0.0;
+  for (int p = 0; p < 32; ++p) s0 = fmax(s0, nrm[p]);
+  double* U = uk + b * out_stride;
+  double* Vo = vk + b * out_stride;
+  double* S = sv + b * sv_stride;
+  {
+    const double r = nrm[lane];
+    const bool live = r > 0.0 && !(r < kZeroSvRtol * s0);
+    if (id_of(lane) < s) S[pos[lane]] = live ? r : 0.0;
+  }
+  if (lane < s) {
+#pragma unroll
+    for (int p = 0; p < 32; ++p) {
+      if (id_of(p) >= s) continue;
+      const double r = nrm[p];
+      const bool live = r > 0.0 && !(r < kZeroSvRtol * s0);
+      U[lane * ldo + pos[p]] = live ? g[p] / r : 0.0;
+      Vo[lane * ldo + pos[p]] = v[p];
+    }
+  }
+  __syncwarp();
+  // dead-column completion (_kernels.pyx:62-79), rare
+  for (int t = 0; t < s; ++t) {
+    if (S[t] > 0.0) continue;
+    for (int axis = 0; axis < s; ++axis) {
+      double val = 0.0;
+      if (lane < s) {
+        val = (lane == axis) ? 1.0 : 0.0;
+        for (int c = 0; c < s; ++c)
+          if (c != t) val -= U[lane * ldo + c] * U[axis * ldo + c];
+      }
+      const double nrm2 = warp_sum(val * val);
+      if (sqrt(nrm2) > 0.5) {
+        __syncwarp();
+        if (lane < s) U[lane * ldo + t] = val / sqrt(nrm2);
+        __syncwarp();
+        break;
+      }
+    }
+  }
+}
+
 }  // namespace
 
 size_t core_svd_smem_bytes(int s, bool v_in_smem) {
@@ -194,6 +391,12 @@ int launch_core_svd(int batch, int s, const double* core, int64_t core_stride, i
     return ISVD_EINVAL;
   }
   if (batch == 0) return ISVD_OK;
+  if (s <= 32 && !active) {
+    jacobi32_kernel<<<ceil_div(batch, kJ32Warps), kJ32Warps * 32, 0, st>>>(
+        s, core, core_stride, ldcore, uk, vk, out_stride, ldo, sv, sv_stride, batch);
+    ISVD_LAUNCHED();
+    return ISVD_OK;
+  }
   bool v_in_smem = s <= kSmemMaxS;
   if (!v_in_smem && !vscratch) {
     set_error("core_svd: s > smem limit needs a V scratch buffer");

@@ -116,6 +116,7 @@ struct isvd_engine {
   std::vector<cudaEvent_t> ev_pool;
   std::vector<cudaEvent_t> ev_marks;  // 5 per recorded tick
   int64_t timed_ticks = 0;
+  std::vector<int> tick_kind;  // 0 = append, 1 = rank-1, per recorded tick
 
   void mark() {
     if (!timing) return;
@@ -434,7 +435,7 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
   e->r = keep;
   ISVD_TRY(launch_complete_zero(e->B, e->r, e->s, e->ld, e->Um(), e->m, e->Vm(), e->n, e->st));
   e->mark();
-  if (e->timing) e->timed_ticks += 1;
+  if (e->timing) { e->timed_ticks += 1; e->tick_kind.push_back(0); }
   e->canonical = false;
   e->step += 1;
   return ISVD_OK;
@@ -484,7 +485,7 @@ int isvd_engine_rank_one(isvd_engine* e, const int64_t* i, const int64_t* j, con
   ISVD_TRY(e->install_from_core(r));
   ISVD_TRY(launch_complete_zero(e->B, e->r, e->s, e->ld, e->Um(), e->m, e->Vm(), e->n, e->st));
   e->mark();
-  if (e->timing) e->timed_ticks += 1;
+  if (e->timing) { e->timed_ticks += 1; e->tick_kind.push_back(1); }
   e->canonical = false;
   e->step += 1;
   return ISVD_OK;
@@ -665,17 +666,22 @@ int isvd_engine_set_timing(isvd_engine* e, int on) {
 int isvd_engine_phase_times(isvd_engine* e, double* ms, int64_t* ticks) {
   if (!e || !ms) { set_error("bad argument"); return ISVD_EINVAL; }
   ISVD_CUDA(cudaStreamSynchronize(e->st));
-  for (int p = 0; p < 4; ++p) ms[p] = 0.0;
+  for (int p = 0; p < 8; ++p) ms[p] = 0.0;
+  int64_t cnt[2] = {0, 0};
   const size_t nt = e->ev_marks.size() / 5;
-  for (size_t t = 0; t < nt; ++t)
+  for (size_t t = 0; t < nt; ++t) {
+    const int kind = t < e->tick_kind.size() ? e->tick_kind[t] : 0;
+    cnt[kind] += 1;
     for (int p = 0; p < 4; ++p) {
       float f = 0.f;
       ISVD_CUDA(cudaEventElapsedTime(&f, e->ev_marks[t * 5 + p], e->ev_marks[t * 5 + p + 1]));
-      ms[p] += f;
+      ms[kind * 4 + p] += f;
     }
-  if (ticks) *ticks = e->timed_ticks;
+  }
+  if (ticks) { ticks[0] = cnt[0]; ticks[1] = cnt[1]; }
   for (auto ev : e->ev_marks) e->ev_pool.push_back(ev);
   e->ev_marks.clear();
+  e->tick_kind.clear();
   e->timed_ticks = 0;
   return ISVD_OK;
 }
