@@ -277,30 +277,51 @@ def run_gpu(args):
     with ClockSampler(str(ROOT / "gpurun_out" / f"clocks_r{rank}.csv")) as clk:
         e0.record(stream)
         run_ticks(eng, steps)
+        eng.flush()  # materialise deferred U rotations inside the timed region
         e1.record(stream)
         barrier()
     launches = _lib.launch_count() - l0
     dev_ms = e0.elapsed_time(e1)
-    ph8 = np.zeros(8)
-    nt2 = np.zeros(2, dtype=np.int64)
-    _lib.check(lib.isvd_engine_phase_times(eng._h.h, _lib.dptr(ph8), nt2.ctypes.data_as(
+    ph = np.zeros(10)
+    nt3 = np.zeros(3, dtype=np.int64)
+    _lib.check(lib.isvd_engine_phase_times(eng._h.h, _lib.dptr(ph), nt3.ctypes.data_as(
         __import__("ctypes").POINTER(__import__("ctypes").c_int64))))
-    phase = ph8[:4] + ph8[4:]
-    nt = np.array([nt2.sum()])
+    n_rows, n_r1, n_flush = (int(v) for v in nt3)
+    flush_ms, flush_bytes = float(ph[8]), float(ph[9])
     phase_by_kind = {
-        kind: {name: float(ph8[4 * i + j] / max(1, nt2[i]))
+        kind: {name: float(ph[4 * i + j] / max(1, nt3[i]))
                for j, name in enumerate(("project", "core_svd", "rotate", "install"))}
         for i, kind in enumerate(("row_append", "rank_one"))}
-    # algorithmic bytes of the timed ticks (dominant kernel = rotation)
-    rot_bytes = 0
-    all_bytes = 0
-    m = M0
+    # algorithmic bytes of the per-tick kernels (simulating the engine's
+    # deferred-U window: W = (32 + b) x 32 rotated in place, flushed every 32 rows)
+    proj_bytes = 0.0
+    rot_bytes = 0.0
+    all_bytes = 0.0
+    m, b_rows, active = M0, 0, False
     for t in range(steps):
         row = t % 2 == 0
-        rot_bytes += rotation_bytes(B, m, N0, K, K, row)
         all_bytes += tick_bytes(B, m, N0, K, row)
         if row:
+            proj_bytes += 8.0 * B * (N0 * K + 2 * N0 + N0)   # V read, x read, A row write, z write
+            vb = N0 * K + N0 * K + N0                         # V read/write + z read
+            if not active:
+                wb = (K + 1) * K                              # W = Uk copy
+                active, b_rows = True, 1
+            else:
+                wb = (K + b_rows) * K + (K + b_rows + 1) * K
+                b_rows += 1
             m += 1
+            if b_rows >= 32:
+                active, b_rows = False, 0
+        else:
+            proj_bytes += 8.0 * B * (2 * K + 2)               # U/V row gathers (+ W row)
+            vb = 2 * N0 * K
+            if not active:
+                wb = K * K
+                active, b_rows = True, 0
+            else:
+                wb = 2 * (K + b_rows) * K
+        rot_bytes += 8.0 * B * (vb + wb)
     t_max = dev_ms
     if world > 1:
         tt = torch.tensor([dev_ms], device=dev)
@@ -329,6 +350,7 @@ def run_gpu(args):
     barrier()
     t0 = time.perf_counter()
     run_ticks(eng, e2e_steps, host=host)
+    eng.flush()
     barrier()
     e2e_s = time.perf_counter() - t0
     if world > 1:
@@ -342,8 +364,26 @@ def run_gpu(args):
 
     if rank == 0:
         peak, peak_kind = _peaks()
-        rot_ms = phase[2] / max(1, int(nt[0]))
-        achieved = rot_bytes / max(1, steps) / (rot_ms / 1e3) / 1e9
+        tot = lambda i: float(ph[i] + ph[4 + i])
+        install_ms = tot(3) - flush_ms
+        kernels = {
+            "project_append/rank1_build (K1/K6)": {"ms": tot(0), "bytes": proj_bytes},
+            "arrow_svd (K2a, append cores)": {"ms": float(ph[1]), "bytes": None},
+            "jacobi32 (K2b, rank-1 cores)": {"ms": float(ph[5]), "bytes": None},
+            "rotate V + W (K3/K4, per tick)": {"ms": tot(2), "bytes": rot_bytes},
+            "rotate U flush (K3, deferred)": {"ms": flush_ms, "bytes": flush_bytes},
+            "install (s copy, zero-sigma check)": {"ms": max(0.0, install_ms), "bytes": None},
+        }
+        busy = sum(v["ms"] for v in kernels.values())
+        for v in kernels.values():
+            v["share"] = v["ms"] / busy if busy else None
+            v["ms_per_step"] = v["ms"] / max(1, steps)
+            v["gbs"] = (v["bytes"] / (v["ms"] / 1e3) / 1e9) if (v["bytes"] and v["ms"]) else None
+        hbm = {k: v for k, v in kernels.items() if v["bytes"]}
+        dom_name = max(kernels, key=lambda k: kernels[k]["ms"])
+        hbm_name = max(hbm, key=lambda k: hbm[k]["ms"])
+        hk = hbm[hbm_name]
+        achieved = hk["gbs"]
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
             "warmup": warm, "ms_per_step": t_max / steps, "higher_is_better": True,
@@ -352,19 +392,20 @@ def run_gpu(args):
                        "streams_per_gpu": B, "m0": M0, "n": N0, "rank": RANK, "k": K,
                        "events": steps, "event_mix": "alternating row append / rank-1",
                        "l2": "inputs larger than L2 (state ~2 GB/GPU touched per step)",
-                       "parallelism": f"streams sharded over {world} GPU(s)"},
+                       "parallelism": f"streams sharded over {world} GPU(s)",
+                       "deferred_u_rows": 32},
             "clocks": clock,
             "gpu_launches": int(launches),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "steps": e2e_steps},
-            "roofline": {"kernel": "rotate_kernel (K3/K4, FP64 DMMA)", "bound": "hbm",
-                         "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "peak_kind": peak_kind, "traffic": None,
-                         "bytes_per_launch": rot_bytes / max(1, steps)},
-            "phase_ms_per_step": {"project": phase[0] / max(1, nt[0]),
-                                  "core_svd": phase[1] / max(1, nt[0]),
-                                  "rotate": phase[2] / max(1, nt[0]),
-                                  "install": phase[3] / max(1, nt[0])},
+            "roofline": {"kernel": hbm_name, "bound": "hbm", "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak, "peak_kind": peak_kind,
+                         "traffic": None,
+                         "bytes_per_launch": hk["bytes"] / max(1, (n_flush if "flush" in hbm_name else steps)),
+                         "dominant_kernel_by_time": dom_name,
+                         "note": "dominant HBM-bound kernel; the core-SVD kernels are FP64/latency bound"},
+            "kernels": kernels,
+            "flushes": n_flush,
             "phase_ms_by_event": phase_by_kind,
             "tick_effective_gbs": all_bytes / (t_max / 1e3) / 1e9,
         }

@@ -148,6 +148,13 @@ int isvd_engine_set_timing(isvd_engine* e, int on);
  * secular-equation kernel for the broken-arrow core.  Both are exact SVDs;
  * the parity tests run both. */
 int isvd_engine_set_append_solver(isvd_engine* e, int jacobi);
+/* Deferred left-basis rotation, on by default: row
+ * appends and rank-1 updates rotate a small W (U = [U_base 0; 0 I] W) and U
+ * is materialised every 32 appended rows and before any read of U.
+ * set_lazy(0) rotates U eagerly every event (the reference's order of
+ * operations); flush() materialises U now. */
+int isvd_engine_set_lazy(isvd_engine* e, int on);
+int isvd_engine_flush(isvd_engine* e);
 int isvd_engine_phase_times(isvd_engine* e, double* ms4, int64_t* ticks);
 
 /* 3. Metrics (metrics.py:56-145, linalg.py:126-153) ------------------------- */

@@ -117,6 +117,49 @@ struct isvd_engine {
   std::vector<cudaEvent_t> ev_marks;  // 5 per recorded tick
   int64_t timed_ticks = 0;
   std::vector<int> tick_kind;  // 0 = append, 1 = rank-1, per recorded tick
+  // Deferred left-basis rotation.  Row appends and rank-1
+  // updates multiply the small W (U = [Ub 0; 0 I] W) instead of the tall U;
+  // U is materialised every kLazyRows appended rows and whenever it is read.
+  static constexpr int kLazyRows = 32;
+  bool lazy_mode = true;
+  bool lazy_active = false;
+  int m_base = 0, r_base = 0, lazy_b = 0;
+  double* W = nullptr;
+  int64_t wstride() const { return (int64_t)(ld + kLazyRows + 1) * ld; }
+  Mat Wm() const { return Mat{W, wstride(), ld}; }
+  LazyBasis lazy() const { return LazyBasis{lazy_active ? 1 : 0, m_base, r_base, Wm()}; }
+
+  // flush timing (CUDA events around each flush) and its algorithmic bytes
+  std::vector<cudaEvent_t> flush_marks;
+  double flush_bytes = 0.0;
+
+  // U <- [Ub 0; 0 I] W ; ends the deferred window
+  int flush() {
+    if (!lazy_active) return ISVD_OK;
+    RotJob ju{Um(), m_base, W, wstride(), ld, nullptr, 0, nullptr, 0};
+    if (timing) {
+      cudaEvent_t ev;
+      cudaEventCreate(&ev);
+      cudaEventRecord(ev, st);
+      flush_marks.push_back(ev);
+      // U base rows read (r_base wide) + written (r wide); W rows read; new rows written
+      flush_bytes += 8.0 * B * ((double)m_base * (r_base + r) + (double)(r_base + lazy_b) * r +
+                                (double)lazy_b * r);
+    }
+    ISVD_TRY(launch_rotate(B, r_base, r, ju, nullptr, st));
+    if (timing) {
+      cudaEvent_t ev;
+      cudaEventCreate(&ev);
+      cudaEventRecord(ev, st);
+      flush_marks.push_back(ev);
+    }
+    if (lazy_b > 0)
+      ISVD_TRY(launch_copy_rows(B, lazy_b, r, W + (int64_t)r_base * ld, wstride(), ld,
+                                U + (int64_t)m_base * ld, ustride(), ld, st));
+    lazy_active = false;
+    lazy_b = 0;
+    return ISVD_OK;
+  }
 
   void mark() {
     if (!timing) return;
@@ -208,6 +251,7 @@ struct isvd_engine {
       set_error("work rank exceeds the supported maximum (" + std::to_string(kCoreMaxS - 1) + ")");
       return ISVD_EINVAL;
     }
+    ISVD_TRY(flush());
     double *U2, *V2, *s2;
     ISVD_TRY(dalloc(&U2, (size_t)B * m_cap * nld));
     ISVD_TRY(dalloc(&V2, (size_t)B * n_cap * nld));
@@ -231,10 +275,14 @@ struct isvd_engine {
     U = U2; V = V2; s = s2;
     if (ref) { dfree(ref); ref = ref2; }
     ld = nld;
+    dfree(W);
+    ISVD_TRY(dalloc(&W, (size_t)B * wstride()));
+    ISVD_CUDA(cudaMemsetAsync(W, 0, sizeof(double) * B * wstride(), st));
     return alloc_core_bufs();
   }
 
   int canonicalize() {
+    ISVD_TRY(flush());
     if (canonical) return ISVD_OK;
     ISVD_TRY(launch_canonicalize(B, r, Um(), m, Vm(), n, st));
     canonical = true;
@@ -255,6 +303,8 @@ struct isvd_engine {
     ISVD_TRY(ensure_work((int64_t)B * P.x_elems(), (int64_t)B * P.j_elems(), 0, 0));
     int w = std::min(k, std::min(m, n));
     int sweeps = 0;
+    lazy_active = false;  // U is recomputed from A
+    lazy_b = 0;
     ISVD_TRY(dense_svd_run(B, m, n, A, astride(), n_cap, w, Um(), Vm(), s, ld, nullptr, 0, wx, wj,
                            wflags, hflags.data(), st, &sweeps));
     r = w;
@@ -268,7 +318,7 @@ struct isvd_engine {
     dfree(U); dfree(V); dfree(s); dfree(A); dfree(N);
     dfree(core); dfree(uk); dfree(vk); dfree(sv); dfree(vscr);
     dfree(z); dfree(inj); dfree(rho); dfree(xnorm); dfree(ev);
-    dfree(ei); dfree(ej); dfree(ed); dfree(dflag); dfree(ref);
+    dfree(ei); dfree(ej); dfree(ed); dfree(dflag); dfree(ref); dfree(W);
     dfree(wx); dfree(wj); dfree(wpart); dfree(wout); dfree(wflags);
     for (auto ev : ev_marks) cudaEventDestroy(ev);
     for (auto ev : ev_pool) cudaEventDestroy(ev);
@@ -326,12 +376,14 @@ int isvd_engine_create(isvd_engine** out, int batch, int m, int n, int k, double
   A(dalloc(&e->ej, (size_t)batch));
   A(dalloc(&e->ed, (size_t)batch));
   A(dalloc(&e->dflag, 4));
+  A(dalloc(&e->W, (size_t)batch * e->wstride()));
   if (rc == ISVD_OK) rc = e->alloc_core_bufs();
   if (rc == ISVD_OK) rc = e->alloc_vec_bufs();
   if (rc == ISVD_OK) {
     cudaMemsetAsync(e->U, 0, sizeof(double) * batch * e->m_cap * e->ld, e->st);
     cudaMemsetAsync(e->V, 0, sizeof(double) * batch * e->n_cap * e->ld, e->st);
     cudaMemsetAsync(e->s, 0, sizeof(double) * batch * e->ld, e->st);
+    cudaMemsetAsync(e->W, 0, sizeof(double) * batch * e->wstride(), e->st);
     std::vector<double> nanv(batch, std::nan(""));
     cudaMemcpyAsync(e->rho, nanv.data(), sizeof(double) * batch, cudaMemcpyHostToDevice, e->st);
     cudaMemcpyAsync(e->xnorm, nanv.data(), sizeof(double) * batch, cudaMemcpyHostToDevice, e->st);
@@ -402,6 +454,7 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
   const int keep = is_row ? std::min(std::min(e->r + 1, e->k), std::min(e->m + 1, e->n))
                           : std::min(std::min(e->r + 1, e->k), std::min(e->m, e->n + 1));
   ISVD_TRY(is_row ? e->grow_rows(e->m + 1) : e->grow_cols(e->n + 1));
+  if (!is_row) ISVD_TRY(e->flush());  // the column append projects on, and rotates, U
   const double* xd = x;
   if (!on_device) {
     ISVD_CUDA(cudaMemcpyAsync(e->ev, x, sizeof(double) * e->B * len, cudaMemcpyHostToDevice, e->st));
@@ -428,12 +481,34 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
               nullptr, 0, nullptr, 1};
   RotJob inj{is_row ? e->Vm() : e->Um(), is_row ? e->n : e->m, e->vk, e->cstride(), e->S(),
              e->z, e->zlen(), e->inj, 0};
-  ISVD_TRY(launch_rotate(e->B, r, keep, grow, &inj, e->st));
+  const bool lazy = is_row && e->lazy_mode;
+  if (!lazy) {
+    ISVD_TRY(launch_rotate(e->B, r, keep, grow, &inj, e->st));
+  } else if (!e->lazy_active) {
+    // open a deferred window: W = Uk[:, :keep] (rows: r base columns + the new row)
+    ISVD_TRY(launch_copy_rows(e->B, r + 1, keep, e->uk, e->cstride(), e->S(), e->W, e->wstride(),
+                              e->ld, e->st));
+    ISVD_TRY(launch_rotate(e->B, r, keep, inj, nullptr, e->st));
+    e->lazy_active = true;
+    e->m_base = e->m;
+    e->r_base = r;
+    e->lazy_b = 1;
+  } else {
+    // W <- [W 0; 0 1] Uk[:, :keep]  (in place, new row appended)
+    RotJob wj{e->Wm(), e->r_base + e->lazy_b, e->uk, e->cstride(), e->S(), nullptr, 0, nullptr, 1};
+    ISVD_TRY(launch_rotate(e->B, r, keep, wj, &inj, e->st));
+    e->lazy_b += 1;
+  }
   e->mark();
   ISVD_TRY(e->install_from_core(keep));
   if (is_row) e->m += 1; else e->n += 1;
   e->r = keep;
-  ISVD_TRY(launch_complete_zero(e->B, e->r, e->s, e->ld, e->Um(), e->m, e->Vm(), e->n, e->st));
+  if (e->lazy_active)
+    ISVD_TRY(launch_complete_zero(e->B, e->r, e->s, e->ld, e->Wm(), e->r_base + e->lazy_b,
+                                  e->Vm(), e->n, e->st));
+  else
+    ISVD_TRY(launch_complete_zero(e->B, e->r, e->s, e->ld, e->Um(), e->m, e->Vm(), e->n, e->st));
+  if (e->lazy_active && e->lazy_b >= isvd_engine::kLazyRows) ISVD_TRY(e->flush());
   e->mark();
   if (e->timing) { e->timed_ticks += 1; e->tick_kind.push_back(0); }
   e->canonical = false;
@@ -473,17 +548,36 @@ int isvd_engine_rank_one(isvd_engine* e, const int64_t* i, const int64_t* j, con
   const int r = e->r;
   e->mark();
   ISVD_TRY(launch_rank1_build(e->B, r, e->Um(), e->Vm(), e->s, e->ld, di, dj, dd, e->core,
-                              e->cstride(), e->S(), e->A, e->astride(), e->n_cap, e->N, e->st));
+                              e->cstride(), e->S(), e->A, e->astride(), e->n_cap, e->N, e->lazy(),
+                              e->st));
   e->mark();
   ISVD_TRY(launch_core_svd(e->B, r, e->core, e->cstride(), e->S(), e->uk, e->vk, e->cstride(),
                            e->S(), e->sv, e->S(), e->vscr, nullptr, e->st));
   e->mark();
   RotJob ju{e->Um(), e->m, e->uk, e->cstride(), e->S(), nullptr, 0, nullptr, 0};
   RotJob jv{e->Vm(), e->n, e->vk, e->cstride(), e->S(), nullptr, 0, nullptr, 0};
-  ISVD_TRY(launch_rotate(e->B, r, r, ju, &jv, e->st));
+  if (!e->lazy_mode) {
+    ISVD_TRY(launch_rotate(e->B, r, r, ju, &jv, e->st));
+  } else if (!e->lazy_active) {
+    // open a deferred window: W = Uk (U' = U Uk)
+    ISVD_TRY(launch_copy_rows(e->B, r, r, e->uk, e->cstride(), e->S(), e->W, e->wstride(), e->ld,
+                              e->st));
+    ISVD_TRY(launch_rotate(e->B, r, r, jv, nullptr, e->st));
+    e->lazy_active = true;
+    e->m_base = e->m;
+    e->r_base = r;
+    e->lazy_b = 0;
+  } else {
+    RotJob wj{e->Wm(), e->r_base + e->lazy_b, e->uk, e->cstride(), e->S(), nullptr, 0, nullptr, 0};
+    ISVD_TRY(launch_rotate(e->B, r, r, wj, &jv, e->st));
+  }
   e->mark();
   ISVD_TRY(e->install_from_core(r));
-  ISVD_TRY(launch_complete_zero(e->B, e->r, e->s, e->ld, e->Um(), e->m, e->Vm(), e->n, e->st));
+  if (e->lazy_active)
+    ISVD_TRY(launch_complete_zero(e->B, e->r, e->s, e->ld, e->Wm(), e->r_base + e->lazy_b,
+                                  e->Vm(), e->n, e->st));
+  else
+    ISVD_TRY(launch_complete_zero(e->B, e->r, e->s, e->ld, e->Um(), e->m, e->Vm(), e->n, e->st));
   e->mark();
   if (e->timing) { e->timed_ticks += 1; e->tick_kind.push_back(1); }
   e->canonical = false;
@@ -525,6 +619,7 @@ int isvd_engine_set_reference(isvd_engine* e) {
 int isvd_engine_set_rank(isvd_engine* e, int k_new) {
   if (!e) { set_error("null engine"); return ISVD_EINVAL; }
   if (k_new < 1) { set_error("work rank must be >= 1, got " + std::to_string(k_new)); return ISVD_EINVAL; }
+  ISVD_TRY(e->flush());
   ISVD_TRY(e->grow_rank(k_new));
   e->k = k_new;
   if (e->r > k_new) e->r = k_new;
@@ -637,6 +732,7 @@ int isvd_engine_device_views(isvd_engine* e, double** u, int64_t* u_stride, int*
                              int64_t* v_stride, int* ldv, double** s, int* lds, double** a,
                              int64_t* a_stride, int* lda) {
   if (!e) { set_error("null engine"); return ISVD_EINVAL; }
+  ISVD_TRY(e->flush());
   if (u) *u = e->U;
   if (u_stride) *u_stride = e->ustride();
   if (ldu) *ldu = e->ld;
@@ -648,6 +744,18 @@ int isvd_engine_device_views(isvd_engine* e, double** u, int64_t* u_stride, int*
   if (a) *a = e->A;
   if (a_stride) *a_stride = e->astride();
   if (lda) *lda = e->n_cap;
+  return ISVD_OK;
+}
+
+int isvd_engine_flush(isvd_engine* e) {
+  if (!e) { set_error("null engine"); return ISVD_EINVAL; }
+  return e->flush();
+}
+
+int isvd_engine_set_lazy(isvd_engine* e, int on) {
+  if (!e) { set_error("null engine"); return ISVD_EINVAL; }
+  ISVD_TRY(e->flush());
+  e->lazy_mode = on != 0;
   return ISVD_OK;
 }
 
@@ -666,7 +774,7 @@ int isvd_engine_set_timing(isvd_engine* e, int on) {
 int isvd_engine_phase_times(isvd_engine* e, double* ms, int64_t* ticks) {
   if (!e || !ms) { set_error("bad argument"); return ISVD_EINVAL; }
   ISVD_CUDA(cudaStreamSynchronize(e->st));
-  for (int p = 0; p < 8; ++p) ms[p] = 0.0;
+  for (int p = 0; p < 10; ++p) ms[p] = 0.0;
   int64_t cnt[2] = {0, 0};
   const size_t nt = e->ev_marks.size() / 5;
   for (size_t t = 0; t < nt; ++t) {
@@ -679,6 +787,18 @@ int isvd_engine_phase_times(isvd_engine* e, double* ms, int64_t* ticks) {
     }
   }
   if (ticks) { ticks[0] = cnt[0]; ticks[1] = cnt[1]; }
+  // [8] = summed flush-rotation ms, [9] = their algorithmic bytes; ticks[2] = flushes
+  ms[8] = 0.0;
+  for (size_t f = 0; f + 1 < e->flush_marks.size(); f += 2) {
+    float v = 0.f;
+    ISVD_CUDA(cudaEventElapsedTime(&v, e->flush_marks[f], e->flush_marks[f + 1]));
+    ms[8] += v;
+  }
+  ms[9] = e->flush_bytes;
+  if (ticks) ticks[2] = (int64_t)(e->flush_marks.size() / 2);
+  for (auto ev : e->flush_marks) cudaEventDestroy(ev);
+  e->flush_marks.clear();
+  e->flush_bytes = 0.0;
   for (auto ev : e->ev_marks) e->ev_pool.push_back(ev);
   e->ev_marks.clear();
   e->tick_kind.clear();
@@ -701,6 +821,7 @@ int isvd_engine_synchronize(isvd_engine* e) {
 
 int isvd_engine_frob_error(isvd_engine* e, double* out) {
   if (!e || !e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
+  ISVD_TRY(e->flush());
   ISVD_TRY(e->ensure_work(0, 0, (int64_t)e->B * frob_nblk(e->m), e->B));
   ISVD_TRY(launch_frob_error_sq(e->B, e->m, e->n, e->r, e->A, e->astride(), e->n_cap, e->Um(), e->s,
                                 e->ld, e->Vm(), e->wpart, e->wout, e->st));
@@ -722,6 +843,7 @@ static int gram_defect(isvd_engine* e, Mat X, int rows, int w, double* host_out)
 
 int isvd_engine_ortho_defect(isvd_engine* e, double* du, double* dv) {
   if (!e || !e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
+  ISVD_TRY(e->flush());
   if (du) ISVD_TRY(gram_defect(e, e->Um(), e->m, e->r, du));
   if (dv) ISVD_TRY(gram_defect(e, e->Vm(), e->n, e->r, dv));
   return ISVD_OK;
@@ -730,6 +852,7 @@ int isvd_engine_ortho_defect(isvd_engine* e, double* du, double* dv) {
 int isvd_engine_angle(isvd_engine* e, int which, const double* q, int q_cols, int on_device,
                       double* out) {
   if (!e || !e->initialized || !out) { set_error("engine not initialised"); return ISVD_ESTATE; }
+  ISVD_TRY(e->flush());
   const int B = e->B, m = e->m, r = e->r;
   Mat Qm;
   double* qbuf = nullptr;
@@ -962,7 +1085,7 @@ static int functional_common(bool is_row, int m, int r, int n, const double* u, 
       cudaMemcpy(di, &i, sizeof(int64_t), cudaMemcpyHostToDevice);
       cudaMemcpy(dj, &j, sizeof(int64_t), cudaMemcpyHostToDevice);
       cudaMemcpy(dd, &delta, sizeof(double), cudaMemcpyHostToDevice);
-      T(launch_rank1_build(1, r, Um, Vm, sd, ld, di, dj, dd, core, 0, S, nullptr, 0, 0, N, st));
+      T(launch_rank1_build(1, r, Um, Vm, sd, ld, di, dj, dd, core, 0, S, nullptr, 0, 0, N, LazyBasis{0, 0, 0, Mat{nullptr, 0, 0}}, st));
       T(launch_core_svd(1, r, core, 0, S, uk, vk, 0, S, sv, 0, vscr, nullptr, st));
       RotJob ju{Um, m, uk, 0, S, nullptr, 0, nullptr, 0};
       RotJob jv{Vm, n, vk, 0, S, nullptr, 0, nullptr, 0};

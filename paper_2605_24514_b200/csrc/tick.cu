@@ -102,17 +102,31 @@ __global__ void rank1_build_kernel(int r, Mat U, Mat V, const double* __restrict
                                    const int64_t* __restrict__ ii, const int64_t* __restrict__ jj,
                                    const double* __restrict__ delta, double* __restrict__ core,
                                    int64_t core_stride, int ldcore, double* __restrict__ A,
-                                   int64_t a_stride, int lda, double* __restrict__ N) {
-  __shared__ double a[kRMax], bb[kRMax];
+                                   int64_t a_stride, int lda, double* __restrict__ N, LazyBasis lz) {
+  __shared__ double a[kRMax], bb[kRMax], ub[kRMax];
   const int b = blockIdx.x;
   const int64_t i = ii[b], j = jj[b];
   const double d = delta[b];
-  const double* ur = U.p + b * U.stride + i * U.ld;
   const double* vr = V.p + b * V.stride + j * V.ld;
-  for (int l = threadIdx.x; l < r; l += blockDim.x) {
-    a[l] = ur[l];
-    bb[l] = vr[l];
+  if (!lz.active) {
+    const double* ur = U.p + b * U.stride + i * U.ld;
+    for (int l = threadIdx.x; l < r; l += blockDim.x) a[l] = ur[l];
+  } else if (i >= lz.m_base) {
+    // an appended row: its coordinates are a row of W (U = [Ub 0; 0 I] W)
+    const double* wr = lz.W.p + b * lz.W.stride + (lz.r_base + (i - lz.m_base)) * lz.W.ld;
+    for (int l = threadIdx.x; l < r; l += blockDim.x) a[l] = wr[l];
+  } else {
+    const double* ur = U.p + b * U.stride + i * U.ld;
+    for (int c = threadIdx.x; c < lz.r_base; c += blockDim.x) ub[c] = ur[c];
+    __syncthreads();
+    const double* Wb = lz.W.p + b * lz.W.stride;
+    for (int l = threadIdx.x; l < r; l += blockDim.x) {
+      double acc = 0.0;
+      for (int c = 0; c < lz.r_base; ++c) acc = fma(ub[c], Wb[c * lz.W.ld + l], acc);
+      a[l] = acc;
+    }
   }
+  for (int l = threadIdx.x; l < r; l += blockDim.x) bb[l] = vr[l];
   __syncthreads();
   double* Kb = core + b * core_stride;
   const double* sb = s + (int64_t)b * lds;
@@ -437,9 +451,9 @@ int launch_project_append(int batch, int rows, int r, Mat F, const double* x, in
 int launch_rank1_build(int batch, int r, Mat U, Mat V, const double* s, int lds,
                        const int64_t* ii, const int64_t* jj, const double* delta, double* core,
                        int64_t core_stride, int ldcore, double* A, int64_t a_stride, int lda,
-                       double* N, cudaStream_t st) {
+                       double* N, LazyBasis lz, cudaStream_t st) {
   rank1_build_kernel<<<batch, 128, 0, st>>>(r, U, V, s, lds, ii, jj, delta, core, core_stride,
-                                            ldcore, A, a_stride, lda, N);
+                                            ldcore, A, a_stride, lda, N, lz);
   ISVD_LAUNCHED();
   return ISVD_OK;
 }

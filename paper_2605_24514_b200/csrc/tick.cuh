@@ -21,12 +21,21 @@ int launch_project_append(int batch, int rows, int r, Mat F, const double* x, in
                           double* rho_out, double* xnorm_out, double* A, int64_t a_stride,
                           int64_t a_off, int64_t a_step, double* N, cudaStream_t st);
 
+// Deferred left basis: while active, the true U is
+// [Ub 0; 0 I] . W where Ub = the first m_base rows of the U buffer (width
+// r_base) and W has r_base + (rows appended since) rows.
+struct LazyBasis {
+  int active;
+  int m_base, r_base;
+  Mat W;
+};
+
 // K6: rank-1 core K = diag(s) + delta U[i,:]^T V[j,:] plus the tracked entry
 // update A[i,j] += delta and N += 2 delta a_old + delta^2 (engine.py:162-166).
 int launch_rank1_build(int batch, int r, Mat U, Mat V, const double* s, int lds,
                        const int64_t* ii, const int64_t* jj, const double* delta, double* core,
                        int64_t core_stride, int ldcore, double* A, int64_t a_stride, int lda,
-                       double* N, cudaStream_t st);
+                       double* N, LazyBasis lz, cudaStream_t st);
 
 // One rotation job: X[b][0:rows, 0:keep] = X[b][0:rows, 0:r] . Q[b][0:r, 0:keep]
 //   (+ z[b][i] * inj_scale[b] * Q[b][r, c])      if z != nullptr

@@ -137,6 +137,14 @@ class BatchedSvdEngine:
     def synchronize(self) -> None:
         _lib.check(self._h.lib.isvd_engine_synchronize(self._h.h))
 
+    def flush(self) -> None:
+        """Materialise deferred basis rotations now."""
+        _lib.check(self._h.lib.isvd_engine_flush(self._h.h))
+
+    def set_lazy(self, on: bool) -> None:
+        """Deferred left-basis rotation on (default) or off (eager per event)."""
+        _lib.check(self._h.lib.isvd_engine_set_lazy(self._h.h, int(bool(on))))
+
     # ------------------------------------------------------------ events
     def row_append(self, x) -> None:
         b, m, n, *_ = self._h.shape()
@@ -424,6 +432,10 @@ class SvdEngine:
         u = np.empty((m, w))
         _lib.check(self._h.lib.isvd_engine_oracle(self._h.h, w, _lib.dptr(s), _lib.dptr(u)))
         return s, u
+
+    def set_lazy(self, on: bool) -> None:
+        """Deferred left-basis rotation on (default) or off (eager per event)."""
+        _lib.check(self._h.lib.isvd_engine_set_lazy(self._h.h, int(bool(on))))
 
     def ortho_defects(self) -> tuple[float, float]:
         du, dv = np.empty(1), np.empty(1)

@@ -330,3 +330,69 @@ def test_append_solvers_agree_on_streams():
     assert rel_err(fs.s, fj.s) < 1e-11
     assert sine_angle(fs.u, fj.u) < 1e-9
     np.testing.assert_allclose(fs.u, fj.u, atol=1e-9)
+
+
+# ------------------------------------------------ deferred (lazy) U rotation
+@pytest.mark.parametrize("k", [5, 32])
+def test_lazy_and_eager_rotation_agree(k):
+    """The deferred left-basis rotation (U = [Ub 0; 0 I] W, flushed every 32
+    appended rows) reproduces the eager per-event rotation."""
+    rng = np.random.default_rng(k)
+    a0 = rng.standard_normal((120, 60)) @ np.diag(np.logspace(0, -2, 60)) @ rng.standard_normal((60, 60))
+    lazy, eager, cpu = SvdEngine(a0, k), SvdEngine(a0, k), OracleEngine(a0, k)
+    eager.set_lazy(False)
+    for t in range(150):
+        kind = t % 5
+        if kind in (0, 2):
+            x = rng.standard_normal(lazy.shape[1])
+            for e in (lazy, eager, cpu):
+                e.row_append(x)
+        elif kind == 4 and t % 25 == 4:
+            y = rng.standard_normal(lazy.shape[0])
+            for e in (lazy, eager, cpu):
+                e.col_append(y)
+        else:
+            i, j = int(rng.integers(lazy.shape[0])), int(rng.integers(lazy.shape[1]))
+            d = float(rng.normal(0, 0.2))
+            for e in (lazy, eager, cpu):
+                e.rank_one_update(i, j, d)
+        if t % 37 == 0:  # observation mid-window flushes
+            assert lazy.factors.rank == eager.factors.rank
+    fl, fe, fc = lazy.factors, eager.factors, cpu.factors
+    assert rel_err(fl.s, fe.s) < 1e-11
+    np.testing.assert_allclose(fl.u, fe.u, atol=1e-9)
+    assert rel_err(fl.s, fc.s) < SIGMA_RTOL
+    assert sine_angle(fl.u, fc.u) < ANGLE_TOL
+    du, dv = lazy.ortho_defects()
+    assert du < 1e-10 and dv < 1e-10
+
+
+def test_batched_lazy_flush_cycle():
+    """Batched 5a-shaped streams across several flush windows (32 rows each)
+    with rank-1 gathers hitting both base rows and rows appended inside the
+    current window."""
+    B, T = 4, 200
+    a0, ticks, streams = workloads.cfg5a_batch(3, B, m=200, n=64, rank=8, n_events=T)
+    eng = BatchedSvdEngine(a0, 8, m_cap=200 + T)
+    for t, tk in enumerate(ticks):
+        if tk[0] == "row":
+            eng.row_append(tk[1])
+        else:
+            # force gathers into the freshly appended rows half of the time
+            ii = tk[1].copy()
+            if t % 4 == 1:
+                ii[:] = eng.shape[0] - 1
+                for b in range(B):
+                    streams[b][1][t] = ("rank1", int(ii[b]), int(tk[2][b]), float(tk[3][b]))
+            eng.rank_one_update(ii, tk[2], tk[3])
+    for b in range(B):
+        oe = OracleEngine(streams[b][0], 8)
+        for e in streams[b][1]:
+            if e[0] == "row":
+                oe.row_append(e[1])
+            else:
+                oe.rank_one_update(e[1], e[2], e[3])
+        f = eng.factors(b)
+        assert rel_err(f.s, oe.factors.s) < SIGMA_RTOL
+        assert sine_angle(f.u, oe.factors.u) < ANGLE_TOL
+        np.testing.assert_allclose(f.u, oe.factors.u, atol=1e-8)
