@@ -229,10 +229,10 @@ def run_gpu(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     from paper_2605_24514_b200 import BatchedSvdEngine, _lib
+    from paper_2605_24514_b200.sharding import max_over_ranks, shard_streams
 
     total = args.streams
-    per = total // world
-    streams = list(range(rank * per, (rank + 1) * per))
+    streams = list(shard_streams(total, world, rank))
     B = len(streams)
     steps, warm = args.steps, args.warmup
     n_events = max(steps, warm)
@@ -322,11 +322,7 @@ def run_gpu(args):
             else:
                 wb = 2 * (K + b_rows) * K
         rot_bytes += 8.0 * B * (vb + wb)
-    t_max = dev_ms
-    if world > 1:
-        tt = torch.tensor([dev_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max = float(tt.item())
+    t_max = max_over_ranks(dev_ms, device=dev)
     value = total * steps / (t_max / 1e3)
     clock = clk.summary(local)
     # sanity: spectrum of stream 0 is finite and sorted
@@ -352,11 +348,7 @@ def run_gpu(args):
     run_ticks(eng, e2e_steps, host=host)
     eng.flush()
     barrier()
-    e2e_s = time.perf_counter() - t0
-    if world > 1:
-        tt = torch.tensor([e2e_s], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_s = float(tt.item())
+    e2e_s = max_over_ranks(time.perf_counter() - t0, device=dev)
     e2e_value = total * e2e_steps / e2e_s
     h2d = (nrow * B * N0 * 8 + nr1 * B * 24) / max(1, e2e_steps)
     d2h = 3 * B * 8

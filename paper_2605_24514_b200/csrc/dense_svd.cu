@@ -312,7 +312,11 @@ int dense_svd_run(int batch, int m, int n, const double* a, int64_t a_stride, in
   }
   ISVD_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * batch, st));
   const double eps = 2.220446049250313e-16;
-  const double tol = std::max(1e-14, 4.0 * std::sqrt((double)P.len) * eps);
+  // Stop when every block-pair Gram has |M_pq| <= tol sqrt(M_pp M_qq): sigma is then
+  // accurate to O(tol^2) relative and the vectors to O(tol / relative gap).  1e-12
+  // also stays above the rounding floor of the Gram-based inner rotations
+  // (eps sqrt(M_pp / M_qq) for strongly graded pairs), so the sweep count stays low.
+  const double tol = std::max(1e-12, 4.0 * std::sqrt((double)P.len) * eps);
   std::vector<int> fl(batch, 0);
   int sweep = 0;
   const int kMaxOuter = 40;
