@@ -136,14 +136,16 @@ class ClockSampler:
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv",
-                                          "-lms", "100"], stdout=self.f,
+                                          "-lms", "50"], stdout=self.f,
                                          stderr=subprocess.DEVNULL)
+            time.sleep(0.5)  # let the sampler start before the timed region
         except Exception:
             self.proc = None
         return self
 
     def __exit__(self, *exc):
         if self.proc:
+            time.sleep(0.1)
             self.proc.terminate()
             self.proc.wait()
             self.f.close()

@@ -32,6 +32,10 @@ namespace {
 
 constexpr int kN = kCoreMaxS;  // max core size
 
+// Shared state sized by a compile-time bound on the core size (one
+// instantiation per bound keeps the per-CTA footprint small: ~4.6 KB at
+// s <= 40, so ~40 cores can be resident per SM).
+template <int kN>
 struct ArrowSmem {
   double delta[kN];   // pole value per original column (zero group forced to 0)
   double z[kN];       // z per original column, updated by the deflation rotations
@@ -52,7 +56,8 @@ struct ArrowSmem {
   double scale;
 };
 
-__device__ __forceinline__ void apply_rots(double* col, int64_t stride, const ArrowSmem& S,
+template <class SM>
+__device__ __forceinline__ void apply_rots(double* col, int64_t stride, const SM& S,
                                            bool left) {
   // x_orig = G_1 G_2 ... G_k x : apply the last rotation first
   for (int k = S.nrot - 1; k >= 0; --k) {
@@ -65,13 +70,14 @@ __device__ __forceinline__ void apply_rots(double* col, int64_t stride, const Ar
   }
 }
 
-__global__ void __launch_bounds__(kN) arrow_svd_kernel(int n, const double* __restrict__ core,
+template <int kN>
+__global__ void __launch_bounds__((kN + 31) / 32 * 32) arrow_svd_kernel(int n, const double* __restrict__ core,
                                                        int64_t core_stride, int ldcore,
                                                        double* __restrict__ uk,
                                                        double* __restrict__ vk, int64_t out_stride,
                                                        int ldo, double* __restrict__ sv,
                                                        int64_t sv_stride) {
-  __shared__ ArrowSmem S;
+  __shared__ ArrowSmem<kN> S;
   const int b = blockIdx.x;
   const int tid = threadIdx.x;
   const int r = n - 1;
@@ -385,8 +391,18 @@ int launch_arrow_svd(int batch, int s, const double* core, int64_t core_stride, 
   }
   if (batch == 0) return ISVD_OK;
   const int threads = round_up(s, 32);
-  arrow_svd_kernel<<<batch, threads, 0, st>>>(s, core, core_stride, ldcore, uk, vk, out_stride, ldo,
-                                              sv, sv_stride);
+  if (s <= 40)
+    arrow_svd_kernel<40><<<batch, threads, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
+                                                    out_stride, ldo, sv, sv_stride);
+  else if (s <= 72)
+    arrow_svd_kernel<72><<<batch, threads, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
+                                                    out_stride, ldo, sv, sv_stride);
+  else if (s <= 136)
+    arrow_svd_kernel<136><<<batch, threads, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
+                                                     out_stride, ldo, sv, sv_stride);
+  else
+    arrow_svd_kernel<kN><<<batch, threads, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
+                                                    out_stride, ldo, sv, sv_stride);
   ISVD_LAUNCHED();
   return ISVD_OK;
 }

@@ -191,6 +191,7 @@ __global__ void jacobi_core_kernel(int s, const double* __restrict__ core, int64
 // and threshold as _kernels.pyx:38-57) is computed there and broadcast
 // through shared memory.
 constexpr int kJ32Warps = 4;
+constexpr double kConvRel = 1e-8;
 
 template <bool ODD>
 __device__ __forceinline__ void j32_pair_products(const double (&g)[32], int k, double& pp,
@@ -214,7 +215,7 @@ __device__ __forceinline__ void halve(double& keep, double lo, double hi, bool u
 
 template <bool ODD>
 __device__ __forceinline__ bool j32_round(double (&g)[32], double (&v)[32], int lane,
-                                          double2* cs_sm) {
+                                          double2* cs_sm, float& relmax) {
   // reduce-scatter of 16 pairs x (pp, qq, pq): lane l ends with pair l >> 1
   double P[8], Q[8], W[8];
   const bool b4 = lane & 16;
@@ -247,8 +248,10 @@ __device__ __forceinline__ bool j32_round(double (&g)[32], double (&v)[32], int 
   const double aqq = Q[0] + __shfl_xor_sync(0xffffffffu, Q[0], 1);
   const double apq = W[0] + __shfl_xor_sync(0xffffffffu, W[0], 1);
   double c = 1.0, s = 0.0;
-  const bool rot = fabs(apq) > kOrthoEps * sqrt(app * aqq);
+  const double scale = sqrt(app * aqq);
+  const bool rot = fabs(apq) > kOrthoEps * scale;
   if (rot) {
+    relmax = fmaxf(relmax, (float)(fabs(apq) / scale));
     const double zeta = (aqq - app) / (2.0 * apq);
     const double t = zeta >= 0.0 ? 1.0 / (zeta + sqrt(1.0 + zeta * zeta))
                                  : -1.0 / (-zeta + sqrt(1.0 + zeta * zeta));
@@ -293,15 +296,21 @@ __global__ void __launch_bounds__(kJ32Warps * 32) jacobi32_kernel(
     g[j] = (lane < s && j < s) ? K[lane * ldcore + j] : 0.0;
     v[j] = (lane == j && lane < s) ? 1.0 : 0.0;
   }
+  // Sweeps until none rotates (_kernels.pyx:58-59).  Quadratic convergence:
+  // once every rotation of a sweep had |a_pq| <= 1e-8 sqrt(a_pp a_qq), the
+  // off-diagonal left after it is O(1e-16) relative, below the reference's
+  // 1e-14 rotation threshold, so the confirming no-op sweep is skipped.
   int sweeps = 0;
   for (; sweeps < kMaxSweeps;) {
     bool any = false;
+    float relmax = 0.0f;
     for (int rr = 0; rr < 16; ++rr) {
-      any |= j32_round<false>(g, v, lane, cs_sm);
-      any |= j32_round<true>(g, v, lane, cs_sm);
+      any |= j32_round<false>(g, v, lane, cs_sm, relmax);
+      any |= j32_round<true>(g, v, lane, cs_sm, relmax);
     }
     ++sweeps;
     if (!any) break;
+    if (warp_max((double)relmax) <= kConvRel) break;
   }
   // column norms: reduce-scatter 32 sums, lane l ends with position l
   double R[16];

@@ -18,6 +18,7 @@
 #include <vector>
 #include "common.cuh"
 #include "dense_svd.cuh"
+#include "metrics.cuh"
 #include "../../include/isvd.h"
 
 namespace isvd {
@@ -280,6 +281,55 @@ __global__ void dsvd_finalize_kernel(int m, int n, int nc, int ldx, int ncp,
   }
 }
 
+// ---- orthonormality polish of the normalised side (one CholeskyQR step):
+// Jacobi leaves the live columns orthogonal to ~tol; U <- U R^{-1} with
+// U^T U = R^T R restores orthonormality to rounding while moving each
+// vector by O(tol) only.  Dead (zero) columns are completed afterwards.
+__global__ void polish_chol_kernel(int w, double* __restrict__ G, const double* __restrict__ s,
+                                   int64_t s_stride, int* __restrict__ live) {
+  const int b = blockIdx.x;
+  double* g = G + (int64_t)b * w * w;
+  const double* sb = s + b * s_stride;
+  __shared__ int wl;
+  if (threadIdx.x == 0) {
+    int c = 0;
+    while (c < w && sb[c] > 0.0) ++c;
+    wl = c;
+  }
+  __syncthreads();
+  const int L = wl;
+  for (int k = 0; k < L; ++k) {
+    if (threadIdx.x == 0) g[k * w + k] = sqrt(fmax(g[k * w + k], 1e-300));
+    __syncthreads();
+    const double d = g[k * w + k];
+    for (int j = k + 1 + threadIdx.x; j < L; j += blockDim.x) g[k * w + j] /= d;
+    __syncthreads();
+    const int rem = L - k - 1;
+    for (int idx = threadIdx.x; idx < rem * rem; idx += blockDim.x) {
+      const int i = k + 1 + idx / rem, j = k + 1 + idx % rem;
+      if (j >= i) g[i * w + j] -= g[k * w + i] * g[k * w + j];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) live[b] = L;
+}
+
+__global__ void polish_trsm_kernel(int rows, int w, Mat X, const double* __restrict__ G,
+                                   const int* __restrict__ live) {
+  const int b = blockIdx.y;
+  const int L = live[b];
+  const double* R = G + (int64_t)b * w * w;
+  double* xb = X.p + b * X.stride;
+  for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < rows; row += gridDim.x * blockDim.x) {
+    double* xr = xb + (int64_t)row * X.ld;
+    for (int j = 0; j < L; ++j) {
+      double acc = xr[j];
+      for (int i = 0; i < j; ++i) acc -= xr[i] * R[i * w + j];
+      xr[j] = acc / R[j * w + j];
+    }
+  }
+}
+
 }  // namespace
 
 DenseSvdPlan dense_svd_plan(int m, int n) {
@@ -316,7 +366,7 @@ int dense_svd_run(int batch, int m, int n, const double* a, int64_t a_stride, in
   // accurate to O(tol^2) relative and the vectors to O(tol / relative gap).  1e-12
   // also stays above the rounding floor of the Gram-based inner rotations
   // (eps sqrt(M_pp / M_qq) for strongly graded pairs), so the sweep count stays low.
-  const double tol = std::max(1e-12, 4.0 * std::sqrt((double)P.len) * eps);
+  const double tol = std::max(1e-12, 16.0 * std::sqrt((double)P.len) * eps);
   std::vector<int> fl(batch, 0);
   int sweep = 0;
   const int kMaxOuter = 40;
@@ -357,6 +407,30 @@ int dense_svd_run(int batch, int m, int n, const double* a, int64_t a_stride, in
     dsvd_finalize_kernel<<<batch, 256, smem, st>>>(m, n, P.nc, P.ldx, P.ncp, x, xs, jac, js, w, u,
                                                    v, s_w, s_w_stride, s_all, s_all_stride);
     ISVD_LAUNCHED();
+  }
+  // orthonormality polish of the normalised side (U if m >= n, else V)
+  const bool tall = m >= n;
+  Mat ns = tall ? u : v;
+  const int rows = tall ? m : n;
+  if (ns.p && s_w && w > 0 && w <= 160) {
+    double *part = nullptr, *G = nullptr;
+    int* live = nullptr;
+    const size_t np = (size_t)batch * gram_nblk(rows) * w * w;
+    ISVD_CUDA(cudaMallocAsync((void**)&part, sizeof(double) * np, st));
+    ISVD_CUDA(cudaMallocAsync((void**)&G, sizeof(double) * batch * w * w, st));
+    ISVD_CUDA(cudaMallocAsync((void**)&live, sizeof(int) * batch, st));
+    int rc = launch_gram(batch, rows, w, w, ns, ns, part, G, st);
+    if (rc == ISVD_OK) {
+      polish_chol_kernel<<<batch, 256, 0, st>>>(w, G, s_w, s_w_stride, live);
+      ISVD_LAUNCHED();
+      const int gx = std::min(ceil_div(rows, 128), 1024);
+      polish_trsm_kernel<<<dim3(gx, batch), 128, 0, st>>>(rows, w, ns, G, live);
+      ISVD_LAUNCHED();
+    }
+    cudaFreeAsync(part, st);
+    cudaFreeAsync(G, st);
+    cudaFreeAsync(live, st);
+    if (rc != ISVD_OK) return rc;
   }
   return ISVD_OK;
 }

@@ -15,6 +15,12 @@ constexpr int kRMax = kCoreMaxS;  // max factor width handled by the tick kernel
 // over rows, coalesced row reads) fused with the tracked-matrix write and
 // ||x||^2.  Pass 2: z = x - F p (warp per row), rho = ||z||.  Then the
 // (r+1) x (r+1) Brand core [[diag s, 0], [p, rho]] (_kernels.pyx:149-157).
+// STAGE: F (contiguous rows x ld) is brought into shared memory with TMA bulk
+// copies (cp.async.bulk + mbarrier) while the CTA streams x; both passes then
+// run on-chip (F read from HBM exactly once, one outstanding 16-64 KB
+// request per CTA).  Pass 2 walks each row with a skewed column index, so
+// the one-thread-per-row reads are bank-conflict free.
+template <bool STAGE>
 __global__ void __launch_bounds__(256) project_append_kernel(
     int rows, int r, Mat F, const double* __restrict__ x, int64_t x_stride,
     const double* __restrict__ s, int lds, double tol, double* __restrict__ core,
@@ -25,27 +31,51 @@ __global__ void __launch_bounds__(256) project_append_kernel(
   __shared__ double part[8][kRMax];
   __shared__ double p[kRMax];
   __shared__ double red[32];
+  __shared__ __align__(8) uint64_t bar;
+  extern __shared__ __align__(128) double Fs[];  // STAGE: [rows][F.ld], then x[rows]
   const int b = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const double* Fb = F.p + b * F.stride;
   const double* xb = x + b * x_stride;
   double* Ab = A ? A + b * a_stride + a_off : nullptr;
+  double* xs = Fs + (size_t)rows * F.ld;
+
+  if (STAGE) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      fence_barrier_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint32_t total = (uint32_t)rows * F.ld * 8u;
+      mbar_expect_tx(&bar, total);
+      const uint32_t kPiece = 32768;
+      for (uint32_t off = 0; off < total; off += kPiece)
+        bulk_g2s(reinterpret_cast<char*>(Fs) + off, reinterpret_cast<const char*>(Fb) + off,
+                 min(kPiece, total - off), &bar);
+    }
+  }
+  // x: norm, tracked-matrix write (and staging) overlap the bulk copy
+  double xx = 0.0;
+  for (int c = threadIdx.x; c < rows; c += blockDim.x) {
+    const double xc = xb[c];
+    xx = fma(xc, xc, xx);
+    if (Ab) Ab[(int64_t)c * a_step] = xc;
+    if (STAGE) xs[c] = xc;
+  }
+  if (STAGE) mbar_wait(&bar, 0);
+  __syncthreads();
 
   double acc[(kRMax + 31) / 32];
 #pragma unroll
   for (int t = 0; t < (kRMax + 31) / 32; ++t) acc[t] = 0.0;
-  double xx = 0.0;
   for (int c = warp; c < rows; c += nw) {
-    double xc = xb[c];
-    const double* fr = Fb + (int64_t)c * F.ld;
+    const double xc = STAGE ? xs[c] : xb[c];
+    const double* fr = STAGE ? Fs + (size_t)c * F.ld : Fb + (int64_t)c * F.ld;
 #pragma unroll
     for (int t = 0; t < (kRMax + 31) / 32; ++t) {
       int l = lane + 32 * t;
       if (l < r) acc[t] = fma(fr[l], xc, acc[t]);
-    }
-    if (lane == 0) {
-      xx = fma(xc, xc, xx);
-      if (Ab) Ab[(int64_t)c * a_step] = xc;
     }
   }
 #pragma unroll
@@ -63,15 +93,30 @@ __global__ void __launch_bounds__(256) project_append_kernel(
 
   double zz = 0.0;
   double* zb = z + b * z_stride;
-  for (int c = warp; c < rows; c += nw) {
-    const double* fr = Fb + (int64_t)c * F.ld;
-    double v = 0.0;
-    for (int l = lane; l < r; l += 32) v = fma(fr[l], p[l], v);
-    v = warp_sum(v);
-    double zc = xb[c] - v;
-    if (lane == 0) {
+  if (STAGE) {
+    for (int c = threadIdx.x; c < rows; c += blockDim.x) {
+      const double* fr = Fs + (size_t)c * F.ld;
+      double v = 0.0;
+      int l = c % r;
+      for (int j = 0; j < r; ++j) {
+        v = fma(fr[l], p[l], v);
+        l = (l + 1 == r) ? 0 : l + 1;
+      }
+      const double zc = xs[c] - v;
       zb[c] = zc;
       zz = fma(zc, zc, zz);
+    }
+  } else {
+    for (int c = warp; c < rows; c += nw) {
+      const double* fr = Fb + (int64_t)c * F.ld;
+      double v = 0.0;
+      for (int l = lane; l < r; l += 32) v = fma(fr[l], p[l], v);
+      v = warp_sum(v);
+      double zc = xb[c] - v;
+      if (lane == 0) {
+        zb[c] = zc;
+        zz = fma(zc, zc, zz);
+      }
     }
   }
   double rho = sqrt(block_sum(zz, red));
@@ -441,9 +486,24 @@ int launch_project_append(int batch, int rows, int r, Mat F, const double* x, in
     set_error("factor width exceeds kernel limit");
     return ISVD_EINVAL;
   }
-  project_append_kernel<<<batch, 256, 0, st>>>(rows, r, F, x, x_stride, s, lds, tol, core,
-                                               core_stride, ldcore, z, z_stride, inj_scale, rho_out,
-                                               xnorm_out, A, a_stride, a_off, a_step, N);
+  const size_t stage = sizeof(double) * ((size_t)rows * F.ld + rows);
+  const bool aligned = (reinterpret_cast<uintptr_t>(F.p) % 16 == 0) && (F.stride % 2 == 0) &&
+                       (F.ld % 2 == 0);
+  if (stage <= 96 * 1024 && aligned) {
+    static bool attr = false;
+    if (!attr) {
+      ISVD_CUDA(cudaFuncSetAttribute(project_append_kernel<true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+      attr = true;
+    }
+    project_append_kernel<true><<<batch, 256, stage, st>>>(
+        rows, r, F, x, x_stride, s, lds, tol, core, core_stride, ldcore, z, z_stride, inj_scale,
+        rho_out, xnorm_out, A, a_stride, a_off, a_step, N);
+  } else {
+    project_append_kernel<false><<<batch, 256, 0, st>>>(
+        rows, r, F, x, x_stride, s, lds, tol, core, core_stride, ldcore, z, z_stride, inj_scale,
+        rho_out, xnorm_out, A, a_stride, a_off, a_step, N);
+  }
   ISVD_LAUNCHED();
   return ISVD_OK;
 }

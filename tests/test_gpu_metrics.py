@@ -26,7 +26,8 @@ class TestDenseSvd:
         a = rng.standard_normal((m, n))
         f, fo = full_svd(a), o_full_svd(a)
         assert rel_err(f.s, fo.s) < 1e-12
-        assert frobenius_norm(a - reconstruct(f)) <= 1e-12 * max(1.0, frobenius_norm(a))
+        # SPEC.md full_svd post-condition: ||A - U S Vt||_F <= 1e-9 max(1, ||A||_F)
+        assert frobenius_norm(a - reconstruct(f)) <= 1e-11 * max(1.0, frobenius_norm(a))
         # SPEC invariant is 1e-8; the accumulated Jacobi rotations sit ~1e-12
         assert orthonormality_defect(f.u) <= 1e-10
         assert orthonormality_defect(f.vt.T) <= 1e-10
