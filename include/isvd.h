@@ -49,6 +49,9 @@ int isvd_version(void);
 /* Number of kernel launches issued by this process so far (evidence counter
  * reported by bench.py as `gpu_launches`). */
 int64_t isvd_launch_count(void);
+/* Device profiling counters (out8[0] = Jacobi sweeps summed over cores,
+ * out8[1] = cores factored by the warp Jacobi kernel); reset if nonzero. */
+int isvd_debug_counters(int64_t* out8, int reset);
 
 /* 1. Functional kernels (backend.py:54-63) ---------------------------------- */
 

@@ -23,6 +23,9 @@
 
 namespace isvd {
 
+// profiling counters: [0] jacobi32 sweeps, [1] jacobi32 cores (isvd_debug_counters)
+__device__ unsigned long long g_debug_counters[8];
+
 namespace {
 
 __device__ __forceinline__ int tour_slot(int j, int round, int ne) {
@@ -312,6 +315,8 @@ __global__ void __launch_bounds__(kJ32Warps * 32) jacobi32_kernel(
     if (!any) break;
     if (warp_max((double)relmax) <= kConvRel) break;
   }
+  if (lane == 0) atomicAdd(&g_debug_counters[0], (unsigned long long)sweeps);
+  if (lane == 0) atomicAdd(&g_debug_counters[1], 1ull);
   // column norms: reduce-scatter 32 sums, lane l ends with position l
   double R[16];
   {
@@ -386,6 +391,17 @@ __global__ void __launch_bounds__(kJ32Warps * 32) jacobi32_kernel(
 }
 
 }  // namespace
+
+int read_debug_counters(int64_t* out, int reset) {
+  unsigned long long h[8];
+  ISVD_CUDA(cudaMemcpyFromSymbol(h, g_debug_counters, sizeof(h)));
+  for (int i = 0; i < 8; ++i) out[i] = (int64_t)h[i];
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    ISVD_CUDA(cudaMemcpyToSymbol(g_debug_counters, z, sizeof(z)));
+  }
+  return ISVD_OK;
+}
 
 size_t core_svd_smem_bytes(int s, bool v_in_smem) {
   int ps = s | 1;

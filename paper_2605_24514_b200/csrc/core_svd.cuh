@@ -8,6 +8,7 @@ constexpr int kCoreMaxS = 160;   // largest core: k_max + 1 (k <= 159)
 constexpr int kSmemMaxS = 112;   // G and V both in shared memory up to here
 
 size_t core_svd_smem_bytes(int s, bool v_in_smem);
+int read_debug_counters(int64_t* out, int reset);
 
 // Batched core SVD.  core[b] is s x s row-major at core + b*core_stride with
 // row pitch ldcore.  Outputs uk[b], vk[b] (row-major s x s, pitch ldo, the

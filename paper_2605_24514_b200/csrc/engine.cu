@@ -355,6 +355,11 @@ extern "C" {
 
 const char* isvd_last_error(void) { return g_err.c_str(); }
 int isvd_version(void) { return 1; }
+int isvd_debug_counters(int64_t* out8, int reset) {
+  if (!out8) { set_error("null argument"); return ISVD_EINVAL; }
+  ISVD_TRY(check_device());
+  return read_debug_counters(out8, reset);
+}
 int64_t isvd_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
 
 int isvd_engine_create(isvd_engine** out, int batch, int m, int n, int k, double tol,

@@ -286,6 +286,89 @@ __global__ void __launch_bounds__(kRotWarps * 32, 2)
   }
 }
 
+// Small-width variant (KP <= 32, keep <= 32): the core rotation is held as
+// DMMA B-fragments in registers (loaded straight from L2, no shared staging,
+// no block barrier); kk-outer / nn-inner ordering gives four independent
+// accumulator chains per lane.
+constexpr int kRegWarps = 4;
+constexpr int kRegRowsPerBlock = 256;
+
+template <int KP>
+__global__ void __launch_bounds__(kRegWarps * 32, 3)
+    rotate_reg_kernel(int r, int keep, RotJob j0, RotJob j1, int nblk0) {
+  constexpr int KQ = KP / 4;
+  const bool second = blockIdx.x >= nblk0;
+  const RotJob& J = second ? j1 : j0;
+  const int blk = second ? blockIdx.x - nblk0 : blockIdx.x;
+  const int b = blockIdx.y;
+  const double* Q = J.Q + b * J.q_stride;
+  const bool has_last = (J.z != nullptr) || J.new_row;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  double bq[KQ][4];
+#pragma unroll
+  for (int kk = 0; kk < KQ; ++kk)
+#pragma unroll
+    for (int nn = 0; nn < 4; ++nn) {
+      const int l = q * KQ + kk, c = nn * 8 + g;
+      bq[kk][nn] = (l < r && c < keep) ? Q[l * J.ldq + c] : 0.0;
+    }
+  double qr[4][2];
+#pragma unroll
+  for (int nn = 0; nn < 4; ++nn)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int c = nn * 8 + 2 * q + e;
+      qr[nn][e] = (J.z && c < keep) ? Q[r * J.ldq + c] : 0.0;
+    }
+  double* X = J.X.p + b * J.X.stride;
+  const int ld = J.X.ld;
+  if (J.new_row && blk == 0) {
+    double* nr = X + (int64_t)J.rows * ld;
+    for (int c = threadIdx.x; c < ld; c += blockDim.x)
+      nr[c] = (has_last && c < keep) ? Q[r * J.ldq + c] : 0.0;
+  }
+  const double zscale = J.z ? J.inj_scale[b] : 0.0;
+  const double* zb = J.z ? J.z + b * J.z_stride : nullptr;
+  const int row_begin = blk * kRegRowsPerBlock;
+  const int row_end = min(J.rows, row_begin + kRegRowsPerBlock);
+  for (int row0 = row_begin + warp * 8; row0 < row_end; row0 += kRegWarps * 8) {
+    const int row = row0 + g;
+    double a[KQ];
+    if (row < row_end) {
+      const double* src = X + (int64_t)row * ld + q * KQ;
+#pragma unroll
+      for (int kk = 0; kk < KQ; kk += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(src + kk);
+        a[kk] = v.x;
+        a[kk + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < KQ; ++kk) a[kk] = 0.0;
+    }
+    const double zr = (zb && row < row_end) ? zb[row] * zscale : 0.0;
+    double d[4][2];
+#pragma unroll
+    for (int nn = 0; nn < 4; ++nn) d[nn][0] = d[nn][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < KQ; ++kk)
+#pragma unroll
+      for (int nn = 0; nn < 4; ++nn) dmma_8x8x4(d[nn][0], d[nn][1], a[kk], bq[kk][nn]);
+    if (row < row_end) {
+#pragma unroll
+      for (int nn = 0; nn < 4; ++nn) {
+        const int c0 = nn * 8 + 2 * q;
+        if (c0 < ld) {
+          const double o0 = fma(zr, qr[nn][0], d[nn][0]);
+          const double o1 = fma(zr, qr[nn][1], d[nn][1]);
+          *reinterpret_cast<double2*>(X + (int64_t)row * ld + c0) = make_double2(o0, o1);
+        }
+      }
+    }
+  }
+}
+
 // ----------------------------------------------------- completion (_install)
 __device__ void complete_column(double* X, int64_t ld, int rows, int w, int t, double* coef,
                                 double* red) {
@@ -538,6 +621,21 @@ static int rotate_dispatch(int batch, int r, int keep, const RotJob& j0, const R
     if (j1->new_row && nb1 == 0) nb1 = 1;
   }
   if (nb0 + nb1 == 0) return ISVD_OK;
+  if constexpr (KP <= 32) {
+    if (NP <= 32) {
+      int rb0 = ceil_div(j0.rows, kRegRowsPerBlock);
+      if (j0.new_row && rb0 == 0) rb0 = 1;
+      int rb1 = 0;
+      if (j1) {
+        rb1 = ceil_div(j1->rows, kRegRowsPerBlock);
+        if (j1->new_row && rb1 == 0) rb1 = 1;
+      }
+      rotate_reg_kernel<KP><<<dim3(rb0 + rb1, batch), kRegWarps * 32, 0, st>>>(
+          r, keep, j0, j1 ? *j1 : j0, rb0);
+      ISVD_LAUNCHED();
+      return ISVD_OK;
+    }
+  }
   dim3 grid(nb0 + nb1, batch);
   rotate_kernel<KP><<<grid, kRotWarps * 32, smem, st>>>(r, keep, NP, j0, j1 ? *j1 : j0, nb0);
   ISVD_LAUNCHED();
