@@ -273,6 +273,9 @@ def run_gpu(args):
     stream = torch.cuda.ExternalStream(eng.cuda_stream, device=dev)
     lib = _lib.load()
     _lib.check(lib.isvd_engine_set_timing(eng._h.h, 1))
+    dbg = np.zeros(8, dtype=np.int64)
+    _lib.check(lib.isvd_debug_counters(dbg.ctypes.data_as(
+        __import__("ctypes").POINTER(__import__("ctypes").c_int64)), 1))
     barrier()
     l0 = _lib.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -283,6 +286,10 @@ def run_gpu(args):
         e1.record(stream)
         barrier()
     launches = _lib.launch_count() - l0
+    _lib.check(lib.isvd_debug_counters(dbg.ctypes.data_as(
+        __import__("ctypes").POINTER(__import__("ctypes").c_int64)), 1))
+    diagnostics = {"jacobi32_sweeps_per_core": float(dbg[0]) / max(1, int(dbg[1])),
+                   "jacobi32_cores": int(dbg[1])}
     dev_ms = e0.elapsed_time(e1)
     ph = np.zeros(10)
     nt3 = np.zeros(3, dtype=np.int64)
@@ -402,6 +409,7 @@ def run_gpu(args):
             "flushes": n_flush,
             "phase_ms_by_event": phase_by_kind,
             "tick_effective_gbs": all_bytes / (t_max / 1e3) / 1e9,
+            "diagnostics": diagnostics,
         }
         if world == 1 and not args.no_cpu_baseline:
             v, cores, updates, secs = cpu_reference(args.cpu_streams, args.cpu_events)

@@ -56,6 +56,17 @@ struct ArrowSmem {
   double scale;
 };
 
+// 1/x to ~1 ulp: MUFU.RCP64H seed + two Newton steps (no IEEE-division
+// fix-up path); used for the secular-function terms and vector entries.
+__device__ __forceinline__ double frcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 template <class SM>
 __device__ __forceinline__ void apply_rots(double* col, int64_t stride, const SM& S,
                                            bool left) {
@@ -213,7 +224,7 @@ __global__ void __launch_bounds__((kN + 31) / 32 * 32) arrow_svd_kernel(int n, c
       double psi = 0.0, dpsi = 0.0, phi = 0.0, dphi = 0.0, aps = 0.0;
       for (int j = 0; j < N; ++j) {
         const double dj = S.kd[j];
-        const double t = 1.0 / ((dj - dorg) * (dj + dorg) - x);
+        const double t = frcp((dj - dorg) * (dj + dorg) - x);
         const double w = S.kz[j] * S.kz[j] * t;
         if (j <= i) {
           psi += w;
@@ -298,6 +309,34 @@ __global__ void __launch_bounds__((kN + 31) / 32 * 32) arrow_svd_kernel(int n, c
   for (int t = 0; t < n; ++t) smax = fmax(smax, S.sig[t]);
 
   // ---- vectors, written straight into their sorted columns
+  if (ND == 0 && S.nrot == 0) {
+    // common case (no deflation): every row of both columns is written once
+    for (int t = tid; t < n; t += blockDim.x) {
+      const int pc = S.pos[t];
+      const int i = t;
+      const double dorg = S.kd[S.org[i]];
+      const double mu = S.mu[i];
+      double nv = 0.0, nu = 1.0;  // the z-row entry of u is -1
+      for (int j = 0; j < N; ++j) {
+        const double dj = S.kd[j];
+        const double vj = S.zhat[j] * frcp((dj - dorg) * (dj + dorg) - mu);
+        nv = fma(vj, vj, nv);
+        nu = fma(dj * vj, dj * vj, nu);
+      }
+      const double iv = rsqrt(nv), iu = rsqrt(nu);
+      const double sg = S.sig[t];
+      const bool dead = !(sg > 0.0) || sg < kZeroSvRtol * smax;
+      for (int j = 0; j < N; ++j) {
+        const double dj = S.kd[j];
+        const double vj = S.zhat[j] * frcp((dj - dorg) * (dj + dorg) - mu);
+        const int row = S.kcol[j];
+        V[row * ldo + pc] = vj * iv;
+        if (row != r) U[row * ldo + pc] = dead ? 0.0 : dj * vj * iu;
+      }
+      U[r * ldo + pc] = dead ? 0.0 : -iu;
+      SV[pc] = dead ? 0.0 : sg * scale;
+    }
+  } else
   for (int t = tid; t < n; t += blockDim.x) {
     const int pc = S.pos[t];
     double* vcol = V + pc;

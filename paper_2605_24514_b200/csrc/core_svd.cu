@@ -197,17 +197,10 @@ constexpr int kJ32Warps = 4;
 constexpr double kConvRel = 1e-8;
 
 template <bool ODD>
-__device__ __forceinline__ void j32_pair_products(const double (&g)[32], int k, double& pp,
-                                                  double& qq, double& pq) {
+__device__ __forceinline__ double j32_pair_product(const double (&g)[32], int k) {
+  if (ODD && k == 15) return 0.0;
   const int p = ODD ? 2 * k + 1 : 2 * k;
-  if (ODD && k == 15) {
-    pp = qq = pq = 0.0;
-    return;
-  }
-  const double x = g[p], y = g[p + 1];
-  pp = x * x;
-  qq = y * y;
-  pq = x * y;
+  return g[p] * g[p + 1];
 }
 
 __device__ __forceinline__ void halve(double& keep, double lo, double hi, bool upper, int off) {
@@ -216,51 +209,62 @@ __device__ __forceinline__ void halve(double& keep, double lo, double hi, bool u
   keep = mine + __shfl_xor_sync(0xffffffffu, other, off);
 }
 
+__device__ __forceinline__ double j32_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// One round: lane l owns pair k = l >> 1 (lanes 2k, 2k+1 redundantly) and
+// carries the squared norms (nlo, nhi) of that pair's two columns.  Only the
+// 16 cross products a_pq are reduce-scattered; the norms are updated in
+// place (a_pp' = a_pp - t a_pq, a_qq' = a_qq + t a_pq) and recomputed
+// exactly at every sweep start.
 template <bool ODD>
 __device__ __forceinline__ bool j32_round(double (&g)[32], double (&v)[32], int lane,
-                                          double2* cs_sm, float& relmax) {
-  // reduce-scatter of 16 pairs x (pp, qq, pq): lane l ends with pair l >> 1
-  double P[8], Q[8], W[8];
+                                          double2* cs_sm, double& nlo, double& nhi,
+                                          float& relmax, double null2) {
+  double W[8];
   const bool b4 = lane & 16;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    double pa, qa, wa, pb, qb, wb;
-    j32_pair_products<ODD>(g, i, pa, qa, wa);
-    j32_pair_products<ODD>(g, i + 8, pb, qb, wb);
-    halve(P[i], pa, pb, b4, 16);
-    halve(Q[i], qa, qb, b4, 16);
-    halve(W[i], wa, wb, b4, 16);
-  }
+  for (int i = 0; i < 8; ++i)
+    halve(W[i], j32_pair_product<ODD>(g, i), j32_pair_product<ODD>(g, i + 8), b4, 16);
   const bool b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    halve(P[i], P[i], P[i + 4], b3, 8);
-    halve(Q[i], Q[i], Q[i + 4], b3, 8);
-    halve(W[i], W[i], W[i + 4], b3, 8);
-  }
+  for (int i = 0; i < 4; ++i) halve(W[i], W[i], W[i + 4], b3, 8);
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    halve(P[i], P[i], P[i + 2], b2, 4);
-    halve(Q[i], Q[i], Q[i + 2], b2, 4);
-    halve(W[i], W[i], W[i + 2], b2, 4);
-  }
-  halve(P[0], P[0], P[1], b1, 2);
-  halve(Q[0], Q[0], Q[1], b1, 2);
+  for (int i = 0; i < 2; ++i) halve(W[i], W[i], W[i + 2], b2, 4);
   halve(W[0], W[0], W[1], b1, 2);
-  const double app = P[0] + __shfl_xor_sync(0xffffffffu, P[0], 1);
-  const double aqq = Q[0] + __shfl_xor_sync(0xffffffffu, Q[0], 1);
   const double apq = W[0] + __shfl_xor_sync(0xffffffffu, W[0], 1);
-  double c = 1.0, s = 0.0;
-  const double scale = sqrt(app * aqq);
-  const bool rot = fabs(apq) > kOrthoEps * scale;
+  const double app = nlo, aqq = nhi;
+  double c = 1.0, s = 0.0, t = 0.0;
+  const double scale = sqrt(fmax(app * aqq, 0.0));
+  // Columns whose norm is below 1e-15 of the largest are numerically zero
+  // (they snap to sigma = 0 and their U column is completed); rotating them
+  // only chases rounding noise towards underflow, so such pairs are left.
+  const bool rot = fabs(apq) > kOrthoEps * scale && fmin(app, aqq) > null2;
   if (rot) {
     relmax = fmaxf(relmax, (float)(fabs(apq) / scale));
-    const double zeta = (aqq - app) / (2.0 * apq);
-    const double t = zeta >= 0.0 ? 1.0 / (zeta + sqrt(1.0 + zeta * zeta))
-                                 : -1.0 / (-zeta + sqrt(1.0 + zeta * zeta));
-    c = 1.0 / sqrt(1.0 + t * t);
+    const double zeta = (aqq - app) * j32_rcp(2.0 * apq);
+    const double root = fabs(zeta) > 1e100 ? fabs(zeta) : sqrt(fma(zeta, zeta, 1.0));
+    t = copysign(j32_rcp(fabs(zeta) + root), zeta);
+    c = rsqrt(fma(t, t, 1.0));
     s = t * c;
   }
+  const bool dummy = ODD && (lane >> 1) == 15;
+  if (!dummy) {
+    // norms after the rotation, then the two columns swap places
+    const double np = fma(-t, apq, app), nq = fma(t, apq, aqq);
+    nlo = nq;
+    nhi = np;
+  }
+#ifdef ISVD_DEBUG_J32
+  if (blockIdx.x == 0 && (lane & 1) == 0 && (rot || c != c || s != s || app != app || aqq != aqq))
+    printf("odd=%d lane=%d app=%g aqq=%g apq=%g rot=%d c=%g s=%g\n", (int)ODD, lane, app, aqq, apq, (int)rot, c, s);
+#endif
   if ((lane & 1) == 0) cs_sm[lane >> 1] = make_double2(c, s);
   __syncwarp();
 #pragma unroll
@@ -307,9 +311,38 @@ __global__ void __launch_bounds__(kJ32Warps * 32) jacobi32_kernel(
   for (; sweeps < kMaxSweeps;) {
     bool any = false;
     float relmax = 0.0f;
+    // exact squared column norms at the sweep start (lane l: position l)
+    double R[16];
+    {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) halve(R[i], g[i] * g[i], g[i + 16] * g[i + 16], lane & 16, 16);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) halve(R[i], R[i], R[i + 8], lane & 8, 8);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) halve(R[i], R[i], R[i + 4], lane & 4, 4);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) halve(R[i], R[i], R[i + 2], lane & 2, 2);
+      halve(R[0], R[0], R[1], lane & 1, 1);
+    }
+    double nlo = __shfl_sync(0xffffffffu, R[0], lane & ~1);
+    double nhi = __shfl_sync(0xffffffffu, R[0], lane | 1);
+    const double null2 = fmax(1e-30 * warp_max(R[0]), 1e-290);
     for (int rr = 0; rr < 16; ++rr) {
-      any |= j32_round<false>(g, v, lane, cs_sm, relmax);
-      any |= j32_round<true>(g, v, lane, cs_sm, relmax);
+      any |= j32_round<false>(g, v, lane, cs_sm, nlo, nhi, relmax, null2);
+      // even -> odd pairing: (2k+1, 2k+2); position 0 sits out
+      const double n0 = nlo;
+      {
+        const double down = __shfl_down_sync(0xffffffffu, nlo, 2);
+        nlo = nhi;
+        nhi = down;
+      }
+      any |= j32_round<true>(g, v, lane, cs_sm, nlo, nhi, relmax, null2);
+      // odd -> even pairing: (2k, 2k+1)
+      {
+        const double up = __shfl_up_sync(0xffffffffu, nhi, 2);
+        nhi = nlo;
+        nlo = (lane < 2) ? n0 : up;
+      }
     }
     ++sweeps;
     if (!any) break;
