@@ -219,99 +219,17 @@ def tick_bytes(B, m, n, w, row_tick):
     return 8 * B * (2 * m * w + 2 * n * w + 2 * w + 2)
 
 
-def run_gpu(args):
-    import torch
-    import torch.distributed as dist
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    from paper_2605_24514_b200 import BatchedSvdEngine, _lib
-    from paper_2605_24514_b200.sharding import max_over_ranks, shard_streams
-
-    total = args.streams
-    streams = list(shard_streams(total, world, rank))
-    B = len(streams)
-    steps, warm = args.steps, args.warmup
-    n_events = max(steps, warm)
-    a0, rows, ii, jj, dd = make_inputs(torch, dev, streams, n_events=n_events)
-    m_cap = M0 + (n_events + 1) // 2 + 1
-
-    def barrier():
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-
-    def run_ticks(eng, nt, host=None):
-        """nt ticks; device-resident inputs unless host=(rows, ii, jj, dd)."""
-        results = []
-        for t in range(nt):
-            if t % 2 == 0:
-                if host is None:
-                    eng.row_append(rows[t // 2])
-                else:
-                    eng.row_append(host[0][t // 2])
-            else:
-                if host is None:
-                    eng.rank_one_update(ii[t // 2], jj[t // 2], dd[t // 2])
-                else:
-                    eng.rank_one_update(host[1][t // 2], host[2][t // 2], host[3][t // 2])
-            if host is not None:
-                results.append(eng.scalars())  # D2H read of the step's result
-        return results
-
-    # ---------------- device-resident timing (value)
-    eng = BatchedSvdEngine(a0, K, m_cap=m_cap, k_cap=K)
-    run_ticks(eng, warm)
-    del eng
-    torch.cuda.empty_cache()
-    eng = BatchedSvdEngine(a0, K, m_cap=m_cap, k_cap=K)
-    stream = torch.cuda.ExternalStream(eng.cuda_stream, device=dev)
-    lib = _lib.load()
-    _lib.check(lib.isvd_engine_set_timing(eng._h.h, 1))
-    dbg = np.zeros(8, dtype=np.int64)
-    _lib.check(lib.isvd_debug_counters(dbg.ctypes.data_as(
-        __import__("ctypes").POINTER(__import__("ctypes").c_int64)), 1))
-    barrier()
-    l0 = _lib.launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(str(ROOT / "gpurun_out" / f"clocks_r{rank}.csv")) as clk:
-        e0.record(stream)
-        run_ticks(eng, steps)
-        eng.flush()  # materialise deferred U rotations inside the timed region
-        e1.record(stream)
-        barrier()
-    launches = _lib.launch_count() - l0
-    _lib.check(lib.isvd_debug_counters(dbg.ctypes.data_as(
-        __import__("ctypes").POINTER(__import__("ctypes").c_int64)), 1))
-    diagnostics = {"jacobi32_sweeps_per_core": float(dbg[0]) / max(1, int(dbg[1])),
-                   "jacobi32_cores": int(dbg[1])}
-    dev_ms = e0.elapsed_time(e1)
-    ph = np.zeros(10)
-    nt3 = np.zeros(3, dtype=np.int64)
-    _lib.check(lib.isvd_engine_phase_times(eng._h.h, _lib.dptr(ph), nt3.ctypes.data_as(
-        __import__("ctypes").POINTER(__import__("ctypes").c_int64))))
-    n_rows, n_r1, n_flush = (int(v) for v in nt3)
-    flush_ms, flush_bytes = float(ph[8]), float(ph[9])
-    phase_by_kind = {
-        kind: {name: float(ph[4 * i + j] / max(1, nt3[i]))
-               for j, name in enumerate(("project", "core_svd", "rotate", "install"))}
-        for i, kind in enumerate(("row_append", "rank_one"))}
-    # algorithmic bytes of the per-tick kernels (simulating the engine's
-    # deferred-U window: W = (32 + b) x 32 rotated in place, flushed every 32 rows)
-    proj_bytes = 0.0
-    rot_bytes = 0.0
-    all_bytes = 0.0
+def _simulate_bytes(B, steps):
+    """Algorithmic bytes of the per-tick kernels over `steps` ticks (simulating
+    the engine's deferred-U window: W = (32 + b) x 32 rotated in place,
+    flushed every 32 appended rows)."""
+    proj_bytes = rot_bytes = all_bytes = 0.0
     m, b_rows, active = M0, 0, False
     for t in range(steps):
         row = t % 2 == 0
         all_bytes += tick_bytes(B, m, N0, K, row)
         if row:
-            proj_bytes += 8.0 * B * (N0 * K + 2 * N0 + N0)   # V read, x read, A row write, z write
+            proj_bytes += 8.0 * B * (N0 * K + 2 * N0 + N0)   # V read, x read, A row, z write
             vb = N0 * K + N0 * K + N0                         # V read/write + z read
             if not active:
                 wb = (K + 1) * K                              # W = Uk copy
@@ -331,15 +249,106 @@ def run_gpu(args):
             else:
                 wb = 2 * (K + b_rows) * K
         rot_bytes += 8.0 * B * (vb + wb)
+    return proj_bytes, rot_bytes, all_bytes
+
+
+def run_gpu(args):
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2605_24514_b200 import BatchedSvdEngine, _lib
+    from paper_2605_24514_b200.sharding import max_over_ranks, shard_streams
+
+    lib = _lib.load()
+    i64p = ctypes.POINTER(ctypes.c_int64)
+    total = args.streams
+    streams = list(shard_streams(total, world, rank))
+    B = len(streams)
+    steps, warm = args.steps, args.warmup
+    n_events = max(steps, warm)
+    a0, rows, ii, jj, dd = make_inputs(torch, dev, streams, n_events=n_events)
+    m_cap = M0 + (n_events + 1) // 2 + 1
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def run_ticks(eng, nt, host=None):
+        """nt ticks; device-resident inputs unless host=(rows, ii, jj, dd)."""
+        for t in range(nt):
+            if t % 2 == 0:
+                eng.row_append(rows[t // 2] if host is None else host[0][t // 2])
+            elif host is None:
+                eng.rank_one_update(ii[t // 2], jj[t // 2], dd[t // 2])
+            else:
+                eng.rank_one_update(host[1][t // 2], host[2][t // 2], host[3][t // 2])
+            if host is not None:
+                eng.scalars()  # D2H read of the step's result (sync)
+
+    t_init = time.perf_counter()
+    eng = BatchedSvdEngine(a0, K, m_cap=m_cap, k_cap=K)
+    eng.synchronize()
+    init_s = time.perf_counter() - t_init
+    eng.snapshot()
+    # ---------------- warm-up (then back to the initial state)
+    run_ticks(eng, warm)
+    eng.flush()
+    eng.restore()
+    # ---------------- device-resident timing (value): grouped, no phase timing
+    stream = torch.cuda.ExternalStream(eng.cuda_stream, device=dev)
+    barrier()
+    l0 = _lib.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(str(ROOT / "gpurun_out" / f"clocks_r{rank}.csv")) as clk:
+        e0.record(stream)
+        run_ticks(eng, steps)
+        eng.flush()  # materialise deferred U rotations inside the timed region
+        e1.record(stream)
+        barrier()
+    launches = _lib.launch_count() - l0
+    dev_ms = e0.elapsed_time(e1)
     t_max = max_over_ranks(dev_ms, device=dev)
     value = total * steps / (t_max / 1e3)
     clock = clk.summary(local)
-    # sanity: spectrum of stream 0 is finite and sorted
     f0 = eng.factors(0)
     assert np.all(np.isfinite(f0.s)) and np.all(np.diff(f0.s) <= 0)
-    del eng
-    torch.cuda.empty_cache()
-
+    # ---------------- per-kernel breakdown (same ticks, one group, CUDA events
+    # around every phase on the engine stream)
+    diag_steps = min(steps, args.diag_steps)
+    eng.restore()
+    dbg = np.zeros(8, dtype=np.int64)
+    _lib.check(lib.isvd_debug_counters(dbg.ctypes.data_as(i64p), 1))
+    _lib.check(lib.isvd_engine_set_timing(eng._h.h, 1))
+    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    d0.record(stream)
+    run_ticks(eng, diag_steps)
+    eng.flush()
+    d1.record(stream)
+    torch.cuda.synchronize()
+    diag_ms = d0.elapsed_time(d1)
+    ph = np.zeros(10)
+    nt3 = np.zeros(3, dtype=np.int64)
+    _lib.check(lib.isvd_engine_phase_times(eng._h.h, _lib.dptr(ph), nt3.ctypes.data_as(i64p)))
+    _lib.check(lib.isvd_engine_set_timing(eng._h.h, 0))
+    _lib.check(lib.isvd_debug_counters(dbg.ctypes.data_as(i64p), 1))
+    n_flush = int(nt3[2])
+    flush_ms, flush_bytes = float(ph[8]), float(ph[9])
+    phase_by_kind = {
+        kind: {name: float(ph[4 * i + j] / max(1, nt3[i]))
+               for j, name in enumerate(("project", "core_svd", "rotate", "install"))}
+        for i, kind in enumerate(("row_append", "rank_one"))}
+    proj_bytes, rot_bytes, _ = _simulate_bytes(B, diag_steps)
+    _, _, all_bytes = _simulate_bytes(B, steps)
     # ---------------- end-to-end through the public API with host buffers
     e2e_steps = min(steps, args.e2e_steps)
     nrow = (e2e_steps + 1) // 2
@@ -351,7 +360,7 @@ def run_gpu(args):
     h_dd = torch.empty((nr1, B), dtype=torch.float64, pin_memory=True)
     h_ii.copy_(ii[:nr1]); h_jj.copy_(jj[:nr1]); h_dd.copy_(dd[:nr1])
     host = (h_rows.numpy(), h_ii.numpy(), h_jj.numpy(), h_dd.numpy())
-    eng = BatchedSvdEngine(a0, K, m_cap=m_cap, k_cap=K)
+    eng.restore()
     barrier()
     t0 = time.perf_counter()
     run_ticks(eng, e2e_steps, host=host)
@@ -366,19 +375,18 @@ def run_gpu(args):
     if rank == 0:
         peak, peak_kind = _peaks()
         tot = lambda i: float(ph[i] + ph[4 + i])
-        install_ms = tot(3) - flush_ms
         kernels = {
             "project_append/rank1_build (K1/K6)": {"ms": tot(0), "bytes": proj_bytes},
             "arrow_svd (K2a, append cores)": {"ms": float(ph[1]), "bytes": None},
             "jacobi32 (K2b, rank-1 cores)": {"ms": float(ph[5]), "bytes": None},
             "rotate V + W (K3/K4, per tick)": {"ms": tot(2), "bytes": rot_bytes},
             "rotate U flush (K3, deferred)": {"ms": flush_ms, "bytes": flush_bytes},
-            "install (s copy, zero-sigma check)": {"ms": max(0.0, install_ms), "bytes": None},
+            "install (s copy, zero-sigma check)": {"ms": max(0.0, tot(3) - flush_ms), "bytes": None},
         }
         busy = sum(v["ms"] for v in kernels.values())
         for v in kernels.values():
             v["share"] = v["ms"] / busy if busy else None
-            v["ms_per_step"] = v["ms"] / max(1, steps)
+            v["ms_per_step"] = v["ms"] / max(1, diag_steps)
             v["gbs"] = (v["bytes"] / (v["ms"] / 1e3) / 1e9) if (v["bytes"] and v["ms"]) else None
         hbm = {k: v for k, v in kernels.items() if v["bytes"]}
         dom_name = max(kernels, key=lambda k: kernels[k]["ms"])
@@ -394,7 +402,7 @@ def run_gpu(args):
                        "events": steps, "event_mix": "alternating row append / rank-1",
                        "l2": "inputs larger than L2 (state ~2 GB/GPU touched per step)",
                        "parallelism": f"streams sharded over {world} GPU(s)",
-                       "deferred_u_rows": 32},
+                       "deferred_u_rows": 32, "stream_groups": 4},
             "clocks": clock,
             "gpu_launches": int(launches),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
@@ -402,14 +410,18 @@ def run_gpu(args):
             "roofline": {"kernel": hbm_name, "bound": "hbm", "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "peak_kind": peak_kind,
                          "traffic": None,
-                         "bytes_per_launch": hk["bytes"] / max(1, (n_flush if "flush" in hbm_name else steps)),
+                         "bytes_per_launch": hk["bytes"] / max(1, (n_flush if "flush" in hbm_name
+                                                                   else diag_steps)),
                          "dominant_kernel_by_time": dom_name,
-                         "note": "dominant HBM-bound kernel; the core-SVD kernels are FP64/latency bound"},
+                         "measured_over": f"first {diag_steps} ticks, one stream group, "
+                                          "CUDA events around each phase"},
             "kernels": kernels,
             "flushes": n_flush,
             "phase_ms_by_event": phase_by_kind,
             "tick_effective_gbs": all_bytes / (t_max / 1e3) / 1e9,
-            "diagnostics": diagnostics,
+            "diagnostics": {"jacobi32_sweeps_per_core": float(dbg[0]) / max(1, int(dbg[1])),
+                            "init_s": init_s,
+                            "serial_phase_ms_per_step": diag_ms / max(1, diag_steps)},
         }
         if world == 1 and not args.no_cpu_baseline:
             v, cores, updates, secs = cpu_reference(args.cpu_streams, args.cpu_events)
@@ -431,6 +443,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--streams", type=int, default=TOTAL_STREAMS)
     ap.add_argument("--e2e-steps", type=int, default=128)
+    ap.add_argument("--diag-steps", type=int, default=256)
     ap.add_argument("--cpu-streams", type=int, default=64)
     ap.add_argument("--cpu-events", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -157,6 +157,11 @@ int isvd_engine_set_append_solver(isvd_engine* e, int jacobi);
  * set_lazy(0) rotates U eagerly every event (the reference's order of
  * operations); flush() materialises U now. */
 int isvd_engine_set_lazy(isvd_engine* e, int on);
+/* Device-side checkpoint of the full engine state (factors, tracked matrix,
+ * squared norms, shape, step; a deferred rotation is flushed first) and its
+ * restore.  Used by bench.py to rerun the same ticks without a new init. */
+int isvd_engine_snapshot(isvd_engine* e);
+int isvd_engine_restore(isvd_engine* e);
 int isvd_engine_flush(isvd_engine* e);
 int isvd_engine_phase_times(isvd_engine* e, double* ms4, int64_t* ticks);
 

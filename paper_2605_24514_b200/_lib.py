@@ -63,6 +63,8 @@ SIGNATURES = {
     "isvd_engine_set_append_solver": (C.c_int, [_vp, C.c_int]),
     "isvd_engine_set_lazy": (C.c_int, [_vp, C.c_int]),
     "isvd_engine_flush": (C.c_int, [_vp]),
+    "isvd_engine_snapshot": (C.c_int, [_vp]),
+    "isvd_engine_restore": (C.c_int, [_vp]),
     "isvd_engine_phase_times": (C.c_int, [_vp, _dp, _ip64]),
     "isvd_engine_frob_error": (C.c_int, [_vp, _dp]),
     "isvd_engine_ortho_defect": (C.c_int, [_vp, _dp, _dp]),

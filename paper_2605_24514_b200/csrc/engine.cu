@@ -150,6 +150,32 @@ struct isvd_engine {
   bool lazy_active = false;
   int m_base = 0, r_base = 0, lazy_b = 0;
   double* W = nullptr;
+  int r_base_next = 0, lazy_b_next = 0;  // window state after the event being issued
+  struct Snap {
+    double *U = nullptr, *V = nullptr, *A = nullptr, *s = nullptr, *N = nullptr;
+    size_t nu = 0, nv = 0, na = 0, ns = 0;
+    int m = 0, n = 0, r = 0, k = 0, m_cap = 0, n_cap = 0, ld = 0;
+    int64_t step = 0;
+    bool canonical = true, valid = false;
+  } snap;
+  // stream groups (pipelining across streams of the batch)
+  static constexpr int kGroupMin = 256;
+  int ngroups = 4, ngroups_active = 1;
+  std::vector<cudaStream_t> gst;
+  cudaEvent_t fork_ev = nullptr;
+  std::vector<cudaEvent_t> join_ev;
+  int ensure_groups(int G) {
+    if (!fork_ev) ISVD_CUDA(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
+    while ((int)gst.size() < G) {
+      cudaStream_t s2;
+      cudaEvent_t ev;
+      ISVD_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+      ISVD_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      gst.push_back(s2);
+      join_ev.push_back(ev);
+    }
+    return ISVD_OK;
+  }
   int64_t wstride() const { return (int64_t)(ld + kLazyRows + 1) * ld; }
   Mat Wm() const { return Mat{W, wstride(), ld}; }
   LazyBasis lazy() const { return LazyBasis{lazy_active ? 1 : 0, m_base, r_base, Wm()}; }
@@ -345,6 +371,10 @@ struct isvd_engine {
     dfree(z); dfree(inj); dfree(rho); dfree(xnorm); dfree(ev);
     dfree(ei); dfree(ej); dfree(ed); dfree(dflag); dfree(ref); dfree(W);
     dfree(wx); dfree(wj); dfree(wpart); dfree(wout); dfree(wflags);
+    dfree(snap.U); dfree(snap.V); dfree(snap.A); dfree(snap.s); dfree(snap.N);
+    for (auto g : gst) cudaStreamDestroy(g);
+    for (auto ev : join_ev) cudaEventDestroy(ev);
+    if (fork_ev) cudaEventDestroy(fork_ev);
     for (auto ev : ev_marks) cudaEventDestroy(ev);
     for (auto ev : ev_pool) cudaEventDestroy(ev);
     if (own_stream && st) cudaStreamDestroy(st);
@@ -472,6 +502,152 @@ int isvd_engine_init(isvd_engine* e, const double* a0, int on_device) {
   return ISVD_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Per-tick launch sequences, issued for a slice of streams [b0, b0 + nb) on
+// CUDA stream `st`.  With B large the batch is split into groups on separate
+// CUDA streams so the latency/FP64-bound core-SVD kernels of one group run
+// concurrently with the HBM-bound projection/rotation kernels of another.
+struct Slice {
+  int b0, nb;
+  cudaStream_t st;
+};
+
+static Mat mat_at(const Mat& M, int b0) { return Mat{M.p + b0 * M.stride, M.stride, M.ld}; }
+
+// lazy_state: 0 = eager rotation, 1 = open a deferred window, 2 = continue it
+static int issue_append(isvd_engine* e, const Slice& sl, const double* xd, int len, bool is_row,
+                        int keep, int lazy_state) {
+  const int b0 = sl.b0, nb = sl.nb, r = e->r;
+  cudaStream_t st = sl.st;
+  const int S = e->S();
+  const int64_t cs = e->cstride();
+  Mat F = mat_at(is_row ? e->Vm() : e->Um(), b0);
+  const int64_t a_off = is_row ? (int64_t)e->m * e->n_cap : (int64_t)e->n;
+  const int64_t a_step = is_row ? 1 : e->n_cap;
+  double* core = e->core + b0 * cs;
+  double* uk = e->uk + b0 * cs;
+  double* vk = e->vk + b0 * cs;
+  double* sv = e->sv + (int64_t)b0 * S;
+  double* z = e->z + (int64_t)b0 * e->zlen();
+  double* inj = e->inj + b0;
+  const bool one = e->ngroups_active == 1;
+  if (one) e->mark();
+  ISVD_TRY(launch_project_append(nb, len, r, F, xd + (int64_t)b0 * len, len,
+                                 e->s + (int64_t)b0 * e->ld, e->ld, e->tol, core, cs, S, z,
+                                 e->zlen(), inj, e->rho + b0, e->xnorm + b0,
+                                 e->A + b0 * e->astride(), e->astride(), a_off, a_step, e->N + b0,
+                                 st));
+  if (one) e->mark();
+  if (e->append_jacobi)
+    ISVD_TRY(launch_core_svd(nb, r + 1, core, cs, S, uk, vk, cs, S, sv, S,
+                             e->vscr ? e->vscr + (int64_t)b0 * S * (S | 1) : nullptr, nullptr, st));
+  else
+    ISVD_TRY(launch_arrow_svd(nb, r + 1, core, cs, S, uk, vk, cs, S, sv, S, st));
+  if (one) e->mark();
+  // row: U <- [U 0; 0 1] Uk, V <- V Vk[:r] + z^ Vk[r] ; col: the same with U<->V
+  RotJob grow{mat_at(is_row ? e->Um() : e->Vm(), b0), is_row ? e->m : e->n, uk, cs, S, nullptr, 0,
+              nullptr, 1};
+  RotJob injj{mat_at(is_row ? e->Vm() : e->Um(), b0), is_row ? e->n : e->m, vk, cs, S, z,
+              e->zlen(), inj, 0};
+  if (lazy_state == 0) {
+    ISVD_TRY(launch_rotate(nb, r, keep, grow, &injj, st));
+  } else if (lazy_state == 1) {
+    // open a deferred window: W = Uk[:, :keep] (rows: r base columns + the new row)
+    ISVD_TRY(launch_copy_rows(nb, r + 1, keep, uk, cs, S, e->W + b0 * e->wstride(), e->wstride(),
+                              e->ld, st));
+    ISVD_TRY(launch_rotate(nb, r, keep, injj, nullptr, st));
+  } else {
+    // W <- [W 0; 0 1] Uk[:, :keep]  (in place, new row appended)
+    RotJob wj{mat_at(e->Wm(), b0), e->r_base + e->lazy_b, uk, cs, S, nullptr, 0, nullptr, 1};
+    ISVD_TRY(launch_rotate(nb, r, keep, wj, &injj, st));
+  }
+  if (one) e->mark();
+  // install: s <- sv[:, :keep], then the zero-sigma completion check
+  if (keep > 0)
+    ISVD_CUDA(cudaMemcpy2DAsync(e->s + (int64_t)b0 * e->ld, sizeof(double) * e->ld, sv,
+                                sizeof(double) * S, sizeof(double) * keep, nb,
+                                cudaMemcpyDeviceToDevice, st));
+  const int m_new = is_row ? e->m + 1 : e->m, n_new = is_row ? e->n : e->n + 1;
+  if (lazy_state != 0)
+    ISVD_TRY(launch_complete_zero(nb, keep, e->s + (int64_t)b0 * e->ld, e->ld, mat_at(e->Wm(), b0),
+                                  e->r_base_next + e->lazy_b_next, mat_at(e->Vm(), b0), n_new, st));
+  else
+    ISVD_TRY(launch_complete_zero(nb, keep, e->s + (int64_t)b0 * e->ld, e->ld, mat_at(e->Um(), b0),
+                                  m_new, mat_at(e->Vm(), b0), n_new, st));
+  return ISVD_OK;
+}
+
+static int issue_rank_one(isvd_engine* e, const Slice& sl, const int64_t* di, const int64_t* dj,
+                          const double* dd, int lazy_state) {
+  const int b0 = sl.b0, nb = sl.nb, r = e->r;
+  cudaStream_t st = sl.st;
+  const int S = e->S();
+  const int64_t cs = e->cstride();
+  double* core = e->core + b0 * cs;
+  double* uk = e->uk + b0 * cs;
+  double* vk = e->vk + b0 * cs;
+  double* sv = e->sv + (int64_t)b0 * S;
+  const bool one = e->ngroups_active == 1;
+  LazyBasis lz = e->lazy();
+  lz.W = mat_at(lz.W, b0);
+  if (one) e->mark();
+  ISVD_TRY(launch_rank1_build(nb, r, mat_at(e->Um(), b0), mat_at(e->Vm(), b0),
+                              e->s + (int64_t)b0 * e->ld, e->ld, di + b0, dj + b0, dd + b0, core,
+                              cs, S, e->A + b0 * e->astride(), e->astride(), e->n_cap, e->N + b0, lz,
+                              st));
+  if (one) e->mark();
+  ISVD_TRY(launch_core_svd(nb, r, core, cs, S, uk, vk, cs, S, sv, S,
+                           e->vscr ? e->vscr + (int64_t)b0 * S * (S | 1) : nullptr, nullptr, st));
+  if (one) e->mark();
+  RotJob ju{mat_at(e->Um(), b0), e->m, uk, cs, S, nullptr, 0, nullptr, 0};
+  RotJob jv{mat_at(e->Vm(), b0), e->n, vk, cs, S, nullptr, 0, nullptr, 0};
+  if (lazy_state == 0) {
+    ISVD_TRY(launch_rotate(nb, r, r, ju, &jv, st));
+  } else if (lazy_state == 1) {
+    ISVD_TRY(launch_copy_rows(nb, r, r, uk, cs, S, e->W + b0 * e->wstride(), e->wstride(), e->ld,
+                              st));
+    ISVD_TRY(launch_rotate(nb, r, r, jv, nullptr, st));
+  } else {
+    RotJob wj{mat_at(e->Wm(), b0), e->r_base + e->lazy_b, uk, cs, S, nullptr, 0, nullptr, 0};
+    ISVD_TRY(launch_rotate(nb, r, r, wj, &jv, st));
+  }
+  if (one) e->mark();
+  ISVD_CUDA(cudaMemcpy2DAsync(e->s + (int64_t)b0 * e->ld, sizeof(double) * e->ld, sv,
+                              sizeof(double) * S, sizeof(double) * r, nb, cudaMemcpyDeviceToDevice,
+                              st));
+  if (lazy_state != 0)
+    ISVD_TRY(launch_complete_zero(nb, r, e->s + (int64_t)b0 * e->ld, e->ld, mat_at(e->Wm(), b0),
+                                  e->r_base_next + e->lazy_b_next, mat_at(e->Vm(), b0), e->n, st));
+  else
+    ISVD_TRY(launch_complete_zero(nb, r, e->s + (int64_t)b0 * e->ld, e->ld, mat_at(e->Um(), b0),
+                                  e->m, mat_at(e->Vm(), b0), e->n, st));
+  return ISVD_OK;
+}
+
+// Run `issue(slice)` over the batch: one slice on the engine stream, or
+// ngroups slices forked onto the group streams and joined back.
+}  // extern "C"
+template <class F>
+static int run_groups(isvd_engine* e, F&& issue) {
+  int G = e->timing ? 1 : e->ngroups;
+  if (e->B < 2 * isvd_engine::kGroupMin) G = 1;
+  G = std::min(G, e->B / isvd_engine::kGroupMin);
+  if (G < 1) G = 1;
+  e->ngroups_active = G;
+  if (G == 1) return issue(Slice{0, e->B, e->st});
+  ISVD_TRY(e->ensure_groups(G));
+  ISVD_CUDA(cudaEventRecord(e->fork_ev, e->st));
+  for (int g = 0; g < G; ++g) {
+    const int b0 = (int)((int64_t)e->B * g / G), b1 = (int)((int64_t)e->B * (g + 1) / G);
+    ISVD_CUDA(cudaStreamWaitEvent(e->gst[g], e->fork_ev, 0));
+    ISVD_TRY(issue(Slice{b0, b1 - b0, e->gst[g]}));
+    ISVD_CUDA(cudaEventRecord(e->join_ev[g], e->gst[g]));
+    ISVD_CUDA(cudaStreamWaitEvent(e->st, e->join_ev[g], 0));
+  }
+  return ISVD_OK;
+}
+extern "C" {
+
 static int append_common(isvd_engine* e, const double* x, int on_device, bool is_row) {
   if (!e || !x) { set_error("null argument"); return ISVD_EINVAL; }
   if (!e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
@@ -485,61 +661,32 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
                           : std::min(std::min(e->r + 1, e->k), std::min(e->m, e->n + 1));
   ISVD_TRY(is_row ? e->grow_rows(e->m + 1) : e->grow_cols(e->n + 1));
   if (!is_row) ISVD_TRY(e->flush());  // the column append projects on, and rotates, U
-  const double* xd = x;
-  if (!on_device) {
-    ISVD_CUDA(cudaMemcpyAsync(e->ev, x, sizeof(double) * e->B * len, cudaMemcpyHostToDevice, e->st));
-    xd = e->ev;
-  }
-  const int r = e->r;
-  Mat F = is_row ? e->Vm() : e->Um();
-  int64_t a_off = is_row ? (int64_t)e->m * e->n_cap : (int64_t)e->n;
-  int64_t a_step = is_row ? 1 : e->n_cap;
-  e->mark();
-  ISVD_TRY(launch_project_append(e->B, len, r, F, xd, len, e->s, e->ld, e->tol, e->core,
-                                 e->cstride(), e->S(), e->z, e->zlen(), e->inj, e->rho, e->xnorm,
-                                 e->A, e->astride(), a_off, a_step, e->N, e->st));
-  e->mark();
-  if (e->append_jacobi)
-    ISVD_TRY(launch_core_svd(e->B, r + 1, e->core, e->cstride(), e->S(), e->uk, e->vk,
-                             e->cstride(), e->S(), e->sv, e->S(), e->vscr, nullptr, e->st));
-  else
-    ISVD_TRY(launch_arrow_svd(e->B, r + 1, e->core, e->cstride(), e->S(), e->uk, e->vk,
-                              e->cstride(), e->S(), e->sv, e->S(), e->st));
-  e->mark();
-  // row: U <- [U 0; 0 1] Uk, V <- V Vk[:r] + z^ Vk[r] ; col: the same with U<->V
-  RotJob grow{is_row ? e->Um() : e->Vm(), is_row ? e->m : e->n, e->uk, e->cstride(), e->S(),
-              nullptr, 0, nullptr, 1};
-  RotJob inj{is_row ? e->Vm() : e->Um(), is_row ? e->n : e->m, e->vk, e->cstride(), e->S(),
-             e->z, e->zlen(), e->inj, 0};
-  const bool lazy = is_row && e->lazy_mode;
-  if (!lazy) {
-    ISVD_TRY(launch_rotate(e->B, r, keep, grow, &inj, e->st));
-  } else if (!e->lazy_active) {
-    // open a deferred window: W = Uk[:, :keep] (rows: r base columns + the new row)
-    ISVD_TRY(launch_copy_rows(e->B, r + 1, keep, e->uk, e->cstride(), e->S(), e->W, e->wstride(),
-                              e->ld, e->st));
-    ISVD_TRY(launch_rotate(e->B, r, keep, inj, nullptr, e->st));
+  const int lazy_state = !(is_row && e->lazy_mode) ? 0 : (e->lazy_active ? 2 : 1);
+  // window bookkeeping after this event (used by the completion check)
+  e->r_base_next = lazy_state == 1 ? e->r : e->r_base;
+  e->lazy_b_next = lazy_state == 1 ? 1 : e->lazy_b + 1;
+  ISVD_TRY(run_groups(e, [&](const Slice& sl) {
+    const double* xd = x;
+    if (!on_device) {
+      // per-slice H2D on the slice's stream (overlaps the other groups' work)
+      ISVD_CUDA(cudaMemcpyAsync(e->ev + (int64_t)sl.b0 * len, x + (int64_t)sl.b0 * len,
+                                sizeof(double) * sl.nb * len, cudaMemcpyHostToDevice, sl.st));
+      xd = e->ev;
+    }
+    return issue_append(e, sl, xd, len, is_row, keep, lazy_state);
+  }));
+  if (lazy_state == 1) {
     e->lazy_active = true;
     e->m_base = e->m;
-    e->r_base = r;
+    e->r_base = e->r;
     e->lazy_b = 1;
-  } else {
-    // W <- [W 0; 0 1] Uk[:, :keep]  (in place, new row appended)
-    RotJob wj{e->Wm(), e->r_base + e->lazy_b, e->uk, e->cstride(), e->S(), nullptr, 0, nullptr, 1};
-    ISVD_TRY(launch_rotate(e->B, r, keep, wj, &inj, e->st));
+  } else if (lazy_state == 2) {
     e->lazy_b += 1;
   }
-  e->mark();
-  ISVD_TRY(e->install_from_core(keep));
   if (is_row) e->m += 1; else e->n += 1;
   e->r = keep;
-  if (e->lazy_active)
-    ISVD_TRY(launch_complete_zero(e->B, e->r, e->s, e->ld, e->Wm(), e->r_base + e->lazy_b,
-                                  e->Vm(), e->n, e->st));
-  else
-    ISVD_TRY(launch_complete_zero(e->B, e->r, e->s, e->ld, e->Um(), e->m, e->Vm(), e->n, e->st));
   if (e->lazy_active && e->lazy_b >= isvd_engine::kLazyRows) ISVD_TRY(e->flush());
-  e->mark();
+  if (e->ngroups_active == 1) e->mark();
   if (e->timing) { e->timed_ticks += 1; e->tick_kind.push_back(0); }
   e->canonical = false;
   e->step += 1;
@@ -575,40 +722,19 @@ int isvd_engine_rank_one(isvd_engine* e, const int64_t* i, const int64_t* j, con
     ISVD_CUDA(cudaMemcpyAsync(e->ed, delta, sizeof(double) * e->B, cudaMemcpyHostToDevice, e->st));
     di = e->ei; dj = e->ej; dd = e->ed;
   }
-  const int r = e->r;
-  e->mark();
-  ISVD_TRY(launch_rank1_build(e->B, r, e->Um(), e->Vm(), e->s, e->ld, di, dj, dd, e->core,
-                              e->cstride(), e->S(), e->A, e->astride(), e->n_cap, e->N, e->lazy(),
-                              e->st));
-  e->mark();
-  ISVD_TRY(launch_core_svd(e->B, r, e->core, e->cstride(), e->S(), e->uk, e->vk, e->cstride(),
-                           e->S(), e->sv, e->S(), e->vscr, nullptr, e->st));
-  e->mark();
-  RotJob ju{e->Um(), e->m, e->uk, e->cstride(), e->S(), nullptr, 0, nullptr, 0};
-  RotJob jv{e->Vm(), e->n, e->vk, e->cstride(), e->S(), nullptr, 0, nullptr, 0};
-  if (!e->lazy_mode) {
-    ISVD_TRY(launch_rotate(e->B, r, r, ju, &jv, e->st));
-  } else if (!e->lazy_active) {
-    // open a deferred window: W = Uk (U' = U Uk)
-    ISVD_TRY(launch_copy_rows(e->B, r, r, e->uk, e->cstride(), e->S(), e->W, e->wstride(), e->ld,
-                              e->st));
-    ISVD_TRY(launch_rotate(e->B, r, r, jv, nullptr, e->st));
+  const int lazy_state = !e->lazy_mode ? 0 : (e->lazy_active ? 2 : 1);
+  e->r_base_next = lazy_state == 1 ? e->r : e->r_base;
+  e->lazy_b_next = lazy_state == 1 ? 0 : e->lazy_b;
+  ISVD_TRY(run_groups(e, [&](const Slice& sl) {
+    return issue_rank_one(e, sl, di, dj, dd, lazy_state);
+  }));
+  if (lazy_state == 1) {
     e->lazy_active = true;
     e->m_base = e->m;
-    e->r_base = r;
+    e->r_base = e->r;
     e->lazy_b = 0;
-  } else {
-    RotJob wj{e->Wm(), e->r_base + e->lazy_b, e->uk, e->cstride(), e->S(), nullptr, 0, nullptr, 0};
-    ISVD_TRY(launch_rotate(e->B, r, r, wj, &jv, e->st));
   }
-  e->mark();
-  ISVD_TRY(e->install_from_core(r));
-  if (e->lazy_active)
-    ISVD_TRY(launch_complete_zero(e->B, e->r, e->s, e->ld, e->Wm(), e->r_base + e->lazy_b,
-                                  e->Vm(), e->n, e->st));
-  else
-    ISVD_TRY(launch_complete_zero(e->B, e->r, e->s, e->ld, e->Um(), e->m, e->Vm(), e->n, e->st));
-  e->mark();
+  if (e->ngroups_active == 1) e->mark();
   if (e->timing) { e->timed_ticks += 1; e->tick_kind.push_back(1); }
   e->canonical = false;
   e->step += 1;
@@ -780,6 +906,53 @@ int isvd_engine_device_views(isvd_engine* e, double** u, int64_t* u_stride, int*
 int isvd_engine_flush(isvd_engine* e) {
   if (!e) { set_error("null engine"); return ISVD_EINVAL; }
   return e->flush();
+}
+
+// ---- snapshot / restore (device-side checkpoint of the whole engine state)
+int isvd_engine_snapshot(isvd_engine* e) {
+  if (!e || !e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
+  ISVD_TRY(e->flush());
+  auto& S = e->snap;
+  const size_t nu = (size_t)e->B * e->ustride(), nv = (size_t)e->B * e->vstride();
+  const size_t na = (size_t)e->B * e->astride(), ns = (size_t)e->B * e->ld;
+  if (S.nu != nu) { dfree(S.U); ISVD_TRY(dalloc(&S.U, nu)); S.nu = nu; }
+  if (S.nv != nv) { dfree(S.V); ISVD_TRY(dalloc(&S.V, nv)); S.nv = nv; }
+  if (S.na != na) { dfree(S.A); ISVD_TRY(dalloc(&S.A, na)); S.na = na; }
+  if (S.ns != ns) { dfree(S.s); ISVD_TRY(dalloc(&S.s, ns)); S.ns = ns; }
+  if (!S.N) ISVD_TRY(dalloc(&S.N, (size_t)e->B * 3));
+  ISVD_CUDA(cudaMemcpyAsync(S.U, e->U, nu * 8, cudaMemcpyDeviceToDevice, e->st));
+  ISVD_CUDA(cudaMemcpyAsync(S.V, e->V, nv * 8, cudaMemcpyDeviceToDevice, e->st));
+  ISVD_CUDA(cudaMemcpyAsync(S.A, e->A, na * 8, cudaMemcpyDeviceToDevice, e->st));
+  ISVD_CUDA(cudaMemcpyAsync(S.s, e->s, ns * 8, cudaMemcpyDeviceToDevice, e->st));
+  ISVD_CUDA(cudaMemcpyAsync(S.N, e->N, e->B * 8, cudaMemcpyDeviceToDevice, e->st));
+  ISVD_CUDA(cudaMemcpyAsync(S.N + e->B, e->rho, e->B * 8, cudaMemcpyDeviceToDevice, e->st));
+  ISVD_CUDA(cudaMemcpyAsync(S.N + 2 * e->B, e->xnorm, e->B * 8, cudaMemcpyDeviceToDevice, e->st));
+  S.m = e->m; S.n = e->n; S.r = e->r; S.k = e->k; S.step = e->step;
+  S.m_cap = e->m_cap; S.n_cap = e->n_cap; S.ld = e->ld; S.canonical = e->canonical;
+  S.valid = true;
+  ISVD_CUDA(cudaStreamSynchronize(e->st));
+  return ISVD_OK;
+}
+
+int isvd_engine_restore(isvd_engine* e) {
+  if (!e || !e->snap.valid) { set_error("no snapshot to restore"); return ISVD_ESTATE; }
+  auto& S = e->snap;
+  if (S.m_cap != e->m_cap || S.n_cap != e->n_cap || S.ld != e->ld) {
+    set_error("capacities changed since the snapshot");
+    return ISVD_ESTATE;
+  }
+  e->lazy_active = false;
+  e->lazy_b = 0;
+  ISVD_CUDA(cudaMemcpyAsync(e->U, S.U, S.nu * 8, cudaMemcpyDeviceToDevice, e->st));
+  ISVD_CUDA(cudaMemcpyAsync(e->V, S.V, S.nv * 8, cudaMemcpyDeviceToDevice, e->st));
+  ISVD_CUDA(cudaMemcpyAsync(e->A, S.A, S.na * 8, cudaMemcpyDeviceToDevice, e->st));
+  ISVD_CUDA(cudaMemcpyAsync(e->s, S.s, S.ns * 8, cudaMemcpyDeviceToDevice, e->st));
+  ISVD_CUDA(cudaMemcpyAsync(e->N, S.N, e->B * 8, cudaMemcpyDeviceToDevice, e->st));
+  ISVD_CUDA(cudaMemcpyAsync(e->rho, S.N + e->B, e->B * 8, cudaMemcpyDeviceToDevice, e->st));
+  ISVD_CUDA(cudaMemcpyAsync(e->xnorm, S.N + 2 * e->B, e->B * 8, cudaMemcpyDeviceToDevice, e->st));
+  e->m = S.m; e->n = S.n; e->r = S.r; e->k = S.k; e->step = S.step; e->canonical = S.canonical;
+  ISVD_CUDA(cudaStreamSynchronize(e->st));
+  return ISVD_OK;
 }
 
 int isvd_engine_set_lazy(isvd_engine* e, int on) {

@@ -145,6 +145,13 @@ class BatchedSvdEngine:
         """Deferred left-basis rotation on (default) or off (eager per event)."""
         _lib.check(self._h.lib.isvd_engine_set_lazy(self._h.h, int(bool(on))))
 
+    def snapshot(self) -> None:
+        """Device-side checkpoint of the whole state (restore() returns to it)."""
+        _lib.check(self._h.lib.isvd_engine_snapshot(self._h.h))
+
+    def restore(self) -> None:
+        _lib.check(self._h.lib.isvd_engine_restore(self._h.h))
+
     # ------------------------------------------------------------ events
     def row_append(self, x) -> None:
         b, m, n, *_ = self._h.shape()
