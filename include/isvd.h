@@ -157,6 +157,9 @@ int isvd_engine_set_append_solver(isvd_engine* e, int jacobi);
  * set_lazy(0) rotates U eagerly every event (the reference's order of
  * operations); flush() materialises U now. */
 int isvd_engine_set_lazy(isvd_engine* e, int on);
+/* Defect threshold of the optional re-orthonormalisation guard
+ * (REORTHO_THRESHOLD, engine.py:30; default 1e-6). */
+int isvd_engine_set_reortho_threshold(isvd_engine* e, double threshold);
 /* Device-side checkpoint of the full engine state (factors, tracked matrix,
  * squared norms, shape, step; a deferred rotation is flushed first) and its
  * restore.  Used by bench.py to rerun the same ticks without a new init. */

@@ -62,6 +62,7 @@ SIGNATURES = {
     "isvd_engine_set_timing": (C.c_int, [_vp, C.c_int]),
     "isvd_engine_set_append_solver": (C.c_int, [_vp, C.c_int]),
     "isvd_engine_set_lazy": (C.c_int, [_vp, C.c_int]),
+    "isvd_engine_set_reortho_threshold": (C.c_int, [_vp, C.c_double]),
     "isvd_engine_flush": (C.c_int, [_vp]),
     "isvd_engine_snapshot": (C.c_int, [_vp]),
     "isvd_engine_restore": (C.c_int, [_vp]),

@@ -25,6 +25,7 @@
 #include "common.cuh"
 #include "core_svd.cuh"
 #include "dense_svd.cuh"
+#include "guard.cuh"
 #include "metrics.cuh"
 #include "tick.cuh"
 #include "../../include/isvd.h"
@@ -112,6 +113,21 @@ struct isvd_engine {
   int64_t step = 0;
   double tol = 1e-10;
   bool guard = false;
+  double reortho_threshold = 1e-6;  // engine.py:30
+  // engine.py:205-206,210-217: after an event, refactor if the factors drifted
+  int guard_step() {
+    if (!guard || r < 1) return ISVD_OK;
+    ISVD_TRY(flush());
+    std::vector<double> du(B), dv(B);
+    ISVD_TRY(reortho_defects(B, r, Um(), m, Vm(), n, du.data(), dv.data(), st));
+    bool any = false;
+    for (int b = 0; b < B; ++b) any |= std::max(du[b], dv[b]) > reortho_threshold;
+    if (!any) return ISVD_OK;
+    ISVD_TRY(reortho_apply(B, r, Um(), m, Vm(), n, s, ld, core, uk, vk, cstride(), S(), sv, vscr,
+                           st));
+    canonical = false;
+    return ISVD_OK;
+  }
   int m_cap = 0, n_cap = 0, ld = 0;
   cudaStream_t st = nullptr;
   bool own_stream = false;
@@ -686,6 +702,7 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
   if (is_row) e->m += 1; else e->n += 1;
   e->r = keep;
   if (e->lazy_active && e->lazy_b >= isvd_engine::kLazyRows) ISVD_TRY(e->flush());
+  ISVD_TRY(e->guard_step());
   if (e->ngroups_active == 1) e->mark();
   if (e->timing) { e->timed_ticks += 1; e->tick_kind.push_back(0); }
   e->canonical = false;
@@ -734,6 +751,7 @@ int isvd_engine_rank_one(isvd_engine* e, const int64_t* i, const int64_t* j, con
     e->r_base = e->r;
     e->lazy_b = 0;
   }
+  ISVD_TRY(e->guard_step());
   if (e->ngroups_active == 1) e->mark();
   if (e->timing) { e->timed_ticks += 1; e->tick_kind.push_back(1); }
   e->canonical = false;
@@ -952,6 +970,12 @@ int isvd_engine_restore(isvd_engine* e) {
   ISVD_CUDA(cudaMemcpyAsync(e->xnorm, S.N + 2 * e->B, e->B * 8, cudaMemcpyDeviceToDevice, e->st));
   e->m = S.m; e->n = S.n; e->r = S.r; e->k = S.k; e->step = S.step; e->canonical = S.canonical;
   ISVD_CUDA(cudaStreamSynchronize(e->st));
+  return ISVD_OK;
+}
+
+int isvd_engine_set_reortho_threshold(isvd_engine* e, double threshold) {
+  if (!e) { set_error("null engine"); return ISVD_EINVAL; }
+  e->reortho_threshold = threshold;
   return ISVD_OK;
 }
 

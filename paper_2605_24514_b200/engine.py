@@ -444,6 +444,16 @@ class SvdEngine:
         """Deferred left-basis rotation on (default) or off (eager per event)."""
         _lib.check(self._h.lib.isvd_engine_set_lazy(self._h.h, int(bool(on))))
 
+    @property
+    def reortho_threshold(self) -> float:
+        """Defect above which the guard re-factors (engine.py:30)."""
+        return getattr(self, "_reortho_threshold", REORTHO_THRESHOLD)
+
+    @reortho_threshold.setter
+    def reortho_threshold(self, value: float) -> None:
+        _lib.check(self._h.lib.isvd_engine_set_reortho_threshold(self._h.h, float(value)))
+        self._reortho_threshold = float(value)
+
     def ortho_defects(self) -> tuple[float, float]:
         du, dv = np.empty(1), np.empty(1)
         _lib.check(self._h.lib.isvd_engine_ortho_defect(self._h.h, _lib.dptr(du), _lib.dptr(dv)))
