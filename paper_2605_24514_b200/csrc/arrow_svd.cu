@@ -385,6 +385,9 @@ __global__ void __launch_bounds__((kN + 31) / 32 * 32) arrow_svd_kernel(int n, c
   __syncthreads();
 
   // ---- dead-column completion over e_0, e_1, ... (_kernels.pyx:62-79)
+  bool mine_dead = false;
+  for (int t = tid; t < n; t += blockDim.x) mine_dead |= !(SV[t] > 0.0);
+  if (!__syncthreads_or(mine_dead)) return;
   if (tid < 32) {
     const int lane = tid;
     for (int t = 0; t < n; ++t) {

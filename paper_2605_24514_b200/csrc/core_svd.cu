@@ -209,6 +209,15 @@ __device__ __forceinline__ void halve(double& keep, double lo, double hi, bool u
   keep = mine + __shfl_xor_sync(0xffffffffu, other, off);
 }
 
+// 1/sqrt(x) to ~1 ulp: MUFU.RSQ64H seed + two Newton steps (x > 0, normal)
+__device__ __forceinline__ double j32_rsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  return y * fma(-hx * y, y, 1.5);
+}
+
 __device__ __forceinline__ double j32_rcp(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
@@ -224,9 +233,8 @@ __device__ __forceinline__ double j32_rcp(double x) {
 // place (a_pp' = a_pp - t a_pq, a_qq' = a_qq + t a_pq) and recomputed
 // exactly at every sweep start.
 template <bool ODD>
-__device__ __forceinline__ bool j32_round(double (&g)[32], double (&v)[32], int lane,
-                                          double2* cs_sm, double& nlo, double& nhi,
-                                          float& relmax, double null2) {
+__device__ __forceinline__ bool j32_round(double (&g)[32], int lane, double2* cs_sm, double& nlo,
+                                          double& nhi, float& relmax, double null2) {
   double W[8];
   const bool b4 = lane & 16;
 #pragma unroll
@@ -241,17 +249,19 @@ __device__ __forceinline__ bool j32_round(double (&g)[32], double (&v)[32], int 
   const double apq = W[0] + __shfl_xor_sync(0xffffffffu, W[0], 1);
   const double app = nlo, aqq = nhi;
   double c = 1.0, s = 0.0, t = 0.0;
-  const double scale = sqrt(fmax(app * aqq, 0.0));
-  // Columns whose norm is below 1e-15 of the largest are numerically zero
-  // (they snap to sigma = 0 and their U column is completed); rotating them
-  // only chases rounding noise towards underflow, so such pairs are left.
-  const bool rot = fabs(apq) > kOrthoEps * scale && fmin(app, aqq) > null2;
+  // Rotate iff |a_pq| > 1e-14 sqrt(a_pp a_qq) (_kernels.pyx:38), compared in
+  // squares so no IEEE sqrt/div (and their slow-path calls) sits on the
+  // round's critical path.  Columns below 1e-15 of the largest norm are
+  // numerically zero (they snap to sigma = 0) and are left alone.
+  const double apq2 = apq * apq, pq = app * aqq;
+  const bool rot = apq2 > (kOrthoEps * kOrthoEps) * pq && fmin(app, aqq) > null2;
   if (rot) {
-    relmax = fmaxf(relmax, (float)(fabs(apq) / scale));
+    relmax = fmaxf(relmax, __fdividef((float)apq2, (float)pq));
     const double zeta = (aqq - app) * j32_rcp(2.0 * apq);
-    const double root = fabs(zeta) > 1e100 ? fabs(zeta) : sqrt(fma(zeta, zeta, 1.0));
+    const double w = fma(zeta, zeta, 1.0);
+    const double root = fabs(zeta) > 1e100 ? fabs(zeta) : w * j32_rsqrt(w);
     t = copysign(j32_rcp(fabs(zeta) + root), zeta);
-    c = rsqrt(fma(t, t, 1.0));
+    c = j32_rsqrt(fma(t, t, 1.0));
     s = t * c;
   }
   const bool dummy = ODD && (lane >> 1) == 15;
@@ -275,33 +285,60 @@ __device__ __forceinline__ bool j32_round(double (&g)[32], double (&v)[32], int 
     const double gp = g[p], gq = g[p + 1];
     g[p] = r.y * gp + r.x * gq;  // columns swap places after meeting
     g[p + 1] = r.x * gp - r.y * gq;
-    const double vp = v[p], vq = v[p + 1];
-    v[p] = r.y * vp + r.x * vq;
-    v[p + 1] = r.x * vp - r.y * vq;
   }
-  __syncwarp();
   return __any_sync(0xffffffffu, rot);
 }
 
-__global__ void __launch_bounds__(kJ32Warps * 32) jacobi32_kernel(
+// Replays the logged rotations of one sweep (32 rounds) on a row of V.
+__device__ __forceinline__ void j32_apply_v(double (&v)[32], const double2* log) {
+  for (int rr = 0; rr < 16; ++rr) {
+    const double2* ev = log + (2 * rr) * 16;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const double2 r = ev[k];
+      const double vp = v[2 * k], vq = v[2 * k + 1];
+      v[2 * k] = r.y * vp + r.x * vq;
+      v[2 * k + 1] = r.x * vp - r.y * vq;
+    }
+    const double2* od = log + (2 * rr + 1) * 16;
+#pragma unroll
+    for (int k = 0; k < 15; ++k) {
+      const double2 r = od[k];
+      const double vp = v[2 * k + 1], vq = v[2 * k + 2];
+      v[2 * k + 1] = r.y * vp + r.x * vq;
+      v[2 * k + 2] = r.x * vp - r.y * vq;
+    }
+  }
+}
+
+// Per-warp shared state: the (c, s) log of one sweep (32 rounds x 16 pairs)
+// and V (32 x 33).  V is kept out of registers while the G rounds run (so
+// the G phase needs ~half the registers and more cores fit per SM) and is
+// rotated once per sweep by replaying the log.
+struct J32Smem {
+  double2 log[32 * 16];
+  double V[32][33];
+  double nrm[32];
+  int pos[32];
+};
+
+__global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32_kernel(
     int s, const double* __restrict__ core, int64_t core_stride, int ldcore, double* __restrict__ uk,
     double* __restrict__ vk, int64_t out_stride, int ldo, double* __restrict__ sv,
     int64_t sv_stride, int batch) {
-  __shared__ double2 cs_all[kJ32Warps][16];
-  __shared__ double nrm_all[kJ32Warps][32];
-  __shared__ int pos_all[kJ32Warps][32];
+  extern __shared__ __align__(16) unsigned char j32_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b = blockIdx.x * kJ32Warps + warp;
   if (b >= batch) return;
-  double2* cs_sm = cs_all[warp];
-  double* nrm = nrm_all[warp];
-  int* pos = pos_all[warp];
+  J32Smem& W = reinterpret_cast<J32Smem*>(j32_raw)[warp];
+  double* nrm = W.nrm;
+  int* pos = W.pos;
   const double* K = core + b * core_stride;
-  double g[32], v[32];
+  double g[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
     g[j] = (lane < s && j < s) ? K[lane * ldcore + j] : 0.0;
-    v[j] = (lane == j && lane < s) ? 1.0 : 0.0;
+    W.V[lane][j] = (lane == j && lane < s) ? 1.0 : 0.0;
   }
   // Sweeps until none rotates (_kernels.pyx:58-59).  Quadratic convergence:
   // once every rotation of a sweep had |a_pq| <= 1e-8 sqrt(a_pp a_qq), the
@@ -328,7 +365,7 @@ __global__ void __launch_bounds__(kJ32Warps * 32) jacobi32_kernel(
     double nhi = __shfl_sync(0xffffffffu, R[0], lane | 1);
     const double null2 = fmax(1e-30 * warp_max(R[0]), 1e-290);
     for (int rr = 0; rr < 16; ++rr) {
-      any |= j32_round<false>(g, v, lane, cs_sm, nlo, nhi, relmax, null2);
+      any |= j32_round<false>(g, lane, W.log + (2 * rr) * 16, nlo, nhi, relmax, null2);
       // even -> odd pairing: (2k+1, 2k+2); position 0 sits out
       const double n0 = nlo;
       {
@@ -336,7 +373,7 @@ __global__ void __launch_bounds__(kJ32Warps * 32) jacobi32_kernel(
         nlo = nhi;
         nhi = down;
       }
-      any |= j32_round<true>(g, v, lane, cs_sm, nlo, nhi, relmax, null2);
+      any |= j32_round<true>(g, lane, W.log + (2 * rr + 1) * 16, nlo, nhi, relmax, null2);
       // odd -> even pairing: (2k, 2k+1)
       {
         const double up = __shfl_up_sync(0xffffffffu, nhi, 2);
@@ -344,9 +381,19 @@ __global__ void __launch_bounds__(kJ32Warps * 32) jacobi32_kernel(
         nlo = (lane < 2) ? n0 : up;
       }
     }
+    // V phase: replay the sweep's rotations (and swaps) on this lane's row
+    {
+      double v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = W.V[lane][j];
+      j32_apply_v(v, W.log);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) W.V[lane][j] = v[j];
+    }
+    __syncwarp();
     ++sweeps;
     if (!any) break;
-    if (warp_max((double)relmax) <= kConvRel) break;
+    if (warp_max((double)relmax) <= kConvRel * kConvRel) break;
   }
   if (lane == 0) atomicAdd(&g_debug_counters[0], (unsigned long long)sweeps);
   if (lane == 0) atomicAdd(&g_debug_counters[1], 1ull);
@@ -386,10 +433,12 @@ __global__ void __launch_bounds__(kJ32Warps * 32) jacobi32_kernel(
   double* U = uk + b * out_stride;
   double* Vo = vk + b * out_stride;
   double* S = sv + b * sv_stride;
+  bool any_dead;
   {
     const double r = nrm[lane];
     const bool live = r > 0.0 && !(r < kZeroSvRtol * s0);
     if (id_of(lane) < s) S[pos[lane]] = live ? r : 0.0;
+    any_dead = __any_sync(0xffffffffu, id_of(lane) < s && !live);
   }
   if (lane < s) {
 #pragma unroll
@@ -398,11 +447,12 @@ __global__ void __launch_bounds__(kJ32Warps * 32) jacobi32_kernel(
       const double r = nrm[p];
       const bool live = r > 0.0 && !(r < kZeroSvRtol * s0);
       U[lane * ldo + pos[p]] = live ? g[p] / r : 0.0;
-      Vo[lane * ldo + pos[p]] = v[p];
+      Vo[lane * ldo + pos[p]] = W.V[lane][p];
     }
   }
   __syncwarp();
   // dead-column completion (_kernels.pyx:62-79), rare
+  if (!any_dead) return;
   for (int t = 0; t < s; ++t) {
     if (S[t] > 0.0) continue;
     for (int axis = 0; axis < s; ++axis) {
@@ -450,7 +500,14 @@ int launch_core_svd(int batch, int s, const double* core, int64_t core_stride, i
   }
   if (batch == 0) return ISVD_OK;
   if (s <= 32 && !active) {
-    jacobi32_kernel<<<ceil_div(batch, kJ32Warps), kJ32Warps * 32, 0, st>>>(
+    static bool j32_attr = false;
+    const size_t smem = sizeof(J32Smem) * kJ32Warps;
+    if (!j32_attr) {
+      ISVD_CUDA(cudaFuncSetAttribute(jacobi32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+      j32_attr = true;
+    }
+    jacobi32_kernel<<<ceil_div(batch, kJ32Warps), kJ32Warps * 32, smem, st>>>(
         s, core, core_stride, ldcore, uk, vk, out_stride, ldo, sv, sv_stride, batch);
     ISVD_LAUNCHED();
     return ISVD_OK;

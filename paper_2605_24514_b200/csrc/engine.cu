@@ -1231,31 +1231,15 @@ int isvd_core_svd(int batch, int s, const double* core, double* u, double* sv, d
   ISVD_TRY(check_device());
   cudaStream_t st = (cudaStream_t)stream;
   double* vscr = nullptr;
-  double* vk = nullptr;
   if (s > kSmemMaxS) ISVD_TRY(dalloc(&vscr, (size_t)batch * s * (s | 1)));
-  ISVD_TRY(dalloc(&vk, (size_t)batch * s * s));
-  int rc = launch_core_svd(batch, s, core, (int64_t)s * s, s, u, vk, (int64_t)s * s, s, sv, s, vscr,
+  // V is produced in vt's storage, then transposed in place on the device
+  int rc = launch_core_svd(batch, s, core, (int64_t)s * s, s, u, vt, (int64_t)s * s, s, sv, s, vscr,
                            nullptr, st);
-  // vt = V^T
-  if (rc == ISVD_OK) {
-    std::vector<double> h((size_t)batch * s * s);
-    if (cudaMemcpyAsync(h.data(), vk, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-        cudaStreamSynchronize(st) != cudaSuccess) {
-      set_error("core_svd: device failure");
-      rc = ISVD_ENODEV;
-    } else {
-      std::vector<double> t(h.size());
-      for (int b = 0; b < batch; ++b)
-        for (int i = 0; i < s; ++i)
-          for (int j = 0; j < s; ++j) t[(size_t)b * s * s + j * s + i] = h[(size_t)b * s * s + i * s + j];
-      if (cudaMemcpy(vt, t.data(), sizeof(double) * t.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
-        set_error("core_svd: device failure");
-        rc = ISVD_ENODEV;
-      }
-    }
+  if (rc == ISVD_OK) rc = launch_transpose_square(batch, s, vt, st);
+  if (vscr) {
+    cudaStreamSynchronize(st);
+    dfree(vscr);
   }
-  dfree(vscr);
-  dfree(vk);
   return rc;
 }
 

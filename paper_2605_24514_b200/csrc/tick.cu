@@ -531,6 +531,18 @@ __global__ void copy_rows_kernel(int rows, int cols, const double* __restrict__ 
   }
 }
 
+__global__ void transpose_square_kernel(int s, double* __restrict__ a) {
+  double* m = a + (int64_t)blockIdx.x * s * s;
+  for (int idx = threadIdx.x; idx < s * s; idx += blockDim.x) {
+    const int i = idx / s, j = idx % s;
+    if (i < j) {
+      const double t = m[i * s + j];
+      m[i * s + j] = m[j * s + i];
+      m[j * s + i] = t;
+    }
+  }
+}
+
 __global__ void zero_kernel(double* p, size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x)
@@ -707,6 +719,13 @@ int launch_copy_rows(int batch, int rows, int cols, const double* src, int64_t s
   int gx = (int)std::min<int64_t>((total + 255) / 256, 4096);
   copy_rows_kernel<<<dim3(gx, batch), 256, 0, st>>>(rows, cols, src, src_stride, ld_src, dst,
                                                     dst_stride, ld_dst);
+  ISVD_LAUNCHED();
+  return ISVD_OK;
+}
+
+int launch_transpose_square(int batch, int s, double* a, cudaStream_t st) {
+  if (batch == 0) return ISVD_OK;
+  transpose_square_kernel<<<batch, 256, 0, st>>>(s, a);
   ISVD_LAUNCHED();
   return ISVD_OK;
 }

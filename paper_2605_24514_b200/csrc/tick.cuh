@@ -68,6 +68,7 @@ int launch_canonicalize(int batch, int w, Mat U, int m, Mat V, int n, cudaStream
 int launch_copy_rows(int batch, int rows, int cols, const double* src, int64_t src_stride,
                      int ld_src, double* dst, int64_t dst_stride, int ld_dst, cudaStream_t st);
 int launch_zero(double* p, size_t n, cudaStream_t st);
+int launch_transpose_square(int batch, int s, double* a, cudaStream_t st);
 int launch_sumsq(int batch, int rows, int cols, const double* a, int64_t a_stride, int lda,
                  double* out, cudaStream_t st);
 int launch_check_finite(size_t n, const double* p, int* flag, cudaStream_t st);
