@@ -153,10 +153,16 @@ int isvd_engine_set_timing(isvd_engine* e, int on);
 int isvd_engine_set_append_solver(isvd_engine* e, int jacobi);
 /* Deferred left-basis rotation, on by default: row
  * appends and rank-1 updates rotate a small W (U = [U_base 0; 0 I] W) and U
- * is materialised every 32 appended rows and before any read of U.
+ * is materialised every lazy-window rows (isvd_engine_set_lazy_window) and
+ * before any read of U.
  * set_lazy(0) rotates U eagerly every event (the reference's order of
  * operations); flush() materialises U now. */
 int isvd_engine_set_lazy(isvd_engine* e, int on);
+/* Rows appended per deferred window before U is materialised (default
+ * ~sqrt(2 m) clamped to [32, 4096]); flushes first.  isvd_engine_lazy_window
+ * returns the current value (-1 for a null handle). */
+int isvd_engine_set_lazy_window(isvd_engine* e, int rows);
+int isvd_engine_lazy_window(isvd_engine* e);
 /* Defect threshold of the optional re-orthonormalisation guard
  * (REORTHO_THRESHOLD, engine.py:30; default 1e-6). */
 int isvd_engine_set_reortho_threshold(isvd_engine* e, double threshold);
@@ -191,6 +197,18 @@ int isvd_dense_svd(int batch, int m, int n, const double* a, int w_keep, double*
                    double* u, double* vt);
 /* Same, from the engine's tracked matrices (no host copy of A). */
 int isvd_engine_oracle(isvd_engine* e, int w_keep, double* s, double* u);
+
+/* The two dense contractions on the FP64 tensor path (DMMA), device
+ * pointers, row-major, asynchronous on `stream` (NULL = legacy stream).
+ * gram: out (wa x wb) = xa(rows x wa, pitch lda)^T xb(rows x wb, pitch ldb);
+ * xa == xb with equal shapes computes the symmetric Gram's upper tiles only.
+ * gemm: c (rows x wc, pitch ldc) = x (rows x n, pitch ldx) q (n x wc, ldq).
+ * These back the Gram/QR of the guard and metrics and the tall-matrix SVD
+ * (init/refresh/oracle of configs 4 and 5b). */
+int isvd_gram(int rows, int wa, int wb, const double* xa, int lda, const double* xb, int ldb,
+              double* out, void* stream);
+int isvd_gemm_tall(int rows, int n, int wc, const double* x, int ldx, const double* q, int ldq,
+                   double* c, int ldc, void* stream);
 
 #ifdef __cplusplus
 }

@@ -62,6 +62,8 @@ SIGNATURES = {
     "isvd_engine_set_timing": (C.c_int, [_vp, C.c_int]),
     "isvd_engine_set_append_solver": (C.c_int, [_vp, C.c_int]),
     "isvd_engine_set_lazy": (C.c_int, [_vp, C.c_int]),
+    "isvd_engine_set_lazy_window": (C.c_int, [_vp, C.c_int]),
+    "isvd_engine_lazy_window": (C.c_int, [_vp]),
     "isvd_engine_set_reortho_threshold": (C.c_int, [_vp, C.c_double]),
     "isvd_engine_flush": (C.c_int, [_vp]),
     "isvd_engine_snapshot": (C.c_int, [_vp]),
@@ -71,6 +73,8 @@ SIGNATURES = {
     "isvd_engine_ortho_defect": (C.c_int, [_vp, _dp, _dp]),
     "isvd_engine_angle": (C.c_int, [_vp, C.c_int, _vp, C.c_int, C.c_int, _dp]),
     "isvd_dense_svd": (C.c_int, [C.c_int, C.c_int, C.c_int, _dp, C.c_int, _dp, _dp, _dp]),
+    "isvd_gram": (C.c_int, [C.c_int, C.c_int, C.c_int, _vp, C.c_int, _vp, C.c_int, _vp, _vp]),
+    "isvd_gemm_tall": (C.c_int, [C.c_int, C.c_int, C.c_int, _vp, C.c_int, _vp, C.c_int, _vp, C.c_int, _vp]),
     "isvd_engine_oracle": (C.c_int, [_vp, C.c_int, _dp, _dp]),
 }
 

@@ -34,6 +34,12 @@ void count_launch(int n = 1);
     }                                                                          \
   } while (0)
 
+#define ISVD_TRY(x)                 \
+  do {                              \
+    int _rc = (x);                  \
+    if (_rc != 0) return _rc;       \
+  } while (0)
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -343,6 +343,7 @@ DenseSvdPlan dense_svd_plan(int m, int n) {
   p.nb = nb;
   p.ncp = nb * BW;
   p.ldx = round_up(p.len, 8);
+  if (use_gram_path(m, n)) p.ldx = p.ncp = 1;  // gram_svd_run allocates its own
   return p;
 }
 
@@ -351,6 +352,20 @@ int dense_svd_run(int batch, int m, int n, const double* a, int64_t a_stride, in
                   int64_t s_all_stride, double* x, double* jac, int* flags, int* flags_host,
                   cudaStream_t st, int* sweeps_out) {
   if (batch == 0) return ISVD_OK;
+  if (use_gram_path(m, n)) {
+    for (int b = 0; b < batch; ++b) {
+      Mat ub{u.p ? u.p + b * u.stride : nullptr, u.stride, u.ld};
+      Mat vb{v.p ? v.p + b * v.stride : nullptr, v.stride, v.ld};
+      if (!ub.p || !vb.p || !s_w) {
+        set_error("dense_svd: the Gram path needs U, V and s outputs");
+        return ISVD_EINVAL;
+      }
+      ISVD_TRY(gram_svd_run(m, n, a + b * a_stride, lda, w, ub, vb, s_w + b * s_w_stride,
+                            s_all ? s_all + b * s_all_stride : nullptr, st));
+    }
+    if (sweeps_out) *sweeps_out = 0;
+    return ISVD_OK;
+  }
   DenseSvdPlan P = dense_svd_plan(m, n);
   const int64_t xs = P.x_elems(), js = P.j_elems();
   {
@@ -415,7 +430,7 @@ int dense_svd_run(int batch, int m, int n, const double* a, int64_t a_stride, in
   if (ns.p && s_w && w > 0 && w <= 160) {
     double *part = nullptr, *G = nullptr;
     int* live = nullptr;
-    const size_t np = (size_t)batch * gram_nblk(rows) * w * w;
+    const size_t np = (size_t)gram_part_elems(batch, rows, w, w);
     ISVD_CUDA(cudaMallocAsync((void**)&part, sizeof(double) * np, st));
     ISVD_CUDA(cudaMallocAsync((void**)&G, sizeof(double) * batch * w * w, st));
     ISVD_CUDA(cudaMallocAsync((void**)&live, sizeof(int) * batch, st));

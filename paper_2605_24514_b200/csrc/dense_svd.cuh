@@ -26,4 +26,11 @@ int dense_svd_run(int batch, int m, int n, const double* a, int64_t a_stride, in
                   int64_t s_all_stride, double* x, double* jac, int* flags, int* flags_host,
                   cudaStream_t st, int* sweeps_out);
 
+// Very tall matrices (m >= 4n, m*n >= kGramMinElems) take the Gram path of
+// gram_svd.cu inside dense_svd_run; the plan then needs no x/jac workspace.
+constexpr int64_t kGramMinElems = int64_t(1) << 24;
+bool use_gram_path(int m, int n);
+int gram_svd_run(int m, int n, const double* a, int lda, int w, Mat u, Mat v, double* s_w,
+                 double* s_all, cudaStream_t st);
+
 }  // namespace isvd

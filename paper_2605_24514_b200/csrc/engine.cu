@@ -25,6 +25,7 @@
 #include "common.cuh"
 #include "core_svd.cuh"
 #include "dense_svd.cuh"
+#include "tall.cuh"
 #include "guard.cuh"
 #include "metrics.cuh"
 #include "tick.cuh"
@@ -56,12 +57,6 @@ static void dfree(T*& p) {
   if (p) cudaFree(p);
   p = nullptr;
 }
-
-#define ISVD_TRY(x)              \
-  do {                           \
-    int _rc = (x);               \
-    if (_rc != ISVD_OK) return _rc; \
-  } while (0)
 
 static int check_device() {
   int n = 0;
@@ -160,8 +155,16 @@ struct isvd_engine {
   std::vector<int> tick_kind;  // 0 = append, 1 = rank-1, per recorded tick
   // Deferred left-basis rotation.  Row appends and rank-1
   // updates multiply the small W (U = [Ub 0; 0 I] W) instead of the tall U;
-  // U is materialised every kLazyRows appended rows and whenever it is read.
+  // U is materialised every lazy_rows appended rows and whenever it is read.
+  // Window: a flush costs ~2 m r doubles, a tick inside the window ~2 (r + t) r,
+  // so T ~ sqrt(2 m) balances them (48 rows at m = 1024; 2896 at m = 2^22).
   static constexpr int kLazyRows = 32;
+  int lazy_rows = kLazyRows;
+  static int lazy_window_for(int m) {
+    int t = (int)std::lround(std::sqrt(2.0 * (double)std::max(m, 1)));
+    t = (t + 7) / 8 * 8;
+    return std::min(std::max(t, kLazyRows), 4096);
+  }
   bool lazy_mode = true;
   bool lazy_active = false;
   int m_base = 0, r_base = 0, lazy_b = 0;
@@ -192,7 +195,7 @@ struct isvd_engine {
     }
     return ISVD_OK;
   }
-  int64_t wstride() const { return (int64_t)(ld + kLazyRows + 1) * ld; }
+  int64_t wstride() const { return (int64_t)(ld + lazy_rows + 1) * ld; }
   Mat Wm() const { return Mat{W, wstride(), ld}; }
   LazyBasis lazy() const { return LazyBasis{lazy_active ? 1 : 0, m_base, r_base, Wm()}; }
 
@@ -423,6 +426,7 @@ int isvd_engine_create(isvd_engine** out, int batch, int m, int n, int k, double
   e->n_cap = std::max(n_cap, n);
   int kc = std::max(std::max(k_cap, k), 1);
   e->ld = round_up(kc, 8);
+  e->lazy_rows = isvd_engine::lazy_window_for(m);
   if (e->ld + 1 > kCoreMaxS) {
     delete e;
     set_error("work rank exceeds the supported maximum");
@@ -701,7 +705,7 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
   }
   if (is_row) e->m += 1; else e->n += 1;
   e->r = keep;
-  if (e->lazy_active && e->lazy_b >= isvd_engine::kLazyRows) ISVD_TRY(e->flush());
+  if (e->lazy_active && e->lazy_b >= e->lazy_rows) ISVD_TRY(e->flush());
   ISVD_TRY(e->guard_step());
   if (e->ngroups_active == 1) e->mark();
   if (e->timing) { e->timed_ticks += 1; e->tick_kind.push_back(0); }
@@ -986,6 +990,20 @@ int isvd_engine_set_lazy(isvd_engine* e, int on) {
   return ISVD_OK;
 }
 
+int isvd_engine_set_lazy_window(isvd_engine* e, int rows) {
+  if (!e) { set_error("null engine"); return ISVD_EINVAL; }
+  if (rows < 1 || rows > 1 << 16) { set_error("lazy window out of range"); return ISVD_EINVAL; }
+  ISVD_TRY(e->flush());
+  ISVD_CUDA(cudaStreamSynchronize(e->st));
+  e->lazy_rows = rows;
+  dfree(e->W);
+  ISVD_TRY(dalloc(&e->W, (size_t)e->B * e->wstride()));
+  ISVD_CUDA(cudaMemsetAsync(e->W, 0, sizeof(double) * e->B * e->wstride(), e->st));
+  return ISVD_OK;
+}
+
+int isvd_engine_lazy_window(isvd_engine* e) { return e ? e->lazy_rows : -1; }
+
 int isvd_engine_set_append_solver(isvd_engine* e, int jacobi) {
   if (!e) { set_error("null engine"); return ISVD_EINVAL; }
   e->append_jacobi = jacobi != 0;
@@ -1059,7 +1077,7 @@ int isvd_engine_frob_error(isvd_engine* e, double* out) {
 }
 
 static int gram_defect(isvd_engine* e, Mat X, int rows, int w, double* host_out) {
-  ISVD_TRY(e->ensure_work(0, 0, (int64_t)e->B * gram_nblk(rows) * w * w, (int64_t)e->B * w * w + e->B));
+  ISVD_TRY(e->ensure_work(0, 0, gram_part_elems(e->B, rows, w, w), (int64_t)e->B * w * w + e->B));
   ISVD_TRY(launch_gram(e->B, rows, w, w, X, X, e->wpart, e->wout, e->st));
   ISVD_TRY(launch_defect(e->B, w, e->wout, e->wout + (int64_t)e->B * w * w, e->st));
   ISVD_CUDA(cudaMemcpyAsync(host_out, e->wout + (int64_t)e->B * w * w, sizeof(double) * e->B,
@@ -1119,7 +1137,7 @@ int isvd_engine_angle(isvd_engine* e, int which, const double* q, int q_cols, in
   if (rc == ISVD_OK) {
     // C = U^T Q (r x r) -> sigma_min via the core SVD kernel
     int S = e->S();
-    rc = e->ensure_work(0, 0, (int64_t)B * gram_nblk(m) * r * r, (int64_t)B * r * r + B);
+    rc = e->ensure_work(0, 0, gram_part_elems(B, m, r, r), (int64_t)B * r * r + B);
     if (rc == ISVD_OK) rc = launch_gram(B, m, r, r, e->Um(), Qm, e->wpart, e->wout, e->st);
     if (rc == ISVD_OK)
       rc = launch_core_svd(B, r, e->wout, (int64_t)r * r, r, e->uk, e->vk, e->cstride(), S, e->sv,
@@ -1223,6 +1241,34 @@ int isvd_engine_oracle(isvd_engine* e, int w_keep, double* s, double* u) {
 }
 
 // --------------------------------------------------------- functional kernels
+
+int isvd_gram(int rows, int wa, int wb, const double* xa, int lda, const double* xb, int ldb,
+              double* out, void* stream) {
+  if (rows < 0 || wa < 0 || wb < 0 || !xa || !xb || !out || lda < wa || ldb < wb) {
+    set_error("gram: bad argument");
+    return ISVD_EINVAL;
+  }
+  ISVD_TRY(check_device());
+  cudaStream_t st = (cudaStream_t)stream;
+  double* part = nullptr;
+  ISVD_CUDA(cudaMallocAsync((void**)&part, sizeof(double) * std::max<int64_t>(1, gram_part_elems(1, rows, wa, wb)), st));
+  Mat Xa{const_cast<double*>(xa), 0, lda}, Xb{const_cast<double*>(xb), 0, ldb};
+  const int sym = (xa == xb && wa == wb && lda == ldb) ? 1 : 0;
+  int rc = launch_gram_tiles(1, rows, wa, wb, Xa, Xb, sym, part, out, st);
+  cudaFreeAsync(part, st);
+  return rc;
+}
+
+int isvd_gemm_tall(int rows, int n, int wc, const double* x, int ldx, const double* q, int ldq,
+                   double* c, int ldc, void* stream) {
+  if (rows < 0 || n < 0 || wc < 0 || !x || !q || !c || ldx < n || ldq < wc || ldc < wc) {
+    set_error("gemm_tall: bad argument");
+    return ISVD_EINVAL;
+  }
+  ISVD_TRY(check_device());
+  Mat X{const_cast<double*>(x), 0, ldx}, Q{const_cast<double*>(q), 0, ldq}, C{c, 0, ldc};
+  return launch_gemm_tall(1, rows, n, wc, X, Q, C, (cudaStream_t)stream);
+}
 
 int isvd_core_svd(int batch, int s, const double* core, double* u, double* sv, double* vt,
                   void* stream) {

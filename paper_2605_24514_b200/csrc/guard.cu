@@ -75,7 +75,7 @@ __global__ void trsm_upper_kernel(int w, const double* __restrict__ R, double* _
 int reortho_defects(int batch, int w, Mat U, int m, Mat V, int n, double* host_du, double* host_dv,
                     cudaStream_t st) {
   const int rows = m > n ? m : n;
-  const size_t np = (size_t)batch * gram_nblk(rows) * w * w;
+  const size_t np = (size_t)gram_part_elems(batch, rows, w, w);
   double *part = nullptr, *G = nullptr, *d = nullptr;
   ISVD_CUDA(cudaMallocAsync((void**)&part, sizeof(double) * np, st));
   ISVD_CUDA(cudaMallocAsync((void**)&G, sizeof(double) * batch * w * w, st));
@@ -100,7 +100,7 @@ int reortho_apply(int batch, int w, Mat U, int m, Mat V, int n, double* s, int l
                   cudaStream_t st) {
   if (w < 1) return ISVD_OK;
   const int rows = m > n ? m : n;
-  const size_t np = (size_t)batch * gram_nblk(rows) * w * w;
+  const size_t np = (size_t)gram_part_elems(batch, rows, w, w);
   double *part = nullptr, *Ru = nullptr, *Rv = nullptr;
   ISVD_CUDA(cudaMallocAsync((void**)&part, sizeof(double) * np, st));
   ISVD_CUDA(cudaMallocAsync((void**)&Ru, sizeof(double) * batch * w * w, st));

@@ -3,6 +3,7 @@
 // bit-identical (tests/test_stream.py:204-215 compares runs exactly).
 #include "common.cuh"
 #include "metrics.cuh"
+#include "tall.cuh"
 #include "../../include/isvd.h"
 
 namespace isvd {
@@ -69,35 +70,6 @@ __global__ void reduce_partials_kernel(const double* partial, int nblk, int widt
   if (threadIdx.x == 0) out[(int64_t)b * width + e] = tot;
 }
 
-constexpr int kGramRows = 128;
-// partial[b][blk][wa][wb] = Xa[rows]^T Xb[rows] over a 128-row slab.
-__global__ void __launch_bounds__(256) gram_partial_kernel(int rows, int wa, int wb, Mat Xa,
-                                                          Mat Xb, double* partial, int nblk) {
-  extern __shared__ double sm[];
-  double* as = sm;                    // [kGramRows][wa]
-  double* bs = sm + kGramRows * wa;   // [kGramRows][wb]
-  const int b = blockIdx.y, blk = blockIdx.x;
-  const int row0 = blk * kGramRows;
-  const double* A = Xa.p + b * Xa.stride;
-  const double* B = Xb.p + b * Xb.stride;
-  for (int idx = threadIdx.x; idx < kGramRows * wa; idx += blockDim.x) {
-    int i = idx / wa, t = idx % wa, row = row0 + i;
-    as[idx] = row < rows ? A[(int64_t)row * Xa.ld + t] : 0.0;
-  }
-  for (int idx = threadIdx.x; idx < kGramRows * wb; idx += blockDim.x) {
-    int i = idx / wb, t = idx % wb, row = row0 + i;
-    bs[idx] = row < rows ? B[(int64_t)row * Xb.ld + t] : 0.0;
-  }
-  __syncthreads();
-  double* out = partial + ((int64_t)b * nblk + blk) * wa * wb;
-  for (int e = threadIdx.x; e < wa * wb; e += blockDim.x) {
-    int p = e / wb, q = e % wb;
-    double acc = 0.0;
-    for (int i = 0; i < kGramRows; ++i) acc = fma(as[i * wa + p], bs[i * wb + q], acc);
-    out[e] = acc;
-  }
-}
-
 // defect[b] = ||G[b] - I||_F for square w x w Gram matrices.
 __global__ void defect_kernel(int w, const double* G, double* out) {
   __shared__ double red[32];
@@ -115,7 +87,6 @@ __global__ void defect_kernel(int w, const double* G, double* out) {
 }  // namespace
 
 int frob_nblk(int m) { return ceil_div(m, kFrobRows); }
-int gram_nblk(int rows) { return ceil_div(rows, kGramRows); }
 
 int launch_frob_error_sq(int batch, int m, int n, int w, const double* A, int64_t a_stride, int lda,
                          Mat U, const double* s, int lds, Mat V, double* partial, double* out,
@@ -142,23 +113,8 @@ int launch_frob_error_sq(int batch, int m, int n, int w, const double* A, int64_
 
 int launch_gram(int batch, int rows, int wa, int wb, Mat Xa, Mat Xb, double* partial, double* out,
                 cudaStream_t st) {
-  if (wa > kWMax || wb > kWMax) {
-    set_error("gram: width too large");
-    return ISVD_EINVAL;
-  }
-  int nblk = gram_nblk(rows);
-  size_t smem = sizeof(double) * kGramRows * (wa + wb);
-  static bool attr = false;
-  if (!attr) {
-    ISVD_CUDA(cudaFuncSetAttribute(gram_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   200 * 1024));
-    attr = true;
-  }
-  gram_partial_kernel<<<dim3(nblk, batch), 256, smem, st>>>(rows, wa, wb, Xa, Xb, partial, nblk);
-  ISVD_LAUNCHED();
-  reduce_partials_kernel<<<dim3(wa * wb, batch), 128, 0, st>>>(partial, nblk, wa * wb, out);
-  ISVD_LAUNCHED();
-  return ISVD_OK;
+  const bool sym = Xa.p == Xb.p && Xa.ld == Xb.ld && Xa.stride == Xb.stride && wa == wb;
+  return launch_gram_tiles(batch, rows, wa, wb, Xa, Xb, sym ? 1 : 0, partial, out, st);
 }
 
 int launch_defect(int batch, int w, const double* G, double* out, cudaStream_t st) {

@@ -2,16 +2,17 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include "tick.cuh"
+#include "tall.cuh"
 
 namespace isvd {
 
 int frob_nblk(int m);
-int gram_nblk(int rows);
 // out[b] = ||A[b] - U[b] diag(s[b]) V[b]^T||_F^2 ; partial: batch * frob_nblk(m)
 int launch_frob_error_sq(int batch, int m, int n, int w, const double* A, int64_t a_stride, int lda,
                          Mat U, const double* s, int lds, Mat V, double* partial, double* out,
                          cudaStream_t st);
-// out[b] (wa x wb) = Xa[b][0:rows,0:wa]^T Xb[b][0:rows,0:wb] ; partial: batch*gram_nblk*wa*wb
+// out[b] (wa x wb) = Xa[b][0:rows,0:wa]^T Xb[b][0:rows,0:wb] (DMMA, tall.cu);
+// partial: gram_part_elems(batch, rows, wa, wb) doubles
 int launch_gram(int batch, int rows, int wa, int wb, Mat Xa, Mat Xb, double* partial, double* out,
                 cudaStream_t st);
 int launch_defect(int batch, int w, const double* G, double* out, cudaStream_t st);

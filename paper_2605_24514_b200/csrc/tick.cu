@@ -549,17 +549,30 @@ __global__ void zero_kernel(double* p, size_t n) {
     p[i] = 0.0;
 }
 
-__global__ void sumsq_kernel(int rows, int cols, const double* __restrict__ a, int64_t a_stride,
-                             int lda, double* __restrict__ out) {
+// partial[b][blk] = sum of squares over rows [blk*rpb, (blk+1)*rpb) of stream b
+__global__ void sumsq_kernel(int rows, int cols, int rpb, const double* __restrict__ a,
+                             int64_t a_stride, int lda, double* __restrict__ partial) {
   __shared__ double red[32];
-  const int b = blockIdx.x;
+  const int b = blockIdx.y, blk = blockIdx.x;
   const double* ab = a + b * a_stride;
+  const int r1 = min(rows, (blk + 1) * rpb);
   double acc = 0.0;
-  for (int i = threadIdx.x >> 5; i < rows; i += blockDim.x >> 5)
+  for (int i = blk * rpb + (threadIdx.x >> 5); i < r1; i += blockDim.x >> 5)
     for (int j = threadIdx.x & 31; j < cols; j += 32) {
       double v = ab[(int64_t)i * lda + j];
       acc = fma(v, v, acc);
     }
+  double t = block_sum(acc, red);
+  if (threadIdx.x == 0) partial[(int64_t)b * gridDim.x + blk] = t;
+}
+
+// out[b] = sum_blk partial[b][blk] in a fixed order
+__global__ void sumsq_reduce_kernel(int nblk, const double* __restrict__ partial,
+                                    double* __restrict__ out) {
+  __shared__ double red[32];
+  const int b = blockIdx.x;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) acc += partial[(int64_t)b * nblk + i];
   double t = block_sum(acc, red);
   if (threadIdx.x == 0) out[b] = t;
 }
@@ -740,8 +753,19 @@ int launch_zero(double* p, size_t n, cudaStream_t st) {
 
 int launch_sumsq(int batch, int rows, int cols, const double* a, int64_t a_stride, int lda,
                  double* out, cudaStream_t st) {
-  sumsq_kernel<<<batch, 512, 0, st>>>(rows, cols, a, a_stride, lda, out);
+  if (batch == 0) return ISVD_OK;
+  // one CTA per stream for small matrices; row blocks + ordered reduce for
+  // tall ones (cfg 4 / 5b), so the result depends on the shape only
+  const int64_t elems = (int64_t)rows * cols;
+  const int nblk = elems < (1 << 20) ? 1 : (int)std::min<int64_t>(ceil_div(rows, 64), 2048);
+  const int rpb = ceil_div(rows, nblk);
+  double* part = nullptr;
+  ISVD_CUDA(cudaMallocAsync((void**)&part, sizeof(double) * batch * nblk, st));
+  sumsq_kernel<<<dim3(nblk, batch), 512, 0, st>>>(rows, cols, rpb, a, a_stride, lda, part);
   ISVD_LAUNCHED();
+  sumsq_reduce_kernel<<<batch, 256, 0, st>>>(nblk, part, out);
+  ISVD_LAUNCHED();
+  ISVD_CUDA(cudaFreeAsync(part, st));
   return ISVD_OK;
 }
 
