@@ -332,7 +332,7 @@ __global__ void polish_trsm_kernel(int rows, int w, Mat X, const double* __restr
 
 }  // namespace
 
-DenseSvdPlan dense_svd_plan(int m, int n) {
+DenseSvdPlan dense_svd_plan(int m, int n, int w) {
   DenseSvdPlan p;
   p.m = m;
   p.n = n;
@@ -343,7 +343,7 @@ DenseSvdPlan dense_svd_plan(int m, int n) {
   p.nb = nb;
   p.ncp = nb * BW;
   p.ldx = round_up(p.len, 8);
-  if (use_gram_path(m, n)) p.ldx = p.ncp = 1;  // gram_svd_run allocates its own
+  if (use_gram_path(m, n, w)) p.ldx = p.ncp = 1;  // gram_svd_run allocates its own
   return p;
 }
 
@@ -352,7 +352,7 @@ int dense_svd_run(int batch, int m, int n, const double* a, int64_t a_stride, in
                   int64_t s_all_stride, double* x, double* jac, int* flags, int* flags_host,
                   cudaStream_t st, int* sweeps_out) {
   if (batch == 0) return ISVD_OK;
-  if (use_gram_path(m, n)) {
+  if (use_gram_path(m, n, w)) {
     for (int b = 0; b < batch; ++b) {
       Mat ub{u.p ? u.p + b * u.stride : nullptr, u.stride, u.ld};
       Mat vb{v.p ? v.p + b * v.stride : nullptr, v.stride, v.ld};
@@ -366,7 +366,7 @@ int dense_svd_run(int batch, int m, int n, const double* a, int64_t a_stride, in
     if (sweeps_out) *sweeps_out = 0;
     return ISVD_OK;
   }
-  DenseSvdPlan P = dense_svd_plan(m, n);
+  DenseSvdPlan P = dense_svd_plan(m, n, w);
   const int64_t xs = P.x_elems(), js = P.j_elems();
   {
     int64_t total = std::max(xs, js);

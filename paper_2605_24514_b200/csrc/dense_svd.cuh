@@ -11,7 +11,8 @@ struct DenseSvdPlan {
   int64_t x_elems() const { return (int64_t)ncp * ldx; }
   int64_t j_elems() const { return (int64_t)ncp * ncp; }
 };
-DenseSvdPlan dense_svd_plan(int m, int n);
+// w = number of leading triplets wanted (selects the Gram path, see below).
+DenseSvdPlan dense_svd_plan(int m, int n, int w);
 
 // Thin SVD of `batch` row-major m x n matrices A[b] = a + b*a_stride (pitch
 // lda), in the reference's canonical form (linalg.py:84-92): singular
@@ -26,10 +27,12 @@ int dense_svd_run(int batch, int m, int n, const double* a, int64_t a_stride, in
                   int64_t s_all_stride, double* x, double* jac, int* flags, int* flags_host,
                   cudaStream_t st, int* sweeps_out);
 
-// Very tall matrices (m >= 4n, m*n >= kGramMinElems) take the Gram path of
-// gram_svd.cu inside dense_svd_run; the plan then needs no x/jac workspace.
+// Very tall matrices (m >= 4n, m*n >= kGramMinElems) with w <= kGramMaxW
+// leading triplets wanted take the Gram path of gram_svd.cu inside
+// dense_svd_run; the plan then needs no x/jac workspace.
 constexpr int64_t kGramMinElems = int64_t(1) << 24;
-bool use_gram_path(int m, int n);
+constexpr int kGramMaxW = 160;  // Rayleigh-Ritz core = one core SVD (kCoreMaxS)
+bool use_gram_path(int m, int n, int w);
 int gram_svd_run(int m, int n, const double* a, int lda, int w, Mat u, Mat v, double* s_w,
                  double* s_all, cudaStream_t st);
 

@@ -369,9 +369,9 @@ struct isvd_engine {
 
   // dense thin SVD of the tracked matrix into U, V, s (engine init/refresh)
   int factor_tracked() {
-    DenseSvdPlan P = dense_svd_plan(m, n);
-    ISVD_TRY(ensure_work((int64_t)B * P.x_elems(), (int64_t)B * P.j_elems(), 0, 0));
     int w = std::min(k, std::min(m, n));
+    DenseSvdPlan P = dense_svd_plan(m, n, w);
+    ISVD_TRY(ensure_work((int64_t)B * P.x_elems(), (int64_t)B * P.j_elems(), 0, 0));
     int sweeps = 0;
     lazy_active = false;  // U is recomputed from A
     lazy_b = 0;
@@ -1166,9 +1166,9 @@ int isvd_engine_angle(isvd_engine* e, int which, const double* q, int q_cols, in
 static int oracle_common(int B, int m, int n, const double* a_dev, int64_t a_stride, int lda,
                          int w_keep, double* s_host, double* u_host, double* vt_host,
                          cudaStream_t st) {
-  DenseSvdPlan P = dense_svd_plan(m, n);
+  const int w = std::max(0, std::min(w_keep, std::min(m, n)));
+  DenseSvdPlan P = dense_svd_plan(m, n, w);
   const int nc = P.nc;
-  const int w = std::max(0, std::min(w_keep, nc));
   const int ldw = round_up(std::max(w, 1), 8);
   double *x = nullptr, *jac = nullptr, *U = nullptr, *V = nullptr, *sa = nullptr, *sw = nullptr;
   int* fl = nullptr;

@@ -56,8 +56,9 @@ __global__ void gram_spectrum_kernel(int w, int nc, double* __restrict__ s_w,
 
 }  // namespace
 
-bool use_gram_path(int m, int n) {
-  return (int64_t)m >= 4 * (int64_t)n && n >= 16 && (int64_t)m * n >= kGramMinElems;
+bool use_gram_path(int m, int n, int w) {
+  return (int64_t)m >= 4 * (int64_t)n && n >= 16 && (int64_t)m * n >= kGramMinElems &&
+         w <= kGramMaxW;
 }
 
 int gram_svd_run(int m, int n, const double* a, int lda, int w, Mat u, Mat v, double* s_w,
@@ -65,7 +66,7 @@ int gram_svd_run(int m, int n, const double* a, int lda, int w, Mat u, Mat v, do
   w = std::max(0, std::min(w, n));
   const int ldq = round_up(std::max(w, 1), 8);
   const int64_t np = gram_part_elems(1, m, n, n);
-  DenseSvdPlan P = dense_svd_plan(n, n);
+  DenseSvdPlan P = dense_svd_plan(n, n, w);
   const int S = std::max(w, 1);
   double *G = nullptr, *part = nullptr, *x = nullptr, *jac = nullptr, *Vq = nullptr,
          *lam = nullptr, *swi = nullptr, *core = nullptr, *uk = nullptr, *vk = nullptr,

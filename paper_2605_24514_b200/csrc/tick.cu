@@ -1,4 +1,5 @@
 // Per-tick kernels of the incremental update (kernels K1, K3-K6, K9).
+#include <algorithm>
 #include "common.cuh"
 #include "core_svd.cuh"
 #include "tick.cuh"
@@ -142,6 +143,137 @@ __global__ void __launch_bounds__(256) project_append_kernel(
   }
 }
 
+// K1 for a few streams with long factors (config 5b: B = 1, n = 1024,
+// r = 128; column appends of configs 4/5b: rows = m): the rows are split over
+// S CTAs per stream.  (a) partial p and ||x||^2 per slice (+ tracked-matrix
+// write); (b) every CTA sums the partials in a fixed order, forms z on its
+// slice and a partial ||z||^2; (c) one CTA per stream builds the core.
+constexpr int kSplitRows = 64;
+
+__global__ void __launch_bounds__(256) proj_split_p_kernel(
+    int rows, int r, int rps, Mat F, const double* __restrict__ x, int64_t x_stride,
+    double* __restrict__ A, int64_t a_stride, int64_t a_off, int64_t a_step,
+    double* __restrict__ part) {
+  __shared__ double pw[8][kRMax];
+  __shared__ double red[32];
+  const int b = blockIdx.y, sp = blockIdx.x, S = gridDim.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int c0 = sp * rps, c1 = min(rows, c0 + rps);
+  const double* Fb = F.p + b * F.stride;
+  const double* xb = x + b * x_stride;
+  double* Ab = A ? A + b * a_stride + a_off : nullptr;
+  double xx = 0.0;
+  for (int c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
+    const double xc = xb[c];
+    xx = fma(xc, xc, xx);
+    if (Ab) Ab[(int64_t)c * a_step] = xc;
+  }
+  double acc[(kRMax + 31) / 32];
+#pragma unroll
+  for (int t = 0; t < (kRMax + 31) / 32; ++t) acc[t] = 0.0;
+  for (int c = c0 + warp; c < c1; c += nw) {
+    const double xc = xb[c];
+    const double* fr = Fb + (int64_t)c * F.ld;
+#pragma unroll
+    for (int t = 0; t < (kRMax + 31) / 32; ++t) {
+      const int l = lane + 32 * t;
+      if (l < r) acc[t] = fma(fr[l], xc, acc[t]);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < (kRMax + 31) / 32; ++t) {
+    const int l = lane + 32 * t;
+    if (l < r) pw[warp][l] = acc[t];
+  }
+  const double xt = block_sum(xx, red);  // also orders the pw writes
+  double* out = part + ((int64_t)b * S + sp) * (r + 1);
+  for (int l = threadIdx.x; l < r; l += blockDim.x) {
+    double v = 0.0;
+    for (int w = 0; w < nw; ++w) v += pw[w][l];
+    out[l] = v;
+  }
+  if (threadIdx.x == 0) out[r] = xt;
+}
+
+__global__ void __launch_bounds__(256) proj_split_z_kernel(
+    int rows, int r, int rps, Mat F, const double* __restrict__ x, int64_t x_stride,
+    const double* __restrict__ part, double* __restrict__ z, int64_t z_stride,
+    double* __restrict__ zpart) {
+  __shared__ double p[kRMax];
+  __shared__ double red[32];
+  const int b = blockIdx.y, sp = blockIdx.x, S = gridDim.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const double* pb = part + (int64_t)b * S * (r + 1);
+  for (int l = threadIdx.x; l < r; l += blockDim.x) {
+    double v = 0.0;
+    for (int t = 0; t < S; ++t) v += pb[(int64_t)t * (r + 1) + l];
+    p[l] = v;
+  }
+  __syncthreads();
+  const int c0 = sp * rps, c1 = min(rows, c0 + rps);
+  const double* Fb = F.p + b * F.stride;
+  const double* xb = x + b * x_stride;
+  double* zb = z + b * z_stride;
+  double zz = 0.0;
+  for (int c = c0 + warp; c < c1; c += nw) {
+    const double* fr = Fb + (int64_t)c * F.ld;
+    double v = 0.0;
+    for (int l = lane; l < r; l += 32) v = fma(fr[l], p[l], v);
+    v = warp_sum(v);
+    const double zc = xb[c] - v;
+    if (lane == 0) {
+      zb[c] = zc;
+      zz = fma(zc, zc, zz);
+    }
+  }
+  const double zt = block_sum(zz, red);
+  if (threadIdx.x == 0) zpart[(int64_t)b * S + sp] = zt;
+}
+
+__global__ void proj_split_core_kernel(int r, int S, const double* __restrict__ part,
+                                       const double* __restrict__ zpart,
+                                       const double* __restrict__ s, int lds, double tol,
+                                       double* __restrict__ core, int64_t core_stride, int ldcore,
+                                       double* __restrict__ inj_scale, double* __restrict__ rho_out,
+                                       double* __restrict__ xnorm_out, double* __restrict__ N) {
+  __shared__ double p[kRMax];
+  __shared__ double sc[2];
+  const int b = blockIdx.x;
+  const double* pb = part + (int64_t)b * S * (r + 1);
+  for (int l = threadIdx.x; l <= r; l += blockDim.x) {
+    double v = 0.0;
+    for (int t = 0; t < S; ++t) v += pb[(int64_t)t * (r + 1) + l];
+    if (l < r) p[l] = v; else sc[0] = v;
+  }
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+    for (int t = 0; t < S; ++t) v += zpart[(int64_t)b * S + t];
+    sc[1] = v;
+  }
+  __syncthreads();
+  const double xnorm2 = sc[0], rho = sqrt(sc[1]);
+  const bool fresh = rho > tol;
+  const int P = r + 1;
+  double* Kb = core + b * core_stride;
+  const double* sb = s + (int64_t)b * lds;
+  for (int idx = threadIdx.x; idx < P * P; idx += blockDim.x) {
+    const int i = idx / P, j = idx % P;
+    double v = 0.0;
+    if (i < r) {
+      if (i == j) v = sb[i];
+    } else {
+      v = (j < r) ? p[j] : (fresh ? rho : 0.0);
+    }
+    Kb[i * ldcore + j] = v;
+  }
+  if (threadIdx.x == 0) {
+    inj_scale[b] = fresh ? 1.0 / rho : 0.0;
+    rho_out[b] = rho;
+    xnorm_out[b] = sqrt(xnorm2);
+    N[b] += xnorm2;
+  }
+}
+
 // -------------------------------------------------------------------- K6
 __global__ void rank1_build_kernel(int r, Mat U, Mat V, const double* __restrict__ s, int lds,
                                    const int64_t* __restrict__ ii, const int64_t* __restrict__ jj,
@@ -196,11 +328,12 @@ __global__ void rank1_build_kernel(int r, Mat U, Mat V, const double* __restrict
 // B fragments are pre-permuted into shared memory in lane order (one
 // conflict-free LDS.64 per DMMA).
 constexpr int kRotWarps = 8;
-constexpr int kRotRowsPerBlock = 512;
+constexpr int kRotRowsPerBlock = 512;  // upper bound; small jobs use fewer (rot_rows_per_block)
+constexpr int kRotNB = 8;              // output n-tiles per pass (independent DMMA chains)
 
 template <int KP>
-__global__ void __launch_bounds__(kRotWarps * 32, 2)
-    rotate_kernel(int r, int keep, int NP, RotJob j0, RotJob j1, int nblk0) {
+__global__ void __launch_bounds__(kRotWarps * 32, 1)
+    rotate_kernel(int r, int keep, int NP, RotJob j0, RotJob j1, int nblk0, int rpb) {
   extern __shared__ double smem[];
   constexpr int KQ = KP / 4;
   const int NT = NP / 8;
@@ -234,8 +367,8 @@ __global__ void __launch_bounds__(kRotWarps * 32, 2)
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
-  const int row_begin = blk * kRotRowsPerBlock;
-  const int row_end = min(J.rows, row_begin + kRotRowsPerBlock);
+  const int row_begin = blk * rpb;
+  const int row_end = min(J.rows, row_begin + rpb);
   const double* qf = Qf + lane;
 
   int row0 = row_begin + warp * 8;
@@ -267,23 +400,44 @@ __global__ void __launch_bounds__(kRotWarps * 32, 2)
     if (nxt < row_end) load(nxt, an);
     const int row = row0 + g;
     const double zr = (zb && row < row_end) ? zb[row] * zscale : 0.0;
-    for (int nn = 0; nn < NT; ++nn) {
-      double d0 = 0.0, d1 = 0.0;
+    // kk-outer / nn-inner: kRotNB independent accumulator chains per pass;
+    // the row's inputs live in a[], so the in-place stores are safe
+    for (int n0 = 0; n0 < NT; n0 += kRotNB) {
+      double d[kRotNB][2];
 #pragma unroll
-      for (int kk = 0; kk < KQ; ++kk) dmma_8x8x4(d0, d1, a[kk], qf[(kk * NT + nn) * 32]);
-      const int c0 = nn * 8 + 2 * q;
-      if (zb) {
-        d0 = fma(zr, Qr[c0], d0);
-        d1 = fma(zr, Qr[c0 + 1], d1);
+      for (int j = 0; j < kRotNB; ++j) d[j][0] = d[j][1] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < KQ; ++kk) {
+#pragma unroll
+        for (int j = 0; j < kRotNB; ++j)
+          if (n0 + j < NT) dmma_8x8x4(d[j][0], d[j][1], a[kk], qf[(kk * NT + n0 + j) * 32]);
       }
-      if (row < row_end)
-        *reinterpret_cast<double2*>(X + (int64_t)row * ld + c0) = make_double2(d0, d1);
+#pragma unroll
+      for (int j = 0; j < kRotNB; ++j) {
+        if (n0 + j >= NT) break;
+        const int c0 = (n0 + j) * 8 + 2 * q;
+        double d0 = d[j][0], d1 = d[j][1];
+        if (zb) {
+          d0 = fma(zr, Qr[c0], d0);
+          d1 = fma(zr, Qr[c0 + 1], d1);
+        }
+        if (row < row_end)
+          *reinterpret_cast<double2*>(X + (int64_t)row * ld + c0) = make_double2(d0, d1);
+      }
     }
     if (nxt < row_end) {
 #pragma unroll
       for (int kk = 0; kk < KQ; ++kk) a[kk] = an[kk];
     }
   }
+}
+
+// Rows per CTA: enough CTAs to cover the SMs twice for small jobs (config 5b's
+// V / W at B = 1), 512 rows for large ones (the Q staging is amortised).
+static int rot_rows_per_block(int64_t total_rows) {
+  int64_t rpb = (total_rows + 2 * 148 - 1) / (2 * 148);
+  rpb = (rpb + 63) / 64 * 64;
+  return (int)std::min<int64_t>(std::max<int64_t>(rpb, 64), kRotRowsPerBlock);
 }
 
 // Small-width variant (KP <= 32, keep <= 32): the core rotation is held as
@@ -594,6 +748,27 @@ int launch_project_append(int batch, int rows, int r, Mat F, const double* x, in
     set_error("factor width exceeds kernel limit");
     return ISVD_EINVAL;
   }
+  if (batch <= 32 && (int64_t)rows * r >= 16384) {
+    // few streams, long factors: split the rows over CTAs (see proj_split_*)
+    const int S = std::max(1, std::min(ceil_div(rows, kSplitRows), std::max(1, 296 / batch)));
+    const int rps = ceil_div(rows, S);
+    double *part = nullptr, *zpart = nullptr;
+    ISVD_CUDA(cudaMallocAsync((void**)&part, sizeof(double) * batch * S * (r + 1), st));
+    ISVD_CUDA(cudaMallocAsync((void**)&zpart, sizeof(double) * batch * S, st));
+    proj_split_p_kernel<<<dim3(S, batch), 256, 0, st>>>(rows, r, rps, F, x, x_stride, A, a_stride,
+                                                         a_off, a_step, part);
+    ISVD_LAUNCHED();
+    proj_split_z_kernel<<<dim3(S, batch), 256, 0, st>>>(rows, r, rps, F, x, x_stride, part, z,
+                                                         z_stride, zpart);
+    ISVD_LAUNCHED();
+    proj_split_core_kernel<<<batch, 256, 0, st>>>(r, S, part, zpart, s, lds, tol, core,
+                                                   core_stride, ldcore, inj_scale, rho_out,
+                                                   xnorm_out, N);
+    ISVD_LAUNCHED();
+    ISVD_CUDA(cudaFreeAsync(part, st));
+    ISVD_CUDA(cudaFreeAsync(zpart, st));
+    return ISVD_OK;
+  }
   const size_t stage = sizeof(double) * ((size_t)rows * F.ld + rows);
   const bool aligned = (reinterpret_cast<uintptr_t>(F.p) % 16 == 0) && (F.stride % 2 == 0) &&
                        (F.ld % 2 == 0);
@@ -638,11 +813,12 @@ static int rotate_dispatch(int batch, int r, int keep, const RotJob& j0, const R
                                    160 * 1024));
     attr = true;
   }
-  int nb0 = ceil_div(j0.rows, kRotRowsPerBlock);
+  const int rpb = rot_rows_per_block((int64_t)batch * (j0.rows + (j1 ? j1->rows : 0)));
+  int nb0 = ceil_div(j0.rows, rpb);
   if (j0.new_row && nb0 == 0) nb0 = 1;
   int nb1 = 0;
   if (j1) {
-    nb1 = ceil_div(j1->rows, kRotRowsPerBlock);
+    nb1 = ceil_div(j1->rows, rpb);
     if (j1->new_row && nb1 == 0) nb1 = 1;
   }
   if (nb0 + nb1 == 0) return ISVD_OK;
@@ -662,7 +838,7 @@ static int rotate_dispatch(int batch, int r, int keep, const RotJob& j0, const R
     }
   }
   dim3 grid(nb0 + nb1, batch);
-  rotate_kernel<KP><<<grid, kRotWarps * 32, smem, st>>>(r, keep, NP, j0, j1 ? *j1 : j0, nb0);
+  rotate_kernel<KP><<<grid, kRotWarps * 32, smem, st>>>(r, keep, NP, j0, j1 ? *j1 : j0, nb0, rpb);
   ISVD_LAUNCHED();
   return ISVD_OK;
 }

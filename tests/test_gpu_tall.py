@@ -11,7 +11,7 @@ from conftest import rel_err, sine_angle
 from oracle import OracleEngine as OEngine
 from oracle import full_svd as o_full_svd
 from paper_2605_24514_b200 import BatchedSvdEngine, SvdEngine, _lib, full_svd, truncated_svd
-from paper_2605_24514_b200.linalg import orthonormality_defect
+from paper_2605_24514_b200.linalg import _device_svd, orthonormality_defect
 
 pytestmark = pytest.mark.gpu
 
@@ -85,11 +85,15 @@ def test_gram_path_svd_matches_lapack(m, n, rank, k):
     assert orthonormality_defect(f.vt.T) <= 1e-10
     lead = np.argmax(np.abs(f.u), axis=0)
     assert np.all(f.u[lead, np.arange(w)] >= 0.0)
-    # full spectrum: head from the Ritz step, tail from the Gram eigenvalues
-    g = full_svd(a)
-    assert rel_err(g.s, fo.s) < 1e-7
-    e_opt = np.linalg.norm(g.s[k:]) if k < n else 0.0
+    # full spectrum (the oracle's E_opt input): head from the Ritz step, tail
+    # from the Gram eigenvalues
+    _, s_all, _ = _device_svd(a, k)
+    assert rel_err(s_all, fo.s) < 1e-7
+    e_opt = np.linalg.norm(s_all[k:]) if k < n else 0.0
     assert abs(e_opt - np.linalg.norm(fo.s[k:])) <= 1e-9 * max(1.0, np.linalg.norm(fo.s))
+    # all n triplets (w > kGramMaxW) take the blocked-Jacobi path
+    g = full_svd(a)
+    assert rel_err(g.s, fo.s) < 1e-10
 
 
 def test_gram_path_rank_deficient():
