@@ -42,6 +42,9 @@ TOTAL_STREAMS = 4096
 EVENTS = 1024
 METRIC = "iSVD updates/sec (k=32)"
 UNIT = "updates/s"
+# BASELINE configs[4] part b: one tall matrix, k = 128, 256 row appends
+M5B, N5B, RANK5B, K5B, T5B = 1 << 22, 1024, 128, 128, 256
+DMMA_PEAK_TFS = 37.06  # measured FP64 DMMA.8x8x4 peak, profiles/r01_fp64_peaks.txt
 
 
 def _peaks():
@@ -99,6 +102,28 @@ def cpu_reference(n_streams: int, n_events: int, seed: int = 0):
     return updates / secs, workers, updates, secs
 
 
+def cpu_reference_5b(ticks: int = 3, seed: int = 0):
+    """The reference's row-append kernel (oracle/ restatement of
+    _kernels_py.row_append, numpy/BLAS on all host cores) on a full-size
+    config-5b factor set: U 4,194,304 x 128, Vt 128 x 1024.  Per SURVEY 8(d)
+    the engine path's 34 GB vstack and infeasible init SVD are excluded."""
+    from oracle import kernel_row_append
+
+    rng = np.random.default_rng([seed, 55])
+    # ~orthonormal columns; a tiled block keeps the 4.3 GB setup to a memcpy
+    u = np.tile(rng.standard_normal((1 << 16, K5B)) / math.sqrt(M5B), (M5B >> 16, 1))
+    vt = np.linalg.qr(rng.standard_normal((N5B, K5B)))[0].T.copy()
+    s_ = np.sort(rng.uniform(1.0, 100.0, K5B))[::-1].copy()
+    xs = rng.standard_normal((ticks, K5B)) @ vt
+    t0 = time.perf_counter()
+    for t in range(ticks):
+        u2, s2, vt2, _ = kernel_row_append(u, s_, vt, xs[t], 1e-10, K5B)
+        u = u2[:M5B]  # keep the height fixed so every sample tick costs the same
+        s_, vt = s2, vt2
+    secs = time.perf_counter() - t0
+    return ticks / secs, len(os.sched_getaffinity(0)), ticks, secs
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -120,6 +145,14 @@ def run_reference(args):
                                    f"per worker, init excluded)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not args.no_k128:
+        v5, c5, t5, s5 = cpu_reference_5b()
+        line["k128"] = {"metric": "iSVD updates/sec (k=128)", "value": v5, "unit": UNIT,
+                        "config": {"workload": "cfg5b_tall", "m": M5B, "n": N5B, "k": K5B},
+                        "cpu_baseline": {"value": v5, "unit": UNIT, "cores": c5, "kind": "port",
+                                         "sample": f"{t5} full-size row appends through the "
+                                                   "oracle row-append kernel (numpy/BLAS, all "
+                                                   "host threads), engine vstack excluded"}}
     print(json.dumps(line), flush=True)
 
 
@@ -219,10 +252,10 @@ def tick_bytes(B, m, n, w, row_tick):
     return 8 * B * (2 * m * w + 2 * n * w + 2 * w + 2)
 
 
-def _simulate_bytes(B, steps):
+def _simulate_bytes(B, steps, window=32):
     """Algorithmic bytes of the per-tick kernels over `steps` ticks (simulating
     the engine's deferred-U window: W = (32 + b) x 32 rotated in place,
-    flushed every 32 appended rows)."""
+    flushed every `window` appended rows)."""
     proj_bytes = rot_bytes = all_bytes = 0.0
     m, b_rows, active = M0, 0, False
     for t in range(steps):
@@ -238,7 +271,7 @@ def _simulate_bytes(B, steps):
                 wb = (K + b_rows) * K + (K + b_rows + 1) * K
                 b_rows += 1
             m += 1
-            if b_rows >= 32:
+            if b_rows >= window:
                 active, b_rows = False, 0
         else:
             proj_bytes += 8.0 * B * (2 * K + 2)               # U/V row gathers (+ W row)
@@ -250,6 +283,118 @@ def _simulate_bytes(B, steps):
                 wb = 2 * (K + b_rows) * K
         rot_bytes += 8.0 * B * (vb + wb)
     return proj_bytes, rot_bytes, all_bytes
+
+
+def make_inputs_5b(torch, dev, seed=0, m=M5B):
+    """Config 5b: A0 = X Y^T (m x 1024, rank 128) + N(0, 1e-3^2), rows l.Y^T
+    (SURVEY 8(d)); generated on the device in row chunks."""
+    g = torch.Generator(device=dev).manual_seed(5_000_011 + seed)
+    y = torch.randn((N5B, RANK5B), dtype=torch.float64, device=dev, generator=g)
+    a0 = torch.empty((1, m, N5B), dtype=torch.float64, device=dev)
+    step = 1 << 18
+    for c in range(0, m, step):
+        h = min(step, m - c)
+        x = torch.randn((h, RANK5B), dtype=torch.float64, device=dev, generator=g)
+        a0[0, c:c + h] = x @ y.T + 1e-3 * torch.randn((h, N5B), dtype=torch.float64, device=dev,
+                                                      generator=g)
+    rows = torch.randn((T5B, RANK5B), dtype=torch.float64, device=dev, generator=g) @ y.T
+    return a0, rows.contiguous()
+
+
+def run_cfg5b(torch, dev, lib, warm):
+    """Config 5b leg (k = 128): value = row appends/s with the final flush
+    (materialising U) inside the timed region; e2e through the public API
+    with pinned host rows; roofline of the deferred U rotation (FP64 DMMA)."""
+    import ctypes
+
+    from paper_2605_24514_b200 import BatchedSvdEngine
+
+    i64p = ctypes.POINTER(ctypes.c_int64)
+    a0, rows = make_inputs_5b(torch, dev)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    eng = BatchedSvdEngine(a0, K5B, m_cap=M5B + T5B + 1, k_cap=K5B)
+    eng.synchronize()
+    init_s = time.perf_counter() - t0
+    del a0
+    torch.cuda.empty_cache()
+    stream = torch.cuda.ExternalStream(eng.cuda_stream, device=dev)
+    for t in range(warm):
+        eng.row_append(rows[t:t + 1])
+    eng.flush()
+    eng.snapshot()
+    steps = T5B - warm
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    l0 = lib.isvd_launch_count()
+    e0.record(stream)
+    for t in range(warm, T5B):
+        eng.row_append(rows[t:t + 1])
+    eng.flush()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = lib.isvd_launch_count() - l0
+    ms = e0.elapsed_time(e1)
+    du, dv = eng.ortho_defect()
+    # per-phase breakdown of the same ticks
+    eng.restore()
+    lib.isvd_engine_set_timing(eng._h.h, 1)
+    for t in range(warm, T5B):
+        eng.row_append(rows[t:t + 1])
+    eng.flush()
+    ph = np.zeros(10)
+    nt3 = np.zeros(3, dtype=np.int64)
+    lib.isvd_engine_phase_times(eng._h.h, ph.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                nt3.ctypes.data_as(i64p))
+    lib.isvd_engine_set_timing(eng._h.h, 0)
+    # end to end: pinned host rows, per-step D2H of the scalars
+    h_rows = torch.empty((T5B, N5B), dtype=torch.float64, pin_memory=True)
+    h_rows.copy_(rows)
+    hr = h_rows.numpy()
+    eng.restore()
+    eng.synchronize()
+    t0 = time.perf_counter()
+    for t in range(warm, T5B):
+        eng.row_append(hr[t:t + 1])
+        eng.scalars()
+    eng.flush()
+    eng.synchronize()
+    e2e_s = time.perf_counter() - t0
+    window = int(lib.isvd_engine_lazy_window(eng._h.h))
+    del eng
+    torch.cuda.empty_cache()
+    nrow = max(1, int(nt3[0]))
+    per = {name: float(ph[j] / nrow) for j, name in enumerate(("project", "core_svd", "rotate",
+                                                                "install"))}
+    flush_ms, flush_bytes = float(ph[8]), float(ph[9])
+    flush_flops = 2.0 * M5B * K5B * K5B
+    tick_ms = sum(per.values())
+    return {
+        "metric": "iSVD updates/sec (k=128)", "value": steps / (ms / 1e3), "unit": UNIT,
+        "steps": steps, "warmup": warm, "ms_per_step": ms / steps,
+        "config": {"workload": "cfg5b_tall", "m": M5B, "n": N5B, "rank": RANK5B, "k": K5B,
+                   "row_appends": T5B, "noise_sd": 1e-3, "parallelism": "1 GPU",
+                   "deferred_u_rows": window},
+        "gpu_launches": int(launches),
+        "e2e": {"value": steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": N5B * 8,
+                "d2h_bytes_per_step": 3 * 8, "steps": steps},
+        "roofline": {"kernel": "rotate U flush (K3, deferred, DMMA)", "bound": "tensor",
+                     "achieved": flush_flops / (flush_ms / 1e3) / 1e12 if flush_ms else None,
+                     "peak": DMMA_PEAK_TFS, "unit": "TFLOP/s",
+                     "frac": (flush_flops / (flush_ms / 1e3) / 1e12 / DMMA_PEAK_TFS)
+                     if flush_ms else None,
+                     "peak_kind": "measured FP64 DMMA (profiles/r01_fp64_peaks.txt)",
+                     "traffic": None,
+                     "hbm_gbs": flush_bytes / (flush_ms / 1e3) / 1e9 if flush_ms else None,
+                     "flops_per_launch": flush_flops, "bytes_per_launch": flush_bytes},
+        "phase_ms_per_tick": per,
+        "flush_ms": flush_ms,
+        "tick_busy_ms": tick_ms,
+        "ortho_defect": [float(du[0]), float(dv[0])],
+        "init_s": init_s,
+        "reference_hbm_ceiling_updates_per_s": 6553.3e9 / (8.0 * (2 * M5B * K5B + 2 * N5B * K5B
+                                                                    + 2 * N5B)),
+    }
 
 
 def run_gpu(args):
@@ -347,8 +492,9 @@ def run_gpu(args):
         kind: {name: float(ph[4 * i + j] / max(1, nt3[i]))
                for j, name in enumerate(("project", "core_svd", "rotate", "install"))}
         for i, kind in enumerate(("row_append", "rank_one"))}
-    proj_bytes, rot_bytes, _ = _simulate_bytes(B, diag_steps)
-    _, _, all_bytes = _simulate_bytes(B, steps)
+    window = int(lib.isvd_engine_lazy_window(eng._h.h))
+    proj_bytes, rot_bytes, _ = _simulate_bytes(B, diag_steps, window)
+    _, _, all_bytes = _simulate_bytes(B, steps, window)
     # ---------------- end-to-end through the public API with host buffers
     e2e_steps = min(steps, args.e2e_steps)
     nrow = (e2e_steps + 1) // 2
@@ -371,6 +517,11 @@ def run_gpu(args):
     h2d = (nrow * B * N0 * 8 + nr1 * B * 24) / max(1, e2e_steps)
     d2h = 3 * B * 8
     del eng
+    del a0, rows, ii, jj, dd
+    torch.cuda.empty_cache()
+    k128 = None
+    if world == 1 and not args.no_k128:
+        k128 = run_cfg5b(torch, dev, lib, warm)
 
     if rank == 0:
         peak, peak_kind = _peaks()
@@ -402,7 +553,7 @@ def run_gpu(args):
                        "events": steps, "event_mix": "alternating row append / rank-1",
                        "l2": "inputs larger than L2 (state ~2 GB/GPU touched per step)",
                        "parallelism": f"streams sharded over {world} GPU(s)",
-                       "deferred_u_rows": 32, "stream_groups": 4},
+                       "deferred_u_rows": window, "stream_groups": 4},
             "clocks": clock,
             "gpu_launches": int(launches),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
@@ -423,6 +574,8 @@ def run_gpu(args):
                             "init_s": init_s,
                             "serial_phase_ms_per_step": diag_ms / max(1, diag_steps)},
         }
+        if k128 is not None:
+            line["k128"] = k128
         if world == 1 and not args.no_cpu_baseline:
             v, cores, updates, secs = cpu_reference(args.cpu_streams, args.cpu_events)
             line["cpu_baseline"] = {
@@ -430,6 +583,12 @@ def run_gpu(args):
                 "sample": f"{args.cpu_streams} cfg5a streams x {args.cpu_events} events on "
                           f"{cores} processes (oracle/ numpy restatement, 1 BLAS thread each, "
                           f"init excluded)"}
+            if k128 is not None:
+                v5, c5, t5, s5 = cpu_reference_5b()
+                k128["cpu_baseline"] = {
+                    "value": v5, "unit": UNIT, "cores": c5, "kind": "port",
+                    "sample": f"{t5} full-size row appends through the oracle row-append "
+                              "kernel (numpy/BLAS, all host threads), engine vstack excluded"}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -447,6 +606,7 @@ def main():
     ap.add_argument("--cpu-streams", type=int, default=64)
     ap.add_argument("--cpu-events", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-k128", action="store_true", help="skip the config-5b (k=128) leg")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -66,6 +66,21 @@ static int check_device() {
     set_error("no CUDA device available (libisvd has no CPU fallback)");
     return ISVD_ENODEV;
   }
+  // Stream-ordered scratch (cudaMallocAsync) comes from the device's default
+  // pool; with the default release threshold (0) every synchronize hands the
+  // memory back to the driver and the next tick re-maps it (~0.1 ms per
+  // allocation on a synchronous per-step loop).  Keep it.
+  static bool pool_set = false;
+  if (!pool_set) {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+    pool_set = true;
+  }
   return ISVD_OK;
 }
 
