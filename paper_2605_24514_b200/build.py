@@ -22,7 +22,7 @@ LIB = PKG / "libisvd.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-         f"-I{ROOT / 'include'}", f"-I{CSRC}"]
+         f"-I{ROOT / 'include'}", f"-I{CSRC}"] + os.environ.get("ISVD_NVCC_FLAGS", "").split()
 
 
 def _sources():

@@ -22,6 +22,7 @@
 //   5. the reference's output conventions (_kernels.pyx:94-109): descending
 //      sort, snap below 1e-12 sigma_0, dead left columns completed over
 //      e_0, e_1, ... in order.
+#include <cooperative_groups.h>
 #include "common.cuh"
 #include "core_svd.cuh"
 #include "../../include/isvd.h"
@@ -31,6 +32,9 @@ namespace isvd {
 namespace {
 
 constexpr int kN = kCoreMaxS;  // max core size
+constexpr int kArrowCluster = 8;      // CTAs per wide core when the batch is small
+constexpr int kClusterMaxBatch = 32;  // up to 256 CTAs
+__device__ unsigned long long g_arrow_counters[4];
 
 // Shared state sized by a compile-time bound on the core size (one
 // instantiation per bound keeps the per-CTA footprint small: ~4.6 KB at
@@ -81,15 +85,37 @@ __device__ __forceinline__ void apply_rots(double* col, int64_t stride, const SM
   }
 }
 
-template <int kN>
-__global__ void __launch_bounds__((kN + 31) / 32 * 32) arrow_svd_kernel(int n, const double* __restrict__ core,
+// WIDE (cores above 40, e.g. config 5b's 129): 512 threads, a parallel
+// no-deflation check, and one warp per root / per Loewner product / per
+// singular vector with the lanes over the poles (the one-thread-per-root
+// form leaves one latency-bound warp per SM sub-partition at B = 1).
+//
+// CL > 1 (WIDE, few cores): a thread-block cluster of CL CTAs per core.
+// Every CTA redoes the cheap O(n) set-up (load, sort, deflation --
+// deterministic, so identical everywhere); roots, Loewner products and
+// vectors are split over the CL * 16 warps, each result is stored into
+// every CTA's shared memory over DSMEM, and cluster barriers separate the
+// phases.  At B = 1 this spreads the 129-root core over CL SMs.
+template <int kN, bool WIDE, int CL>
+__global__ void __launch_bounds__(WIDE ? 512 : (kN + 31) / 32 * 32) arrow_svd_kernel(int n, const double* __restrict__ core,
                                                        int64_t core_stride, int ldcore,
                                                        double* __restrict__ uk,
                                                        double* __restrict__ vk, int64_t out_stride,
                                                        int ldo, double* __restrict__ sv,
                                                        int64_t sv_stride) {
   __shared__ ArrowSmem<kN> S;
-  const int b = blockIdx.x;
+  namespace cg = cooperative_groups;
+  const int crank = CL > 1 ? (int)cg::this_cluster().block_rank() : 0;
+  const int b = blockIdx.x / CL;
+  // cluster-wide barrier (release/acquire at cluster scope) or a CTA barrier
+  auto csync = [&]() {
+    if constexpr (CL > 1) cg::this_cluster().sync(); else __syncthreads();
+  };
+  // pointer to member `p` of S in CTA `rk` of the cluster (DSMEM)
+  auto remote = [&](auto* p, int rk) {
+    if constexpr (CL > 1) return cg::this_cluster().map_shared_rank(p, rk);
+    else return p;
+  };
   const int tid = threadIdx.x;
   const int r = n - 1;
   const double* K = core + b * core_stride;
@@ -129,8 +155,46 @@ __global__ void __launch_bounds__((kN + 31) / 32 * 32) arrow_svd_kernel(int n, c
   }
   __syncthreads();
 
-  // ---- deflation (sequential; O(n))
+  // ---- deflation.  WIDE: if no pole needs deflating (every |z| > tol, no
+  // pole pair closer than tol, only the rho column at zero) every pole is kept
+  // in sorted order -- filled in parallel; otherwise the sequential pass.
+  bool serial = true;
+  if (WIDE) {
+    const double tol = 8.0 * eps;
+    bool need = false;
+    for (int p = tid; p < n; p += blockDim.x) {
+      const int c = S.order[p];
+      const double dc = S.delta[c];
+      need |= fabs(S.z[c]) <= tol;
+      if (p > 0) {
+        const double dp = S.delta[S.order[p - 1]];
+        need |= dc <= tol || dc - dp <= tol;
+      }
+    }
+    serial = __syncthreads_or(need);
+    if (!serial) {
+      for (int p = tid; p < n; p += blockDim.x) {
+        const int c = S.order[p];
+        const double dc = p == 0 ? 0.0 : S.delta[c];
+        S.kcol[p] = c;
+        S.kd[p] = dc;
+        S.kz[p] = S.z[c];
+        if (p == 0) S.delta[c] = 0.0;
+      }
+      if (tid == 0) {
+        S.nkept = n;
+        S.ndefl = 0;
+        S.nrot = 0;
+      }
+    }
+  }
+#ifdef ISVD_ARROW_STATS
   if (tid == 0) {
+    atomicAdd(&g_arrow_counters[2], 1ull);
+    if (serial) atomicAdd(&g_arrow_counters[3], 1ull);
+  }
+#endif
+  if (serial && tid == 0) {
     const double tol = 8.0 * eps;  // all values scaled to <= 1
     int nk = 0, nd = 0, nr = 0;
     // zero group: poles <= tol, combined into the first one (column r)
@@ -187,10 +251,118 @@ __global__ void __launch_bounds__((kN + 31) / 32 * 32) arrow_svd_kernel(int n, c
     S.ndefl = nd;
     S.nrot = nr;
   }
-  __syncthreads();
+  csync();  // CL > 1: also guarantees every CTA of the cluster is resident before DSMEM use
   const int N = S.nkept, ND = S.ndefl;
 
-  // ---- roots: thread i solves for sigma_i in (kd[i], kd[i+1])
+  // ---- roots: thread (WIDE: warp) i solves for sigma_i in (kd[i], kd[i+1])
+  if (WIDE) {
+    const int lane = tid & 31, nwarp = (blockDim.x >> 5) * CL;
+    for (int i = crank * (blockDim.x >> 5) + (tid >> 5); i < N; i += nwarp) {
+      int o;
+      double lo, hi;
+      const double di = S.kd[i];
+      if (i < N - 1) {
+        const double dn = S.kd[i + 1];
+        const double sm = 0.5 * (di + dn);
+        const double mum = (sm - di) * (sm + di);
+        double f = 0.0;
+        for (int j = lane; j < N; j += 32) {
+          const double dj = S.kd[j];
+          f += S.kz[j] * S.kz[j] / ((dj - di) * (dj + di) - mum);
+        }
+        f = 1.0 + warp_sum(f);
+        if (f > 0.0) {
+          o = i; lo = 0.0; hi = mum;
+        } else {
+          o = i + 1; lo = (sm - dn) * (sm + dn); hi = 0.0;
+        }
+      } else {
+        o = i;
+        double zz = 0.0;
+        for (int j = lane; j < N; j += 32) zz += S.kz[j] * S.kz[j];
+        lo = 0.0;
+        hi = warp_sum(zz);
+      }
+      const double dorg = S.kd[o];
+      const double Di = (di - dorg) * (di + dorg);
+      const double Dn = (i < N - 1) ? (S.kd[i + 1] - dorg) * (S.kd[i + 1] + dorg) : 0.0;
+      double x = 0.5 * (lo + hi);
+      int iters = 0;
+      for (int it = 0; it < 80; ++it) {
+        ++iters;
+        double psi = 0.0, dpsi = 0.0, phi = 0.0, dphi = 0.0, aps = 0.0;
+        for (int j = lane; j < N; j += 32) {
+          const double dj = S.kd[j];
+          const double t = frcp((dj - dorg) * (dj + dorg) - x);
+          const double w = S.kz[j] * S.kz[j] * t;
+          if (j <= i) {
+            psi += w;
+            dpsi += w * t;
+          } else {
+            phi += w;
+            dphi += w * t;
+          }
+          aps += fabs(w);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          psi += __shfl_xor_sync(0xffffffffu, psi, off);
+          dpsi += __shfl_xor_sync(0xffffffffu, dpsi, off);
+          phi += __shfl_xor_sync(0xffffffffu, phi, off);
+          dphi += __shfl_xor_sync(0xffffffffu, dphi, off);
+          aps += __shfl_xor_sync(0xffffffffu, aps, off);
+        }
+        // identical in every lane from here on (xor-reduced inputs)
+        const double g = 1.0 + psi + phi;
+        if (g < 0.0) lo = x; else hi = x;
+        if (fabs(g) <= 4.0 * eps * (1.0 + aps) * N || !(g == g)) break;
+        const double pi_ = Di - x;
+        const double b1 = dpsi * pi_ * pi_;
+        const double a1 = psi - b1 / pi_;
+        double xn;
+        if (i < N - 1) {
+          const double qn = Dn - x;
+          const double b2 = dphi * qn * qn;
+          const double a2 = phi - b2 / qn;
+          const double A = 1.0 + a1 + a2;
+          const double Dl = Dn - Di;
+          const double B = A * Dl + b1 + b2, C = b1 * Dl;
+          const double disc = B * B - 4.0 * A * C;
+          xn = 0.5 * (lo + hi);
+          if (disc >= 0.0) {
+            const double q = -0.5 * (B + copysign(sqrt(disc), B));
+            const double p1 = (A != 0.0) ? q / A : -1e300;
+            const double p2 = (q != 0.0) ? C / q : -1e300;
+            const double x1 = Di - p1, x2 = Di - p2;
+            if (x1 > lo && x1 < hi) xn = x1;
+            else if (x2 > lo && x2 < hi) xn = x2;
+          }
+        } else {
+          const double A = 1.0 + a1 + phi;
+          xn = (A > 0.0) ? Di + b1 / A : 0.5 * (lo + hi);
+          if (!(xn > lo && xn < hi)) xn = 0.5 * (lo + hi);
+        }
+        if (fabs(xn - x) <= 2.0 * eps * fmax(fabs(xn), 1e-300) ||
+            hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi))) {
+          x = xn;
+          break;
+        }
+        x = xn;
+      }
+      if (lane < CL) {
+        auto* R = remote(&S, lane);
+        R->org[i] = o;
+        R->mu[i] = x;
+        R->sig[ND + i] = sqrt(dorg * dorg + x);
+      }
+      if (lane == 0) {
+#ifdef ISVD_ARROW_STATS
+        atomicAdd(&g_arrow_counters[0], 1ull);
+        atomicAdd(&g_arrow_counters[1], (unsigned long long)iters);
+#endif
+      }
+    }
+  } else
   for (int i = tid; i < N; i += blockDim.x) {
     int o;
     double lo, hi;
@@ -278,9 +450,28 @@ __global__ void __launch_bounds__((kN + 31) / 32 * 32) arrow_svd_kernel(int n, c
   }
   // deflated singular values (unscaled positions 0..ND-1)
   for (int k = tid; k < ND; k += blockDim.x) S.sig[k] = S.dzero[k] ? 0.0 : S.delta[S.dcol[k]];
-  __syncthreads();
+  csync();
 
   // ---- Loewner: zhat_j^2 = prod_k (sigma_k^2 - d_j^2) / prod_{k != j} (d_k^2 - d_j^2)
+  if (WIDE) {
+    const int lane = tid & 31, nwarp = (blockDim.x >> 5) * CL;
+    for (int j = crank * (blockDim.x >> 5) + (tid >> 5); j < N; j += nwarp) {
+      const double dj = S.kd[j];
+      auto sdiff = [&](int k) {
+        const double dk = S.kd[S.org[k]];
+        return S.mu[k] - (dj - dk) * (dj + dk);
+      };
+      double acc = 1.0;
+      for (int k = lane; k < N - 1; k += 32) {
+        const double dk = k < j ? S.kd[k] : S.kd[k + 1];
+        acc *= sdiff(k) / ((dk - dj) * (dk + dj));
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc *= __shfl_xor_sync(0xffffffffu, acc, off);
+      acc *= sdiff(N - 1);
+      if (lane < CL) remote(&S, lane)->zhat[j] = copysign(sqrt(fmax(acc, 0.0)), S.kz[j]);
+    }
+  } else
   for (int j = tid; j < N; j += blockDim.x) {
     const double dj = S.kd[j];
     auto sdiff = [&](int k) {  // sigma_k^2 - d_j^2, accurate
@@ -302,14 +493,42 @@ __global__ void __launch_bounds__((kN + 31) / 32 * 32) arrow_svd_kernel(int n, c
     }
     S.pos[t] = rank;
   }
-  __syncthreads();
-  const double s0 = S.sig[0] > 0.0 ? 0.0 : 0.0;  // placeholder (max computed below)
-  (void)s0;
+  csync();
   double smax = 0.0;
   for (int t = 0; t < n; ++t) smax = fmax(smax, S.sig[t]);
 
   // ---- vectors, written straight into their sorted columns
-  if (ND == 0 && S.nrot == 0) {
+  if (WIDE && ND == 0 && S.nrot == 0) {
+    const int lane = tid & 31, nwarp = (blockDim.x >> 5) * CL;
+    for (int t = crank * (blockDim.x >> 5) + (tid >> 5); t < n; t += nwarp) {
+      const int pc = S.pos[t];
+      const double dorg = S.kd[S.org[t]];
+      const double mu = S.mu[t];
+      double nv = 0.0, nu = 0.0;
+      for (int j = lane; j < N; j += 32) {
+        const double dj = S.kd[j];
+        const double vj = S.zhat[j] * frcp((dj - dorg) * (dj + dorg) - mu);
+        nv = fma(vj, vj, nv);
+        nu = fma(dj * vj, dj * vj, nu);
+      }
+      nv = warp_sum(nv);
+      nu = 1.0 + warp_sum(nu);  // the z-row entry of u is -1
+      const double iv = rsqrt(nv), iu = rsqrt(nu);
+      const double sg = S.sig[t];
+      const bool dead = !(sg > 0.0) || sg < kZeroSvRtol * smax;
+      for (int j = lane; j < N; j += 32) {
+        const double dj = S.kd[j];
+        const double vj = S.zhat[j] * frcp((dj - dorg) * (dj + dorg) - mu);
+        const int row = S.kcol[j];
+        V[row * ldo + pc] = vj * iv;
+        if (row != r) U[row * ldo + pc] = dead ? 0.0 : dj * vj * iu;
+      }
+      if (lane == 0) {
+        U[r * ldo + pc] = dead ? 0.0 : -iu;
+        SV[pc] = dead ? 0.0 : sg * scale;
+      }
+    }
+  } else if (ND == 0 && S.nrot == 0) {
     // common case (no deflation): every row of both columns is written once
     for (int t = tid; t < n; t += blockDim.x) {
       const int pc = S.pos[t];
@@ -337,7 +556,7 @@ __global__ void __launch_bounds__((kN + 31) / 32 * 32) arrow_svd_kernel(int n, c
       SV[pc] = dead ? 0.0 : sg * scale;
     }
   } else
-  for (int t = tid; t < n; t += blockDim.x) {
+  for (int t = crank * blockDim.x + tid; t < n; t += blockDim.x * CL) {
     const int pc = S.pos[t];
     double* vcol = V + pc;
     double* ucol = U + pc;
@@ -382,7 +601,8 @@ __global__ void __launch_bounds__((kN + 31) / 32 * 32) arrow_svd_kernel(int n, c
     }
     SV[pc] = dead ? 0.0 : sg * scale;
   }
-  __syncthreads();
+  csync();  // every column of U / V / SV written (global, cluster scope)
+  if (crank != 0) return;
 
   // ---- dead-column completion over e_0, e_1, ... (_kernels.pyx:62-79)
   bool mine_dead = false;
@@ -424,6 +644,17 @@ __global__ void __launch_bounds__((kN + 31) / 32 * 32) arrow_svd_kernel(int n, c
 
 }  // namespace
 
+int read_arrow_counters(int64_t* out4, int reset) {
+  unsigned long long h[4];
+  ISVD_CUDA(cudaMemcpyFromSymbol(h, g_arrow_counters, sizeof(h)));
+  for (int i = 0; i < 4; ++i) out4[i] = (int64_t)h[i];
+  if (reset) {
+    unsigned long long z[4] = {0, 0, 0, 0};
+    ISVD_CUDA(cudaMemcpyToSymbol(g_arrow_counters, z, sizeof(z)));
+  }
+  return ISVD_OK;
+}
+
 int launch_arrow_svd(int batch, int s, const double* core, int64_t core_stride, int ldcore,
                      double* uk, double* vk, int64_t out_stride, int ldo, double* sv,
                      int64_t sv_stride, cudaStream_t st) {
@@ -433,18 +664,44 @@ int launch_arrow_svd(int batch, int s, const double* core, int64_t core_stride, 
   }
   if (batch == 0) return ISVD_OK;
   const int threads = round_up(s, 32);
-  if (s <= 40)
-    arrow_svd_kernel<40><<<batch, threads, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
-                                                    out_stride, ldo, sv, sv_stride);
-  else if (s <= 72)
-    arrow_svd_kernel<72><<<batch, threads, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
-                                                    out_stride, ldo, sv, sv_stride);
-  else if (s <= 136)
-    arrow_svd_kernel<136><<<batch, threads, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
-                                                     out_stride, ldo, sv, sv_stride);
-  else
-    arrow_svd_kernel<kN><<<batch, threads, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
-                                                    out_stride, ldo, sv, sv_stride);
+  if (s <= 40) {
+    arrow_svd_kernel<40, false, 1><<<batch, threads, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
+                                                              out_stride, ldo, sv, sv_stride);
+  } else if (batch <= kClusterMaxBatch) {
+    // few wide cores (config 5b: one 129 core per tick): a cluster per core
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(batch * kArrowCluster);
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kArrowCluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e;
+    if (s <= 72)
+      e = cudaLaunchKernelEx(&cfg, arrow_svd_kernel<72, true, kArrowCluster>, s, core, core_stride,
+                             ldcore, uk, vk, out_stride, ldo, sv, sv_stride);
+    else if (s <= 136)
+      e = cudaLaunchKernelEx(&cfg, arrow_svd_kernel<136, true, kArrowCluster>, s, core,
+                             core_stride, ldcore, uk, vk, out_stride, ldo, sv, sv_stride);
+    else
+      e = cudaLaunchKernelEx(&cfg, arrow_svd_kernel<kN, true, kArrowCluster>, s, core, core_stride,
+                             ldcore, uk, vk, out_stride, ldo, sv, sv_stride);
+    ISVD_CUDA(e);
+  } else if (s <= 72) {
+    arrow_svd_kernel<72, true, 1><<<batch, 512, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
+                                                         out_stride, ldo, sv, sv_stride);
+  } else if (s <= 136) {
+    arrow_svd_kernel<136, true, 1><<<batch, 512, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
+                                                          out_stride, ldo, sv, sv_stride);
+  } else {
+    arrow_svd_kernel<kN, true, 1><<<batch, 512, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
+                                                         out_stride, ldo, sv, sv_stride);
+  }
   ISVD_LAUNCHED();
   return ISVD_OK;
 }

@@ -478,12 +478,12 @@ __global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32_kernel(
 int read_debug_counters(int64_t* out, int reset) {
   unsigned long long h[8];
   ISVD_CUDA(cudaMemcpyFromSymbol(h, g_debug_counters, sizeof(h)));
-  for (int i = 0; i < 8; ++i) out[i] = (int64_t)h[i];
+  for (int i = 0; i < 2; ++i) out[i] = (int64_t)h[i];
   if (reset) {
     unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     ISVD_CUDA(cudaMemcpyToSymbol(g_debug_counters, z, sizeof(z)));
   }
-  return ISVD_OK;
+  return read_arrow_counters(out + 2, reset);
 }
 
 size_t core_svd_smem_bytes(int s, bool v_in_smem) {

@@ -9,6 +9,9 @@ constexpr int kSmemMaxS = 112;   // G and V both in shared memory up to here
 
 size_t core_svd_smem_bytes(int s, bool v_in_smem);
 int read_debug_counters(int64_t* out, int reset);
+// [0] secular roots solved, [1] their iterations, [2] cores, [3] cores that
+// took the sequential deflation pass (arrow_svd.cu)
+int read_arrow_counters(int64_t* out4, int reset);
 
 // Batched core SVD.  core[b] is s x s row-major at core + b*core_stride with
 // row pitch ldcore.  Outputs uk[b], vk[b] (row-major s x s, pitch ldo, the

@@ -206,6 +206,7 @@ __global__ void __launch_bounds__(256) proj_split_z_kernel(
   const double* pb = part + (int64_t)b * S * (r + 1);
   for (int l = threadIdx.x; l < r; l += blockDim.x) {
     double v = 0.0;
+#pragma unroll 8
     for (int t = 0; t < S; ++t) v += pb[(int64_t)t * (r + 1) + l];
     p[l] = v;
   }
@@ -242,6 +243,7 @@ __global__ void proj_split_core_kernel(int r, int S, const double* __restrict__ 
   const double* pb = part + (int64_t)b * S * (r + 1);
   for (int l = threadIdx.x; l <= r; l += blockDim.x) {
     double v = 0.0;
+#pragma unroll 8
     for (int t = 0; t < S; ++t) v += pb[(int64_t)t * (r + 1) + l];
     if (l < r) p[l] = v; else sc[0] = v;
   }
@@ -256,17 +258,20 @@ __global__ void proj_split_core_kernel(int r, int S, const double* __restrict__ 
   const int P = r + 1;
   double* Kb = core + b * core_stride;
   const double* sb = s + (int64_t)b * lds;
-  for (int idx = threadIdx.x; idx < P * P; idx += blockDim.x) {
-    const int i = idx / P, j = idx % P;
-    double v = 0.0;
-    if (i < r) {
-      if (i == j) v = sb[i];
-    } else {
-      v = (j < r) ? p[j] : (fresh ? rho : 0.0);
+  // rows i = blockIdx.y + k * gridDim.y of the core; row r on block 0
+  for (int i = blockIdx.y; i < P; i += gridDim.y) {
+    const double si = i < r ? sb[i] : 0.0;
+    for (int j = threadIdx.x; j < P; j += blockDim.x) {
+      double v = 0.0;
+      if (i < r) {
+        if (i == j) v = si;
+      } else {
+        v = (j < r) ? p[j] : (fresh ? rho : 0.0);
+      }
+      Kb[i * ldcore + j] = v;
     }
-    Kb[i * ldcore + j] = v;
   }
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && blockIdx.y == 0) {
     inj_scale[b] = fresh ? 1.0 / rho : 0.0;
     rho_out[b] = rho;
     xnorm_out[b] = sqrt(xnorm2);
@@ -587,6 +592,10 @@ __global__ void complete_zero_kernel(int w, const double* __restrict__ s, int ld
   __shared__ double red[32];
   const int b = blockIdx.x;
   const double* sb = s + (int64_t)b * lds;
+  // common case: no zero sigma -- one parallel scan instead of w serial loads
+  bool any_zero = false;
+  for (int t = threadIdx.x; t < w; t += blockDim.x) any_zero |= sb[t] == 0.0;
+  if (!__syncthreads_or(any_zero)) return;
   for (int t = 0; t < w; ++t) {
     if (sb[t] != 0.0) continue;
     for (int side = 0; side < 2; ++side) {
@@ -761,7 +770,7 @@ int launch_project_append(int batch, int rows, int r, Mat F, const double* x, in
     proj_split_z_kernel<<<dim3(S, batch), 256, 0, st>>>(rows, r, rps, F, x, x_stride, part, z,
                                                          z_stride, zpart);
     ISVD_LAUNCHED();
-    proj_split_core_kernel<<<batch, 256, 0, st>>>(r, S, part, zpart, s, lds, tol, core,
+    proj_split_core_kernel<<<dim3(batch, std::min(r + 1, 16)), 256, 0, st>>>(r, S, part, zpart, s, lds, tol, core,
                                                    core_stride, ldcore, inj_scale, rho_out,
                                                    xnorm_out, N);
     ISVD_LAUNCHED();
