@@ -351,6 +351,8 @@ __global__ void __launch_bounds__(kRotWarps * 32, 1)
   const double* Q = J.Q + b * J.q_stride;
   const bool has_last = (J.z != nullptr) || J.new_row;
 
+  // independent L2 loads in flight (the permuted gather is latency-bound)
+#pragma unroll 8
   for (int idx = threadIdx.x; idx < KQ * NT * 32; idx += blockDim.x) {
     int ln = idx & 31, nn = (idx >> 5) % NT, kk = (idx >> 5) / NT;
     int g = ln >> 2, q = ln & 3;
