@@ -87,6 +87,30 @@ int isvd_engine_create(isvd_engine** out, int batch, int m, int n, int k,
                        int k_cap, void* stream);
 int isvd_engine_destroy(isvd_engine* e);
 
+/* Row sharding of one tall stream over ranks (BASELINE config 5b, SURVEY.md
+ * 8(e); north star: "U is row-sharded, with an NCCL allreduce of the
+ * k-length projections and k x k Gram blocks").  Call after create (B = 1,
+ * m = this rank's rows) and before init.  This rank holds global rows
+ * [row0, row0 + m) of U and of the tracked matrix; the rank with
+ * owns_appends = 1 (the last shard) also stores every appended row.  s, V
+ * and the deferred-window W are replicated and updated identically on every
+ * rank, so a row append needs no communication; `fn` is called (in the same
+ * order on every rank) to sum `count` doubles of a device buffer in place
+ * across ranks, ordered after the work already issued on `stream` and before
+ * the work issued after it returns:
+ *   init / refresh   n x n Gram, two w x w CholeskyQR Grams, ||A||^2
+ *   column append    the projection U^T y (+ ||y||^2), then ||z||^2
+ *   rank-1 update    the (owner's) row U[i, :] and A[i, j]
+ *   metrics / signs  U Grams (k x k), ||A - U S V^T||^2, column-max packets
+ * Observation calls (factors, metrics, set_reference, flush) are therefore
+ * collective in this mode.  Not available: eager U rotation (set_lazy(0)),
+ * the device oracle on the tracked matrix. */
+typedef int (*isvd_allreduce_fn)(void* ctx, double* buf, int64_t count, void* stream);
+int isvd_engine_set_shard(isvd_engine* e, int rank, int world, int64_t row0, int m_global,
+                          int owns_appends, isvd_allreduce_fn fn, void* ctx);
+/* row0, local rows, global rows (m_local = m_global when not sharded). */
+int isvd_engine_shard_info(const isvd_engine* e, int64_t* row0, int* m_local, int* m_global);
+
 /* Initialise from a0 (B x m x n, row-major per stream): copies the tracked
  * matrix, N0 = sum a0^2, factors = truncated_svd(a0, k) on the device
  * (engine.py:87-89, linalg.py:84-109).  Non-finite entries -> ISVD_EINVAL. */

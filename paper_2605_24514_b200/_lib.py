@@ -62,6 +62,9 @@ SIGNATURES = {
     "isvd_engine_set_timing": (C.c_int, [_vp, C.c_int]),
     "isvd_engine_set_append_solver": (C.c_int, [_vp, C.c_int]),
     "isvd_engine_set_lazy": (C.c_int, [_vp, C.c_int]),
+    "isvd_engine_set_shard": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int,
+                                        C.c_void_p, C.c_void_p]),
+    "isvd_engine_shard_info": (C.c_int, [_vp, _ip64, _ip, _ip]),
     "isvd_engine_set_lazy_window": (C.c_int, [_vp, C.c_int]),
     "isvd_engine_lazy_window": (C.c_int, [_vp]),
     "isvd_engine_set_reortho_threshold": (C.c_int, [_vp, C.c_double]),
@@ -123,6 +126,10 @@ def vptr(a) -> int:
     if isinstance(a, np.ndarray):
         return a.ctypes.data
     return a.data_ptr()
+
+
+# int (*)(void* ctx, double* buf, int64_t count, void* stream)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
 
 
 def launch_count() -> int:

@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include "tick.cuh"
+#include "shard.cuh"
 
 namespace isvd {
 
@@ -33,7 +34,9 @@ int dense_svd_run(int batch, int m, int n, const double* a, int64_t a_stride, in
 constexpr int64_t kGramMinElems = int64_t(1) << 24;
 constexpr int kGramMaxW = 160;  // Rayleigh-Ritz core = one core SVD (kCoreMaxS)
 bool use_gram_path(int m, int n, int w);
+// ar: row-sharded A (each rank holds m of the rows): the Grams are summed
+// across ranks, everything else is replicated or row-local.
 int gram_svd_run(int m, int n, const double* a, int lda, int w, Mat u, Mat v, double* s_w,
-                 double* s_all, cudaStream_t st);
+                 double* s_all, cudaStream_t st, const Allreducer* ar = nullptr);
 
 }  // namespace isvd

@@ -25,6 +25,7 @@
 #include "common.cuh"
 #include "core_svd.cuh"
 #include "dense_svd.cuh"
+#include "shard.cuh"
 #include "tall.cuh"
 #include "guard.cuh"
 #include "metrics.cuh"
@@ -120,6 +121,20 @@ using namespace isvd;
 
 struct isvd_engine {
   int B = 0, m = 0, n = 0, r = 0, k = 0;
+  // Row sharding (isvd_engine_set_shard): this rank holds global rows
+  // [row0, row0 + m) of U and A; m_glob counts all rows; the owner (last
+  // shard) also stores the appended rows.  Not sharded: m_glob == m.
+  bool sharded = false, owner = true;
+  int shard_rank = 0, shard_world = 1;
+  int64_t row0 = 0;
+  int m_glob = 0;
+  Allreducer ar;
+  const Allreducer* arp() const { return sharded ? &ar : nullptr; }
+  int allreduce(double* p, int64_t cnt) { return sharded ? ar(p, cnt) : ISVD_OK; }
+  int gm() const { return sharded ? m_glob : m; }
+  int64_t sh_i = 0, sh_j = 0;  // the rank-1 event being issued (sharded)
+  double sh_d = 0.0;
+  double* shv = nullptr;  // [kCoreMaxS + 2] cross-shard vector scratch
   int64_t step = 0;
   double tol = 1e-10;
   bool guard = false;
@@ -129,12 +144,12 @@ struct isvd_engine {
     if (!guard || r < 1) return ISVD_OK;
     ISVD_TRY(flush());
     std::vector<double> du(B), dv(B);
-    ISVD_TRY(reortho_defects(B, r, Um(), m, Vm(), n, du.data(), dv.data(), st));
+    ISVD_TRY(reortho_defects(B, r, Um(), m, Vm(), n, du.data(), dv.data(), st, arp()));
     bool any = false;
     for (int b = 0; b < B; ++b) any |= std::max(du[b], dv[b]) > reortho_threshold;
     if (!any) return ISVD_OK;
     ISVD_TRY(reortho_apply(B, r, Um(), m, Vm(), n, s, ld, core, uk, vk, cstride(), S(), sv, vscr,
-                           st));
+                           st, arp()));
     canonical = false;
     return ISVD_OK;
   }
@@ -188,7 +203,7 @@ struct isvd_engine {
   struct Snap {
     double *U = nullptr, *V = nullptr, *A = nullptr, *s = nullptr, *N = nullptr;
     size_t nu = 0, nv = 0, na = 0, ns = 0;
-    int m = 0, n = 0, r = 0, k = 0, m_cap = 0, n_cap = 0, ld = 0;
+    int m = 0, n = 0, r = 0, k = 0, m_cap = 0, n_cap = 0, ld = 0, m_glob = 0;
     int64_t step = 0;
     bool canonical = true, valid = false;
   } snap;
@@ -238,7 +253,7 @@ struct isvd_engine {
       cudaEventRecord(ev, st);
       flush_marks.push_back(ev);
     }
-    if (lazy_b > 0)
+    if (lazy_b > 0 && owner)  // appended rows live on the owner shard only
       ISVD_TRY(launch_copy_rows(B, lazy_b, r, W + (int64_t)r_base * ld, wstride(), ld,
                                 U + (int64_t)m_base * ld, ustride(), ld, st));
     lazy_active = false;
@@ -369,7 +384,20 @@ struct isvd_engine {
   int canonicalize() {
     ISVD_TRY(flush());
     if (canonical) return ISVD_OK;
-    ISVD_TRY(launch_canonicalize(B, r, Um(), m, Vm(), n, st));
+    if (sharded) {
+      // global argmax |U[:, c]| (lowest global row on ties): every rank posts
+      // its column maxima into its own slot, one sum-allreduce gathers them
+      double* pk = nullptr;
+      const int64_t cnt = (int64_t)shard_world * r * 3;
+      ISVD_CUDA(cudaMallocAsync((void**)&pk, sizeof(double) * std::max<int64_t>(cnt, 1), st));
+      int rc = launch_canon_shard_post(r, Um(), m, row0, shard_rank, shard_world, pk, st);
+      if (rc == ISVD_OK) rc = ar(pk, cnt);
+      if (rc == ISVD_OK) rc = launch_canon_shard_apply(r, Um(), m, Vm(), n, shard_world, pk, st);
+      cudaFreeAsync(pk, st);
+      ISVD_TRY(rc);
+    } else {
+      ISVD_TRY(launch_canonicalize(B, r, Um(), m, Vm(), n, st));
+    }
     canonical = true;
     return ISVD_OK;
   }
@@ -384,16 +412,22 @@ struct isvd_engine {
 
   // dense thin SVD of the tracked matrix into U, V, s (engine init/refresh)
   int factor_tracked() {
-    int w = std::min(k, std::min(m, n));
-    DenseSvdPlan P = dense_svd_plan(m, n, w);
-    ISVD_TRY(ensure_work((int64_t)B * P.x_elems(), (int64_t)B * P.j_elems(), 0, 0));
+    int w = std::min(k, std::min(gm(), n));
     int sweeps = 0;
     lazy_active = false;  // U is recomputed from A
     lazy_b = 0;
-    ISVD_TRY(dense_svd_run(B, m, n, A, astride(), n_cap, w, Um(), Vm(), s, ld, nullptr, 0, wx, wj,
-                           wflags, hflags.data(), st, &sweeps));
+    if (sharded) {
+      ISVD_TRY(gram_svd_run(m, n, A, n_cap, w, Um(), Vm(), s, nullptr, st, arp()));
+    } else {
+      DenseSvdPlan P = dense_svd_plan(m, n, w);
+      ISVD_TRY(ensure_work((int64_t)B * P.x_elems(), (int64_t)B * P.j_elems(), 0, 0));
+      ISVD_TRY(dense_svd_run(B, m, n, A, astride(), n_cap, w, Um(), Vm(), s, ld, nullptr, 0, wx, wj,
+                             wflags, hflags.data(), st, &sweeps));
+    }
     r = w;
-    ISVD_TRY(launch_complete_zero(B, r, s, ld, Um(), m, Vm(), n, st));
+    // (sharded: U's zero-sigma columns would need a distributed completion;
+    // only V -- replicated -- is completed here)
+    ISVD_TRY(launch_complete_zero(B, r, s, ld, Um(), sharded ? 0 : m, Vm(), n, st));
     canonical = false;
     ISVD_TRY(canonicalize());
     return ISVD_OK;
@@ -405,7 +439,7 @@ struct isvd_engine {
     dfree(z); dfree(inj); dfree(rho); dfree(xnorm); dfree(ev);
     dfree(ei); dfree(ej); dfree(ed); dfree(dflag); dfree(ref); dfree(W);
     dfree(wx); dfree(wj); dfree(wpart); dfree(wout); dfree(wflags);
-    dfree(snap.U); dfree(snap.V); dfree(snap.A); dfree(snap.s); dfree(snap.N);
+    dfree(snap.U); dfree(snap.V); dfree(snap.A); dfree(snap.s); dfree(snap.N); dfree(shv);
     for (auto g : gst) cudaStreamDestroy(g);
     for (auto ev : join_ev) cudaEventDestroy(ev);
     if (fork_ev) cudaEventDestroy(fork_ev);
@@ -437,6 +471,7 @@ int isvd_engine_create(isvd_engine** out, int batch, int m, int n, int k, double
   ISVD_TRY(check_device());
   auto* e = new isvd_engine();
   e->B = batch; e->m = m; e->n = n; e->k = k; e->tol = tol; e->guard = reortho_guard != 0;
+  e->m_glob = m;
   e->m_cap = std::max(m_cap, m + 1);
   e->n_cap = std::max(n_cap, n);
   int kc = std::max(std::max(k_cap, k), 1);
@@ -505,6 +540,40 @@ int isvd_engine_destroy(isvd_engine* e) {
 
 void* isvd_engine_stream(isvd_engine* e) { return e ? (void*)e->st : nullptr; }
 
+int isvd_engine_set_shard(isvd_engine* e, int rank, int world, int64_t row0, int m_global,
+                          int owns_appends, isvd_allreduce_fn fn, void* ctx) {
+  if (!e) { set_error("null engine"); return ISVD_EINVAL; }
+  if (e->initialized) { set_error("set_shard must precede init"); return ISVD_ESTATE; }
+  if (e->B != 1) { set_error("row sharding needs a single stream (B = 1)"); return ISVD_EINVAL; }
+  if (!fn || world < 1 || rank < 0 || rank >= world || row0 < 0 || m_global < e->m ||
+      row0 + e->m > m_global) {
+    set_error("set_shard: bad arguments");
+    return ISVD_EINVAL;
+  }
+  e->sharded = true;
+  e->shard_rank = rank;
+  e->shard_world = world;
+  e->row0 = row0;
+  e->m_glob = m_global;
+  e->owner = owns_appends != 0;
+  e->ar = Allreducer{fn, ctx, e->st};
+  if (!e->shv) ISVD_TRY(dalloc(&e->shv, (size_t)kCoreMaxS + 2));
+  e->lazy_mode = true;
+  e->lazy_rows = isvd_engine::lazy_window_for(m_global);
+  dfree(e->W);
+  ISVD_TRY(dalloc(&e->W, (size_t)e->B * e->wstride()));
+  ISVD_CUDA(cudaMemsetAsync(e->W, 0, sizeof(double) * e->B * e->wstride(), e->st));
+  return ISVD_OK;
+}
+
+int isvd_engine_shard_info(const isvd_engine* e, int64_t* row0, int* m_local, int* m_global) {
+  if (!e) { set_error("null engine"); return ISVD_EINVAL; }
+  if (row0) *row0 = e->row0;
+  if (m_local) *m_local = e->m;
+  if (m_global) *m_global = e->gm();
+  return ISVD_OK;
+}
+
 int isvd_engine_init(isvd_engine* e, const double* a0, int on_device) {
   if (!e || !a0) { set_error("null argument"); return ISVD_EINVAL; }
   const size_t cnt = (size_t)e->B * e->m * e->n;
@@ -526,6 +595,7 @@ int isvd_engine_init(isvd_engine* e, const double* a0, int on_device) {
                               e->n_cap, e->st));
   }
   ISVD_TRY(launch_sumsq(e->B, e->m, e->n, e->A, e->astride(), e->n_cap, e->N, e->st));
+  ISVD_TRY(e->allreduce(e->N, 1));
   ISVD_TRY(e->factor_tracked());
   e->step = 0;
   e->has_ref = false;
@@ -567,11 +637,14 @@ static int issue_append(isvd_engine* e, const Slice& sl, const double* xd, int l
   double* inj = e->inj + b0;
   const bool one = e->ngroups_active == 1;
   if (one) e->mark();
+  // sharded: only the owner stores an appended row; a column append projects
+  // on the row-sharded U (sums across shards)
+  double* Adst = (is_row && !e->owner) ? nullptr : e->A + b0 * e->astride();
   ISVD_TRY(launch_project_append(nb, len, r, F, xd + (int64_t)b0 * len, len,
                                  e->s + (int64_t)b0 * e->ld, e->ld, e->tol, core, cs, S, z,
-                                 e->zlen(), inj, e->rho + b0, e->xnorm + b0,
-                                 e->A + b0 * e->astride(), e->astride(), a_off, a_step, e->N + b0,
-                                 st));
+                                 e->zlen(), inj, e->rho + b0, e->xnorm + b0, Adst, e->astride(),
+                                 a_off, a_step, e->N + b0, st,
+                                 (e->sharded && !is_row) ? &e->ar : nullptr));
   if (one) e->mark();
   if (e->append_jacobi)
     ISVD_TRY(launch_core_svd(nb, r + 1, core, cs, S, uk, vk, cs, S, sv, S,
@@ -608,7 +681,7 @@ static int issue_append(isvd_engine* e, const Slice& sl, const double* xd, int l
                                   e->r_base_next + e->lazy_b_next, mat_at(e->Vm(), b0), n_new, st));
   else
     ISVD_TRY(launch_complete_zero(nb, keep, e->s + (int64_t)b0 * e->ld, e->ld, mat_at(e->Um(), b0),
-                                  m_new, mat_at(e->Vm(), b0), n_new, st));
+                                  e->sharded ? 0 : m_new, mat_at(e->Vm(), b0), n_new, st));
   return ISVD_OK;
 }
 
@@ -626,10 +699,22 @@ static int issue_rank_one(isvd_engine* e, const Slice& sl, const int64_t* di, co
   LazyBasis lz = e->lazy();
   lz.W = mat_at(lz.W, b0);
   if (one) e->mark();
-  ISVD_TRY(launch_rank1_build(nb, r, mat_at(e->Um(), b0), mat_at(e->Vm(), b0),
-                              e->s + (int64_t)b0 * e->ld, e->ld, di + b0, dj + b0, dd + b0, core,
-                              cs, S, e->A + b0 * e->astride(), e->astride(), e->n_cap, e->N + b0, lz,
-                              st));
+  if (e->sharded) {
+    // U[i, :] and A[i, j] from the shard owning row i, summed across shards
+    const int64_t il = e->sh_i - e->row0;
+    const bool mine = 0 <= il && il < e->m;
+    ISVD_CUDA(cudaMemsetAsync(e->shv, 0, sizeof(double) * (r + 1), st));
+    if (mine)
+      ISVD_TRY(launch_rank1_gather(r, e->Um(), il, e->sh_j, e->A, e->n_cap, lz, e->shv, st));
+    ISVD_TRY(e->allreduce(e->shv, r + 1));
+    ISVD_TRY(launch_rank1_vec_build(r, e->shv, e->Vm(), e->s, e->sh_j, e->sh_d, core, S, e->N,
+                                    mine ? e->A + il * e->n_cap + e->sh_j : nullptr, st));
+  } else {
+    ISVD_TRY(launch_rank1_build(nb, r, mat_at(e->Um(), b0), mat_at(e->Vm(), b0),
+                                e->s + (int64_t)b0 * e->ld, e->ld, di + b0, dj + b0, dd + b0, core,
+                                cs, S, e->A + b0 * e->astride(), e->astride(), e->n_cap, e->N + b0,
+                                lz, st));
+  }
   if (one) e->mark();
   ISVD_TRY(launch_core_svd(nb, r, core, cs, S, uk, vk, cs, S, sv, S,
                            e->vscr ? e->vscr + (int64_t)b0 * S * (S | 1) : nullptr, nullptr, st));
@@ -692,9 +777,13 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
     return ISVD_EINVAL;
   }
   // keep = min(r+1, k, m+1, n) (row) | min(r+1, k, m, n+1) (col): engine.py:122,136
-  const int keep = is_row ? std::min(std::min(e->r + 1, e->k), std::min(e->m + 1, e->n))
-                          : std::min(std::min(e->r + 1, e->k), std::min(e->m, e->n + 1));
-  ISVD_TRY(is_row ? e->grow_rows(e->m + 1) : e->grow_cols(e->n + 1));
+  const int keep = is_row ? std::min(std::min(e->r + 1, e->k), std::min(e->gm() + 1, e->n))
+                          : std::min(std::min(e->r + 1, e->k), std::min(e->gm(), e->n + 1));
+  if (is_row) {
+    if (e->owner) ISVD_TRY(e->grow_rows(e->m + 1));  // appended rows live on the owner
+  } else {
+    ISVD_TRY(e->grow_cols(e->n + 1));
+  }
   if (!is_row) ISVD_TRY(e->flush());  // the column append projects on, and rotates, U
   const int lazy_state = !(is_row && e->lazy_mode) ? 0 : (e->lazy_active ? 2 : 1);
   // window bookkeeping after this event (used by the completion check)
@@ -718,7 +807,12 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
   } else if (lazy_state == 2) {
     e->lazy_b += 1;
   }
-  if (is_row) e->m += 1; else e->n += 1;
+  if (is_row) {
+    if (e->owner) e->m += 1;
+    e->m_glob += 1;
+  } else {
+    e->n += 1;
+  }
   e->r = keep;
   if (e->lazy_active && e->lazy_b >= e->lazy_rows) ISVD_TRY(e->flush());
   ISVD_TRY(e->guard_step());
@@ -743,11 +837,24 @@ int isvd_engine_rank_one(isvd_engine* e, const int64_t* i, const int64_t* j, con
   if (!e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
   const int64_t *di = i, *dj = j;
   const double* dd = delta;
+  if (e->sharded) {
+    // the owner of row i is decided on the host
+    if (on_device) {
+      ISVD_CUDA(cudaMemcpyAsync(&e->sh_i, i, sizeof(int64_t), cudaMemcpyDeviceToHost, e->st));
+      ISVD_CUDA(cudaMemcpyAsync(&e->sh_j, j, sizeof(int64_t), cudaMemcpyDeviceToHost, e->st));
+      ISVD_CUDA(cudaMemcpyAsync(&e->sh_d, delta, sizeof(double), cudaMemcpyDeviceToHost, e->st));
+      ISVD_CUDA(cudaStreamSynchronize(e->st));
+    } else {
+      e->sh_i = i[0];
+      e->sh_j = j[0];
+      e->sh_d = delta[0];
+    }
+  }
   if (!on_device) {
     for (int b = 0; b < e->B; ++b) {
-      if (!(0 <= i[b] && i[b] < e->m && 0 <= j[b] && j[b] < e->n)) {
+      if (!(0 <= i[b] && i[b] < e->gm() && 0 <= j[b] && j[b] < e->n)) {
         set_error("index (" + std::to_string(i[b]) + ", " + std::to_string(j[b]) +
-                  ") out of bounds for shape (" + std::to_string(e->m) + ", " +
+                  ") out of bounds for shape (" + std::to_string(e->gm()) + ", " +
                   std::to_string(e->n) + ")");
         return ISVD_EINVAL;
       }
@@ -798,6 +905,7 @@ int isvd_engine_refresh(isvd_engine* e, int store_reference) {
   ISVD_TRY(e->grow_rank(e->k));
   ISVD_TRY(e->factor_tracked());
   ISVD_TRY(launch_sumsq(e->B, e->m, e->n, e->A, e->astride(), e->n_cap, e->N, e->st));
+  ISVD_TRY(e->allreduce(e->N, 1));
   if (store_reference) ISVD_TRY(copy_reference(e));
   ISVD_CUDA(cudaStreamSynchronize(e->st));
   return ISVD_OK;
@@ -823,7 +931,7 @@ int isvd_engine_shape(const isvd_engine* e, int* batch, int* m, int* n, int* ran
                       int64_t* step) {
   if (!e) { set_error("null engine"); return ISVD_EINVAL; }
   if (batch) *batch = e->B;
-  if (m) *m = e->m;
+  if (m) *m = e->gm();
   if (n) *n = e->n;
   if (rank) *rank = e->r;
   if (work_rank) *work_rank = e->k;
@@ -964,7 +1072,7 @@ int isvd_engine_snapshot(isvd_engine* e) {
   ISVD_CUDA(cudaMemcpyAsync(S.N, e->N, e->B * 8, cudaMemcpyDeviceToDevice, e->st));
   ISVD_CUDA(cudaMemcpyAsync(S.N + e->B, e->rho, e->B * 8, cudaMemcpyDeviceToDevice, e->st));
   ISVD_CUDA(cudaMemcpyAsync(S.N + 2 * e->B, e->xnorm, e->B * 8, cudaMemcpyDeviceToDevice, e->st));
-  S.m = e->m; S.n = e->n; S.r = e->r; S.k = e->k; S.step = e->step;
+  S.m = e->m; S.n = e->n; S.r = e->r; S.k = e->k; S.step = e->step; S.m_glob = e->m_glob;
   S.m_cap = e->m_cap; S.n_cap = e->n_cap; S.ld = e->ld; S.canonical = e->canonical;
   S.valid = true;
   ISVD_CUDA(cudaStreamSynchronize(e->st));
@@ -988,6 +1096,7 @@ int isvd_engine_restore(isvd_engine* e) {
   ISVD_CUDA(cudaMemcpyAsync(e->rho, S.N + e->B, e->B * 8, cudaMemcpyDeviceToDevice, e->st));
   ISVD_CUDA(cudaMemcpyAsync(e->xnorm, S.N + 2 * e->B, e->B * 8, cudaMemcpyDeviceToDevice, e->st));
   e->m = S.m; e->n = S.n; e->r = S.r; e->k = S.k; e->step = S.step; e->canonical = S.canonical;
+  e->m_glob = S.m_glob;
   ISVD_CUDA(cudaStreamSynchronize(e->st));
   return ISVD_OK;
 }
@@ -1000,6 +1109,7 @@ int isvd_engine_set_reortho_threshold(isvd_engine* e, double threshold) {
 
 int isvd_engine_set_lazy(isvd_engine* e, int on) {
   if (!e) { set_error("null engine"); return ISVD_EINVAL; }
+  if (e->sharded && !on) { set_error("eager U rotation is not available in shard mode"); return ISVD_EINVAL; }
   ISVD_TRY(e->flush());
   e->lazy_mode = on != 0;
   return ISVD_OK;
@@ -1085,15 +1195,18 @@ int isvd_engine_frob_error(isvd_engine* e, double* out) {
   ISVD_TRY(e->ensure_work(0, 0, (int64_t)e->B * frob_nblk(e->m), e->B));
   ISVD_TRY(launch_frob_error_sq(e->B, e->m, e->n, e->r, e->A, e->astride(), e->n_cap, e->Um(), e->s,
                                 e->ld, e->Vm(), e->wpart, e->wout, e->st));
+  ISVD_TRY(e->allreduce(e->wout, e->B));  // row shards: sum of the per-shard squares
   ISVD_CUDA(cudaMemcpyAsync(out, e->wout, sizeof(double) * e->B, cudaMemcpyDeviceToHost, e->st));
   ISVD_CUDA(cudaStreamSynchronize(e->st));
   for (int b = 0; b < e->B; ++b) out[b] = std::sqrt(out[b]);
   return ISVD_OK;
 }
 
-static int gram_defect(isvd_engine* e, Mat X, int rows, int w, double* host_out) {
+static int gram_defect(isvd_engine* e, Mat X, int rows, int w, double* host_out,
+                       bool row_sharded = false) {
   ISVD_TRY(e->ensure_work(0, 0, gram_part_elems(e->B, rows, w, w), (int64_t)e->B * w * w + e->B));
   ISVD_TRY(launch_gram(e->B, rows, w, w, X, X, e->wpart, e->wout, e->st));
+  if (row_sharded) ISVD_TRY(e->allreduce(e->wout, (int64_t)e->B * w * w));
   ISVD_TRY(launch_defect(e->B, w, e->wout, e->wout + (int64_t)e->B * w * w, e->st));
   ISVD_CUDA(cudaMemcpyAsync(host_out, e->wout + (int64_t)e->B * w * w, sizeof(double) * e->B,
                             cudaMemcpyDeviceToHost, e->st));
@@ -1104,7 +1217,7 @@ static int gram_defect(isvd_engine* e, Mat X, int rows, int w, double* host_out)
 int isvd_engine_ortho_defect(isvd_engine* e, double* du, double* dv) {
   if (!e || !e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
   ISVD_TRY(e->flush());
-  if (du) ISVD_TRY(gram_defect(e, e->Um(), e->m, e->r, du));
+  if (du) ISVD_TRY(gram_defect(e, e->Um(), e->m, e->r, du, e->sharded));
   if (dv) ISVD_TRY(gram_defect(e, e->Vm(), e->n, e->r, dv));
   return ISVD_OK;
 }
@@ -1139,8 +1252,8 @@ int isvd_engine_angle(isvd_engine* e, int which, const double* q, int q_cols, in
   }
   int rc = ISVD_OK;
   std::vector<double> d1(B), d2(B);
-  rc = gram_defect(e, e->Um(), m, r, d1.data());
-  if (rc == ISVD_OK) rc = gram_defect(e, Qm, m, r, d2.data());
+  rc = gram_defect(e, e->Um(), m, r, d1.data(), e->sharded);
+  if (rc == ISVD_OK) rc = gram_defect(e, Qm, m, r, d2.data(), e->sharded);
   if (rc == ISVD_OK) {
     for (int b = 0; b < B; ++b)
       if (d1[b] > 1e-6 || d2[b] > 1e-6) {
@@ -1154,6 +1267,7 @@ int isvd_engine_angle(isvd_engine* e, int which, const double* q, int q_cols, in
     int S = e->S();
     rc = e->ensure_work(0, 0, gram_part_elems(B, m, r, r), (int64_t)B * r * r + B);
     if (rc == ISVD_OK) rc = launch_gram(B, m, r, r, e->Um(), Qm, e->wpart, e->wout, e->st);
+    if (rc == ISVD_OK) rc = e->allreduce(e->wout, (int64_t)B * r * r);  // U^T Q over shards
     if (rc == ISVD_OK)
       rc = launch_core_svd(B, r, e->wout, (int64_t)r * r, r, e->uk, e->vk, e->cstride(), S, e->sv,
                            S, e->vscr, nullptr, e->st);
@@ -1252,6 +1366,7 @@ int isvd_dense_svd(int batch, int m, int n, const double* a, int w_keep, double*
 
 int isvd_engine_oracle(isvd_engine* e, int w_keep, double* s, double* u) {
   if (!e || !e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
+  if (e->sharded) { set_error("the device oracle needs the whole tracked matrix (not in shard mode)"); return ISVD_EINVAL; }
   return oracle_common(e->B, e->m, e->n, e->A, e->astride(), e->n_cap, w_keep, s, u, nullptr, e->st);
 }
 

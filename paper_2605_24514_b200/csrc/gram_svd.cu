@@ -62,7 +62,7 @@ bool use_gram_path(int m, int n, int w) {
 }
 
 int gram_svd_run(int m, int n, const double* a, int lda, int w, Mat u, Mat v, double* s_w,
-                 double* s_all, cudaStream_t st) {
+                 double* s_all, cudaStream_t st, const Allreducer* ar) {
   w = std::max(0, std::min(w, n));
   const int ldq = round_up(std::max(w, 1), 8);
   const int64_t np = gram_part_elems(1, m, n, n);
@@ -99,6 +99,7 @@ int gram_svd_run(int m, int n, const double* a, int lda, int w, Mat u, Mat v, do
   Mat Gm{G, 0, n};
   Mat Vqm{Vq, 0, ldq};
   T(launch_gram_tiles(1, m, n, n, Am, Am, 1, part, G, st));
+  if (ar) T((*ar)(G, (int64_t)n * n));  // A^T A over all row shards
   // eigenvectors of the PSD Gram = its right singular vectors (rotation side)
   T(dense_svd_run(1, n, n, G, (int64_t)n * n, n, w, Mat{nullptr, 0, 0}, Vqm, swi, ldq, lam, n, x,
                   jac, flags, hflags.data(), st, nullptr));
@@ -126,7 +127,7 @@ int gram_svd_run(int m, int n, const double* a, int lda, int w, Mat u, Mat v, do
     ISVD_LAUNCHED();
     // two CholeskyQR + core-SVD passes (CholeskyQR2): B = Q R, R = Ur S Vr^T
     for (int pass = 0; pass < 2 && rc == ISVD_OK; ++pass)
-      T(reortho_apply(1, we, u, m, v, n, s_w, S, core, uk, vk, (int64_t)S * S, S, sv, vscr, st));
+      T(reortho_apply(1, we, u, m, v, n, s_w, S, core, uk, vk, (int64_t)S * S, S, sv, vscr, st, ar));
   }
   if (rc == ISVD_OK) {
     gram_spectrum_kernel<<<1, 256, 0, st>>>(w, std::min(m, n), s_w, lam, s_all);

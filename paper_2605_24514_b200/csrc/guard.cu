@@ -73,7 +73,7 @@ __global__ void trsm_upper_kernel(int w, const double* __restrict__ R, double* _
 }  // namespace
 
 int reortho_defects(int batch, int w, Mat U, int m, Mat V, int n, double* host_du, double* host_dv,
-                    cudaStream_t st) {
+                    cudaStream_t st, const Allreducer* ar) {
   const int rows = m > n ? m : n;
   const size_t np = (size_t)gram_part_elems(batch, rows, w, w);
   double *part = nullptr, *G = nullptr, *d = nullptr;
@@ -81,6 +81,7 @@ int reortho_defects(int batch, int w, Mat U, int m, Mat V, int n, double* host_d
   ISVD_CUDA(cudaMallocAsync((void**)&G, sizeof(double) * batch * w * w, st));
   ISVD_CUDA(cudaMallocAsync((void**)&d, sizeof(double) * batch * 2, st));
   int rc = launch_gram(batch, m, w, w, U, U, part, G, st);
+  if (rc == ISVD_OK && ar) rc = (*ar)(G, (int64_t)batch * w * w);
   if (rc == ISVD_OK) rc = launch_defect(batch, w, G, d, st);
   if (rc == ISVD_OK) rc = launch_gram(batch, n, w, w, V, V, part, G, st);
   if (rc == ISVD_OK) rc = launch_defect(batch, w, G, d + batch, st);
@@ -97,7 +98,7 @@ int reortho_defects(int batch, int w, Mat U, int m, Mat V, int n, double* host_d
 
 int reortho_apply(int batch, int w, Mat U, int m, Mat V, int n, double* s, int lds, double* core,
                   double* uk, double* vk, int64_t cstride, int S, double* sv, double* vscr,
-                  cudaStream_t st) {
+                  cudaStream_t st, const Allreducer* ar) {
   if (w < 1) return ISVD_OK;
   const int rows = m > n ? m : n;
   const size_t np = (size_t)gram_part_elems(batch, rows, w, w);
@@ -106,6 +107,7 @@ int reortho_apply(int batch, int w, Mat U, int m, Mat V, int n, double* s, int l
   ISVD_CUDA(cudaMallocAsync((void**)&Ru, sizeof(double) * batch * w * w, st));
   ISVD_CUDA(cudaMallocAsync((void**)&Rv, sizeof(double) * batch * w * w, st));
   int rc = launch_gram(batch, m, w, w, U, U, part, Ru, st);
+  if (rc == ISVD_OK && ar) rc = (*ar)(Ru, (int64_t)batch * w * w);  // U^T U over all shards
   if (rc == ISVD_OK) rc = launch_gram(batch, n, w, w, V, V, part, Rv, st);
   if (rc == ISVD_OK) {
     chol_kernel<<<batch, 128, 0, st>>>(w, Ru);

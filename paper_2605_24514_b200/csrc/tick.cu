@@ -3,6 +3,7 @@
 #include "common.cuh"
 #include "core_svd.cuh"
 #include "tick.cuh"
+#include "shard.cuh"
 #include "../../include/isvd.h"
 
 namespace isvd {
@@ -197,17 +198,17 @@ __global__ void __launch_bounds__(256) proj_split_p_kernel(
 
 __global__ void __launch_bounds__(256) proj_split_z_kernel(
     int rows, int r, int rps, Mat F, const double* __restrict__ x, int64_t x_stride,
-    const double* __restrict__ part, double* __restrict__ z, int64_t z_stride,
+    const double* __restrict__ part, int np, double* __restrict__ z, int64_t z_stride,
     double* __restrict__ zpart) {
   __shared__ double p[kRMax];
   __shared__ double red[32];
   const int b = blockIdx.y, sp = blockIdx.x, S = gridDim.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const double* pb = part + (int64_t)b * S * (r + 1);
+  const double* pb = part + (int64_t)b * np * (r + 1);
   for (int l = threadIdx.x; l < r; l += blockDim.x) {
     double v = 0.0;
 #pragma unroll 8
-    for (int t = 0; t < S; ++t) v += pb[(int64_t)t * (r + 1) + l];
+    for (int t = 0; t < np; ++t) v += pb[(int64_t)t * (r + 1) + l];
     p[l] = v;
   }
   __syncthreads();
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(256) proj_split_z_kernel(
   if (threadIdx.x == 0) zpart[(int64_t)b * S + sp] = zt;
 }
 
-__global__ void proj_split_core_kernel(int r, int S, const double* __restrict__ part,
+__global__ void proj_split_core_kernel(int r, int S, int Sz, const double* __restrict__ part,
                                        const double* __restrict__ zpart,
                                        const double* __restrict__ s, int lds, double tol,
                                        double* __restrict__ core, int64_t core_stride, int ldcore,
@@ -249,7 +250,7 @@ __global__ void proj_split_core_kernel(int r, int S, const double* __restrict__ 
   }
   if (threadIdx.x == 0) {
     double v = 0.0;
-    for (int t = 0; t < S; ++t) v += zpart[(int64_t)b * S + t];
+    for (int t = 0; t < Sz; ++t) v += zpart[(int64_t)b * Sz + t];
     sc[1] = v;
   }
   __syncthreads();
@@ -276,6 +277,137 @@ __global__ void proj_split_core_kernel(int r, int S, const double* __restrict__ 
     rho_out[b] = rho;
     xnorm_out[b] = sqrt(xnorm2);
     N[b] += xnorm2;
+  }
+}
+
+// out[l] = sum_t part[t * cnt + l], fixed order (row-sharded reductions, B = 1)
+__global__ void split_reduce_kernel(int cnt, int np, const double* __restrict__ part,
+                                    double* __restrict__ out) {
+  for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < cnt; l += gridDim.x * blockDim.x) {
+    double v = 0.0;
+#pragma unroll 8
+    for (int t = 0; t < np; ++t) v += part[(int64_t)t * cnt + l];
+    out[l] = v;
+  }
+}
+
+// Row-sharded rank-1 update (B = 1).  gather: out[0:r] = U[i, :] (through the
+// deferred window, as rank1_build_kernel), out[r] = A[i, j] -- on the shard
+// owning row i, zeros elsewhere, then summed across shards.  vec_build: the
+// replicated core diag(s) + delta out[0:r] V[j, :]^T, N += 2 delta out[r] +
+// delta^2 (engine.py:162-166) and, on the owner, A[i, j] += delta.
+__global__ void rank1_gather_kernel(int r, Mat U, int64_t i, int64_t j, const double* __restrict__ A,
+                                    int lda, LazyBasis lz, double* __restrict__ out) {
+  __shared__ double ub[kRMax];
+  if (!lz.active) {
+    const double* ur = U.p + i * U.ld;
+    for (int l = threadIdx.x; l < r; l += blockDim.x) out[l] = ur[l];
+  } else if (i >= lz.m_base) {
+    const double* wr = lz.W.p + (lz.r_base + (i - lz.m_base)) * lz.W.ld;
+    for (int l = threadIdx.x; l < r; l += blockDim.x) out[l] = wr[l];
+  } else {
+    const double* ur = U.p + i * U.ld;
+    for (int c = threadIdx.x; c < lz.r_base; c += blockDim.x) ub[c] = ur[c];
+    __syncthreads();
+    for (int l = threadIdx.x; l < r; l += blockDim.x) {
+      double acc = 0.0;
+      for (int c = 0; c < lz.r_base; ++c) acc = fma(ub[c], lz.W.p[c * lz.W.ld + l], acc);
+      out[l] = acc;
+    }
+  }
+  if (threadIdx.x == 0) out[r] = A[i * lda + j];
+}
+
+__global__ void rank1_vec_build_kernel(int r, const double* __restrict__ vec, Mat V,
+                                       const double* __restrict__ s, int64_t j, double d,
+                                       double* __restrict__ core, int ldcore,
+                                       double* __restrict__ N, double* __restrict__ Aij) {
+  const double* vr = V.p + j * V.ld;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < r * r;
+       idx += gridDim.x * blockDim.x) {
+    const int p = idx / r, q = idx % r;
+    double v = d * vec[p] * vr[q];  // _kernels.pyx:209-213
+    if (p == q) v += s[p];
+    core[p * ldcore + q] = v;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const double old = vec[r];
+    N[0] += 2.0 * d * old + d * d;
+    if (Aij) *Aij = old + d;
+  }
+}
+
+// ---- K5 for tall / row-sharded factors: per row block, per column, the
+// first row of max |U[:, c]| (linalg.py:63-75: numpy argmax = first max);
+// blocks (and shards) combine by (larger |u|, then lower global row).
+__device__ __forceinline__ bool canon_better(double v1, double r1, double v2, double r2) {
+  return v1 > v2 || (v1 == v2 && r1 < r2);
+}
+
+__global__ void canon_partial_kernel(int w, Mat U, int m, int64_t row0, int rpb,
+                                     double* __restrict__ part) {
+  const int b = blockIdx.y, blk = blockIdx.x, nblk = gridDim.x;
+  const double* Ub = U.p + b * U.stride;
+  const int r0 = blk * rpb, r1 = min(m, r0 + rpb);
+  for (int c = threadIdx.x; c < w; c += blockDim.x) {
+    double best = -1.0, row = 0.0, sgn = 1.0;
+#pragma unroll 4
+    for (int i = r0; i < r1; ++i) {
+      const double v = Ub[(int64_t)i * U.ld + c];
+      if (fabs(v) > best) {
+        best = fabs(v);
+        row = (double)(row0 + i);
+        sgn = v < 0.0 ? -1.0 : 1.0;
+      }
+    }
+    double* o = part + (((int64_t)b * nblk + blk) * w + c) * 3;
+    o[0] = best;
+    o[1] = row;
+    o[2] = sgn;
+  }
+}
+
+// Combine np candidate triples per column.  slot >= 0: write the winner to
+// out slot `slot` (the cross-shard packet); slot < 0: write the sign flag.
+__global__ void canon_select_kernel(int w, int np, const double* __restrict__ part, int slot,
+                                    double* __restrict__ out) {
+  const int b = blockIdx.x;
+  for (int c = threadIdx.x; c < w; c += blockDim.x) {
+    double best = -2.0, row = 0.0, sgn = 1.0;
+    for (int t = 0; t < np; ++t) {
+      const double* q = part + (((int64_t)b * np + t) * w + c) * 3;
+      if (canon_better(q[0], q[1], best, row)) {
+        best = q[0];
+        row = q[1];
+        sgn = q[2];
+      }
+    }
+    if (slot >= 0) {
+      double* o = out + ((int64_t)slot * w + c) * 3;
+      o[0] = best;
+      o[1] = row;
+      o[2] = sgn;
+    } else {
+      out[(int64_t)b * w + c] = sgn;
+    }
+  }
+}
+
+__global__ void canon_flip_kernel(int w, const double* __restrict__ sgn, Mat U, int m, Mat V,
+                                  int n) {
+  const int b = blockIdx.y;
+  const double* fb = sgn + (int64_t)b * w;
+  const int64_t tu = (int64_t)m * w, tv = (int64_t)n * w;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tu + tv;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const bool onu = e < tu;
+    const int64_t k = onu ? e : e - tu;
+    const int c = (int)(k % w);
+    if (fb[c] < 0.0) {
+      double* p = onu ? U.p + b * U.stride + (k / w) * U.ld + c
+                      : V.p + b * V.stride + (k / w) * V.ld + c;
+      *p = -*p;
+    }
   }
 }
 
@@ -754,10 +886,41 @@ int launch_project_append(int batch, int rows, int r, Mat F, const double* x, in
                           const double* s, int lds, double tol, double* core, int64_t core_stride,
                           int ldcore, double* z, int64_t z_stride, double* inj_scale,
                           double* rho_out, double* xnorm_out, double* A, int64_t a_stride,
-                          int64_t a_off, int64_t a_step, double* N, cudaStream_t st) {
+                          int64_t a_off, int64_t a_step, double* N, cudaStream_t st,
+                          const Allreducer* ar) {
   if (r > kRMax) {
     set_error("factor width exceeds kernel limit");
     return ISVD_EINVAL;
+  }
+  if (ar) {
+    // row-sharded F (column append of a sharded stream, B = 1): p and
+    // ||y||^2 are summed across shards, then ||z||^2
+    const int S = std::max(1, std::min(ceil_div(std::max(rows, 1), kSplitRows), 296));
+    const int rps = std::max(1, ceil_div(rows, S));
+    double *part = nullptr, *zpart = nullptr, *vec = nullptr;
+    ISVD_CUDA(cudaMallocAsync((void**)&part, sizeof(double) * S * (r + 1), st));
+    ISVD_CUDA(cudaMallocAsync((void**)&zpart, sizeof(double) * S, st));
+    ISVD_CUDA(cudaMallocAsync((void**)&vec, sizeof(double) * (r + 2), st));
+    proj_split_p_kernel<<<dim3(S, 1), 256, 0, st>>>(rows, r, rps, F, x, x_stride, A, a_stride,
+                                                     a_off, a_step, part);
+    ISVD_LAUNCHED();
+    split_reduce_kernel<<<1, 256, 0, st>>>(r + 1, S, part, vec);
+    ISVD_LAUNCHED();
+    ISVD_TRY((*ar)(vec, r + 1));
+    proj_split_z_kernel<<<dim3(S, 1), 256, 0, st>>>(rows, r, rps, F, x, x_stride, vec, 1, z,
+                                                     z_stride, zpart);
+    ISVD_LAUNCHED();
+    split_reduce_kernel<<<1, 32, 0, st>>>(1, S, zpart, vec + r + 1);
+    ISVD_LAUNCHED();
+    ISVD_TRY((*ar)(vec + r + 1, 1));
+    proj_split_core_kernel<<<dim3(1, std::min(r + 1, 16)), 256, 0, st>>>(
+        r, 1, 1, vec, vec + r + 1, s, lds, tol, core, core_stride, ldcore, inj_scale, rho_out,
+        xnorm_out, N);
+    ISVD_LAUNCHED();
+    ISVD_CUDA(cudaFreeAsync(part, st));
+    ISVD_CUDA(cudaFreeAsync(zpart, st));
+    ISVD_CUDA(cudaFreeAsync(vec, st));
+    return ISVD_OK;
   }
   if (batch <= 32 && (int64_t)rows * r >= 16384) {
     // few streams, long factors: split the rows over CTAs (see proj_split_*)
@@ -769,10 +932,10 @@ int launch_project_append(int batch, int rows, int r, Mat F, const double* x, in
     proj_split_p_kernel<<<dim3(S, batch), 256, 0, st>>>(rows, r, rps, F, x, x_stride, A, a_stride,
                                                          a_off, a_step, part);
     ISVD_LAUNCHED();
-    proj_split_z_kernel<<<dim3(S, batch), 256, 0, st>>>(rows, r, rps, F, x, x_stride, part, z,
+    proj_split_z_kernel<<<dim3(S, batch), 256, 0, st>>>(rows, r, rps, F, x, x_stride, part, S, z,
                                                          z_stride, zpart);
     ISVD_LAUNCHED();
-    proj_split_core_kernel<<<dim3(batch, std::min(r + 1, 16)), 256, 0, st>>>(r, S, part, zpart, s, lds, tol, core,
+    proj_split_core_kernel<<<dim3(batch, std::min(r + 1, 16)), 256, 0, st>>>(r, S, S, part, zpart, s, lds, tol, core,
                                                    core_stride, ldcore, inj_scale, rho_out,
                                                    xnorm_out, N);
     ISVD_LAUNCHED();
@@ -798,6 +961,21 @@ int launch_project_append(int batch, int rows, int r, Mat F, const double* x, in
         rows, r, F, x, x_stride, s, lds, tol, core, core_stride, ldcore, z, z_stride, inj_scale,
         rho_out, xnorm_out, A, a_stride, a_off, a_step, N);
   }
+  ISVD_LAUNCHED();
+  return ISVD_OK;
+}
+
+int launch_rank1_gather(int r, Mat U, int64_t i, int64_t j, const double* A, int lda,
+                        LazyBasis lz, double* out, cudaStream_t st) {
+  rank1_gather_kernel<<<1, 128, 0, st>>>(r, U, i, j, A, lda, lz, out);
+  ISVD_LAUNCHED();
+  return ISVD_OK;
+}
+
+int launch_rank1_vec_build(int r, const double* vec, Mat V, const double* s, int64_t j, double d,
+                           double* core, int ldcore, double* N, double* Aij, cudaStream_t st) {
+  rank1_vec_build_kernel<<<std::max(1, std::min(ceil_div(r * r, 256), 64)), 256, 0, st>>>(
+      r, vec, V, s, j, d, core, ldcore, N, Aij);
   ISVD_LAUNCHED();
   return ISVD_OK;
 }
@@ -905,8 +1083,62 @@ int launch_complete_zero(int batch, int w, const double* s, int lds, Mat U, int 
   return ISVD_OK;
 }
 
+static int canon_blocks(int batch, int m) {
+  return std::max(1, std::min(ceil_div(std::max(m, 1), 1024), std::max(1, 1184 / std::max(batch, 1))));
+}
+
+int launch_canon_shard_post(int w, Mat U, int m, int64_t row0, int rank, int world, double* pk,
+                            cudaStream_t st) {
+  if (w == 0) return ISVD_OK;
+  const int nblk = canon_blocks(1, m);
+  const int rpb = ceil_div(std::max(m, 1), nblk);
+  double* part = nullptr;
+  ISVD_CUDA(cudaMemsetAsync(pk, 0, sizeof(double) * world * w * 3, st));
+  ISVD_CUDA(cudaMallocAsync((void**)&part, sizeof(double) * nblk * w * 3, st));
+  canon_partial_kernel<<<dim3(nblk, 1), 128, 0, st>>>(w, U, m, row0, rpb, part);
+  ISVD_LAUNCHED();
+  canon_select_kernel<<<1, 128, 0, st>>>(w, nblk, part, rank, pk);
+  ISVD_LAUNCHED();
+  ISVD_CUDA(cudaFreeAsync(part, st));
+  return ISVD_OK;
+}
+
+int launch_canon_shard_apply(int w, Mat U, int m, Mat V, int n, int world, const double* pk,
+                             cudaStream_t st) {
+  if (w == 0) return ISVD_OK;
+  double* sg = nullptr;
+  ISVD_CUDA(cudaMallocAsync((void**)&sg, sizeof(double) * w, st));
+  canon_select_kernel<<<1, 128, 0, st>>>(w, world, pk, -1, sg);
+  ISVD_LAUNCHED();
+  const int64_t tot = (int64_t)(m + n) * w;
+  const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((tot + 255) / 256, 4096));
+  canon_flip_kernel<<<dim3(gx, 1), 256, 0, st>>>(w, sg, U, m, V, n);
+  ISVD_LAUNCHED();
+  ISVD_CUDA(cudaFreeAsync(sg, st));
+  return ISVD_OK;
+}
+
 int launch_canonicalize(int batch, int w, Mat U, int m, Mat V, int n, cudaStream_t st) {
   if (batch == 0 || w == 0) return ISVD_OK;
+  if (batch <= 8 && (int64_t)m * w >= (1 << 22)) {
+    // few tall streams: row blocks over the whole GPU, then one select + flip
+    const int nblk = canon_blocks(batch, m);
+    const int rpb = ceil_div(m, nblk);
+    double *part = nullptr, *sg = nullptr;
+    ISVD_CUDA(cudaMallocAsync((void**)&part, sizeof(double) * batch * nblk * w * 3, st));
+    ISVD_CUDA(cudaMallocAsync((void**)&sg, sizeof(double) * batch * w, st));
+    canon_partial_kernel<<<dim3(nblk, batch), 128, 0, st>>>(w, U, m, 0, rpb, part);
+    ISVD_LAUNCHED();
+    canon_select_kernel<<<batch, 128, 0, st>>>(w, nblk, part, -1, sg);
+    ISVD_LAUNCHED();
+    const int64_t tot = (int64_t)(m + n) * w;
+    const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((tot + 255) / 256, 4096));
+    canon_flip_kernel<<<dim3(gx, batch), 256, 0, st>>>(w, sg, U, m, V, n);
+    ISVD_LAUNCHED();
+    ISVD_CUDA(cudaFreeAsync(part, st));
+    ISVD_CUDA(cudaFreeAsync(sg, st));
+    return ISVD_OK;
+  }
   canonicalize_kernel<<<batch, 256, 0, st>>>(w, U, m, V, n);
   ISVD_LAUNCHED();
   return ISVD_OK;

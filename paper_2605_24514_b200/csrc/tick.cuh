@@ -4,6 +4,8 @@
 
 namespace isvd {
 
+struct Allreducer;  // shard.cuh
+
 // Strided view of B per-stream matrices: X[b] = base + b*stride, row pitch ld.
 struct Mat {
   double* p;
@@ -19,7 +21,8 @@ int launch_project_append(int batch, int rows, int r, Mat F, const double* x, in
                           const double* s, int lds, double tol, double* core, int64_t core_stride,
                           int ldcore, double* z, int64_t z_stride, double* inj_scale,
                           double* rho_out, double* xnorm_out, double* A, int64_t a_stride,
-                          int64_t a_off, int64_t a_step, double* N, cudaStream_t st);
+                          int64_t a_off, int64_t a_step, double* N, cudaStream_t st,
+                          const struct Allreducer* ar = nullptr);
 
 // Deferred left basis: while active, the true U is
 // [Ub 0; 0 I] . W where Ub = the first m_base rows of the U buffer (width
@@ -29,6 +32,13 @@ struct LazyBasis {
   int m_base, r_base;
   Mat W;
 };
+
+// Row-sharded rank-1 pieces (B = 1, see tick.cu): gather U[i,:] / A[i,j] on
+// the owning shard into out (r + 1), then the replicated core from out.
+int launch_rank1_gather(int r, Mat U, int64_t i, int64_t j, const double* A, int lda,
+                        struct LazyBasis lz, double* out, cudaStream_t st);
+int launch_rank1_vec_build(int r, const double* vec, Mat V, const double* s, int64_t j, double d,
+                           double* core, int ldcore, double* N, double* Aij, cudaStream_t st);
 
 // K6: rank-1 core K = diag(s) + delta U[i,:]^T V[j,:] plus the tracked entry
 // update A[i,j] += delta and N += 2 delta a_old + delta^2 (engine.py:162-166).
@@ -63,6 +73,13 @@ int launch_complete_zero(int batch, int w, const double* s, int lds, Mat U, int 
 
 // linalg.py:63-75 -- sign canonicalisation of (U, V) per stream.
 int launch_canonicalize(int batch, int w, Mat U, int m, Mat V, int n, cudaStream_t st);
+// Row-sharded K5 (B = 1): post writes this shard's per-column candidates
+// (max |u|, global row, sign) into slot `rank` of pk (world x w x 3, zeroed
+// elsewhere); after a cross-shard sum, apply picks the winners and flips.
+int launch_canon_shard_post(int w, Mat U, int m, int64_t row0, int rank, int world, double* pk,
+                            cudaStream_t st);
+int launch_canon_shard_apply(int w, Mat U, int m, Mat V, int n, int world, const double* pk,
+                             cudaStream_t st);
 
 // Copy helpers.
 int launch_copy_rows(int batch, int rows, int cols, const double* src, int64_t src_stride,
