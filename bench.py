@@ -285,35 +285,56 @@ def _simulate_bytes(B, steps, window=32):
     return proj_bytes, rot_bytes, all_bytes
 
 
-def make_inputs_5b(torch, dev, seed=0, m=M5B):
-    """Config 5b: A0 = X Y^T (m x 1024, rank 128) + N(0, 1e-3^2), rows l.Y^T
-    (SURVEY 8(d)); generated on the device in row chunks."""
+def make_inputs_5b(torch, dev, seed=0, m=M5B, row0=0, rows=None):
+    """Config 5b: A0 = X Y^T (m x 1024, rank 128) + N(0, 1e-3^2), appended rows
+    l.Y^T.  Generated on the device in 2^18-row chunks, each
+    from its own seed, so a rank builds exactly its row block [row0, row0 +
+    rows) and every world size sees the same matrix."""
+    rows = m - row0 if rows is None else rows
+    chunk = 1 << 18
     g = torch.Generator(device=dev).manual_seed(5_000_011 + seed)
     y = torch.randn((N5B, RANK5B), dtype=torch.float64, device=dev, generator=g)
-    a0 = torch.empty((1, m, N5B), dtype=torch.float64, device=dev)
-    step = 1 << 18
-    for c in range(0, m, step):
-        h = min(step, m - c)
+    app = torch.randn((T5B, RANK5B), dtype=torch.float64, device=dev, generator=g) @ y.T
+    a0 = torch.empty((1, rows, N5B), dtype=torch.float64, device=dev)
+    for c0 in range(row0 // chunk * chunk, row0 + rows, chunk):
+        g.manual_seed(5_100_000 + 1000 * seed + c0 // chunk)
+        h = min(chunk, m - c0)
         x = torch.randn((h, RANK5B), dtype=torch.float64, device=dev, generator=g)
-        a0[0, c:c + h] = x @ y.T + 1e-3 * torch.randn((h, N5B), dtype=torch.float64, device=dev,
-                                                      generator=g)
-    rows = torch.randn((T5B, RANK5B), dtype=torch.float64, device=dev, generator=g) @ y.T
-    return a0, rows.contiguous()
+        blk = x @ y.T + 1e-3 * torch.randn((h, N5B), dtype=torch.float64, device=dev, generator=g)
+        lo, hi = max(row0, c0), min(row0 + rows, c0 + h)
+        a0[0, lo - row0:hi - row0] = blk[lo - c0:hi - c0]
+        del x, blk
+    return a0, app.contiguous()
 
 
-def run_cfg5b(torch, dev, lib, warm):
+def run_cfg5b(torch, dev, lib, warm, world=1, rank=0):
     """Config 5b leg (k = 128): value = row appends/s with the final flush
-    (materialising U) inside the timed region; e2e through the public API
-    with pinned host rows; roofline of the deferred U rotation (FP64 DMMA)."""
+    (materialising U) inside the timed region, max over ranks; e2e through the
+    public API with pinned host rows; roofline of the deferred U rotation
+    (FP64 DMMA).  N > 1: U and A row-sharded over the ranks
+    (ShardedSvdEngine, NCCL allreduce of the Grams at init)."""
     import ctypes
 
     from paper_2605_24514_b200 import BatchedSvdEngine
+    from paper_2605_24514_b200.sharded import ShardedSvdEngine, shard_rows
+    from paper_2605_24514_b200.sharding import max_over_ranks
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
 
     i64p = ctypes.POINTER(ctypes.c_int64)
-    a0, rows = make_inputs_5b(torch, dev)
-    torch.cuda.synchronize()
+    r0, ml = shard_rows(M5B, world, rank)
+    a0, rows = make_inputs_5b(torch, dev, row0=r0, rows=ml)
+    barrier()
     t0 = time.perf_counter()
-    eng = BatchedSvdEngine(a0, K5B, m_cap=M5B + T5B + 1, k_cap=K5B)
+    if world == 1:
+        eng = BatchedSvdEngine(a0, K5B, m_cap=M5B + T5B + 1, k_cap=K5B)
+    else:
+        eng = ShardedSvdEngine(a0[0], K5B, m_global=M5B, row0=r0, rows_cap=ml + T5B + 1,
+                               k_cap=K5B)
     eng.synchronize()
     init_s = time.perf_counter() - t0
     del a0
@@ -325,17 +346,17 @@ def run_cfg5b(torch, dev, lib, warm):
     eng.snapshot()
     steps = T5B - warm
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
+    barrier()
     l0 = lib.isvd_launch_count()
     e0.record(stream)
     for t in range(warm, T5B):
         eng.row_append(rows[t:t + 1])
     eng.flush()
     e1.record(stream)
-    torch.cuda.synchronize()
+    barrier()
     launches = lib.isvd_launch_count() - l0
-    ms = e0.elapsed_time(e1)
-    du, dv = eng.ortho_defect()
+    ms = max_over_ranks(e0.elapsed_time(e1), device=dev)
+    du, dv = (np.ravel(v)[0] for v in eng.ortho_defect())
     # per-phase breakdown of the same ticks
     eng.restore()
     lib.isvd_engine_set_timing(eng._h.h, 1)
@@ -352,14 +373,14 @@ def run_cfg5b(torch, dev, lib, warm):
     h_rows.copy_(rows)
     hr = h_rows.numpy()
     eng.restore()
-    eng.synchronize()
+    barrier()
     t0 = time.perf_counter()
     for t in range(warm, T5B):
         eng.row_append(hr[t:t + 1])
         eng.scalars()
     eng.flush()
     eng.synchronize()
-    e2e_s = time.perf_counter() - t0
+    e2e_s = max_over_ranks(time.perf_counter() - t0, device=dev)
     window = int(lib.isvd_engine_lazy_window(eng._h.h))
     del eng
     torch.cuda.empty_cache()
@@ -367,14 +388,16 @@ def run_cfg5b(torch, dev, lib, warm):
     per = {name: float(ph[j] / nrow) for j, name in enumerate(("project", "core_svd", "rotate",
                                                                 "install"))}
     flush_ms, flush_bytes = float(ph[8]), float(ph[9])
-    flush_flops = 2.0 * M5B * K5B * K5B
+    flush_flops = 2.0 * ml * K5B * K5B
     tick_ms = sum(per.values())
     return {
         "metric": "iSVD updates/sec (k=128)", "value": steps / (ms / 1e3), "unit": UNIT,
-        "steps": steps, "warmup": warm, "ms_per_step": ms / steps,
+        "steps": steps, "warmup": warm, "ms_per_step": ms / steps, "scaling": "strong",
         "config": {"workload": "cfg5b_tall", "m": M5B, "n": N5B, "rank": RANK5B, "k": K5B,
-                   "row_appends": T5B, "noise_sd": 1e-3, "parallelism": "1 GPU",
-                   "deferred_u_rows": window},
+                   "row_appends": T5B, "noise_sd": 1e-3,
+                   "parallelism": "1 GPU" if world == 1 else
+                   f"U and A row-sharded over {world} GPUs (NCCL allreduce of Grams)",
+                   "rows_per_gpu": ml, "deferred_u_rows": window},
         "gpu_launches": int(launches),
         "e2e": {"value": steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": N5B * 8,
                 "d2h_bytes_per_step": 3 * 8, "steps": steps},
@@ -390,7 +413,7 @@ def run_cfg5b(torch, dev, lib, warm):
         "phase_ms_per_tick": per,
         "flush_ms": flush_ms,
         "tick_busy_ms": tick_ms,
-        "ortho_defect": [float(du[0]), float(dv[0])],
+        "ortho_defect": [float(du), float(dv)],
         "init_s": init_s,
         "reference_hbm_ceiling_updates_per_s": 6553.3e9 / (8.0 * (2 * M5B * K5B + 2 * N5B * K5B
                                                                     + 2 * N5B)),
@@ -520,8 +543,8 @@ def run_gpu(args):
     del a0, rows, ii, jj, dd
     torch.cuda.empty_cache()
     k128 = None
-    if world == 1 and not args.no_k128:
-        k128 = run_cfg5b(torch, dev, lib, warm)
+    if not args.no_k128:
+        k128 = run_cfg5b(torch, dev, lib, warm, world, rank)
 
     if rank == 0:
         peak, peak_kind = _peaks()
