@@ -12,7 +12,8 @@ over N GPUs, no data-path collective).
           engine's stream, max over ranks).
 `e2e`     the same through the public API with pinned HOST event buffers:
           host validation + H2D copy + kernels + D2H read of the step's
-          result (per-stream sq_norm, residual and input norm) every step.
+          result (per-stream sq_norm, residual and input norm) every step;
+          the host waits for step t's result after issuing step t+1.
 `roofline` dominant kernel (the factor rotation K3/K4): algorithmic bytes /
           its measured average duration (CUDA events on the engine stream).
 
@@ -372,12 +373,16 @@ def run_cfg5b(torch, dev, lib, warm, world=1, rank=0):
     h_rows = torch.empty((T5B, N5B), dtype=torch.float64, pin_memory=True)
     h_rows.copy_(rows)
     hr = h_rows.numpy()
+    res = torch.empty((2, 3), dtype=torch.float64, pin_memory=True)
     eng.restore()
     barrier()
     t0 = time.perf_counter()
     for t in range(warm, T5B):
         eng.row_append(hr[t:t + 1])
-        eng.scalars()
+        eng.scalars_async(res[t % 2].numpy(), t % 2)  # step result, read with one step of lag
+        if t > warm:
+            eng.scalars_wait((t - 1) % 2)
+    eng.scalars_wait((T5B - 1) % 2)
     eng.flush()
     eng.synchronize()
     e2e_s = max_over_ranks(time.perf_counter() - t0, device=dev)
@@ -451,8 +456,14 @@ def run_gpu(args):
         if world > 1:
             dist.barrier()
 
+    res = torch.empty((2, 3 * B), dtype=torch.float64, pin_memory=True)
+
     def run_ticks(eng, nt, host=None):
-        """nt ticks; device-resident inputs unless host=(rows, ii, jj, dd)."""
+        """nt ticks; device-resident inputs unless host=(rows, ii, jj, dd).
+        With host inputs every step's result (sq_norm, residual, input norm
+        per stream) is read back to pinned host memory; the host waits for
+        step t's result after issuing step t+1 (one step of lag), so input
+        validation and upload overlap the previous step's kernels."""
         for t in range(nt):
             if t % 2 == 0:
                 eng.row_append(rows[t // 2] if host is None else host[0][t // 2])
@@ -461,7 +472,12 @@ def run_gpu(args):
             else:
                 eng.rank_one_update(host[1][t // 2], host[2][t // 2], host[3][t // 2])
             if host is not None:
-                eng.scalars()  # D2H read of the step's result (sync)
+                eng.scalars_async(res[t % 2].numpy(), t % 2)
+                if t > 0:
+                    eng.scalars_wait((t - 1) % 2)
+        if host is not None and nt > 0:
+            eng.scalars_wait((nt - 1) % 2)
+            assert np.all(np.isfinite(res[(nt - 1) % 2].numpy()))
 
     t_init = time.perf_counter()
     eng = BatchedSvdEngine(a0, K, m_cap=m_cap, k_cap=K)

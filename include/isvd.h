@@ -144,6 +144,13 @@ int isvd_engine_get_factors(isvd_engine* e, int b, double* u, double* s, double*
 int isvd_engine_get_tracked(isvd_engine* e, int b, double* a);
 int isvd_engine_get_reference(isvd_engine* e, int b, double* ref);
 /* sq_norm: B values; last_residual / last_input_norm: B values each. */
+/* Pipelined read of the per-step result: enqueue the copy of (sq_norm,
+ * last_residual, last_input_norm) -- 3 x B doubles, stream-major -- into
+ * `host` (pinned memory) on the engine stream and return at once; ticket
+ * `slot` (0..7) completes with isvd_engine_scalars_wait.  Lets a host loop
+ * issue step t+1 before step t's result lands (one step of lag). */
+int isvd_engine_scalars_async(isvd_engine* e, double* host, int slot);
+int isvd_engine_scalars_wait(isvd_engine* e, int slot);
 int isvd_engine_get_scalars(isvd_engine* e, double* sq_norm, double* last_residual,
                             double* last_input_norm);
 /* Overwrite the factors / reference of stream b from host memory (test and

@@ -18,9 +18,10 @@
 // canonical form is produced whenever factors are read.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
-#include <thread>
 #include <vector>
 #include "common.cuh"
 #include "core_svd.cuh"
@@ -86,8 +87,7 @@ static int check_device() {
 }
 
 // Host-side finiteness check of event payloads (the reference's as_vector,
-// linalg.py:31-40).  Branch-free exponent test so the loop vectorises, split
-// over host threads for large batches (a 5a row tick carries 8 MB).
+// linalg.py:31-40).  Branch-free exponent test so the loop vectorises.
 static bool finite_chunk(const double* p, size_t n) {
   const uint64_t* u = reinterpret_cast<const uint64_t*>(p);
   const uint64_t ex = 0x7ff0000000000000ull;
@@ -96,24 +96,10 @@ static bool finite_chunk(const double* p, size_t n) {
   return bad == 0;
 }
 
-static bool all_finite(const double* p, size_t n) {
-  const size_t kChunk = size_t(1) << 17;
-  if (n <= 2 * kChunk) return finite_chunk(p, n);
-  unsigned hw = std::thread::hardware_concurrency();
-  int nt = (int)std::min<size_t>(std::max(1u, std::min(hw, 16u)), n / kChunk);
-  std::vector<std::thread> th;
-  std::vector<char> ok(nt, 1);
-  const size_t per = (n + nt - 1) / nt;
-  for (int t = 0; t < nt; ++t)
-    th.emplace_back([&, t] {
-      size_t a = t * per, b = std::min(n, a + per);
-      if (a < b) ok[t] = finite_chunk(p + a, b - a);
-    });
-  for (auto& x : th) x.join();
-  for (char v : ok)
-    if (!v) return false;
-  return true;
-}
+// One pass on the calling thread: the scan is memory-bound (~20 GB/s on one
+// core), and helper threads measurably slowed the GPU work the host overlaps
+// it with (tools/e2e_probe5a_loop.py), so it stays serial.
+static bool all_finite(const double* p, size_t n) { return finite_chunk(p, n); }
 
 }  // namespace isvd
 
@@ -135,6 +121,21 @@ struct isvd_engine {
   int64_t sh_i = 0, sh_j = 0;  // the rank-1 event being issued (sharded)
   double sh_d = 0.0;
   double* shv = nullptr;  // [kCoreMaxS + 2] cross-shard vector scratch
+  cudaEvent_t sc_ev[8] = {};  // isvd_engine_scalars_async tickets
+  // host-payload staging: copy stream, two slots of ev, their events
+  cudaStream_t cp_st = nullptr;
+  cudaEvent_t stage_free[2] = {}, stage_ready = nullptr;
+  int stage_slot = 0;
+  int ensure_copy_stream() {
+    if (cp_st) return ISVD_OK;
+    ISVD_CUDA(cudaStreamCreateWithFlags(&cp_st, cudaStreamNonBlocking));
+    for (auto& ev2 : stage_free) {
+      ISVD_CUDA(cudaEventCreateWithFlags(&ev2, cudaEventDisableTiming));
+      ISVD_CUDA(cudaEventRecord(ev2, st));
+    }
+    ISVD_CUDA(cudaEventCreateWithFlags(&stage_ready, cudaEventDisableTiming));
+    return ISVD_OK;
+  }
   int64_t step = 0;
   double tol = 1e-10;
   bool guard = false;
@@ -297,7 +298,7 @@ struct isvd_engine {
   int alloc_vec_bufs() {
     dfree(z); dfree(ev);
     ISVD_TRY(dalloc(&z, (size_t)B * zlen()));
-    ISVD_TRY(dalloc(&ev, (size_t)B * zlen()));
+    ISVD_TRY(dalloc(&ev, (size_t)2 * B * zlen()));  // two staging slots
     return ISVD_OK;
   }
 
@@ -445,6 +446,12 @@ struct isvd_engine {
     if (fork_ev) cudaEventDestroy(fork_ev);
     for (auto ev : ev_marks) cudaEventDestroy(ev);
     for (auto ev : ev_pool) cudaEventDestroy(ev);
+    for (auto ev : sc_ev)
+      if (ev) cudaEventDestroy(ev);
+    for (auto ev : stage_free)
+      if (ev) cudaEventDestroy(ev);
+    if (stage_ready) cudaEventDestroy(stage_ready);
+    if (cp_st) cudaStreamDestroy(cp_st);
     if (own_stream && st) cudaStreamDestroy(st);
   }
 };
@@ -776,6 +783,7 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
     set_error(std::string(is_row ? "appended row" : "appended column") + " contains non-finite entries");
     return ISVD_EINVAL;
   }
+
   // keep = min(r+1, k, m+1, n) (row) | min(r+1, k, m, n+1) (col): engine.py:122,136
   const int keep = is_row ? std::min(std::min(e->r + 1, e->k), std::min(e->gm() + 1, e->n))
                           : std::min(std::min(e->r + 1, e->k), std::min(e->gm(), e->n + 1));
@@ -789,16 +797,29 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
   // window bookkeeping after this event (used by the completion check)
   e->r_base_next = lazy_state == 1 ? e->r : e->r_base;
   e->lazy_b_next = lazy_state == 1 ? 1 : e->lazy_b + 1;
+  // Host payload: one H2D on the copy stream into a double-buffered staging
+  // slot, issued before this tick's kernels wait for the previous tick, so
+  // the upload overlaps the previous tick's work; the slot is reused only
+  // after the tick that last read it has finished.
+  double* staged = nullptr;
+  int slot = 0;
+  if (!on_device) {
+    ISVD_TRY(e->ensure_copy_stream());
+    slot = e->stage_slot;
+    e->stage_slot ^= 1;
+    staged = e->ev + (int64_t)slot * e->B * e->zlen();
+    ISVD_CUDA(cudaStreamWaitEvent(e->cp_st, e->stage_free[slot], 0));
+    ISVD_CUDA(cudaMemcpyAsync(staged, x, sizeof(double) * e->B * len, cudaMemcpyHostToDevice,
+                              e->cp_st));
+    ISVD_CUDA(cudaEventRecord(e->stage_ready, e->cp_st));
+    ISVD_CUDA(cudaStreamWaitEvent(e->st, e->stage_ready, 0));
+  }
   ISVD_TRY(run_groups(e, [&](const Slice& sl) {
     const double* xd = x;
-    if (!on_device) {
-      // per-slice H2D on the slice's stream (overlaps the other groups' work)
-      ISVD_CUDA(cudaMemcpyAsync(e->ev + (int64_t)sl.b0 * len, x + (int64_t)sl.b0 * len,
-                                sizeof(double) * sl.nb * len, cudaMemcpyHostToDevice, sl.st));
-      xd = e->ev;
-    }
+    if (!on_device) xd = staged;
     return issue_append(e, sl, xd, len, is_row, keep, lazy_state);
   }));
+  if (!on_device) ISVD_CUDA(cudaEventRecord(e->stage_free[slot], e->st));
   if (lazy_state == 1) {
     e->lazy_active = true;
     e->m_base = e->m;
@@ -992,6 +1013,23 @@ int isvd_engine_get_scalars(isvd_engine* e, double* sq_norm, double* last_residu
   if (last_residual) ISVD_CUDA(cudaMemcpyAsync(last_residual, e->rho, sizeof(double) * e->B, cudaMemcpyDeviceToHost, e->st));
   if (last_input_norm) ISVD_CUDA(cudaMemcpyAsync(last_input_norm, e->xnorm, sizeof(double) * e->B, cudaMemcpyDeviceToHost, e->st));
   ISVD_CUDA(cudaStreamSynchronize(e->st));
+  return ISVD_OK;
+}
+
+int isvd_engine_scalars_async(isvd_engine* e, double* host, int slot) {
+  if (!e || !host || slot < 0 || slot >= 8) { set_error("bad argument"); return ISVD_EINVAL; }
+  if (!e->sc_ev[slot]) ISVD_CUDA(cudaEventCreateWithFlags(&e->sc_ev[slot], cudaEventDisableTiming));
+  ISVD_CUDA(cudaMemcpyAsync(host, e->N, sizeof(double) * e->B, cudaMemcpyDeviceToHost, e->st));
+  ISVD_CUDA(cudaMemcpyAsync(host + e->B, e->rho, sizeof(double) * e->B, cudaMemcpyDeviceToHost, e->st));
+  ISVD_CUDA(cudaMemcpyAsync(host + 2 * e->B, e->xnorm, sizeof(double) * e->B, cudaMemcpyDeviceToHost,
+                            e->st));
+  ISVD_CUDA(cudaEventRecord(e->sc_ev[slot], e->st));
+  return ISVD_OK;
+}
+
+int isvd_engine_scalars_wait(isvd_engine* e, int slot) {
+  if (!e || slot < 0 || slot >= 8 || !e->sc_ev[slot]) { set_error("bad ticket"); return ISVD_EINVAL; }
+  ISVD_CUDA(cudaEventSynchronize(e->sc_ev[slot]));
   return ISVD_OK;
 }
 

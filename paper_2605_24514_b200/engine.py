@@ -121,6 +121,16 @@ class BatchedSvdEngine:
                                                        _lib.dptr(xn)))
         return sq, rho, xn
 
+    def scalars_async(self, out, slot: int = 0) -> None:
+        """Enqueue the step's (sq_norm, residual, input norm) into `out`
+        (pinned host memory, 3 x B doubles) without waiting; pair with
+        scalars_wait(slot).  A host loop that waits on step t after issuing
+        step t+1 keeps the GPU busy while it validates and uploads inputs."""
+        _lib.check(self._h.lib.isvd_engine_scalars_async(self._h.h, _lib.vptr(out), int(slot)))
+
+    def scalars_wait(self, slot: int = 0) -> None:
+        _lib.check(self._h.lib.isvd_engine_scalars_wait(self._h.h, int(slot)))
+
     def factors(self, b: int = 0) -> SvdFactors:
         _, m, n, r, _, _ = self._h.shape()
         u, s, v = np.empty((m, r)), np.empty(r), np.empty((n, r))

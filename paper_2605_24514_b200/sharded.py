@@ -150,6 +150,12 @@ class ShardedSvdEngine:
                                                        _lib.dptr(xn)))
         return float(sq[0]), float(rho[0]), float(xn[0])
 
+    def scalars_async(self, out, slot: int = 0) -> None:
+        _lib.check(self._h.lib.isvd_engine_scalars_async(self._h.h, _lib.vptr(out), int(slot)))
+
+    def scalars_wait(self, slot: int = 0) -> None:
+        _lib.check(self._h.lib.isvd_engine_scalars_wait(self._h.h, int(slot)))
+
     @property
     def sq_norm(self) -> float:
         return self.scalars()[0]
