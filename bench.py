@@ -48,6 +48,17 @@ M5B, N5B, RANK5B, K5B, T5B = 1 << 22, 1024, 128, 128, 256
 DMMA_PEAK_TFS = 37.06  # measured FP64 DMMA.8x8x4 peak, profiles/r01_fp64_peaks.txt
 
 
+def _ncu_summary():
+    """Per-kernel ncu --set full figures committed under profiles/ (for the
+    roofline `traffic` field); {} when absent."""
+    for p in sorted((ROOT / "profiles").glob("r*_ncu_summary.json"), reverse=True):
+        try:
+            return json.loads(p.read_text()), p.name
+        except Exception:
+            continue
+    return {}, None
+
+
 def _peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -395,6 +406,8 @@ def run_cfg5b(torch, dev, lib, warm, world=1, rank=0):
     flush_ms, flush_bytes = float(ph[8]), float(ph[9])
     flush_flops = 2.0 * ml * K5B * K5B
     tick_ms = sum(per.values())
+    summ, summ_file = _ncu_summary()
+    traffic = summ.get("rot5b_flush", {}).get("dram_bytes") if world == 1 else None
     return {
         "metric": "iSVD updates/sec (k=128)", "value": steps / (ms / 1e3), "unit": UNIT,
         "steps": steps, "warmup": warm, "ms_per_step": ms / steps, "scaling": "strong",
@@ -412,7 +425,9 @@ def run_cfg5b(torch, dev, lib, warm, world=1, rank=0):
                      "frac": (flush_flops / (flush_ms / 1e3) / 1e12 / DMMA_PEAK_TFS)
                      if flush_ms else None,
                      "peak_kind": "measured FP64 DMMA (profiles/r01_fp64_peaks.txt)",
-                     "traffic": None,
+                     "traffic": traffic,
+                     "traffic_source": f"profiles/{summ_file}: rot5b_flush (ncu)" if traffic
+                     else None,
                      "hbm_gbs": flush_bytes / (flush_ms / 1e3) / 1e9 if flush_ms else None,
                      "flops_per_launch": flush_flops, "bytes_per_launch": flush_bytes},
         "phase_ms_per_tick": per,
@@ -494,10 +509,12 @@ def run_gpu(args):
     l0 = _lib.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(str(ROOT / "gpurun_out" / f"clocks_r{rank}.csv")) as clk:
+        torch.cuda.nvtx.range_push("isvd_timed")  # ncu --nvtx-include isvd_timed/
         e0.record(stream)
         run_ticks(eng, steps)
         eng.flush()  # materialise deferred U rotations inside the timed region
         e1.record(stream)
+        torch.cuda.nvtx.range_pop()
         barrier()
     launches = _lib.launch_count() - l0
     dev_ms = e0.elapsed_time(e1)
@@ -583,6 +600,11 @@ def run_gpu(args):
         hbm_name = max(hbm, key=lambda k: hbm[k]["ms"])
         hk = hbm[hbm_name]
         achieved = hk["gbs"]
+        summ, summ_file = _ncu_summary()
+        traffic = None
+        if "rot5a" in summ and "dram_bytes" in summ["rot5a"]:
+            # the capture is one stream-group launch (B / 4 streams)
+            traffic = summ["rot5a"]["dram_bytes"] * 4.0 * B / TOTAL_STREAMS
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
             "warmup": warm, "ms_per_step": t_max / steps, "higher_is_better": True,
@@ -599,7 +621,11 @@ def run_gpu(args):
                     "d2h_bytes_per_step": int(d2h), "steps": e2e_steps},
             "roofline": {"kernel": hbm_name, "bound": "hbm", "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "peak_kind": peak_kind,
-                         "traffic": None,
+                         "traffic": traffic,
+                         "traffic_source": (f"profiles/{summ_file}: rot5a dram__bytes_read+write "
+                                            "of one stream-group launch x 4 groups (ncu, "
+                                            "cold-cache); V partly L2-resident after K1")
+                         if traffic else None,
                          "bytes_per_launch": hk["bytes"] / max(1, (n_flush if "flush" in hbm_name
                                                                    else diag_steps)),
                          "dominant_kernel_by_time": dom_name,
