@@ -220,6 +220,18 @@ int isvd_engine_ortho_defect(isvd_engine* e, double* du, double* dv);
 int isvd_engine_angle(isvd_engine* e, int which, const double* q, int q_cols,
                       int on_device, double* out);
 
+/* Per-tick risk of BASELINE config 3 (finance.py:326-371), for every stream:
+ * cov = V diag(s^2) V^T / (t - 1) symmetrised (low_rank_covariance),
+ * D = max(0, diag(A^T A) / (t - 1) - diag(cov)) over the mean-centred tracked
+ * returns (the diagonal term BASELINE adds), and for each of the P
+ * portfolios w (host, P x n): out[b][p] = {sqrt(w'cov w) (portfolio_vol),
+ * sqrt(w'(cov + D) w), 2.3263478740408408 * that (99% Gaussian VaR, zero
+ * mean), w'cov w}.  cov_out (B x n x n) and diag_out (B x n) may be NULL.
+ * t = rows the covariance is estimated from (>= 2, else ISVD_EINVAL); a
+ * quadratic form below -1e-10 is the reference's not-PSD ValueError. */
+int isvd_engine_risk(isvd_engine* e, int t, const double* w, int P, double* cov_out,
+                     double* diag_out, double* out);
+
 /* Dense thin SVD of B matrices (m x n each) on the device, in canonical
  * form (linalg.py:84-92).  Outputs: s (B x min(m,n)); u (B x m x w) and
  * vt (B x w x n) for the leading w = min(w_keep, min(m,n)) triplets; u/vt

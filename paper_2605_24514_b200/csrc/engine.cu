@@ -1240,6 +1240,44 @@ int isvd_engine_frob_error(isvd_engine* e, double* out) {
   return ISVD_OK;
 }
 
+int isvd_engine_risk(isvd_engine* e, int t, const double* w, int P, double* cov_out,
+                     double* diag_out, double* out) {
+  if (!e || !e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
+  if (!w || !out || P < 1) { set_error("risk: bad argument"); return ISVD_EINVAL; }
+  if (t < 2) { set_error("need at least 2 rows for a covariance, got t=" + std::to_string(t)); return ISVD_EINVAL; }
+  if (e->sharded) { set_error("risk needs the whole tracked matrix (not in shard mode)"); return ISVD_EINVAL; }
+  const int B = e->B, n = e->n;
+  double *wd = nullptr, *cd = nullptr, *dd = nullptr, *od = nullptr;
+  int rc = ISVD_OK;
+  auto T = [&](int v) { if (rc == ISVD_OK) rc = v; };
+  T(dalloc(&wd, (size_t)P * n));
+  T(dalloc(&od, (size_t)B * P * 4));
+  if (cov_out) T(dalloc(&cd, (size_t)B * n * n));
+  if (diag_out) T(dalloc(&dd, (size_t)B * n));
+  if (rc == ISVD_OK)
+    T(cudaMemcpyAsync(wd, w, sizeof(double) * P * n, cudaMemcpyHostToDevice, e->st) == cudaSuccess
+          ? ISVD_OK : ISVD_ENODEV);
+  if (rc == ISVD_OK)
+    T(launch_risk(B, n, e->r, e->Vm(), e->s, e->ld, e->A, e->astride(), e->n_cap, e->m,
+                  1.0 / (t - 1.0), wd, P, cd, dd, od, e->st));
+  if (rc == ISVD_OK) {
+    cudaMemcpyAsync(out, od, sizeof(double) * B * P * 4, cudaMemcpyDeviceToHost, e->st);
+    if (cov_out) cudaMemcpyAsync(cov_out, cd, sizeof(double) * B * n * n, cudaMemcpyDeviceToHost, e->st);
+    if (diag_out) cudaMemcpyAsync(diag_out, dd, sizeof(double) * B * n, cudaMemcpyDeviceToHost, e->st);
+    if (cudaStreamSynchronize(e->st) != cudaSuccess) { set_error("risk: device failure"); rc = ISVD_ENODEV; }
+  }
+  if (rc == ISVD_OK)
+    for (int i = 0; i < B * P; ++i)
+      if (out[(size_t)i * 4 + 3] < -1e-10) {
+        set_error("covariance is not PSD: w'Cw = " + std::to_string(out[(size_t)i * 4 + 3]));
+        rc = ISVD_EINVAL;
+        break;
+      }
+  cudaStreamSynchronize(e->st);
+  dfree(wd); dfree(cd); dfree(dd); dfree(od);
+  return rc;
+}
+
 static int gram_defect(isvd_engine* e, Mat X, int rows, int w, double* host_out,
                        bool row_sharded = false) {
   ISVD_TRY(e->ensure_work(0, 0, gram_part_elems(e->B, rows, w, w), (int64_t)e->B * w * w + e->B));

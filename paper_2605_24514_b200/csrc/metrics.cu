@@ -117,6 +117,89 @@ int launch_gram(int batch, int rows, int wa, int wb, Mat Xa, Mat Xb, double* par
   return launch_gram_tiles(batch, rows, wa, wb, Xa, Xb, sym ? 1 : 0, partial, out, st);
 }
 
+// ---- a13: per-tick risk of BASELINE config 3 (finance.py:326-364).
+// cov = V diag(s^2) V^T / (t-1), symmetrised as the reference does;
+// D_j = max(0, sum_i A_ij^2 / (t-1) - cov_jj) (the diagonal term BASELINE
+// asks for over the mean-centred returns); per portfolio p:
+// out[p] = {sqrt(max(0, w'cov w)), sqrt(max(0, w'(cov + D)w)), z99 * that,
+// w'cov w} (the last lets the host raise the reference's not-PSD error).
+__global__ void risk_kernel(int n, int r, Mat V, const double* __restrict__ s, int lds,
+                            const double* __restrict__ A, int64_t a_stride, int lda, int m,
+                            double inv_t1, const double* __restrict__ w, int P,
+                            double* __restrict__ cov, double* __restrict__ diag,
+                            double* __restrict__ out) {
+  extern __shared__ double rsm[];
+  double* c = rsm;            // [n][n]
+  double* dd = rsm + n * n;   // [n]
+  __shared__ double red[32];
+  const int b = blockIdx.x;
+  const double* Vb = V.p + b * V.stride;
+  const double* sb = s + (int64_t)b * lds;
+  const double* Ab = A + b * a_stride;
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+    const int i = idx / n, j = idx % n;
+    double cij = 0.0, cji = 0.0;
+    for (int l = 0; l < r; ++l) {
+      const double s2 = sb[l] * sb[l];
+      cij = fma(Vb[i * V.ld + l] * s2, Vb[j * V.ld + l], cij);
+      cji = fma(Vb[j * V.ld + l] * s2, Vb[i * V.ld + l], cji);
+    }
+    // no FMA contraction, so c_ij and c_ji round identically (bit-symmetric)
+    c[idx] = 0.5 * __dadd_rn(__dmul_rn(cij, inv_t1), __dmul_rn(cji, inv_t1));
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    double acc = 0.0;
+    for (int i = 0; i < m; ++i) acc = fma(Ab[(int64_t)i * lda + j], Ab[(int64_t)i * lda + j], acc);
+    dd[j] = fmax(0.0, acc * inv_t1 - c[j * n + j]);
+  }
+  __syncthreads();
+  if (cov)
+    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) cov[(int64_t)b * n * n + idx] = c[idx];
+  if (diag)
+    for (int j = threadIdx.x; j < n; j += blockDim.x) diag[(int64_t)b * n + j] = dd[j];
+  for (int p = 0; p < P; ++p) {
+    const double* wp = w + (int64_t)p * n;
+    double q = 0.0, qd = 0.0;
+    for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+      const int i = idx / n, j = idx % n;
+      q = fma(wp[i] * c[idx], wp[j], q);
+    }
+    for (int j = threadIdx.x; j < n; j += blockDim.x) qd = fma(wp[j] * wp[j], dd[j], qd);
+    q = block_sum(q, red);
+    qd = block_sum(qd, red);
+    if (threadIdx.x == 0) {
+      const double z99 = 2.3263478740408408;  // Phi^{-1}(0.99)
+      const double vd = sqrt(fmax(0.0, q + qd));
+      double* o = out + ((int64_t)b * P + p) * 4;
+      o[0] = sqrt(fmax(0.0, q));
+      o[1] = vd;
+      o[2] = z99 * vd;
+      o[3] = q;
+    }
+  }
+}
+
+int launch_risk(int batch, int n, int r, Mat V, const double* s, int lds, const double* A,
+                int64_t a_stride, int lda, int m, double inv_t1, const double* w, int P,
+                double* cov, double* diag, double* out, cudaStream_t st) {
+  const size_t smem = sizeof(double) * ((size_t)n * n + n);
+  if (smem > 200 * 1024) {
+    set_error("risk: too many assets for the on-chip covariance");
+    return ISVD_EINVAL;
+  }
+  static bool attr = false;
+  if (!attr) {
+    ISVD_CUDA(cudaFuncSetAttribute(risk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   200 * 1024));
+    attr = true;
+  }
+  risk_kernel<<<batch, 256, smem, st>>>(n, r, V, s, lds, A, a_stride, lda, m, inv_t1, w, P, cov,
+                                        diag, out);
+  ISVD_LAUNCHED();
+  return ISVD_OK;
+}
+
 int launch_defect(int batch, int w, const double* G, double* out, cudaStream_t st) {
   defect_kernel<<<batch, 256, 0, st>>>(w, G, out);
   ISVD_LAUNCHED();
