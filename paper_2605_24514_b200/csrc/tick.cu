@@ -579,17 +579,21 @@ static int rot_rows_per_block(int64_t total_rows) {
   return (int)std::min<int64_t>(std::max<int64_t>(rpb, 64), kRotRowsPerBlock);
 }
 
-// Small-width variant (KP <= 32, keep <= 32): the core rotation is held as
-// DMMA B-fragments in registers (loaded straight from L2, no shared staging,
-// no block barrier); kk-outer / nn-inner ordering gives four independent
-// accumulator chains per lane.
+// Small-width variant (KP <= 32, keep <= 32): the core rotation's DMMA
+// B-fragments sit in 8 KB of shared memory (64 registers per thread, 8 CTAs
+// per SM); kk-outer / nn-inner ordering gives four independent accumulator
+// chains per lane.
 constexpr int kRegWarps = 4;
 constexpr int kRegRowsPerBlock = 256;
 
 template <int KP>
-__global__ void __launch_bounds__(kRegWarps * 32, 3)
+__global__ void __launch_bounds__(kRegWarps * 32, 8)
     rotate_reg_kernel(int r, int keep, RotJob j0, RotJob j1, int nblk0) {
   constexpr int KQ = KP / 4;
+  // B fragments of the core rotation in lane order (one conflict-free LDS.64
+  // per DMMA); keeping them out of registers (64 regs at KP = 32) lets 8
+  // CTAs share an SM, which this latency-bound stream of 8-row groups needs
+  __shared__ double qf[KQ * 4 * 32];
   const bool second = blockIdx.x >= nblk0;
   const RotJob& J = second ? j1 : j0;
   const int blk = second ? blockIdx.x - nblk0 : blockIdx.x;
@@ -598,14 +602,12 @@ __global__ void __launch_bounds__(kRegWarps * 32, 3)
   const bool has_last = (J.z != nullptr) || J.new_row;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
-  double bq[KQ][4];
-#pragma unroll
-  for (int kk = 0; kk < KQ; ++kk)
-#pragma unroll
-    for (int nn = 0; nn < 4; ++nn) {
-      const int l = q * KQ + kk, c = nn * 8 + g;
-      bq[kk][nn] = (l < r && c < keep) ? Q[l * J.ldq + c] : 0.0;
-    }
+#pragma unroll 4
+  for (int idx = threadIdx.x; idx < KQ * 4 * 32; idx += blockDim.x) {
+    const int ln = idx & 31, nn = (idx >> 5) & 3, kk = idx >> 7;
+    const int l = (ln & 3) * KQ + kk, c = nn * 8 + (ln >> 2);
+    qf[idx] = (l < r && c < keep) ? Q[l * J.ldq + c] : 0.0;
+  }
   double qr[4][2];
 #pragma unroll
   for (int nn = 0; nn < 4; ++nn)
@@ -625,6 +627,7 @@ __global__ void __launch_bounds__(kRegWarps * 32, 3)
   const double* zb = J.z ? J.z + b * J.z_stride : nullptr;
   const int row_begin = blk * kRegRowsPerBlock;
   const int row_end = min(J.rows, row_begin + kRegRowsPerBlock);
+  __syncthreads();
   for (int row0 = row_begin + warp * 8; row0 < row_end; row0 += kRegWarps * 8) {
     const int row = row0 + g;
     double a[KQ];
@@ -647,7 +650,8 @@ __global__ void __launch_bounds__(kRegWarps * 32, 3)
 #pragma unroll
     for (int kk = 0; kk < KQ; ++kk)
 #pragma unroll
-      for (int nn = 0; nn < 4; ++nn) dmma_8x8x4(d[nn][0], d[nn][1], a[kk], bq[kk][nn]);
+      for (int nn = 0; nn < 4; ++nn)
+        dmma_8x8x4(d[nn][0], d[nn][1], a[kk], qf[(kk * 4 + nn) * 32 + lane]);
     if (row < row_end) {
 #pragma unroll
       for (int nn = 0; nn < 4; ++nn) {
