@@ -19,6 +19,7 @@
 // a_pp, a_qq, a_pq.  For s > kSmemMaxS, V is kept in a global scratch.
 #include "common.cuh"
 #include "core_svd.cuh"
+#include "tick.cuh"
 #include "../../include/isvd.h"
 
 namespace isvd {
@@ -329,10 +330,11 @@ struct J32Smem {
   int pos[32];
 };
 
+template <bool BUILD>
 __global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32_kernel(
     int s, const double* __restrict__ core, int64_t core_stride, int ldcore, double* __restrict__ uk,
     double* __restrict__ vk, int64_t out_stride, int ldo, double* __restrict__ sv,
-    int64_t sv_stride, int batch) {
+    int64_t sv_stride, int batch, Rank1Core rc) {
   extern __shared__ __align__(16) unsigned char j32_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b = blockIdx.x * kJ32Warps + warp;
@@ -340,12 +342,54 @@ __global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32_kernel(
   J32Smem& W = reinterpret_cast<J32Smem*>(j32_raw)[warp];
   double* nrm = W.nrm;
   int* pos = W.pos;
-  const double* K = core + b * core_stride;
   double g[32];
+  if constexpr (BUILD) {
+    // Fused K6: lane p builds row p of K = diag(s) + delta U[i,:]^T Vt[:,j]^T
+    // (_kernels.pyx:209-213, same arithmetic as rank1_build_kernel) in
+    // registers -- the core never goes through HBM -- and lane 0 applies the
+    // tracked-entry update A[i,j] += delta, N += 2 delta a_old + delta^2
+    // (engine.py:162-166).
+    const int64_t i = rc.ii[b], j = rc.jj[b];
+    const double d = rc.delta[b];
+    const LazyBasis& lz = rc.lz;
+    double ap = 0.0;
+    if (lane < s) {
+      if (!lz.active) {
+        ap = rc.U.p[b * rc.U.stride + i * rc.U.ld + lane];
+      } else if (i >= lz.m_base) {
+        ap = lz.W.p[b * lz.W.stride + (lz.r_base + (i - lz.m_base)) * lz.W.ld + lane];
+      } else {
+        const double* ur = rc.U.p + b * rc.U.stride + i * rc.U.ld;
+        const double* Wb = lz.W.p + b * lz.W.stride;
+        for (int c = 0; c < lz.r_base; ++c) ap = fma(ur[c], Wb[c * lz.W.ld + lane], ap);
+      }
+    }
+    const double* vr = rc.V.p + b * rc.V.stride + j * rc.V.ld;
+    const double sp = lane < s ? rc.s[(int64_t)b * rc.lds + lane] : 0.0;
+    const double da = d * ap;
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    g[j] = (lane < s && j < s) ? K[lane * ldcore + j] : 0.0;
-    W.V[lane][j] = (lane == j && lane < s) ? 1.0 : 0.0;
+    for (int q = 0; q < 32; ++q) {
+      double v = 0.0;
+      if (lane < s && q < s) {
+        v = da * vr[q];
+        if (q == lane) v += sp;
+      }
+      g[q] = v;
+      W.V[lane][q] = (lane == q && lane < s) ? 1.0 : 0.0;
+    }
+    if (lane == 0 && rc.A) {
+      double* e = rc.A + b * rc.a_stride + i * rc.lda + j;
+      const double old = *e;
+      *e = old + d;
+      rc.N[b] += 2.0 * d * old + d * d;
+    }
+  } else {
+    const double* K = core + b * core_stride;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      g[j] = (lane < s && j < s) ? K[lane * ldcore + j] : 0.0;
+      W.V[lane][j] = (lane == j && lane < s) ? 1.0 : 0.0;
+    }
   }
   // Sweeps until none rotates (_kernels.pyx:58-59), or until a sweep whose
   // rotations were all below kConvRel (quadratic convergence, see kConvRel):
@@ -497,6 +541,27 @@ size_t core_svd_smem_bytes(int s, bool v_in_smem) {
   return sizeof(double) * (size_t)s * ps * (v_in_smem ? 2 : 1);
 }
 
+int launch_rank1_core_svd32(int batch, int s, const Rank1Core& rc, double* uk, double* vk,
+                            int64_t out_stride, int ldo, double* sv, int64_t sv_stride,
+                            cudaStream_t st) {
+  if (s < 1 || s > 32) {
+    set_error("fused rank-1 core: width out of range");
+    return ISVD_EINVAL;
+  }
+  if (batch == 0) return ISVD_OK;
+  static bool attr = false;
+  const size_t smem = sizeof(J32Smem) * kJ32Warps;
+  if (!attr) {
+    ISVD_CUDA(cudaFuncSetAttribute(jacobi32_kernel<true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  jacobi32_kernel<true><<<ceil_div(batch, kJ32Warps), kJ32Warps * 32, smem, st>>>(
+      s, nullptr, 0, 0, uk, vk, out_stride, ldo, sv, sv_stride, batch, rc);
+  ISVD_LAUNCHED();
+  return ISVD_OK;
+}
+
 int launch_core_svd(int batch, int s, const double* core, int64_t core_stride, int ldcore,
                     double* uk, double* vk, int64_t out_stride, int ldo, double* sv,
                     int64_t sv_stride, double* vscratch, const int* active, cudaStream_t st) {
@@ -509,12 +574,12 @@ int launch_core_svd(int batch, int s, const double* core, int64_t core_stride, i
     static bool j32_attr = false;
     const size_t smem = sizeof(J32Smem) * kJ32Warps;
     if (!j32_attr) {
-      ISVD_CUDA(cudaFuncSetAttribute(jacobi32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
+      ISVD_CUDA(cudaFuncSetAttribute(jacobi32_kernel<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       j32_attr = true;
     }
-    jacobi32_kernel<<<ceil_div(batch, kJ32Warps), kJ32Warps * 32, smem, st>>>(
-        s, core, core_stride, ldcore, uk, vk, out_stride, ldo, sv, sv_stride, batch);
+    jacobi32_kernel<false><<<ceil_div(batch, kJ32Warps), kJ32Warps * 32, smem, st>>>(
+        s, core, core_stride, ldcore, uk, vk, out_stride, ldo, sv, sv_stride, batch, Rank1Core{});
     ISVD_LAUNCHED();
     return ISVD_OK;
   }

@@ -24,7 +24,28 @@ int launch_core_svd(int batch, int s, const double* core, int64_t core_stride, i
 
 }  // namespace isvd
 
+#include "tick.cuh"
 namespace isvd {
+// Rank-1 core description for the fused build + Jacobi (K6 + K2b) kernel.
+struct Rank1Core {
+  Mat U, V;
+  const double* s = nullptr;
+  int lds = 0;
+  const int64_t* ii = nullptr;
+  const int64_t* jj = nullptr;
+  const double* delta = nullptr;
+  double* A = nullptr;
+  int64_t a_stride = 0;
+  int lda = 0;
+  double* N = nullptr;
+  LazyBasis lz{};
+};
+// K = diag(s) + delta U[i,:]^T Vt[:,j]^T built in registers and factored by
+// the warp Jacobi (s <= 32); also applies A[i,j] += delta and the N update.
+int launch_rank1_core_svd32(int batch, int s, const Rank1Core& rc, double* uk, double* vk,
+                            int64_t out_stride, int ldo, double* sv, int64_t sv_stride,
+                            cudaStream_t st);
+
 // Secular-equation SVD of the Brand append core [[diag d, 0], [p, rho]]
 // (arrow_svd.cu).  Same outputs and conventions as launch_core_svd.
 int launch_arrow_svd(int batch, int s, const double* core, int64_t core_stride, int ldcore,

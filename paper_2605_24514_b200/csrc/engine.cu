@@ -705,8 +705,26 @@ static int issue_rank_one(isvd_engine* e, const Slice& sl, const int64_t* di, co
   const bool one = e->ngroups_active == 1;
   LazyBasis lz = e->lazy();
   lz.W = mat_at(lz.W, b0);
+  const bool fused = !e->sharded && r <= 32;
   if (one) e->mark();
-  if (e->sharded) {
+  if (fused) {
+    // K6 + K2b in one kernel: the core is built in registers (no HBM round trip)
+    Rank1Core rc;
+    rc.U = mat_at(e->Um(), b0);
+    rc.V = mat_at(e->Vm(), b0);
+    rc.s = e->s + (int64_t)b0 * e->ld;
+    rc.lds = e->ld;
+    rc.ii = di + b0;
+    rc.jj = dj + b0;
+    rc.delta = dd + b0;
+    rc.A = e->A + b0 * e->astride();
+    rc.a_stride = e->astride();
+    rc.lda = e->n_cap;
+    rc.N = e->N + b0;
+    rc.lz = lz;
+    if (one) e->mark();
+    ISVD_TRY(launch_rank1_core_svd32(nb, r, rc, uk, vk, cs, S, sv, S, st));
+  } else if (e->sharded) {
     // U[i, :] and A[i, j] from the shard owning row i, summed across shards
     const int64_t il = e->sh_i - e->row0;
     const bool mine = 0 <= il && il < e->m;
@@ -722,9 +740,12 @@ static int issue_rank_one(isvd_engine* e, const Slice& sl, const int64_t* di, co
                                 cs, S, e->A + b0 * e->astride(), e->astride(), e->n_cap, e->N + b0,
                                 lz, st));
   }
-  if (one) e->mark();
-  ISVD_TRY(launch_core_svd(nb, r, core, cs, S, uk, vk, cs, S, sv, S,
-                           e->vscr ? e->vscr + (int64_t)b0 * S * (S | 1) : nullptr, nullptr, st));
+  if (!fused) {
+    if (one) e->mark();
+    ISVD_TRY(launch_core_svd(nb, r, core, cs, S, uk, vk, cs, S, sv, S,
+                             e->vscr ? e->vscr + (int64_t)b0 * S * (S | 1) : nullptr, nullptr,
+                             st));
+  }
   if (one) e->mark();
   RotJob ju{mat_at(e->Um(), b0), e->m, uk, cs, S, nullptr, 0, nullptr, 0};
   RotJob jv{mat_at(e->Vm(), b0), e->n, vk, cs, S, nullptr, 0, nullptr, 0};
