@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : (kN + 31) / 32 * 32) arrow_svd_ke
         double f = 0.0;
         for (int j = lane; j < N; j += 32) {
           const double dj = S.kd[j];
-          f += S.kz[j] * S.kz[j] / ((dj - di) * (dj + di) - mum);
+          f += S.kz[j] * S.kz[j] * frcp((dj - di) * (dj + di) - mum);
         }
         f = 1.0 + warp_sum(f);
         if (f > 0.0) {
@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : (kN + 31) / 32 * 32) arrow_svd_ke
       double f = 1.0;
       for (int j = 0; j < N; ++j) {
         const double dj = S.kd[j];
-        f += S.kz[j] * S.kz[j] / ((dj - di) * (dj + di) - mum);
+        f += S.kz[j] * S.kz[j] * frcp((dj - di) * (dj + di) - mum);
       }
       if (f > 0.0) {
         o = i; lo = 0.0; hi = mum;
@@ -464,7 +464,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : (kN + 31) / 32 * 32) arrow_svd_ke
       double acc = 1.0;
       for (int k = lane; k < N - 1; k += 32) {
         const double dk = k < j ? S.kd[k] : S.kd[k + 1];
-        acc *= sdiff(k) / ((dk - dj) * (dk + dj));
+        acc *= sdiff(k) * frcp((dk - dj) * (dk + dj));
       }
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) acc *= __shfl_xor_sync(0xffffffffu, acc, off);
@@ -479,8 +479,8 @@ __global__ void __launch_bounds__(WIDE ? 512 : (kN + 31) / 32 * 32) arrow_svd_ke
       return S.mu[k] - (dj - dk) * (dj + dk);
     };
     double acc = sdiff(N - 1);
-    for (int k = 0; k < j; ++k) acc *= sdiff(k) / ((S.kd[k] - dj) * (S.kd[k] + dj));
-    for (int k = j; k < N - 1; ++k) acc *= sdiff(k) / ((S.kd[k + 1] - dj) * (S.kd[k + 1] + dj));
+    for (int k = 0; k < j; ++k) acc *= sdiff(k) * frcp((S.kd[k] - dj) * (S.kd[k] + dj));
+    for (int k = j; k < N - 1; ++k) acc *= sdiff(k) * frcp((S.kd[k + 1] - dj) * (S.kd[k + 1] + dj));
     S.zhat[j] = copysign(sqrt(fmax(acc, 0.0)), S.kz[j]);
   }
   // ---- sorted output positions: descending sigma, ties by triple index
