@@ -651,7 +651,8 @@ static int issue_append(isvd_engine* e, const Slice& sl, const double* xd, int l
                                  e->s + (int64_t)b0 * e->ld, e->ld, e->tol, core, cs, S, z,
                                  e->zlen(), inj, e->rho + b0, e->xnorm + b0, Adst, e->astride(),
                                  a_off, a_step, e->N + b0, st,
-                                 (e->sharded && !is_row) ? &e->ar : nullptr));
+                                 (e->sharded && !is_row) ? &e->ar : nullptr,
+                                 e->append_jacobi ? 0 : 1));
   if (one) e->mark();
   if (e->append_jacobi)
     ISVD_TRY(launch_core_svd(nb, r + 1, core, cs, S, uk, vk, cs, S, sv, S,

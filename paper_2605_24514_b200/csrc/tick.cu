@@ -1,5 +1,6 @@
 // Per-tick kernels of the incremental update (kernels K1, K3-K6, K9).
 #include <algorithm>
+#include <type_traits>
 #include "common.cuh"
 #include "core_svd.cuh"
 #include "tick.cuh"
@@ -22,14 +23,14 @@ constexpr int kRMax = kCoreMaxS;  // max factor width handled by the tick kernel
 // run on-chip (F read from HBM exactly once, one outstanding 16-64 KB
 // request per CTA).  Pass 2 walks each row with a skewed column index, so
 // the one-thread-per-row reads are bank-conflict free.
-template <bool STAGE>
+template <bool STAGE, int RT>
 __global__ void __launch_bounds__(256) project_append_kernel(
     int rows, int r, Mat F, const double* __restrict__ x, int64_t x_stride,
     const double* __restrict__ s, int lds, double tol, double* __restrict__ core,
     int64_t core_stride, int ldcore, double* __restrict__ z, int64_t z_stride,
     double* __restrict__ inj_scale, double* __restrict__ rho_out, double* __restrict__ xnorm_out,
     double* __restrict__ A, int64_t a_stride, int64_t a_off, int64_t a_step,
-    double* __restrict__ N) {
+    double* __restrict__ N, int arrow_only) {
   __shared__ double part[8][kRMax];
   __shared__ double p[kRMax];
   __shared__ double red[32];
@@ -68,20 +69,20 @@ __global__ void __launch_bounds__(256) project_append_kernel(
   if (STAGE) mbar_wait(&bar, 0);
   __syncthreads();
 
-  double acc[(kRMax + 31) / 32];
+  double acc[RT];  // RT = ceil(r / 32) column tiles per lane
 #pragma unroll
-  for (int t = 0; t < (kRMax + 31) / 32; ++t) acc[t] = 0.0;
+  for (int t = 0; t < RT; ++t) acc[t] = 0.0;
   for (int c = warp; c < rows; c += nw) {
     const double xc = STAGE ? xs[c] : xb[c];
     const double* fr = STAGE ? Fs + (size_t)c * F.ld : Fb + (int64_t)c * F.ld;
 #pragma unroll
-    for (int t = 0; t < (kRMax + 31) / 32; ++t) {
+    for (int t = 0; t < RT; ++t) {
       int l = lane + 32 * t;
       if (l < r) acc[t] = fma(fr[l], xc, acc[t]);
     }
   }
 #pragma unroll
-  for (int t = 0; t < (kRMax + 31) / 32; ++t) {
+  for (int t = 0; t < RT; ++t) {
     int l = lane + 32 * t;
     if (l < r) part[warp][l] = acc[t];
   }
@@ -126,15 +127,23 @@ __global__ void __launch_bounds__(256) project_append_kernel(
   const int P = r + 1;
   double* Kb = core + b * core_stride;
   const double* sb = s + (int64_t)b * lds;
-  for (int idx = threadIdx.x; idx < P * P; idx += blockDim.x) {
-    int i = idx / P, j = idx % P;
-    double v = 0.0;
-    if (i < r) {
-      if (i == j) v = sb[i];
-    } else {
-      v = (j < r) ? p[j] : (fresh ? rho : 0.0);
+  if (arrow_only) {
+    // the secular solver reads only the diagonal and the last row
+    for (int j = threadIdx.x; j < P; j += blockDim.x) {
+      if (j < r) Kb[j * ldcore + j] = sb[j];
+      Kb[r * ldcore + j] = (j < r) ? p[j] : (fresh ? rho : 0.0);
     }
-    Kb[i * ldcore + j] = v;
+  } else {
+    for (int idx = threadIdx.x; idx < P * P; idx += blockDim.x) {
+      int i = idx / P, j = idx % P;
+      double v = 0.0;
+      if (i < r) {
+        if (i == j) v = sb[i];
+      } else {
+        v = (j < r) ? p[j] : (fresh ? rho : 0.0);
+      }
+      Kb[i * ldcore + j] = v;
+    }
   }
   if (threadIdx.x == 0) {
     inj_scale[b] = fresh ? 1.0 / rho : 0.0;
@@ -891,7 +900,7 @@ int launch_project_append(int batch, int rows, int r, Mat F, const double* x, in
                           int ldcore, double* z, int64_t z_stride, double* inj_scale,
                           double* rho_out, double* xnorm_out, double* A, int64_t a_stride,
                           int64_t a_off, int64_t a_step, double* N, cudaStream_t st,
-                          const Allreducer* ar) {
+                          const Allreducer* ar, int arrow_only) {
   if (r > kRMax) {
     set_error("factor width exceeds kernel limit");
     return ISVD_EINVAL;
@@ -950,21 +959,44 @@ int launch_project_append(int batch, int rows, int r, Mat F, const double* x, in
   const size_t stage = sizeof(double) * ((size_t)rows * F.ld + rows);
   const bool aligned = (reinterpret_cast<uintptr_t>(F.p) % 16 == 0) && (F.stride % 2 == 0) &&
                        (F.ld % 2 == 0);
-  if (stage <= 96 * 1024 && aligned) {
-    static bool attr = false;
-    if (!attr) {
-      ISVD_CUDA(cudaFuncSetAttribute(project_append_kernel<true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-      attr = true;
+  const bool staged = stage <= 96 * 1024 && aligned;
+  const int rt = (r + 31) / 32;
+  auto go = [&](auto stage_tag, auto rt_tag) -> int {
+    constexpr bool SG = decltype(stage_tag)::value;
+    constexpr int RT = decltype(rt_tag)::value;
+    if (SG) {
+      static bool attr = false;
+      if (!attr) {
+        ISVD_CUDA(cudaFuncSetAttribute(project_append_kernel<SG, RT>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+        attr = true;
+      }
     }
-    project_append_kernel<true><<<batch, 256, stage, st>>>(
+    project_append_kernel<SG, RT><<<batch, 256, SG ? stage : 0, st>>>(
         rows, r, F, x, x_stride, s, lds, tol, core, core_stride, ldcore, z, z_stride, inj_scale,
-        rho_out, xnorm_out, A, a_stride, a_off, a_step, N);
-  } else {
-    project_append_kernel<false><<<batch, 256, 0, st>>>(
-        rows, r, F, x, x_stride, s, lds, tol, core, core_stride, ldcore, z, z_stride, inj_scale,
-        rho_out, xnorm_out, A, a_stride, a_off, a_step, N);
+        rho_out, xnorm_out, A, a_stride, a_off, a_step, N, arrow_only);
+    return ISVD_OK;
+  };
+  using T1 = std::integral_constant<bool, true>;
+  using F1 = std::integral_constant<bool, false>;
+  int rc2 = ISVD_OK;
+  switch (rt) {
+#define ISVD_PROJ_CASE(K)                                                          \
+  case K:                                                                          \
+    rc2 = staged ? go(T1{}, std::integral_constant<int, K>{})                      \
+                 : go(F1{}, std::integral_constant<int, K>{});                     \
+    break;
+    ISVD_PROJ_CASE(1)
+    ISVD_PROJ_CASE(2)
+    ISVD_PROJ_CASE(3)
+    ISVD_PROJ_CASE(4)
+    ISVD_PROJ_CASE(5)
+#undef ISVD_PROJ_CASE
+    default:
+      set_error("factor width exceeds kernel limit");
+      return ISVD_EINVAL;
   }
+  ISVD_TRY(rc2);
   ISVD_LAUNCHED();
   return ISVD_OK;
 }

@@ -22,7 +22,7 @@ int launch_project_append(int batch, int rows, int r, Mat F, const double* x, in
                           int ldcore, double* z, int64_t z_stride, double* inj_scale,
                           double* rho_out, double* xnorm_out, double* A, int64_t a_stride,
                           int64_t a_off, int64_t a_step, double* N, cudaStream_t st,
-                          const struct Allreducer* ar = nullptr);
+                          const struct Allreducer* ar = nullptr, int arrow_only = 0);
 
 // Deferred left basis: while active, the true U is
 // [Ub 0; 0 I] . W where Ub = the first m_base rows of the U buffer (width
