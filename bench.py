@@ -496,6 +496,8 @@ def run_gpu(args):
 
     t_init = time.perf_counter()
     eng = BatchedSvdEngine(a0, K, m_cap=m_cap, k_cap=K)
+    if args.window:
+        _lib.check(lib.isvd_engine_set_lazy_window(eng._h.h, args.window))
     eng.synchronize()
     init_s = time.perf_counter() - t_init
     eng.snapshot()
@@ -672,6 +674,8 @@ def main():
     ap.add_argument("--cpu-events", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-k128", action="store_true", help="skip the config-5b (k=128) leg")
+    ap.add_argument("--window", type=int, default=0,
+                    help="deferred-U window for config 5a (0 = the engine default)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

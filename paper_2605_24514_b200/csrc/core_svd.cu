@@ -324,10 +324,12 @@ __device__ __forceinline__ void j32_apply_v(double (&v)[32], const double2* log)
 // the G phase needs ~half the registers and more cores fit per SM) and is
 // rotated once per sweep by replaying the log.
 struct J32Smem {
-  double2 log[32 * 16];
+  double2 log[32 * 16];  // also the 32 x 32 (XOR-swizzled) staging tile of G for the U output
   double V[32][33];
   double nrm[32];
+  double inv[32];
   int pos[32];
+  int ipos[32];
 };
 
 template <bool BUILD>
@@ -361,7 +363,13 @@ __global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32_kernel(
       } else {
         const double* ur = rc.U.p + b * rc.U.stride + i * rc.U.ld;
         const double* Wb = lz.W.p + b * lz.W.stride;
-        for (int c = 0; c < lz.r_base; ++c) ap = fma(ur[c], Wb[c * lz.W.ld + lane], ap);
+        double a4[4] = {0.0, 0.0, 0.0, 0.0};  // four independent chains
+        int c = 0;
+        for (; c + 4 <= lz.r_base; c += 4)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) a4[u] = fma(ur[c + u], Wb[(c + u) * lz.W.ld + lane], a4[u]);
+        for (; c < lz.r_base; ++c) a4[0] = fma(ur[c], Wb[c * lz.W.ld + lane], a4[0]);
+        ap = (a4[0] + a4[1]) + (a4[2] + a4[3]);
       }
     }
     const double* vr = rc.V.p + b * rc.V.stride + j * rc.V.ld;
@@ -476,10 +484,9 @@ __global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32_kernel(
       rank += (o > mine) || (o == mine && oid < myid);
     }
     pos[lane] = rank;
+    W.ipos[rank] = lane;
   }
-  __syncwarp();
-  double s0 = 0.0;
-  for (int p = 0; p < 32; ++p) s0 = fmax(s0, nrm[p]);
+  const double s0 = warp_max(nrm[lane]);
   double* U = uk + b * out_stride;
   double* Vo = vk + b * out_stride;
   double* S = sv + b * sv_stride;
@@ -488,16 +495,22 @@ __global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32_kernel(
     const double r = nrm[lane];
     const bool live = r > 0.0 && !(r < kZeroSvRtol * s0);
     if (id_of(lane) < s) S[pos[lane]] = live ? r : 0.0;
+    W.inv[lane] = live ? 1.0 / r : 0.0;  // U = G / sigma_raw (_kernels.pyx:104)
     any_dead = __any_sync(0xffffffffu, id_of(lane) < s && !live);
   }
-  if (lane < s) {
+  // Coalesced output: stage this lane's row of G in smem (column p at p ^ row
+  // so the 32 rows hit distinct banks), then write U and V one row per
+  // instruction with the lanes over the sorted output columns.
+  double* Gs = reinterpret_cast<double*>(W.log);
 #pragma unroll
-    for (int p = 0; p < 32; ++p) {
-      if (id_of(p) >= s) continue;
-      const double r = nrm[p];
-      const bool live = r > 0.0 && !(r < kZeroSvRtol * s0);
-      U[lane * ldo + pos[p]] = live ? g[p] / r : 0.0;
-      Vo[lane * ldo + pos[p]] = W.V[lane][p];
+  for (int p = 0; p < 32; ++p) Gs[lane * 32 + (p ^ lane)] = g[p];
+  __syncwarp();
+  if (lane < s) {
+    const int src = W.ipos[lane];  // the column that lands in output column `lane`
+    const double iv = W.inv[src];
+    for (int i = 0; i < s; ++i) {
+      U[i * ldo + lane] = Gs[i * 32 + (src ^ i)] * iv;
+      Vo[i * ldo + lane] = W.V[i][src];
     }
   }
   __syncwarp();
