@@ -124,16 +124,22 @@ __global__ void __launch_bounds__(WIDE ? 512 : (kN + 31) / 32 * 32) arrow_svd_ke
   double* SV = sv + b * sv_stride;
   const double eps = 2.220446049250313e-16;
 
-  // ---- load, scale
+  // ---- load, scale (max over the block: warp maxima, then one smem pass)
+  __shared__ double wmax[16];
+  double mx = 0.0;
   for (int c = tid; c < n; c += blockDim.x) {
-    S.delta[c] = c < r ? fabs(K[c * ldcore + c]) : 0.0;
-    S.z[c] = K[r * ldcore + c];
+    const double dc = c < r ? fabs(K[c * ldcore + c]) : 0.0, zc = K[r * ldcore + c];
+    S.delta[c] = dc;
+    S.z[c] = zc;
+    mx = fmax(mx, fmax(dc, fabs(zc)));
   }
+  mx = warp_max(mx);
+  if ((tid & 31) == 0) wmax[tid >> 5] = mx;
   __syncthreads();
   if (tid == 0) {
-    double mx = 0.0;
-    for (int c = 0; c < n; ++c) mx = fmax(mx, fmax(S.delta[c], fabs(S.z[c])));
-    S.scale = mx > 0.0 ? mx : 1.0;
+    double m2 = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m2 = fmax(m2, wmax[w]);
+    S.scale = m2 > 0.0 ? m2 : 1.0;
   }
   __syncthreads();
   const double scale = S.scale;
@@ -155,11 +161,11 @@ __global__ void __launch_bounds__(WIDE ? 512 : (kN + 31) / 32 * 32) arrow_svd_ke
   }
   __syncthreads();
 
-  // ---- deflation.  WIDE: if no pole needs deflating (every |z| > tol, no
-  // pole pair closer than tol, only the rho column at zero) every pole is kept
-  // in sorted order -- filled in parallel; otherwise the sequential pass.
+  // ---- deflation.  If no pole needs deflating (every |z| > tol, no pole
+  // pair closer than tol, only the rho column at zero) every pole is kept in
+  // sorted order -- filled in parallel; otherwise the sequential pass.
   bool serial = true;
-  if (WIDE) {
+  {
     const double tol = 8.0 * eps;
     bool need = false;
     for (int p = tid; p < n; p += blockDim.x) {
@@ -493,9 +499,16 @@ __global__ void __launch_bounds__(WIDE ? 512 : (kN + 31) / 32 * 32) arrow_svd_ke
     }
     S.pos[t] = rank;
   }
+  // largest singular value: block max (the previous sync made sig visible)
+  {
+    double m1 = 0.0;
+    for (int t = tid; t < n; t += blockDim.x) m1 = fmax(m1, S.sig[t]);
+    m1 = warp_max(m1);
+    if ((tid & 31) == 0) wmax[tid >> 5] = m1;
+  }
   csync();
   double smax = 0.0;
-  for (int t = 0; t < n; ++t) smax = fmax(smax, S.sig[t]);
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) smax = fmax(smax, wmax[w]);
 
   // ---- vectors, written straight into their sorted columns
   if (WIDE && ND == 0 && S.nrot == 0) {
