@@ -20,6 +20,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -89,16 +91,22 @@ static int check_device() {
 // Host-side finiteness check of event payloads (the reference's as_vector,
 // linalg.py:31-40).  Branch-free exponent test so the loop vectorises.
 static bool finite_chunk(const double* p, size_t n) {
-  const uint64_t* u = reinterpret_cast<const uint64_t*>(p);
-  const uint64_t ex = 0x7ff0000000000000ull;
-  uint64_t bad = 0;
-  for (size_t i = 0; i < n; ++i) bad |= (uint64_t)((u[i] & ex) == ex);
-  return bad == 0;
+  // x - x is 0 for finite x and NaN for +-inf / NaN; eight independent
+  // accumulators let the compiler keep the loop in SIMD registers (the scan
+  // is bound by host memory bandwidth, one pass)
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  size_t i = 0;
+  for (; i + 8 <= n; i += 8)
+    for (int k = 0; k < 8; ++k) acc[k] += p[i + k] - p[i + k];
+  double tail = 0.0;
+  for (; i < n; ++i) tail += p[i] - p[i];
+  const double tot = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7])) + tail;
+  return tot == 0.0;
 }
 
-// One pass on the calling thread: the scan is memory-bound (~20 GB/s on one
-// core), and helper threads measurably slowed the GPU work the host overlaps
-// it with (tools/e2e_probe5a_loop.py), so it stays serial.
+// One pass on the calling thread (a 5a row tick carries 8 MB): helper
+// threads were measured to slow the GPU work the host overlaps the scan with
+// (tools/e2e_loop_probe.py), so it stays serial.
 static bool all_finite(const double* p, size_t n) { return finite_chunk(p, n); }
 
 }  // namespace isvd
