@@ -97,7 +97,7 @@ __device__ __forceinline__ void apply_rots(double* col, int64_t stride, const SM
 // every CTA's shared memory over DSMEM, and cluster barriers separate the
 // phases.  At B = 1 this spreads the 129-root core over CL SMs.
 template <int kN, bool WIDE, int CL>
-__global__ void __launch_bounds__(WIDE ? 512 : (kN + 31) / 32 * 32) arrow_svd_kernel(int n, const double* __restrict__ core,
+__global__ void __launch_bounds__(WIDE ? 512 : 32) arrow_svd_kernel(int n, const double* __restrict__ core,
                                                        int64_t core_stride, int ldcore,
                                                        double* __restrict__ uk,
                                                        double* __restrict__ vk, int64_t out_stride,
@@ -260,10 +260,12 @@ __global__ void __launch_bounds__(WIDE ? 512 : (kN + 31) / 32 * 32) arrow_svd_ke
   csync();  // CL > 1: also guarantees every CTA of the cluster is resident before DSMEM use
   const int N = S.nkept, ND = S.ndefl;
 
-  // ---- roots: thread (WIDE: warp) i solves for sigma_i in (kd[i], kd[i+1])
-  if (WIDE) {
-    const int lane = tid & 31, nwarp = (blockDim.x >> 5) * CL;
-    for (int i = crank * (blockDim.x >> 5) + (tid >> 5); i < N; i += nwarp) {
+  // ---- roots: thread (WIDE: warp) i solves for sigma_i in (kd[i], kd[i+1]).
+  // warp_root: the 32 lanes of a warp solve one root together (lanes over the
+  // poles); used for every root when WIDE and, otherwise, for the roots left
+  // over once every thread has one (n = 33 with one warp per core).
+  auto warp_root = [&](int i) {
+    const int lane = tid & 31;
       int o;
       double lo, hi;
       const double di = S.kd[i];
@@ -367,9 +369,15 @@ __global__ void __launch_bounds__(WIDE ? 512 : (kN + 31) / 32 * 32) arrow_svd_ke
         atomicAdd(&g_arrow_counters[1], (unsigned long long)iters);
 #endif
       }
-    }
-  } else
-  for (int i = tid; i < N; i += blockDim.x) {
+      };
+  if (WIDE) {
+    const int nwarp = (blockDim.x >> 5) * CL;
+    for (int i = crank * (blockDim.x >> 5) + (tid >> 5); i < N; i += nwarp) warp_root(i);
+  } else {
+    for (int i = (int)blockDim.x + (tid >> 5); i < N; i += (int)(blockDim.x >> 5)) warp_root(i);
+  }
+  if (!WIDE)
+  for (int i = tid; i < N && i < (int)blockDim.x; i += blockDim.x) {
     int o;
     double lo, hi;
     const double di = S.kd[i];
@@ -676,10 +684,11 @@ int launch_arrow_svd(int batch, int s, const double* core, int64_t core_stride, 
     return ISVD_EINVAL;
   }
   if (batch == 0) return ISVD_OK;
-  const int threads = round_up(s, 32);
   if (s <= 40) {
-    arrow_svd_kernel<40, false, 1><<<batch, threads, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
-                                                              out_stride, ldo, sv, sv_stride);
+    // one warp per core: roots 32..39 (s = 33 is the k = 32 append core) are
+    // solved warp-cooperatively after the one-root-per-lane pass
+    arrow_svd_kernel<40, false, 1><<<batch, 32, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
+                                                         out_stride, ldo, sv, sv_stride);
   } else if (batch <= kClusterMaxBatch) {
     // few wide cores (config 5b: one 129 core per tick): a cluster per core
     cudaLaunchConfig_t cfg = {};
