@@ -72,14 +72,37 @@ __global__ void __launch_bounds__(256) project_append_kernel(
   double acc[RT];  // RT = ceil(r / 32) column tiles per lane
 #pragma unroll
   for (int t = 0; t < RT; ++t) acc[t] = 0.0;
-  for (int c = warp; c < rows; c += nw) {
-    const double xc = STAGE ? xs[c] : xb[c];
-    const double* fr = STAGE ? Fs + (size_t)c * F.ld : Fb + (int64_t)c * F.ld;
+  {
+    // two interleaved accumulator sets break the row-to-row FMA dependence
+    double acc2[RT];
 #pragma unroll
-    for (int t = 0; t < RT; ++t) {
-      int l = lane + 32 * t;
-      if (l < r) acc[t] = fma(fr[l], xc, acc[t]);
+    for (int t = 0; t < RT; ++t) acc2[t] = 0.0;
+    int c = warp;
+    for (; c + nw < rows; c += 2 * nw) {
+      const double xc = STAGE ? xs[c] : xb[c];
+      const double xd = STAGE ? xs[c + nw] : xb[c + nw];
+      const double* fr = STAGE ? Fs + (size_t)c * F.ld : Fb + (int64_t)c * F.ld;
+      const double* fd = STAGE ? Fs + (size_t)(c + nw) * F.ld : Fb + (int64_t)(c + nw) * F.ld;
+#pragma unroll
+      for (int t = 0; t < RT; ++t) {
+        const int l = lane + 32 * t;
+        if (l < r) {
+          acc[t] = fma(fr[l], xc, acc[t]);
+          acc2[t] = fma(fd[l], xd, acc2[t]);
+        }
+      }
     }
+    for (; c < rows; c += nw) {
+      const double xc = STAGE ? xs[c] : xb[c];
+      const double* fr = STAGE ? Fs + (size_t)c * F.ld : Fb + (int64_t)c * F.ld;
+#pragma unroll
+      for (int t = 0; t < RT; ++t) {
+        const int l = lane + 32 * t;
+        if (l < r) acc[t] = fma(fr[l], xc, acc[t]);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < RT; ++t) acc[t] += acc2[t];
   }
 #pragma unroll
   for (int t = 0; t < RT; ++t) {
@@ -99,12 +122,13 @@ __global__ void __launch_bounds__(256) project_append_kernel(
   if (STAGE) {
     for (int c = threadIdx.x; c < rows; c += blockDim.x) {
       const double* fr = Fs + (size_t)c * F.ld;
-      double v = 0.0;
+      double v4[4] = {0.0, 0.0, 0.0, 0.0};  // four independent chains
       int l = c % r;
       for (int j = 0; j < r; ++j) {
-        v = fma(fr[l], p[l], v);
+        v4[j & 3] = fma(fr[l], p[l], v4[j & 3]);
         l = (l + 1 == r) ? 0 : l + 1;
       }
+      const double v = (v4[0] + v4[1]) + (v4[2] + v4[3]);
       const double zc = xs[c] - v;
       zb[c] = zc;
       zz = fma(zc, zc, zz);
