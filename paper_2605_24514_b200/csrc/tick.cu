@@ -1,6 +1,7 @@
 // Per-tick kernels of the incremental update (kernels K1, K3-K6, K9).
 #include <algorithm>
 #include <type_traits>
+#include <cooperative_groups.h>
 #include "common.cuh"
 #include "core_svd.cuh"
 #include "tick.cuh"
@@ -311,6 +312,139 @@ __global__ void proj_split_core_kernel(int r, int S, int Sz, const double* __res
     xnorm_out[b] = sqrt(xnorm2);
     N[b] += xnorm2;
   }
+}
+
+// K1 for few long streams as ONE launch: a thread-block cluster of
+// kProjCluster CTAs per stream splits the rows; the partial projections and
+// residual norms meet in distributed shared memory (every CTA sums the
+// cluster's partials in the same order, so all hold the same p).
+constexpr int kProjCluster = 16;  // non-portable cluster size (B200 allows 16)
+
+template <int RT>
+__global__ void __launch_bounds__(256) proj_cluster_kernel(
+    int rows, int r, Mat F, const double* __restrict__ x, int64_t x_stride,
+    const double* __restrict__ s, int lds, double tol, double* __restrict__ core,
+    int64_t core_stride, int ldcore, double* __restrict__ z, int64_t z_stride,
+    double* __restrict__ inj_scale, double* __restrict__ rho_out, double* __restrict__ xnorm_out,
+    double* __restrict__ A, int64_t a_stride, int64_t a_off, int64_t a_step,
+    double* __restrict__ N, int arrow_only) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ double pw[8][kRMax];
+  __shared__ double ppart[kRMax + 1];  // this CTA's partial F^T x (and ||x||^2 at [r])
+  __shared__ double p[kRMax];
+  __shared__ double zpart;
+  __shared__ double red[32];
+  const int crank = (int)cl.block_rank();
+  const int b = blockIdx.x / kProjCluster;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int rps = (rows + kProjCluster - 1) / kProjCluster;
+  const int c0 = min(rows, crank * rps), c1 = min(rows, c0 + rps);
+  const double* Fb = F.p + b * F.stride;
+  const double* xb = x + b * x_stride;
+  double* Ab = A ? A + b * a_stride + a_off : nullptr;
+  double xx = 0.0;
+  for (int c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
+    const double xc = xb[c];
+    xx = fma(xc, xc, xx);
+    if (Ab) Ab[(int64_t)c * a_step] = xc;
+  }
+  double acc[RT], acc2[RT];
+#pragma unroll
+  for (int t = 0; t < RT; ++t) acc[t] = acc2[t] = 0.0;
+  {
+    int c = c0 + warp;
+    for (; c + nw < c1; c += 2 * nw) {
+      const double xc = xb[c], xd = xb[c + nw];
+      const double* fr = Fb + (int64_t)c * F.ld;
+      const double* fd = Fb + (int64_t)(c + nw) * F.ld;
+#pragma unroll
+      for (int t = 0; t < RT; ++t) {
+        const int l = lane + 32 * t;
+        if (l < r) {
+          acc[t] = fma(fr[l], xc, acc[t]);
+          acc2[t] = fma(fd[l], xd, acc2[t]);
+        }
+      }
+    }
+    for (; c < c1; c += nw) {
+      const double xc = xb[c];
+      const double* fr = Fb + (int64_t)c * F.ld;
+#pragma unroll
+      for (int t = 0; t < RT; ++t) {
+        const int l = lane + 32 * t;
+        if (l < r) acc[t] = fma(fr[l], xc, acc[t]);
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < RT; ++t) {
+    const int l = lane + 32 * t;
+    if (l < r) pw[warp][l] = acc[t] + acc2[t];
+  }
+  const double xt = block_sum(xx, red);  // also orders pw
+  for (int l = threadIdx.x; l < r; l += blockDim.x) {
+    double v = 0.0;
+    for (int w = 0; w < nw; ++w) v += pw[w][l];
+    ppart[l] = v;
+  }
+  if (threadIdx.x == 0) ppart[r] = xt;
+  cl.sync();
+  // p (and ||x||^2) = sum over the cluster's partials, fixed order
+  for (int l = threadIdx.x; l <= r; l += blockDim.x) {
+    double v = 0.0;
+    for (int k = 0; k < kProjCluster; ++k) v += cl.map_shared_rank(ppart, k)[l];
+    if (l < r) p[l] = v; else red[31] = v;
+  }
+  __syncthreads();
+  const double xnorm2 = red[31];
+  double* zb = z + b * z_stride;
+  double zz = 0.0;
+  for (int c = c0 + warp; c < c1; c += nw) {
+    const double* fr = Fb + (int64_t)c * F.ld;
+    double v = 0.0;
+    for (int l = lane; l < r; l += 32) v = fma(fr[l], p[l], v);
+    v = warp_sum(v);
+    const double zc = xb[c] - v;
+    if (lane == 0) {
+      zb[c] = zc;
+      zz = fma(zc, zc, zz);
+    }
+  }
+  const double zt = block_sum(zz, red);
+  if (threadIdx.x == 0) zpart = zt;
+  cl.sync();
+  double zsum = 0.0;
+  for (int k = 0; k < kProjCluster; ++k) zsum += *cl.map_shared_rank(&zpart, k);
+  const double rho = sqrt(zsum);
+  const bool fresh = rho > tol;
+  const int P = r + 1;
+  double* Kb = core + b * core_stride;
+  const double* sb = s + (int64_t)b * lds;
+  if (arrow_only) {
+    for (int j = crank * blockDim.x + threadIdx.x; j < P; j += kProjCluster * blockDim.x) {
+      if (j < r) Kb[j * ldcore + j] = sb[j];
+      Kb[r * ldcore + j] = (j < r) ? p[j] : (fresh ? rho : 0.0);
+    }
+  } else {
+    for (int i = crank; i < P; i += kProjCluster)
+      for (int j = threadIdx.x; j < P; j += blockDim.x) {
+        double v = 0.0;
+        if (i < r) {
+          if (i == j) v = sb[i];
+        } else {
+          v = (j < r) ? p[j] : (fresh ? rho : 0.0);
+        }
+        Kb[i * ldcore + j] = v;
+      }
+  }
+  if (crank == 0 && threadIdx.x == 0) {
+    inj_scale[b] = fresh ? 1.0 / rho : 0.0;
+    rho_out[b] = rho;
+    xnorm_out[b] = sqrt(xnorm2);
+    N[b] += xnorm2;
+  }
+  cl.sync();  // no CTA leaves while its partials may still be read
 }
 
 // out[l] = sum_t part[t * cnt + l], fixed order (row-sharded reductions, B = 1)
@@ -957,6 +1091,51 @@ int launch_project_append(int batch, int rows, int r, Mat F, const double* x, in
     ISVD_CUDA(cudaFreeAsync(part, st));
     ISVD_CUDA(cudaFreeAsync(zpart, st));
     ISVD_CUDA(cudaFreeAsync(vec, st));
+    return ISVD_OK;
+  }
+  if (batch <= 32 && (int64_t)rows * r >= 16384 && rows <= 8192) {
+    // few streams, moderate rows (config 5b's V: 1024 x 128): one cluster
+    // launch per tick instead of three kernels
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(batch * kProjCluster);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kProjCluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const int rt = (r + 31) / 32;
+    cudaError_t e;
+    switch (rt) {
+#define ISVD_PC_CASE(K)                                                                        \
+  case K:                                                                                      \
+    {                                                                                          \
+      static bool attr = false;                                                                \
+      if (!attr) {                                                                             \
+        ISVD_CUDA(cudaFuncSetAttribute(proj_cluster_kernel<K>,                                 \
+                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1));    \
+        attr = true;                                                                           \
+      }                                                                                        \
+    }                                                                                          \
+    e = cudaLaunchKernelEx(&cfg, proj_cluster_kernel<K>, rows, r, F, x, x_stride, s, lds, tol, \
+                           core, core_stride, ldcore, z, z_stride, inj_scale, rho_out,         \
+                           xnorm_out, A, a_stride, a_off, a_step, N, arrow_only);             \
+    break;
+      ISVD_PC_CASE(1)
+      ISVD_PC_CASE(2)
+      ISVD_PC_CASE(3)
+      ISVD_PC_CASE(4)
+      ISVD_PC_CASE(5)
+#undef ISVD_PC_CASE
+      default:
+        set_error("factor width exceeds kernel limit");
+        return ISVD_EINVAL;
+    }
+    ISVD_CUDA(e);
+    ISVD_LAUNCHED();
     return ISVD_OK;
   }
   if (batch <= 32 && (int64_t)rows * r >= 16384) {
