@@ -231,6 +231,10 @@ int isvd_engine_angle(isvd_engine* e, int which, const double* q, int q_cols,
  * quadratic form below -1e-10 is the reference's not-PSD ValueError. */
 int isvd_engine_risk(isvd_engine* e, int t, const double* w, int P, double* cov_out,
                      double* diag_out, double* out);
+/* low_rank_covariance (finance.py:326-335) of host factors: cov (n x n) =
+ * V diag(s^2) V^T / (t - 1), symmetrised, computed by the same device kernel
+ * (v is n x r row-major, i.e. Vt^T).  t >= 2 else ISVD_EINVAL. */
+int isvd_low_rank_cov(int n, int r, const double* v, const double* s, int t, double* cov);
 
 /* Dense thin SVD of B matrices (m x n each) on the device, in canonical
  * form (linalg.py:84-92).  Outputs: s (B x min(m,n)); u (B x m x w) and

@@ -63,6 +63,7 @@ SIGNATURES = {
     "isvd_engine_set_append_solver": (C.c_int, [_vp, C.c_int]),
     "isvd_engine_set_lazy": (C.c_int, [_vp, C.c_int]),
     "isvd_engine_risk": (C.c_int, [_vp, C.c_int, _dp, C.c_int, _dp, _dp, _dp]),
+    "isvd_low_rank_cov": (C.c_int, [C.c_int, C.c_int, _dp, _dp, C.c_int, _dp]),
     "isvd_engine_scalars_async": (C.c_int, [_vp, _vp, C.c_int]),
     "isvd_engine_scalars_wait": (C.c_int, [_vp, C.c_int]),
     "isvd_engine_set_shard": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int,

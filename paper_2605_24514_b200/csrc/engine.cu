@@ -1308,6 +1308,31 @@ int isvd_engine_risk(isvd_engine* e, int t, const double* w, int P, double* cov_
   return rc;
 }
 
+int isvd_low_rank_cov(int n, int r, const double* v, const double* s, int t, double* cov) {
+  if (n < 1 || r < 0 || !cov || (r > 0 && (!v || !s))) { set_error("bad argument"); return ISVD_EINVAL; }
+  if (t < 2) { set_error("need at least 2 rows for a covariance, got t=" + std::to_string(t)); return ISVD_EINVAL; }
+  ISVD_TRY(check_device());
+  double *vd = nullptr, *sd = nullptr, *cd = nullptr;
+  int rc = ISVD_OK;
+  auto T = [&](int x) { if (rc == ISVD_OK) rc = x; };
+  const int rr = std::max(r, 1);
+  T(dalloc(&vd, (size_t)n * rr));
+  T(dalloc(&sd, (size_t)rr));
+  T(dalloc(&cd, (size_t)n * n));
+  cudaStream_t st = 0;
+  if (rc == ISVD_OK && r > 0) {
+    T(cudaMemcpy(vd, v, sizeof(double) * n * r, cudaMemcpyHostToDevice) == cudaSuccess ? ISVD_OK : ISVD_ENODEV);
+    T(cudaMemcpy(sd, s, sizeof(double) * r, cudaMemcpyHostToDevice) == cudaSuccess ? ISVD_OK : ISVD_ENODEV);
+  }
+  if (rc == ISVD_OK)
+    T(launch_risk(1, n, r, Mat{vd, 0, rr}, sd, rr, nullptr, 0, 0, 0, 1.0 / (t - 1.0), nullptr, 0,
+                  cd, nullptr, nullptr, st));
+  if (rc == ISVD_OK)
+    T(cudaMemcpy(cov, cd, sizeof(double) * n * n, cudaMemcpyDeviceToHost) == cudaSuccess ? ISVD_OK : ISVD_ENODEV);
+  dfree(vd); dfree(sd); dfree(cd);
+  return rc;
+}
+
 static int gram_defect(isvd_engine* e, Mat X, int rows, int w, double* host_out,
                        bool row_sharded = false) {
   ISVD_TRY(e->ensure_work(0, 0, gram_part_elems(e->B, rows, w, w), (int64_t)e->B * w * w + e->B));

@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(256) frob_partial_kernel(int m, int n, int w, 
   __shared__ double red[32];
   const int b = blockIdx.y, blk = blockIdx.x;
   const int row0 = blk * kFrobRows;
-  const double* Ab = A + b * a_stride;
+  const double* Ab = A ? A + b * a_stride : nullptr;
   const double* Ub = U.p + b * U.stride;
   const double* Vb = V.p + b * V.stride;
   const double* sb = s + (int64_t)b * lds;
@@ -135,7 +135,7 @@ __global__ void risk_kernel(int n, int r, Mat V, const double* __restrict__ s, i
   const int b = blockIdx.x;
   const double* Vb = V.p + b * V.stride;
   const double* sb = s + (int64_t)b * lds;
-  const double* Ab = A + b * a_stride;
+  const double* Ab = A ? A + b * a_stride : nullptr;
   for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
     const int i = idx / n, j = idx % n;
     double cij = 0.0, cji = 0.0;
@@ -150,7 +150,8 @@ __global__ void risk_kernel(int n, int r, Mat V, const double* __restrict__ s, i
   __syncthreads();
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
     double acc = 0.0;
-    for (int i = 0; i < m; ++i) acc = fma(Ab[(int64_t)i * lda + j], Ab[(int64_t)i * lda + j], acc);
+    if (A)
+      for (int i = 0; i < m; ++i) acc = fma(Ab[(int64_t)i * lda + j], Ab[(int64_t)i * lda + j], acc);
     dd[j] = fmax(0.0, acc * inv_t1 - c[j * n + j]);
   }
   __syncthreads();

@@ -86,12 +86,21 @@ def risk(engine, t: int, portfolios, b: int = 0) -> RiskRecord:
                       {p.label: float(o[i, 2]) for i, p in enumerate(ports)})
 
 
-def low_rank_covariance(engine, t: int) -> np.ndarray:
-    """finance.py:326-335 from the engine's device factors."""
+def low_rank_covariance(f, t: int) -> np.ndarray:
+    """finance.py:326-335: V diag(s^2) V^T / (t - 1), symmetrised, on the
+    device -- from an engine's factors (no host copy) or from SvdFactors."""
     if t < 2:
         raise ValueError(f"need at least 2 rows for a covariance, got t={t}")
-    n = engine._h.shape()[2]
-    return risk(engine, t, [equal_weights(n)]).cov
+    if hasattr(f, "_h"):
+        n = f._h.shape()[2]
+        return risk(f, t, [equal_weights(n)]).cov
+    v = np.ascontiguousarray(np.asarray(f.vt, dtype=np.float64).T)
+    s = np.ascontiguousarray(np.asarray(f.s, dtype=np.float64))
+    n, r = v.shape
+    cov = np.empty((n, n))
+    _lib.check(_lib.load().isvd_low_rank_cov(n, r, _lib.dptr(v), _lib.dptr(s), int(t),
+                                             _lib.dptr(cov)))
+    return cov
 
 
 def covariance_rel_error(inc, orc) -> float:

@@ -52,3 +52,39 @@ def test_cfg3_risk_matches_host_restatement():
         risk(eng, 1, ports)
     with pytest.raises(ValueError):
         PortfolioSpec(np.array([0.5, 0.6]), "bad")
+
+
+class TestLowRankCovariance:
+    """finance.py:326-335 on the device (ported from the reference's
+    tests/test_finance.py TestLowRankCovariance)."""
+
+    def test_two_day_single_asset(self):
+        from paper_2605_24514_b200 import full_svd
+        f = full_svd(np.array([[1.0], [-1.0]]))
+        cov = low_rank_covariance(f, t=2)
+        assert cov.shape == (1, 1)
+        assert abs(cov[0, 0] - 2.0) < 1e-12
+
+    def test_orthogonal_columns_give_diagonal(self):
+        from paper_2605_24514_b200 import full_svd
+        r = np.array([[1.0, 0.0], [0.0, 2.0], [-1.0, 0.0], [0.0, -2.0]])
+        cov = low_rank_covariance(full_svd(r), t=4)
+        assert abs(cov[0, 1]) < 1e-12 and abs(cov[1, 0]) < 1e-12
+
+    def test_matches_gram_matrix(self):
+        from paper_2605_24514_b200 import full_svd
+        rng = np.random.default_rng(6)
+        r = rng.standard_normal((50, 6))
+        cov = low_rank_covariance(full_svd(r), t=50)
+        assert np.allclose(cov, r.T @ r / 49.0, atol=1e-9)
+
+    def test_symmetric(self):
+        from paper_2605_24514_b200 import full_svd
+        rng = np.random.default_rng(7)
+        cov = low_rank_covariance(full_svd(rng.standard_normal((30, 5))), t=30)
+        assert np.array_equal(cov, cov.T)
+
+    def test_needs_two_rows(self):
+        from paper_2605_24514_b200 import full_svd
+        with pytest.raises(ValueError):
+            low_rank_covariance(full_svd(np.ones((1, 2))), t=1)
