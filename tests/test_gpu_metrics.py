@@ -234,3 +234,43 @@ class TestStream:
         recs, eng = run_stream(a0, ev, 3, pol, log_every=10, return_engine=True)
         assert eng.work_rank > 3 and max(r.rank for r in recs) > 3
         assert eng.shape == (60, 15)
+
+    # ported from the reference's tests/test_stream.py simulation tests
+    def test_empty_stream_single_init_record(self):
+        a0, _ = _spec_events(20, 15, 3, "rank1", 0, 6)
+        recs = run_stream(a0, [], 3, log_every=50)
+        assert len(recs) == 1 and recs[0].step == 0
+        assert is_defined(recs[0].frob_opt)
+
+    def test_oracle_only_at_cadence(self):
+        a0, ev = _spec_events(20, 15, 3, "rank1", 120, 7)
+        recs = run_stream(a0, ev, 3, log_every=50)
+        for r in recs:
+            assert (r.opt_time is not None) == (r.step % 50 == 0)
+
+    def test_update_time_excludes_oracle_cost(self):
+        a0, ev = _spec_events(20, 15, 3, "rank1", 60, 8)
+        recs = run_stream(a0, ev, 3, log_every=60)
+        logged = [r for r in recs if r.step == 60][0]
+        assert logged.update_time >= 0.0 and logged.opt_time >= 0.0
+
+    def test_evr_rule_shrinks_oversized_rank(self):
+        rng = np.random.default_rng(9)
+        a0 = rng.standard_normal((20, 2)) @ rng.standard_normal((2, 15))
+        from paper_2605_24514_b200.stream import RankOneUpdate
+        ev = [RankOneUpdate(int(rng.integers(20)), int(rng.integers(15)),
+                            float(rng.normal(0, 0.01))) for _ in range(120)]
+        pol = PolicyConfig(kind="periodic", period=60,
+                           adaptive=AdaptiveRankConfig(tau=0.999, k_min=1, k_max=8, eta=0.5))
+        recs, eng = run_stream(a0, ev, 6, pol, log_every=20, return_engine=True)
+        assert eng.work_rank < 6
+
+    def test_rank1_stream_preserves_shape(self):
+        a0, ev = _spec_events(20, 15, 3, "rank1", 50, 10)
+        _, eng = run_stream(a0, ev, 3, log_every=50, return_engine=True)
+        assert eng.shape == (20, 15)
+
+    def test_structural_row_stream_grows_matrix(self):
+        a0, ev = _spec_events(20, 15, 3, "rows", 30, 11)
+        _, eng = run_stream(a0, ev, 3, log_every=50, return_engine=True)
+        assert eng.shape == (50, 15)
