@@ -102,7 +102,8 @@ __global__ void __launch_bounds__(WIDE ? 512 : 32) arrow_svd_kernel(int n, const
                                                        double* __restrict__ uk,
                                                        double* __restrict__ vk, int64_t out_stride,
                                                        int ldo, double* __restrict__ sv,
-                                                       int64_t sv_stride) {
+                                                       int64_t sv_stride, double* __restrict__ s_out,
+                                                       int64_t s_out_stride, int nkeep) {
   __shared__ ArrowSmem<kN> S;
   namespace cg = cooperative_groups;
   const int crank = CL > 1 ? (int)cg::this_cluster().block_rank() : 0;
@@ -122,6 +123,12 @@ __global__ void __launch_bounds__(WIDE ? 512 : 32) arrow_svd_kernel(int n, const
   double* U = uk + b * out_stride;
   double* V = vk + b * out_stride;
   double* SV = sv + b * sv_stride;
+  // the engine's s (first nkeep values) is written directly: no separate install copy
+  double* SO = s_out ? s_out + b * s_out_stride : nullptr;
+  auto put_sv = [&](int pc, double v) {
+    SV[pc] = v;
+    if (SO && pc < nkeep) SO[pc] = v;
+  };
   const double eps = 2.220446049250313e-16;
 
   // ---- load, scale (max over the block: warp maxima, then one smem pass)
@@ -546,7 +553,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 32) arrow_svd_kernel(int n, const
       }
       if (lane == 0) {
         U[r * ldo + pc] = dead ? 0.0 : -iu;
-        SV[pc] = dead ? 0.0 : sg * scale;
+        put_sv(pc, dead ? 0.0 : sg * scale);
       }
     }
   } else if (ND == 0 && S.nrot == 0) {
@@ -574,7 +581,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 32) arrow_svd_kernel(int n, const
         if (row != r) U[row * ldo + pc] = dead ? 0.0 : dj * vj * iu;
       }
       U[r * ldo + pc] = dead ? 0.0 : -iu;
-      SV[pc] = dead ? 0.0 : sg * scale;
+      put_sv(pc, dead ? 0.0 : sg * scale);
     }
   } else
   for (int t = crank * blockDim.x + tid; t < n; t += blockDim.x * CL) {
@@ -620,7 +627,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 32) arrow_svd_kernel(int n, const
       if (dead)
         for (int l = 0; l < n; ++l) ucol[l * ldo] = 0.0;
     }
-    SV[pc] = dead ? 0.0 : sg * scale;
+    put_sv(pc, dead ? 0.0 : sg * scale);
   }
   csync();  // every column of U / V / SV written (global, cluster scope)
   if (crank != 0) return;
@@ -678,7 +685,8 @@ int read_arrow_counters(int64_t* out4, int reset) {
 
 int launch_arrow_svd(int batch, int s, const double* core, int64_t core_stride, int ldcore,
                      double* uk, double* vk, int64_t out_stride, int ldo, double* sv,
-                     int64_t sv_stride, cudaStream_t st) {
+                     int64_t sv_stride, cudaStream_t st, double* s_out, int64_t s_out_stride,
+                     int nkeep) {
   if (s < 1 || s > kN) {
     set_error("arrow core size out of range");
     return ISVD_EINVAL;
@@ -688,7 +696,7 @@ int launch_arrow_svd(int batch, int s, const double* core, int64_t core_stride, 
     // one warp per core: roots 32..39 (s = 33 is the k = 32 append core) are
     // solved warp-cooperatively after the one-root-per-lane pass
     arrow_svd_kernel<40, false, 1><<<batch, 32, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
-                                                         out_stride, ldo, sv, sv_stride);
+                                                         out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep);
   } else if (batch <= kClusterMaxBatch) {
     // few wide cores (config 5b: one 129 core per tick): a cluster per core
     cudaLaunchConfig_t cfg = {};
@@ -706,23 +714,23 @@ int launch_arrow_svd(int batch, int s, const double* core, int64_t core_stride, 
     cudaError_t e;
     if (s <= 72)
       e = cudaLaunchKernelEx(&cfg, arrow_svd_kernel<72, true, kArrowCluster>, s, core, core_stride,
-                             ldcore, uk, vk, out_stride, ldo, sv, sv_stride);
+                             ldcore, uk, vk, out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep);
     else if (s <= 136)
       e = cudaLaunchKernelEx(&cfg, arrow_svd_kernel<136, true, kArrowCluster>, s, core,
-                             core_stride, ldcore, uk, vk, out_stride, ldo, sv, sv_stride);
+                             core_stride, ldcore, uk, vk, out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep);
     else
       e = cudaLaunchKernelEx(&cfg, arrow_svd_kernel<kN, true, kArrowCluster>, s, core, core_stride,
-                             ldcore, uk, vk, out_stride, ldo, sv, sv_stride);
+                             ldcore, uk, vk, out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep);
     ISVD_CUDA(e);
   } else if (s <= 72) {
     arrow_svd_kernel<72, true, 1><<<batch, 512, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
-                                                         out_stride, ldo, sv, sv_stride);
+                                                         out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep);
   } else if (s <= 136) {
     arrow_svd_kernel<136, true, 1><<<batch, 512, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
-                                                          out_stride, ldo, sv, sv_stride);
+                                                          out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep);
   } else {
     arrow_svd_kernel<kN, true, 1><<<batch, 512, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
-                                                         out_stride, ldo, sv, sv_stride);
+                                                         out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep);
   }
   ISVD_LAUNCHED();
   return ISVD_OK;

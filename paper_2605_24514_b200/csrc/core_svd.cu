@@ -336,7 +336,7 @@ template <bool BUILD>
 __global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32_kernel(
     int s, const double* __restrict__ core, int64_t core_stride, int ldcore, double* __restrict__ uk,
     double* __restrict__ vk, int64_t out_stride, int ldo, double* __restrict__ sv,
-    int64_t sv_stride, int batch, Rank1Core rc) {
+    int64_t sv_stride, int batch, Rank1Core rc, double* __restrict__ s_out, int64_t s_out_stride) {
   extern __shared__ __align__(16) unsigned char j32_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int b = blockIdx.x * kJ32Warps + warp;
@@ -494,7 +494,10 @@ __global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32_kernel(
   {
     const double r = nrm[lane];
     const bool live = r > 0.0 && !(r < kZeroSvRtol * s0);
-    if (id_of(lane) < s) S[pos[lane]] = live ? r : 0.0;
+    if (id_of(lane) < s) {
+      S[pos[lane]] = live ? r : 0.0;
+      if (s_out) s_out[b * s_out_stride + pos[lane]] = live ? r : 0.0;  // install s directly
+    }
     W.inv[lane] = live ? 1.0 / r : 0.0;  // U = G / sigma_raw (_kernels.pyx:104)
     any_dead = __any_sync(0xffffffffu, id_of(lane) < s && !live);
   }
@@ -556,7 +559,7 @@ size_t core_svd_smem_bytes(int s, bool v_in_smem) {
 
 int launch_rank1_core_svd32(int batch, int s, const Rank1Core& rc, double* uk, double* vk,
                             int64_t out_stride, int ldo, double* sv, int64_t sv_stride,
-                            cudaStream_t st) {
+                            cudaStream_t st, double* s_out, int64_t s_out_stride) {
   if (s < 1 || s > 32) {
     set_error("fused rank-1 core: width out of range");
     return ISVD_EINVAL;
@@ -570,7 +573,7 @@ int launch_rank1_core_svd32(int batch, int s, const Rank1Core& rc, double* uk, d
     attr = true;
   }
   jacobi32_kernel<true><<<ceil_div(batch, kJ32Warps), kJ32Warps * 32, smem, st>>>(
-      s, nullptr, 0, 0, uk, vk, out_stride, ldo, sv, sv_stride, batch, rc);
+      s, nullptr, 0, 0, uk, vk, out_stride, ldo, sv, sv_stride, batch, rc, s_out, s_out_stride);
   ISVD_LAUNCHED();
   return ISVD_OK;
 }
@@ -592,7 +595,8 @@ int launch_core_svd(int batch, int s, const double* core, int64_t core_stride, i
       j32_attr = true;
     }
     jacobi32_kernel<false><<<ceil_div(batch, kJ32Warps), kJ32Warps * 32, smem, st>>>(
-        s, core, core_stride, ldcore, uk, vk, out_stride, ldo, sv, sv_stride, batch, Rank1Core{});
+        s, core, core_stride, ldcore, uk, vk, out_stride, ldo, sv, sv_stride, batch, Rank1Core{},
+        nullptr, 0);
     ISVD_LAUNCHED();
     return ISVD_OK;
   }

@@ -44,11 +44,14 @@ struct Rank1Core {
 // the warp Jacobi (s <= 32); also applies A[i,j] += delta and the N update.
 int launch_rank1_core_svd32(int batch, int s, const Rank1Core& rc, double* uk, double* vk,
                             int64_t out_stride, int ldo, double* sv, int64_t sv_stride,
-                            cudaStream_t st);
+                            cudaStream_t st, double* s_out = nullptr, int64_t s_out_stride = 0);
 
 // Secular-equation SVD of the Brand append core [[diag d, 0], [p, rho]]
 // (arrow_svd.cu).  Same outputs and conventions as launch_core_svd.
+// s_out (optional): the first nkeep singular values are also written there
+// (the engine's s), replacing the separate install copy.
 int launch_arrow_svd(int batch, int s, const double* core, int64_t core_stride, int ldcore,
                      double* uk, double* vk, int64_t out_stride, int ldo, double* sv,
-                     int64_t sv_stride, cudaStream_t st);
+                     int64_t sv_stride, cudaStream_t st, double* s_out = nullptr,
+                     int64_t s_out_stride = 0, int nkeep = 0);
 }  // namespace isvd

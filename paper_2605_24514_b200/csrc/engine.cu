@@ -666,7 +666,8 @@ static int issue_append(isvd_engine* e, const Slice& sl, const double* xd, int l
     ISVD_TRY(launch_core_svd(nb, r + 1, core, cs, S, uk, vk, cs, S, sv, S,
                              e->vscr ? e->vscr + (int64_t)b0 * S * (S | 1) : nullptr, nullptr, st));
   else
-    ISVD_TRY(launch_arrow_svd(nb, r + 1, core, cs, S, uk, vk, cs, S, sv, S, st));
+    ISVD_TRY(launch_arrow_svd(nb, r + 1, core, cs, S, uk, vk, cs, S, sv, S, st,
+                              e->s + (int64_t)b0 * e->ld, e->ld, keep));
   if (one) e->mark();
   // row: U <- [U 0; 0 1] Uk, V <- V Vk[:r] + z^ Vk[r] ; col: the same with U<->V
   RotJob grow{mat_at(is_row ? e->Um() : e->Vm(), b0), is_row ? e->m : e->n, uk, cs, S, nullptr, 0,
@@ -686,8 +687,9 @@ static int issue_append(isvd_engine* e, const Slice& sl, const double* xd, int l
     ISVD_TRY(launch_rotate(nb, r, keep, wj, &injj, st));
   }
   if (one) e->mark();
-  // install: s <- sv[:, :keep], then the zero-sigma completion check
-  if (keep > 0)
+  // install: s <- sv[:, :keep] (the secular kernel already wrote it), then the
+  // zero-sigma completion check
+  if (keep > 0 && e->append_jacobi)
     ISVD_CUDA(cudaMemcpy2DAsync(e->s + (int64_t)b0 * e->ld, sizeof(double) * e->ld, sv,
                                 sizeof(double) * S, sizeof(double) * keep, nb,
                                 cudaMemcpyDeviceToDevice, st));
@@ -732,7 +734,8 @@ static int issue_rank_one(isvd_engine* e, const Slice& sl, const int64_t* di, co
     rc.N = e->N + b0;
     rc.lz = lz;
     if (one) e->mark();
-    ISVD_TRY(launch_rank1_core_svd32(nb, r, rc, uk, vk, cs, S, sv, S, st));
+    ISVD_TRY(launch_rank1_core_svd32(nb, r, rc, uk, vk, cs, S, sv, S, st,
+                                     e->s + (int64_t)b0 * e->ld, e->ld));
   } else if (e->sharded) {
     // U[i, :] and A[i, j] from the shard owning row i, summed across shards
     const int64_t il = e->sh_i - e->row0;
@@ -769,9 +772,10 @@ static int issue_rank_one(isvd_engine* e, const Slice& sl, const int64_t* di, co
     ISVD_TRY(launch_rotate(nb, r, r, wj, &jv, st));
   }
   if (one) e->mark();
-  ISVD_CUDA(cudaMemcpy2DAsync(e->s + (int64_t)b0 * e->ld, sizeof(double) * e->ld, sv,
-                              sizeof(double) * S, sizeof(double) * r, nb, cudaMemcpyDeviceToDevice,
-                              st));
+  if (!fused)  // the fused kernel installed s itself
+    ISVD_CUDA(cudaMemcpy2DAsync(e->s + (int64_t)b0 * e->ld, sizeof(double) * e->ld, sv,
+                                sizeof(double) * S, sizeof(double) * r, nb,
+                                cudaMemcpyDeviceToDevice, st));
   if (lazy_state != 0)
     ISVD_TRY(launch_complete_zero(nb, r, e->s + (int64_t)b0 * e->ld, e->ld, mat_at(e->Wm(), b0),
                                   e->r_base_next + e->lazy_b_next, mat_at(e->Vm(), b0), e->n, st));
