@@ -104,6 +104,8 @@ __global__ void __launch_bounds__(WIDE ? 512 : 32) arrow_svd_kernel(int n, const
                                                        int ldo, double* __restrict__ sv,
                                                        int64_t sv_stride, double* __restrict__ s_out,
                                                        int64_t s_out_stride, int nkeep) {
+  griddep_launch_dependents();
+  griddep_wait();
   __shared__ ArrowSmem<kN> S;
   namespace cg = cooperative_groups;
   const int crank = CL > 1 ? (int)cg::this_cluster().block_rank() : 0;
@@ -704,13 +706,15 @@ int launch_arrow_svd(int batch, int s, const double* core, int64_t core_stride, 
     cfg.blockDim = dim3(512);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = kArrowCluster;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     cudaError_t e;
     if (s <= 72)
       e = cudaLaunchKernelEx(&cfg, arrow_svd_kernel<72, true, kArrowCluster>, s, core, core_stride,

@@ -330,6 +330,8 @@ __global__ void __launch_bounds__(256) proj_cluster_kernel(
     double* __restrict__ N, int arrow_only) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
+  griddep_launch_dependents();
+  griddep_wait();
   __shared__ double pw[8][kRMax];
   __shared__ double ppart[kRMax + 1];  // this CTA's partial F^T x (and ||x||^2 at [r])
   __shared__ double p[kRMax];
@@ -638,6 +640,8 @@ constexpr int kRotNB = 8;              // output n-tiles per pass (independent D
 template <int KP>
 __global__ void __launch_bounds__(kRotWarps * 32, 1)
     rotate_kernel(int r, int keep, int NP, RotJob j0, RotJob j1, int nblk0, int rpb) {
+  griddep_launch_dependents();
+  griddep_wait();
   extern __shared__ double smem[];
   constexpr int KQ = KP / 4;
   const int NT = NP / 8;
@@ -893,6 +897,8 @@ __device__ void complete_column(double* X, int64_t ld, int rows, int w, int t, d
 
 __global__ void complete_zero_kernel(int w, const double* __restrict__ s, int lds, Mat U, int m,
                                      Mat V, int n) {
+  griddep_launch_dependents();
+  griddep_wait();
   extern __shared__ double coef[];  // [w]
   __shared__ double red[32];
   const int b = blockIdx.x;
@@ -1100,7 +1106,7 @@ int launch_project_append(int batch, int rows, int r, Mat F, const double* x, in
     cfg.gridDim = dim3(batch * kProjCluster);
     cfg.blockDim = dim3(256);
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = kProjCluster;
     at[0].val.clusterDim.y = 1;
@@ -1108,6 +1114,9 @@ int launch_project_append(int batch, int rows, int r, Mat F, const double* x, in
     cfg.attrs = at;
     cfg.numAttrs = 1;
     const int rt = (r + 31) / 32;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.numAttrs = 2;
     cudaError_t e;
     switch (rt) {
 #define ISVD_PC_CASE(K)                                                                        \
@@ -1266,7 +1275,8 @@ static int rotate_dispatch(int batch, int r, int keep, const RotJob& j0, const R
     }
   }
   dim3 grid(nb0 + nb1, batch);
-  rotate_kernel<KP><<<grid, kRotWarps * 32, smem, st>>>(r, keep, NP, j0, j1 ? *j1 : j0, nb0, rpb);
+  ISVD_CUDA(launch_ex(batch <= 32, 1, rotate_kernel<KP>, grid, dim3(kRotWarps * 32), smem, st, r,
+                      keep, NP, j0, j1 ? *j1 : j0, nb0, rpb));
   ISVD_LAUNCHED();
   return ISVD_OK;
 }
@@ -1317,7 +1327,8 @@ int launch_complete_zero(int batch, int w, const double* s, int lds, Mat U, int 
     set_error("complete_zero: width too large");
     return ISVD_EINVAL;
   }
-  complete_zero_kernel<<<batch, 256, smem, st>>>(w, s, lds, U, m, V, n);
+  ISVD_CUDA(launch_ex(batch <= 32, 1, complete_zero_kernel, dim3(batch), dim3(256), smem, st, w, s,
+                      lds, U, m, V, n));
   ISVD_LAUNCHED();
   return ISVD_OK;
 }
