@@ -449,10 +449,18 @@ def run_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("ISVD_BENCH_BACKEND", "nccl") != "nccl":
+        local %= max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        # ISVD_BENCH_BACKEND=gloo: functional check of the N > 1 path with all
+        # ranks on one GPU (not a measurement); NCCL otherwise
+        backend = os.environ.get("ISVD_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     from paper_2605_24514_b200 import BatchedSvdEngine, _lib
     from paper_2605_24514_b200.sharding import max_over_ranks, shard_streams
 

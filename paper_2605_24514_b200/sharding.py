@@ -29,6 +29,8 @@ def max_over_ranks(value: float, device=None) -> float:
 
     if not (dist.is_available() and dist.is_initialized()):
         return float(value)
+    if dist.get_backend() != "nccl":
+        device = None  # gloo reduces host tensors
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
@@ -40,6 +42,8 @@ def sum_over_ranks(value: float, device=None) -> float:
 
     if not (dist.is_available() and dist.is_initialized()):
         return float(value)
+    if dist.get_backend() != "nccl":
+        device = None
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
