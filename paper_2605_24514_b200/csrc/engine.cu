@@ -134,8 +134,11 @@ struct isvd_engine {
   cudaStream_t cp_st = nullptr;
   cudaEvent_t stage_free[2] = {}, stage_ready = nullptr;
   int stage_slot = 0;
+  volatile int* vflag_h = nullptr;  // pinned: the device finiteness verdict
   int ensure_copy_stream() {
     if (cp_st) return ISVD_OK;
+    ISVD_CUDA(cudaHostAlloc((void**)&vflag_h, sizeof(int), cudaHostAllocDefault));
+    *vflag_h = 0;
     ISVD_CUDA(cudaStreamCreateWithFlags(&cp_st, cudaStreamNonBlocking));
     for (auto& ev2 : stage_free) {
       ISVD_CUDA(cudaEventCreateWithFlags(&ev2, cudaEventDisableTiming));
@@ -460,6 +463,7 @@ struct isvd_engine {
       if (ev) cudaEventDestroy(ev);
     if (stage_ready) cudaEventDestroy(stage_ready);
     if (cp_st) cudaStreamDestroy(cp_st);
+    if (vflag_h) cudaFreeHost((void*)vflag_h);
     if (own_stream && st) cudaStreamDestroy(st);
   }
 };
@@ -813,8 +817,17 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
   if (!e || !x) { set_error("null argument"); return ISVD_EINVAL; }
   if (!e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
   const int len = is_row ? e->n : e->m;
-  if (!on_device && !all_finite(x, (size_t)e->B * len)) {
-    set_error(std::string(is_row ? "appended row" : "appended column") + " contains non-finite entries");
+  // Finiteness of a host payload (the reference's as_vector, linalg.py:31-40)
+  // is checked before anything changes the engine's logical state: small
+  // payloads on the host, large ones (a 5a row tick carries 8 MB) on the
+  // device right after the upload (below) -- the host then waits only for the
+  // transfer instead of scanning 8 MB itself.
+  const size_t nelem = (size_t)e->B * len;
+  const bool device_check = !on_device && nelem >= (size_t(1) << 16);
+  const std::string bad_msg =
+      std::string(is_row ? "appended row" : "appended column") + " contains non-finite entries";
+  if (!on_device && !device_check && !all_finite(x, nelem)) {
+    set_error(bad_msg);
     return ISVD_EINVAL;
   }
 
@@ -845,7 +858,20 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
     ISVD_CUDA(cudaStreamWaitEvent(e->cp_st, e->stage_free[slot], 0));
     ISVD_CUDA(cudaMemcpyAsync(staged, x, sizeof(double) * e->B * len, cudaMemcpyHostToDevice,
                               e->cp_st));
+    if (device_check) {
+      ISVD_CUDA(cudaMemsetAsync(e->dflag + 1, 0, sizeof(int), e->cp_st));
+      ISVD_TRY(launch_check_finite(nelem, staged, e->dflag + 1, e->cp_st));
+      ISVD_CUDA(cudaMemcpyAsync((void*)e->vflag_h, e->dflag + 1, sizeof(int), cudaMemcpyDeviceToHost,
+                                e->cp_st));
+    }
     ISVD_CUDA(cudaEventRecord(e->stage_ready, e->cp_st));
+    if (device_check) {
+      ISVD_CUDA(cudaEventSynchronize(e->stage_ready));
+      if (*e->vflag_h) {
+        set_error(bad_msg);
+        return ISVD_EINVAL;  // nothing consumed the staging slot; state unchanged
+      }
+    }
     ISVD_CUDA(cudaStreamWaitEvent(e->st, e->stage_ready, 0));
   }
   ISVD_TRY(run_groups(e, [&](const Slice& sl) {
