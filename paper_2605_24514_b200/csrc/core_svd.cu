@@ -265,12 +265,29 @@ __device__ __forceinline__ bool j32_round(double (&g)[32], int lane, double2* cs
   const bool rot = apq2 > (kOrthoEps * kOrthoEps) * pq && fmin(app, aqq) > null2;
   if (rot) {
     relmax = fmaxf(relmax, __fdividef((float)apq2, (float)pq));
-    const double zeta = (aqq - app) * j32_rcp(2.0 * apq);
-    const double w = fma(zeta, zeta, 1.0);
-    const double root = fabs(zeta) > 1e100 ? fabs(zeta) : w * j32_rsqrt(w);
-    t = copysign(j32_rcp(fabs(zeta) + root), zeta);
-    c = j32_rsqrt(fma(t, t, 1.0));
-    s = t * c;
+    // the same rotation as _kernels.pyx:40-44 (t = sign(zeta) / (|zeta| +
+    // sqrt(1 + zeta^2)), zeta = (a_qq - a_pp) / 2a_pq) written with d = a_qq -
+    // a_pp, h = 2 a_pq, u = |d| + sqrt(d^2 + h^2): t = sign(d) h / u,
+    // c = u / sqrt(u^2 + h^2), s = sign(d) h / sqrt(u^2 + h^2) -- two
+    // reciprocal square roots on the critical path instead of four MUFU steps
+    const double d = aqq - app, h = 2.0 * apq;
+    const double big = fmax(fabs(d), fabs(h));
+    if (big < 1e150 && big > 1e-140) {
+      const double x2 = fma(d, d, h * h);
+      const double u = fabs(d) + x2 * j32_rsqrt(x2);
+      const double qq = j32_rsqrt(fma(u, u, h * h));
+      const double sh = d < 0.0 ? -h : h;  // sign(d) h
+      c = u * qq;
+      s = sh * qq;
+      t = sh * j32_rcp(u);
+    } else {
+      const double zeta = d * j32_rcp(h);
+      const double w = fma(zeta, zeta, 1.0);
+      const double root = fabs(zeta) > 1e100 ? fabs(zeta) : w * j32_rsqrt(w);
+      t = copysign(j32_rcp(fabs(zeta) + root), zeta);
+      c = j32_rsqrt(fma(t, t, 1.0));
+      s = t * c;
+    }
   }
   const bool dummy = ODD && (lane >> 1) == 15;
   if (!dummy) {
