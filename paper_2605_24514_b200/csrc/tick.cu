@@ -32,8 +32,10 @@ __global__ void __launch_bounds__(256) project_append_kernel(
     double* __restrict__ inj_scale, double* __restrict__ rho_out, double* __restrict__ xnorm_out,
     double* __restrict__ A, int64_t a_stride, int64_t a_off, int64_t a_step,
     double* __restrict__ N, int arrow_only) {
-  __shared__ double part[8][kRMax];
-  __shared__ double p[kRMax];
+  // sized by RT, not kRMax: with a 64 KB staged F the static arrays decide
+  // whether 2 or 3 CTAs fit per SM
+  __shared__ double part[8][RT * 32];
+  __shared__ double p[RT * 32];
   __shared__ double red[32];
   __shared__ __align__(8) uint64_t bar;
   extern __shared__ __align__(128) double Fs[];  // STAGE: [rows][F.ld], then x[rows]
