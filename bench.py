@@ -264,18 +264,22 @@ def tick_bytes(B, m, n, w, row_tick):
     return 8 * B * (2 * m * w + 2 * n * w + 2 * w + 2)
 
 
-def _simulate_bytes(B, steps, window=32):
+def _simulate_bytes(B, steps, window=32, vdefer=True):
     """Algorithmic bytes of the per-tick kernels over `steps` ticks (simulating
     the engine's deferred-U window: W = (32 + b) x 32 rotated in place,
-    flushed every `window` appended rows)."""
+    flushed every `window` appended rows; and the deferred right basis: a
+    rank-1 tick writes its K x K right rotation G instead of rotating V, the
+    next row append reads G in its projection and folds it into its V pass)."""
     proj_bytes = rot_bytes = all_bytes = 0.0
-    m, b_rows, active = M0, 0, False
+    m, b_rows, active, vpend = M0, 0, False, False
     for t in range(steps):
         row = t % 2 == 0
         all_bytes += tick_bytes(B, m, N0, K, row)
         if row:
-            proj_bytes += 8.0 * B * (N0 * K + 2 * N0 + N0)   # V read, x read, A row, z write
-            vb = N0 * K + N0 * K + N0                         # V read/write + z read
+            g = K * K if vpend else 0                         # G read (projection, rotation)
+            proj_bytes += 8.0 * B * (N0 * K + 2 * N0 + N0 + g)  # V read, x read, A row, z write
+            vb = N0 * K + N0 * K + N0 + g                     # V read/write + z read
+            vpend = False
             if not active:
                 wb = (K + 1) * K                              # W = Uk copy
                 active, b_rows = True, 1
@@ -287,7 +291,11 @@ def _simulate_bytes(B, steps, window=32):
                 active, b_rows = False, 0
         else:
             proj_bytes += 8.0 * B * (2 * K + 2)               # U/V row gathers (+ W row)
-            vb = 2 * N0 * K
+            if not vdefer:
+                vb = 2 * N0 * K
+            else:                                             # G <- G Vk, or Vk written as G
+                vb = 2 * K * K if vpend else 0
+                vpend = True
             if not active:
                 wb = K * K
                 active, b_rows = True, 0

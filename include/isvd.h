@@ -194,6 +194,13 @@ int isvd_engine_set_lazy(isvd_engine* e, int on);
  * returns the current value (-1 for a null handle). */
 int isvd_engine_set_lazy_window(isvd_engine* e, int rows);
 int isvd_engine_lazy_window(isvd_engine* e);
+/* Deferred right-basis rotation: rank-1 updates rotate a small r x r G
+ * (V = V_base G) instead of V; the next row append projects through G and
+ * folds it into its own V rotation; flush() and every read of V materialise
+ * it.  mode 0 = off, 1 = on for batches >= 64 streams with r <= 32 (default),
+ * 2 = whenever the kernels support it (r <= 32, not row-sharded).  Flushes
+ * first. */
+int isvd_engine_set_vdefer(isvd_engine* e, int mode);
 /* Defect threshold of the optional re-orthonormalisation guard
  * (REORTHO_THRESHOLD, engine.py:30; default 1e-6). */
 int isvd_engine_set_reortho_threshold(isvd_engine* e, double threshold);

@@ -71,6 +71,7 @@ SIGNATURES = {
     "isvd_engine_shard_info": (C.c_int, [_vp, _ip64, _ip, _ip]),
     "isvd_engine_set_lazy_window": (C.c_int, [_vp, C.c_int]),
     "isvd_engine_lazy_window": (C.c_int, [_vp]),
+    "isvd_engine_set_vdefer": (C.c_int, [_vp, C.c_int]),
     "isvd_engine_set_reortho_threshold": (C.c_int, [_vp, C.c_double]),
     "isvd_engine_flush": (C.c_int, [_vp]),
     "isvd_engine_snapshot": (C.c_int, [_vp]),

@@ -390,13 +390,30 @@ __global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32_kernel(
       }
     }
     const double* vr = rc.V.p + b * rc.V.stride + j * rc.V.ld;
+    // lane q holds V_eff[j, q] (= V[j, :] . G[:, q] while V is deferred)
+    double vq = 0.0;
+    if (lane < s) {
+      if (!rc.G) {
+        vq = vr[lane];
+      } else {
+        const double* Gb = rc.G + b * rc.g_stride;
+        double a4[4] = {0.0, 0.0, 0.0, 0.0};
+        int c = 0;
+        for (; c + 4 <= s; c += 4)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) a4[u] = fma(vr[c + u], Gb[(c + u) * rc.ldg + lane], a4[u]);
+        for (; c < s; ++c) a4[0] = fma(vr[c], Gb[c * rc.ldg + lane], a4[0]);
+        vq = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+      }
+    }
     const double sp = lane < s ? rc.s[(int64_t)b * rc.lds + lane] : 0.0;
     const double da = d * ap;
 #pragma unroll
     for (int q = 0; q < 32; ++q) {
+      const double bq = __shfl_sync(0xffffffffu, vq, q);
       double v = 0.0;
       if (lane < s && q < s) {
-        v = da * vr[q];
+        v = da * bq;
         if (q == lane) v += sp;
       }
       g[q] = v;
@@ -505,7 +522,8 @@ __global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32_kernel(
   }
   const double s0 = warp_max(nrm[lane]);
   double* U = uk + b * out_stride;
-  double* Vo = vk + b * out_stride;
+  double* Vo = (BUILD && rc.vk_out) ? rc.vk_out + b * rc.vk_stride : vk + b * out_stride;
+  const int ldv = (BUILD && rc.vk_out) ? rc.ldvk : ldo;
   double* S = sv + b * sv_stride;
   bool any_dead;
   {
@@ -530,7 +548,7 @@ __global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32_kernel(
     const double iv = W.inv[src];
     for (int i = 0; i < s; ++i) {
       U[i * ldo + lane] = Gs[i * 32 + (src ^ i)] * iv;
-      Vo[i * ldo + lane] = W.V[i][src];
+      Vo[i * ldv + lane] = W.V[i][src];
     }
   }
   __syncwarp();

@@ -39,6 +39,15 @@ struct Rank1Core {
   int lda = 0;
   double* N = nullptr;
   LazyBasis lz{};
+  // Deferred right basis: V_eff = V . G (G: s x s per stream) when G != null
+  const double* G = nullptr;
+  int64_t g_stride = 0;
+  int ldg = 0;
+  // Optional separate destination for the core's right vectors (row-major,
+  // vk_stride per stream, leading dimension ldvk) instead of vk/ldo
+  double* vk_out = nullptr;
+  int64_t vk_stride = 0;
+  int ldvk = 0;
 };
 // K = diag(s) + delta U[i,:]^T Vt[:,j]^T built in registers and factored by
 // the warp Jacobi (s <= 32); also applies A[i,j] += delta and the N update.

@@ -212,6 +212,23 @@ struct isvd_engine {
   int m_base = 0, r_base = 0, lazy_b = 0;
   double* W = nullptr;
   int r_base_next = 0, lazy_b_next = 0;  // window state after the event being issued
+  // Deferred right-basis rotation: while vpend, the true V is V . Gv (Gv is
+  // r x r per stream; ld + 1 rows so a row append can grow it in place).
+  // Rank-1 ticks rotate the small Gv instead of the n x r V; the next row
+  // append projects through Gv and folds it into its own V rotation, so a
+  // rank-1 tick costs no pass over V.
+  int vdefer_mode = 1;  // 0 off, 1 on for batches >= 64, 2 whenever the kernels allow
+  bool vpend = false;
+  double* Gv = nullptr;
+  int64_t gstride() const { return (int64_t)(ld + 1) * ld; }
+  Mat Gm() const { return Mat{Gv, gstride(), ld}; }
+  bool vdefer_ok() const {
+    return vdefer_mode != 0 && !sharded && r >= 1 && k <= 32 && (vdefer_mode == 2 || B >= 64);
+  }
+  int ensure_gv() {
+    if (!Gv) ISVD_TRY(dalloc(&Gv, (size_t)B * gstride()));
+    return ISVD_OK;
+  }
   struct Snap {
     double *U = nullptr, *V = nullptr, *A = nullptr, *s = nullptr, *N = nullptr;
     size_t nu = 0, nv = 0, na = 0, ns = 0;
@@ -245,8 +262,22 @@ struct isvd_engine {
   std::vector<cudaEvent_t> flush_marks;
   double flush_bytes = 0.0;
 
-  // U <- [Ub 0; 0 I] W ; ends the deferred window
+  // V <- V Gv ; ends the deferred right basis
+  int flush_v() {
+    if (!vpend) return ISVD_OK;
+    RotJob jv{Vm(), n, Gv, gstride(), ld, nullptr, 0, nullptr, 0};
+    ISVD_TRY(launch_rotate(B, r, r, jv, nullptr, st));
+    vpend = false;
+    return ISVD_OK;
+  }
+  // materialise both deferred bases
   int flush() {
+    ISVD_TRY(flush_u());
+    return flush_v();
+  }
+
+  // U <- [Ub 0; 0 I] W ; ends the deferred window
+  int flush_u() {
     if (!lazy_active) return ISVD_OK;
     RotJob ju{Um(), m_base, W, wstride(), ld, nullptr, 0, nullptr, 0};
     if (timing) {
@@ -387,6 +418,7 @@ struct isvd_engine {
     U = U2; V = V2; s = s2;
     if (ref) { dfree(ref); ref = ref2; }
     ld = nld;
+    dfree(Gv);  // re-allocated with the new leading dimension when next used
     dfree(W);
     ISVD_TRY(dalloc(&W, (size_t)B * wstride()));
     ISVD_CUDA(cudaMemsetAsync(W, 0, sizeof(double) * B * wstride(), st));
@@ -428,6 +460,7 @@ struct isvd_engine {
     int sweeps = 0;
     lazy_active = false;  // U is recomputed from A
     lazy_b = 0;
+    vpend = false;
     if (sharded) {
       ISVD_TRY(gram_svd_run(m, n, A, n_cap, w, Um(), Vm(), s, nullptr, st, arp()));
     } else {
@@ -449,7 +482,7 @@ struct isvd_engine {
     dfree(U); dfree(V); dfree(s); dfree(A); dfree(N);
     dfree(core); dfree(uk); dfree(vk); dfree(sv); dfree(vscr);
     dfree(z); dfree(inj); dfree(rho); dfree(xnorm); dfree(ev);
-    dfree(ei); dfree(ej); dfree(ed); dfree(dflag); dfree(ref); dfree(W);
+    dfree(ei); dfree(ej); dfree(ed); dfree(dflag); dfree(ref); dfree(W); dfree(Gv);
     dfree(wx); dfree(wj); dfree(wpart); dfree(wout); dfree(wflags);
     dfree(snap.U); dfree(snap.V); dfree(snap.A); dfree(snap.s); dfree(snap.N); dfree(shv);
     for (auto g : gst) cudaStreamDestroy(g);
@@ -639,8 +672,10 @@ struct Slice {
 static Mat mat_at(const Mat& M, int b0) { return Mat{M.p + b0 * M.stride, M.stride, M.ld}; }
 
 // lazy_state: 0 = eager rotation, 1 = open a deferred window, 2 = continue it
+// vp: the right basis is deferred (V_eff = V Gv); this row append projects
+// through Gv and folds it into the V rotation
 static int issue_append(isvd_engine* e, const Slice& sl, const double* xd, int len, bool is_row,
-                        int keep, int lazy_state) {
+                        int keep, int lazy_state, bool vp) {
   const int b0 = sl.b0, nb = sl.nb, r = e->r;
   cudaStream_t st = sl.st;
   const int S = e->S();
@@ -664,7 +699,8 @@ static int issue_append(isvd_engine* e, const Slice& sl, const double* xd, int l
                                  e->zlen(), inj, e->rho + b0, e->xnorm + b0, Adst, e->astride(),
                                  a_off, a_step, e->N + b0, st,
                                  (e->sharded && !is_row) ? &e->ar : nullptr,
-                                 e->append_jacobi ? 0 : 1));
+                                 e->append_jacobi ? 0 : 1, vp ? e->Gv + b0 * e->gstride() : nullptr,
+                                 e->gstride(), e->ld));
   if (one) e->mark();
   if (e->append_jacobi)
     ISVD_TRY(launch_core_svd(nb, r + 1, core, cs, S, uk, vk, cs, S, sv, S,
@@ -678,17 +714,28 @@ static int issue_append(isvd_engine* e, const Slice& sl, const double* xd, int l
               nullptr, 1};
   RotJob injj{mat_at(is_row ? e->Vm() : e->Um(), b0), is_row ? e->n : e->m, vk, cs, S, z,
               e->zlen(), inj, 0};
-  if (lazy_state == 0) {
-    ISVD_TRY(launch_rotate(nb, r, keep, grow, &injj, st));
-  } else if (lazy_state == 1) {
+  RotJob uj = grow;  // the left side: U itself, or the deferred window W
+  bool has_u = true;
+  if (lazy_state == 1) {
     // open a deferred window: W = Uk[:, :keep] (rows: r base columns + the new row)
     ISVD_TRY(launch_copy_rows(nb, r + 1, keep, uk, cs, S, e->W + b0 * e->wstride(), e->wstride(),
                               e->ld, st));
-    ISVD_TRY(launch_rotate(nb, r, keep, injj, nullptr, st));
-  } else {
+    has_u = false;
+  } else if (lazy_state == 2) {
     // W <- [W 0; 0 1] Uk[:, :keep]  (in place, new row appended)
-    RotJob wj{mat_at(e->Wm(), b0), e->r_base + e->lazy_b, uk, cs, S, nullptr, 0, nullptr, 1};
-    ISVD_TRY(launch_rotate(nb, r, keep, wj, &injj, st));
+    uj = RotJob{mat_at(e->Wm(), b0), e->r_base + e->lazy_b, uk, cs, S, nullptr, 0, nullptr, 1};
+  }
+  if (vp) {
+    // fold the deferred right basis into this rotation: V <- V (Gv Vk[:r]) +
+    // z^ Vk[r] (the kernel forms Gv Vk[:r] per CTA) -- one pass over V
+    injj.G = e->Gv + b0 * e->gstride();
+    injj.g_stride = e->gstride();
+    injj.ldg = e->ld;
+  }
+  if (has_u) {
+    ISVD_TRY(launch_rotate(nb, r, keep, uj, &injj, st));
+  } else {
+    ISVD_TRY(launch_rotate(nb, r, keep, injj, nullptr, st));
   }
   if (one) e->mark();
   // install: s <- sv[:, :keep] (the secular kernel already wrote it), then the
@@ -707,8 +754,10 @@ static int issue_append(isvd_engine* e, const Slice& sl, const double* xd, int l
   return ISVD_OK;
 }
 
+// defer: leave V in place and rotate the deferred basis Gv instead (vp: Gv
+// is already pending; otherwise the core's right vectors open it)
 static int issue_rank_one(isvd_engine* e, const Slice& sl, const int64_t* di, const int64_t* dj,
-                          const double* dd, int lazy_state) {
+                          const double* dd, int lazy_state, bool defer, bool vp) {
   const int b0 = sl.b0, nb = sl.nb, r = e->r;
   cudaStream_t st = sl.st;
   const int S = e->S();
@@ -737,6 +786,15 @@ static int issue_rank_one(isvd_engine* e, const Slice& sl, const int64_t* di, co
     rc.lda = e->n_cap;
     rc.N = e->N + b0;
     rc.lz = lz;
+    if (vp) {
+      rc.G = e->Gv + b0 * e->gstride();
+      rc.g_stride = e->gstride();
+      rc.ldg = e->ld;
+    } else if (defer) {
+      rc.vk_out = e->Gv + b0 * e->gstride();
+      rc.vk_stride = e->gstride();
+      rc.ldvk = e->ld;
+    }
     if (one) e->mark();
     ISVD_TRY(launch_rank1_core_svd32(nb, r, rc, uk, vk, cs, S, sv, S, st,
                                      e->s + (int64_t)b0 * e->ld, e->ld));
@@ -763,29 +821,40 @@ static int issue_rank_one(isvd_engine* e, const Slice& sl, const int64_t* di, co
                              st));
   }
   if (one) e->mark();
-  RotJob ju{mat_at(e->Um(), b0), e->m, uk, cs, S, nullptr, 0, nullptr, 0};
-  RotJob jv{mat_at(e->Vm(), b0), e->n, vk, cs, S, nullptr, 0, nullptr, 0};
-  if (lazy_state == 0) {
-    ISVD_TRY(launch_rotate(nb, r, r, ju, &jv, st));
-  } else if (lazy_state == 1) {
+  RotJob uj{mat_at(e->Um(), b0), e->m, uk, cs, S, nullptr, 0, nullptr, 0};
+  bool has_u = true;
+  if (lazy_state == 1) {
     ISVD_TRY(launch_copy_rows(nb, r, r, uk, cs, S, e->W + b0 * e->wstride(), e->wstride(), e->ld,
                               st));
-    ISVD_TRY(launch_rotate(nb, r, r, jv, nullptr, st));
-  } else {
-    RotJob wj{mat_at(e->Wm(), b0), e->r_base + e->lazy_b, uk, cs, S, nullptr, 0, nullptr, 0};
-    ISVD_TRY(launch_rotate(nb, r, r, wj, &jv, st));
+    has_u = false;
+  } else if (lazy_state == 2) {
+    uj = RotJob{mat_at(e->Wm(), b0), e->r_base + e->lazy_b, uk, cs, S, nullptr, 0, nullptr, 0};
   }
+  // the right side: V itself, or Gv <- Gv Vk while deferred (nothing when
+  // the core kernel wrote Vk straight into a fresh Gv)
+  RotJob vj{mat_at(e->Vm(), b0), e->n, vk, cs, S, nullptr, 0, nullptr, 0};
+  bool has_v = true;
+  if (defer) {
+    if (vp)
+      vj = RotJob{mat_at(e->Gm(), b0), r, vk, cs, S, nullptr, 0, nullptr, 0};
+    else
+      has_v = false;
+  }
+  if (has_u || has_v)
+    ISVD_TRY(launch_rotate(nb, r, r, has_u ? uj : vj, (has_u && has_v) ? &vj : nullptr, st));
   if (one) e->mark();
   if (!fused)  // the fused kernel installed s itself
     ISVD_CUDA(cudaMemcpy2DAsync(e->s + (int64_t)b0 * e->ld, sizeof(double) * e->ld, sv,
                                 sizeof(double) * S, sizeof(double) * r, nb,
                                 cudaMemcpyDeviceToDevice, st));
+  const Mat vside = defer ? mat_at(e->Gm(), b0) : mat_at(e->Vm(), b0);
+  const int vrows = defer ? r : e->n;
   if (lazy_state != 0)
     ISVD_TRY(launch_complete_zero(nb, r, e->s + (int64_t)b0 * e->ld, e->ld, mat_at(e->Wm(), b0),
-                                  e->r_base_next + e->lazy_b_next, mat_at(e->Vm(), b0), e->n, st));
+                                  e->r_base_next + e->lazy_b_next, vside, vrows, st));
   else
     ISVD_TRY(launch_complete_zero(nb, r, e->s + (int64_t)b0 * e->ld, e->ld, mat_at(e->Um(), b0),
-                                  e->m, mat_at(e->Vm(), b0), e->n, st));
+                                  e->m, vside, vrows, st));
   return ISVD_OK;
 }
 
@@ -840,6 +909,10 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
     ISVD_TRY(e->grow_cols(e->n + 1));
   }
   if (!is_row) ISVD_TRY(e->flush());  // the column append projects on, and rotates, U
+  // a pending right basis is folded by this row append when its projection
+  // path can read through Gv, else materialised first
+  if (e->vpend && !project_append_takes_g(e->B, e->n, e->r)) ISVD_TRY(e->flush_v());
+  const bool vp = is_row && e->vpend;
   const int lazy_state = !(is_row && e->lazy_mode) ? 0 : (e->lazy_active ? 2 : 1);
   // window bookkeeping after this event (used by the completion check)
   e->r_base_next = lazy_state == 1 ? e->r : e->r_base;
@@ -877,8 +950,9 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
   ISVD_TRY(run_groups(e, [&](const Slice& sl) {
     const double* xd = x;
     if (!on_device) xd = staged;
-    return issue_append(e, sl, xd, len, is_row, keep, lazy_state);
+    return issue_append(e, sl, xd, len, is_row, keep, lazy_state, vp);
   }));
+  if (vp) e->vpend = false;
   if (!on_device) ISVD_CUDA(cudaEventRecord(e->stage_free[slot], e->st));
   if (lazy_state == 1) {
     e->lazy_active = true;
@@ -895,7 +969,7 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
     e->n += 1;
   }
   e->r = keep;
-  if (e->lazy_active && e->lazy_b >= e->lazy_rows) ISVD_TRY(e->flush());
+  if (e->lazy_active && e->lazy_b >= e->lazy_rows) ISVD_TRY(e->flush_u());
   ISVD_TRY(e->guard_step());
   if (e->ngroups_active == 1) e->mark();
   if (e->timing) { e->timed_ticks += 1; e->tick_kind.push_back(0); }
@@ -949,9 +1023,13 @@ int isvd_engine_rank_one(isvd_engine* e, const int64_t* i, const int64_t* j, con
   const int lazy_state = !e->lazy_mode ? 0 : (e->lazy_active ? 2 : 1);
   e->r_base_next = lazy_state == 1 ? e->r : e->r_base;
   e->lazy_b_next = lazy_state == 1 ? 0 : e->lazy_b;
+  if (e->vpend && !e->vdefer_ok()) ISVD_TRY(e->flush_v());
+  const bool defer = e->vdefer_ok(), vp = e->vpend;
+  if (defer) ISVD_TRY(e->ensure_gv());
   ISVD_TRY(run_groups(e, [&](const Slice& sl) {
-    return issue_rank_one(e, sl, di, dj, dd, lazy_state);
+    return issue_rank_one(e, sl, di, dj, dd, lazy_state, defer, vp);
   }));
+  if (defer) e->vpend = true;
   if (lazy_state == 1) {
     e->lazy_active = true;
     e->m_base = e->m;
@@ -1186,6 +1264,7 @@ int isvd_engine_restore(isvd_engine* e) {
   }
   e->lazy_active = false;
   e->lazy_b = 0;
+  e->vpend = false;
   ISVD_CUDA(cudaMemcpyAsync(e->U, S.U, S.nu * 8, cudaMemcpyDeviceToDevice, e->st));
   ISVD_CUDA(cudaMemcpyAsync(e->V, S.V, S.nv * 8, cudaMemcpyDeviceToDevice, e->st));
   ISVD_CUDA(cudaMemcpyAsync(e->A, S.A, S.na * 8, cudaMemcpyDeviceToDevice, e->st));
@@ -1226,6 +1305,14 @@ int isvd_engine_set_lazy_window(isvd_engine* e, int rows) {
 }
 
 int isvd_engine_lazy_window(isvd_engine* e) { return e ? e->lazy_rows : -1; }
+
+int isvd_engine_set_vdefer(isvd_engine* e, int mode) {
+  if (!e) { set_error("null engine"); return ISVD_EINVAL; }
+  if (mode < 0 || mode > 2) { set_error("vdefer mode must be 0, 1 or 2"); return ISVD_EINVAL; }
+  ISVD_TRY(e->flush_v());
+  e->vdefer_mode = mode;
+  return ISVD_OK;
+}
 
 int isvd_engine_set_append_solver(isvd_engine* e, int jacobi) {
   if (!e) { set_error("null engine"); return ISVD_EINVAL; }
@@ -1306,6 +1393,7 @@ int isvd_engine_risk(isvd_engine* e, int t, const double* w, int P, double* cov_
   if (!w || !out || P < 1) { set_error("risk: bad argument"); return ISVD_EINVAL; }
   if (t < 2) { set_error("need at least 2 rows for a covariance, got t=" + std::to_string(t)); return ISVD_EINVAL; }
   if (e->sharded) { set_error("risk needs the whole tracked matrix (not in shard mode)"); return ISVD_EINVAL; }
+  ISVD_TRY(e->flush_v());
   const int B = e->B, n = e->n;
   double *wd = nullptr, *cd = nullptr, *dd = nullptr, *od = nullptr;
   int rc = ISVD_OK;

@@ -31,11 +31,13 @@ __global__ void __launch_bounds__(256) project_append_kernel(
     int64_t core_stride, int ldcore, double* __restrict__ z, int64_t z_stride,
     double* __restrict__ inj_scale, double* __restrict__ rho_out, double* __restrict__ xnorm_out,
     double* __restrict__ A, int64_t a_stride, int64_t a_off, int64_t a_step,
-    double* __restrict__ N, int arrow_only) {
+    double* __restrict__ N, int arrow_only, const double* __restrict__ G, int64_t g_stride,
+    int ldg) {
   // sized by RT, not kRMax: with a 64 KB staged F the static arrays decide
   // whether 2 or 3 CTAs fit per SM
   __shared__ double part[8][RT * 32];
   __shared__ double p[RT * 32];
+  __shared__ double pg[2][RT * 32];  // deferred basis: G^T p and G G^T p
   __shared__ double red[32];
   __shared__ __align__(8) uint64_t bar;
   extern __shared__ __align__(128) double Fs[];  // STAGE: [rows][F.ld], then x[rows]
@@ -59,6 +61,17 @@ __global__ void __launch_bounds__(256) project_append_kernel(
       for (uint32_t off = 0; off < total; off += kPiece)
         bulk_g2s(reinterpret_cast<char*>(Fs) + off, reinterpret_cast<const char*>(Fb) + off,
                  min(kPiece, total - off), &bar);
+    }
+  }
+  // deferred right basis (r <= 32): lane l of warp w holds G[w + 8i][l],
+  // loaded while the bulk copy is in flight
+  double greg[4] = {0.0, 0.0, 0.0, 0.0};
+  if (RT == 1 && G) {
+    const double* Gb = G + b * g_stride;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int c = warp + 8 * i;
+      if (c < r && lane < r) greg[i] = Gb[c * ldg + lane];
     }
   }
   // x: norm, tracked-matrix write (and staging) overlap the bulk copy
@@ -119,6 +132,38 @@ __global__ void __launch_bounds__(256) project_append_kernel(
     p[l] = v;
   }
   double xnorm2 = block_sum(xx, red);  // contains __syncthreads, p visible after
+  // Deferred right basis (F_eff = F G, G r x r): the core takes G^T (F^T x)
+  // and the residual subtracts F (G G^T F^T x); F_eff is never formed.
+  const double* pc = p;  // projection coefficients of the core
+  const double* pz = p;  // coefficients multiplying F in z = x - F pz
+  if (RT == 1 && G) {
+    // G^T p: per-warp partial over its 4 rows of G, then across the 8 warps
+    // (part[] is free again: block_sum above synchronised after its reads)
+    double v = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int c = warp + 8 * i;
+      if (c < r) v = fma(greg[i], p[c], v);
+    }
+    part[warp][lane] = v;
+    __syncthreads();
+    if (warp == 0) {
+      double t = 0.0;
+      for (int w = 0; w < nw; ++w) t += part[w][lane];
+      pg[0][lane] = t;
+    }
+    __syncthreads();
+    // G (G^T p): one warp reduction per row of G
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int c = warp + 8 * i;
+      const double t = warp_sum(greg[i] * pg[0][lane]);
+      if (lane == 0 && c < r) pg[1][c] = t;
+    }
+    __syncthreads();
+    pc = pg[0];
+    pz = pg[1];
+  }
 
   double zz = 0.0;
   double* zb = z + b * z_stride;
@@ -128,7 +173,7 @@ __global__ void __launch_bounds__(256) project_append_kernel(
       double v4[4] = {0.0, 0.0, 0.0, 0.0};  // four independent chains
       int l = c % r;
       for (int j = 0; j < r; ++j) {
-        v4[j & 3] = fma(fr[l], p[l], v4[j & 3]);
+        v4[j & 3] = fma(fr[l], pz[l], v4[j & 3]);
         l = (l + 1 == r) ? 0 : l + 1;
       }
       const double v = (v4[0] + v4[1]) + (v4[2] + v4[3]);
@@ -140,7 +185,7 @@ __global__ void __launch_bounds__(256) project_append_kernel(
     for (int c = warp; c < rows; c += nw) {
       const double* fr = Fb + (int64_t)c * F.ld;
       double v = 0.0;
-      for (int l = lane; l < r; l += 32) v = fma(fr[l], p[l], v);
+      for (int l = lane; l < r; l += 32) v = fma(fr[l], pz[l], v);
       v = warp_sum(v);
       double zc = xb[c] - v;
       if (lane == 0) {
@@ -158,7 +203,7 @@ __global__ void __launch_bounds__(256) project_append_kernel(
     // the secular solver reads only the diagonal and the last row
     for (int j = threadIdx.x; j < P; j += blockDim.x) {
       if (j < r) Kb[j * ldcore + j] = sb[j];
-      Kb[r * ldcore + j] = (j < r) ? p[j] : (fresh ? rho : 0.0);
+      Kb[r * ldcore + j] = (j < r) ? pc[j] : (fresh ? rho : 0.0);
     }
   } else {
     for (int idx = threadIdx.x; idx < P * P; idx += blockDim.x) {
@@ -167,7 +212,7 @@ __global__ void __launch_bounds__(256) project_append_kernel(
       if (i < r) {
         if (i == j) v = sb[i];
       } else {
-        v = (j < r) ? p[j] : (fresh ? rho : 0.0);
+        v = (j < r) ? pc[j] : (fresh ? rho : 0.0);
       }
       Kb[i * ldcore + j] = v;
     }
@@ -775,11 +820,49 @@ __global__ void __launch_bounds__(kRegWarps * 32, 8)
   const bool has_last = (J.z != nullptr) || J.new_row;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
+  // deferred basis: this lane's G fragments, loaded before the fragment fill
+  // so the two latencies overlap
+  double ga[KQ];
+  if (J.G) {
+    const double* Gb = J.G + b * J.g_stride;
+    const int row = warp * 8 + g;
+#pragma unroll
+    for (int kk = 0; kk < KQ; ++kk) {
+      const int k = q * KQ + kk;
+      ga[kk] = (row < r && k < r) ? Gb[row * J.ldg + k] : 0.0;
+    }
+  }
 #pragma unroll 4
   for (int idx = threadIdx.x; idx < KQ * 4 * 32; idx += blockDim.x) {
     const int ln = idx & 31, nn = (idx >> 5) & 3, kk = idx >> 7;
     const int l = (ln & 3) * KQ + kk, c = nn * 8 + (ln >> 2);
     qf[idx] = (l < r && c < keep) ? Q[l * J.ldq + c] : 0.0;
+  }
+  if (J.G) {
+    // deferred right basis: Q[:r] <- G Q[:r] (G r x r) on the DMMA pipe, in
+    // the same k order as the fragments, written back in fragment order
+    __syncthreads();
+    const int row = warp * 8 + g;
+    double d[4][2];
+#pragma unroll
+    for (int nn = 0; nn < 4; ++nn) d[nn][0] = d[nn][1] = 0.0;
+    if (warp * 8 < KP) {
+#pragma unroll
+      for (int kk = 0; kk < KQ; ++kk)
+#pragma unroll
+        for (int nn = 0; nn < 4; ++nn)
+          dmma_8x8x4(d[nn][0], d[nn][1], ga[kk], qf[(kk * 4 + nn) * 32 + lane]);
+    }
+    __syncthreads();
+    if (warp * 8 < KP) {
+#pragma unroll
+      for (int nn = 0; nn < 4; ++nn)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = nn * 8 + 2 * q + e;
+          qf[((row % KQ) * 4 + nn) * 32 + (((c & 7) << 2) | (row / KQ))] = d[nn][e];
+        }
+    }
   }
   double qr[4][2];
 #pragma unroll
@@ -1061,14 +1144,23 @@ __global__ void check_finite_kernel(size_t n, const double* __restrict__ p, int*
 
 }  // namespace
 
+bool project_append_takes_g(int batch, int rows, int r) {
+  return r <= 32 && !(batch <= 32 && (int64_t)rows * r >= 16384);
+}
+
 int launch_project_append(int batch, int rows, int r, Mat F, const double* x, int64_t x_stride,
                           const double* s, int lds, double tol, double* core, int64_t core_stride,
                           int ldcore, double* z, int64_t z_stride, double* inj_scale,
                           double* rho_out, double* xnorm_out, double* A, int64_t a_stride,
                           int64_t a_off, int64_t a_step, double* N, cudaStream_t st,
-                          const Allreducer* ar, int arrow_only) {
+                          const Allreducer* ar, int arrow_only, const double* G,
+                          int64_t g_stride, int ldg) {
   if (r > kRMax) {
     set_error("factor width exceeds kernel limit");
+    return ISVD_EINVAL;
+  }
+  if (G && (ar || !project_append_takes_g(batch, rows, r))) {
+    set_error("deferred right basis not supported on this projection path");
     return ISVD_EINVAL;
   }
   if (ar) {
@@ -1188,7 +1280,7 @@ int launch_project_append(int batch, int rows, int r, Mat F, const double* x, in
     }
     project_append_kernel<SG, RT><<<batch, 256, SG ? stage : 0, st>>>(
         rows, r, F, x, x_stride, s, lds, tol, core, core_stride, ldcore, z, z_stride, inj_scale,
-        rho_out, xnorm_out, A, a_stride, a_off, a_step, N, arrow_only);
+        rho_out, xnorm_out, A, a_stride, a_off, a_step, N, arrow_only, G, g_stride, ldg);
     return ISVD_OK;
   };
   using T1 = std::integral_constant<bool, true>;
@@ -1288,6 +1380,10 @@ int launch_rotate(int batch, int r, int keep, const RotJob& j0, const RotJob* j1
   int KP = round_up(r < 1 ? 1 : r, 8);
   if (KP > kRMax || round_up(keep, 8) > j0.X.ld || (j1 && round_up(keep, 8) > j1->X.ld)) {
     set_error("rotation width exceeds kernel limit / leading dimension");
+    return ISVD_EINVAL;
+  }
+  if ((j0.G || (j1 && j1->G)) && (KP > 32 || round_up(keep, 8) > 32)) {
+    set_error("deferred right basis needs r, keep <= 32");
     return ISVD_EINVAL;
   }
   switch (KP) {

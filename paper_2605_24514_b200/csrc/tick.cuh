@@ -22,7 +22,12 @@ int launch_project_append(int batch, int rows, int r, Mat F, const double* x, in
                           int ldcore, double* z, int64_t z_stride, double* inj_scale,
                           double* rho_out, double* xnorm_out, double* A, int64_t a_stride,
                           int64_t a_off, int64_t a_step, double* N, cudaStream_t st,
-                          const struct Allreducer* ar = nullptr, int arrow_only = 0);
+                          const struct Allreducer* ar = nullptr, int arrow_only = 0,
+                          const double* G = nullptr, int64_t g_stride = 0, int ldg = 0);
+// Whether launch_project_append accepts a deferred right basis G (F_eff =
+// F G) for this shape (the one-CTA-per-stream path does; the split and
+// cluster paths for few long streams do not).
+bool project_append_takes_g(int batch, int rows, int r);
 
 // Deferred left basis: while active, the true U is
 // [Ub 0; 0 I] . W where Ub = the first m_base rows of the U buffer (width
@@ -61,6 +66,11 @@ struct RotJob {
   int64_t z_stride;
   const double* inj_scale;
   int new_row;
+  // optional deferred right basis: Q[:r] is replaced by G[:r, :r] Q[:r]
+  // (rotate_reg_kernel only: KP <= 32, keep <= 32)
+  const double* G = nullptr;
+  int64_t g_stride = 0;
+  int ldg = 0;
 };
 
 // K3/K4: both factor rotations of a tick in one launch (FP64 DMMA).

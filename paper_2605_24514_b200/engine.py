@@ -155,6 +155,11 @@ class BatchedSvdEngine:
         """Deferred left-basis rotation on (default) or off (eager per event)."""
         _lib.check(self._h.lib.isvd_engine_set_lazy(self._h.h, int(bool(on))))
 
+    def set_vdefer(self, mode: int) -> None:
+        """Deferred right-basis rotation on rank-1 updates: 0 off, 1 auto
+        (batches >= 64 streams, the default), 2 whenever supported."""
+        _lib.check(self._h.lib.isvd_engine_set_vdefer(self._h.h, int(mode)))
+
     def snapshot(self) -> None:
         """Device-side checkpoint of the whole state (restore() returns to it)."""
         _lib.check(self._h.lib.isvd_engine_snapshot(self._h.h))
@@ -453,6 +458,11 @@ class SvdEngine:
     def set_lazy(self, on: bool) -> None:
         """Deferred left-basis rotation on (default) or off (eager per event)."""
         _lib.check(self._h.lib.isvd_engine_set_lazy(self._h.h, int(bool(on))))
+
+    def set_vdefer(self, mode: int) -> None:
+        """Deferred right-basis rotation on rank-1 updates: 0 off, 1 auto
+        (batches >= 64 streams, the default), 2 whenever supported."""
+        _lib.check(self._h.lib.isvd_engine_set_vdefer(self._h.h, int(mode)))
 
     @property
     def reortho_threshold(self) -> float:
