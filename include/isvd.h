@@ -201,6 +201,10 @@ int isvd_engine_lazy_window(isvd_engine* e);
  * 2 = whenever the kernels support it (r <= 32, not row-sharded).  Flushes
  * first. */
 int isvd_engine_set_vdefer(isvd_engine* e, int mode);
+/* Stream groups: a batch of B streams is split into up to `groups` slices
+ * (each >= 256 streams) issued on separate CUDA streams so one slice's
+ * latency-bound core SVDs overlap another's HBM-bound passes (default 4). */
+int isvd_engine_set_groups(isvd_engine* e, int groups);
 /* Defect threshold of the optional re-orthonormalisation guard
  * (REORTHO_THRESHOLD, engine.py:30; default 1e-6). */
 int isvd_engine_set_reortho_threshold(isvd_engine* e, double threshold);

@@ -72,6 +72,7 @@ SIGNATURES = {
     "isvd_engine_set_lazy_window": (C.c_int, [_vp, C.c_int]),
     "isvd_engine_lazy_window": (C.c_int, [_vp]),
     "isvd_engine_set_vdefer": (C.c_int, [_vp, C.c_int]),
+    "isvd_engine_set_groups": (C.c_int, [_vp, C.c_int]),
     "isvd_engine_set_reortho_threshold": (C.c_int, [_vp, C.c_double]),
     "isvd_engine_flush": (C.c_int, [_vp]),
     "isvd_engine_snapshot": (C.c_int, [_vp]),

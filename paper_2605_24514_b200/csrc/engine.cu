@@ -129,10 +129,17 @@ struct isvd_engine {
   int64_t sh_i = 0, sh_j = 0;  // the rank-1 event being issued (sharded)
   double sh_d = 0.0;
   double* shv = nullptr;  // [kCoreMaxS + 2] cross-shard vector scratch
-  cudaEvent_t sc_ev[8] = {};  // isvd_engine_scalars_async tickets
+  // Completion ticket of work that may still run on the group streams: one
+  // event per pending group (or one on st).
+  struct Ticket {
+    std::vector<cudaEvent_t> ev;
+    int n = 0;
+  };
+  Ticket sc_tk[8];  // isvd_engine_scalars_async tickets
   // host-payload staging: copy stream, two slots of ev, their events
   cudaStream_t cp_st = nullptr;
-  cudaEvent_t stage_free[2] = {}, stage_ready = nullptr;
+  Ticket stage_tk[2];  // the ticks that last read each staging slot
+  cudaEvent_t stage_ready = nullptr;
   int stage_slot = 0;
   volatile int* vflag_h = nullptr;  // pinned: the device finiteness verdict
   int ensure_copy_stream() {
@@ -140,10 +147,6 @@ struct isvd_engine {
     ISVD_CUDA(cudaHostAlloc((void**)&vflag_h, sizeof(int), cudaHostAllocDefault));
     *vflag_h = 0;
     ISVD_CUDA(cudaStreamCreateWithFlags(&cp_st, cudaStreamNonBlocking));
-    for (auto& ev2 : stage_free) {
-      ISVD_CUDA(cudaEventCreateWithFlags(&ev2, cudaEventDisableTiming));
-      ISVD_CUDA(cudaEventRecord(ev2, st));
-    }
     ISVD_CUDA(cudaEventCreateWithFlags(&stage_ready, cudaEventDisableTiming));
     return ISVD_OK;
   }
@@ -154,6 +157,7 @@ struct isvd_engine {
   // engine.py:205-206,210-217: after an event, refactor if the factors drifted
   int guard_step() {
     if (!guard || r < 1) return ISVD_OK;
+    join();
     ISVD_TRY(flush());
     std::vector<double> du(B), dv(B);
     ISVD_TRY(reortho_defects(B, r, Um(), m, Vm(), n, du.data(), dv.data(), st, arp()));
@@ -242,6 +246,38 @@ struct isvd_engine {
   std::vector<cudaStream_t> gst;
   cudaEvent_t fork_ev = nullptr;
   std::vector<cudaEvent_t> join_ev;
+  // Deferred join: a tick leaves its group streams running (each group's next
+  // tick is ordered after its own previous one on the same group stream), so
+  // successive ticks of different groups overlap -- one group's core SVDs run
+  // beside another's HBM passes.  Every other use of the engine stream joins
+  // first (join()), so st still orders all engine work for the caller.
+  bool async_groups = true, pend = false;
+  int pend_G = 0;
+  void join() {
+    if (!pend) return;
+    for (int g = 0; g < pend_G; ++g) cudaStreamWaitEvent(st, join_ev[g], 0);
+    pend = false;
+  }
+  // record: the point every group stream (or st) has reached now
+  int ticket_record(Ticket& t) {
+    const int n = pend ? pend_G : 1;
+    while ((int)t.ev.size() < n) {
+      cudaEvent_t ev;
+      ISVD_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      t.ev.push_back(ev);
+    }
+    for (int g = 0; g < n; ++g) ISVD_CUDA(cudaEventRecord(t.ev[g], pend ? gst[g] : st));
+    t.n = n;
+    return ISVD_OK;
+  }
+  int ticket_wait(cudaStream_t s2, const Ticket& t) {
+    for (int g = 0; g < t.n; ++g) ISVD_CUDA(cudaStreamWaitEvent(s2, t.ev[g], 0));
+    return ISVD_OK;
+  }
+  int ticket_sync(const Ticket& t) {
+    for (int g = 0; g < t.n; ++g) ISVD_CUDA(cudaEventSynchronize(t.ev[g]));
+    return ISVD_OK;
+  }
   int ensure_groups(int G) {
     if (!fork_ev) ISVD_CUDA(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
     while ((int)gst.size() < G) {
@@ -265,6 +301,7 @@ struct isvd_engine {
   // V <- V Gv ; ends the deferred right basis
   int flush_v() {
     if (!vpend) return ISVD_OK;
+    join();
     RotJob jv{Vm(), n, Gv, gstride(), ld, nullptr, 0, nullptr, 0};
     ISVD_TRY(launch_rotate(B, r, r, jv, nullptr, st));
     vpend = false;
@@ -276,10 +313,12 @@ struct isvd_engine {
     return flush_v();
   }
 
-  // U <- [Ub 0; 0 I] W ; ends the deferred window
-  int flush_u() {
+  // U <- [Ub 0; 0 I] W ; ends the deferred window.  in_tick: issued per
+  // stream group on the group streams (no join) when the groups are pending.
+  int flush_u(bool in_tick = false) {
     if (!lazy_active) return ISVD_OK;
-    RotJob ju{Um(), m_base, W, wstride(), ld, nullptr, 0, nullptr, 0};
+    const bool grouped = in_tick && pend && !timing;
+    if (!grouped) join();
     if (timing) {
       cudaEvent_t ev;
       cudaEventCreate(&ev);
@@ -289,16 +328,31 @@ struct isvd_engine {
       flush_bytes += 8.0 * B * ((double)m_base * (r_base + r) + (double)(r_base + lazy_b) * r +
                                 (double)lazy_b * r);
     }
-    ISVD_TRY(launch_rotate(B, r_base, r, ju, nullptr, st));
-    if (timing) {
-      cudaEvent_t ev;
-      cudaEventCreate(&ev);
-      cudaEventRecord(ev, st);
-      flush_marks.push_back(ev);
+    auto body = [&](int b0, int nb, cudaStream_t s2) -> int {
+      RotJob ju{Mat{U + b0 * ustride(), ustride(), ld}, m_base, W + b0 * wstride(), wstride(), ld,
+                nullptr, 0, nullptr, 0};
+      ISVD_TRY(launch_rotate(nb, r_base, r, ju, nullptr, s2));
+      if (timing) {
+        cudaEvent_t ev;
+        cudaEventCreate(&ev);
+        cudaEventRecord(ev, s2);
+        flush_marks.push_back(ev);
+      }
+      if (lazy_b > 0 && owner)  // appended rows live on the owner shard only
+        ISVD_TRY(launch_copy_rows(nb, lazy_b, r, W + b0 * wstride() + (int64_t)r_base * ld,
+                                  wstride(), ld, U + b0 * ustride() + (int64_t)m_base * ld,
+                                  ustride(), ld, s2));
+      return ISVD_OK;
+    };
+    if (grouped) {
+      for (int g = 0; g < pend_G; ++g) {
+        const int b0 = (int)((int64_t)B * g / pend_G), b1 = (int)((int64_t)B * (g + 1) / pend_G);
+        ISVD_TRY(body(b0, b1 - b0, gst[g]));
+        ISVD_CUDA(cudaEventRecord(join_ev[g], gst[g]));
+      }
+    } else {
+      ISVD_TRY(body(0, B, st));
     }
-    if (lazy_b > 0 && owner)  // appended rows live on the owner shard only
-      ISVD_TRY(launch_copy_rows(B, lazy_b, r, W + (int64_t)r_base * ld, wstride(), ld,
-                                U + (int64_t)m_base * ld, ustride(), ld, st));
     lazy_active = false;
     lazy_b = 0;
     return ISVD_OK;
@@ -357,6 +411,7 @@ struct isvd_engine {
   // grow U (rows) and A (rows) to hold at least rows_needed rows
   int grow_rows(int rows_needed) {
     if (rows_needed <= m_cap) return ISVD_OK;
+    join();
     int nc = std::max(rows_needed, m_cap * 2);
     double *U2, *A2;
     ISVD_TRY(dalloc(&U2, (size_t)B * nc * ld));
@@ -373,6 +428,7 @@ struct isvd_engine {
 
   int grow_cols(int cols_needed) {
     if (cols_needed <= n_cap) return ISVD_OK;
+    join();
     int nc = std::max(cols_needed, n_cap * 2);
     double *V2, *A2;
     ISVD_TRY(dalloc(&V2, (size_t)B * nc * ld));
@@ -490,10 +546,10 @@ struct isvd_engine {
     if (fork_ev) cudaEventDestroy(fork_ev);
     for (auto ev : ev_marks) cudaEventDestroy(ev);
     for (auto ev : ev_pool) cudaEventDestroy(ev);
-    for (auto ev : sc_ev)
-      if (ev) cudaEventDestroy(ev);
-    for (auto ev : stage_free)
-      if (ev) cudaEventDestroy(ev);
+    for (auto& t : sc_tk)
+      for (auto ev : t.ev) cudaEventDestroy(ev);
+    for (auto& t : stage_tk)
+      for (auto ev : t.ev) cudaEventDestroy(ev);
     if (stage_ready) cudaEventDestroy(stage_ready);
     if (cp_st) cudaStreamDestroy(cp_st);
     if (vflag_h) cudaFreeHost((void*)vflag_h);
@@ -554,9 +610,9 @@ int isvd_engine_create(isvd_engine** out, int batch, int m, int n, int k, double
   A(dalloc(&e->inj, (size_t)batch));
   A(dalloc(&e->rho, (size_t)batch));
   A(dalloc(&e->xnorm, (size_t)batch));
-  A(dalloc(&e->ei, (size_t)batch));
-  A(dalloc(&e->ej, (size_t)batch));
-  A(dalloc(&e->ed, (size_t)batch));
+  A(dalloc(&e->ei, (size_t)2 * batch));  // two staging slots
+  A(dalloc(&e->ej, (size_t)2 * batch));
+  A(dalloc(&e->ed, (size_t)2 * batch));
   A(dalloc(&e->dflag, 4));
   A(dalloc(&e->W, (size_t)batch * e->wstride()));
   if (rc == ISVD_OK) rc = e->alloc_core_bufs();
@@ -583,6 +639,7 @@ int isvd_engine_create(isvd_engine** out, int batch, int m, int n, int k, double
 }
 
 int isvd_engine_destroy(isvd_engine* e) {
+  if (e) e->join();
   if (e) {
     if (e->st) cudaStreamSynchronize(e->st);
     delete e;
@@ -590,10 +647,15 @@ int isvd_engine_destroy(isvd_engine* e) {
   return ISVD_OK;
 }
 
-void* isvd_engine_stream(isvd_engine* e) { return e ? (void*)e->st : nullptr; }
+void* isvd_engine_stream(isvd_engine* e) {
+  if (!e) return nullptr;
+  e->join();
+  return (void*)e->st;
+}
 
 int isvd_engine_set_shard(isvd_engine* e, int rank, int world, int64_t row0, int m_global,
                           int owns_appends, isvd_allreduce_fn fn, void* ctx) {
+  if (e) e->join();
   if (!e) { set_error("null engine"); return ISVD_EINVAL; }
   if (e->initialized) { set_error("set_shard must precede init"); return ISVD_ESTATE; }
   if (e->B != 1) { set_error("row sharding needs a single stream (B = 1)"); return ISVD_EINVAL; }
@@ -627,6 +689,7 @@ int isvd_engine_shard_info(const isvd_engine* e, int64_t* row0, int* m_local, in
 }
 
 int isvd_engine_init(isvd_engine* e, const double* a0, int on_device) {
+  if (e) e->join();
   if (!e || !a0) { set_error("null argument"); return ISVD_EINVAL; }
   const size_t cnt = (size_t)e->B * e->m * e->n;
   if (!on_device) {
@@ -868,6 +931,7 @@ static int run_groups(isvd_engine* e, F&& issue) {
   G = std::min(G, e->B / isvd_engine::kGroupMin);
   if (G < 1) G = 1;
   e->ngroups_active = G;
+  if (G == 1 || (e->pend && e->pend_G != G)) e->join();
   if (G == 1) return issue(Slice{0, e->B, e->st});
   ISVD_TRY(e->ensure_groups(G));
   ISVD_CUDA(cudaEventRecord(e->fork_ev, e->st));
@@ -876,7 +940,11 @@ static int run_groups(isvd_engine* e, F&& issue) {
     ISVD_CUDA(cudaStreamWaitEvent(e->gst[g], e->fork_ev, 0));
     ISVD_TRY(issue(Slice{b0, b1 - b0, e->gst[g]}));
     ISVD_CUDA(cudaEventRecord(e->join_ev[g], e->gst[g]));
-    ISVD_CUDA(cudaStreamWaitEvent(e->st, e->join_ev[g], 0));
+    if (!e->async_groups) ISVD_CUDA(cudaStreamWaitEvent(e->st, e->join_ev[g], 0));
+  }
+  if (e->async_groups) {
+    e->pend = true;
+    e->pend_G = G;
   }
   return ISVD_OK;
 }
@@ -928,7 +996,7 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
     slot = e->stage_slot;
     e->stage_slot ^= 1;
     staged = e->ev + (int64_t)slot * e->B * e->zlen();
-    ISVD_CUDA(cudaStreamWaitEvent(e->cp_st, e->stage_free[slot], 0));
+    ISVD_TRY(e->ticket_wait(e->cp_st, e->stage_tk[slot]));
     ISVD_CUDA(cudaMemcpyAsync(staged, x, sizeof(double) * e->B * len, cudaMemcpyHostToDevice,
                               e->cp_st));
     if (device_check) {
@@ -953,7 +1021,8 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
     return issue_append(e, sl, xd, len, is_row, keep, lazy_state, vp);
   }));
   if (vp) e->vpend = false;
-  if (!on_device) ISVD_CUDA(cudaEventRecord(e->stage_free[slot], e->st));
+  // the staging slot is free again once every group has run this tick
+  if (!on_device) ISVD_TRY(e->ticket_record(e->stage_tk[slot]));
   if (lazy_state == 1) {
     e->lazy_active = true;
     e->m_base = e->m;
@@ -969,7 +1038,7 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
     e->n += 1;
   }
   e->r = keep;
-  if (e->lazy_active && e->lazy_b >= e->lazy_rows) ISVD_TRY(e->flush_u());
+  if (e->lazy_active && e->lazy_b >= e->lazy_rows) ISVD_TRY(e->flush_u(true));
   ISVD_TRY(e->guard_step());
   if (e->ngroups_active == 1) e->mark();
   if (e->timing) { e->timed_ticks += 1; e->tick_kind.push_back(0); }
@@ -992,7 +1061,9 @@ int isvd_engine_rank_one(isvd_engine* e, const int64_t* i, const int64_t* j, con
   if (!e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
   const int64_t *di = i, *dj = j;
   const double* dd = delta;
+  int rslot = 0;
   if (e->sharded) {
+    e->join();
     // the owner of row i is decided on the host
     if (on_device) {
       ISVD_CUDA(cudaMemcpyAsync(&e->sh_i, i, sizeof(int64_t), cudaMemcpyDeviceToHost, e->st));
@@ -1015,10 +1086,20 @@ int isvd_engine_rank_one(isvd_engine* e, const int64_t* i, const int64_t* j, con
       }
       if (!std::isfinite(delta[b])) { set_error("delta must be finite"); return ISVD_EINVAL; }
     }
-    ISVD_CUDA(cudaMemcpyAsync(e->ei, i, sizeof(int64_t) * e->B, cudaMemcpyHostToDevice, e->st));
-    ISVD_CUDA(cudaMemcpyAsync(e->ej, j, sizeof(int64_t) * e->B, cudaMemcpyHostToDevice, e->st));
-    ISVD_CUDA(cudaMemcpyAsync(e->ed, delta, sizeof(double) * e->B, cudaMemcpyHostToDevice, e->st));
-    di = e->ei; dj = e->ej; dd = e->ed;
+    // double-buffered staging on the copy stream, as for appended rows
+    ISVD_TRY(e->ensure_copy_stream());
+    rslot = e->stage_slot;
+    e->stage_slot ^= 1;
+    int64_t* si = e->ei + (int64_t)rslot * e->B;
+    int64_t* sj = e->ej + (int64_t)rslot * e->B;
+    double* sd = e->ed + (int64_t)rslot * e->B;
+    ISVD_TRY(e->ticket_wait(e->cp_st, e->stage_tk[rslot]));
+    ISVD_CUDA(cudaMemcpyAsync(si, i, sizeof(int64_t) * e->B, cudaMemcpyHostToDevice, e->cp_st));
+    ISVD_CUDA(cudaMemcpyAsync(sj, j, sizeof(int64_t) * e->B, cudaMemcpyHostToDevice, e->cp_st));
+    ISVD_CUDA(cudaMemcpyAsync(sd, delta, sizeof(double) * e->B, cudaMemcpyHostToDevice, e->cp_st));
+    ISVD_CUDA(cudaEventRecord(e->stage_ready, e->cp_st));
+    ISVD_CUDA(cudaStreamWaitEvent(e->st, e->stage_ready, 0));
+    di = si; dj = sj; dd = sd;
   }
   const int lazy_state = !e->lazy_mode ? 0 : (e->lazy_active ? 2 : 1);
   e->r_base_next = lazy_state == 1 ? e->r : e->r_base;
@@ -1030,6 +1111,7 @@ int isvd_engine_rank_one(isvd_engine* e, const int64_t* i, const int64_t* j, con
     return issue_rank_one(e, sl, di, dj, dd, lazy_state, defer, vp);
   }));
   if (defer) e->vpend = true;
+  if (!on_device) ISVD_TRY(e->ticket_record(e->stage_tk[rslot]));
   if (lazy_state == 1) {
     e->lazy_active = true;
     e->m_base = e->m;
@@ -1060,6 +1142,7 @@ static int copy_reference(isvd_engine* e) {
 }
 
 int isvd_engine_refresh(isvd_engine* e, int store_reference) {
+  if (e) e->join();
   if (!e || !e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
   ISVD_TRY(e->grow_rank(e->k));
   ISVD_TRY(e->factor_tracked());
@@ -1071,12 +1154,14 @@ int isvd_engine_refresh(isvd_engine* e, int store_reference) {
 }
 
 int isvd_engine_set_reference(isvd_engine* e) {
+  if (e) e->join();
   if (!e || !e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
   ISVD_TRY(copy_reference(e));
   return ISVD_OK;
 }
 
 int isvd_engine_set_rank(isvd_engine* e, int k_new) {
+  if (e) e->join();
   if (!e) { set_error("null engine"); return ISVD_EINVAL; }
   if (k_new < 1) { set_error("work rank must be >= 1, got " + std::to_string(k_new)); return ISVD_EINVAL; }
   ISVD_TRY(e->flush());
@@ -1107,6 +1192,7 @@ int isvd_engine_has_reference(const isvd_engine* e, int* has_ref, int* ref_m, in
 }
 
 int isvd_engine_get_factors(isvd_engine* e, int b, double* u, double* sv, double* v) {
+  if (e) e->join();
   if (!e || b < 0 || b >= e->B) { set_error("bad stream index"); return ISVD_EINVAL; }
   ISVD_TRY(e->canonicalize());
   const int r = e->r;
@@ -1126,6 +1212,7 @@ int isvd_engine_get_factors(isvd_engine* e, int b, double* u, double* sv, double
 }
 
 int isvd_engine_get_tracked(isvd_engine* e, int b, double* a) {
+  if (e) e->join();
   if (!e || b < 0 || b >= e->B || !a) { set_error("bad argument"); return ISVD_EINVAL; }
   ISVD_CUDA(cudaMemcpy2DAsync(a, sizeof(double) * e->n, e->A + b * e->astride(),
                               sizeof(double) * e->n_cap, sizeof(double) * e->n, e->m,
@@ -1135,6 +1222,7 @@ int isvd_engine_get_tracked(isvd_engine* e, int b, double* a) {
 }
 
 int isvd_engine_get_reference(isvd_engine* e, int b, double* out) {
+  if (e) e->join();
   if (!e || b < 0 || b >= e->B || !out) { set_error("bad argument"); return ISVD_EINVAL; }
   if (!e->has_ref) { set_error("no reference stored"); return ISVD_ESTATE; }
   ISVD_CUDA(cudaMemcpy2DAsync(out, sizeof(double) * e->ref_r, e->ref + (int64_t)b * e->ref_cap * e->ld,
@@ -1146,6 +1234,7 @@ int isvd_engine_get_reference(isvd_engine* e, int b, double* out) {
 
 int isvd_engine_get_scalars(isvd_engine* e, double* sq_norm, double* last_residual,
                             double* last_input_norm) {
+  if (e) e->join();
   if (!e) { set_error("null engine"); return ISVD_EINVAL; }
   if (sq_norm) ISVD_CUDA(cudaMemcpyAsync(sq_norm, e->N, sizeof(double) * e->B, cudaMemcpyDeviceToHost, e->st));
   if (last_residual) ISVD_CUDA(cudaMemcpyAsync(last_residual, e->rho, sizeof(double) * e->B, cudaMemcpyDeviceToHost, e->st));
@@ -1156,23 +1245,27 @@ int isvd_engine_get_scalars(isvd_engine* e, double* sq_norm, double* last_residu
 
 int isvd_engine_scalars_async(isvd_engine* e, double* host, int slot) {
   if (!e || !host || slot < 0 || slot >= 8) { set_error("bad argument"); return ISVD_EINVAL; }
-  if (!e->sc_ev[slot]) ISVD_CUDA(cudaEventCreateWithFlags(&e->sc_ev[slot], cudaEventDisableTiming));
-  ISVD_CUDA(cudaMemcpyAsync(host, e->N, sizeof(double) * e->B, cudaMemcpyDeviceToHost, e->st));
-  ISVD_CUDA(cudaMemcpyAsync(host + e->B, e->rho, sizeof(double) * e->B, cudaMemcpyDeviceToHost, e->st));
-  ISVD_CUDA(cudaMemcpyAsync(host + 2 * e->B, e->xnorm, sizeof(double) * e->B, cudaMemcpyDeviceToHost,
-                            e->st));
-  ISVD_CUDA(cudaEventRecord(e->sc_ev[slot], e->st));
-  return ISVD_OK;
+  // per group on the group streams while they run ahead (no join), else on st
+  const int G = e->pend ? e->pend_G : 1;
+  for (int g = 0; g < G; ++g) {
+    const int b0 = (int)((int64_t)e->B * g / G), b1 = (int)((int64_t)e->B * (g + 1) / G);
+    cudaStream_t s2 = e->pend ? e->gst[g] : e->st;
+    const size_t nb = sizeof(double) * (b1 - b0);
+    ISVD_CUDA(cudaMemcpyAsync(host + b0, e->N + b0, nb, cudaMemcpyDeviceToHost, s2));
+    ISVD_CUDA(cudaMemcpyAsync(host + e->B + b0, e->rho + b0, nb, cudaMemcpyDeviceToHost, s2));
+    ISVD_CUDA(cudaMemcpyAsync(host + 2 * e->B + b0, e->xnorm + b0, nb, cudaMemcpyDeviceToHost, s2));
+  }
+  return e->ticket_record(e->sc_tk[slot]);
 }
 
 int isvd_engine_scalars_wait(isvd_engine* e, int slot) {
-  if (!e || slot < 0 || slot >= 8 || !e->sc_ev[slot]) { set_error("bad ticket"); return ISVD_EINVAL; }
-  ISVD_CUDA(cudaEventSynchronize(e->sc_ev[slot]));
-  return ISVD_OK;
+  if (!e || slot < 0 || slot >= 8 || e->sc_tk[slot].n == 0) { set_error("bad ticket"); return ISVD_EINVAL; }
+  return e->ticket_sync(e->sc_tk[slot]);
 }
 
 int isvd_engine_set_factors(isvd_engine* e, int b, int r, const double* u, const double* sv,
                             const double* v) {
+  if (e) e->join();
   if (!e || b < 0 || b >= e->B) { set_error("bad stream index"); return ISVD_EINVAL; }
   if (r != e->r) { set_error("set_factors: rank must match the current factor width"); return ISVD_EINVAL; }
   ISVD_TRY(e->canonicalize());
@@ -1187,6 +1280,7 @@ int isvd_engine_set_factors(isvd_engine* e, int b, int r, const double* u, const
 }
 
 int isvd_engine_put_reference(isvd_engine* e, int b, int ref_m, int ref_r, const double* refh) {
+  if (e) e->join();
   if (!e || b < 0 || b >= e->B || ref_r < 0 || ref_m < 0) { set_error("bad argument"); return ISVD_EINVAL; }
   if (!refh) { e->has_ref = false; return ISVD_OK; }
   if (ref_r > e->ld) { set_error("reference wider than the rank capacity"); return ISVD_EINVAL; }
@@ -1208,6 +1302,7 @@ int isvd_engine_put_reference(isvd_engine* e, int b, int ref_m, int ref_r, const
 int isvd_engine_device_views(isvd_engine* e, double** u, int64_t* u_stride, int* ldu, double** v,
                              int64_t* v_stride, int* ldv, double** s, int* lds, double** a,
                              int64_t* a_stride, int* lda) {
+  if (e) e->join();
   if (!e) { set_error("null engine"); return ISVD_EINVAL; }
   ISVD_TRY(e->flush());
   if (u) *u = e->U;
@@ -1225,12 +1320,14 @@ int isvd_engine_device_views(isvd_engine* e, double** u, int64_t* u_stride, int*
 }
 
 int isvd_engine_flush(isvd_engine* e) {
+  if (e) e->join();
   if (!e) { set_error("null engine"); return ISVD_EINVAL; }
   return e->flush();
 }
 
 // ---- snapshot / restore (device-side checkpoint of the whole engine state)
 int isvd_engine_snapshot(isvd_engine* e) {
+  if (e) e->join();
   if (!e || !e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
   ISVD_TRY(e->flush());
   auto& S = e->snap;
@@ -1256,6 +1353,7 @@ int isvd_engine_snapshot(isvd_engine* e) {
 }
 
 int isvd_engine_restore(isvd_engine* e) {
+  if (e) e->join();
   if (!e || !e->snap.valid) { set_error("no snapshot to restore"); return ISVD_ESTATE; }
   auto& S = e->snap;
   if (S.m_cap != e->m_cap || S.n_cap != e->n_cap || S.ld != e->ld) {
@@ -1279,12 +1377,14 @@ int isvd_engine_restore(isvd_engine* e) {
 }
 
 int isvd_engine_set_reortho_threshold(isvd_engine* e, double threshold) {
+  if (e) e->join();
   if (!e) { set_error("null engine"); return ISVD_EINVAL; }
   e->reortho_threshold = threshold;
   return ISVD_OK;
 }
 
 int isvd_engine_set_lazy(isvd_engine* e, int on) {
+  if (e) e->join();
   if (!e) { set_error("null engine"); return ISVD_EINVAL; }
   if (e->sharded && !on) { set_error("eager U rotation is not available in shard mode"); return ISVD_EINVAL; }
   ISVD_TRY(e->flush());
@@ -1293,6 +1393,7 @@ int isvd_engine_set_lazy(isvd_engine* e, int on) {
 }
 
 int isvd_engine_set_lazy_window(isvd_engine* e, int rows) {
+  if (e) e->join();
   if (!e) { set_error("null engine"); return ISVD_EINVAL; }
   if (rows < 1 || rows > 1 << 16) { set_error("lazy window out of range"); return ISVD_EINVAL; }
   ISVD_TRY(e->flush());
@@ -1307,6 +1408,7 @@ int isvd_engine_set_lazy_window(isvd_engine* e, int rows) {
 int isvd_engine_lazy_window(isvd_engine* e) { return e ? e->lazy_rows : -1; }
 
 int isvd_engine_set_vdefer(isvd_engine* e, int mode) {
+  if (e) e->join();
   if (!e) { set_error("null engine"); return ISVD_EINVAL; }
   if (mode < 0 || mode > 2) { set_error("vdefer mode must be 0, 1 or 2"); return ISVD_EINVAL; }
   ISVD_TRY(e->flush_v());
@@ -1314,19 +1416,29 @@ int isvd_engine_set_vdefer(isvd_engine* e, int mode) {
   return ISVD_OK;
 }
 
+int isvd_engine_set_groups(isvd_engine* e, int groups) {
+  if (!e) { set_error("null engine"); return ISVD_EINVAL; }
+  if (groups < 1 || groups > 64) { set_error("groups must be in 1..64"); return ISVD_EINVAL; }
+  e->ngroups = groups;
+  return ISVD_OK;
+}
+
 int isvd_engine_set_append_solver(isvd_engine* e, int jacobi) {
+  if (e) e->join();
   if (!e) { set_error("null engine"); return ISVD_EINVAL; }
   e->append_jacobi = jacobi != 0;
   return ISVD_OK;
 }
 
 int isvd_engine_set_timing(isvd_engine* e, int on) {
+  if (e) e->join();
   if (!e) { set_error("null engine"); return ISVD_EINVAL; }
   e->timing = on != 0;
   return ISVD_OK;
 }
 
 int isvd_engine_phase_times(isvd_engine* e, double* ms, int64_t* ticks) {
+  if (e) e->join();
   if (!e || !ms) { set_error("bad argument"); return ISVD_EINVAL; }
   ISVD_CUDA(cudaStreamSynchronize(e->st));
   for (int p = 0; p < 10; ++p) ms[p] = 0.0;
@@ -1362,11 +1474,13 @@ int isvd_engine_phase_times(isvd_engine* e, double* ms, int64_t* ticks) {
 }
 
 int isvd_engine_canonicalize(isvd_engine* e) {
+  if (e) e->join();
   if (!e) { set_error("null engine"); return ISVD_EINVAL; }
   return e->canonicalize();
 }
 
 int isvd_engine_synchronize(isvd_engine* e) {
+  if (e) e->join();
   if (!e) { set_error("null engine"); return ISVD_EINVAL; }
   ISVD_CUDA(cudaStreamSynchronize(e->st));
   return ISVD_OK;
@@ -1375,6 +1489,7 @@ int isvd_engine_synchronize(isvd_engine* e) {
 // ------------------------------------------------------------------ metrics
 
 int isvd_engine_frob_error(isvd_engine* e, double* out) {
+  if (e) e->join();
   if (!e || !e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
   ISVD_TRY(e->flush());
   ISVD_TRY(e->ensure_work(0, 0, (int64_t)e->B * frob_nblk(e->m), e->B));
@@ -1389,6 +1504,7 @@ int isvd_engine_frob_error(isvd_engine* e, double* out) {
 
 int isvd_engine_risk(isvd_engine* e, int t, const double* w, int P, double* cov_out,
                      double* diag_out, double* out) {
+  if (e) e->join();
   if (!e || !e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
   if (!w || !out || P < 1) { set_error("risk: bad argument"); return ISVD_EINVAL; }
   if (t < 2) { set_error("need at least 2 rows for a covariance, got t=" + std::to_string(t)); return ISVD_EINVAL; }
@@ -1464,6 +1580,7 @@ static int gram_defect(isvd_engine* e, Mat X, int rows, int w, double* host_out,
 }
 
 int isvd_engine_ortho_defect(isvd_engine* e, double* du, double* dv) {
+  if (e) e->join();
   if (!e || !e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
   ISVD_TRY(e->flush());
   if (du) ISVD_TRY(gram_defect(e, e->Um(), e->m, e->r, du, e->sharded));
@@ -1473,6 +1590,7 @@ int isvd_engine_ortho_defect(isvd_engine* e, double* du, double* dv) {
 
 int isvd_engine_angle(isvd_engine* e, int which, const double* q, int q_cols, int on_device,
                       double* out) {
+  if (e) e->join();
   if (!e || !e->initialized || !out) { set_error("engine not initialised"); return ISVD_ESTATE; }
   ISVD_TRY(e->flush());
   const int B = e->B, m = e->m, r = e->r;
@@ -1614,6 +1732,7 @@ int isvd_dense_svd(int batch, int m, int n, const double* a, int w_keep, double*
 }
 
 int isvd_engine_oracle(isvd_engine* e, int w_keep, double* s, double* u) {
+  if (e) e->join();
   if (!e || !e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
   if (e->sharded) { set_error("the device oracle needs the whole tracked matrix (not in shard mode)"); return ISVD_EINVAL; }
   return oracle_common(e->B, e->m, e->n, e->A, e->astride(), e->n_cap, w_keep, s, u, nullptr, e->st);

@@ -9,6 +9,10 @@ dev = torch.device("cuda", 0)
 T = 64
 a0, rows, ii, jj, dd = bench.make_inputs(torch, dev, list(range(4096)), n_events=T)
 eng = BatchedSvdEngine(a0, 32, m_cap=1024 + 4 * T, k_cap=32)
+import os
+from paper_2605_24514_b200 import _lib
+if os.environ.get("G"):
+    _lib.check(_lib.load().isvd_engine_set_groups(eng._h.h, int(os.environ["G"])))
 hr = torch.empty(rows.shape, dtype=torch.float64, pin_memory=True); hr.copy_(rows); hr = hr.numpy()
 hi = torch.empty(ii.shape, dtype=torch.int64, pin_memory=True); hi.copy_(ii); hi = hi.numpy()
 hj = torch.empty(jj.shape, dtype=torch.int64, pin_memory=True); hj.copy_(jj); hj = hj.numpy()
