@@ -103,9 +103,11 @@ __global__ void __launch_bounds__(WIDE ? 512 : 32) arrow_svd_kernel(int n, const
                                                        double* __restrict__ vk, int64_t out_stride,
                                                        int ldo, double* __restrict__ sv,
                                                        int64_t sv_stride, double* __restrict__ s_out,
-                                                       int64_t s_out_stride, int nkeep) {
+                                                       int64_t s_out_stride, int nkeep,
+                                                       const int* __restrict__ gate) {
   griddep_launch_dependents();
   griddep_wait();
+  if (gate && *gate) return;
   __shared__ ArrowSmem<kN> S;
   namespace cg = cooperative_groups;
   const int crank = CL > 1 ? (int)cg::this_cluster().block_rank() : 0;
@@ -698,7 +700,7 @@ int launch_arrow_svd(int batch, int s, const double* core, int64_t core_stride, 
     // one warp per core: roots 32..39 (s = 33 is the k = 32 append core) are
     // solved warp-cooperatively after the one-root-per-lane pass
     arrow_svd_kernel<40, false, 1><<<batch, 32, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
-                                                         out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep);
+                                                         out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate);
   } else if (batch <= kClusterMaxBatch) {
     // few wide cores (config 5b: one 129 core per tick): a cluster per core
     cudaLaunchConfig_t cfg = {};
@@ -718,23 +720,23 @@ int launch_arrow_svd(int batch, int s, const double* core, int64_t core_stride, 
     cudaError_t e;
     if (s <= 72)
       e = cudaLaunchKernelEx(&cfg, arrow_svd_kernel<72, true, kArrowCluster>, s, core, core_stride,
-                             ldcore, uk, vk, out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep);
+                             ldcore, uk, vk, out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate);
     else if (s <= 136)
       e = cudaLaunchKernelEx(&cfg, arrow_svd_kernel<136, true, kArrowCluster>, s, core,
-                             core_stride, ldcore, uk, vk, out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep);
+                             core_stride, ldcore, uk, vk, out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate);
     else
       e = cudaLaunchKernelEx(&cfg, arrow_svd_kernel<kN, true, kArrowCluster>, s, core, core_stride,
-                             ldcore, uk, vk, out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep);
+                             ldcore, uk, vk, out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate);
     ISVD_CUDA(e);
   } else if (s <= 72) {
     arrow_svd_kernel<72, true, 1><<<batch, 512, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
-                                                         out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep);
+                                                         out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate);
   } else if (s <= 136) {
     arrow_svd_kernel<136, true, 1><<<batch, 512, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
-                                                          out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep);
+                                                          out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate);
   } else {
     arrow_svd_kernel<kN, true, 1><<<batch, 512, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
-                                                         out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep);
+                                                         out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate);
   }
   ISVD_LAUNCHED();
   return ISVD_OK;

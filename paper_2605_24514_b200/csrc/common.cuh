@@ -14,6 +14,10 @@ constexpr double kOrthoEps = 1e-14;
 constexpr int kMaxSweeps = 64;
 
 void set_error(const std::string& msg);
+// Tick gate (engine.cu): while set, the launchers of the append path pass it
+// to their kernels, which exit at once when *gate != 0 (a rejected payload
+// leaves the engine state untouched though its kernels were already queued).
+extern thread_local const int* g_gate;
 void count_launch(int n = 1);
 
 #define ISVD_CUDA(call)                                                        \

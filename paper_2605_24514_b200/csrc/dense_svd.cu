@@ -191,7 +191,12 @@ __global__ void __launch_bounds__(kThreads) dsvd_round_kernel(int ldx, int ncp, 
       }
       __syncthreads();
     }
-    if (!rot) break;
+    // every thread reads the flag before thread 0 clears it for the next
+    // sweep (without this barrier a late warp could see the cleared flag,
+    // leave the loop alone and desynchronise the CTA)
+    const int more = rot;
+    __syncthreads();
+    if (!more) break;
   }
 
   // ---- apply X[:, cols] <- X[:, cols] Q and J[:, cols] <- J[:, cols] Q (DMMA)

@@ -38,6 +38,7 @@
 namespace isvd {
 
 static thread_local std::string g_err;
+thread_local const int* g_gate = nullptr;
 static int64_t g_launches = 0;
 void set_error(const std::string& msg) { g_err = msg; }
 void count_launch(int n) { __atomic_add_fetch(&g_launches, n, __ATOMIC_RELAXED); }
@@ -141,11 +142,11 @@ struct isvd_engine {
   Ticket stage_tk[2];  // the ticks that last read each staging slot
   cudaEvent_t stage_ready = nullptr;
   int stage_slot = 0;
-  volatile int* vflag_h = nullptr;  // pinned: the device finiteness verdict
+  volatile int* vflag_h = nullptr;  // pinned: the device finiteness verdict per slot
   int ensure_copy_stream() {
     if (cp_st) return ISVD_OK;
-    ISVD_CUDA(cudaHostAlloc((void**)&vflag_h, sizeof(int), cudaHostAllocDefault));
-    *vflag_h = 0;
+    ISVD_CUDA(cudaHostAlloc((void**)&vflag_h, 2 * sizeof(int), cudaHostAllocDefault));
+    vflag_h[0] = vflag_h[1] = 0;
     ISVD_CUDA(cudaStreamCreateWithFlags(&cp_st, cudaStreamNonBlocking));
     ISVD_CUDA(cudaEventCreateWithFlags(&stage_ready, cudaEventDisableTiming));
     return ISVD_OK;
@@ -961,6 +962,9 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
   // transfer instead of scanning 8 MB itself.
   const size_t nelem = (size_t)e->B * len;
   const bool device_check = !on_device && nelem >= (size_t(1) << 16);
+  // every kernel this tick can launch honours the gate (g_gate) on these paths
+  const bool gated = device_check && !e->append_jacobi && !e->sharded && !e->timing && !e->guard &&
+                     project_append_gateable(e->B, len, e->r);
   const std::string bad_msg =
       std::string(is_row ? "appended row" : "appended column") + " contains non-finite entries";
   if (!on_device && !device_check && !all_finite(x, nelem)) {
@@ -1000,29 +1004,42 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
     ISVD_CUDA(cudaMemcpyAsync(staged, x, sizeof(double) * e->B * len, cudaMemcpyHostToDevice,
                               e->cp_st));
     if (device_check) {
-      ISVD_CUDA(cudaMemsetAsync(e->dflag + 1, 0, sizeof(int), e->cp_st));
-      ISVD_TRY(launch_check_finite(nelem, staged, e->dflag + 1, e->cp_st));
-      ISVD_CUDA(cudaMemcpyAsync((void*)e->vflag_h, e->dflag + 1, sizeof(int), cudaMemcpyDeviceToHost,
-                                e->cp_st));
+      ISVD_CUDA(cudaMemsetAsync(e->dflag + 1 + slot, 0, sizeof(int), e->cp_st));
+      ISVD_TRY(launch_check_finite(nelem, staged, e->dflag + 1 + slot, e->cp_st));
+      ISVD_CUDA(cudaMemcpyAsync((void*)(e->vflag_h + slot), e->dflag + 1 + slot, sizeof(int),
+                                cudaMemcpyDeviceToHost, e->cp_st));
     }
     ISVD_CUDA(cudaEventRecord(e->stage_ready, e->cp_st));
-    if (device_check) {
+    if (device_check && !gated) {
       ISVD_CUDA(cudaEventSynchronize(e->stage_ready));
-      if (*e->vflag_h) {
+      if (e->vflag_h[slot]) {
         set_error(bad_msg);
         return ISVD_EINVAL;  // nothing consumed the staging slot; state unchanged
       }
     }
     ISVD_CUDA(cudaStreamWaitEvent(e->st, e->stage_ready, 0));
   }
-  ISVD_TRY(run_groups(e, [&](const Slice& sl) {
+  // Gated tick: the kernels are queued before the verdict is known and skip
+  // themselves on the device if the payload was rejected, so the host's wait
+  // for the upload overlaps their launch instead of preceding it.
+  g_gate = gated ? e->dflag + 1 + slot : nullptr;
+  const int rc_issue = run_groups(e, [&](const Slice& sl) {
     const double* xd = x;
     if (!on_device) xd = staged;
     return issue_append(e, sl, xd, len, is_row, keep, lazy_state, vp);
-  }));
-  if (vp) e->vpend = false;
+  });
+  g_gate = nullptr;
+  ISVD_TRY(rc_issue);
   // the staging slot is free again once every group has run this tick
   if (!on_device) ISVD_TRY(e->ticket_record(e->stage_tk[slot]));
+  if (gated) {
+    ISVD_CUDA(cudaEventSynchronize(e->stage_ready));
+    if (e->vflag_h[slot]) {
+      set_error(bad_msg);
+      return ISVD_EINVAL;  // every queued kernel of this tick exits at once; state unchanged
+    }
+  }
+  if (vp) e->vpend = false;
   if (lazy_state == 1) {
     e->lazy_active = true;
     e->m_base = e->m;

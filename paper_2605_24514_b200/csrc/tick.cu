@@ -32,7 +32,8 @@ __global__ void __launch_bounds__(256) project_append_kernel(
     double* __restrict__ inj_scale, double* __restrict__ rho_out, double* __restrict__ xnorm_out,
     double* __restrict__ A, int64_t a_stride, int64_t a_off, int64_t a_step,
     double* __restrict__ N, int arrow_only, const double* __restrict__ G, int64_t g_stride,
-    int ldg) {
+    int ldg, const int* __restrict__ gate) {
+  if (gate && *gate) return;
   // sized by RT, not kRMax: with a 64 KB staged F the static arrays decide
   // whether 2 or 3 CTAs fit per SM
   __shared__ double part[8][RT * 32];
@@ -686,9 +687,11 @@ constexpr int kRotNB = 8;              // output n-tiles per pass (independent D
 
 template <int KP>
 __global__ void __launch_bounds__(kRotWarps * 32, 1)
-    rotate_kernel(int r, int keep, int NP, RotJob j0, RotJob j1, int nblk0, int rpb) {
+    rotate_kernel(int r, int keep, int NP, RotJob j0, RotJob j1, int nblk0, int rpb,
+                  const int* __restrict__ gate) {
   griddep_launch_dependents();
   griddep_wait();
+  if (gate && *gate) return;
   extern __shared__ double smem[];
   constexpr int KQ = KP / 4;
   const int NT = NP / 8;
@@ -806,7 +809,8 @@ constexpr int kRegRowsPerBlock = 256;
 
 template <int KP>
 __global__ void __launch_bounds__(kRegWarps * 32, 8)
-    rotate_reg_kernel(int r, int keep, RotJob j0, RotJob j1, int nblk0) {
+    rotate_reg_kernel(int r, int keep, RotJob j0, RotJob j1, int nblk0, const int* __restrict__ gate) {
+  if (gate && *gate) return;
   constexpr int KQ = KP / 4;
   // B fragments of the core rotation in lane order (one conflict-free LDS.64
   // per DMMA); keeping them out of registers (64 regs at KP = 32) lets 8
@@ -981,9 +985,10 @@ __device__ void complete_column(double* X, int64_t ld, int rows, int w, int t, d
 }
 
 __global__ void complete_zero_kernel(int w, const double* __restrict__ s, int lds, Mat U, int m,
-                                     Mat V, int n) {
+                                     Mat V, int n, const int* __restrict__ gate) {
   griddep_launch_dependents();
   griddep_wait();
+  if (gate && *gate) return;
   extern __shared__ double coef[];  // [w]
   __shared__ double red[32];
   const int b = blockIdx.x;
@@ -1078,7 +1083,8 @@ __global__ void canonicalize_kernel(int w, Mat U, int m, Mat V, int n) {
 // ---------------------------------------------------------------- helpers
 __global__ void copy_rows_kernel(int rows, int cols, const double* __restrict__ src,
                                  int64_t src_stride, int ld_src, double* __restrict__ dst,
-                                 int64_t dst_stride, int ld_dst) {
+                                 int64_t dst_stride, int ld_dst, const int* __restrict__ gate) {
+  if (gate && *gate) return;
   const int b = blockIdx.y;
   const double* sb = src + b * src_stride;
   double* db = dst + b * dst_stride;
@@ -1143,6 +1149,11 @@ __global__ void check_finite_kernel(size_t n, const double* __restrict__ p, int*
 }
 
 }  // namespace
+
+// the launch goes to project_append_kernel (which honours g_gate)
+bool project_append_gateable(int batch, int rows, int r) {
+  return !(batch <= 32 && (int64_t)rows * r >= 16384);
+}
 
 bool project_append_takes_g(int batch, int rows, int r) {
   return r <= 32 && !(batch <= 32 && (int64_t)rows * r >= 16384);
@@ -1280,7 +1291,7 @@ int launch_project_append(int batch, int rows, int r, Mat F, const double* x, in
     }
     project_append_kernel<SG, RT><<<batch, 256, SG ? stage : 0, st>>>(
         rows, r, F, x, x_stride, s, lds, tol, core, core_stride, ldcore, z, z_stride, inj_scale,
-        rho_out, xnorm_out, A, a_stride, a_off, a_step, N, arrow_only, G, g_stride, ldg);
+        rho_out, xnorm_out, A, a_stride, a_off, a_step, N, arrow_only, G, g_stride, ldg, g_gate);
     return ISVD_OK;
   };
   using T1 = std::integral_constant<bool, true>;
@@ -1363,14 +1374,14 @@ static int rotate_dispatch(int batch, int r, int keep, const RotJob& j0, const R
         if (j1->new_row && rb1 == 0) rb1 = 1;
       }
       rotate_reg_kernel<KP><<<dim3(rb0 + rb1, batch), kRegWarps * 32, 0, st>>>(
-          r, keep, j0, j1 ? *j1 : j0, rb0);
+          r, keep, j0, j1 ? *j1 : j0, rb0, g_gate);
       ISVD_LAUNCHED();
       return ISVD_OK;
     }
   }
   dim3 grid(nb0 + nb1, batch);
   ISVD_CUDA(launch_ex(batch <= 32, 1, rotate_kernel<KP>, grid, dim3(kRotWarps * 32), smem, st, r,
-                      keep, NP, j0, j1 ? *j1 : j0, nb0, rpb));
+                      keep, NP, j0, j1 ? *j1 : j0, nb0, rpb, g_gate));
   ISVD_LAUNCHED();
   return ISVD_OK;
 }
@@ -1426,7 +1437,7 @@ int launch_complete_zero(int batch, int w, const double* s, int lds, Mat U, int 
     return ISVD_EINVAL;
   }
   ISVD_CUDA(launch_ex(batch <= 32, 1, complete_zero_kernel, dim3(batch), dim3(256), smem, st, w, s,
-                      lds, U, m, V, n));
+                      lds, U, m, V, n, g_gate));
   ISVD_LAUNCHED();
   return ISVD_OK;
 }
@@ -1498,7 +1509,7 @@ int launch_copy_rows(int batch, int rows, int cols, const double* src, int64_t s
   int64_t total = (int64_t)rows * cols;
   int gx = (int)std::min<int64_t>((total + 255) / 256, 4096);
   copy_rows_kernel<<<dim3(gx, batch), 256, 0, st>>>(rows, cols, src, src_stride, ld_src, dst,
-                                                    dst_stride, ld_dst);
+                                                    dst_stride, ld_dst, g_gate);
   ISVD_LAUNCHED();
   return ISVD_OK;
 }

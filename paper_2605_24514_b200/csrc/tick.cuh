@@ -28,6 +28,7 @@ int launch_project_append(int batch, int rows, int r, Mat F, const double* x, in
 // F G) for this shape (the one-CTA-per-stream path does; the split and
 // cluster paths for few long streams do not).
 bool project_append_takes_g(int batch, int rows, int r);
+bool project_append_gateable(int batch, int rows, int r);
 
 // Deferred left basis: while active, the true U is
 // [Ub 0; 0 I] . W where Ub = the first m_base rows of the U buffer (width
