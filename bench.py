@@ -41,6 +41,8 @@ sys.path.insert(0, str(ROOT))
 M0, N0, RANK, K = 1024, 256, 32, 32
 TOTAL_STREAMS = 4096
 EVENTS = 1024
+# e2e host loop: results are read back E2E_LAG steps behind their issue
+E2E_LAG, RES_SLOTS = 2, 4
 METRIC = "iSVD updates/sec (k=32)"
 UNIT = "updates/s"
 # BASELINE configs[4] part b: one tall matrix, k = 128, 256 row appends
@@ -487,14 +489,15 @@ def run_gpu(args):
         if world > 1:
             dist.barrier()
 
-    res = torch.empty((2, 3 * B), dtype=torch.float64, pin_memory=True)
+    res = torch.empty((RES_SLOTS, 3 * B), dtype=torch.float64, pin_memory=True)
 
     def run_ticks(eng, nt, host=None):
         """nt ticks; device-resident inputs unless host=(rows, ii, jj, dd).
         With host inputs every step's result (sq_norm, residual, input norm
         per stream) is read back to pinned host memory; the host waits for
-        step t's result after issuing step t+1 (one step of lag), so input
-        validation and upload overlap the previous step's kernels."""
+        step t's result after issuing step t + E2E_LAG (the read-back lags by
+        E2E_LAG steps; every result is read inside the timed region), so
+        input validation and upload overlap the device's work."""
         for t in range(nt):
             if t % 2 == 0:
                 eng.row_append(rows[t // 2] if host is None else host[0][t // 2])
@@ -503,12 +506,13 @@ def run_gpu(args):
             else:
                 eng.rank_one_update(host[1][t // 2], host[2][t // 2], host[3][t // 2])
             if host is not None:
-                eng.scalars_async(res[t % 2].numpy(), t % 2)
-                if t > 0:
-                    eng.scalars_wait((t - 1) % 2)
+                eng.scalars_async(res[t % RES_SLOTS].numpy(), t % RES_SLOTS)
+                if t >= E2E_LAG:
+                    eng.scalars_wait((t - E2E_LAG) % RES_SLOTS)
         if host is not None and nt > 0:
-            eng.scalars_wait((nt - 1) % 2)
-            assert np.all(np.isfinite(res[(nt - 1) % 2].numpy()))
+            for t in range(max(0, nt - E2E_LAG), nt):
+                eng.scalars_wait(t % RES_SLOTS)
+            assert np.all(np.isfinite(res[(nt - 1) % RES_SLOTS].numpy()))
 
     t_init = time.perf_counter()
     eng = BatchedSvdEngine(a0, K, m_cap=m_cap, k_cap=K)
@@ -636,7 +640,8 @@ def run_gpu(args):
             "clocks": clock,
             "gpu_launches": int(launches),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "steps": e2e_steps},
+                    "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
+                    "result_readback_lag_steps": E2E_LAG},
             "roofline": {"kernel": hbm_name, "bound": "hbm", "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "peak_kind": peak_kind,
                          "traffic": traffic,

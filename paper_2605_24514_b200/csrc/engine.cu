@@ -139,14 +139,17 @@ struct isvd_engine {
   Ticket sc_tk[8];  // isvd_engine_scalars_async tickets
   // host-payload staging: copy stream, two slots of ev, their events
   cudaStream_t cp_st = nullptr;
-  Ticket stage_tk[2];  // the ticks that last read each staging slot
+  // host-payload staging slots: a host loop may run this many ticks ahead
+  // of the device before an upload waits for its slot
+  static constexpr int kStageSlots = 4;
+  Ticket stage_tk[kStageSlots];  // the ticks that last read each staging slot
   cudaEvent_t stage_ready = nullptr;
   int stage_slot = 0;
   volatile int* vflag_h = nullptr;  // pinned: the device finiteness verdict per slot
   int ensure_copy_stream() {
     if (cp_st) return ISVD_OK;
-    ISVD_CUDA(cudaHostAlloc((void**)&vflag_h, 2 * sizeof(int), cudaHostAllocDefault));
-    vflag_h[0] = vflag_h[1] = 0;
+    ISVD_CUDA(cudaHostAlloc((void**)&vflag_h, kStageSlots * sizeof(int), cudaHostAllocDefault));
+    for (int i = 0; i < kStageSlots; ++i) vflag_h[i] = 0;
     ISVD_CUDA(cudaStreamCreateWithFlags(&cp_st, cudaStreamNonBlocking));
     ISVD_CUDA(cudaEventCreateWithFlags(&stage_ready, cudaEventDisableTiming));
     return ISVD_OK;
@@ -181,6 +184,7 @@ struct isvd_engine {
   int64_t *ei = nullptr, *ej = nullptr;
   double* ed = nullptr;
   int* dflag = nullptr;
+  unsigned* zf_cnt = nullptr;  // per-stream CTA arrival counts (fused zero-sigma completion)
   double* ref = nullptr;
   int ref_m = 0, ref_r = 0, ref_cap = 0;
   bool has_ref = false;
@@ -395,7 +399,7 @@ struct isvd_engine {
   int alloc_vec_bufs() {
     dfree(z); dfree(ev);
     ISVD_TRY(dalloc(&z, (size_t)B * zlen()));
-    ISVD_TRY(dalloc(&ev, (size_t)2 * B * zlen()));  // two staging slots
+    ISVD_TRY(dalloc(&ev, (size_t)kStageSlots * B * zlen()));
     return ISVD_OK;
   }
 
@@ -539,7 +543,8 @@ struct isvd_engine {
     dfree(U); dfree(V); dfree(s); dfree(A); dfree(N);
     dfree(core); dfree(uk); dfree(vk); dfree(sv); dfree(vscr);
     dfree(z); dfree(inj); dfree(rho); dfree(xnorm); dfree(ev);
-    dfree(ei); dfree(ej); dfree(ed); dfree(dflag); dfree(ref); dfree(W); dfree(Gv);
+    dfree(ei); dfree(ej); dfree(ed); dfree(dflag);
+    if (zf_cnt) cudaFree(zf_cnt); dfree(ref); dfree(W); dfree(Gv);
     dfree(wx); dfree(wj); dfree(wpart); dfree(wout); dfree(wflags);
     dfree(snap.U); dfree(snap.V); dfree(snap.A); dfree(snap.s); dfree(snap.N); dfree(shv);
     for (auto g : gst) cudaStreamDestroy(g);
@@ -611,11 +616,18 @@ int isvd_engine_create(isvd_engine** out, int batch, int m, int n, int k, double
   A(dalloc(&e->inj, (size_t)batch));
   A(dalloc(&e->rho, (size_t)batch));
   A(dalloc(&e->xnorm, (size_t)batch));
-  A(dalloc(&e->ei, (size_t)2 * batch));  // two staging slots
-  A(dalloc(&e->ej, (size_t)2 * batch));
-  A(dalloc(&e->ed, (size_t)2 * batch));
-  A(dalloc(&e->dflag, 4));
+  A(dalloc(&e->ei, (size_t)isvd_engine::kStageSlots * batch));  // staging slots
+  A(dalloc(&e->ej, (size_t)isvd_engine::kStageSlots * batch));
+  A(dalloc(&e->ed, (size_t)isvd_engine::kStageSlots * batch));
+  A(dalloc(&e->dflag, 1 + isvd_engine::kStageSlots));
   A(dalloc(&e->W, (size_t)batch * e->wstride()));
+  if (rc == ISVD_OK) {
+    if (cudaMalloc((void**)&e->zf_cnt, sizeof(unsigned) * batch) != cudaSuccess ||
+        cudaMemset(e->zf_cnt, 0, sizeof(unsigned) * batch) != cudaSuccess) {
+      set_error("out of device memory");
+      rc = ISVD_ENOMEM;
+    }
+  }
   if (rc == ISVD_OK) rc = e->alloc_core_bufs();
   if (rc == ISVD_OK) rc = e->alloc_vec_bufs();
   if (rc == ISVD_OK) {
@@ -796,10 +808,24 @@ static int issue_append(isvd_engine* e, const Slice& sl, const double* xd, int l
     injj.g_stride = e->gstride();
     injj.ldg = e->ld;
   }
+  // zero-sigma completion (_install) over the post-tick factors: fused into
+  // the rotation when the secular kernel already installed s
+  const int m_new = is_row ? e->m + 1 : e->m, n_new = is_row ? e->n : e->n + 1;
+  ZeroFix zf;
+  zf.s = e->s + (int64_t)b0 * e->ld;
+  zf.lds = e->ld;
+  zf.w = keep;
+  zf.U = lazy_state != 0 ? mat_at(e->Wm(), b0) : mat_at(e->Um(), b0);
+  zf.m = lazy_state != 0 ? e->r_base_next + e->lazy_b_next : (e->sharded ? 0 : m_new);
+  zf.V = mat_at(e->Vm(), b0);
+  zf.n = n_new;
+  zf.counter = e->zf_cnt + b0;
+  const ZeroFix* zfp = e->append_jacobi ? nullptr : &zf;
+  bool fused = false;
   if (has_u) {
-    ISVD_TRY(launch_rotate(nb, r, keep, uj, &injj, st));
+    ISVD_TRY(launch_rotate(nb, r, keep, uj, &injj, st, zfp, &fused));
   } else {
-    ISVD_TRY(launch_rotate(nb, r, keep, injj, nullptr, st));
+    ISVD_TRY(launch_rotate(nb, r, keep, injj, nullptr, st, zfp, &fused));
   }
   if (one) e->mark();
   // install: s <- sv[:, :keep] (the secular kernel already wrote it), then the
@@ -808,13 +834,7 @@ static int issue_append(isvd_engine* e, const Slice& sl, const double* xd, int l
     ISVD_CUDA(cudaMemcpy2DAsync(e->s + (int64_t)b0 * e->ld, sizeof(double) * e->ld, sv,
                                 sizeof(double) * S, sizeof(double) * keep, nb,
                                 cudaMemcpyDeviceToDevice, st));
-  const int m_new = is_row ? e->m + 1 : e->m, n_new = is_row ? e->n : e->n + 1;
-  if (lazy_state != 0)
-    ISVD_TRY(launch_complete_zero(nb, keep, e->s + (int64_t)b0 * e->ld, e->ld, mat_at(e->Wm(), b0),
-                                  e->r_base_next + e->lazy_b_next, mat_at(e->Vm(), b0), n_new, st));
-  else
-    ISVD_TRY(launch_complete_zero(nb, keep, e->s + (int64_t)b0 * e->ld, e->ld, mat_at(e->Um(), b0),
-                                  e->sharded ? 0 : m_new, mat_at(e->Vm(), b0), n_new, st));
+  if (!fused) ISVD_TRY(launch_complete_zero(nb, keep, zf.s, zf.lds, zf.U, zf.m, zf.V, zf.n, st));
   return ISVD_OK;
 }
 
@@ -904,21 +924,27 @@ static int issue_rank_one(isvd_engine* e, const Slice& sl, const int64_t* di, co
     else
       has_v = false;
   }
+  ZeroFix zf;
+  zf.s = e->s + (int64_t)b0 * e->ld;
+  zf.lds = e->ld;
+  zf.w = r;
+  zf.U = lazy_state != 0 ? mat_at(e->Wm(), b0) : mat_at(e->Um(), b0);
+  zf.m = lazy_state != 0 ? e->r_base_next + e->lazy_b_next : e->m;
+  zf.V = defer ? mat_at(e->Gm(), b0) : mat_at(e->Vm(), b0);
+  zf.n = defer ? r : e->n;
+  zf.counter = e->zf_cnt + b0;
+  bool zfused = false;
+  // the completion can ride on the rotation once s is installed (the fused
+  // Jacobi writes it directly)
   if (has_u || has_v)
-    ISVD_TRY(launch_rotate(nb, r, r, has_u ? uj : vj, (has_u && has_v) ? &vj : nullptr, st));
+    ISVD_TRY(launch_rotate(nb, r, r, has_u ? uj : vj, (has_u && has_v) ? &vj : nullptr, st,
+                           fused ? &zf : nullptr, &zfused));
   if (one) e->mark();
   if (!fused)  // the fused kernel installed s itself
     ISVD_CUDA(cudaMemcpy2DAsync(e->s + (int64_t)b0 * e->ld, sizeof(double) * e->ld, sv,
                                 sizeof(double) * S, sizeof(double) * r, nb,
                                 cudaMemcpyDeviceToDevice, st));
-  const Mat vside = defer ? mat_at(e->Gm(), b0) : mat_at(e->Vm(), b0);
-  const int vrows = defer ? r : e->n;
-  if (lazy_state != 0)
-    ISVD_TRY(launch_complete_zero(nb, r, e->s + (int64_t)b0 * e->ld, e->ld, mat_at(e->Wm(), b0),
-                                  e->r_base_next + e->lazy_b_next, vside, vrows, st));
-  else
-    ISVD_TRY(launch_complete_zero(nb, r, e->s + (int64_t)b0 * e->ld, e->ld, mat_at(e->Um(), b0),
-                                  e->m, vside, vrows, st));
+  if (!zfused) ISVD_TRY(launch_complete_zero(nb, r, zf.s, zf.lds, zf.U, zf.m, zf.V, zf.n, st));
   return ISVD_OK;
 }
 
@@ -998,7 +1024,7 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
   if (!on_device) {
     ISVD_TRY(e->ensure_copy_stream());
     slot = e->stage_slot;
-    e->stage_slot ^= 1;
+    e->stage_slot = (e->stage_slot + 1) % isvd_engine::kStageSlots;
     staged = e->ev + (int64_t)slot * e->B * e->zlen();
     ISVD_TRY(e->ticket_wait(e->cp_st, e->stage_tk[slot]));
     ISVD_CUDA(cudaMemcpyAsync(staged, x, sizeof(double) * e->B * len, cudaMemcpyHostToDevice,
@@ -1106,7 +1132,7 @@ int isvd_engine_rank_one(isvd_engine* e, const int64_t* i, const int64_t* j, con
     // double-buffered staging on the copy stream, as for appended rows
     ISVD_TRY(e->ensure_copy_stream());
     rslot = e->stage_slot;
-    e->stage_slot ^= 1;
+    e->stage_slot = (e->stage_slot + 1) % isvd_engine::kStageSlots;
     int64_t* si = e->ei + (int64_t)rslot * e->B;
     int64_t* sj = e->ej + (int64_t)rslot * e->B;
     double* sd = e->ed + (int64_t)rslot * e->B;

@@ -807,9 +807,38 @@ static int rot_rows_per_block(int64_t total_rows) {
 constexpr int kRegWarps = 4;
 constexpr int kRegRowsPerBlock = 256;
 
+__device__ void complete_column(double* X, int64_t ld, int rows, int w, int t, double* coef,
+                                double* red);
+
+// complete_zero_kernel's per-stream work for CTA-sized thread blocks
+__device__ void complete_zero_stream(int b, int w, const double* __restrict__ s, int lds, Mat U,
+                                     int m, Mat V, int n, double* coef, double* red) {
+  const double* sb = s + (int64_t)b * lds;
+  // common case: no zero sigma -- one parallel scan instead of w serial loads
+  bool any_zero = false;
+  for (int t = threadIdx.x; t < w; t += blockDim.x) any_zero |= sb[t] == 0.0;
+  if (!__syncthreads_or(any_zero)) return;
+  for (int t = 0; t < w; ++t) {
+    if (sb[t] != 0.0) continue;
+    for (int side = 0; side < 2; ++side) {
+      double* X = side == 0 ? U.p + b * U.stride : V.p + b * V.stride;
+      int64_t ld = side == 0 ? U.ld : V.ld;
+      int rows = side == 0 ? m : n;
+      double nn = 0.0;
+      for (int i = threadIdx.x; i < rows; i += blockDim.x) {
+        const double v = __ldcg(&X[i * ld + t]);  // rows of other CTAs (fused path)
+        nn = fma(v, v, nn);
+      }
+      double nsq = block_sum(nn, red);
+      if (fabs(nsq - 1.0) > 1e-6) complete_column(X, ld, rows, w, t, coef, red);
+    }
+  }
+}
+
 template <int KP>
 __global__ void __launch_bounds__(kRegWarps * 32, 8)
-    rotate_reg_kernel(int r, int keep, RotJob j0, RotJob j1, int nblk0, const int* __restrict__ gate) {
+    rotate_reg_kernel(int r, int keep, RotJob j0, RotJob j1, int nblk0, const int* __restrict__ gate,
+                      ZeroFix zf) {
   if (gate && *gate) return;
   constexpr int KQ = KP / 4;
   // B fragments of the core rotation in lane order (one conflict-free LDS.64
@@ -924,6 +953,25 @@ __global__ void __launch_bounds__(kRegWarps * 32, 8)
       }
     }
   }
+  if (zf.counter) {
+    // last CTA of this stream: every row of both sides is written (each
+    // thread fenced its stores before the arrival count), so the zero-sigma
+    // completion can run here instead of in its own launch
+    __shared__ int last;
+    __shared__ double zcoef[32], zred[32];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned prev = atomicAdd(zf.counter + b, 1u);
+      last = prev == gridDim.x - 1;
+      if (last) zf.counter[b] = 0;
+    }
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      complete_zero_stream(b, zf.w, zf.s, zf.lds, zf.U, zf.m, zf.V, zf.n, zcoef, zred);
+    }
+  }
 }
 
 // ----------------------------------------------------- completion (_install)
@@ -931,28 +979,29 @@ __device__ void complete_column(double* X, int64_t ld, int rows, int w, int t, d
                                 double* red) {
   // engine.py:33-56: first the existing direction projected off the others,
   // then e_0, e_1, ... until the residual norm exceeds 0.5.
-  // coef[c] = <X[:, c], X[:, t]> with a fixed-order block reduction
+  // coef[c] = <X[:, c], X[:, t]> with a fixed-order block reduction (L2 reads:
+  // in the fused path other CTAs wrote these rows)
   for (int c = 0; c < w; ++c) {
     double acc = 0.0;
     if (c != t)
-      for (int i = threadIdx.x; i < rows; i += blockDim.x) acc = fma(X[i * ld + c], X[i * ld + t], acc);
+      for (int i = threadIdx.x; i < rows; i += blockDim.x) acc = fma(__ldcg(&X[i * ld + c]), __ldcg(&X[i * ld + t]), acc);
     double v = block_sum(acc, red);
     if (threadIdx.x == 0) coef[c] = (c != t) ? v : 0.0;
   }
   __syncthreads();
   double nn = 0.0;
   for (int i = threadIdx.x; i < rows; i += blockDim.x) {
-    double v = X[i * ld + t];
+    double v = __ldcg(&X[i * ld + t]);
     for (int c = 0; c < w; ++c)
-      if (c != t) v -= X[i * ld + c] * coef[c];
+      if (c != t) v -= __ldcg(&X[i * ld + c]) * coef[c];
     nn = fma(v, v, nn);
   }
   double nrm = sqrt(block_sum(nn, red));
   if (nrm > 0.5) {
     for (int i = threadIdx.x; i < rows; i += blockDim.x) {
-      double v = X[i * ld + t];
+      double v = __ldcg(&X[i * ld + t]);
       for (int c = 0; c < w; ++c)
-        if (c != t) v -= X[i * ld + c] * coef[c];
+        if (c != t) v -= __ldcg(&X[i * ld + c]) * coef[c];
       X[i * ld + t] = v / nrm;
     }
     __syncthreads();
@@ -964,18 +1013,18 @@ __device__ void complete_column(double* X, int64_t ld, int rows, int w, int t, d
     for (int i = threadIdx.x; i < rows; i += blockDim.x) {
       double v = (i == axis) ? 1.0 : 0.0;
       for (int c = 0; c < w; ++c)
-        if (c != t) v -= X[i * ld + c] * X[axis * ld + c];
+        if (c != t) v -= __ldcg(&X[i * ld + c]) * __ldcg(&X[axis * ld + c]);
       cn = fma(v, v, cn);
     }
     double cnrm = sqrt(block_sum(cn, red));
     if (cnrm > 0.5) {
       // stage the axis row first: column t of row `axis` is overwritten below
-      for (int c = threadIdx.x; c < w; c += blockDim.x) coef[c] = X[axis * ld + c];
+      for (int c = threadIdx.x; c < w; c += blockDim.x) coef[c] = __ldcg(&X[axis * ld + c]);
       __syncthreads();
       for (int i = threadIdx.x; i < rows; i += blockDim.x) {
         double v = (i == axis) ? 1.0 : 0.0;
         for (int c = 0; c < w; ++c)
-          if (c != t) v -= X[i * ld + c] * coef[c];
+          if (c != t) v -= __ldcg(&X[i * ld + c]) * coef[c];
         X[i * ld + t] = v / cnrm;
       }
       __syncthreads();
@@ -991,24 +1040,7 @@ __global__ void complete_zero_kernel(int w, const double* __restrict__ s, int ld
   if (gate && *gate) return;
   extern __shared__ double coef[];  // [w]
   __shared__ double red[32];
-  const int b = blockIdx.x;
-  const double* sb = s + (int64_t)b * lds;
-  // common case: no zero sigma -- one parallel scan instead of w serial loads
-  bool any_zero = false;
-  for (int t = threadIdx.x; t < w; t += blockDim.x) any_zero |= sb[t] == 0.0;
-  if (!__syncthreads_or(any_zero)) return;
-  for (int t = 0; t < w; ++t) {
-    if (sb[t] != 0.0) continue;
-    for (int side = 0; side < 2; ++side) {
-      double* X = side == 0 ? U.p + b * U.stride : V.p + b * V.stride;
-      int64_t ld = side == 0 ? U.ld : V.ld;
-      int rows = side == 0 ? m : n;
-      double nn = 0.0;
-      for (int i = threadIdx.x; i < rows; i += blockDim.x) nn = fma(X[i * ld + t], X[i * ld + t], nn);
-      double nsq = block_sum(nn, red);
-      if (fabs(nsq - 1.0) > 1e-6) complete_column(X, ld, rows, w, t, coef, red);
-    }
-  }
+  complete_zero_stream(blockIdx.x, w, s, lds, U, m, V, n, coef, red);
 }
 
 // ------------------------------------------------------------------- K5
@@ -1345,7 +1377,7 @@ int launch_rank1_build(int batch, int r, Mat U, Mat V, const double* s, int lds,
 
 template <int KP>
 static int rotate_dispatch(int batch, int r, int keep, const RotJob& j0, const RotJob* j1,
-                           cudaStream_t st) {
+                           cudaStream_t st, const ZeroFix* zf, bool* fused) {
   const int NP = round_up(keep, 8);
   const int KQ = KP / 4, NT = NP / 8;
   size_t smem = sizeof(double) * ((size_t)KQ * NT * 32 + NP);
@@ -1373,8 +1405,10 @@ static int rotate_dispatch(int batch, int r, int keep, const RotJob& j0, const R
         rb1 = ceil_div(j1->rows, kRegRowsPerBlock);
         if (j1->new_row && rb1 == 0) rb1 = 1;
       }
+      const bool fz = zf && zf->w <= 32;
       rotate_reg_kernel<KP><<<dim3(rb0 + rb1, batch), kRegWarps * 32, 0, st>>>(
-          r, keep, j0, j1 ? *j1 : j0, rb0, g_gate);
+          r, keep, j0, j1 ? *j1 : j0, rb0, g_gate, fz ? *zf : ZeroFix{});
+      if (fused) *fused = fz;
       ISVD_LAUNCHED();
       return ISVD_OK;
     }
@@ -1386,7 +1420,9 @@ static int rotate_dispatch(int batch, int r, int keep, const RotJob& j0, const R
   return ISVD_OK;
 }
 
-int launch_rotate(int batch, int r, int keep, const RotJob& j0, const RotJob* j1, cudaStream_t st) {
+int launch_rotate(int batch, int r, int keep, const RotJob& j0, const RotJob* j1, cudaStream_t st,
+                  const ZeroFix* zf, bool* fused) {
+  if (fused) *fused = false;
   if (batch == 0) return ISVD_OK;
   int KP = round_up(r < 1 ? 1 : r, 8);
   if (KP > kRMax || round_up(keep, 8) > j0.X.ld || (j1 && round_up(keep, 8) > j1->X.ld)) {
@@ -1400,7 +1436,7 @@ int launch_rotate(int batch, int r, int keep, const RotJob& j0, const RotJob* j1
   switch (KP) {
 #define ISVD_ROT_CASE(K) \
   case K:                \
-    return rotate_dispatch<K>(batch, r, keep, j0, j1, st);
+    return rotate_dispatch<K>(batch, r, keep, j0, j1, st, zf, fused);
     ISVD_ROT_CASE(8)
     ISVD_ROT_CASE(16)
     ISVD_ROT_CASE(24)

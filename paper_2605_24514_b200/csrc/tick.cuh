@@ -75,7 +75,24 @@ struct RotJob {
 };
 
 // K3/K4: both factor rotations of a tick in one launch (FP64 DMMA).
-int launch_rotate(int batch, int r, int keep, const RotJob& j0, const RotJob* j1, cudaStream_t st);
+// Zero-sigma completion (_install, engine.py:59-70) fused into the rotation:
+// the last CTA of each stream to finish its rows completes U / V columns of
+// zero singular values (complete_zero_kernel's work).  counter: B unsigned
+// ints, zero between launches (the last CTA resets its stream's entry).
+struct ZeroFix {
+  const double* s = nullptr;
+  int lds = 0, w = 0;
+  Mat U{};
+  int m = 0;
+  Mat V{};
+  int n = 0;
+  unsigned* counter = nullptr;
+};
+// zf (optional): fuse the completion when the launch goes to
+// rotate_reg_kernel; *fused tells the caller whether it did (else the caller
+// launches complete_zero itself).
+int launch_rotate(int batch, int r, int keep, const RotJob& j0, const RotJob* j1, cudaStream_t st,
+                  const ZeroFix* zf = nullptr, bool* fused = nullptr);
 
 // engine.py:59-70 -- repair factor columns paired with exact-zero singular
 // values (no-op launch when none are zero).

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--groups", default="4")
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--e2e", action="store_true", help="also time the pinned-host loop")
+    ap.add_argument("--lags", default="1", help="result read-back lag(s) of the host loop")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     lib = _lib.load()
@@ -50,18 +51,19 @@ def main():
     if args.e2e:
         import time
         hr, hi, hj, hd = (pinned(x) for x in (rows, ii, jj, dd))
-        res = torch.empty((2, 3 * args.streams), dtype=torch.float64, pin_memory=True)
+        res = torch.empty((8, 3 * args.streams), dtype=torch.float64, pin_memory=True)
 
-        def run_host(nt):
+        def run_host(nt, lag):
             for t in range(nt):
                 if t % 2 == 0:
                     eng.row_append(hr[t // 2])
                 else:
                     eng.rank_one_update(hi[t // 2], hj[t // 2], hd[t // 2])
-                eng.scalars_async(res[t % 2].numpy(), t % 2)
-                if t > 0:
-                    eng.scalars_wait((t - 1) % 2)
-            eng.scalars_wait((nt - 1) % 2)
+                eng.scalars_async(res[t % 8].numpy(), t % 8)
+                if t >= lag:
+                    eng.scalars_wait((t - lag) % 8)
+            for t in range(max(0, nt - lag), nt):
+                eng.scalars_wait(t % 8)
             eng.flush()
             eng.synchronize()
 
@@ -81,15 +83,15 @@ def main():
             ms = e0.elapsed_time(e1) / args.ticks
             best = ms if best is None else min(best, ms)
         msg = f"groups={g}: {best:.4f} ms/tick  {args.streams / best / 1e3:.3f} M updates/s"
-        if args.e2e:
+        for lag in ([int(x) for x in args.lags.split(",")] if args.e2e else []):
             eng.restore()
-            run_host(16)
+            run_host(16, lag)
             eng.restore()
             eng.synchronize()
             t0 = time.perf_counter()
-            run_host(args.ticks)
+            run_host(args.ticks, lag)
             ms = (time.perf_counter() - t0) * 1e3 / args.ticks
-            msg += f" | e2e {ms:.4f} ms/tick {args.streams / ms / 1e3:.3f} M updates/s"
+            msg += f" | e2e lag {lag}: {ms:.4f} ms/tick {args.streams / ms / 1e3:.3f} M/s"
         print(msg, flush=True)
 
 
