@@ -574,6 +574,250 @@ __global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32_kernel(
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Column-layout variant of the warp-per-core Jacobi (s <= 32): lane l holds
+// the column at position l (32 doubles in registers).  The ordering, rotation
+// formulas, threshold, column swaps, incremental norms, V log and exit rule
+// are those of jacobi32_kernel above; what changes is the data movement of a
+// round: the two lanes of a pair exchange their columns with 32 register
+// shuffles and both compute a_pq = <g_p, g_q> with the same operands in the
+// same order (bit-identical on both lanes), so no cross-lane reduction tree
+// and no selects sit on the round's critical path (about half the
+// instructions per core of the row layout).
+template <bool ODD>
+__device__ __forceinline__ void j32c_round(double (&x)[32], int lane, double2* cs_log, double& nrm,
+                                           bool& any, float& relmax, double null2) {
+  // even rounds pair positions (2k, 2k+1); odd rounds (2k+1, 2k+2), 0 and 31 idle
+  const int partner = ODD ? ((lane & 1) ? lane + 1 : lane - 1) : (lane ^ 1);
+  const bool idle = ODD && (lane == 0 || lane == 31);
+  const int src = idle ? lane : partner;
+  const bool lower = lane < partner;
+  double y[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) y[i] = __shfl_sync(0xffffffffu, x[i], src);
+  const double pn = __shfl_sync(0xffffffffu, nrm, src);
+  // fma(x, y, .) == fma(y, x, .): both lanes get the same a_pq bit for bit
+  double d4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int i = 0; i < 32; ++i) d4[i & 3] = fma(x[i], y[i], d4[i & 3]);
+  const double apq = (d4[0] + d4[1]) + (d4[2] + d4[3]);
+  const double app = lower ? nrm : pn, aqq = lower ? pn : nrm;
+  double c = 1.0, sn = 0.0, t = 0.0;
+  const double apq2 = apq * apq, pq = app * aqq;
+  const bool rot = !idle && apq2 > (kOrthoEps * kOrthoEps) * pq && fmin(app, aqq) > null2;
+  if (rot) {
+    relmax = fmaxf(relmax, __fdividef((float)apq2, (float)pq));
+    const double d = aqq - app, h = 2.0 * apq;
+    const double big = fmax(fabs(d), fabs(h));
+    if (big < 1e150 && big > 1e-140) {
+      const double x2 = fma(d, d, h * h);
+      const double u = fabs(d) + x2 * j32_rsqrt(x2);
+      const double qq = j32_rsqrt(fma(u, u, h * h));
+      const double sh = d < 0.0 ? -h : h;
+      c = u * qq;
+      sn = sh * qq;
+      t = sh * j32_rcp(u);
+    } else {
+      const double zeta = d * j32_rcp(h);
+      const double w = fma(zeta, zeta, 1.0);
+      const double root = fabs(zeta) > 1e100 ? fabs(zeta) : w * j32_rsqrt(w);
+      t = copysign(j32_rcp(fabs(zeta) + root), zeta);
+      c = j32_rsqrt(fma(t, t, 1.0));
+      sn = t * c;
+    }
+  }
+  any |= rot;
+  // rotate and swap places: position p <- s g_p + c g_q, p+1 <- c g_p - s g_q
+  // (idle lanes: c = 1, s = 0, y = x, so x is kept exactly)
+  const double al = lower ? sn : -sn;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) x[i] = fma(al, x[i], c * y[i]);
+  if (!idle) {
+    nrm = lower ? fma(t, apq, aqq) : fma(-t, apq, app);
+    if (lower) cs_log[ODD ? (lane - 1) >> 1 : lane >> 1] = make_double2(c, sn);
+  }
+}
+
+template <bool BUILD>
+__global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32c_kernel(
+    int s, const double* __restrict__ core, int64_t core_stride, int ldcore, double* __restrict__ uk,
+    double* __restrict__ vk, int64_t out_stride, int ldo, double* __restrict__ sv,
+    int64_t sv_stride, int batch, Rank1Core rc, double* __restrict__ s_out, int64_t s_out_stride) {
+  extern __shared__ __align__(16) unsigned char j32_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int b = blockIdx.x * kJ32Warps + warp;
+  if (b >= batch) return;
+  J32Smem& W = reinterpret_cast<J32Smem*>(j32_raw)[warp];
+  double* nrmv = W.nrm;
+  int* pos = W.pos;
+  double x[32];  // column `lane` of G
+  if constexpr (BUILD) {
+    // Fused K6 (_kernels.pyx:209-213): K = diag(s) + delta U[i,:]^T Vt[:,j]^T,
+    // column q = s_q e_q + (delta b_q) a, with a = U[i, :] and b = V_eff[j, :]
+    // gathered through the deferred bases exactly as in jacobi32_kernel
+    const int64_t i = rc.ii[b], j = rc.jj[b];
+    const double d = rc.delta[b];
+    const LazyBasis& lz = rc.lz;
+    double ap = 0.0;
+    if (lane < s) {
+      if (!lz.active) {
+        ap = rc.U.p[b * rc.U.stride + i * rc.U.ld + lane];
+      } else if (i >= lz.m_base) {
+        ap = lz.W.p[b * lz.W.stride + (lz.r_base + (i - lz.m_base)) * lz.W.ld + lane];
+      } else {
+        const double* ur = rc.U.p + b * rc.U.stride + i * rc.U.ld;
+        const double* Wb = lz.W.p + b * lz.W.stride;
+        double a4[4] = {0.0, 0.0, 0.0, 0.0};
+        int c = 0;
+        for (; c + 4 <= lz.r_base; c += 4)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) a4[u] = fma(ur[c + u], Wb[(c + u) * lz.W.ld + lane], a4[u]);
+        for (; c < lz.r_base; ++c) a4[0] = fma(ur[c], Wb[c * lz.W.ld + lane], a4[0]);
+        ap = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+      }
+    }
+    const double* vr = rc.V.p + b * rc.V.stride + j * rc.V.ld;
+    double vq = 0.0;
+    if (lane < s) {
+      if (!rc.G) {
+        vq = vr[lane];
+      } else {
+        const double* Gb = rc.G + b * rc.g_stride;
+        double a4[4] = {0.0, 0.0, 0.0, 0.0};
+        int c = 0;
+        for (; c + 4 <= s; c += 4)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) a4[u] = fma(vr[c + u], Gb[(c + u) * rc.ldg + lane], a4[u]);
+        for (; c < s; ++c) a4[0] = fma(vr[c], Gb[c * rc.ldg + lane], a4[0]);
+        vq = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+      }
+    }
+    const double sp = lane < s ? rc.s[(int64_t)b * rc.lds + lane] : 0.0;
+    // the same product as the row layout (delta a_p) b_q, computed by lane q
+#pragma unroll
+    for (int r2 = 0; r2 < 32; ++r2) {
+      const double da = d * __shfl_sync(0xffffffffu, ap, r2);
+      double v = 0.0;
+      if (lane < s && r2 < s) {
+        v = da * vq;
+        if (r2 == lane) v += sp;
+      }
+      x[r2] = v;
+      W.V[lane][r2] = (lane == r2 && lane < s) ? 1.0 : 0.0;
+    }
+    if (lane == 0 && rc.A) {
+      double* e = rc.A + b * rc.a_stride + i * rc.lda + j;
+      const double old = *e;
+      *e = old + d;
+      rc.N[b] += 2.0 * d * old + d * d;
+    }
+  } else {
+    const double* K = core + b * core_stride;
+#pragma unroll
+    for (int r2 = 0; r2 < 32; ++r2) {
+      x[r2] = (lane < s && r2 < s) ? K[r2 * ldcore + lane] : 0.0;
+      W.V[lane][r2] = (lane == r2 && lane < s) ? 1.0 : 0.0;
+    }
+  }
+  auto col_norm = [&]() {
+    double n4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < 32; ++i) n4[i & 3] = fma(x[i], x[i], n4[i & 3]);
+    return (n4[0] + n4[1]) + (n4[2] + n4[3]);
+  };
+  int sweeps = 0;
+  for (; sweeps < kMaxSweeps;) {
+    bool any = false;
+    float relmax = 0.0f;
+    double nrm = col_norm();  // exact squared norm at the sweep start
+    const double null2 = fmax(1e-30 * warp_max(nrm), 1e-290);
+    for (int rr = 0; rr < 16; ++rr) {
+      j32c_round<false>(x, lane, W.log + (2 * rr) * 16, nrm, any, relmax, null2);
+      j32c_round<true>(x, lane, W.log + (2 * rr + 1) * 16, nrm, any, relmax, null2);
+    }
+    __syncwarp();
+    {
+      double v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = W.V[lane][j];
+      j32_apply_v(v, W.log);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) W.V[lane][j] = v[j];
+    }
+    __syncwarp();
+    ++sweeps;
+    if (!__any_sync(0xffffffffu, any)) break;
+    if (warp_max((double)relmax) <= kConvRel * kConvRel) break;
+  }
+  if (lane == 0) atomicAdd(&g_debug_counters[0], (unsigned long long)sweeps);
+  if (lane == 0) atomicAdd(&g_debug_counters[1], 1ull);
+  // position l holds original column id(l): a sweep reverses the order
+  const bool rev = sweeps & 1;
+  auto id_of = [&](int p) { return rev ? 31 - p : p; };
+  const double myn = sqrt(col_norm());
+  nrmv[lane] = myn;
+  __syncwarp();
+  {
+    const int myid = id_of(lane);
+    int rank = 0;
+    for (int p = 0; p < 32; ++p) {
+      const double o = nrmv[p];
+      const int oid = id_of(p);
+      rank += (o > myn) || (o == myn && oid < myid);
+    }
+    pos[lane] = rank;
+    W.ipos[rank] = lane;
+  }
+  const double s0 = warp_max(myn);
+  double* U = uk + b * out_stride;
+  double* Vo = (BUILD && rc.vk_out) ? rc.vk_out + b * rc.vk_stride : vk + b * out_stride;
+  const int ldv = (BUILD && rc.vk_out) ? rc.ldvk : ldo;
+  double* S = sv + b * sv_stride;
+  const bool live = myn > 0.0 && !(myn < kZeroSvRtol * s0);
+  const bool mine = id_of(lane) < s;
+  if (mine) {
+    S[pos[lane]] = live ? myn : 0.0;
+    if (s_out) s_out[b * s_out_stride + pos[lane]] = live ? myn : 0.0;  // install s directly
+  }
+  const bool any_dead = __any_sync(0xffffffffu, mine && !live);
+  __syncwarp();
+  // U = G / sigma_raw (_kernels.pyx:104): row i is written by all lanes at
+  // their sorted columns (one 256-byte row per instruction); V from smem
+  {
+    const double iv = live ? 1.0 / myn : 0.0;
+    const int oc = pos[lane];
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < s && mine) U[i * ldo + oc] = x[i] * iv;
+    if (lane < s) {
+      const int srcl = W.ipos[lane];
+      for (int i = 0; i < s; ++i) Vo[i * ldv + lane] = W.V[i][srcl];
+    }
+  }
+  __syncwarp();
+  if (!any_dead) return;
+  __threadfence_block();
+  for (int t = 0; t < s; ++t) {
+    if (S[t] > 0.0) continue;
+    for (int axis = 0; axis < s; ++axis) {
+      double val = 0.0;
+      if (lane < s) {
+        val = (lane == axis) ? 1.0 : 0.0;
+        for (int c = 0; c < s; ++c)
+          if (c != t) val -= U[lane * ldo + c] * U[axis * ldo + c];
+      }
+      const double nrm2 = warp_sum(val * val);
+      if (sqrt(nrm2) > 0.5) {
+        __syncwarp();
+        if (lane < s) U[lane * ldo + t] = val / sqrt(nrm2);
+        __syncwarp();
+        break;
+      }
+    }
+  }
+}
+
 }  // namespace
 
 int read_debug_counters(int64_t* out, int reset) {
@@ -603,11 +847,11 @@ int launch_rank1_core_svd32(int batch, int s, const Rank1Core& rc, double* uk, d
   static bool attr = false;
   const size_t smem = sizeof(J32Smem) * kJ32Warps;
   if (!attr) {
-    ISVD_CUDA(cudaFuncSetAttribute(jacobi32_kernel<true>,
+    ISVD_CUDA(cudaFuncSetAttribute(jacobi32c_kernel<true>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  jacobi32_kernel<true><<<ceil_div(batch, kJ32Warps), kJ32Warps * 32, smem, st>>>(
+  jacobi32c_kernel<true><<<ceil_div(batch, kJ32Warps), kJ32Warps * 32, smem, st>>>(
       s, nullptr, 0, 0, uk, vk, out_stride, ldo, sv, sv_stride, batch, rc, s_out, s_out_stride);
   ISVD_LAUNCHED();
   return ISVD_OK;
@@ -625,11 +869,11 @@ int launch_core_svd(int batch, int s, const double* core, int64_t core_stride, i
     static bool j32_attr = false;
     const size_t smem = sizeof(J32Smem) * kJ32Warps;
     if (!j32_attr) {
-      ISVD_CUDA(cudaFuncSetAttribute(jacobi32_kernel<false>,
+      ISVD_CUDA(cudaFuncSetAttribute(jacobi32c_kernel<false>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       j32_attr = true;
     }
-    jacobi32_kernel<false><<<ceil_div(batch, kJ32Warps), kJ32Warps * 32, smem, st>>>(
+    jacobi32c_kernel<false><<<ceil_div(batch, kJ32Warps), kJ32Warps * 32, smem, st>>>(
         s, core, core_stride, ldcore, uk, vk, out_stride, ldo, sv, sv_stride, batch, Rank1Core{},
         nullptr, 0);
     ISVD_LAUNCHED();
