@@ -185,15 +185,12 @@ __global__ void jacobi_core_kernel(int s, const double* __restrict__ core, int64
 
 // ---------------------------------------------------------------------------
 // Warp-per-core variant for s <= 32 (the rank-1 core of a k <= 32 stream).
-// Lane l holds row l of G and of V in registers.  Ordering: odd-even
-// transposition -- rounds alternate pairs (2k, 2k+1) and (2k+1, 2k+2) and
-// every rotated pair swaps places, so each pair of columns meets exactly once
-// per sweep of 32 rounds and all register indices are compile-time; after a
-// sweep the column order is reversed (tracked for the stable sort).  The 16
-// pair Grams (a_pp, a_qq, a_pq) of a round are reduce-scattered across the
-// warp with shuffles (lane l ends with pair l/2); the rotation (same formulas
-// and threshold as _kernels.pyx:38-57) is computed there and broadcast
-// through shared memory.
+// Ordering: odd-even transposition -- rounds alternate pairs (2k, 2k+1) and
+// (2k+1, 2k+2) and every rotated pair swaps places, so each pair of columns
+// meets exactly once per sweep of 32 rounds and all register indices are
+// compile-time; after a sweep the column order is reversed (tracked for the
+// stable sort).  Rotation formulas and threshold as _kernels.pyx:38-57.  V
+// is rotated once per sweep from a shared-memory (c, s) log (row layout).
 constexpr int kJ32Warps = 4;
 // Sweep exit: once every rotation of a sweep had |a_pq| <= kConvRel
 // sqrt(a_pp a_qq), the off-diagonal left is O(kConvRel^2) relative (cyclic
@@ -203,19 +200,6 @@ constexpr int kJ32Warps = 4;
 // off-diagonals ~1e-5 relative, so one sweep suffices (measured 1.00
 // sweeps/core on config 5a; 1.97 with kConvRel = 1e-8).
 constexpr double kConvRel = 1e-6;
-
-template <bool ODD>
-__device__ __forceinline__ double j32_pair_product(const double (&g)[32], int k) {
-  if (ODD && k == 15) return 0.0;
-  const int p = ODD ? 2 * k + 1 : 2 * k;
-  return g[p] * g[p + 1];
-}
-
-__device__ __forceinline__ void halve(double& keep, double lo, double hi, bool upper, int off) {
-  const double mine = upper ? hi : lo;
-  const double other = upper ? lo : hi;
-  keep = mine + __shfl_xor_sync(0xffffffffu, other, off);
-}
 
 // 1/sqrt(x) to ~1 ulp: MUFU.RSQ64H seed + two Newton steps (x > 0, normal)
 __device__ __forceinline__ double j32_rsqrt(double x) {
@@ -233,85 +217,6 @@ __device__ __forceinline__ double j32_rcp(double x) {
   r = fma(r, e, r);
   e = fma(-x, r, 1.0);
   return fma(r, e, r);
-}
-
-// One round: lane l owns pair k = l >> 1 (lanes 2k, 2k+1 redundantly) and
-// carries the squared norms (nlo, nhi) of that pair's two columns.  Only the
-// 16 cross products a_pq are reduce-scattered; the norms are updated in
-// place (a_pp' = a_pp - t a_pq, a_qq' = a_qq + t a_pq) and recomputed
-// exactly at every sweep start.
-template <bool ODD>
-__device__ __forceinline__ bool j32_round(double (&g)[32], int lane, double2* cs_sm, double& nlo,
-                                          double& nhi, float& relmax, double null2) {
-  double W[8];
-  const bool b4 = lane & 16;
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-    halve(W[i], j32_pair_product<ODD>(g, i), j32_pair_product<ODD>(g, i + 8), b4, 16);
-  const bool b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) halve(W[i], W[i], W[i + 4], b3, 8);
-#pragma unroll
-  for (int i = 0; i < 2; ++i) halve(W[i], W[i], W[i + 2], b2, 4);
-  halve(W[0], W[0], W[1], b1, 2);
-  const double apq = W[0] + __shfl_xor_sync(0xffffffffu, W[0], 1);
-  const double app = nlo, aqq = nhi;
-  double c = 1.0, s = 0.0, t = 0.0;
-  // Rotate iff |a_pq| > 1e-14 sqrt(a_pp a_qq) (_kernels.pyx:38), compared in
-  // squares so no IEEE sqrt/div (and their slow-path calls) sits on the
-  // round's critical path.  Columns below 1e-15 of the largest norm are
-  // numerically zero (they snap to sigma = 0) and are left alone.
-  const double apq2 = apq * apq, pq = app * aqq;
-  const bool rot = apq2 > (kOrthoEps * kOrthoEps) * pq && fmin(app, aqq) > null2;
-  if (rot) {
-    relmax = fmaxf(relmax, __fdividef((float)apq2, (float)pq));
-    // the same rotation as _kernels.pyx:40-44 (t = sign(zeta) / (|zeta| +
-    // sqrt(1 + zeta^2)), zeta = (a_qq - a_pp) / 2a_pq) written with d = a_qq -
-    // a_pp, h = 2 a_pq, u = |d| + sqrt(d^2 + h^2): t = sign(d) h / u,
-    // c = u / sqrt(u^2 + h^2), s = sign(d) h / sqrt(u^2 + h^2) -- two
-    // reciprocal square roots on the critical path instead of four MUFU steps
-    const double d = aqq - app, h = 2.0 * apq;
-    const double big = fmax(fabs(d), fabs(h));
-    if (big < 1e150 && big > 1e-140) {
-      const double x2 = fma(d, d, h * h);
-      const double u = fabs(d) + x2 * j32_rsqrt(x2);
-      const double qq = j32_rsqrt(fma(u, u, h * h));
-      const double sh = d < 0.0 ? -h : h;  // sign(d) h
-      c = u * qq;
-      s = sh * qq;
-      t = sh * j32_rcp(u);
-    } else {
-      const double zeta = d * j32_rcp(h);
-      const double w = fma(zeta, zeta, 1.0);
-      const double root = fabs(zeta) > 1e100 ? fabs(zeta) : w * j32_rsqrt(w);
-      t = copysign(j32_rcp(fabs(zeta) + root), zeta);
-      c = j32_rsqrt(fma(t, t, 1.0));
-      s = t * c;
-    }
-  }
-  const bool dummy = ODD && (lane >> 1) == 15;
-  if (!dummy) {
-    // norms after the rotation, then the two columns swap places
-    const double np = fma(-t, apq, app), nq = fma(t, apq, aqq);
-    nlo = nq;
-    nhi = np;
-  }
-#ifdef ISVD_DEBUG_J32
-  if (blockIdx.x == 0 && (lane & 1) == 0 && (rot || c != c || s != s || app != app || aqq != aqq))
-    printf("odd=%d lane=%d app=%g aqq=%g apq=%g rot=%d c=%g s=%g\n", (int)ODD, lane, app, aqq, apq, (int)rot, c, s);
-#endif
-  if ((lane & 1) == 0) cs_sm[lane >> 1] = make_double2(c, s);
-  __syncwarp();
-#pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    if (ODD && k == 15) break;
-    const int p = ODD ? 2 * k + 1 : 2 * k;
-    const double2 r = cs_sm[k];
-    const double gp = g[p], gq = g[p + 1];
-    g[p] = r.y * gp + r.x * gq;  // columns swap places after meeting
-    g[p + 1] = r.x * gp - r.y * gq;
-  }
-  return __any_sync(0xffffffffu, rot);
 }
 
 // Replays the logged rotations of one sweep (32 rounds) on a row of V.
@@ -349,242 +254,14 @@ struct J32Smem {
   int ipos[32];
 };
 
-template <bool BUILD>
-__global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32_kernel(
-    int s, const double* __restrict__ core, int64_t core_stride, int ldcore, double* __restrict__ uk,
-    double* __restrict__ vk, int64_t out_stride, int ldo, double* __restrict__ sv,
-    int64_t sv_stride, int batch, Rank1Core rc, double* __restrict__ s_out, int64_t s_out_stride) {
-  extern __shared__ __align__(16) unsigned char j32_raw[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int b = blockIdx.x * kJ32Warps + warp;
-  if (b >= batch) return;
-  J32Smem& W = reinterpret_cast<J32Smem*>(j32_raw)[warp];
-  double* nrm = W.nrm;
-  int* pos = W.pos;
-  double g[32];
-  if constexpr (BUILD) {
-    // Fused K6: lane p builds row p of K = diag(s) + delta U[i,:]^T Vt[:,j]^T
-    // (_kernels.pyx:209-213, same arithmetic as rank1_build_kernel) in
-    // registers -- the core never goes through HBM -- and lane 0 applies the
-    // tracked-entry update A[i,j] += delta, N += 2 delta a_old + delta^2
-    // (engine.py:162-166).
-    const int64_t i = rc.ii[b], j = rc.jj[b];
-    const double d = rc.delta[b];
-    const LazyBasis& lz = rc.lz;
-    double ap = 0.0;
-    if (lane < s) {
-      if (!lz.active) {
-        ap = rc.U.p[b * rc.U.stride + i * rc.U.ld + lane];
-      } else if (i >= lz.m_base) {
-        ap = lz.W.p[b * lz.W.stride + (lz.r_base + (i - lz.m_base)) * lz.W.ld + lane];
-      } else {
-        const double* ur = rc.U.p + b * rc.U.stride + i * rc.U.ld;
-        const double* Wb = lz.W.p + b * lz.W.stride;
-        double a4[4] = {0.0, 0.0, 0.0, 0.0};  // four independent chains
-        int c = 0;
-        for (; c + 4 <= lz.r_base; c += 4)
-#pragma unroll
-          for (int u = 0; u < 4; ++u) a4[u] = fma(ur[c + u], Wb[(c + u) * lz.W.ld + lane], a4[u]);
-        for (; c < lz.r_base; ++c) a4[0] = fma(ur[c], Wb[c * lz.W.ld + lane], a4[0]);
-        ap = (a4[0] + a4[1]) + (a4[2] + a4[3]);
-      }
-    }
-    const double* vr = rc.V.p + b * rc.V.stride + j * rc.V.ld;
-    // lane q holds V_eff[j, q] (= V[j, :] . G[:, q] while V is deferred)
-    double vq = 0.0;
-    if (lane < s) {
-      if (!rc.G) {
-        vq = vr[lane];
-      } else {
-        const double* Gb = rc.G + b * rc.g_stride;
-        double a4[4] = {0.0, 0.0, 0.0, 0.0};
-        int c = 0;
-        for (; c + 4 <= s; c += 4)
-#pragma unroll
-          for (int u = 0; u < 4; ++u) a4[u] = fma(vr[c + u], Gb[(c + u) * rc.ldg + lane], a4[u]);
-        for (; c < s; ++c) a4[0] = fma(vr[c], Gb[c * rc.ldg + lane], a4[0]);
-        vq = (a4[0] + a4[1]) + (a4[2] + a4[3]);
-      }
-    }
-    const double sp = lane < s ? rc.s[(int64_t)b * rc.lds + lane] : 0.0;
-    const double da = d * ap;
-#pragma unroll
-    for (int q = 0; q < 32; ++q) {
-      const double bq = __shfl_sync(0xffffffffu, vq, q);
-      double v = 0.0;
-      if (lane < s && q < s) {
-        v = da * bq;
-        if (q == lane) v += sp;
-      }
-      g[q] = v;
-      W.V[lane][q] = (lane == q && lane < s) ? 1.0 : 0.0;
-    }
-    if (lane == 0 && rc.A) {
-      double* e = rc.A + b * rc.a_stride + i * rc.lda + j;
-      const double old = *e;
-      *e = old + d;
-      rc.N[b] += 2.0 * d * old + d * d;
-    }
-  } else {
-    const double* K = core + b * core_stride;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      g[j] = (lane < s && j < s) ? K[lane * ldcore + j] : 0.0;
-      W.V[lane][j] = (lane == j && lane < s) ? 1.0 : 0.0;
-    }
-  }
-  // Sweeps until none rotates (_kernels.pyx:58-59), or until a sweep whose
-  // rotations were all below kConvRel (quadratic convergence, see kConvRel):
-  // the confirming sweeps are skipped.
-  int sweeps = 0;
-  for (; sweeps < kMaxSweeps;) {
-    bool any = false;
-    float relmax = 0.0f;
-    // exact squared column norms at the sweep start (lane l: position l)
-    double R[16];
-    {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) halve(R[i], g[i] * g[i], g[i + 16] * g[i + 16], lane & 16, 16);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) halve(R[i], R[i], R[i + 8], lane & 8, 8);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) halve(R[i], R[i], R[i + 4], lane & 4, 4);
-#pragma unroll
-      for (int i = 0; i < 2; ++i) halve(R[i], R[i], R[i + 2], lane & 2, 2);
-      halve(R[0], R[0], R[1], lane & 1, 1);
-    }
-    double nlo = __shfl_sync(0xffffffffu, R[0], lane & ~1);
-    double nhi = __shfl_sync(0xffffffffu, R[0], lane | 1);
-    const double null2 = fmax(1e-30 * warp_max(R[0]), 1e-290);
-    for (int rr = 0; rr < 16; ++rr) {
-      any |= j32_round<false>(g, lane, W.log + (2 * rr) * 16, nlo, nhi, relmax, null2);
-      // even -> odd pairing: (2k+1, 2k+2); position 0 sits out
-      const double n0 = nlo;
-      {
-        const double down = __shfl_down_sync(0xffffffffu, nlo, 2);
-        nlo = nhi;
-        nhi = down;
-      }
-      any |= j32_round<true>(g, lane, W.log + (2 * rr + 1) * 16, nlo, nhi, relmax, null2);
-      // odd -> even pairing: (2k, 2k+1)
-      {
-        const double up = __shfl_up_sync(0xffffffffu, nhi, 2);
-        nhi = nlo;
-        nlo = (lane < 2) ? n0 : up;
-      }
-    }
-    // V phase: replay the sweep's rotations (and swaps) on this lane's row
-    {
-      double v[32];
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = W.V[lane][j];
-      j32_apply_v(v, W.log);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) W.V[lane][j] = v[j];
-    }
-    __syncwarp();
-    ++sweeps;
-    if (!any) break;
-    if (warp_max((double)relmax) <= kConvRel * kConvRel) break;
-  }
-  if (lane == 0) atomicAdd(&g_debug_counters[0], (unsigned long long)sweeps);
-  if (lane == 0) atomicAdd(&g_debug_counters[1], 1ull);
-  // column norms: reduce-scatter 32 sums, lane l ends with position l
-  double R[16];
-  {
-    const bool b4 = lane & 16;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) halve(R[i], g[i] * g[i], g[i + 16] * g[i + 16], b4, 16);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) halve(R[i], R[i], R[i + 8], lane & 8, 8);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) halve(R[i], R[i], R[i + 4], lane & 4, 4);
-#pragma unroll
-    for (int i = 0; i < 2; ++i) halve(R[i], R[i], R[i + 2], lane & 2, 2);
-    halve(R[0], R[0], R[1], lane & 1, 1);
-  }
-  // position l holds original column id(l): a sweep reverses the order
-  const bool rev = sweeps & 1;
-  auto id_of = [&](int p) { return rev ? 31 - p : p; };
-  nrm[lane] = sqrt(R[0]);
-  __syncwarp();
-  {
-    const double mine = nrm[lane];
-    const int myid = id_of(lane);
-    int rank = 0;
-    for (int p = 0; p < 32; ++p) {
-      const double o = nrm[p];
-      const int oid = id_of(p);
-      rank += (o > mine) || (o == mine && oid < myid);
-    }
-    pos[lane] = rank;
-    W.ipos[rank] = lane;
-  }
-  const double s0 = warp_max(nrm[lane]);
-  double* U = uk + b * out_stride;
-  double* Vo = (BUILD && rc.vk_out) ? rc.vk_out + b * rc.vk_stride : vk + b * out_stride;
-  const int ldv = (BUILD && rc.vk_out) ? rc.ldvk : ldo;
-  double* S = sv + b * sv_stride;
-  bool any_dead;
-  {
-    const double r = nrm[lane];
-    const bool live = r > 0.0 && !(r < kZeroSvRtol * s0);
-    if (id_of(lane) < s) {
-      S[pos[lane]] = live ? r : 0.0;
-      if (s_out) s_out[b * s_out_stride + pos[lane]] = live ? r : 0.0;  // install s directly
-    }
-    W.inv[lane] = live ? 1.0 / r : 0.0;  // U = G / sigma_raw (_kernels.pyx:104)
-    any_dead = __any_sync(0xffffffffu, id_of(lane) < s && !live);
-  }
-  // Coalesced output: stage this lane's row of G in smem (column p at p ^ row
-  // so the 32 rows hit distinct banks), then write U and V one row per
-  // instruction with the lanes over the sorted output columns.
-  double* Gs = reinterpret_cast<double*>(W.log);
-#pragma unroll
-  for (int p = 0; p < 32; ++p) Gs[lane * 32 + (p ^ lane)] = g[p];
-  __syncwarp();
-  if (lane < s) {
-    const int src = W.ipos[lane];  // the column that lands in output column `lane`
-    const double iv = W.inv[src];
-    for (int i = 0; i < s; ++i) {
-      U[i * ldo + lane] = Gs[i * 32 + (src ^ i)] * iv;
-      Vo[i * ldv + lane] = W.V[i][src];
-    }
-  }
-  __syncwarp();
-  // dead-column completion (_kernels.pyx:62-79), rare
-  if (!any_dead) return;
-  for (int t = 0; t < s; ++t) {
-    if (S[t] > 0.0) continue;
-    for (int axis = 0; axis < s; ++axis) {
-      double val = 0.0;
-      if (lane < s) {
-        val = (lane == axis) ? 1.0 : 0.0;
-        for (int c = 0; c < s; ++c)
-          if (c != t) val -= U[lane * ldo + c] * U[axis * ldo + c];
-      }
-      const double nrm2 = warp_sum(val * val);
-      if (sqrt(nrm2) > 0.5) {
-        __syncwarp();
-        if (lane < s) U[lane * ldo + t] = val / sqrt(nrm2);
-        __syncwarp();
-        break;
-      }
-    }
-  }
-}
-
-
 // ---------------------------------------------------------------------------
-// Column-layout variant of the warp-per-core Jacobi (s <= 32): lane l holds
-// the column at position l (32 doubles in registers).  The ordering, rotation
-// formulas, threshold, column swaps, incremental norms, V log and exit rule
-// are those of jacobi32_kernel above; what changes is the data movement of a
-// round: the two lanes of a pair exchange their columns with 32 register
-// shuffles and both compute a_pq = <g_p, g_q> with the same operands in the
-// same order (bit-identical on both lanes), so no cross-lane reduction tree
-// and no selects sit on the round's critical path (about half the
-// instructions per core of the row layout).
+// Column layout: lane l holds the column at position l (32 doubles in
+// registers).  A round's two lanes of a pair exchange their columns with 32
+// register shuffles and both compute a_pq = <g_p, g_q> with the same
+// operands in the same order (bit-identical on both lanes), so no
+// cross-lane reduction tree and no selects sit on the round's critical path
+// (a row layout -- lane = row, pair Grams reduce-scattered across the warp --
+// needed ~30% more instructions per core).
 template <bool ODD>
 __device__ __forceinline__ void j32c_round(double (&x)[32], int lane, double2* cs_log, double& nrm,
                                            bool& any, float& relmax, double null2) {
@@ -655,7 +332,7 @@ __global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32c_kernel(
   if constexpr (BUILD) {
     // Fused K6 (_kernels.pyx:209-213): K = diag(s) + delta U[i,:]^T Vt[:,j]^T,
     // column q = s_q e_q + (delta b_q) a, with a = U[i, :] and b = V_eff[j, :]
-    // gathered through the deferred bases exactly as in jacobi32_kernel
+    // gathered through the deferred bases (U = [Ub 0; 0 I] W, V_eff = [V | Z^T] G)
     const int64_t i = rc.ii[b], j = rc.jj[b];
     const double d = rc.delta[b];
     const LazyBasis& lz = rc.lz;
@@ -680,16 +357,21 @@ __global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32c_kernel(
     const double* vr = rc.V.p + b * rc.V.stride + j * rc.V.ld;
     double vq = 0.0;
     if (lane < s) {
-      if (!rc.G) {
+      const VDefer& vd = rc.vd;
+      if (!vd.G) {
         vq = vr[lane];
       } else {
-        const double* Gb = rc.G + b * rc.g_stride;
+        // V_eff[j, :] = [V[j, :fw] | Z[:, j]^T] G
+        const double* Gb = vd.G + b * vd.g_stride;
         double a4[4] = {0.0, 0.0, 0.0, 0.0};
         int c = 0;
-        for (; c + 4 <= s; c += 4)
+        for (; c + 4 <= vd.fw; c += 4)
 #pragma unroll
-          for (int u = 0; u < 4; ++u) a4[u] = fma(vr[c + u], Gb[(c + u) * rc.ldg + lane], a4[u]);
-        for (; c < s; ++c) a4[0] = fma(vr[c], Gb[c * rc.ldg + lane], a4[0]);
+          for (int u = 0; u < 4; ++u) a4[u] = fma(vr[c + u], Gb[(c + u) * vd.ldg + lane], a4[u]);
+        for (; c < vd.fw; ++c) a4[0] = fma(vr[c], Gb[c * vd.ldg + lane], a4[0]);
+        const double* Zb = vd.Z + b * vd.z_stride + j;
+        for (int t = 0; t < vd.nz; ++t)
+          a4[t & 3] = fma(Zb[(int64_t)t * vd.ldz], Gb[(vd.fw + t) * vd.ldg + lane], a4[t & 3]);
         vq = (a4[0] + a4[1]) + (a4[2] + a4[3]);
       }
     }

@@ -39,10 +39,8 @@ struct Rank1Core {
   int lda = 0;
   double* N = nullptr;
   LazyBasis lz{};
-  // Deferred right basis: V_eff = V . G (G: s x s per stream) when G != null
-  const double* G = nullptr;
-  int64_t g_stride = 0;
-  int ldg = 0;
+  // Deferred right basis (tick.cuh VDefer): V_eff = [V | Z^T] G when vd.G
+  VDefer vd{};
   // Optional separate destination for the core's right vectors (row-major,
   // vk_stride per stream, leading dimension ldvk) instead of vk/ldo
   double* vk_out = nullptr;

@@ -226,16 +226,41 @@ struct isvd_engine {
   // Rank-1 ticks rotate the small Gv instead of the n x r V; the next row
   // append projects through Gv and folds it into its own V rotation, so a
   // rank-1 tick costs no pass over V.
+  // Full-rank row appends defer V as well: V_eff = [V(:, :vfw) | Z^T] Gv
+  // with Z the vnz unnormalised residuals appended since (kVWin at most);
+  // the row tick then writes one residual and grows Gv by a row instead of
+  // rotating V, and V is materialised every kVWin row appends.
   int vdefer_mode = 1;  // 0 off, 1 on for batches >= 64, 2 whenever the kernels allow
   bool vpend = false;
   double* Gv = nullptr;
-  int64_t gstride() const { return (int64_t)(ld + 1) * ld; }
+  double* Zv = nullptr;
+  int zv_ncap = 0;
+  int vfw = 0, vnz = 0;
+  int64_t gstride() const { return (int64_t)(ld + kVWin + 1) * ld; }
   Mat Gm() const { return Mat{Gv, gstride(), ld}; }
+  int64_t zvstride() const { return (int64_t)kVWin * n_cap; }
+  VDefer vdesc(int b0, int nz) const {
+    VDefer d;
+    d.G = Gv + b0 * gstride();
+    d.g_stride = gstride();
+    d.ldg = ld;
+    d.fw = vfw;
+    d.nz = nz;
+    d.Z = Zv ? Zv + b0 * zvstride() : nullptr;
+    d.z_stride = zvstride();
+    d.ldz = n_cap;
+    return d;
+  }
   bool vdefer_ok() const {
     return vdefer_mode != 0 && !sharded && r >= 1 && k <= 32 && (vdefer_mode == 2 || B >= 64);
   }
   int ensure_gv() {
     if (!Gv) ISVD_TRY(dalloc(&Gv, (size_t)B * gstride()));
+    if (Zv && zv_ncap != n_cap) dfree(Zv);
+    if (!Zv) {
+      ISVD_TRY(dalloc(&Zv, (size_t)B * zvstride()));
+      zv_ncap = n_cap;
+    }
     return ISVD_OK;
   }
   struct Snap {
@@ -303,13 +328,34 @@ struct isvd_engine {
   std::vector<cudaEvent_t> flush_marks;
   double flush_bytes = 0.0;
 
-  // V <- V Gv ; ends the deferred right basis
-  int flush_v() {
+  // V <- [V(:, :vfw) | Z^T] Gv ; ends the deferred right basis.  in_tick:
+  // per stream group on the group streams when they are pending.
+  int flush_v(bool in_tick = false) {
     if (!vpend) return ISVD_OK;
-    join();
-    RotJob jv{Vm(), n, Gv, gstride(), ld, nullptr, 0, nullptr, 0};
-    ISVD_TRY(launch_rotate(B, r, r, jv, nullptr, st));
+    const bool grouped = in_tick && pend && !timing;
+    if (!grouped) join();
+    auto body = [&](int b0, int nb, cudaStream_t s2) -> int {
+      RotJob jv{Mat{V + b0 * vstride(), vstride(), ld}, n, Gv + b0 * gstride(), gstride(), ld,
+                nullptr, 0, nullptr, 0};
+      if (vnz > 0) {
+        jv.zs = Zv + b0 * zvstride();
+        jv.zs_stride = zvstride();
+        jv.ldzs = n_cap;
+        jv.zfw = vfw;
+      }
+      return launch_rotate(nb, vfw + vnz, r, jv, nullptr, s2);
+    };
+    if (grouped) {
+      for (int g = 0; g < pend_G; ++g) {
+        const int b0 = (int)((int64_t)B * g / pend_G), b1 = (int)((int64_t)B * (g + 1) / pend_G);
+        ISVD_TRY(body(b0, b1 - b0, gst[g]));
+        ISVD_CUDA(cudaEventRecord(join_ev[g], gst[g]));
+      }
+    } else {
+      ISVD_TRY(body(0, B, st));
+    }
     vpend = false;
+    vnz = 0;
     return ISVD_OK;
   }
   // materialise both deferred bases
@@ -433,6 +479,7 @@ struct isvd_engine {
 
   int grow_cols(int cols_needed) {
     if (cols_needed <= n_cap) return ISVD_OK;
+    ISVD_TRY(flush_v());  // Z and Gv describe the old V layout
     join();
     int nc = std::max(cols_needed, n_cap * 2);
     double *V2, *A2;
@@ -522,6 +569,7 @@ struct isvd_engine {
     lazy_active = false;  // U is recomputed from A
     lazy_b = 0;
     vpend = false;
+    vnz = 0;
     if (sharded) {
       ISVD_TRY(gram_svd_run(m, n, A, n_cap, w, Um(), Vm(), s, nullptr, st, arp()));
     } else {
@@ -544,7 +592,7 @@ struct isvd_engine {
     dfree(core); dfree(uk); dfree(vk); dfree(sv); dfree(vscr);
     dfree(z); dfree(inj); dfree(rho); dfree(xnorm); dfree(ev);
     dfree(ei); dfree(ej); dfree(ed); dfree(dflag);
-    if (zf_cnt) cudaFree(zf_cnt); dfree(ref); dfree(W); dfree(Gv);
+    if (zf_cnt) cudaFree(zf_cnt); dfree(ref); dfree(W); dfree(Gv); dfree(Zv);
     dfree(wx); dfree(wj); dfree(wpart); dfree(wout); dfree(wflags);
     dfree(snap.U); dfree(snap.V); dfree(snap.A); dfree(snap.s); dfree(snap.N); dfree(shv);
     for (auto g : gst) cudaStreamDestroy(g);
@@ -750,8 +798,10 @@ static Mat mat_at(const Mat& M, int b0) { return Mat{M.p + b0 * M.stride, M.stri
 // lazy_state: 0 = eager rotation, 1 = open a deferred window, 2 = continue it
 // vp: the right basis is deferred (V_eff = V Gv); this row append projects
 // through Gv and folds it into the V rotation
+// vrow: full-rank row append with the right basis deferred -- the residual
+// goes to Z, Gv grows by a row, V is not touched (vstart: Gv <- I first)
 static int issue_append(isvd_engine* e, const Slice& sl, const double* xd, int len, bool is_row,
-                        int keep, int lazy_state, bool vp) {
+                        int keep, int lazy_state, bool vp, bool vrow, bool vstart) {
   const int b0 = sl.b0, nb = sl.nb, r = e->r;
   cudaStream_t st = sl.st;
   const int S = e->S();
@@ -770,13 +820,20 @@ static int issue_append(isvd_engine* e, const Slice& sl, const double* xd, int l
   // sharded: only the owner stores an appended row; a column append projects
   // on the row-sharded U (sums across shards)
   double* Adst = (is_row && !e->owner) ? nullptr : e->A + b0 * e->astride();
+  if (vstart) ISVD_TRY(launch_eye(nb, mat_at(e->Gm(), b0), r, r, st));
+  VDefer vd = e->vdesc(b0, vrow ? e->vnz : 0);
+  double* zdst = z;
+  int64_t zdst_stride = e->zlen();
+  if (vrow) {  // the residual becomes column vfw + vnz of the deferred basis
+    zdst = e->Zv + b0 * e->zvstride() + (int64_t)e->vnz * e->n_cap;
+    zdst_stride = e->zvstride();
+  }
   ISVD_TRY(launch_project_append(nb, len, r, F, xd + (int64_t)b0 * len, len,
-                                 e->s + (int64_t)b0 * e->ld, e->ld, e->tol, core, cs, S, z,
-                                 e->zlen(), inj, e->rho + b0, e->xnorm + b0, Adst, e->astride(),
+                                 e->s + (int64_t)b0 * e->ld, e->ld, e->tol, core, cs, S, zdst,
+                                 zdst_stride, inj, e->rho + b0, e->xnorm + b0, Adst, e->astride(),
                                  a_off, a_step, e->N + b0, st,
                                  (e->sharded && !is_row) ? &e->ar : nullptr,
-                                 e->append_jacobi ? 0 : 1, vp ? e->Gv + b0 * e->gstride() : nullptr,
-                                 e->gstride(), e->ld));
+                                 e->append_jacobi ? 0 : 1, (vp || vrow) ? &vd : nullptr));
   if (one) e->mark();
   if (e->append_jacobi)
     ISVD_TRY(launch_core_svd(nb, r + 1, core, cs, S, uk, vk, cs, S, sv, S,
@@ -808,6 +865,12 @@ static int issue_append(isvd_engine* e, const Slice& sl, const double* xd, int l
     injj.g_stride = e->gstride();
     injj.ldg = e->ld;
   }
+  if (vrow) {
+    // Gv <- [Gv 0; 0 1/rho] Vk[:, :keep]: the rows of the basis rotate, the
+    // new residual's row is (1/rho) Vk[r, :] (0 when rho <= tol)
+    injj = RotJob{mat_at(e->Gm(), b0), e->vfw + e->vnz, vk, cs, S, nullptr, 0, nullptr, 1};
+    injj.nr_scale = inj;
+  }
   // zero-sigma completion (_install) over the post-tick factors: fused into
   // the rotation when the secular kernel already installed s
   const int m_new = is_row ? e->m + 1 : e->m, n_new = is_row ? e->n : e->n + 1;
@@ -820,6 +883,7 @@ static int issue_append(isvd_engine* e, const Slice& sl, const double* xd, int l
   zf.V = mat_at(e->Vm(), b0);
   zf.n = n_new;
   zf.counter = e->zf_cnt + b0;
+  if (vrow) zf.vd = e->vdesc(b0, e->vnz + 1);
   const ZeroFix* zfp = e->append_jacobi ? nullptr : &zf;
   bool fused = false;
   if (has_u) {
@@ -834,7 +898,9 @@ static int issue_append(isvd_engine* e, const Slice& sl, const double* xd, int l
     ISVD_CUDA(cudaMemcpy2DAsync(e->s + (int64_t)b0 * e->ld, sizeof(double) * e->ld, sv,
                                 sizeof(double) * S, sizeof(double) * keep, nb,
                                 cudaMemcpyDeviceToDevice, st));
-  if (!fused) ISVD_TRY(launch_complete_zero(nb, keep, zf.s, zf.lds, zf.U, zf.m, zf.V, zf.n, st));
+  if (!fused)
+    ISVD_TRY(launch_complete_zero(nb, keep, zf.s, zf.lds, zf.U, zf.m, zf.V, zf.n, st,
+                                  vrow ? &zf.vd : nullptr));
   return ISVD_OK;
 }
 
@@ -871,9 +937,7 @@ static int issue_rank_one(isvd_engine* e, const Slice& sl, const int64_t* di, co
     rc.N = e->N + b0;
     rc.lz = lz;
     if (vp) {
-      rc.G = e->Gv + b0 * e->gstride();
-      rc.g_stride = e->gstride();
-      rc.ldg = e->ld;
+      rc.vd = e->vdesc(b0, e->vnz);
     } else if (defer) {
       rc.vk_out = e->Gv + b0 * e->gstride();
       rc.vk_stride = e->gstride();
@@ -920,7 +984,7 @@ static int issue_rank_one(isvd_engine* e, const Slice& sl, const int64_t* di, co
   bool has_v = true;
   if (defer) {
     if (vp)
-      vj = RotJob{mat_at(e->Gm(), b0), r, vk, cs, S, nullptr, 0, nullptr, 0};
+      vj = RotJob{mat_at(e->Gm(), b0), e->vfw + e->vnz, vk, cs, S, nullptr, 0, nullptr, 0};
     else
       has_v = false;
   }
@@ -930,9 +994,10 @@ static int issue_rank_one(isvd_engine* e, const Slice& sl, const int64_t* di, co
   zf.w = r;
   zf.U = lazy_state != 0 ? mat_at(e->Wm(), b0) : mat_at(e->Um(), b0);
   zf.m = lazy_state != 0 ? e->r_base_next + e->lazy_b_next : e->m;
-  zf.V = defer ? mat_at(e->Gm(), b0) : mat_at(e->Vm(), b0);
-  zf.n = defer ? r : e->n;
+  zf.V = mat_at(e->Vm(), b0);
+  zf.n = e->n;
   zf.counter = e->zf_cnt + b0;
+  if (defer) zf.vd = e->vdesc(b0, e->vnz);
   bool zfused = false;
   // the completion can ride on the rotation once s is installed (the fused
   // Jacobi writes it directly)
@@ -944,7 +1009,9 @@ static int issue_rank_one(isvd_engine* e, const Slice& sl, const int64_t* di, co
     ISVD_CUDA(cudaMemcpy2DAsync(e->s + (int64_t)b0 * e->ld, sizeof(double) * e->ld, sv,
                                 sizeof(double) * S, sizeof(double) * r, nb,
                                 cudaMemcpyDeviceToDevice, st));
-  if (!zfused) ISVD_TRY(launch_complete_zero(nb, r, zf.s, zf.lds, zf.U, zf.m, zf.V, zf.n, st));
+  if (!zfused)
+    ISVD_TRY(launch_complete_zero(nb, r, zf.s, zf.lds, zf.U, zf.m, zf.V, zf.n, st,
+                                  defer ? &zf.vd : nullptr));
   return ISVD_OK;
 }
 
@@ -1009,8 +1076,21 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
   if (!is_row) ISVD_TRY(e->flush());  // the column append projects on, and rotates, U
   // a pending right basis is folded by this row append when its projection
   // path can read through Gv, else materialised first
-  if (e->vpend && !project_append_takes_g(e->B, e->n, e->r)) ISVD_TRY(e->flush_v());
-  const bool vp = is_row && e->vpend;
+  // full-rank row appends of a deferral-capable batch keep V deferred (the
+  // residual joins Z); other appends fold a pending rank-1-only Gv into
+  // their V rotation when the projection path can, else materialise V first
+  static const bool vrow_env = !getenv("ISVD_NO_VROW");
+  const bool vrow = vrow_env && is_row && e->vdefer_ok() && keep == e->r &&
+                    project_append_takes_g(e->B, e->n, e->r);
+  if (e->vpend && !vrow && (e->vnz > 0 || !project_append_takes_g(e->B, e->n, e->r)))
+    ISVD_TRY(e->flush_v());
+  const bool vp = is_row && e->vpend && !vrow;
+  const bool vstart = vrow && !e->vpend;
+  if (vrow) ISVD_TRY(e->ensure_gv());
+  if (vstart) {
+    e->vfw = e->r;
+    e->vnz = 0;
+  }
   const int lazy_state = !(is_row && e->lazy_mode) ? 0 : (e->lazy_active ? 2 : 1);
   // window bookkeeping after this event (used by the completion check)
   e->r_base_next = lazy_state == 1 ? e->r : e->r_base;
@@ -1052,7 +1132,7 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
   const int rc_issue = run_groups(e, [&](const Slice& sl) {
     const double* xd = x;
     if (!on_device) xd = staged;
-    return issue_append(e, sl, xd, len, is_row, keep, lazy_state, vp);
+    return issue_append(e, sl, xd, len, is_row, keep, lazy_state, vp, vrow, vstart);
   });
   g_gate = nullptr;
   ISVD_TRY(rc_issue);
@@ -1066,6 +1146,10 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
     }
   }
   if (vp) e->vpend = false;
+  if (vrow) {
+    e->vpend = true;
+    e->vnz += 1;
+  }
   if (lazy_state == 1) {
     e->lazy_active = true;
     e->m_base = e->m;
@@ -1082,6 +1166,7 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
   }
   e->r = keep;
   if (e->lazy_active && e->lazy_b >= e->lazy_rows) ISVD_TRY(e->flush_u(true));
+  if (e->vpend && e->vnz >= kVWin) ISVD_TRY(e->flush_v(true));
   ISVD_TRY(e->guard_step());
   if (e->ngroups_active == 1) e->mark();
   if (e->timing) { e->timed_ticks += 1; e->tick_kind.push_back(0); }
@@ -1150,6 +1235,10 @@ int isvd_engine_rank_one(isvd_engine* e, const int64_t* i, const int64_t* j, con
   if (e->vpend && !e->vdefer_ok()) ISVD_TRY(e->flush_v());
   const bool defer = e->vdefer_ok(), vp = e->vpend;
   if (defer) ISVD_TRY(e->ensure_gv());
+  if (defer && !vp) {  // the core writes Vk straight into a fresh Gv
+    e->vfw = e->r;
+    e->vnz = 0;
+  }
   ISVD_TRY(run_groups(e, [&](const Slice& sl) {
     return issue_rank_one(e, sl, di, dj, dd, lazy_state, defer, vp);
   }));
@@ -1406,6 +1495,7 @@ int isvd_engine_restore(isvd_engine* e) {
   e->lazy_active = false;
   e->lazy_b = 0;
   e->vpend = false;
+  e->vnz = 0;
   ISVD_CUDA(cudaMemcpyAsync(e->U, S.U, S.nu * 8, cudaMemcpyDeviceToDevice, e->st));
   ISVD_CUDA(cudaMemcpyAsync(e->V, S.V, S.nv * 8, cudaMemcpyDeviceToDevice, e->st));
   ISVD_CUDA(cudaMemcpyAsync(e->A, S.A, S.na * 8, cudaMemcpyDeviceToDevice, e->st));

@@ -2,6 +2,7 @@
 #include <algorithm>
 #include <type_traits>
 #include <cooperative_groups.h>
+#include <cstdlib>
 #include "common.cuh"
 #include "core_svd.cuh"
 #include "tick.cuh"
@@ -31,14 +32,19 @@ __global__ void __launch_bounds__(256) project_append_kernel(
     int64_t core_stride, int ldcore, double* __restrict__ z, int64_t z_stride,
     double* __restrict__ inj_scale, double* __restrict__ rho_out, double* __restrict__ xnorm_out,
     double* __restrict__ A, int64_t a_stride, int64_t a_off, int64_t a_step,
-    double* __restrict__ N, int arrow_only, const double* __restrict__ G, int64_t g_stride,
-    int ldg, const int* __restrict__ gate) {
+    double* __restrict__ N, int arrow_only, VDefer vd, const int* __restrict__ gate) {
   if (gate && *gate) return;
   // sized by RT, not kRMax: with a 64 KB staged F the static arrays decide
   // whether 2 or 3 CTAs fit per SM
+  constexpr int PN = (RT == 1) ? kGMaxRows : RT * 32;
   __shared__ double part[8][RT * 32];
-  __shared__ double p[RT * 32];
-  __shared__ double pg[2][RT * 32];  // deferred basis: G^T p and G G^T p
+  __shared__ double p[PN];
+  __shared__ double pg[2][PN];  // deferred basis: G^T p and G G^T p
+  const double* __restrict__ G = vd.G;
+  // deferred basis: F holds fw columns, Z nz more (V_eff = [F | Z^T] G)
+  const int fw = G ? vd.fw : r;
+  const int nz = G ? vd.nz : 0;
+  const int gr = fw + nz;
   __shared__ double red[32];
   __shared__ __align__(8) uint64_t bar;
   extern __shared__ __align__(128) double Fs[];  // STAGE: [rows][F.ld], then x[rows]
@@ -66,15 +72,19 @@ __global__ void __launch_bounds__(256) project_append_kernel(
   }
   // deferred right basis (r <= 32): lane l of warp w holds G[w + 8i][l],
   // loaded while the bulk copy is in flight
-  double greg[4] = {0.0, 0.0, 0.0, 0.0};
-  if (RT == 1 && G) {
-    const double* Gb = G + b * g_stride;
+  constexpr int GI = (kGMaxRows + 7) / 8;
+  double greg[GI];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < GI; ++i) greg[i] = 0.0;
+  if (RT == 1 && G) {
+    const double* Gb = G + b * vd.g_stride;
+#pragma unroll
+    for (int i = 0; i < GI; ++i) {
       const int c = warp + 8 * i;
-      if (c < r && lane < r) greg[i] = Gb[c * ldg + lane];
+      if (c < gr && lane < r) greg[i] = Gb[c * vd.ldg + lane];
     }
   }
+  const double* Zb = (RT == 1 && G && nz > 0) ? vd.Z + b * vd.z_stride : nullptr;
   // x: norm, tracked-matrix write (and staging) overlap the bulk copy
   double xx = 0.0;
   for (int c = threadIdx.x; c < rows; c += blockDim.x) {
@@ -103,7 +113,7 @@ __global__ void __launch_bounds__(256) project_append_kernel(
 #pragma unroll
       for (int t = 0; t < RT; ++t) {
         const int l = lane + 32 * t;
-        if (l < r) {
+        if (l < fw) {
           acc[t] = fma(fr[l], xc, acc[t]);
           acc2[t] = fma(fd[l], xd, acc2[t]);
         }
@@ -115,7 +125,7 @@ __global__ void __launch_bounds__(256) project_append_kernel(
 #pragma unroll
       for (int t = 0; t < RT; ++t) {
         const int l = lane + 32 * t;
-        if (l < r) acc[t] = fma(fr[l], xc, acc[t]);
+        if (l < fw) acc[t] = fma(fr[l], xc, acc[t]);
       }
     }
 #pragma unroll
@@ -124,13 +134,23 @@ __global__ void __launch_bounds__(256) project_append_kernel(
 #pragma unroll
   for (int t = 0; t < RT; ++t) {
     int l = lane + 32 * t;
-    if (l < r) part[warp][l] = acc[t];
+    if (l < fw) part[warp][l] = acc[t];
   }
   __syncthreads();
-  for (int l = threadIdx.x; l < r; l += blockDim.x) {
+  for (int l = threadIdx.x; l < fw; l += blockDim.x) {
     double v = 0.0;
     for (int w = 0; w < nw; ++w) v += part[w][l];
     p[l] = v;
+  }
+  // appended residual columns: p[fw + t] = <Z[t], x> (one warp per column)
+  if (Zb) {
+    for (int t = warp; t < nz; t += nw) {
+      const double* zt = Zb + (int64_t)t * vd.ldz;
+      double v = 0.0;
+      for (int c = lane; c < rows; c += 32) v = fma(zt[c], STAGE ? xs[c] : xb[c], v);
+      v = warp_sum(v);
+      if (lane == 0) p[fw + t] = v;
+    }
   }
   double xnorm2 = block_sum(xx, red);  // contains __syncthreads, p visible after
   // Deferred right basis (F_eff = F G, G r x r): the core takes G^T (F^T x)
@@ -138,13 +158,13 @@ __global__ void __launch_bounds__(256) project_append_kernel(
   const double* pc = p;  // projection coefficients of the core
   const double* pz = p;  // coefficients multiplying F in z = x - F pz
   if (RT == 1 && G) {
-    // G^T p: per-warp partial over its 4 rows of G, then across the 8 warps
+    // G^T p: per-warp partial over its rows of G, then across the 8 warps
     // (part[] is free again: block_sum above synchronised after its reads)
     double v = 0.0;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < GI; ++i) {
       const int c = warp + 8 * i;
-      if (c < r) v = fma(greg[i], p[c], v);
+      if (c < gr) v = fma(greg[i], p[c], v);
     }
     part[warp][lane] = v;
     __syncthreads();
@@ -156,10 +176,10 @@ __global__ void __launch_bounds__(256) project_append_kernel(
     __syncthreads();
     // G (G^T p): one warp reduction per row of G
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < GI; ++i) {
       const int c = warp + 8 * i;
       const double t = warp_sum(greg[i] * pg[0][lane]);
-      if (lane == 0 && c < r) pg[1][c] = t;
+      if (lane == 0 && c < gr) pg[1][c] = t;
     }
     __syncthreads();
     pc = pg[0];
@@ -172,11 +192,13 @@ __global__ void __launch_bounds__(256) project_append_kernel(
     for (int c = threadIdx.x; c < rows; c += blockDim.x) {
       const double* fr = Fs + (size_t)c * F.ld;
       double v4[4] = {0.0, 0.0, 0.0, 0.0};  // four independent chains
-      int l = c % r;
-      for (int j = 0; j < r; ++j) {
+      int l = c % fw;
+      for (int j = 0; j < fw; ++j) {
         v4[j & 3] = fma(fr[l], pz[l], v4[j & 3]);
-        l = (l + 1 == r) ? 0 : l + 1;
+        l = (l + 1 == fw) ? 0 : l + 1;
       }
+      if (Zb)
+        for (int t = 0; t < nz; ++t) v4[t & 3] = fma(Zb[(int64_t)t * vd.ldz + c], pz[fw + t], v4[t & 3]);
       const double v = (v4[0] + v4[1]) + (v4[2] + v4[3]);
       const double zc = xs[c] - v;
       zb[c] = zc;
@@ -186,7 +208,8 @@ __global__ void __launch_bounds__(256) project_append_kernel(
     for (int c = warp; c < rows; c += nw) {
       const double* fr = Fb + (int64_t)c * F.ld;
       double v = 0.0;
-      for (int l = lane; l < r; l += 32) v = fma(fr[l], pz[l], v);
+      for (int l = lane; l < fw; l += 32) v = fma(fr[l], pz[l], v);
+      if (Zb && lane < nz) v = fma(Zb[(int64_t)lane * vd.ldz + c], pz[fw + lane], v);
       v = warp_sum(v);
       double zc = xb[c] - v;
       if (lane == 0) {
@@ -810,14 +833,45 @@ constexpr int kRegRowsPerBlock = 256;
 __device__ void complete_column(double* X, int64_t ld, int rows, int w, int t, double* coef,
                                 double* red);
 
-// complete_zero_kernel's per-stream work for CTA-sized thread blocks
+// V <- [V(:, :fw) | Z^T] G for stream b, G <- [I_w; 0] (so V_eff is
+// unchanged): one warp per row, lane q forms output column q from the old row
+// (broadcast loads), then the warp writes the row back (rare path)
+__device__ __noinline__ void vdefer_materialise(int b, int w, Mat V, int n, const VDefer& vd) {
+  double* Vb = V.p + b * V.stride;
+  double* Gb = const_cast<double*>(vd.G) + b * vd.g_stride;
+  const double* Zb = vd.nz ? vd.Z + b * vd.z_stride : nullptr;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int c = warp; c < n; c += nw) {
+    double* vr = Vb + (int64_t)c * V.ld;
+    double acc = 0.0;
+    if (lane < w) {
+      for (int l = 0; l < vd.fw; ++l) acc = fma(__ldcg(vr + l), __ldcg(Gb + l * vd.ldg + lane), acc);
+      for (int t = 0; t < vd.nz; ++t)
+        acc = fma(__ldcg(Zb + (int64_t)t * vd.ldz + c), __ldcg(Gb + (vd.fw + t) * vd.ldg + lane), acc);
+    }
+    __syncwarp();
+    if (lane < vd.fw || lane < w) vr[lane] = lane < w ? acc : 0.0;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < (vd.fw + vd.nz) * w; idx += blockDim.x) {
+    const int l = idx / w, q = idx % w;
+    Gb[l * vd.ldg + q] = (l == q) ? 1.0 : 0.0;
+  }
+  __threadfence();
+  __syncthreads();
+}
+
+// complete_zero_kernel's per-stream work for CTA-sized thread blocks; with a
+// deferred right basis (vd.G) V is materialised first (rare path)
 __device__ void complete_zero_stream(int b, int w, const double* __restrict__ s, int lds, Mat U,
-                                     int m, Mat V, int n, double* coef, double* red) {
+                                     int m, Mat V, int n, double* coef, double* red,
+                                     const VDefer& vd) {
   const double* sb = s + (int64_t)b * lds;
   // common case: no zero sigma -- one parallel scan instead of w serial loads
   bool any_zero = false;
   for (int t = threadIdx.x; t < w; t += blockDim.x) any_zero |= sb[t] == 0.0;
   if (!__syncthreads_or(any_zero)) return;
+  if (vd.G) vdefer_materialise(b, w, V, n, vd);
   for (int t = 0; t < w; ++t) {
     if (sb[t] != 0.0) continue;
     for (int side = 0; side < 2; ++side) {
@@ -835,7 +889,8 @@ __device__ void complete_zero_stream(int b, int w, const double* __restrict__ s,
   }
 }
 
-template <int KP>
+// ZS: the left operand has a second source (RotJob::zs, the deferred-V flush)
+template <int KP, bool ZS>
 __global__ void __launch_bounds__(kRegWarps * 32, 8)
     rotate_reg_kernel(int r, int keep, RotJob j0, RotJob j1, int nblk0, const int* __restrict__ gate,
                       ZeroFix zf) {
@@ -909,18 +964,34 @@ __global__ void __launch_bounds__(kRegWarps * 32, 8)
   const int ld = J.X.ld;
   if (J.new_row && blk == 0) {
     double* nr = X + (int64_t)J.rows * ld;
+    const double sc = J.nr_scale ? J.nr_scale[b] : 1.0;
     for (int c = threadIdx.x; c < ld; c += blockDim.x)
-      nr[c] = (has_last && c < keep) ? Q[r * J.ldq + c] : 0.0;
+      nr[c] = (has_last && c < keep) ? sc * Q[r * J.ldq + c] : 0.0;
   }
   const double zscale = J.z ? J.inj_scale[b] : 0.0;
   const double* zb = J.z ? J.z + b * J.z_stride : nullptr;
   const int row_begin = blk * kRegRowsPerBlock;
   const int row_end = min(J.rows, row_begin + kRegRowsPerBlock);
-  __syncthreads();
+  // zero-sigma completion needed?  s is final (the core kernel ran before),
+  // so every CTA of the stream decides alike; the common case skips the
+  // arrival fence and count entirely
+  bool zf_need = false;
+  if (zf.counter)
+    for (int t = threadIdx.x; t < zf.w; t += blockDim.x) zf_need |= zf.s[(int64_t)b * zf.lds + t] == 0.0;
+  zf_need = __syncthreads_or(zf_need);
   for (int row0 = row_begin + warp * 8; row0 < row_end; row0 += kRegWarps * 8) {
     const int row = row0 + g;
     double a[KQ];
-    if (row < row_end) {
+    if (ZS && row < row_end) {
+      // [X(:, :zfw) | Z^T] (deferred right basis flush)
+      const double* src = X + (int64_t)row * ld;
+      const double* zsb = J.zs + b * J.zs_stride + row;
+#pragma unroll
+      for (int kk = 0; kk < KQ; ++kk) {
+        const int k = q * KQ + kk;
+        a[kk] = k < J.zfw ? src[k] : (k < r ? zsb[(int64_t)(k - J.zfw) * J.ldzs] : 0.0);
+      }
+    } else if (row < row_end) {
       const double* src = X + (int64_t)row * ld + q * KQ;
 #pragma unroll
       for (int kk = 0; kk < KQ; kk += 2) {
@@ -953,7 +1024,7 @@ __global__ void __launch_bounds__(kRegWarps * 32, 8)
       }
     }
   }
-  if (zf.counter) {
+  if (zf_need) {
     // last CTA of this stream: every row of both sides is written (each
     // thread fenced its stores before the arrival count), so the zero-sigma
     // completion can run here instead of in its own launch
@@ -969,7 +1040,7 @@ __global__ void __launch_bounds__(kRegWarps * 32, 8)
     __syncthreads();
     if (last) {
       __threadfence();
-      complete_zero_stream(b, zf.w, zf.s, zf.lds, zf.U, zf.m, zf.V, zf.n, zcoef, zred);
+      complete_zero_stream(b, zf.w, zf.s, zf.lds, zf.U, zf.m, zf.V, zf.n, zcoef, zred, zf.vd);
     }
   }
 }
@@ -1034,13 +1105,13 @@ __device__ void complete_column(double* X, int64_t ld, int rows, int w, int t, d
 }
 
 __global__ void complete_zero_kernel(int w, const double* __restrict__ s, int lds, Mat U, int m,
-                                     Mat V, int n, const int* __restrict__ gate) {
+                                     Mat V, int n, const int* __restrict__ gate, VDefer vd) {
   griddep_launch_dependents();
   griddep_wait();
   if (gate && *gate) return;
   extern __shared__ double coef[];  // [w]
   __shared__ double red[32];
-  complete_zero_stream(blockIdx.x, w, s, lds, U, m, V, n, coef, red);
+  complete_zero_stream(blockIdx.x, w, s, lds, U, m, V, n, coef, red, vd);
 }
 
 // ------------------------------------------------------------------- K5
@@ -1196,8 +1267,8 @@ int launch_project_append(int batch, int rows, int r, Mat F, const double* x, in
                           int ldcore, double* z, int64_t z_stride, double* inj_scale,
                           double* rho_out, double* xnorm_out, double* A, int64_t a_stride,
                           int64_t a_off, int64_t a_step, double* N, cudaStream_t st,
-                          const Allreducer* ar, int arrow_only, const double* G,
-                          int64_t g_stride, int ldg) {
+                          const Allreducer* ar, int arrow_only, const VDefer* vd) {
+  const double* G = vd ? vd->G : nullptr;
   if (r > kRMax) {
     set_error("factor width exceeds kernel limit");
     return ISVD_EINVAL;
@@ -1323,7 +1394,7 @@ int launch_project_append(int batch, int rows, int r, Mat F, const double* x, in
     }
     project_append_kernel<SG, RT><<<batch, 256, SG ? stage : 0, st>>>(
         rows, r, F, x, x_stride, s, lds, tol, core, core_stride, ldcore, z, z_stride, inj_scale,
-        rho_out, xnorm_out, A, a_stride, a_off, a_step, N, arrow_only, G, g_stride, ldg, g_gate);
+        rho_out, xnorm_out, A, a_stride, a_off, a_step, N, arrow_only, vd ? *vd : VDefer{}, g_gate);
     return ISVD_OK;
   };
   using T1 = std::integral_constant<bool, true>;
@@ -1396,8 +1467,8 @@ static int rotate_dispatch(int batch, int r, int keep, const RotJob& j0, const R
     if (j1->new_row && nb1 == 0) nb1 = 1;
   }
   if (nb0 + nb1 == 0) return ISVD_OK;
-  if constexpr (KP <= 32) {
-    if (NP <= 32) {
+  if constexpr (KP <= kGMaxRows) {
+    if (NP <= 32 && (KP <= 32 || j0.zs)) {
       int rb0 = ceil_div(j0.rows, kRegRowsPerBlock);
       if (j0.new_row && rb0 == 0) rb0 = 1;
       int rb1 = 0;
@@ -1405,9 +1476,14 @@ static int rotate_dispatch(int batch, int r, int keep, const RotJob& j0, const R
         rb1 = ceil_div(j1->rows, kRegRowsPerBlock);
         if (j1->new_row && rb1 == 0) rb1 = 1;
       }
-      const bool fz = zf && zf->w <= 32;
-      rotate_reg_kernel<KP><<<dim3(rb0 + rb1, batch), kRegWarps * 32, 0, st>>>(
-          r, keep, j0, j1 ? *j1 : j0, rb0, g_gate, fz ? *zf : ZeroFix{});
+      static const bool no_fuse = getenv("ISVD_NO_ZFUSE") != nullptr;
+      const bool fz = zf && zf->w <= 32 && !no_fuse;
+      if (j0.zs)
+        rotate_reg_kernel<KP, true><<<dim3(rb0 + rb1, batch), kRegWarps * 32, 0, st>>>(
+            r, keep, j0, j1 ? *j1 : j0, rb0, g_gate, fz ? *zf : ZeroFix{});
+      else
+        rotate_reg_kernel<KP, false><<<dim3(rb0 + rb1, batch), kRegWarps * 32, 0, st>>>(
+            r, keep, j0, j1 ? *j1 : j0, rb0, g_gate, fz ? *zf : ZeroFix{});
       if (fused) *fused = fz;
       ISVD_LAUNCHED();
       return ISVD_OK;
@@ -1465,7 +1541,7 @@ int launch_rotate(int batch, int r, int keep, const RotJob& j0, const RotJob* j1
 }
 
 int launch_complete_zero(int batch, int w, const double* s, int lds, Mat U, int m, Mat V, int n,
-                         cudaStream_t st) {
+                         cudaStream_t st, const VDefer* vd) {
   if (batch == 0 || w == 0) return ISVD_OK;
   size_t smem = sizeof(double) * w;
   if (smem > 48 * 1024) {
@@ -1473,7 +1549,7 @@ int launch_complete_zero(int batch, int w, const double* s, int lds, Mat U, int 
     return ISVD_EINVAL;
   }
   ISVD_CUDA(launch_ex(batch <= 32, 1, complete_zero_kernel, dim3(batch), dim3(256), smem, st, w, s,
-                      lds, U, m, V, n, g_gate));
+                      lds, U, m, V, n, g_gate, vd ? *vd : VDefer{}));
   ISVD_LAUNCHED();
   return ISVD_OK;
 }
@@ -1535,6 +1611,21 @@ int launch_canonicalize(int batch, int w, Mat U, int m, Mat V, int n, cudaStream
     return ISVD_OK;
   }
   canonicalize_kernel<<<batch, 256, 0, st>>>(w, U, m, V, n);
+  ISVD_LAUNCHED();
+  return ISVD_OK;
+}
+
+__global__ void eye_kernel(Mat X, int rows, int cols) {
+  double* xb = X.p + blockIdx.x * X.stride;
+  for (int idx = threadIdx.x; idx < rows * cols; idx += blockDim.x) {
+    const int i = idx / cols, j = idx % cols;
+    xb[(int64_t)i * X.ld + j] = (i == j) ? 1.0 : 0.0;
+  }
+}
+
+int launch_eye(int batch, Mat X, int rows, int cols, cudaStream_t st) {
+  if (batch == 0 || rows == 0 || cols == 0) return ISVD_OK;
+  eye_kernel<<<batch, 256, 0, st>>>(X, rows, cols);
   ISVD_LAUNCHED();
   return ISVD_OK;
 }

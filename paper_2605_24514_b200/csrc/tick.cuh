@@ -17,13 +17,32 @@ struct Mat {
 // F[b] (rows x r, row-major pitch F.ld) is the factor whose row space the
 // appended vector x[b] (length rows) is projected on: V for a row append,
 // U for a column append (engine.py:137-139 transpose trick).
+// Deferred right basis (engine.cu): V_eff = [F(:, :fw) | Z^T] G with G
+// (gr = fw + nz rows, r columns, leading dimension ldg, g_stride per stream)
+// and Z holding nz appended residuals (Z[t * ldz + c], z_stride per stream).
+// nz = 0 and fw = r is the rank-1-only deferral V_eff = V G.
+constexpr int kVWin = 8;             // residual columns per deferred window
+constexpr int kGMaxRows = 32 + kVWin;  // rows of G the k <= 32 kernels handle
+struct VDefer {
+  const double* G = nullptr;
+  int64_t g_stride = 0;
+  int ldg = 0;
+  int fw = 0, nz = 0;
+  const double* Z = nullptr;
+  int64_t z_stride = 0;
+  int ldz = 0;
+};
+
+// K1.  With vd.G set, the projection goes through the deferred basis and z
+// (the unnormalised residual) is written to z (the next Z slot when nz is
+// being appended).
 int launch_project_append(int batch, int rows, int r, Mat F, const double* x, int64_t x_stride,
                           const double* s, int lds, double tol, double* core, int64_t core_stride,
                           int ldcore, double* z, int64_t z_stride, double* inj_scale,
                           double* rho_out, double* xnorm_out, double* A, int64_t a_stride,
                           int64_t a_off, int64_t a_step, double* N, cudaStream_t st,
                           const struct Allreducer* ar = nullptr, int arrow_only = 0,
-                          const double* G = nullptr, int64_t g_stride = 0, int ldg = 0);
+                          const VDefer* vd = nullptr);
 // Whether launch_project_append accepts a deferred right basis G (F_eff =
 // F G) for this shape (the one-CTA-per-stream path does; the split and
 // cluster paths for few long streams do not).
@@ -72,6 +91,15 @@ struct RotJob {
   const double* G = nullptr;
   int64_t g_stride = 0;
   int ldg = 0;
+  // new_row: the appended row is nr_scale[b] * Q[r, :] (1 when null)
+  const double* nr_scale = nullptr;
+  // optional second source of the left operand (rotate_reg_kernel): columns
+  // k >= zfw of X are read from zs[(k - zfw) * ldzs + row] (the deferred
+  // residuals Z of a VDefer, materialised by V <- [V | Z^T] G)
+  const double* zs = nullptr;
+  int64_t zs_stride = 0;
+  int ldzs = 0;
+  int zfw = 0;
 };
 
 // K3/K4: both factor rotations of a tick in one launch (FP64 DMMA).
@@ -87,6 +115,9 @@ struct ZeroFix {
   Mat V{};
   int n = 0;
   unsigned* counter = nullptr;
+  // V deferred (vd.G set): V is V_base; a stream that needs a completion
+  // first materialises V_eff into V and resets its G to [I; 0]
+  VDefer vd{};
 };
 // zf (optional): fuse the completion when the launch goes to
 // rotate_reg_kernel; *fused tells the caller whether it did (else the caller
@@ -97,7 +128,7 @@ int launch_rotate(int batch, int r, int keep, const RotJob& j0, const RotJob* j1
 // engine.py:59-70 -- repair factor columns paired with exact-zero singular
 // values (no-op launch when none are zero).
 int launch_complete_zero(int batch, int w, const double* s, int lds, Mat U, int m, Mat V, int n,
-                         cudaStream_t st);
+                         cudaStream_t st, const VDefer* vd = nullptr);
 
 // linalg.py:63-75 -- sign canonicalisation of (U, V) per stream.
 int launch_canonicalize(int batch, int w, Mat U, int m, Mat V, int n, cudaStream_t st);
@@ -110,6 +141,8 @@ int launch_canon_shard_apply(int w, Mat U, int m, Mat V, int n, int world, const
                              cudaStream_t st);
 
 // Copy helpers.
+// X[:rows, :cols] <- I per stream
+int launch_eye(int batch, Mat X, int rows, int cols, cudaStream_t st);
 int launch_copy_rows(int batch, int rows, int cols, const double* src, int64_t src_stride,
                      int ld_src, double* dst, int64_t dst_stride, int ld_dst, cudaStream_t st);
 int launch_zero(double* p, size_t n, cudaStream_t st);

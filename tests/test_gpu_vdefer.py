@@ -167,3 +167,44 @@ def test_vdefer_risk_reads_materialised_basis():
         e.rank_one_update(2, 11, -0.2)
     r_on, r_off = risk(on, 80, [equal_weights(20)]), risk(off, 80, [equal_weights(20)])
     np.testing.assert_allclose(r_on.cov, r_off.cov, atol=1e-12)
+
+
+@pytest.mark.parametrize("lazy_u", [True, False])
+def test_deferred_rows_with_exact_zero_sigma(lazy_u):
+    """Full-rank row appends keep V deferred (V_eff = [V | Z^T] G); when a
+    tick leaves an exact zero singular value the completion first
+    materialises that stream's V (tick.cu vdefer_materialise).  A rank-3
+    start with k = 5 and in-span rows keeps sigma_4 = sigma_5 = 0 on every
+    tick: the result must match the eager engine's live subspace and stay
+    orthonormal through several deferral windows."""
+    rng = np.random.default_rng(11)
+    B, m0, n0, k = 64, 40, 30, 5
+    a0 = rng.standard_normal((B, m0, 3)) @ rng.standard_normal((B, 3, n0))
+    dfr, eag = BatchedSvdEngine(a0, k), BatchedSvdEngine(a0, k)
+    dfr.set_vdefer(2)
+    eag.set_vdefer(0)
+    for e in (dfr, eag):
+        e.set_lazy(lazy_u)
+    basis = np.stack([eag.factors(b).vt[:3] for b in range(B)])
+    cpu = OracleEngine(a0[9], k)
+    for t in range(20):
+        xs = np.einsum("bi,bij->bj", rng.standard_normal((B, 3)), basis)
+        for e in (dfr, eag):
+            e.row_append(xs)
+        cpu.row_append(xs[9])
+        if t % 7 == 6:
+            ii = rng.integers(0, m0, B)
+            jj = rng.integers(0, n0, B)
+            for e in (dfr, eag):
+                e.rank_one_update(ii, jj, np.zeros(B))
+            cpu.rank_one_update(int(ii[9]), int(jj[9]), 0.0)
+    for b in (0, 9, 63):
+        fd, fe = dfr.factors(b), eag.factors(b)
+        assert fd.s[3] == 0.0 and fd.s[4] == 0.0
+        assert rel_err(fd.s[:3], fe.s[:3]) < 1e-11
+        assert sine_angle(fd.vt[:3].T, fe.vt[:3].T) < 1e-9
+        assert np.max(np.abs(fd.vt @ fd.vt.T - np.eye(k))) < 1e-10
+        assert np.max(np.abs(fd.u.T @ fd.u - np.eye(k))) < 1e-10
+    fc = cpu.factors
+    assert rel_err(dfr.factors(9).s[:3], fc.s[:3]) < SIGMA_RTOL
+    assert sine_angle(dfr.factors(9).vt[:3].T, fc.vt[:3].T) < ANGLE_TOL
