@@ -266,22 +266,32 @@ def tick_bytes(B, m, n, w, row_tick):
     return 8 * B * (2 * m * w + 2 * n * w + 2 * w + 2)
 
 
-def _simulate_bytes(B, steps, window=32, vdefer=True):
-    """Algorithmic bytes of the per-tick kernels over `steps` ticks (simulating
-    the engine's deferred-U window: W = (32 + b) x 32 rotated in place,
-    flushed every `window` appended rows; and the deferred right basis: a
-    rank-1 tick writes its K x K right rotation G instead of rotating V, the
-    next row append reads G in its projection and folds it into its V pass)."""
-    proj_bytes = rot_bytes = all_bytes = 0.0
-    m, b_rows, active, vpend = M0, 0, False, False
+def _simulate_bytes(B, steps, window=32, vwin=8):
+    """Algorithmic bytes of the per-tick kernels over `steps` ticks, following
+    the engine's data flow: the deferred left basis (W =
+    (32 + b) x 32 rotated in place, flushed every `window` appended rows) and
+    the deferred right basis V_eff = [V | Z^T] G (a rank-1 tick rotates G; a
+    full-rank row tick projects through V, Z and G, writes its residual as the
+    next Z column and grows G by a row; V is materialised every `vwin` row
+    appends).  Returns (projection bytes, rotation bytes, V-materialisation
+    bytes, SURVEY 8(d) reference-algorithm bytes)."""
+    proj_bytes = rot_bytes = vflush_bytes = all_bytes = 0.0
+    m, b_rows, active = M0, 0, False
+    vpend, nz = False, 0
     for t in range(steps):
         row = t % 2 == 0
         all_bytes += tick_bytes(B, m, N0, K, row)
+        g = (K + nz) * K if vpend else 0                      # rows of G x K
         if row:
-            g = K * K if vpend else 0                         # G read (projection, rotation)
-            proj_bytes += 8.0 * B * (N0 * K + 2 * N0 + N0 + g)  # V read, x read, A row, z write
-            vb = N0 * K + N0 * K + N0 + g                     # V read/write + z read
-            vpend = False
+            # V and Z read once, x read, A row + residual written, G read
+            proj_bytes += 8.0 * B * (N0 * K + nz * N0 + N0 + 2 * N0 + g)
+            vb = g + (K + nz + 1) * K                         # G read, grown G written
+            if not vpend:
+                vpend, nz = True, 0
+            nz += 1
+            if nz >= vwin:                                    # V <- [V | Z^T] G
+                vflush_bytes += 8.0 * B * (N0 * K + nz * N0 + (K + nz) * K + N0 * K)
+                vpend, nz = False, 0
             if not active:
                 wb = (K + 1) * K                              # W = Uk copy
                 active, b_rows = True, 1
@@ -292,19 +302,16 @@ def _simulate_bytes(B, steps, window=32, vdefer=True):
             if b_rows >= window:
                 active, b_rows = False, 0
         else:
-            proj_bytes += 8.0 * B * (2 * K + 2)               # U/V row gathers (+ W row)
-            if not vdefer:
-                vb = 2 * N0 * K
-            else:                                             # G <- G Vk, or Vk written as G
-                vb = 2 * K * K if vpend else 0
-                vpend = True
+            proj_bytes += 8.0 * B * (2 * K + 2 + nz)          # U/V row gathers (+ Z entries)
+            vb = 2 * g if vpend else K * K                    # G <- G Vk, or Vk written as G
+            vpend = True
             if not active:
                 wb = K * K
                 active, b_rows = True, 0
             else:
                 wb = 2 * (K + b_rows) * K
         rot_bytes += 8.0 * B * (vb + wb)
-    return proj_bytes, rot_bytes, all_bytes
+    return proj_bytes, rot_bytes, vflush_bytes, all_bytes
 
 
 def make_inputs_5b(torch, dev, seed=0, m=M5B, row0=0, rows=None):
@@ -571,8 +578,8 @@ def run_gpu(args):
                for j, name in enumerate(("project", "core_svd", "rotate", "install"))}
         for i, kind in enumerate(("row_append", "rank_one"))}
     window = int(lib.isvd_engine_lazy_window(eng._h.h))
-    proj_bytes, rot_bytes, _ = _simulate_bytes(B, diag_steps, window)
-    _, _, all_bytes = _simulate_bytes(B, steps, window)
+    proj_bytes, rot_bytes, vflush_bytes, _ = _simulate_bytes(B, diag_steps, window)
+    all_bytes = _simulate_bytes(B, steps, window)[3]
     # ---------------- end-to-end through the public API with host buffers
     e2e_steps = min(steps, args.e2e_steps)
     nrow = (e2e_steps + 1) // 2
@@ -608,9 +615,10 @@ def run_gpu(args):
             "project_append/rank1_build (K1/K6)": {"ms": tot(0), "bytes": proj_bytes},
             "arrow_svd (K2a, append cores)": {"ms": float(ph[1]), "bytes": None},
             "jacobi32 (K2b, rank-1 cores)": {"ms": float(ph[5]), "bytes": None},
-            "rotate V + W (K3/K4, per tick)": {"ms": tot(2), "bytes": rot_bytes},
+            "rotate W + G (K3/K4, per tick)": {"ms": tot(2), "bytes": rot_bytes},
             "rotate U flush (K3, deferred)": {"ms": flush_ms, "bytes": flush_bytes},
-            "install (s copy, zero-sigma check)": {"ms": max(0.0, tot(3) - flush_ms), "bytes": None},
+            "install (V materialisation, zero-sigma check)": {"ms": max(0.0, tot(3) - flush_ms),
+                                                              "bytes": vflush_bytes or None},
         }
         busy = sum(v["ms"] for v in kernels.values())
         for v in kernels.values():
@@ -624,9 +632,14 @@ def run_gpu(args):
         achieved = hk["gbs"]
         summ, summ_file = _ncu_summary()
         traffic = None
-        if "rot5a" in summ and "dram_bytes" in summ["rot5a"]:
-            # the capture is one stream-group launch (B / 4 streams)
-            traffic = summ["rot5a"]["dram_bytes"] * 4.0 * B / TOTAL_STREAMS
+        ncu_key = {"project_append/rank1_build (K1/K6)": "proj5a",
+                   "rotate W + G (K3/K4, per tick)": "rot5a"}.get(hbm_name)
+        if ncu_key in summ and "dram_bytes" in summ[ncu_key]:
+            # the capture is one stream-group launch (B / 4 streams) of a row
+            # tick; per tick on average over both event kinds for K1
+            traffic = summ[ncu_key]["dram_bytes"] * 4.0 * B / TOTAL_STREAMS
+            if ncu_key == "proj5a":
+                traffic *= 0.5
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
             "warmup": warm, "ms_per_step": t_max / steps, "higher_is_better": True,
@@ -645,9 +658,9 @@ def run_gpu(args):
             "roofline": {"kernel": hbm_name, "bound": "hbm", "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "peak_kind": peak_kind,
                          "traffic": traffic,
-                         "traffic_source": (f"profiles/{summ_file}: rot5a dram__bytes_read+write "
-                                            "of one stream-group launch x 4 groups (ncu, "
-                                            "cold-cache); V partly L2-resident after K1")
+                         "traffic_source": (f"profiles/{summ_file}: {ncu_key} dram__bytes_read"
+                                            "+write of one stream-group launch x 4 groups "
+                                            "(ncu, cold-cache), per tick")
                          if traffic else None,
                          "bytes_per_launch": hk["bytes"] / max(1, (n_flush if "flush" in hbm_name
                                                                    else diag_steps)),
