@@ -392,7 +392,13 @@ __global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32c_kernel(
       double* e = rc.A + b * rc.a_stride + i * rc.lda + j;
       const double old = *e;
       *e = old + d;
-      rc.N[b] += 2.0 * d * old + d * d;
+      const double nn = rc.N[b] + (2.0 * d * old + d * d);
+      rc.N[b] = nn;
+      if (rc.ring) {
+        rc.ring[b] = nn;
+        rc.ring[rc.ring_stride + b] = rc.rho[b];
+        rc.ring[2 * rc.ring_stride + b] = rc.xnorm[b];
+      }
     }
   } else {
     const double* K = core + b * core_stride;

@@ -41,6 +41,12 @@ struct Rank1Core {
   LazyBasis lz{};
   // Deferred right basis (tick.cuh VDefer): V_eff = [V | Z^T] G when vd.G
   VDefer vd{};
+  // optional read-back ring row of this tick: (N, rho, xnorm) at b,
+  // ring_stride + b, 2 ring_stride + b (rho / xnorm unchanged by the tick)
+  double* ring = nullptr;
+  int64_t ring_stride = 0;
+  const double* rho = nullptr;
+  const double* xnorm = nullptr;
   // Optional separate destination for the core's right vectors (row-major,
   // vk_stride per stream, leading dimension ldvk) instead of vk/ldo
   double* vk_out = nullptr;

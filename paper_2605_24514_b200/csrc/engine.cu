@@ -150,7 +150,11 @@ struct isvd_engine {
     if (cp_st) return ISVD_OK;
     ISVD_CUDA(cudaHostAlloc((void**)&vflag_h, kStageSlots * sizeof(int), cudaHostAllocDefault));
     for (int i = 0; i < kStageSlots; ++i) vflag_h[i] = 0;
-    ISVD_CUDA(cudaStreamCreateWithFlags(&cp_st, cudaStreamNonBlocking));
+    // highest priority: the payload check gates the tick kernels queued
+    // behind it, so its CTAs go ahead of the running ticks'
+    int lo = 0, hi = 0;
+    ISVD_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    ISVD_CUDA(cudaStreamCreateWithPriority(&cp_st, cudaStreamNonBlocking, hi));
     ISVD_CUDA(cudaEventCreateWithFlags(&stage_ready, cudaEventDisableTiming));
     return ISVD_OK;
   }
@@ -284,10 +288,24 @@ struct isvd_engine {
   bool async_groups = true, pend = false;
   int pend_G = 0;
   void join() {
+    ring_last = -1;  // conservatively: the next read-back takes the general path
     if (!pend) return;
     for (int g = 0; g < pend_G; ++g) cudaStreamWaitEvent(st, join_ev[g], 0);
     pend = false;
   }
+  // Read-back ring: the tick kernels that update (N, rho, xnorm) also write
+  // them to ring slot tick % kRing, so isvd_engine_scalars_async copies that
+  // slot on its own stream after the groups' tick instead of putting a copy
+  // between two ticks of every group stream.
+  static constexpr int kRing = 8;
+  double* sring = nullptr;
+  int64_t ring_cnt = 0;
+  int ring_slot = 0, ring_last = -1;
+  cudaStream_t rd_st = nullptr;
+  cudaEvent_t rd_done[kRing] = {};
+  bool rd_used[kRing] = {};
+  Ticket rd_tk;  // the groups' point a ring copy waits for
+  double* ring_row(int slot, int b0) const { return sring + (int64_t)slot * 3 * B + b0; }
   // record: the point every group stream (or st) has reached now
   int ticket_record(Ticket& t) {
     const int n = pend ? pend_G : 1;
@@ -298,6 +316,16 @@ struct isvd_engine {
     }
     for (int g = 0; g < n; ++g) ISVD_CUDA(cudaEventRecord(t.ev[g], pend ? gst[g] : st));
     t.n = n;
+    return ISVD_OK;
+  }
+  int ticket_record_on(Ticket& t, cudaStream_t s2) {
+    if (t.ev.empty()) {
+      cudaEvent_t ev;
+      ISVD_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      t.ev.push_back(ev);
+    }
+    ISVD_CUDA(cudaEventRecord(t.ev[0], s2));
+    t.n = 1;
     return ISVD_OK;
   }
   int ticket_wait(cudaStream_t s2, const Ticket& t) {
@@ -605,6 +633,11 @@ struct isvd_engine {
     for (auto& t : stage_tk)
       for (auto ev : t.ev) cudaEventDestroy(ev);
     if (stage_ready) cudaEventDestroy(stage_ready);
+    for (auto ev : rd_done)
+      if (ev) cudaEventDestroy(ev);
+    for (auto ev : rd_tk.ev) cudaEventDestroy(ev);
+    if (rd_st) cudaStreamDestroy(rd_st);
+    dfree(sring);
     if (cp_st) cudaStreamDestroy(cp_st);
     if (vflag_h) cudaFreeHost((void*)vflag_h);
     if (own_stream && st) cudaStreamDestroy(st);
@@ -669,6 +702,7 @@ int isvd_engine_create(isvd_engine** out, int batch, int m, int n, int k, double
   A(dalloc(&e->ed, (size_t)isvd_engine::kStageSlots * batch));
   A(dalloc(&e->dflag, 1 + isvd_engine::kStageSlots));
   A(dalloc(&e->W, (size_t)batch * e->wstride()));
+  A(dalloc(&e->sring, (size_t)isvd_engine::kRing * 3 * batch));
   if (rc == ISVD_OK) {
     if (cudaMalloc((void**)&e->zf_cnt, sizeof(unsigned) * batch) != cudaSuccess ||
         cudaMemset(e->zf_cnt, 0, sizeof(unsigned) * batch) != cudaSuccess) {
@@ -820,6 +854,8 @@ static int issue_append(isvd_engine* e, const Slice& sl, const double* xd, int l
   // sharded: only the owner stores an appended row; a column append projects
   // on the row-sharded U (sums across shards)
   double* Adst = (is_row && !e->owner) ? nullptr : e->A + b0 * e->astride();
+  // the read-back ring slot this tick writes must have been copied out
+  if (e->rd_used[e->ring_slot]) ISVD_CUDA(cudaStreamWaitEvent(st, e->rd_done[e->ring_slot], 0));
   if (vstart) ISVD_TRY(launch_eye(nb, mat_at(e->Gm(), b0), r, r, st));
   VDefer vd = e->vdesc(b0, vrow ? e->vnz : 0);
   double* zdst = z;
@@ -833,7 +869,8 @@ static int issue_append(isvd_engine* e, const Slice& sl, const double* xd, int l
                                  zdst_stride, inj, e->rho + b0, e->xnorm + b0, Adst, e->astride(),
                                  a_off, a_step, e->N + b0, st,
                                  (e->sharded && !is_row) ? &e->ar : nullptr,
-                                 e->append_jacobi ? 0 : 1, (vp || vrow) ? &vd : nullptr));
+                                 e->append_jacobi ? 0 : 1, (vp || vrow) ? &vd : nullptr,
+                                 e->ring_row(e->ring_slot, b0), e->B));
   if (one) e->mark();
   if (e->append_jacobi)
     ISVD_TRY(launch_core_svd(nb, r + 1, core, cs, S, uk, vk, cs, S, sv, S,
@@ -920,6 +957,7 @@ static int issue_rank_one(isvd_engine* e, const Slice& sl, const int64_t* di, co
   LazyBasis lz = e->lazy();
   lz.W = mat_at(lz.W, b0);
   const bool fused = !e->sharded && r <= 32;
+  if (e->rd_used[e->ring_slot]) ISVD_CUDA(cudaStreamWaitEvent(st, e->rd_done[e->ring_slot], 0));
   if (one) e->mark();
   if (fused) {
     // K6 + K2b in one kernel: the core is built in registers (no HBM round trip)
@@ -936,6 +974,10 @@ static int issue_rank_one(isvd_engine* e, const Slice& sl, const int64_t* di, co
     rc.lda = e->n_cap;
     rc.N = e->N + b0;
     rc.lz = lz;
+    rc.ring = e->ring_row(e->ring_slot, b0);
+    rc.ring_stride = e->B;
+    rc.rho = e->rho + b0;
+    rc.xnorm = e->xnorm + b0;
     if (vp) {
       rc.vd = e->vdesc(b0, e->vnz);
     } else if (defer) {
@@ -1068,6 +1110,7 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
   // keep = min(r+1, k, m+1, n) (row) | min(r+1, k, m, n+1) (col): engine.py:122,136
   const int keep = is_row ? std::min(std::min(e->r + 1, e->k), std::min(e->gm() + 1, e->n))
                           : std::min(std::min(e->r + 1, e->k), std::min(e->gm(), e->n + 1));
+  const int r_before = e->r;
   if (is_row) {
     if (e->owner) ISVD_TRY(e->grow_rows(e->m + 1));  // appended rows live on the owner
   } else {
@@ -1079,8 +1122,7 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
   // full-rank row appends of a deferral-capable batch keep V deferred (the
   // residual joins Z); other appends fold a pending rank-1-only Gv into
   // their V rotation when the projection path can, else materialise V first
-  static const bool vrow_env = !getenv("ISVD_NO_VROW");
-  const bool vrow = vrow_env && is_row && e->vdefer_ok() && keep == e->r &&
+  const bool vrow = is_row && e->vdefer_ok() && keep == e->r &&
                     project_append_takes_g(e->B, e->n, e->r);
   if (e->vpend && !vrow && (e->vnz > 0 || !project_append_takes_g(e->B, e->n, e->r)))
     ISVD_TRY(e->flush_v());
@@ -1125,6 +1167,7 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
     }
     ISVD_CUDA(cudaStreamWaitEvent(e->st, e->stage_ready, 0));
   }
+  e->ring_slot = (int)(e->ring_cnt % isvd_engine::kRing);
   // Gated tick: the kernels are queued before the verdict is known and skip
   // themselves on the device if the payload was rejected, so the host's wait
   // for the upload overlaps their launch instead of preceding it.
@@ -1170,6 +1213,10 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
   ISVD_TRY(e->guard_step());
   if (e->ngroups_active == 1) e->mark();
   if (e->timing) { e->timed_ticks += 1; e->tick_kind.push_back(0); }
+  // K1's main path wrote this tick's (N, rho, xnorm) into the ring slot
+  e->rd_used[e->ring_slot] = false;
+  e->ring_last = (!e->sharded && project_append_gateable(e->B, len, r_before)) ? e->ring_slot : -1;
+  e->ring_cnt += 1;
   e->canonical = false;
   e->step += 1;
   return ISVD_OK;
@@ -1239,6 +1286,7 @@ int isvd_engine_rank_one(isvd_engine* e, const int64_t* i, const int64_t* j, con
     e->vfw = e->r;
     e->vnz = 0;
   }
+  e->ring_slot = (int)(e->ring_cnt % isvd_engine::kRing);
   ISVD_TRY(run_groups(e, [&](const Slice& sl) {
     return issue_rank_one(e, sl, di, dj, dd, lazy_state, defer, vp);
   }));
@@ -1253,6 +1301,10 @@ int isvd_engine_rank_one(isvd_engine* e, const int64_t* i, const int64_t* j, con
   ISVD_TRY(e->guard_step());
   if (e->ngroups_active == 1) e->mark();
   if (e->timing) { e->timed_ticks += 1; e->tick_kind.push_back(1); }
+  // the fused rank-1 kernel wrote this tick's (N, rho, xnorm) into the ring
+  e->rd_used[e->ring_slot] = false;
+  e->ring_last = (!e->sharded && e->r <= 32) ? e->ring_slot : -1;
+  e->ring_cnt += 1;
   e->canonical = false;
   e->step += 1;
   return ISVD_OK;
@@ -1377,11 +1429,41 @@ int isvd_engine_get_scalars(isvd_engine* e, double* sq_norm, double* last_residu
 
 int isvd_engine_scalars_async(isvd_engine* e, double* host, int slot) {
   if (!e || !host || slot < 0 || slot >= 8) { set_error("bad argument"); return ISVD_EINVAL; }
+  if (e->ring_last >= 0) {
+    // the last tick's kernels left (N, rho, xnorm) in a ring slot: copy it on
+    // the read-back stream once every group has finished that tick
+    if (!e->rd_st) {
+      ISVD_CUDA(cudaStreamCreateWithFlags(&e->rd_st, cudaStreamNonBlocking));
+      for (auto& ev : e->rd_done) ISVD_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
+    ISVD_TRY(e->ticket_record(e->rd_tk));
+    ISVD_TRY(e->ticket_wait(e->rd_st, e->rd_tk));
+    ISVD_CUDA(cudaMemcpyAsync(host, e->ring_row(e->ring_last, 0), sizeof(double) * 3 * e->B,
+                              cudaMemcpyDeviceToHost, e->rd_st));
+    ISVD_CUDA(cudaEventRecord(e->rd_done[e->ring_last], e->rd_st));
+    e->rd_used[e->ring_last] = true;
+    return e->ticket_record_on(e->sc_tk[slot], e->rd_st);
+  }
+  // Pinned (device-mapped) destinations are written by one small kernel per
+  // group straight over PCIe: three DMA copies per group would each hold the
+  // group stream for their latency between two ticks.  Others: DMA copies.
+  double* mapped = nullptr;
+  {
+    cudaPointerAttributes pa;
+    if (cudaPointerGetAttributes(&pa, host) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+        pa.devicePointer)
+      mapped = static_cast<double*>(pa.devicePointer);
+    cudaGetLastError();
+  }
   // per group on the group streams while they run ahead (no join), else on st
   const int G = e->pend ? e->pend_G : 1;
   for (int g = 0; g < G; ++g) {
     const int b0 = (int)((int64_t)e->B * g / G), b1 = (int)((int64_t)e->B * (g + 1) / G);
     cudaStream_t s2 = e->pend ? e->gst[g] : e->st;
+    if (mapped) {
+      ISVD_TRY(launch_scalars_out(b0, b1 - b0, e->B, e->N, e->rho, e->xnorm, mapped, s2));
+      continue;
+    }
     const size_t nb = sizeof(double) * (b1 - b0);
     ISVD_CUDA(cudaMemcpyAsync(host + b0, e->N + b0, nb, cudaMemcpyDeviceToHost, s2));
     ISVD_CUDA(cudaMemcpyAsync(host + e->B + b0, e->rho + b0, nb, cudaMemcpyDeviceToHost, s2));

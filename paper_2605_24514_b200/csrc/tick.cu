@@ -32,7 +32,8 @@ __global__ void __launch_bounds__(256) project_append_kernel(
     int64_t core_stride, int ldcore, double* __restrict__ z, int64_t z_stride,
     double* __restrict__ inj_scale, double* __restrict__ rho_out, double* __restrict__ xnorm_out,
     double* __restrict__ A, int64_t a_stride, int64_t a_off, int64_t a_step,
-    double* __restrict__ N, int arrow_only, VDefer vd, const int* __restrict__ gate) {
+    double* __restrict__ N, int arrow_only, VDefer vd, const int* __restrict__ gate,
+    double* __restrict__ ring, int64_t ring_stride) {
   if (gate && *gate) return;
   // sized by RT, not kRMax: with a 64 KB staged F the static arrays decide
   // whether 2 or 3 CTAs fit per SM
@@ -245,7 +246,13 @@ __global__ void __launch_bounds__(256) project_append_kernel(
     inj_scale[b] = fresh ? 1.0 / rho : 0.0;
     rho_out[b] = rho;
     xnorm_out[b] = sqrt(xnorm2);
-    N[b] += xnorm2;
+    const double nn = N[b] + xnorm2;
+    N[b] = nn;
+    if (ring) {  // this tick's result row for the host read-back (engine.cu)
+      ring[b] = nn;
+      ring[ring_stride + b] = rho;
+      ring[2 * ring_stride + b] = sqrt(xnorm2);
+    }
   }
 }
 
@@ -1245,10 +1252,23 @@ __global__ void sumsq_reduce_kernel(int nblk, const double* __restrict__ partial
   if (threadIdx.x == 0) out[b] = t;
 }
 
+// x - x is 0 for finite x and NaN otherwise; 16-byte loads, a few CTAs per
+// SM (the check shares the GPU with the ticks already queued)
 __global__ void check_finite_kernel(size_t n, const double* __restrict__ p, int* flag) {
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
-       i += (size_t)gridDim.x * blockDim.x)
-    if (!isfinite(p[i])) *flag = 1;
+  const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  double acc = 0.0;
+  if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+    const double2* p2 = reinterpret_cast<const double2*>(p);
+    for (size_t i = tid; i < n / 2; i += stride) {
+      const double2 v = p2[i];
+      acc += (v.x - v.x) + (v.y - v.y);
+    }
+    if (tid == 0 && (n & 1)) acc += p[n - 1] - p[n - 1];
+  } else {
+    for (size_t i = tid; i < n; i += stride) acc += p[i] - p[i];
+  }
+  if (acc != 0.0 || acc != acc) *flag = 1;
 }
 
 }  // namespace
@@ -1267,7 +1287,8 @@ int launch_project_append(int batch, int rows, int r, Mat F, const double* x, in
                           int ldcore, double* z, int64_t z_stride, double* inj_scale,
                           double* rho_out, double* xnorm_out, double* A, int64_t a_stride,
                           int64_t a_off, int64_t a_step, double* N, cudaStream_t st,
-                          const Allreducer* ar, int arrow_only, const VDefer* vd) {
+                          const Allreducer* ar, int arrow_only, const VDefer* vd,
+                          double* ring, int64_t ring_stride) {
   const double* G = vd ? vd->G : nullptr;
   if (r > kRMax) {
     set_error("factor width exceeds kernel limit");
@@ -1394,7 +1415,8 @@ int launch_project_append(int batch, int rows, int r, Mat F, const double* x, in
     }
     project_append_kernel<SG, RT><<<batch, 256, SG ? stage : 0, st>>>(
         rows, r, F, x, x_stride, s, lds, tol, core, core_stride, ldcore, z, z_stride, inj_scale,
-        rho_out, xnorm_out, A, a_stride, a_off, a_step, N, arrow_only, vd ? *vd : VDefer{}, g_gate);
+        rho_out, xnorm_out, A, a_stride, a_off, a_step, N, arrow_only, vd ? *vd : VDefer{}, g_gate,
+        ring, ring_stride);
     return ISVD_OK;
   };
   using T1 = std::integral_constant<bool, true>;
@@ -1476,8 +1498,7 @@ static int rotate_dispatch(int batch, int r, int keep, const RotJob& j0, const R
         rb1 = ceil_div(j1->rows, kRegRowsPerBlock);
         if (j1->new_row && rb1 == 0) rb1 = 1;
       }
-      static const bool no_fuse = getenv("ISVD_NO_ZFUSE") != nullptr;
-      const bool fz = zf && zf->w <= 32 && !no_fuse;
+      const bool fz = zf && zf->w <= 32;
       if (j0.zs)
         rotate_reg_kernel<KP, true><<<dim3(rb0 + rb1, batch), kRegWarps * 32, 0, st>>>(
             r, keep, j0, j1 ? *j1 : j0, rb0, g_gate, fz ? *zf : ZeroFix{});
@@ -1615,6 +1636,25 @@ int launch_canonicalize(int batch, int w, Mat U, int m, Mat V, int n, cudaStream
   return ISVD_OK;
 }
 
+__global__ void scalars_out_kernel(int b0, int nb, int B, const double* __restrict__ N,
+                                   const double* __restrict__ rho,
+                                   const double* __restrict__ xnorm, double* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
+    const int b = b0 + i;
+    out[b] = N[b];
+    out[B + b] = rho[b];
+    out[2 * B + b] = xnorm[b];
+  }
+}
+
+int launch_scalars_out(int b0, int nb, int B, const double* N, const double* rho,
+                       const double* xnorm, double* out, cudaStream_t st) {
+  if (nb == 0) return ISVD_OK;
+  scalars_out_kernel<<<std::min(ceil_div(nb, 256), 64), 256, 0, st>>>(b0, nb, B, N, rho, xnorm, out);
+  ISVD_LAUNCHED();
+  return ISVD_OK;
+}
+
 __global__ void eye_kernel(Mat X, int rows, int cols) {
   double* xb = X.p + blockIdx.x * X.stride;
   for (int idx = threadIdx.x; idx < rows * cols; idx += blockDim.x) {
@@ -1676,7 +1716,7 @@ int launch_sumsq(int batch, int rows, int cols, const double* a, int64_t a_strid
 
 int launch_check_finite(size_t n, const double* p, int* flag, cudaStream_t st) {
   if (n == 0) return ISVD_OK;
-  int g = (int)std::min<size_t>((n + 255) / 256, 4096);
+  int g = (int)std::min<size_t>((n + 511) / 512, 296);
   check_finite_kernel<<<g, 256, 0, st>>>(n, p, flag);
   ISVD_LAUNCHED();
   return ISVD_OK;

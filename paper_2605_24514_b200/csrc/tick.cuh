@@ -42,7 +42,8 @@ int launch_project_append(int batch, int rows, int r, Mat F, const double* x, in
                           double* rho_out, double* xnorm_out, double* A, int64_t a_stride,
                           int64_t a_off, int64_t a_step, double* N, cudaStream_t st,
                           const struct Allreducer* ar = nullptr, int arrow_only = 0,
-                          const VDefer* vd = nullptr);
+                          const VDefer* vd = nullptr, double* ring = nullptr,
+                          int64_t ring_stride = 0);
 // Whether launch_project_append accepts a deferred right basis G (F_eff =
 // F G) for this shape (the one-CTA-per-stream path does; the split and
 // cluster paths for few long streams do not).
@@ -141,6 +142,10 @@ int launch_canon_shard_apply(int w, Mat U, int m, Mat V, int n, int world, const
                              cudaStream_t st);
 
 // Copy helpers.
+// out[0:B] = N, out[B:2B] = rho, out[2B:3B] = xnorm for streams [b0, b0+nb)
+// (out: a device-mapped pinned host buffer)
+int launch_scalars_out(int b0, int nb, int B, const double* N, const double* rho,
+                       const double* xnorm, double* out, cudaStream_t st);
 // X[:rows, :cols] <- I per stream
 int launch_eye(int batch, Mat X, int rows, int cols, cudaStream_t st);
 int launch_copy_rows(int batch, int rows, int cols, const double* src, int64_t src_stride,
