@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "core_svd.cuh"
 #include "tick.cuh"
+#include "warp_rot.cuh"
 #include "../../include/isvd.h"
 
 namespace isvd {
@@ -470,6 +471,65 @@ __global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32c_kernel(
   }
   const bool any_dead = __any_sync(0xffffffffu, mine && !live);
   __syncwarp();
+  if (BUILD && rc.uw_mode) {
+    // Fused epilogue: Uk (= G / sigma_raw) staged in smem (the free log area,
+    // columns XOR-swizzled by row parity so the B-fragment reads are
+    // conflict-free), the core's dead-column completion done there, then the
+    // deferred bases rotated by this warp and the engine-level completion.
+    double* Us = reinterpret_cast<double*>(W.log);
+    auto us = [&](int k, int n) -> double& { return Us[k * 32 + (n ^ ((k & 1) << 3))]; };
+    {
+      const double iv = live ? 1.0 / myn : 0.0;
+      const int oc = pos[lane];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) us(k, oc) = (k < s && mine) ? x[k] * iv : 0.0;
+    }
+    __syncwarp();
+    if (any_dead) {
+      for (int t = 0; t < s; ++t) {
+        if (S[t] > 0.0) continue;
+        for (int axis = 0; axis < s; ++axis) {
+          double val = 0.0;
+          if (lane < s) {
+            val = (lane == axis) ? 1.0 : 0.0;
+            for (int c = 0; c < s; ++c)
+              if (c != t) val -= us(lane, c) * us(axis, c);
+          }
+          const double nrm2 = warp_sum(val * val);
+          if (sqrt(nrm2) > 0.5) {
+            __syncwarp();
+            if (lane < s) us(lane, t) = val / sqrt(nrm2);
+            __syncwarp();
+            break;
+          }
+        }
+      }
+    }
+    double* uwb = rc.uw.p + b * rc.uw.stride;
+    if (rc.uw_mode == 1) {
+      for (int i = 0; i < s; ++i)
+        for (int c = lane; c < rc.uw.ld; c += 32) uwb[(int64_t)i * rc.uw.ld + c] = c < s ? us(i, c) : 0.0;
+    } else {
+      warp_rotate(uwb, rc.uw.ld, rc.uw_rows, s, s, [&](int k, int n) { return us(k, n); }, false, 1.0);
+    }
+    const int* ipos = W.ipos;
+    if (rc.gw_rows > 0) {
+      warp_rotate(rc.gw.p + b * rc.gw.stride, rc.gw.ld, rc.gw_rows, s, s,
+                  [&](int k, int n) { return W.V[k][ipos[n]]; }, false, 1.0);
+    } else if (lane < s) {
+      const int srcl = ipos[lane];
+      for (int i = 0; i < s; ++i) Vo[i * ldv + lane] = W.V[i][srcl];
+    }
+    __syncwarp();
+    VDefer zvd = rc.zvd;
+    if (zvd.G) {
+      zvd.G += b * zvd.g_stride;
+      if (zvd.Z) zvd.Z += b * zvd.z_stride;
+    }
+    warp_complete_zero(s, s_out + b * s_out_stride, Mat{rc.zU.p + b * rc.zU.stride, 0, rc.zU.ld},
+                       rc.zm, Mat{rc.zV.p + b * rc.zV.stride, 0, rc.zV.ld}, rc.zn, zvd, nrmv);
+    return;
+  }
   // U = G / sigma_raw (_kernels.pyx:104): row i is written by all lanes at
   // their sorted columns (one 256-byte row per instruction); V from smem
   {

@@ -47,6 +47,21 @@ struct Rank1Core {
   int64_t ring_stride = 0;
   const double* rho = nullptr;
   const double* xnorm = nullptr;
+  // Fused rotations (one warp per stream, warp_rot.cuh; the steady state of
+  // a batched k <= 32 stream): uw_mode 1 = the core's U becomes the new
+  // deferred window uw (s rows), 2 = uw[0:uw_rows] <- uw Uk; gw_rows > 0:
+  // gw[0:gw_rows] <- gw Vk (the deferred right basis; else Vk goes to
+  // vk_out).  Then the engine-level zero-sigma completion (engine.py:59-70)
+  // on (zU, zm rows) and (zV, zn rows) with zvd the deferred right basis.
+  // The core's U / V are not written to uk / vk.
+  int uw_mode = 0;
+  Mat uw{};
+  int uw_rows = 0;
+  Mat gw{};
+  int gw_rows = 0;
+  Mat zU{}, zV{};
+  int zm = 0, zn = 0;
+  VDefer zvd{};
   // Optional separate destination for the core's right vectors (row-major,
   // vk_stride per stream, leading dimension ldvk) instead of vk/ldo
   double* vk_out = nullptr;

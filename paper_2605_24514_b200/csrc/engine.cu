@@ -957,6 +957,7 @@ static int issue_rank_one(isvd_engine* e, const Slice& sl, const int64_t* di, co
   LazyBasis lz = e->lazy();
   lz.W = mat_at(lz.W, b0);
   const bool fused = !e->sharded && r <= 32;
+  const bool fuse_rot = fused && defer && lazy_state != 0;
   if (e->rd_used[e->ring_slot]) ISVD_CUDA(cudaStreamWaitEvent(st, e->rd_done[e->ring_slot], 0));
   if (one) e->mark();
   if (fused) {
@@ -985,9 +986,29 @@ static int issue_rank_one(isvd_engine* e, const Slice& sl, const int64_t* di, co
       rc.vk_stride = e->gstride();
       rc.ldvk = e->ld;
     }
+    if (fuse_rot) {
+      // the deferred bases are rotated by the core kernel's warps (no
+      // rotation launch, no Uk / Vk round trip through HBM)
+      rc.uw_mode = lazy_state;
+      rc.uw = mat_at(e->Wm(), b0);
+      rc.uw_rows = lazy_state == 2 ? e->r_base + e->lazy_b : r;
+      if (vp) {
+        rc.gw = mat_at(e->Gm(), b0);
+        rc.gw_rows = e->vfw + e->vnz;
+      }
+      rc.zU = mat_at(e->Wm(), b0);
+      rc.zm = e->r_base_next + e->lazy_b_next;
+      rc.zV = mat_at(e->Vm(), b0);
+      rc.zn = e->n;
+      rc.zvd = e->vdesc(b0, e->vnz);
+    }
     if (one) e->mark();
     ISVD_TRY(launch_rank1_core_svd32(nb, r, rc, uk, vk, cs, S, sv, S, st,
                                      e->s + (int64_t)b0 * e->ld, e->ld));
+    if (fuse_rot) {
+      if (one) { e->mark(); e->mark(); }
+      return ISVD_OK;
+    }
   } else if (e->sharded) {
     // U[i, :] and A[i, j] from the shard owning row i, summed across shards
     const int64_t il = e->sh_i - e->row0;
