@@ -25,6 +25,7 @@
 #include <cooperative_groups.h>
 #include "common.cuh"
 #include "core_svd.cuh"
+#include "warp_rot.cuh"
 #include "../../include/isvd.h"
 
 namespace isvd {
@@ -104,7 +105,8 @@ __global__ void __launch_bounds__(WIDE ? 512 : 32) arrow_svd_kernel(int n, const
                                                        int ldo, double* __restrict__ sv,
                                                        int64_t sv_stride, double* __restrict__ s_out,
                                                        int64_t s_out_stride, int nkeep,
-                                                       const int* __restrict__ gate) {
+                                                       const int* __restrict__ gate,
+                                                       ArrowFuse af) {
   griddep_launch_dependents();
   griddep_wait();
   if (gate && *gate) return;
@@ -639,8 +641,7 @@ __global__ void __launch_bounds__(WIDE ? 512 : 32) arrow_svd_kernel(int n, const
   // ---- dead-column completion over e_0, e_1, ... (_kernels.pyx:62-79)
   bool mine_dead = false;
   for (int t = tid; t < n; t += blockDim.x) mine_dead |= !(SV[t] > 0.0);
-  if (!__syncthreads_or(mine_dead)) return;
-  if (tid < 32) {
+  if (__syncthreads_or(mine_dead) && tid < 32) {
     const int lane = tid;
     for (int t = 0; t < n; ++t) {
       if (SV[t] > 0.0) continue;
@@ -672,6 +673,33 @@ __global__ void __launch_bounds__(WIDE ? 512 : 32) arrow_svd_kernel(int n, const
       }
     }
   }
+  if constexpr (!WIDE && CL == 1) {
+    if (af.uw_mode) {
+      // fused epilogue (ArrowFuse): this warp's Uk / Vk are in global memory
+      // (L2) -- read them back through L2 and rotate the deferred bases
+      __syncthreads();
+      const int keep = nkeep;
+      double* uwb = af.uw.p + b * af.uw.stride;
+      if (af.uw_mode == 1) {
+        for (int i = 0; i < n; ++i)
+          for (int c = tid; c < af.uw.ld; c += 32)
+            uwb[(int64_t)i * af.uw.ld + c] = c < keep ? __ldcg(U + i * ldo + c) : 0.0;
+      } else {
+        warp_rotate(uwb, af.uw.ld, af.uw_rows, r, keep,
+                    [&](int k, int c) { return __ldcg(U + k * ldo + c); }, true, 1.0);
+      }
+      warp_rotate(af.gw.p + b * af.gw.stride, af.gw.ld, af.gw_rows, r, keep,
+                  [&](int k, int c) { return __ldcg(V + k * ldo + c); }, true, af.inj[b]);
+      __syncwarp();
+      VDefer zvd = af.zvd;
+      if (zvd.G) {
+        zvd.G += b * zvd.g_stride;
+        if (zvd.Z) zvd.Z += b * zvd.z_stride;
+      }
+      warp_complete_zero(keep, SO, Mat{af.zU.p + b * af.zU.stride, 0, af.zU.ld}, af.zm,
+                         Mat{af.zV.p + b * af.zV.stride, 0, af.zV.ld}, af.zn, zvd, S.delta);  // S.delta: free scratch by now
+    }
+  }
 }
 
 }  // namespace
@@ -690,7 +718,7 @@ int read_arrow_counters(int64_t* out4, int reset) {
 int launch_arrow_svd(int batch, int s, const double* core, int64_t core_stride, int ldcore,
                      double* uk, double* vk, int64_t out_stride, int ldo, double* sv,
                      int64_t sv_stride, cudaStream_t st, double* s_out, int64_t s_out_stride,
-                     int nkeep) {
+                     int nkeep, const ArrowFuse* af) {
   if (s < 1 || s > kN) {
     set_error("arrow core size out of range");
     return ISVD_EINVAL;
@@ -700,7 +728,8 @@ int launch_arrow_svd(int batch, int s, const double* core, int64_t core_stride, 
     // one warp per core: roots 32..39 (s = 33 is the k = 32 append core) are
     // solved warp-cooperatively after the one-root-per-lane pass
     arrow_svd_kernel<40, false, 1><<<batch, 32, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
-                                                         out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate);
+                                                         out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate,
+                                                         af ? *af : ArrowFuse{});
   } else if (batch <= kClusterMaxBatch) {
     // few wide cores (config 5b: one 129 core per tick): a cluster per core
     cudaLaunchConfig_t cfg = {};
@@ -720,23 +749,23 @@ int launch_arrow_svd(int batch, int s, const double* core, int64_t core_stride, 
     cudaError_t e;
     if (s <= 72)
       e = cudaLaunchKernelEx(&cfg, arrow_svd_kernel<72, true, kArrowCluster>, s, core, core_stride,
-                             ldcore, uk, vk, out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate);
+                             ldcore, uk, vk, out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate, ArrowFuse{});
     else if (s <= 136)
       e = cudaLaunchKernelEx(&cfg, arrow_svd_kernel<136, true, kArrowCluster>, s, core,
-                             core_stride, ldcore, uk, vk, out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate);
+                             core_stride, ldcore, uk, vk, out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate, ArrowFuse{});
     else
       e = cudaLaunchKernelEx(&cfg, arrow_svd_kernel<kN, true, kArrowCluster>, s, core, core_stride,
-                             ldcore, uk, vk, out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate);
+                             ldcore, uk, vk, out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate, ArrowFuse{});
     ISVD_CUDA(e);
   } else if (s <= 72) {
     arrow_svd_kernel<72, true, 1><<<batch, 512, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
-                                                         out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate);
+                                                         out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate, ArrowFuse{});
   } else if (s <= 136) {
     arrow_svd_kernel<136, true, 1><<<batch, 512, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
-                                                          out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate);
+                                                          out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate, ArrowFuse{});
   } else {
     arrow_svd_kernel<kN, true, 1><<<batch, 512, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
-                                                         out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate);
+                                                         out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate, ArrowFuse{});
   }
   ISVD_LAUNCHED();
   return ISVD_OK;

@@ -78,8 +78,26 @@ int launch_rank1_core_svd32(int batch, int s, const Rank1Core& rc, double* uk, d
 // (arrow_svd.cu).  Same outputs and conventions as launch_core_svd.
 // s_out (optional): the first nkeep singular values are also written there
 // (the engine's s), replacing the separate install copy.
+// Fused row-append epilogue of the one-warp arrow kernel (s <= 40): the
+// deferred bases are rotated by the core's warp (warp_rot.cuh) --
+// uw_mode 1: the core's U[:, :keep] becomes the new window uw (s rows);
+// 2: uw <- [uw 0; 0 1] Uk[:, :keep] (uw_rows old rows); gw <- [gw 0; 0
+// inj] Vk[:, :keep] (gw_rows old rows, inj = 1/rho per stream); then the
+// engine-level zero-sigma completion on (zU, zm) / (zV, zn, zvd).  All Mats
+// and pointers per batch (stride applied per stream).
+struct ArrowFuse {
+  int uw_mode = 0;
+  Mat uw{};
+  int uw_rows = 0;
+  Mat gw{};
+  int gw_rows = 0;
+  const double* inj = nullptr;
+  Mat zU{}, zV{};
+  int zm = 0, zn = 0;
+  VDefer zvd{};
+};
 int launch_arrow_svd(int batch, int s, const double* core, int64_t core_stride, int ldcore,
                      double* uk, double* vk, int64_t out_stride, int ldo, double* sv,
                      int64_t sv_stride, cudaStream_t st, double* s_out = nullptr,
-                     int64_t s_out_stride = 0, int nkeep = 0);
+                     int64_t s_out_stride = 0, int nkeep = 0, const ArrowFuse* af = nullptr);
 }  // namespace isvd

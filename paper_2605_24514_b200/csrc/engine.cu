@@ -872,12 +872,34 @@ static int issue_append(isvd_engine* e, const Slice& sl, const double* xd, int l
                                  e->append_jacobi ? 0 : 1, (vp || vrow) ? &vd : nullptr,
                                  e->ring_row(e->ring_slot, b0), e->B));
   if (one) e->mark();
+  // steady state of a batched k <= 32 stream: the arrow kernel's warp also
+  // rotates the deferred bases (no rotation launch, no Uk / Vk re-read)
+  const bool fuse_rot = !e->append_jacobi && !e->sharded && is_row && vrow && lazy_state != 0 &&
+                        r + 1 <= 40;
+  ArrowFuse af;
+  if (fuse_rot) {
+    af.uw_mode = lazy_state;
+    af.uw = mat_at(e->Wm(), b0);
+    af.uw_rows = lazy_state == 2 ? e->r_base + e->lazy_b : 0;
+    af.gw = mat_at(e->Gm(), b0);
+    af.gw_rows = e->vfw + e->vnz;
+    af.inj = inj;
+    af.zU = mat_at(e->Wm(), b0);
+    af.zm = e->r_base_next + e->lazy_b_next;
+    af.zV = mat_at(e->Vm(), b0);
+    af.zn = e->n;
+    af.zvd = e->vdesc(b0, e->vnz + 1);
+  }
   if (e->append_jacobi)
     ISVD_TRY(launch_core_svd(nb, r + 1, core, cs, S, uk, vk, cs, S, sv, S,
                              e->vscr ? e->vscr + (int64_t)b0 * S * (S | 1) : nullptr, nullptr, st));
   else
     ISVD_TRY(launch_arrow_svd(nb, r + 1, core, cs, S, uk, vk, cs, S, sv, S, st,
-                              e->s + (int64_t)b0 * e->ld, e->ld, keep));
+                              e->s + (int64_t)b0 * e->ld, e->ld, keep, fuse_rot ? &af : nullptr));
+  if (fuse_rot) {
+    if (one) { e->mark(); e->mark(); }
+    return ISVD_OK;
+  }
   if (one) e->mark();
   // row: U <- [U 0; 0 1] Uk, V <- V Vk[:r] + z^ Vk[r] ; col: the same with U<->V
   RotJob grow{mat_at(is_row ? e->Um() : e->Vm(), b0), is_row ? e->m : e->n, uk, cs, S, nullptr, 0,
