@@ -273,9 +273,10 @@ def _simulate_bytes(B, steps, window=32, vwin=8):
     the deferred right basis V_eff = [V | Z^T] G (a rank-1 tick rotates G; a
     full-rank row tick projects through V, Z and G, writes its residual as the
     next Z column and grows G by a row; V is materialised every `vwin` row
-    appends).  Returns (projection bytes, rotation bytes, V-materialisation
-    bytes, SURVEY 8(d) reference-algorithm bytes)."""
-    proj_bytes = rot_bytes = vflush_bytes = all_bytes = 0.0
+    appends).  Returns (projection bytes, row-tick and rank-1-tick rotation
+    bytes (moved inside the core kernels), V-materialisation bytes, SURVEY
+    8(d) reference-algorithm bytes)."""
+    proj_bytes = rot_row = rot_r1 = vflush_bytes = all_bytes = 0.0
     m, b_rows, active = M0, 0, False
     vpend, nz = False, 0
     for t in range(steps):
@@ -302,7 +303,7 @@ def _simulate_bytes(B, steps, window=32, vwin=8):
             if b_rows >= window:
                 active, b_rows = False, 0
         else:
-            proj_bytes += 8.0 * B * (2 * K + 2 + nz)          # U/V row gathers (+ Z entries)
+            rot_r1 += 8.0 * B * (2 * K + 2 + nz)              # U/V row gathers (+ Z entries)
             vb = 2 * g if vpend else K * K                    # G <- G Vk, or Vk written as G
             vpend = True
             if not active:
@@ -310,8 +311,11 @@ def _simulate_bytes(B, steps, window=32, vwin=8):
                 active, b_rows = True, 0
             else:
                 wb = 2 * (K + b_rows) * K
-        rot_bytes += 8.0 * B * (vb + wb)
-    return proj_bytes, rot_bytes, vflush_bytes, all_bytes
+        if row:
+            rot_row += 8.0 * B * (vb + wb)
+        else:
+            rot_r1 += 8.0 * B * (vb + wb)
+    return proj_bytes, rot_row, rot_r1, vflush_bytes, all_bytes
 
 
 def make_inputs_5b(torch, dev, seed=0, m=M5B, row0=0, rows=None):
@@ -578,8 +582,8 @@ def run_gpu(args):
                for j, name in enumerate(("project", "core_svd", "rotate", "install"))}
         for i, kind in enumerate(("row_append", "rank_one"))}
     window = int(lib.isvd_engine_lazy_window(eng._h.h))
-    proj_bytes, rot_bytes, vflush_bytes, _ = _simulate_bytes(B, diag_steps, window)
-    all_bytes = _simulate_bytes(B, steps, window)[3]
+    proj_bytes, rot_row, rot_r1, vflush_bytes, _ = _simulate_bytes(B, diag_steps, window)
+    all_bytes = _simulate_bytes(B, steps, window)[4]
     # ---------------- end-to-end through the public API with host buffers
     e2e_steps = min(steps, args.e2e_steps)
     nrow = (e2e_steps + 1) // 2
@@ -611,35 +615,37 @@ def run_gpu(args):
     if rank == 0:
         peak, peak_kind = _peaks()
         tot = lambda i: float(ph[i] + ph[4 + i])
+        # the deferred-basis rotations run inside the core kernels (warp DMMA
+        # epilogues), so their bytes are accounted with them
         kernels = {
-            "project_append/rank1_build (K1/K6)": {"ms": tot(0), "bytes": proj_bytes},
-            "arrow_svd (K2a, append cores)": {"ms": float(ph[1]), "bytes": None},
-            "jacobi32 (K2b, rank-1 cores)": {"ms": float(ph[5]), "bytes": None},
-            "rotate W + G (K3/K4, per tick)": {"ms": tot(2), "bytes": rot_bytes},
+            "project_append (K1, row ticks)": {"ms": float(ph[0]), "bytes": proj_bytes},
+            "arrow_svd + fused W/G rotation (K2a, row ticks)": {
+                "ms": float(ph[1] + ph[2]), "bytes": rot_row},
+            "jacobi32c + fused W/G rotation (K2b, rank-1 ticks)": {
+                "ms": float(ph[4] + ph[5] + ph[6]), "bytes": rot_r1},
             "rotate U flush (K3, deferred)": {"ms": flush_ms, "bytes": flush_bytes},
-            "install (V materialisation, zero-sigma check)": {"ms": max(0.0, tot(3) - flush_ms),
-                                                              "bytes": vflush_bytes or None},
+            "V materialisation (K3, every 8 row appends)": {"ms": max(0.0, tot(3) - flush_ms),
+                                                            "bytes": vflush_bytes or None},
         }
         busy = sum(v["ms"] for v in kernels.values())
         for v in kernels.values():
             v["share"] = v["ms"] / busy if busy else None
             v["ms_per_step"] = v["ms"] / max(1, diag_steps)
             v["gbs"] = (v["bytes"] / (v["ms"] / 1e3) / 1e9) if (v["bytes"] and v["ms"]) else None
-        hbm = {k: v for k, v in kernels.items() if v["bytes"]}
         dom_name = max(kernels, key=lambda k: kernels[k]["ms"])
-        hbm_name = max(hbm, key=lambda k: hbm[k]["ms"])
+        # the HBM-bound kernel of the tick (the core kernels are FP64-latency
+        # bound: see profiles/ for their pipe utilisation)
+        hbm_name = "project_append (K1, row ticks)"
+        hbm = kernels
         hk = hbm[hbm_name]
         achieved = hk["gbs"]
         summ, summ_file = _ncu_summary()
         traffic = None
-        ncu_key = {"project_append/rank1_build (K1/K6)": "proj5a",
-                   "rotate W + G (K3/K4, per tick)": "rot5a"}.get(hbm_name)
+        ncu_key = "proj5a"
         if ncu_key in summ and "dram_bytes" in summ[ncu_key]:
             # the capture is one stream-group launch (B / 4 streams) of a row
             # tick; per tick on average over both event kinds for K1
             traffic = summ[ncu_key]["dram_bytes"] * 4.0 * B / TOTAL_STREAMS
-            if ncu_key == "proj5a":
-                traffic *= 0.5
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
             "warmup": warm, "ms_per_step": t_max / steps, "higher_is_better": True,
@@ -662,11 +668,12 @@ def run_gpu(args):
                                             "+write of one stream-group launch x 4 groups "
                                             "(ncu, cold-cache), per tick")
                          if traffic else None,
-                         "bytes_per_launch": hk["bytes"] / max(1, (n_flush if "flush" in hbm_name
-                                                                   else diag_steps)),
+                         "bytes_per_launch": hk["bytes"] / max(1, (diag_steps + 1) // 2),
+                         "launch": "one K1 launch over all streams of the GPU (a row tick)",
                          "dominant_kernel_by_time": dom_name,
-                         "measured_over": f"first {diag_steps} ticks, one stream group, "
-                                          "CUDA events around each phase"},
+                         "measured_over": f"first {diag_steps} ticks in timing mode (one "
+                                          "launch per kernel over all streams, CUDA events "
+                                          "around each phase on the engine stream)"},
             "kernels": kernels,
             "flushes": n_flush,
             "phase_ms_by_event": phase_by_kind,

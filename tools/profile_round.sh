@@ -9,7 +9,7 @@ SHORT="python bench.py --steps 16 --warmup 3 --no-cpu-baseline --e2e-steps 4 --d
 timeout 300 $SHORT > gpurun_out/plain.log 2>&1 || exit 1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "isvd_timed/" --csv --log-file gpurun_out/launches.csv $SHORT > gpurun_out/ncu_launch.log 2>&1
 FULL="timeout 600 ncu --set full --clock-control none --import-source on"
-for spec in "project_append:proj5a:8" "rotate_reg_kernel:rot5a:8" "jacobi32c:jacobi32:8" "arrow_svd:arrow40:8"; do
+for spec in "project_append:proj5a:8" "rotate_reg_kernel:vflush5a:0" "jacobi32c:jacobi32:8" "arrow_svd:arrow40:8"; do
   IFS=: read k name sk <<< "$spec"
   $FULL -k regex:$k -s $sk -c 1 -o gpurun_out/$name $SHORT > gpurun_out/ncu_$name.log 2>&1
 done
