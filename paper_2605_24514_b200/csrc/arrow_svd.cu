@@ -681,9 +681,16 @@ __global__ void __launch_bounds__(WIDE ? 512 : 32) arrow_svd_kernel(int n, const
       const int keep = nkeep;
       double* uwb = af.uw.p + b * af.uw.stride;
       if (af.uw_mode == 1) {
-        for (int i = 0; i < n; ++i)
-          for (int c = tid; c < af.uw.ld; c += 32)
-            uwb[(int64_t)i * af.uw.ld + c] = c < keep ? __ldcg(U + i * ldo + c) : 0.0;
+        // lane = column; eight rows of loads in flight before their stores
+        for (int i0 = 0; i0 < n; i0 += 8) {
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            v[u] = (i0 + u < n && tid < keep) ? __ldcg(U + (i0 + u) * ldo + tid) : 0.0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (i0 + u < n && tid < af.uw.ld) uwb[(int64_t)(i0 + u) * af.uw.ld + tid] = v[u];
+        }
       } else {
         warp_rotate(uwb, af.uw.ld, af.uw_rows, r, keep,
                     [&](int k, int c) { return __ldcg(U + k * ldo + c); }, true, 1.0);

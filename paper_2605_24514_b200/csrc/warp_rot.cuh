@@ -30,14 +30,23 @@ __device__ __forceinline__ void warp_rotate(double* X, int ld, int rows, int r, 
       const int k = kk * 4 + qd, n = nn * 8 + g;
       bq[kk][nn] = (k < r && n < keep) ? q(k, n) : 0.0;
     }
-  for (int row0 = 0; row0 < rows; row0 += 8) {
+  // the next row group's operands are loaded before this group's results
+  // are stored (the stores may alias the loads as far as the compiler
+  // knows, which would otherwise serialise one memory latency per group)
+  auto load_a = [&](double (&a)[8], int row0) {
     const int row = row0 + g;
-    double a[8];
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
       const int k = kk * 4 + qd;
       a[kk] = (row < rows && k < r) ? X[(int64_t)row * ld + k] : 0.0;
     }
+  };
+  double a[8];
+  load_a(a, 0);
+  for (int row0 = 0; row0 < rows; row0 += 8) {
+    const int row = row0 + g;
+    double an[8];
+    if (row0 + 8 < rows) load_a(an, row0 + 8);
     double d[4][2];
 #pragma unroll
     for (int nn = 0; nn < 4; ++nn) d[nn][0] = d[nn][1] = 0.0;
@@ -52,6 +61,8 @@ __device__ __forceinline__ void warp_rotate(double* X, int ld, int rows, int r, 
         if (c0 < ld) *reinterpret_cast<double2*>(X + (int64_t)row * ld + c0) = make_double2(d[nn][0], d[nn][1]);
       }
     }
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) a[kk] = an[kk];
   }
   if (new_row)
     for (int c = lane; c < ld; c += 32) X[(int64_t)rows * ld + c] = c < keep ? scale * q(r, c) : 0.0;
