@@ -145,10 +145,13 @@ int isvd_engine_get_tracked(isvd_engine* e, int b, double* a);
 int isvd_engine_get_reference(isvd_engine* e, int b, double* ref);
 /* sq_norm: B values; last_residual / last_input_norm: B values each. */
 /* Pipelined read of the per-step result: enqueue the copy of (sq_norm,
- * last_residual, last_input_norm) -- 3 x B doubles, stream-major -- into
- * `host` (pinned memory) on the engine stream and return at once; ticket
+ * last_residual, last_input_norm) -- 3 x B doubles: [sq_norm | residual |
+ * input norm] -- into `host` (pinned memory) and return at once; ticket
  * `slot` (0..7) completes with isvd_engine_scalars_wait.  Lets a host loop
- * issue step t+1 before step t's result lands (one step of lag). */
+ * issue steps t+1.. before step t's result lands.  After a tick whose
+ * kernels wrote the read-back ring (the batched K1 / fused rank-1 paths) the
+ * copy runs on a separate read-back stream once every stream group has
+ * finished that tick; otherwise it is issued per group. */
 int isvd_engine_scalars_async(isvd_engine* e, double* host, int slot);
 int isvd_engine_scalars_wait(isvd_engine* e, int slot);
 int isvd_engine_get_scalars(isvd_engine* e, double* sq_norm, double* last_residual,
@@ -168,7 +171,11 @@ int isvd_engine_device_views(isvd_engine* e, double** u, int64_t* u_stride, int*
                              double** v, int64_t* v_stride, int* ldv, double** s,
                              int* lds, double** a, int64_t* a_stride, int* lda);
 int isvd_engine_canonicalize(isvd_engine* e);
-/* The cudaStream_t (as void*) every launch of this engine goes to. */
+/* The engine stream (cudaStream_t as void*).  Batches of >= 512 streams
+ * run their ticks on stream groups that may run ahead of it; every entry
+ * point other than the three event calls (and this one) first makes the
+ * engine stream wait for them, so work enqueued on the returned stream after
+ * a call of this function is ordered after all engine work so far. */
 void* isvd_engine_stream(isvd_engine* e);
 int isvd_engine_synchronize(isvd_engine* e);
 /* Per-phase device timing (CUDA events on the engine stream around each
