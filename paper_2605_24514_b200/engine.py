@@ -288,6 +288,10 @@ class SvdEngine:
         self._version += 1
         self._cache.clear()
 
+    def synchronize(self) -> None:
+        """Wait for this engine's queued device work (events are asynchronous)."""
+        _lib.check(self._h.lib.isvd_engine_synchronize(self._h.h))
+
     def _shape_all(self):
         return self._h.shape()
 
