@@ -22,7 +22,9 @@ struct Mat {
 // and Z holding nz appended residuals (Z[t * ldz + c], z_stride per stream).
 // nz = 0 and fw = r is the rank-1-only deferral V_eff = V G.
 constexpr int kVWin = 8;             // residual columns per deferred window
-constexpr int kGMaxRows = 32 + kVWin;  // rows of G the k <= 32 kernels handle
+// rows of G the k <= 32 kernels handle (a multiple of 8: the materialising
+// rotation's K dimension is rounded up to 8)
+constexpr int kGMaxRows = (32 + kVWin + 7) / 8 * 8;
 struct VDefer {
   const double* G = nullptr;
   int64_t g_stride = 0;
