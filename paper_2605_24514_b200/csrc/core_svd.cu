@@ -288,7 +288,23 @@ __device__ __forceinline__ void j32c_round(double (&x)[32], int lane, double2* c
     relmax = fmaxf(relmax, __fdividef((float)apq2, (float)pq));
     const double d = aqq - app, h = 2.0 * apq;
     const double big = fmax(fabs(d), fabs(h));
-    if (big < 1e150 && big > 1e-140) {
+    const double ad = fabs(d), ah = fabs(h);
+    if (ah <= 1e-3 * ad && ad < 1e150 && ad > 1e-140) {
+      // small rotation (the Brand rank-1 cores: |h / d| ~ 1e-5): the same
+      // t, c, s as below from series in eps = (h/d)^2 <= 1e-6 -- one
+      // reciprocal instead of two reciprocal square roots and a reciprocal
+      // on the round's critical path; truncation < 1e-19 relative.
+      //   u / |d| = 1 + sqrt(1 + eps) = 2 + del, del = eps/2 - eps^2/8
+      //   tau = |h| / u = (|h|/|d|) / (2 + del),  c = (1 + tau^2)^(-1/2)
+      const double hr = ah * j32_rcp(ad);
+      const double eps = hr * hr;
+      const double del = eps * fma(-0.125, eps, 0.5);
+      const double tau = 0.5 * hr * fma(del, fma(0.25, del, -0.5), 1.0);
+      const double tau2 = tau * tau;
+      c = fma(tau2, fma(0.375, tau2, -0.5), 1.0);
+      t = ((d < 0.0) != (h < 0.0)) ? -tau : tau;  // sign(d) h / u
+      sn = t * c;
+    } else if (big < 1e150 && big > 1e-140) {
       const double x2 = fma(d, d, h * h);
       const double u = fabs(d) + x2 * j32_rsqrt(x2);
       const double qq = j32_rsqrt(fma(u, u, h * h));
