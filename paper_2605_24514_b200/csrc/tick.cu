@@ -990,13 +990,23 @@ __global__ void __launch_bounds__(kRegWarps * 32, 8)
     const int row = row0 + g;
     double a[KQ];
     if (ZS && row < row_end) {
-      // [X(:, :zfw) | Z^T] (deferred right basis flush)
+      // [X(:, :zfw) | Z^T] (deferred right basis flush); a lane's k range
+      // that lies inside X is read with 16-byte loads
       const double* src = X + (int64_t)row * ld;
       const double* zsb = J.zs + b * J.zs_stride + row;
+      if ((KQ & 1) == 0 && q * KQ + KQ <= J.zfw) {
 #pragma unroll
-      for (int kk = 0; kk < KQ; ++kk) {
-        const int k = q * KQ + kk;
-        a[kk] = k < J.zfw ? src[k] : (k < r ? zsb[(int64_t)(k - J.zfw) * J.ldzs] : 0.0);
+        for (int kk = 0; kk < KQ; kk += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(src + q * KQ + kk);
+          a[kk] = v.x;
+          a[kk + 1] = v.y;
+        }
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < KQ; ++kk) {
+          const int k = q * KQ + kk;
+          a[kk] = k < J.zfw ? src[k] : (k < r ? zsb[(int64_t)(k - J.zfw) * J.ldzs] : 0.0);
+        }
       }
     } else if (row < row_end) {
       const double* src = X + (int64_t)row * ld + q * KQ;
