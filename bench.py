@@ -709,7 +709,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=8)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--streams", type=int, default=TOTAL_STREAMS)
-    ap.add_argument("--e2e-steps", type=int, default=128)
+    ap.add_argument("--e2e-steps", type=int, default=512)
     ap.add_argument("--diag-steps", type=int, default=256)
     ap.add_argument("--cpu-streams", type=int, default=64)
     ap.add_argument("--cpu-events", type=int, default=128)
