@@ -177,6 +177,16 @@ int isvd_engine_canonicalize(isvd_engine* e);
  * engine stream wait for them, so work enqueued on the returned stream after
  * a call of this function is ordered after all engine work so far. */
 void* isvd_engine_stream(isvd_engine* e);
+/* Every CUDA stream that may read a device-resident event payload (the
+ * engine stream first, then the stream groups created so far), without
+ * joining them.  Writes min(count, cap) handles to out; returns the count.
+ * A caller passing device buffers to the event calls keeps them alive until
+ * all of these streams pass the call (torch: Tensor.record_stream on each). */
+int isvd_engine_streams(isvd_engine* e, void** out, int cap);
+/* Waits for the engine's work.  Device-resident rank-1 payloads are checked
+ * on the device (index in bounds, finite delta); a rejected entry is applied
+ * as a no-op to its stream and this call (and get_scalars / get_factors)
+ * then returns ISVD_EINVAL once. */
 int isvd_engine_synchronize(isvd_engine* e);
 /* Per-phase device timing (CUDA events on the engine stream around each
  * phase of every event): phase 0 = projection / rank-1 gather (K1/K6),

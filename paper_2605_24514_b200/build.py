@@ -29,12 +29,32 @@ def _sources():
     return sorted(CSRC.glob("*.cu"))
 
 
+STAMP = PKG / "libisvd.so.sha256"
+
+
+def _source_hash() -> str:
+    """Digest of every input of the library (sources, header, flags, nvcc
+    version): the library is rebuilt whenever it differs from the digest
+    recorded next to it by the last build, whatever the file times say."""
+    import hashlib
+
+    h = hashlib.sha256()
+    deps = sorted(CSRC.glob("*")) + [ROOT / "include" / "isvd.h", Path(__file__)]
+    for p in deps:
+        h.update(p.name.encode())
+        h.update(p.read_bytes())
+    h.update(" ".join(ARCH + FLAGS).encode())
+    try:
+        h.update(subprocess.run([NVCC, "--version"], capture_output=True, text=True).stdout.encode())
+    except OSError:
+        pass
+    return h.hexdigest()
+
+
 def _needs_build() -> bool:
-    if not LIB.exists():
+    if not LIB.exists() or not STAMP.exists():
         return True
-    t = LIB.stat().st_mtime
-    deps = list(CSRC.glob("*")) + [ROOT / "include" / "isvd.h", Path(__file__)]
-    return any(p.stat().st_mtime > t for p in deps)
+    return STAMP.read_text().strip() != _source_hash()
 
 
 def _compile(src: Path, verbose: bool) -> Path:
@@ -62,6 +82,7 @@ def build_lib(force: bool = False, verbose: bool = False) -> Path:
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")
     os.replace(tmp, LIB)
+    STAMP.write_text(_source_hash() + "\n")
     return LIB
 
 

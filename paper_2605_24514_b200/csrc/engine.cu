@@ -146,6 +146,23 @@ struct isvd_engine {
   cudaEvent_t stage_ready = nullptr;
   int stage_slot = 0;
   volatile int* vflag_h = nullptr;  // pinned: the device finiteness verdict per slot
+  // Device-resident rank-1 payloads are validated by the staging kernel;
+  // a rejected entry sets dflag[kDevBad] (sticky) and is applied as a no-op.
+  // The verdict is read at the next synchronisation point.
+  static constexpr int kDevBad = 1 + kStageSlots;
+  bool dev_inputs = false;
+  int dev_input_verdict() {
+    if (!dev_inputs) return ISVD_OK;
+    dev_inputs = false;
+    int bad = 0;
+    ISVD_CUDA(cudaMemcpyAsync(&bad, dflag + kDevBad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    ISVD_CUDA(cudaStreamSynchronize(st));
+    if (!bad) return ISVD_OK;
+    ISVD_CUDA(cudaMemsetAsync(dflag + kDevBad, 0, sizeof(int), st));
+    set_error("a device-resident rank-1 event had an index out of bounds or a non-finite delta; "
+              "it was applied as a no-op to its stream");
+    return ISVD_EINVAL;
+  }
   int ensure_copy_stream() {
     if (cp_st) return ISVD_OK;
     ISVD_CUDA(cudaHostAlloc((void**)&vflag_h, kStageSlots * sizeof(int), cudaHostAllocDefault));
@@ -269,10 +286,12 @@ struct isvd_engine {
   }
   struct Snap {
     double *U = nullptr, *V = nullptr, *A = nullptr, *s = nullptr, *N = nullptr;
-    size_t nu = 0, nv = 0, na = 0, ns = 0;
+    double* ref = nullptr;  // the drift reference (set_reference / refresh(store_reference))
+    size_t nu = 0, nv = 0, na = 0, ns = 0, nref = 0;
     int m = 0, n = 0, r = 0, k = 0, m_cap = 0, n_cap = 0, ld = 0, m_glob = 0;
+    int ref_m = 0, ref_r = 0, ref_cap = 0;
     int64_t step = 0;
-    bool canonical = true, valid = false;
+    bool canonical = true, valid = false, has_ref = false;
   } snap;
   // stream groups (pipelining across streams of the batch)
   static constexpr int kGroupMin = 256;
@@ -622,7 +641,8 @@ struct isvd_engine {
     dfree(ei); dfree(ej); dfree(ed); dfree(dflag);
     if (zf_cnt) cudaFree(zf_cnt); dfree(ref); dfree(W); dfree(Gv); dfree(Zv);
     dfree(wx); dfree(wj); dfree(wpart); dfree(wout); dfree(wflags);
-    dfree(snap.U); dfree(snap.V); dfree(snap.A); dfree(snap.s); dfree(snap.N); dfree(shv);
+    dfree(snap.U); dfree(snap.V); dfree(snap.A); dfree(snap.s); dfree(snap.N); dfree(snap.ref);
+    dfree(shv);
     for (auto g : gst) cudaStreamDestroy(g);
     for (auto ev : join_ev) cudaEventDestroy(ev);
     if (fork_ev) cudaEventDestroy(fork_ev);
@@ -700,7 +720,11 @@ int isvd_engine_create(isvd_engine** out, int batch, int m, int n, int k, double
   A(dalloc(&e->ei, (size_t)isvd_engine::kStageSlots * batch));  // staging slots
   A(dalloc(&e->ej, (size_t)isvd_engine::kStageSlots * batch));
   A(dalloc(&e->ed, (size_t)isvd_engine::kStageSlots * batch));
-  A(dalloc(&e->dflag, 1 + isvd_engine::kStageSlots));
+  A(dalloc(&e->dflag, 2 + isvd_engine::kStageSlots));
+  if (rc == ISVD_OK && cudaMemset(e->dflag, 0, sizeof(int) * (2 + isvd_engine::kStageSlots)) != cudaSuccess) {
+    set_error("cudaMemset failed");
+    rc = ISVD_ENODEV;
+  }
   A(dalloc(&e->W, (size_t)batch * e->wstride()));
   A(dalloc(&e->sring, (size_t)isvd_engine::kRing * 3 * batch));
   if (rc == ISVD_OK) {
@@ -1318,6 +1342,20 @@ int isvd_engine_rank_one(isvd_engine* e, const int64_t* i, const int64_t* j, con
     ISVD_CUDA(cudaEventRecord(e->stage_ready, e->cp_st));
     ISVD_CUDA(cudaStreamWaitEvent(e->st, e->stage_ready, 0));
     di = si; dj = sj; dd = sd;
+  } else if (!e->sharded) {
+    // device payload: copied into a staging slot on the engine stream and
+    // bounds/finiteness-checked there (the caller's buffer is then free
+    // once the engine stream passes this point)
+    rslot = e->stage_slot;
+    e->stage_slot = (e->stage_slot + 1) % isvd_engine::kStageSlots;
+    int64_t* si = e->ei + (int64_t)rslot * e->B;
+    int64_t* sj = e->ej + (int64_t)rslot * e->B;
+    double* sd = e->ed + (int64_t)rslot * e->B;
+    ISVD_TRY(e->ticket_wait(e->st, e->stage_tk[rslot]));
+    ISVD_TRY(launch_stage_rank1(e->B, i, j, delta, si, sj, sd, e->gm(), e->n,
+                                e->dflag + isvd_engine::kDevBad, e->st));
+    e->dev_inputs = true;
+    di = si; dj = sj; dd = sd;
   }
   const int lazy_state = !e->lazy_mode ? 0 : (e->lazy_active ? 2 : 1);
   e->r_base_next = lazy_state == 1 ? e->r : e->r_base;
@@ -1334,7 +1372,7 @@ int isvd_engine_rank_one(isvd_engine* e, const int64_t* i, const int64_t* j, con
     return issue_rank_one(e, sl, di, dj, dd, lazy_state, defer, vp);
   }));
   if (defer) e->vpend = true;
-  if (!on_device) ISVD_TRY(e->ticket_record(e->stage_tk[rslot]));
+  if (!on_device || !e->sharded) ISVD_TRY(e->ticket_record(e->stage_tk[rslot]));
   if (lazy_state == 1) {
     e->lazy_active = true;
     e->m_base = e->m;
@@ -1435,7 +1473,7 @@ int isvd_engine_get_factors(isvd_engine* e, int b, double* u, double* sv, double
                                 cudaMemcpyDeviceToHost, e->st));
   }
   ISVD_CUDA(cudaStreamSynchronize(e->st));
-  return ISVD_OK;
+  return e->dev_input_verdict();
 }
 
 int isvd_engine_get_tracked(isvd_engine* e, int b, double* a) {
@@ -1467,7 +1505,7 @@ int isvd_engine_get_scalars(isvd_engine* e, double* sq_norm, double* last_residu
   if (last_residual) ISVD_CUDA(cudaMemcpyAsync(last_residual, e->rho, sizeof(double) * e->B, cudaMemcpyDeviceToHost, e->st));
   if (last_input_norm) ISVD_CUDA(cudaMemcpyAsync(last_input_norm, e->xnorm, sizeof(double) * e->B, cudaMemcpyDeviceToHost, e->st));
   ISVD_CUDA(cudaStreamSynchronize(e->st));
-  return ISVD_OK;
+  return e->dev_input_verdict();
 }
 
 int isvd_engine_scalars_async(isvd_engine* e, double* host, int slot) {
@@ -1604,6 +1642,13 @@ int isvd_engine_snapshot(isvd_engine* e) {
   ISVD_CUDA(cudaMemcpyAsync(S.N + 2 * e->B, e->xnorm, e->B * 8, cudaMemcpyDeviceToDevice, e->st));
   S.m = e->m; S.n = e->n; S.r = e->r; S.k = e->k; S.step = e->step; S.m_glob = e->m_glob;
   S.m_cap = e->m_cap; S.n_cap = e->n_cap; S.ld = e->ld; S.canonical = e->canonical;
+  S.has_ref = e->has_ref && e->ref;
+  if (S.has_ref) {
+    const size_t nref = (size_t)e->B * e->ref_cap * e->ld;
+    if (S.nref != nref) { dfree(S.ref); ISVD_TRY(dalloc(&S.ref, nref)); S.nref = nref; }
+    ISVD_CUDA(cudaMemcpyAsync(S.ref, e->ref, nref * 8, cudaMemcpyDeviceToDevice, e->st));
+    S.ref_m = e->ref_m; S.ref_r = e->ref_r; S.ref_cap = e->ref_cap;
+  }
   S.valid = true;
   ISVD_CUDA(cudaStreamSynchronize(e->st));
   return ISVD_OK;
@@ -1630,6 +1675,18 @@ int isvd_engine_restore(isvd_engine* e) {
   ISVD_CUDA(cudaMemcpyAsync(e->xnorm, S.N + 2 * e->B, e->B * 8, cudaMemcpyDeviceToDevice, e->st));
   e->m = S.m; e->n = S.n; e->r = S.r; e->k = S.k; e->step = S.step; e->canonical = S.canonical;
   e->m_glob = S.m_glob;
+  // the drift reference belongs to the checkpointed timeline too
+  e->has_ref = S.has_ref;
+  if (S.has_ref) {
+    if (!e->ref || e->ref_cap != S.ref_cap) {
+      dfree(e->ref);
+      ISVD_TRY(dalloc(&e->ref, S.nref));
+      e->ref_cap = S.ref_cap;
+    }
+    ISVD_CUDA(cudaMemcpyAsync(e->ref, S.ref, S.nref * 8, cudaMemcpyDeviceToDevice, e->st));
+    e->ref_m = S.ref_m;
+    e->ref_r = S.ref_r;
+  }
   ISVD_CUDA(cudaStreamSynchronize(e->st));
   return ISVD_OK;
 }
@@ -1741,7 +1798,19 @@ int isvd_engine_synchronize(isvd_engine* e) {
   if (e) e->join();
   if (!e) { set_error("null engine"); return ISVD_EINVAL; }
   ISVD_CUDA(cudaStreamSynchronize(e->st));
-  return ISVD_OK;
+  return e->dev_input_verdict();
+}
+
+int isvd_engine_streams(isvd_engine* e, void** out, int cap) {
+  if (!e) { set_error("null engine"); return ISVD_EINVAL; }
+  int cnt = 0;
+  if (out && cap > 0) out[cnt] = (void*)e->st;
+  cnt += 1;
+  for (auto g : e->gst) {
+    if (out && cnt < cap) out[cnt] = (void*)g;
+    cnt += 1;
+  }
+  return cnt;
 }
 
 // ------------------------------------------------------------------ metrics

@@ -1281,7 +1281,35 @@ __global__ void check_finite_kernel(size_t n, const double* __restrict__ p, int*
   if (acc != 0.0 || acc != acc) *flag = 1;
 }
 
+// Device-resident rank-1 payloads (i, j, delta per stream) are copied into
+// the engine's staging slot and validated on the way: an index outside the
+// current shape or a non-finite delta becomes the no-op event (0, 0, 0.0) --
+// K = diag(s), no rotation, A and N unchanged -- and raises the sticky flag
+// the host reports at its next synchronisation point (engine.py:155-160
+// raise before any mutation; a device payload can only be checked on the
+// device, so the stream is left unchanged instead).
+__global__ void stage_rank1_kernel(int B, const int64_t* __restrict__ i, const int64_t* __restrict__ j,
+                                   const double* __restrict__ d, int64_t* si, int64_t* sj, double* sd,
+                                   int64_t m, int64_t n, int* flag) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int64_t ib = i[b], jb = j[b];
+  const double db = d[b];
+  const bool ok = 0 <= ib && ib < m && 0 <= jb && jb < n && db - db == 0.0;
+  si[b] = ok ? ib : 0;
+  sj[b] = ok ? jb : 0;
+  sd[b] = ok ? db : 0.0;
+  if (!ok) atomicOr(flag, 1);
+}
+
 }  // namespace
+
+int launch_stage_rank1(int B, const int64_t* i, const int64_t* j, const double* d, int64_t* si,
+                       int64_t* sj, double* sd, int64_t m, int64_t n, int* flag, cudaStream_t st) {
+  stage_rank1_kernel<<<(B + 255) / 256, 256, 0, st>>>(B, i, j, d, si, sj, sd, m, n, flag);
+  ISVD_LAUNCHED();
+  return ISVD_OK;
+}
 
 // the launch goes to project_append_kernel (which honours g_gate)
 bool project_append_gateable(int batch, int rows, int r) {

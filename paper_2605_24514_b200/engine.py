@@ -53,6 +53,67 @@ class _Handle:
     def stream(self) -> int:
         return int(self.lib.isvd_engine_stream(self.h) or 0)
 
+    def streams(self) -> list[int]:
+        """Engine stream + stream groups (no join): every stream that may
+        read a device-resident event payload."""
+        cap = 16
+        buf = (C.c_void_p * cap)()
+        n = int(self.lib.isvd_engine_streams(self.h, buf, cap))
+        return [int(buf[i] or 0) for i in range(min(n, cap))]
+
+
+class _DeviceInputs:
+    """Stream ordering and lifetime of device-resident (torch) event payloads.
+
+    The engine reads a payload on its own stream (rank-1 triples are staged
+    and bounds-checked there) and, for appended rows / columns, on its stream
+    groups, which may run ahead of the caller.  Before an event the engine
+    stream waits for the caller's current torch stream (the producer); after
+    it the tensor is marked as in use on every engine stream
+    (Tensor.record_stream), so the caching allocator cannot hand its memory
+    out again while a group still reads it."""
+
+    def __init__(self, handle: _Handle):
+        self._h = handle
+        self._st0 = handle.stream()  # fixed for the engine's lifetime (join is a no-op here)
+        self._ext = {}
+        self._device = None
+
+    def _wrap(self, torch, s: int):
+        ext = self._ext.get(s)
+        if ext is None:
+            ext = self._ext[s] = torch.cuda.ExternalStream(s, device=self._device)
+        return ext
+
+    def check(self, t, dtype_name: str, shape, name: str):
+        import torch
+
+        if tuple(t.shape) != tuple(shape):
+            raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+        want = getattr(torch, dtype_name)
+        if t.dtype != want:
+            raise ValueError(f"{name} must be {dtype_name}, got {t.dtype}")
+        if self._device is None:
+            self._device = torch.device("cuda", torch.cuda.current_device())
+        if t.device != self._device:
+            raise ValueError(f"{name} is on {t.device}, the engine runs on {self._device}")
+        return t.contiguous()
+
+    def before(self):
+        import torch
+
+        cur = torch.cuda.current_stream(self._device)
+        if cur.cuda_stream != self._st0:
+            self._wrap(torch, self._st0).wait_stream(cur)
+
+    def after(self, *tensors):
+        import torch
+
+        for s in self._h.streams():
+            ext = self._wrap(torch, s)
+            for t in tensors:
+                t.record_stream(ext)
+
 
 class BatchedSvdEngine:
     """B independent incremental-SVD streams of identical shape.
@@ -84,6 +145,10 @@ class BatchedSvdEngine:
         self._h = _Handle(batch, m, n, k, tol, reortho_guard, m_cap, n_cap, k_cap, stream)
         self.tol = float(tol)
         self.reortho_guard = bool(reortho_guard)
+        self._dev = _DeviceInputs(self._h)
+        if on_dev:
+            src = self._dev.check(src, "float64", (batch, m, n), "a0")
+            self._dev.before()
         _lib.check(self._h.lib.isvd_engine_init(self._h.h, _lib.vptr(src), int(on_dev)))
 
     # ------------------------------------------------------------ state
@@ -170,26 +235,41 @@ class BatchedSvdEngine:
     # ------------------------------------------------------------ events
     def row_append(self, x) -> None:
         b, m, n, *_ = self._h.shape()
-        src, dev = _event_array(x, (b, n), "appended row")
-        _lib.check(self._h.lib.isvd_engine_row_append(self._h.h, _lib.vptr(src), int(dev)))
+        self._append(x, (b, n), "appended row", self._h.lib.isvd_engine_row_append)
 
     def col_append(self, y) -> None:
         b, m, n, *_ = self._h.shape()
-        src, dev = _event_array(y, (b, m), "appended column")
-        _lib.check(self._h.lib.isvd_engine_col_append(self._h.h, _lib.vptr(src), int(dev)))
+        self._append(y, (b, m), "appended column", self._h.lib.isvd_engine_col_append)
+
+    def _append(self, x, shape, name, fn) -> None:
+        if _is_device(x):
+            src = self._dev.check(x, "float64", shape, name)
+            self._dev.before()
+            _lib.check(fn(self._h.h, _lib.vptr(src), 1))
+            self._dev.after(src)
+            return
+        src, _ = _event_array(x, shape, name)
+        _lib.check(fn(self._h.h, _lib.vptr(src), 0))
 
     def rank_one_update(self, i, j, delta) -> None:
+        """Device tensors (int64 i, j; float64 delta) are bounds- and
+        finiteness-checked on the device: a rejected entry is applied as a
+        no-op and the next synchronising call raises ValueError."""
         b = self.batch
         if _is_device(i):
-            ii, jj, dd = i.contiguous(), j.contiguous(), delta.contiguous()
-            dev = 1
-        else:
-            ii = np.ascontiguousarray(np.asarray(i, dtype=np.int64).reshape(b))
-            jj = np.ascontiguousarray(np.asarray(j, dtype=np.int64).reshape(b))
-            dd = np.ascontiguousarray(np.asarray(delta, dtype=np.float64).reshape(b))
-            dev = 0
+            ii = self._dev.check(i, "int64", (b,), "row index")
+            jj = self._dev.check(j, "int64", (b,), "column index")
+            dd = self._dev.check(delta, "float64", (b,), "delta")
+            self._dev.before()
+            _lib.check(self._h.lib.isvd_engine_rank_one(self._h.h, _lib.vptr(ii), _lib.vptr(jj),
+                                                        _lib.vptr(dd), 1))
+            self._dev.after(ii, jj, dd)
+            return
+        ii = np.ascontiguousarray(np.asarray(i, dtype=np.int64).reshape(b))
+        jj = np.ascontiguousarray(np.asarray(j, dtype=np.int64).reshape(b))
+        dd = np.ascontiguousarray(np.asarray(delta, dtype=np.float64).reshape(b))
         _lib.check(self._h.lib.isvd_engine_rank_one(self._h.h, _lib.vptr(ii), _lib.vptr(jj),
-                                                    _lib.vptr(dd), dev))
+                                                    _lib.vptr(dd), 0))
 
     def refresh(self, store_reference: bool = False) -> None:
         _lib.check(self._h.lib.isvd_engine_refresh(self._h.h, int(bool(store_reference))))
@@ -246,10 +326,6 @@ def _is_device(x) -> bool:
 
 
 def _event_array(x, shape, name):
-    if _is_device(x):
-        if tuple(x.shape) != tuple(shape):
-            raise ValueError(f"{name} has shape {tuple(x.shape)}, expected {shape}")
-        return x.contiguous(), 1
     arr = np.asarray(x, dtype=np.float64)
     if arr.shape != tuple(shape):
         raise ValueError(f"{name} has shape {arr.shape}, expected {shape}")
@@ -279,6 +355,10 @@ class SvdEngine:
         self._h = _Handle(1, m, n, k, tol, reortho_guard, mc, nc, kc, stream)
         self.tol = float(tol)
         self.reortho_guard = bool(reortho_guard)
+        # the module constant is read when the engine is built, so a test can
+        # force the guard the way the reference's does (monkeypatching
+        # engine.REORTHO_THRESHOLD, tests/test_engine.py:309-323)
+        self.reortho_threshold = REORTHO_THRESHOLD
         _lib.check(self._h.lib.isvd_engine_init(self._h.h, _lib.dptr(a0), 0))
         self._version = 0
         self._cache: dict = {}

@@ -27,7 +27,7 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
-from .engine import _Handle, _event_array, _is_device
+from .engine import _DeviceInputs, _Handle, _event_array, _is_device
 from .linalg import SvdFactors
 
 
@@ -108,6 +108,10 @@ class ShardedSvdEngine:
                                                      C.cast(self._cb, C.c_void_p), None))
         self.row0 = int(row0)
         self.tol = float(tol)
+        self._dev = _DeviceInputs(self._h)
+        if on_dev:
+            src = self._dev.check(src, "float64", (m_loc, n), "a_local")
+            self._dev.before()
         self._check(self._h.lib.isvd_engine_init(self._h.h, _lib.vptr(src), int(on_dev)))
 
     def _check(self, rc):
@@ -204,10 +208,15 @@ class ShardedSvdEngine:
     # ------------------------------------------------------------ events
     def row_append(self, x) -> None:
         n = self.shape[1]
-        if not _is_device(x):
-            x = np.asarray(x, dtype=np.float64).reshape(1, -1)
-        src, dev = _event_array(x, (1, n), "appended row")
-        self._check(self._h.lib.isvd_engine_row_append(self._h.h, _lib.vptr(src), int(dev)))
+        if _is_device(x):
+            src = self._dev.check(x.reshape(1, -1), "float64", (1, n), "appended row")
+            self._dev.before()
+            self._check(self._h.lib.isvd_engine_row_append(self._h.h, _lib.vptr(src), 1))
+            self._dev.after(src)
+            return
+        x = np.asarray(x, dtype=np.float64).reshape(1, -1)
+        src, _ = _event_array(x, (1, n), "appended row")
+        self._check(self._h.lib.isvd_engine_row_append(self._h.h, _lib.vptr(src), 0))
 
     def col_append(self, y) -> None:
         """y: the full global column (length m_global); this rank uses its rows."""
@@ -216,14 +225,19 @@ class ShardedSvdEngine:
         if _is_device(y):
             if tuple(y.shape) not in ((m,), (1, m)):
                 raise ValueError(f"appended column has shape {tuple(y.shape)}, expected ({m},)")
-            part = y.reshape(-1)[r0:r0 + ml].contiguous().reshape(1, ml)
+            part = self._dev.check(y.reshape(-1)[r0:r0 + ml].reshape(1, ml), "float64", (1, ml),
+                                   "appended column")
+            self._dev.before()
+            self._check(self._h.lib.isvd_engine_col_append(self._h.h, _lib.vptr(part), 1))
+            self._dev.after(part)
+            return
         else:
             arr = np.asarray(y, dtype=np.float64).reshape(-1)
             if arr.shape != (m,):
                 raise ValueError(f"appended column has shape {arr.shape}, expected ({m},)")
             part = np.ascontiguousarray(arr[r0:r0 + ml]).reshape(1, ml)
-        src, dev = _event_array(part, (1, ml), "appended column")
-        self._check(self._h.lib.isvd_engine_col_append(self._h.h, _lib.vptr(src), int(dev)))
+        src, _ = _event_array(part, (1, ml), "appended column")
+        self._check(self._h.lib.isvd_engine_col_append(self._h.h, _lib.vptr(src), 0))
 
     def rank_one_update(self, i: int, j: int, delta: float) -> None:
         ii = np.array([int(i)], dtype=np.int64)

@@ -49,3 +49,83 @@ def sine_angle(q1, q2):
     q2 = np.asarray(q2)
     r = q2 - q1 @ (q1.T @ q2)
     return float(np.arcsin(min(1.0, np.linalg.norm(r, 2)))) if r.size else 0.0
+
+
+# --------------------------------------------------- reference trajectories
+# tests/golden/make_golden.py runs whole BASELINE streams through the
+# reference's own loop (svdstream.stream.run_simulation) and stores one row
+# per MetricsRecord: step, frob_error, evr, rank, refreshed, frob_opt,
+# frob_ratio, angle_ref, angle_opt (None -> NaN).
+SIM_TRAJ_RTOL = 1e-8  # north_star: metric trajectories within 1e-8 relative
+SIM_ANGLE_ATOL = 1e-6  # north_star: principal angles below 1e-6 rad
+
+
+def sim_array(records):
+    nan = lambda v: np.nan if v is None else float(v)
+    return np.array([[r.step, r.frob_error, r.evr, r.rank, float(r.refreshed), nan(r.frob_opt),
+                      nan(r.frob_ratio), nan(r.angle_ref), nan(r.angle_opt)] for r in records])
+
+
+def check_sim(golden, tag, got, n=None):
+    """Compare a trajectory (prefix of length n) with the reference's."""
+    ref = golden[f"sim_{tag}_records"]
+    if n is not None:
+        ref = ref[:n]
+    assert got.shape == ref.shape, (got.shape, ref.shape)
+    # step, rank and refresh flags exactly
+    np.testing.assert_array_equal(got[:, [0, 3, 4]], ref[:, [0, 3, 4]])
+    for c in (1, 2, 5, 6):  # frob_error, evr, frob_opt, frob_ratio
+        ok = ~np.isnan(ref[:, c])
+        np.testing.assert_array_equal(np.isnan(got[:, c]), ~ok, err_msg=f"column {c} NaN pattern")
+        np.testing.assert_allclose(got[ok, c], ref[ok, c], rtol=SIM_TRAJ_RTOL, atol=1e-300,
+                                   err_msg=f"column {c}")
+    for c in (7, 8):  # angle_ref, angle_opt (arccos-based, as the reference)
+        ok = ~np.isnan(ref[:, c])
+        np.testing.assert_array_equal(np.isnan(got[:, c]), ~ok, err_msg=f"column {c} NaN pattern")
+        if ok.any():
+            assert np.max(np.abs(got[ok, c] - ref[ok, c])) < SIM_ANGLE_ATOL, f"column {c}"
+
+
+def decode_events(kinds, vecs, m, n):
+    """Inverse of make_golden._encode_events."""
+    ev, off = [], 0
+    for k, i, j, d in kinds:
+        if k == 0:
+            ev.append(("row", vecs[off:off + n]))
+            off += n
+            m += 1
+        elif k == 1:
+            ev.append(("col", vecs[off:off + m]))
+            off += m
+            n += 1
+        else:
+            ev.append(("rank1", int(i), int(j), float(d)))
+    return ev
+
+
+def sim_inputs(golden, tag):
+    """(a0, events, k, policy kwargs, log_every) of a stored reference run,
+    regenerated from the same seeded workloads as make_golden.py."""
+    from paper_2605_24514_b200 import workloads
+
+    if tag == "cfg1":
+        a0, ev, _ = workloads.cfg1(0, n_events=1000)
+        return a0, ev, 10, dict(kind="periodic", period=100), 1
+    if tag == "cfg2":
+        a0, ev, _ = workloads.cfg2(0, n_events=2000)
+        return a0, ev, 20, dict(kind="error", gamma=1.05, min_spacing=0), 1
+    if tag == "cfg3":
+        a0, ev, _ = workloads.cfg3(0)
+        return a0, ev, 5, dict(kind="angle", theta_max=float(np.deg2rad(5.0))), 1
+    if tag in ("cfg4r", "cfg4b"):
+        a0, ev, _ = workloads.cfg4(0, m=400, n=120, rank=64, n_blocks=200)
+        if tag == "cfg4r":
+            return a0, ev, 64, dict(kind="periodic", period=200,
+                                    adaptive=dict(tau=0.95, k_min=1, k_max=128, eta=0.5)), 50
+        return a0, ev[:600], 12, dict(kind="periodic", period=150,
+                                      adaptive=dict(tau=0.99, k_min=4, k_max=40, eta=0.05)), 25
+    if tag == "guard":
+        a0 = golden["sim_guard_a0"]
+        ev = decode_events(golden["sim_guard_kinds"], golden["sim_guard_vecs"], *a0.shape)
+        return a0, ev, 6, dict(kind="periodic", period=80), 10
+    raise KeyError(tag)

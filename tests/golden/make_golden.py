@@ -53,6 +53,33 @@ def _import_reference():
     return svdstream
 
 
+def _mixed_stream(g, m, n, count):
+    """Random mix: 10 % row appends, 10 % column appends, 80 % rank-1."""
+    ev = []
+    for _ in range(count):
+        kind = int(g.integers(10))
+        if kind == 0:
+            ev.append(("row", g.standard_normal(n)))
+            m += 1
+        elif kind == 1:
+            ev.append(("col", g.standard_normal(m)))
+            n += 1
+        else:
+            ev.append(("rank1", int(g.integers(m)), int(g.integers(n)), float(g.normal(0, 0.05))))
+    return ev
+
+
+def _encode_events(ev):
+    kinds, vecs = [], []
+    for e in ev:
+        if e[0] == "rank1":
+            kinds.append([2, e[1], e[2], e[3]])
+        else:
+            kinds.append([0 if e[0] == "row" else 1, 0, 0, 0.0])
+            vecs.append(e[1])
+    return np.array(kinds, dtype=np.float64), np.concatenate(vecs) if vecs else np.zeros(0)
+
+
 def main():
     sv = _import_reference()
     from svdstream import backend
@@ -139,47 +166,84 @@ def main():
         out[f"traj_{tag}_vt"] = f.vt
         out[f"traj_{tag}_sq_norm"] = np.array(eng.sq_norm)
 
-    a0, ev, _ = workloads.cfg1(0, n_events=120)
-    trajectory(a0, ev, 10, "cfg1", "periodic", period=100)
+    # ---- whole BASELINE streams through the reference's OWN loop
+    # (stream.run_simulation, stream.py:257-333), fed our seeded inputs by
+    # replacing its two generator hooks (gen_low_rank, build_events).
+    import svdstream.engine as ref_engine
+    import svdstream.stream as S
+    from svdstream.policies import AdaptiveRankConfig, PolicyConfig
 
-    a0, ev, _ = workloads.cfg2(0, n_events=60)
-    trajectory(a0, ev, 20, "cfg2", "error", gamma=1.05)
+    def simulate(tag, a0, events, k, policy, log_every, reortho_guard=False):
+        ref_events = [S.RowAppend(e[1]) if e[0] == "row" else S.ColAppend(e[1]) if e[0] == "col"
+                      else S.RankOneUpdate(e[1], e[2], e[3]) for e in events]
+        gen0, build0 = S.gen_low_rank, S.build_events
+        S.gen_low_rank = lambda *a, **kw: np.array(a0, dtype=np.float64, copy=True)
+        S.build_events = lambda spec: ref_events
+        try:
+            spec = S.StreamSpec(m=a0.shape[0], n=a0.shape[1], true_rank=1, k=k,
+                                events=len(events), policy=policy, log_every=log_every,
+                                reortho_guard=reortho_guard)
+            recs, eng = S.run_simulation(spec, return_engine=True)
+        finally:
+            S.gen_low_rank, S.build_events = gen0, build0
+        nan = lambda v: np.nan if v is None else float(v)
+        out[f"sim_{tag}_records"] = np.array(
+            [[r.step, r.frob_error, r.evr, r.rank, float(r.refreshed), nan(r.frob_opt),
+              nan(r.frob_ratio), nan(r.angle_ref), nan(r.angle_opt)] for r in recs])
+        f = eng.factors
+        out[f"sim_{tag}_s"] = f.s
+        out[f"sim_{tag}_u"] = f.u
+        out[f"sim_{tag}_vt"] = f.vt
+        out[f"sim_{tag}_sq_norm"] = np.array(eng.sq_norm)
+        r = out[f"sim_{tag}_records"]
+        print(f"  {tag}: {len(recs)} records, refreshes {int(np.nansum(r[:, 4]))}, "
+              f"ranks {sorted(set(r[:, 3].astype(int).tolist()))}")
 
-    a0, ev, _ = workloads.cfg3(0, t_total=352)
-    trajectory(a0, ev, 5, "cfg3", "angle", theta=float(np.deg2rad(5.0)))
+    # config 1: all 1000 row appends, periodic 100, oracle every tick
+    a0, ev, _ = workloads.cfg1(0, n_events=1000)
+    simulate("cfg1", a0, ev, 10, PolicyConfig(kind="periodic", period=100), 1)
+    # config 2: 2000 of the 10,000 rank-1 updates, error trigger 1.05, oracle every tick
+    a0, ev, _ = workloads.cfg2(0, n_events=2000)
+    simulate("cfg2", a0, ev, 20, PolicyConfig(kind="error", gamma=1.05, min_spacing=0), 1)
+    # config 3: all 2268 daily appends, angle trigger 5 deg, oracle every tick
+    a0, ev, _ = workloads.cfg3(0)
+    simulate("cfg3", a0, ev, 5, PolicyConfig(kind="angle", theta_max=float(np.deg2rad(5.0))), 1)
+    # config 4 at reduced size, same code path: sigma_i = 0.9^i rank 64, 5 rows : 1 col,
+    # k0 = 64, adaptive rank (EVR 0.95, k_max 128, novelty eta 0.5), periodic refresh 200,
+    # oracle every 50 ticks (4 observations per refresh for the two-step hysteresis)
+    a0, ev, _ = workloads.cfg4(0, m=400, n=120, rank=64, n_blocks=200)
+    simulate("cfg4r", a0, ev, 64,
+             PolicyConfig(kind="periodic", period=200,
+                          adaptive=AdaptiveRankConfig(tau=0.95, k_min=1, k_max=128, eta=0.5)), 50)
+    # the same with a rank floor high enough for the novelty bump to fire
+    simulate("cfg4b", a0, ev[:600], 12,
+             PolicyConfig(kind="periodic", period=150,
+                          adaptive=AdaptiveRankConfig(tau=0.99, k_min=4, k_max=40, eta=0.05)), 25)
+    # reortho guard forced on every tick (tests/test_engine.py:309-323 monkeypatches the
+    # threshold the same way), on the mixed stream below
+    guard_events = _mixed_stream(np.random.default_rng(13), 40, 30, 240)
+    thr0 = ref_engine.REORTHO_THRESHOLD
+    ref_engine.REORTHO_THRESHOLD = -1.0
+    try:
+        g0 = np.random.default_rng(14).standard_normal((40, 30))
+        out["sim_guard_a0"] = g0
+        out["sim_guard_kinds"], out["sim_guard_vecs"] = _encode_events(guard_events)
+        simulate("guard", g0, guard_events, 6, PolicyConfig(kind="periodic", period=80), 10,
+                 reortho_guard=True)
+    finally:
+        ref_engine.REORTHO_THRESHOLD = thr0
 
     # mixed small stream: rows, cols, rank-1 (tests/test_engine.py:290-306 shape)
     g = np.random.default_rng(12)
     a0 = g.standard_normal((30, 25))
-    m, n = 30, 25
-    ev = []
-    for t in range(300):
-        kind = int(g.integers(10))
-        if kind == 0:
-            ev.append(("row", g.standard_normal(n)))
-            m += 1
-        elif kind == 1:
-            ev.append(("col", g.standard_normal(m)))
-            n += 1
-        else:
-            ev.append(("rank1", int(g.integers(m)), int(g.integers(n)), float(g.normal(0, 0.05))))
+    ev = _mixed_stream(g, 30, 25, 300)
     out["traj_mixed_a0"] = a0
-    kinds = []
-    vecs = []
-    for e in ev:
-        if e[0] == "rank1":
-            kinds.append([2, e[1], e[2], e[3]])
-            vecs.append(np.zeros(0))
-        else:
-            kinds.append([0 if e[0] == "row" else 1, 0, 0, 0.0])
-            vecs.append(e[1])
-    out["traj_mixed_kinds"] = np.array(kinds, dtype=np.float64)
-    out["traj_mixed_vecs"] = np.concatenate(vecs)
+    out["traj_mixed_kinds"], out["traj_mixed_vecs"] = _encode_events(ev)
     trajectory(a0, ev, 6, "mixed")
 
-    # ---- 5a streams (two sampled streams, first 64 events)
+    # ---- 5a streams (two sampled streams, all 1024 events)
     for b in (0, 1):
-        a0, ev = workloads.cfg5a_stream(0, b, n_events=64)
+        a0, ev = workloads.cfg5a_stream(0, b, n_events=1024)
         eng = SvdEngine(a0, 32)
         for e in ev:
             if e[0] == "row":

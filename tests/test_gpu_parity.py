@@ -11,7 +11,7 @@ import ctypes as C
 import numpy as np
 import pytest
 
-from conftest import rel_err, sine_angle
+from conftest import check_sim, rel_err, sim_array, sim_inputs, sine_angle
 from oracle import OracleEngine, kernel_rank_one, kernel_row_append, core_svd_jacobi
 from paper_2605_24514_b200 import BatchedSvdEngine, SvdEngine, _lib, workloads
 from paper_2605_24514_b200.metrics import (angle_to_opt, collect, compute_oracle, error_ratio,
@@ -167,6 +167,7 @@ def _check(golden, tag, recs, eng):
     ok = ~np.isnan(ref[:, 5])
     np.testing.assert_array_equal(np.isnan(recs[:, 5]), ~ok)
     np.testing.assert_allclose(recs[ok, 5], ref[ok, 5], rtol=TRAJ_RTOL)
+    assert np.max(np.abs(recs[:, 6] - ref[:, 6])) < ANGLE_TOL  # angle_opt
     f = eng.factors
     np.testing.assert_allclose(f.s, golden[f"traj_{tag}_s"], rtol=SIGMA_RTOL)
     assert sine_angle(f.u, golden[f"traj_{tag}_u"]) < ANGLE_TOL
@@ -175,22 +176,34 @@ def _check(golden, tag, recs, eng):
     assert abs(eng.sq_norm - float(golden[f"traj_{tag}_sq_norm"])) <= 1e-12 * eng.sq_norm
 
 
-def test_golden_cfg1(golden):
-    a0, ev, _ = workloads.cfg1(0, n_events=120)
-    recs, eng = _run_traj(a0, ev, 10, "periodic", period=100)
-    _check(golden, "cfg1", recs, eng)
+# whole BASELINE streams through the product loop (stream.run_stream) vs the
+# reference's own run_simulation on the same inputs (make_golden.py): cfg1
+# (1000 appends), cfg2 (2000 rank-1 updates, error trigger), cfg3 (all 2268
+# daily appends, angle trigger), config 4 at reduced size with the adaptive
+# rank policy (EVR selection, hysteresis, armed rank at refresh; and a
+# variant where the novelty bump fires), and the reortho guard forced on
+# every tick.
+@pytest.mark.parametrize("tag", ["cfg1", "cfg2", "cfg3", "cfg4r", "cfg4b", "guard"])
+def test_reference_loop_trajectory(golden, tag, monkeypatch):
+    import paper_2605_24514_b200.engine as E
+    from paper_2605_24514_b200.policies import AdaptiveRankConfig, PolicyConfig
+    from paper_2605_24514_b200.stream import run_stream
 
-
-def test_golden_cfg2(golden):
-    a0, ev, _ = workloads.cfg2(0, n_events=60)
-    recs, eng = _run_traj(a0, ev, 20, "error", gamma=1.05)
-    _check(golden, "cfg2", recs, eng)
-
-
-def test_golden_cfg3(golden):
-    a0, ev, _ = workloads.cfg3(0, t_total=352)
-    recs, eng = _run_traj(a0, ev, 5, "angle", theta=float(np.deg2rad(5.0)))
-    _check(golden, "cfg3", recs, eng)
+    a0, ev, k, pol, log_every = sim_inputs(golden, tag)
+    guard = tag == "guard"
+    if guard:  # as the reference's tests/test_engine.py:309-311
+        monkeypatch.setattr(E, "REORTHO_THRESHOLD", -1.0)
+    ad = pol.pop("adaptive", None)
+    policy = PolicyConfig(**pol, adaptive=AdaptiveRankConfig(**ad) if ad else None)
+    recs, eng = run_stream(a0, workloads.to_stream_events(ev), k, policy, log_every,
+                           reortho_guard=guard, return_engine=True)
+    check_sim(golden, tag, sim_array(recs))
+    f = eng.factors
+    np.testing.assert_allclose(f.s, golden[f"sim_{tag}_s"], rtol=SIGMA_RTOL)
+    assert sine_angle(f.u, golden[f"sim_{tag}_u"]) < ANGLE_TOL
+    assert sine_angle(f.vt.T, golden[f"sim_{tag}_vt"].T) < ANGLE_TOL
+    np.testing.assert_allclose(f.u, golden[f"sim_{tag}_u"], atol=1e-7)  # canonical signs
+    assert abs(eng.sq_norm - float(golden[f"sim_{tag}_sq_norm"])) <= 1e-12 * eng.sq_norm
 
 
 def test_golden_mixed(golden):
@@ -201,36 +214,74 @@ def test_golden_mixed(golden):
 
 
 # ------------------------------------------------------------- batched 5a
-def test_cfg5a_batched_matches_oracle(golden):
-    """8 sampled streams, 64 interleaved events each, through the batched
-    engine vs one oracle engine per stream; streams 0 and 1 also against the
-    reference's own golden output."""
-    B, T = 8, 64
-    a0, ticks, streams = workloads.cfg5a_batch(0, B, n_events=T)
-    eng = BatchedSvdEngine(a0, 32, m_cap=1024 + T)
+def _oracle_stream(a0, events, k):
+    oe = OracleEngine(a0, k)
+    for e in events:
+        if e[0] == "row":
+            oe.row_append(e[1])
+        else:
+            oe.rank_one_update(e[1], e[2], e[3])
+    return oe
+
+
+def _run_batched(eng, ticks):
     for tk in ticks:
         if tk[0] == "row":
             eng.row_append(tk[1])
         else:
             eng.rank_one_update(tk[1], tk[2], tk[3])
+
+
+def test_cfg5a_batched_matches_oracle():
+    """8 streams, 64 interleaved events each, through the batched engine vs
+    one oracle engine per stream."""
+    B, T = 8, 64
+    a0, ticks, streams = workloads.cfg5a_batch(0, B, n_events=T)
+    eng = BatchedSvdEngine(a0, 32, m_cap=1024 + T)
+    _run_batched(eng, ticks)
     for b in range(B):
-        oe = OracleEngine(streams[b][0], 32)
-        for e in streams[b][1]:
-            if e[0] == "row":
-                oe.row_append(e[1])
-            else:
-                oe.rank_one_update(e[1], e[2], e[3])
+        oe = _oracle_stream(*streams[b], 32)
         f = eng.factors(b)
         assert rel_err(f.s, oe.factors.s) < SIGMA_RTOL
         assert sine_angle(f.u, oe.factors.u) < ANGLE_TOL
         assert sine_angle(f.vt.T, oe.factors.vt.T) < ANGLE_TOL
         assert np.array_equal(eng.tracked(b), oe.tracked)
-        if b < 2:
-            assert rel_err(f.s, golden[f"s5a_{b}_s"]) < SIGMA_RTOL
-            np.testing.assert_allclose(f.u[:64], golden[f"s5a_{b}_u"], atol=1e-8)
     sq, rho, xn = eng.scalars()
     for b in range(B):
         assert abs(sq[b] - float(np.sum(eng.tracked(b) ** 2))) <= 1e-12 * sq[b]
+
+
+def test_cfg5a_benchmarked_configuration(golden):
+    """The exact path bench.py times: config 5a shape (1024 x 256, rank 32,
+    k = 32, all 1024 alternating events) on a 512-stream batch, so the
+    deferred right basis (B >= 64) and the four run-ahead stream groups
+    (B >= 512) are on, with the default deferred-U window.  Eight sampled
+    streams are replayed through the oracle (sigma 1e-9, sine angles 1e-6,
+    tracked matrix and N bit-exact / 1e-12); streams 0 and 1 also against the
+    reference's own 1024-event output."""
+    B, T = 512, 1024
+    a0, ticks, streams = workloads.cfg5a_batch(0, B, n_events=T)
+    eng = BatchedSvdEngine(a0, 32, m_cap=1024 + T // 2 + 1, k_cap=32)
+    del a0
+    _run_batched(eng, ticks)
+    eng.flush()
+    assert eng.shape == (1536, 256)
+    sq, _, _ = eng.scalars()
+    for b in (0, 1, 63, 64, 127, 255, 256, 383, 384, 511):
+        oe = _oracle_stream(*streams[b], 32)
+        f = eng.factors(b)
+        assert rel_err(f.s, oe.factors.s) < SIGMA_RTOL, b
+        assert sine_angle(f.u, oe.factors.u) < ANGLE_TOL, b
+        assert sine_angle(f.vt.T, oe.factors.vt.T) < ANGLE_TOL, b
+        np.testing.assert_allclose(f.u, oe.factors.u, atol=1e-8)  # canonical signs
+        assert np.array_equal(eng.tracked(b), oe.tracked), b
+        assert abs(sq[b] - oe.sq_norm) <= 1e-12 * oe.sq_norm, b
+        if b < 2:
+            assert rel_err(f.s, golden[f"s5a_{b}_s"]) < SIGMA_RTOL
+            assert sine_angle(f.vt.T, golden[f"s5a_{b}_vt"].T) < ANGLE_TOL
+            np.testing.assert_allclose(f.u[:64], golden[f"s5a_{b}_u"], atol=1e-8)
+    du, dv = eng.ortho_defect()
+    assert np.all(du <= 1e-10) and np.all(dv <= 1e-10)
 
 
 def test_cfg5a_full_length_properties():

@@ -5,9 +5,10 @@ kernel backends).  CPU only."""
 import numpy as np
 import pytest
 
-from conftest import rel_err, sine_angle
-from oracle import (OracleEngine, collect, compute_oracle, core_svd_jacobi, core_svd_lapack,
-                    error_ratio, frob_error, angle_to_opt, kernel_rank_one, kernel_row_append)
+from conftest import check_sim, rel_err, sim_array, sim_inputs, sine_angle
+from oracle import (AdaptiveRankConfig, OracleEngine, PolicyConfig, angle_to_opt, collect,
+                    compute_oracle, core_svd_jacobi, core_svd_lapack, error_ratio, frob_error,
+                    kernel_rank_one, kernel_row_append, run_stream)
 from paper_2605_24514_b200 import workloads
 
 CORES = ["rand1", "rand2", "rand5", "rand9", "rand16", "rand33", "dead", "brand33"]
@@ -75,27 +76,41 @@ def _check_traj(golden, tag, recs, eng):
     ok = ~np.isnan(ref[:, 5])
     np.testing.assert_array_equal(np.isnan(recs[:, 5]), ~ok)
     np.testing.assert_allclose(recs[ok, 5], ref[ok, 5], rtol=1e-8)
+    assert np.max(np.abs(recs[:, 6] - ref[:, 6])) < 1e-6
     np.testing.assert_allclose(eng.factors.s, golden[f"traj_{tag}_s"], rtol=1e-9)
     assert sine_angle(eng.factors.u, golden[f"traj_{tag}_u"]) < 1e-6
     assert abs(eng.sq_norm - float(golden[f"traj_{tag}_sq_norm"])) <= 1e-12 * eng.sq_norm
 
 
-def test_cfg1_trajectory(golden):
-    a0, ev, _ = workloads.cfg1(0, n_events=120)
-    recs, eng = _trajectory(a0, ev, 10, "periodic", period=100)
-    _check_traj(golden, "cfg1", recs, eng)
+# whole-stream trajectories through the reference's own loop
+# (stream.py:257-333); cfg2's oracle is a 1000 x 500 SVD per tick, so the CPU
+# suite checks a prefix of it (the GPU suite runs all of it)
+SIM_PREFIX = {"cfg1": None, "cfg2": 150, "cfg3": None, "cfg4r": None, "cfg4b": None,
+              "guard": None}
 
 
-def test_cfg2_trajectory(golden):
-    a0, ev, _ = workloads.cfg2(0, n_events=60)
-    recs, eng = _trajectory(a0, ev, 20, "error", gamma=1.05)
-    _check_traj(golden, "cfg2", recs, eng)
+@pytest.mark.parametrize("tag", list(SIM_PREFIX))
+def test_oracle_matches_reference_loop(golden, tag, monkeypatch):
+    import oracle.isvd_oracle as O
 
-
-def test_cfg3_trajectory(golden):
-    a0, ev, _ = workloads.cfg3(0, t_total=352)
-    recs, eng = _trajectory(a0, ev, 5, "angle", theta=float(np.deg2rad(5.0)))
-    _check_traj(golden, "cfg3", recs, eng)
+    a0, ev, k, pol, log_every = sim_inputs(golden, tag)
+    n = SIM_PREFIX[tag]
+    if n is not None:
+        ev = ev[:n - 1]
+    guard = tag == "guard"
+    if guard:  # tests/test_engine.py:309-311
+        monkeypatch.setattr(O, "REORTHO_THRESHOLD", -1.0)
+    ad = pol.pop("adaptive", None)
+    policy = PolicyConfig(**pol, adaptive=AdaptiveRankConfig(**ad) if ad else None)
+    eng = OracleEngine(a0, k, reortho_guard=guard)
+    recs = run_stream(eng, ev, policy, log_every)
+    check_sim(golden, tag, sim_array(recs), n)
+    if n is None:
+        f = eng.factors
+        np.testing.assert_allclose(f.s, golden[f"sim_{tag}_s"], rtol=1e-9)
+        assert sine_angle(f.u, golden[f"sim_{tag}_u"]) < 1e-6
+        assert sine_angle(f.vt.T, golden[f"sim_{tag}_vt"].T) < 1e-6
+        assert abs(eng.sq_norm - float(golden[f"sim_{tag}_sq_norm"])) <= 1e-12 * eng.sq_norm
 
 
 def _mixed_events(golden):
@@ -124,7 +139,7 @@ def test_mixed_trajectory(golden):
 
 @pytest.mark.parametrize("b", [0, 1])
 def test_cfg5a_streams(golden, b):
-    a0, ev = workloads.cfg5a_stream(0, b, n_events=64)
+    a0, ev = workloads.cfg5a_stream(0, b, n_events=1024)
     eng = OracleEngine(a0, 32)
     for e in ev:
         if e[0] == "row":
