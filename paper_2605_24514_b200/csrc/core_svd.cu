@@ -193,13 +193,13 @@ __global__ void jacobi_core_kernel(int s, const double* __restrict__ core, int64
 // stable sort).  Rotation formulas and threshold as _kernels.pyx:38-57.  V
 // is rotated once per sweep from a shared-memory (c, s) log (row layout).
 constexpr int kJ32Warps = 4;
-// Sweep exit: once every rotation of a sweep had |a_pq| <= kConvRel
+// Rank-1 sweep exit: once every rotation of a sweep had |a_pq| <= kConvRel
 // sqrt(a_pp a_qq), the off-diagonal left is O(kConvRel^2) relative (cyclic
-// Jacobi converges quadratically): sigma is then exact to O(1e-24) and the
-// vectors to O(1e-12 / relative gap), far inside the parity bar (sigma 1e-9,
-// angles 1e-6).  Brand rank-1 cores diag(s) + delta a b^T start with
-// off-diagonals ~1e-5 relative, so one sweep suffices (measured 1.00
-// sweeps/core on config 5a; 1.97 with kConvRel = 1e-8).
+// Jacobi converges quadratically) and one first-order simultaneous step
+// (j32_polish) takes it below the reference's 1e-14 stop; Brand rank-1
+// cores diag(s) + delta a b^T start with off-diagonals ~1e-5 relative, so
+// one sweep suffices.  Generic cores (functional core_svd, angles, guard)
+// sweep until a sweep makes no rotation, as _kernels.pyx:38-59.
 constexpr double kConvRel = 1e-6;
 
 // 1/sqrt(x) to ~1 ulp: MUFU.RSQ64H seed + two Newton steps (x > 0, normal)
@@ -240,6 +240,119 @@ __device__ __forceinline__ void j32_apply_v(double (&v)[32], const double2* log)
       v[2 * k + 2] = r.x * vp - r.y * vq;
     }
   }
+}
+
+// First-order simultaneous Jacobi step (the finishing step of a one-sweep
+// rank-1 core).  After a sweep whose rotations were all small the columns of
+// G are orthogonal to O(1e-12) relative, not to the reference's 1e-14 stop
+// (_kernels.pyx:38-57 keeps sweeping: one more sweep of tiny rotations and a
+// check sweep).  With the Gram M = G^T G the rotation every pair (p, q)
+// would get is, to first order, theta_pq = M_pq / (M_qq - M_pp); applying
+// all of them at once, G <- G (I + Theta) (Theta skew), leaves off-diagonals
+// O(theta^2) and departs from orthogonality by O(theta^2) -- below 1e-14
+// when every |theta| <= 1e-7.  Both products run on the FP64 tensor path
+// (DMMA.8x8x4: 80 for the upper half of M, 128 for G Theta); theta is formed
+// in the accumulator layout, so shared memory is touched only to stage G
+// (gs, XOR-swizzled rows) and -- once the step is known to apply -- to pass
+// Theta and G Theta between layouts (ws).  Returns 0 if G already meets the
+// reference's stop (|M_pq| <= 1e-14 sqrt(M_pp M_qq) for every pair: G
+// unchanged), 1 after the step, -1 (ws untouched, G unchanged) if some theta
+// is too large for a first-order step (nearly equal columns).
+__device__ __forceinline__ int j32_polish(double (&x)[32], double* gs, double* ws, double* dg,
+                                          int lane, double null2) {
+  auto T = [&](double* t, int i, int j) -> double& { return t[i * 32 + (j ^ ((i & 1) << 3))]; };
+  const int g = lane >> 2, qd = lane & 3;
+  double n4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    T(gs, i, lane) = x[i];
+    n4[i & 3] = fma(x[i], x[i], n4[i & 3]);
+  }
+  dg[lane] = (n4[0] + n4[1]) + (n4[2] + n4[3]);
+  __syncwarp();
+  // M tile (mi, ni), mi <= ni: A = G^T rows 8mi.., B = G columns 8ni..; both
+  // fragments are G(4kk + qd, 8t + g).  acc -> theta in place.
+  double th[10][2];
+#pragma unroll
+  for (int t = 0; t < 10; ++t) th[t][0] = th[t][1] = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    double f[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) f[t] = T(gs, 4 * kk + qd, 8 * t + g);
+    int idx = 0;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = mi; ni < 4; ++ni, ++idx) dmma_8x8x4(th[idx][0], th[idx][1], f[mi], f[ni]);
+  }
+  bool viol = false;
+  double tmax = 0.0;
+  {
+    int idx = 0;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = mi; ni < 4; ++ni, ++idx)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = 8 * mi + g, c = 8 * ni + 2 * qd + e;
+          const double dr = dg[r], dc = dg[c], mrc = th[idx][e];
+          const bool live = r != c && dr > null2 && dc > null2;
+          viol |= live && mrc * mrc > (kOrthoEps * kOrthoEps) * (dr * dc);
+          const double t = live ? mrc * j32_rcp(dc - dr) : 0.0;  // theta_rc
+          tmax = fmax(tmax, (t - t == 0.0) ? fabs(t) : 1e300);  // inf / NaN: fail
+          th[idx][e] = t;
+        }
+  }
+  if (!__any_sync(0xffffffffu, viol)) return 0;
+  if (warp_max(tmax) > 1e-7) return -1;
+  {
+    int idx = 0;
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = mi; ni < 4; ++ni, ++idx) {
+        const int r = 8 * mi + g, c = 8 * ni + 2 * qd;
+        *reinterpret_cast<double2*>(&T(ws, r, c)) = make_double2(th[idx][0], th[idx][1]);
+        if (mi != ni) {  // theta is skew
+          T(ws, c, r) = -th[idx][0];
+          T(ws, c + 1, r) = -th[idx][1];
+        }
+      }
+  }
+  __syncwarp();
+  // G Theta: A = G rows 8mi.. (G(8mi + g, 4kk + qd)), B = Theta rows 4kk..
+  double d[4][4][2];
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) d[mi][ni][0] = d[mi][ni][1] = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    double a[4], b[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      a[t] = T(gs, 8 * t + g, 4 * kk + qd);
+      b[t] = T(ws, 4 * kk + qd, 8 * t + g);
+    }
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(d[mi][ni][0], d[mi][ni][1], a[mi], b[ni]);
+  }
+  __syncwarp();  // every lane has read Theta
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+      *reinterpret_cast<double2*>(&T(ws, 8 * mi + g, 8 * ni + 2 * qd)) =
+          make_double2(d[mi][ni][0], d[mi][ni][1]);
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 32; ++i) x[i] = T(gs, i, lane) + T(ws, i, lane);
+  __syncwarp();
+  return 1;
 }
 
 // Per-warp shared state: the (c, s) log of one sweep (32 rounds x 16 pairs)
@@ -447,35 +560,38 @@ __global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32c_kernel(
       j32c_round<true>(x, lane, W.log + (2 * rr + 1) * 16, nrm, any, relmax, null2);
     }
     __syncwarp();
-    const bool done =
-        !__any_sync(0xffffffffu, any) || warp_max((double)relmax) <= kConvRel * kConvRel;
-    // One-sweep rank-1 cores of moderate condition: the right vectors follow
-    // from the structure instead of replaying the sweep's rotations on V:
-    // G = K V = U Sigma, so v = K^T g / sigma^2 with K^T g = s o g +
-    // delta b (a . g) (O(s^2) per core; error ~ eps sigma_max / sigma, kept
-    // to <= 1e-13 by the condition bound)
+    const bool rotated = __any_sync(0xffffffffu, any);
+    // generic cores -- and rank-1 cores off the fast path -- stop exactly as
+    // the reference: after a sweep without a rotation (_kernels.pyx:38-59)
+    bool done = !rotated;
+    // One-sweep rank-1 cores of moderate condition (every rotation of the
+    // first sweep below kConvRel, sigma_max / sigma_min <= 100): the
+    // finishing step (j32_polish) brings G to the reference's stop, and the
+    // right vectors follow from the structure instead of replaying the
+    // sweep's rotations on V: G = K V = U Sigma, so v = K^T g / sigma^2 with
+    // K^T g = s o g + delta b (a . g) (O(s^2) per core; error ~ eps
+    // sigma_max / sigma_min per tick with G orthogonal to working precision).
     bool formula = false;
     if constexpr (BUILD) {
-      if (done && sweeps == 0) {
+      if (rotated && sweeps == 0 && warp_max((double)relmax) <= kConvRel * kConvRel) {
         const double n2 = col_norm();
         const bool live_col = (31 - lane) < s;  // one sweep reverses the positions
         const double mx = warp_max(live_col ? n2 : 0.0);
         const double mn = -warp_max(live_col ? -n2 : -1e300);
-        formula = mn >= 1e-6 * mx && mx > 0.0;
-        if (formula) {
-          double* kv = reinterpret_cast<double*>(W.log);  // [a | b | s] (the log is not needed)
-          kv[lane] = ka;
-          kv[32 + lane] = kb;
-          kv[64 + lane] = ks;
-          __syncwarp();
-          double d4[4] = {0.0, 0.0, 0.0, 0.0};
+        if (mn >= 1e-4 * mx && mx > 0.0) {
+          // V's tile (identity so far) holds the staged G; the log is the scratch
+          const int pol = j32_polish(x, &W.V[0][0], reinterpret_cast<double*>(W.log), W.nrm,
+                                     lane, null2);
+          if (pol >= 0) {
+            formula = true;
+            done = true;
+          } else {
+            // nearly equal columns: V's tile back to the identity (the log is
+            // intact), replay this sweep and keep sweeping
 #pragma unroll
-          for (int i = 0; i < 32; ++i) d4[i & 3] = fma(kv[i], x[i], d4[i & 3]);
-          const double dot = kdel * ((d4[0] + d4[1]) + (d4[2] + d4[3]));
-          const double in2 = live_col ? 1.0 / n2 : 0.0;
-#pragma unroll
-          for (int k = 0; k < 32; ++k) W.V[k][lane] = fma(kv[64 + k], x[k], kv[32 + k] * dot) * in2;
-          __syncwarp();
+            for (int r2 = 0; r2 < 32; ++r2) W.V[lane][r2] = (lane == r2 && lane < s) ? 1.0 : 0.0;
+            __syncwarp();
+          }
         }
       }
     }
@@ -486,6 +602,23 @@ __global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32c_kernel(
       j32_apply_v(v, W.log);
 #pragma unroll
       for (int j = 0; j < 32; ++j) W.V[lane][j] = v[j];
+    }
+    if (formula) {
+      const double n2 = col_norm();
+      const bool live_col = (31 - lane) < s;
+      double* kv = reinterpret_cast<double*>(W.log);  // [a | b | s] (the log is not needed)
+      kv[lane] = ka;
+      kv[32 + lane] = kb;
+      kv[64 + lane] = ks;
+      __syncwarp();
+      double d4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int i = 0; i < 32; ++i) d4[i & 3] = fma(kv[i], x[i], d4[i & 3]);
+      const double dot = kdel * ((d4[0] + d4[1]) + (d4[2] + d4[3]));
+      const double in2 = live_col ? 1.0 / n2 : 0.0;
+      __syncwarp();  // every lane's reads of the staged G are done before V's tile is written
+#pragma unroll
+      for (int k = 0; k < 32; ++k) W.V[k][lane] = fma(kv[64 + k], x[k], kv[32 + k] * dot) * in2;
     }
     __syncwarp();
     ++sweeps;

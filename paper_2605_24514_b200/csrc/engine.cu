@@ -23,6 +23,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 #include "common.cuh"
@@ -87,6 +89,37 @@ static int check_device() {
     pool_set = true;
   }
   return ISVD_OK;
+}
+
+// Work streams (the engine stream and the stream groups) come from a
+// process-wide pool per device and return to it when an engine is destroyed,
+// instead of being destroyed: a caller that passed device payloads may still
+// have its caching allocator record events on the streams that read them
+// (isvd_engine_streams, Tensor.record_stream) after the engine is gone.
+// An engine synchronises its streams before returning them.
+static std::mutex g_pool_mu;
+static std::map<int, std::vector<cudaStream_t>> g_pool;
+static cudaError_t stream_get(cudaStream_t* s) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    auto& v = g_pool[dev];
+    if (!v.empty()) {
+      *s = v.back();
+      v.pop_back();
+      return cudaSuccess;
+    }
+  }
+  return cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
+}
+static void stream_put(cudaStream_t s) {
+  int dev = 0;
+  if (!s || cudaGetDevice(&dev) != cudaSuccess) return;
+  cudaStreamSynchronize(s);
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  g_pool[dev].push_back(s);
 }
 
 // Host-side finiteness check of event payloads (the reference's as_vector,
@@ -360,7 +393,7 @@ struct isvd_engine {
     while ((int)gst.size() < G) {
       cudaStream_t s2;
       cudaEvent_t ev;
-      ISVD_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+      ISVD_CUDA(stream_get(&s2));
       ISVD_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
       gst.push_back(s2);
       join_ev.push_back(ev);
@@ -643,7 +676,7 @@ struct isvd_engine {
     dfree(wx); dfree(wj); dfree(wpart); dfree(wout); dfree(wflags);
     dfree(snap.U); dfree(snap.V); dfree(snap.A); dfree(snap.s); dfree(snap.N); dfree(snap.ref);
     dfree(shv);
-    for (auto g : gst) cudaStreamDestroy(g);
+    for (auto g : gst) stream_put(g);
     for (auto ev : join_ev) cudaEventDestroy(ev);
     if (fork_ev) cudaEventDestroy(fork_ev);
     for (auto ev : ev_marks) cudaEventDestroy(ev);
@@ -660,7 +693,7 @@ struct isvd_engine {
     dfree(sring);
     if (cp_st) cudaStreamDestroy(cp_st);
     if (vflag_h) cudaFreeHost((void*)vflag_h);
-    if (own_stream && st) cudaStreamDestroy(st);
+    if (own_stream && st) stream_put(st);
   }
 };
 
@@ -700,7 +733,7 @@ int isvd_engine_create(isvd_engine** out, int batch, int m, int n, int k, double
   if (stream) {
     e->st = (cudaStream_t)stream;
   } else {
-    if (cudaStreamCreateWithFlags(&e->st, cudaStreamNonBlocking) != cudaSuccess) {
+    if (stream_get(&e->st) != cudaSuccess) {
       delete e;
       set_error("cudaStreamCreate failed");
       return ISVD_ENODEV;

@@ -478,3 +478,32 @@ def test_snapshot_restore_and_groups_reproduce():
                 oe.rank_one_update(e[1], e[2], e[3])
         assert rel_err(outs[0][idx].s, oe.factors.s) < SIGMA_RTOL
         assert sine_angle(outs[0][idx].u, oe.factors.u) < ANGLE_TOL
+
+
+@pytest.mark.parametrize("kappa", [99.0, 101.0, 5e3])
+def test_rank_one_orthogonality_near_the_structure_gate(kappa):
+    """Long rank-1 streams whose spectrum sits just inside (99) and just
+    outside (101) the sigma_max / sigma_min <= 100 gate of the structured
+    right-vector path, and far outside it (5e3): the factors stay orthonormal
+    to the reference's level (its one-sided Jacobi stops at 1e-14,
+    _kernels.pyx:38-59) over 2000 ticks, and match the oracle."""
+    rng = np.random.default_rng(int(kappa))
+    m, n, k, T = 160, 96, 20, 2000
+    qu = np.linalg.qr(rng.standard_normal((m, k)))[0]
+    qv = np.linalg.qr(rng.standard_normal((n, k)))[0]
+    sig = np.geomspace(10.0, 10.0 / kappa, k)
+    a0 = (qu * sig) @ qv.T
+    B = 64  # batched: deferred right basis and the fused rank-1 kernel, as config 5a
+    eng = BatchedSvdEngine(np.repeat(a0[None], B, axis=0), k)
+    oe = OracleEngine(a0, k)
+    ii, jj = rng.integers(0, m, T), rng.integers(0, n, T)
+    dd = rng.normal(0.0, 1e-3, T)
+    for t in range(T):
+        eng.rank_one_update(np.full(B, ii[t]), np.full(B, jj[t]), np.full(B, dd[t]))
+        oe.rank_one_update(int(ii[t]), int(jj[t]), float(dd[t]))
+    du, dv = eng.ortho_defect()
+    assert np.max(du) <= 5e-12 and np.max(dv) <= 5e-12, (np.max(du), np.max(dv))
+    f = eng.factors(0)
+    assert rel_err(f.s, oe.factors.s) < SIGMA_RTOL
+    assert sine_angle(f.u, oe.factors.u) < ANGLE_TOL
+    assert sine_angle(f.vt.T, oe.factors.vt.T) < ANGLE_TOL
