@@ -679,6 +679,8 @@ def run_gpu(args):
             "phase_ms_by_event": phase_by_kind,
             "tick_effective_gbs": all_bytes / (t_max / 1e3) / 1e9,
             "diagnostics": {"jacobi32_sweeps_per_core": float(dbg[0]) / max(1, int(dbg[1])),
+                            "rank1_fast_path_fraction": float(dbg[7]) / max(1, int(dbg[1])),
+                            "rank1_steps_per_core": float(dbg[6]) / max(1, int(dbg[1])),
                             "init_s": init_s,
                             "serial_phase_ms_per_step": diag_ms / max(1, diag_steps)},
         }

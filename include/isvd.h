@@ -50,7 +50,9 @@ int isvd_version(void);
  * reported by bench.py as `gpu_launches`). */
 int64_t isvd_launch_count(void);
 /* Device profiling counters (out8[0] = Jacobi sweeps summed over cores,
- * out8[1] = cores factored by the warp Jacobi kernel); reset if nonzero. */
+ * out8[1] = cores factored by the warp Jacobi kernel, out8[2..5] = arrow
+ * solver counters, out8[6] = simultaneous steps on the rank-1 fast path,
+ * out8[7] = rank-1 cores finished on it); reset if nonzero. */
 int isvd_debug_counters(int64_t* out8, int reset);
 
 /* 1. Functional kernels (backend.py:54-63) ---------------------------------- */

@@ -196,7 +196,7 @@ constexpr int kJ32Warps = 4;
 // Rank-1 sweep exit: once every rotation of a sweep had |a_pq| <= kConvRel
 // sqrt(a_pp a_qq), the off-diagonal left is O(kConvRel^2) relative (cyclic
 // Jacobi converges quadratically) and one first-order simultaneous step
-// (j32_polish) takes it below the reference's 1e-14 stop; Brand rank-1
+// (j32_step) takes it below the reference's 1e-14 stop; Brand rank-1
 // cores diag(s) + delta a b^T start with off-diagonals ~1e-5 relative, so
 // one sweep suffices.  Generic cores (functional core_svd, angles, guard)
 // sweep until a sweep makes no rotation, as _kernels.pyx:38-59.
@@ -209,6 +209,14 @@ __device__ __forceinline__ double j32_rsqrt(double x) {
   const double hx = 0.5 * x;
   y = y * fma(-hx * y, y, 1.5);
   return y * fma(-hx * y, y, 1.5);
+}
+
+// 1/x to ~1e-12 relative (seed + one Newton step): enough for a rotation
+// angle that only has to be right to first order
+__device__ __forceinline__ double j32_rcp1(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return fma(r, fma(-x, r, 1.0), r);
 }
 
 __device__ __forceinline__ double j32_rcp(double x) {
@@ -242,24 +250,33 @@ __device__ __forceinline__ void j32_apply_v(double (&v)[32], const double2* log)
   }
 }
 
-// First-order simultaneous Jacobi step (the finishing step of a one-sweep
-// rank-1 core).  After a sweep whose rotations were all small the columns of
-// G are orthogonal to O(1e-12) relative, not to the reference's 1e-14 stop
-// (_kernels.pyx:38-57 keeps sweeping: one more sweep of tiny rotations and a
-// check sweep).  With the Gram M = G^T G the rotation every pair (p, q)
-// would get is, to first order, theta_pq = M_pq / (M_qq - M_pp); applying
-// all of them at once, G <- G (I + Theta) (Theta skew), leaves off-diagonals
-// O(theta^2) and departs from orthogonality by O(theta^2) -- below 1e-14
-// when every |theta| <= 1e-7.  Both products run on the FP64 tensor path
-// (DMMA.8x8x4: 80 for the upper half of M, 128 for G Theta); theta is formed
-// in the accumulator layout, so shared memory is touched only to stage G
-// (gs, XOR-swizzled rows) and -- once the step is known to apply -- to pass
-// Theta and G Theta between layouts (ws).  Returns 0 if G already meets the
-// reference's stop (|M_pq| <= 1e-14 sqrt(M_pp M_qq) for every pair: G
-// unchanged), 1 after the step, -1 (ws untouched, G unchanged) if some theta
-// is too large for a first-order step (nearly equal columns).
-__device__ __forceinline__ int j32_polish(double (&x)[32], double* gs, double* ws, double* dg,
-                                          int lane, double null2) {
+// Simultaneous Jacobi step on the FP64 tensor path.  With the Gram
+// M = G^T G of the current columns, the rotation each pair (p, q) would get
+// is, to first order, theta_pq = M_pq / (M_qq - M_pp); all of them are
+// applied at once, G <- G J with Theta skew and
+//   J = I + Theta + Theta^2 / 2   (J^T J = I + Theta^4 / 4), or
+//   J = I + Theta                 when every |theta| <= 1e-8 (J^T J = I - Theta^2,
+//                                 below rounding),
+// which leaves off-diagonals O(theta^2) (quadratic convergence while the
+// columns' norms are well separated).  Products on DMMA.8x8x4: 80 for the
+// upper half of M, 128 for Theta^2, 128 for G (J - I); theta is formed in
+// the accumulator layout, so shared memory carries only the staged G (gs,
+// XOR-swizzled rows) and -- once the step is known to apply -- Theta,
+// J - I and G (J - I) between layouts (ws).  Uses:
+//  * the finishing step after one Jacobi sweep of small rotations (cap
+//    1e-7): the sweep leaves O(1e-12) relative off-diagonals, the reference
+//    stops at 1e-14 (_kernels.pyx:38-57: one more sweep of tiny rotations
+//    and a check sweep);
+//  * the whole factorisation of a well-conditioned Brand rank-1 core (cap
+//    1e-4): off-diagonals ~1e-7 relative reach the stop in two steps, with
+//    no dependent chain of 32 rotation rounds.
+// Returns 0 if G already meets the reference's stop (|M_pq| <= 1e-14
+// sqrt(M_pp M_qq) for every pair: G unchanged); 1 after a step; 2 after a
+// step with every |theta| <= 1e-8, which leaves O(1e-16) off-diagonals (past
+// the stop without another Gram); -1 (G and ws unchanged) if some |theta|
+// exceeds tcap (nearly equal columns).
+__device__ __forceinline__ int j32_step(double (&x)[32], double* gs, double* ws, double* dg,
+                                        int lane, double null2, double tcap) {
   auto T = [&](double* t, int i, int j) -> double& { return t[i * 32 + (j ^ ((i & 1) << 3))]; };
   const int g = lane >> 2, qd = lane & 3;
   double n4[4] = {0.0, 0.0, 0.0, 0.0};
@@ -300,13 +317,18 @@ __device__ __forceinline__ int j32_polish(double (&x)[32], double* gs, double* w
           const double dr = dg[r], dc = dg[c], mrc = th[idx][e];
           const bool live = r != c && dr > null2 && dc > null2;
           viol |= live && mrc * mrc > (kOrthoEps * kOrthoEps) * (dr * dc);
-          const double t = live ? mrc * j32_rcp(dc - dr) : 0.0;  // theta_rc
+          const double t = live ? mrc * j32_rcp1(dc - dr) : 0.0;  // theta_rc
           tmax = fmax(tmax, (t - t == 0.0) ? fabs(t) : 1e300);  // inf / NaN: fail
           th[idx][e] = t;
         }
   }
   if (!__any_sync(0xffffffffu, viol)) return 0;
-  if (warp_max(tmax) > 1e-7) return -1;
+  const double tm = warp_max(tmax);
+  if (tm > tcap) return -1;
+  // |theta| <= 1e-8: the Theta^2 term is below rounding and the step
+  // leaves O(theta^2) <= 1e-16 relative off-diagonals -- past the stop
+  // without another Gram (returns 2)
+  const bool second = tm > 1e-8;
   {
     int idx = 0;
 #pragma unroll
@@ -322,8 +344,44 @@ __device__ __forceinline__ int j32_polish(double (&x)[32], double* gs, double* w
       }
   }
   __syncwarp();
-  // G Theta: A = G rows 8mi.. (G(8mi + g, 4kk + qd)), B = Theta rows 4kk..
   double d[4][4][2];
+  if (second) {
+    // ws <- Theta + Theta^2 / 2 (tile-wise in the accumulator layout)
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) d[mi][ni][0] = d[mi][ni][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        a[t] = T(ws, 8 * t + g, 4 * kk + qd);
+        b[t] = T(ws, 4 * kk + qd, 8 * t + g);
+      }
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(d[mi][ni][0], d[mi][ni][1], a[mi], b[ni]);
+    }
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const double2 t2 = *reinterpret_cast<const double2*>(&T(ws, 8 * mi + g, 8 * ni + 2 * qd));
+        d[mi][ni][0] = fma(0.5, d[mi][ni][0], t2.x);
+        d[mi][ni][1] = fma(0.5, d[mi][ni][1], t2.y);
+      }
+    __syncwarp();  // every lane has read Theta
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+        *reinterpret_cast<double2*>(&T(ws, 8 * mi + g, 8 * ni + 2 * qd)) =
+            make_double2(d[mi][ni][0], d[mi][ni][1]);
+    __syncwarp();
+  }
+  // G (J - I): A = G rows 8mi.. (G(8mi + g, 4kk + qd)), B = (J - I) rows 4kk..
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -341,7 +399,7 @@ __device__ __forceinline__ int j32_polish(double (&x)[32], double* gs, double* w
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(d[mi][ni][0], d[mi][ni][1], a[mi], b[ni]);
   }
-  __syncwarp();  // every lane has read Theta
+  __syncwarp();  // every lane has read J - I
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -352,7 +410,7 @@ __device__ __forceinline__ int j32_polish(double (&x)[32], double* gs, double* w
 #pragma unroll
   for (int i = 0; i < 32; ++i) x[i] = T(gs, i, lane) + T(ws, i, lane);
   __syncwarp();
-  return 1;
+  return second ? 1 : 2;
 }
 
 // Per-warp shared state: the (c, s) log of one sweep (32 rounds x 16 pairs)
@@ -474,14 +532,20 @@ __global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32c_kernel(
       } else if (i >= lz.m_base) {
         ap = lz.W.p[b * lz.W.stride + (lz.r_base + (i - lz.m_base)) * lz.W.ld + lane];
       } else {
+        // every load issued before the first FMA (the gather is otherwise a
+        // chain of dependent L2 round trips)
         const double* ur = rc.U.p + b * rc.U.stride + i * rc.U.ld;
         const double* Wb = lz.W.p + b * lz.W.stride;
-        double a4[4] = {0.0, 0.0, 0.0, 0.0};
-        int c = 0;
-        for (; c + 4 <= lz.r_base; c += 4)
+        double uv[32], wv[32];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) a4[u] = fma(ur[c + u], Wb[(c + u) * lz.W.ld + lane], a4[u]);
-        for (; c < lz.r_base; ++c) a4[0] = fma(ur[c], Wb[c * lz.W.ld + lane], a4[0]);
+        for (int c = 0; c < 32; ++c) {
+          const bool ok = c < lz.r_base;
+          uv[c] = ok ? ur[c] : 0.0;
+          wv[c] = ok ? Wb[c * lz.W.ld + lane] : 0.0;
+        }
+        double a4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int c = 0; c < 32; ++c) a4[c & 3] = fma(uv[c], wv[c], a4[c & 3]);
         ap = (a4[0] + a4[1]) + (a4[2] + a4[3]);
       }
     }
@@ -494,15 +558,30 @@ __global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32c_kernel(
       } else {
         // V_eff[j, :] = [V[j, :fw] | Z[:, j]^T] G
         const double* Gb = vd.G + b * vd.g_stride;
-        double a4[4] = {0.0, 0.0, 0.0, 0.0};
-        int c = 0;
-        for (; c + 4 <= vd.fw; c += 4)
-#pragma unroll
-          for (int u = 0; u < 4; ++u) a4[u] = fma(vr[c + u], Gb[(c + u) * vd.ldg + lane], a4[u]);
-        for (; c < vd.fw; ++c) a4[0] = fma(vr[c], Gb[c * vd.ldg + lane], a4[0]);
         const double* Zb = vd.Z + b * vd.z_stride + j;
-        for (int t = 0; t < vd.nz; ++t)
-          a4[t & 3] = fma(Zb[(int64_t)t * vd.ldz], Gb[(vd.fw + t) * vd.ldg + lane], a4[t & 3]);
+        double a4[4] = {0.0, 0.0, 0.0, 0.0};
+        {
+          double vv[32], gv[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            const bool ok = c < vd.fw;
+            vv[c] = ok ? vr[c] : 0.0;
+            gv[c] = ok ? Gb[c * vd.ldg + lane] : 0.0;
+          }
+#pragma unroll
+          for (int c = 0; c < 32; ++c) a4[c & 3] = fma(vv[c], gv[c], a4[c & 3]);
+        }
+        {
+          double zv[kVWin], gz[kVWin];
+#pragma unroll
+          for (int t = 0; t < kVWin; ++t) {
+            const bool ok = t < vd.nz;
+            zv[t] = ok ? Zb[(int64_t)t * vd.ldz] : 0.0;
+            gz[t] = ok ? Gb[(vd.fw + t) * vd.ldg + lane] : 0.0;
+          }
+#pragma unroll
+          for (int t = 0; t < kVWin; ++t) a4[t & 3] = fma(zv[t], gz[t], a4[t & 3]);
+        }
         vq = (a4[0] + a4[1]) + (a4[2] + a4[3]);
       }
     }
@@ -549,8 +628,71 @@ __global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32c_kernel(
     for (int i = 0; i < 32; ++i) n4[i & 3] = fma(x[i], x[i], n4[i & 3]);
     return (n4[0] + n4[1]) + (n4[2] + n4[3]);
   };
+  // V from the structure of a rank-1 core (G = K V = U Sigma, so v =
+  // K^T g / sigma^2 with K^T g = s o g + delta b (a . g); error ~ eps
+  // sigma_max / sigma_min per tick once G is orthogonal to working
+  // precision).  `reversed`: one sweep reversed the column positions.
+  auto formula_v = [&](bool reversed) {
+    const double n2 = col_norm();
+    const bool live_col = (reversed ? 31 - lane : lane) < s;
+    double* kv = reinterpret_cast<double*>(W.log);  // [a | b | s] (the log is not needed)
+    kv[lane] = ka;
+    kv[32 + lane] = kb;
+    kv[64 + lane] = ks;
+    __syncwarp();
+    double d4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < 32; ++i) d4[i & 3] = fma(kv[i], x[i], d4[i & 3]);
+    const double dot = kdel * ((d4[0] + d4[1]) + (d4[2] + d4[3]));
+    const double in2 = live_col ? 1.0 / n2 : 0.0;
+    __syncwarp();  // every lane's reads of the staged G are done before V's tile is written
+#pragma unroll
+    for (int k = 0; k < 32; ++k) W.V[k][lane] = fma(kv[64 + k], x[k], kv[32 + k] * dot) * in2;
+  };
   int sweeps = 0;
-  for (; sweeps < kMaxSweeps;) {
+  bool fast = false, formula = false;
+  // delta == 0 (a rejected device payload is staged as (0, 0, 0.0)): K =
+  // diag(s) and the factors must come out bit for bit unchanged, so Uk and
+  // Vk are written as exact identities below instead of G / sigma and the
+  // structure formula (whose x * (1 / x) need not round to 1)
+  const bool trivial = BUILD && kdel == 0.0;
+  if (trivial) fast = true;
+  if (BUILD && !trivial) {
+    // Fast path for a well-conditioned Brand rank-1 core (every s live and
+    // within a factor of 100): simultaneous steps (j32_step,
+    // DMMA) from K itself to the reference's stop -- no chain of 32
+    // dependent rotation rounds -- and V from the structure.  Cores with
+    // close or dead singular values (a step's theta above 1e-4, or no
+    // convergence in 4 steps) restart from K on the sweep path below.
+    const double smax = warp_max(lane < s ? ks : 0.0);
+    const double smin = -warp_max(lane < s ? -ks : -1e300);
+    if (smin >= 1e-2 * smax && smin > 0.0) {
+      const double null2 = fmax(1e-30 * warp_max(col_norm()), 1e-290);
+      int pol = 1, steps = 0;
+      for (; steps < 4 && pol == 1; ++steps)
+        pol = j32_step(x, &W.V[0][0], reinterpret_cast<double*>(W.log), W.nrm, lane, null2, 1e-4);
+      if (lane == 0) atomicAdd(&g_debug_counters[2], (unsigned long long)steps);
+      if (pol == 0 || pol == 2) {
+        fast = formula = true;
+        if (lane == 0) atomicAdd(&g_debug_counters[3], 1ull);
+      } else {
+        // back to K and V = I (bit-identical to the fused build above)
+#pragma unroll
+        for (int r2 = 0; r2 < 32; ++r2) {
+          const double da = kdel * __shfl_sync(0xffffffffu, ka, r2);
+          double v = 0.0;
+          if (lane < s && r2 < s) {
+            v = da * kb;
+            if (r2 == lane) v += ks;
+          }
+          x[r2] = v;
+          W.V[lane][r2] = (lane == r2 && lane < s) ? 1.0 : 0.0;
+        }
+        __syncwarp();
+      }
+    }
+  }
+  for (; !fast && sweeps < kMaxSweeps;) {
     bool any = false;
     float relmax = 0.0f;
     double nrm = col_norm();  // exact squared norm at the sweep start
@@ -566,12 +708,11 @@ __global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32c_kernel(
     bool done = !rotated;
     // One-sweep rank-1 cores of moderate condition (every rotation of the
     // first sweep below kConvRel, sigma_max / sigma_min <= 100): the
-    // finishing step (j32_polish) brings G to the reference's stop, and the
+    // finishing step (j32_step) brings G to the reference's stop, and the
     // right vectors follow from the structure instead of replaying the
     // sweep's rotations on V: G = K V = U Sigma, so v = K^T g / sigma^2 with
     // K^T g = s o g + delta b (a . g) (O(s^2) per core; error ~ eps
     // sigma_max / sigma_min per tick with G orthogonal to working precision).
-    bool formula = false;
     if constexpr (BUILD) {
       if (rotated && sweeps == 0 && warp_max((double)relmax) <= kConvRel * kConvRel) {
         const double n2 = col_norm();
@@ -580,8 +721,8 @@ __global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32c_kernel(
         const double mn = -warp_max(live_col ? -n2 : -1e300);
         if (mn >= 1e-4 * mx && mx > 0.0) {
           // V's tile (identity so far) holds the staged G; the log is the scratch
-          const int pol = j32_polish(x, &W.V[0][0], reinterpret_cast<double*>(W.log), W.nrm,
-                                     lane, null2);
+          const int pol = j32_step(x, &W.V[0][0], reinterpret_cast<double*>(W.log), W.nrm,
+                                   lane, null2, 1e-7);
           if (pol >= 0) {
             formula = true;
             done = true;
@@ -603,27 +744,13 @@ __global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32c_kernel(
 #pragma unroll
       for (int j = 0; j < 32; ++j) W.V[lane][j] = v[j];
     }
-    if (formula) {
-      const double n2 = col_norm();
-      const bool live_col = (31 - lane) < s;
-      double* kv = reinterpret_cast<double*>(W.log);  // [a | b | s] (the log is not needed)
-      kv[lane] = ka;
-      kv[32 + lane] = kb;
-      kv[64 + lane] = ks;
-      __syncwarp();
-      double d4[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-      for (int i = 0; i < 32; ++i) d4[i & 3] = fma(kv[i], x[i], d4[i & 3]);
-      const double dot = kdel * ((d4[0] + d4[1]) + (d4[2] + d4[3]));
-      const double in2 = live_col ? 1.0 / n2 : 0.0;
-      __syncwarp();  // every lane's reads of the staged G are done before V's tile is written
-#pragma unroll
-      for (int k = 0; k < 32; ++k) W.V[k][lane] = fma(kv[64 + k], x[k], kv[32 + k] * dot) * in2;
-    }
+    if (formula) formula_v(true);
     __syncwarp();
     ++sweeps;
     if (done) break;
   }
+  if (fast && !trivial) formula_v(false);
+  __syncwarp();
   if (lane == 0) atomicAdd(&g_debug_counters[0], (unsigned long long)sweeps);
   if (lane == 0) atomicAdd(&g_debug_counters[1], 1ull);
   // position l holds original column id(l): a sweep reverses the order
@@ -667,7 +794,8 @@ __global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32c_kernel(
       const double iv = live ? 1.0 / myn : 0.0;
       const int oc = pos[lane];
 #pragma unroll
-      for (int k = 0; k < 32; ++k) us(k, oc) = (k < s && mine) ? x[k] * iv : 0.0;
+      for (int k = 0; k < 32; ++k)
+        us(k, oc) = (k < s && mine) ? (trivial ? (x[k] != 0.0 ? 1.0 : 0.0) : x[k] * iv) : 0.0;
     }
     __syncwarp();
     if (any_dead) {
@@ -722,7 +850,7 @@ __global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32c_kernel(
     const int oc = pos[lane];
 #pragma unroll
     for (int i = 0; i < 32; ++i)
-      if (i < s && mine) U[i * ldo + oc] = x[i] * iv;
+      if (i < s && mine) U[i * ldo + oc] = trivial ? (x[i] != 0.0 ? 1.0 : 0.0) : x[i] * iv;
     if (lane < s) {
       const int srcl = W.ipos[lane];
       for (int i = 0; i < s; ++i) Vo[i * ldv + lane] = W.V[i][srcl];
@@ -757,6 +885,8 @@ int read_debug_counters(int64_t* out, int reset) {
   unsigned long long h[8];
   ISVD_CUDA(cudaMemcpyFromSymbol(h, g_debug_counters, sizeof(h)));
   for (int i = 0; i < 2; ++i) out[i] = (int64_t)h[i];
+  out[6] = (int64_t)h[2];  // simultaneous-step (fast path) steps
+  out[7] = (int64_t)h[3];  // rank-1 cores finished on the fast path
   if (reset) {
     unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     ISVD_CUDA(cudaMemcpyToSymbol(g_debug_counters, z, sizeof(z)));
