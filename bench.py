@@ -14,8 +14,12 @@ over N GPUs, no data-path collective).
           host validation + H2D copy + kernels + D2H read of the step's
           result (per-stream sq_norm, residual and input norm) every step;
           the host waits for step t's result after issuing step t+1.
-`roofline` dominant kernel (the factor rotation K3/K4): algorithmic bytes /
-          its measured average duration (CUDA events on the engine stream).
+`roofline` the dominant kernel by time against its binding resource (FP64
+          tensor peak for the core kernels, HBM for K1 / rotations):
+          algorithmic flops or bytes / its measured duration (CUDA events on
+          the engine stream).
+`rotation` BASELINE's "basis-rotation HBM GB/s": the deferred U flush and the
+          V materialisation (algorithmic bytes / measured time vs HBM peak).
 
 `--impl reference` times the reference algorithm's CPU implementation (the
 numpy restatement in oracle/, all host cores) on a bounded sample of the
@@ -316,6 +320,49 @@ def _simulate_bytes(B, steps, window=32, vwin=8):
         else:
             rot_r1 += 8.0 * B * (vb + wb)
     return proj_bytes, rot_row, rot_r1, vflush_bytes, all_bytes
+
+
+def _simulate_flops(B, steps, window=32, vwin=8, rank1_steps=2.0):
+    """Algorithmic FP64 flops of the two core kernels over `steps` ticks,
+    following the same data flow as _simulate_bytes:
+    * rank-1 tick (jacobi32c): the core factorisation as the simultaneous
+      Jacobi steps run it -- per step the 32 x 32 Gram (2 k^3, symmetric half
+      counted in full as DMMA computes it), Theta^2 on the first step, and
+      G (J - I) (2 k^3 each) -- plus the fused rotations of the deferred
+      bases: W (rows_W x k) . Uk and G (rows_G x k) . Vk (2 rows k^2 each);
+    * row tick (arrow): the secular solve is O(k^2) (counted as 40 (k+1)^2)
+      plus the fused rotations [W 0; 0 1] . Q and [G 0; 0 1] . Vk (2 rows (k+1) k).
+    Returns (rank-1 flops, row flops)."""
+    k = K
+    f_r1 = f_row = 0.0
+    b_rows, active = 0, False
+    vpend, nz = False, 0
+    core = 2.0 * k ** 3 * (3.0 + 2.0 * max(0.0, rank1_steps - 1.0))
+    for t in range(steps):
+        row = t % 2 == 0
+        g_rows = (k + nz) if vpend else 0
+        if row:
+            w_rows = k + b_rows if active else 0
+            f_row += B * (40.0 * (k + 1) ** 2 + 2.0 * (w_rows + 1) * (k + 1) * k
+                          + 2.0 * (g_rows + 1) * (k + 1) * k)
+            if not vpend:
+                vpend, nz = True, 0
+            nz += 1
+            if nz >= vwin:
+                vpend, nz = False, 0
+            if not active:
+                active, b_rows = True, 1
+            else:
+                b_rows += 1
+            if b_rows >= window:
+                active, b_rows = False, 0
+        else:
+            w_rows = k + b_rows if active else k
+            f_r1 += B * (core + 2.0 * w_rows * k * k + 2.0 * g_rows * k * k)
+            vpend = True
+            if not active:
+                active, b_rows = True, 0
+    return f_r1, f_row
 
 
 def make_inputs_5b(torch, dev, seed=0, m=M5B, row0=0, rows=None):
@@ -632,20 +679,76 @@ def run_gpu(args):
             v["share"] = v["ms"] / busy if busy else None
             v["ms_per_step"] = v["ms"] / max(1, diag_steps)
             v["gbs"] = (v["bytes"] / (v["ms"] / 1e3) / 1e9) if (v["bytes"] and v["ms"]) else None
-        dom_name = max(kernels, key=lambda k: kernels[k]["ms"])
-        # the HBM-bound kernel of the tick (the core kernels are FP64-latency
-        # bound: see profiles/ for their pipe utilisation)
-        hbm_name = "project_append (K1, row ticks)"
-        hbm = kernels
-        hk = hbm[hbm_name]
-        achieved = hk["gbs"]
+        # algorithmic flops of the two FP64-latency-bound core kernels
+        r1_steps = float(dbg[6]) / max(1, int(dbg[7])) if dbg[7] else 2.0
+        f_r1, f_row = _simulate_flops(B, diag_steps, window, rank1_steps=r1_steps)
+        kernels["jacobi32c + fused W/G rotation (K2b, rank-1 ticks)"]["flops"] = f_r1
+        kernels["arrow_svd + fused W/G rotation (K2a, row ticks)"]["flops"] = f_row
+        for v in kernels.values():
+            v["tflops"] = (v["flops"] / (v["ms"] / 1e3) / 1e12) if (v.get("flops") and v["ms"]) \
+                else None
+        flush_k = kernels["rotate U flush (K3, deferred)"]
+        flush_k["flops"] = 2.0 * B * M0 * K * K * n_flush if n_flush else None
         summ, summ_file = _ncu_summary()
-        traffic = None
-        ncu_key = "proj5a"
-        if ncu_key in summ and "dram_bytes" in summ[ncu_key]:
-            # the capture is one stream-group launch (B / 4 streams) of a row
-            # tick; per tick on average over both event kinds for K1
-            traffic = summ[ncu_key]["dram_bytes"] * 4.0 * B / TOTAL_STREAMS
+
+        def ncu_traffic(key):
+            # captures are one stream-group launch (B / 4 streams); scaled to all B
+            if key in summ and "dram_bytes" in summ[key]:
+                return summ[key]["dram_bytes"] * 4.0 * B / TOTAL_STREAMS
+            return None
+
+        # roofline of the dominant kernel by time, against the resource that
+        # binds it: K1 and the rotations stream HBM; the core kernels run on
+        # the FP64 pipes (DMMA for the Gram / rotation products, DFMA for the
+        # secular solve), so their roof is the measured DMMA peak
+        dom_name = max(kernels, key=lambda k: kernels[k]["ms"])
+        dom = kernels[dom_name]
+        n_launch = max(1, (diag_steps + 1) // 2 if "row ticks" in dom_name else diag_steps // 2)
+        ncu_key = {"project_append (K1, row ticks)": "proj5a",
+                   "arrow_svd + fused W/G rotation (K2a, row ticks)": "arrow5a",
+                   "jacobi32c + fused W/G rotation (K2b, rank-1 ticks)": "jacobi5a"}.get(dom_name)
+        traffic = ncu_traffic(ncu_key) if ncu_key else None
+        measured = (f"first {diag_steps} ticks in timing mode (one launch per kernel over all "
+                    "streams, CUDA events around each phase on the engine stream)")
+        if dom.get("flops"):
+            roof = {"kernel": dom_name, "bound": "tensor", "achieved": dom["tflops"],
+                    "peak": DMMA_PEAK_TFS, "unit": "TFLOP/s", "frac": dom["tflops"] / DMMA_PEAK_TFS,
+                    "peak_kind": "measured FP64 DMMA.8x8x4 peak (profiles/r01_fp64_peaks.txt); "
+                                 "FP64 has no tcgen05 kind",
+                    "flops_per_launch": dom["flops"] / n_launch,
+                    "bytes_per_launch": dom["bytes"] / n_launch,
+                    "hbm_frac": dom["gbs"] / peak if dom.get("gbs") else None}
+        else:
+            roof = {"kernel": dom_name, "bound": "hbm", "achieved": dom["gbs"], "peak": peak,
+                    "unit": "GB/s", "frac": dom["gbs"] / peak, "peak_kind": peak_kind,
+                    "bytes_per_launch": dom["bytes"] / n_launch}
+        roof.update({"traffic": traffic,
+                     "traffic_source": f"profiles/{summ_file}: {ncu_key} dram__bytes_read+write of "
+                                       "one stream-group launch x 4 groups (ncu, cold cache)"
+                     if traffic else None,
+                     "launch": "one launch over all streams of the GPU",
+                     "measured_over": measured})
+        if ncu_key and ncu_key in summ:
+            roof["ncu"] = {k2: summ[ncu_key].get(k2) for k2 in
+                           ("fp64_pipe_pct", "dmma_pipe_pct", "occupancy_pct", "dram_pct_peak",
+                            "regs", "warp_instructions")}
+        # BASELINE's second metric: basis-rotation HBM GB/s -- the deferred U
+        # flush and the V materialisation, the two launches that stream a
+        # tall basis through HBM
+        rot_k = kernels["rotate U flush (K3, deferred)"]
+        vm_k = kernels["V materialisation (K3, every 8 row appends)"]
+        rotation = {
+            "metric": "basis-rotation HBM GB/s", "unit": "GB/s", "peak": peak,
+            "u_flush": {"achieved": rot_k["gbs"], "frac": rot_k["gbs"] / peak if rot_k["gbs"] else None,
+                        "bytes": rot_k["bytes"], "ms": rot_k["ms"], "launches": n_flush,
+                        "traffic": ncu_traffic("flush5a")},
+            "v_materialisation": {"achieved": vm_k["gbs"],
+                                  "frac": vm_k["gbs"] / peak if vm_k["gbs"] else None,
+                                  "bytes": vm_k["bytes"], "ms": vm_k["ms"],
+                                  "traffic": ncu_traffic("vflush5a")},
+            "k1_projection": {"achieved": kernels["project_append (K1, row ticks)"]["gbs"],
+                              "frac": kernels["project_append (K1, row ticks)"]["gbs"] / peak},
+        }
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
             "warmup": warm, "ms_per_step": t_max / steps, "higher_is_better": True,
@@ -661,23 +764,15 @@ def run_gpu(args):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
                     "result_readback_lag_steps": E2E_LAG},
-            "roofline": {"kernel": hbm_name, "bound": "hbm", "achieved": achieved, "peak": peak,
-                         "unit": "GB/s", "frac": achieved / peak, "peak_kind": peak_kind,
-                         "traffic": traffic,
-                         "traffic_source": (f"profiles/{summ_file}: {ncu_key} dram__bytes_read"
-                                            "+write of one stream-group launch x 4 groups "
-                                            "(ncu, cold-cache), per tick")
-                         if traffic else None,
-                         "bytes_per_launch": hk["bytes"] / max(1, (diag_steps + 1) // 2),
-                         "launch": "one K1 launch over all streams of the GPU (a row tick)",
-                         "dominant_kernel_by_time": dom_name,
-                         "measured_over": f"first {diag_steps} ticks in timing mode (one "
-                                          "launch per kernel over all streams, CUDA events "
-                                          "around each phase on the engine stream)"},
+            "roofline": roof,
+            "rotation": rotation,
             "kernels": kernels,
             "flushes": n_flush,
             "phase_ms_by_event": phase_by_kind,
-            "tick_effective_gbs": all_bytes / (t_max / 1e3) / 1e9,
+            # the reference algorithm's compulsory bytes per second of
+            # this run: a throughput in the reference's units, NOT an achieved
+            # bandwidth (the deferred bases move far fewer bytes)
+            "reference_algorithm_bytes_rate_gbs": all_bytes / (t_max / 1e3) / 1e9,
             "diagnostics": {"jacobi32_sweeps_per_core": float(dbg[0]) / max(1, int(dbg[1])),
                             "rank1_fast_path_fraction": float(dbg[7]) / max(1, int(dbg[1])),
                             "rank1_steps_per_core": float(dbg[6]) / max(1, int(dbg[1])),

@@ -274,6 +274,13 @@ int isvd_dense_svd(int batch, int m, int n, const double* a, int w_keep, double*
                    double* u, double* vt);
 /* Same, from the engine's tracked matrices (no host copy of A). */
 int isvd_engine_oracle(isvd_engine* e, int w_keep, double* s, double* u);
+/* Host-basis metrics on the device (linalg.py:126-153), host pointers,
+ * synchronous.  ortho_defect: out[b] = ||Q_b^T Q_b - I||_F for B bases
+ * (rows x w each).  principal_angle: largest principal angle between the
+ * spans of q1 and q2 (rows x w each, w <= 160); ISVD_EINVAL if either basis
+ * is not orthonormal to 1e-6. */
+int isvd_ortho_defect(int batch, int rows, int w, const double* q, double* out);
+int isvd_principal_angle(int rows, int w, const double* q1, const double* q2, double* out);
 
 /* The two dense contractions on the FP64 tensor path (DMMA), device
  * pointers, row-major, asynchronous on `stream` (NULL = legacy stream).

@@ -58,6 +58,8 @@ SIGNATURES = {
                                            _ip, C.POINTER(_vp), _ip, C.POINTER(_vp), _ip64, _ip]),
     "isvd_engine_canonicalize": (C.c_int, [_vp]),
     "isvd_engine_stream": (_vp, [_vp]),
+    "isvd_ortho_defect": (C.c_int, [C.c_int, C.c_int, C.c_int, _dp, _dp]),
+    "isvd_principal_angle": (C.c_int, [C.c_int, C.c_int, _dp, _dp, _dp]),
     "isvd_engine_streams": (C.c_int, [_vp, C.POINTER(_vp), C.c_int]),
     "isvd_engine_synchronize": (C.c_int, [_vp]),
     "isvd_engine_set_timing": (C.c_int, [_vp, C.c_int]),

@@ -2098,6 +2098,77 @@ int isvd_engine_oracle(isvd_engine* e, int w_keep, double* s, double* u) {
   return oracle_common(e->B, e->m, e->n, e->A, e->astride(), e->n_cap, w_keep, s, u, nullptr, e->st);
 }
 
+// ------------------------------------------- functional metrics (host bases)
+
+// ||Q^T Q - I||_F of host bases Q (B x rows x w), Gram on the FP64 tensor path
+// (linalg.py:126-130).  Host pointers; synchronous.
+int isvd_ortho_defect(int batch, int rows, int w, const double* q, double* out) {
+  if (batch < 1 || rows < 1 || w < 1 || !q || !out) { set_error("bad argument"); return ISVD_EINVAL; }
+  ISVD_TRY(check_device());
+  double *qd = nullptr, *part = nullptr, *g = nullptr;
+  int rc = dalloc(&qd, (size_t)batch * rows * w);
+  if (rc == ISVD_OK) rc = dalloc(&part, (size_t)std::max<int64_t>(1, gram_part_elems(batch, rows, w, w)));
+  if (rc == ISVD_OK) rc = dalloc(&g, (size_t)batch * w * w);
+  if (rc == ISVD_OK && cudaMemcpy(qd, q, sizeof(double) * batch * rows * w, cudaMemcpyHostToDevice) != cudaSuccess)
+    rc = ISVD_ENODEV;
+  Mat Q{qd, (int64_t)rows * w, w};
+  if (rc == ISVD_OK) rc = launch_gram(batch, rows, w, w, Q, Q, part, g, 0);
+  std::vector<double> gh((size_t)batch * w * w);
+  if (rc == ISVD_OK && cudaMemcpy(gh.data(), g, sizeof(double) * gh.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+    rc = ISVD_ENODEV;
+  if (rc == ISVD_OK)
+    for (int b = 0; b < batch; ++b) {
+      double acc = 0.0;
+      for (int i = 0; i < w; ++i)
+        for (int j = 0; j < w; ++j) {
+          const double d = gh[((size_t)b * w + i) * w + j] - (i == j ? 1.0 : 0.0);
+          acc += d * d;
+        }
+      out[b] = std::sqrt(acc);
+    }
+  dfree(qd); dfree(part); dfree(g);
+  return rc;
+}
+
+// Largest principal angle between host bases q1, q2 (rows x w each):
+// arccos of the smallest singular value of q1^T q2, clamped into [0, 1]
+// (linalg.py:133-153); the Gram on DMMA, the w x w SVD by the core kernel.
+// Each basis must be orthonormal to 1e-6 (else ISVD_EINVAL, as the reference).
+int isvd_principal_angle(int rows, int w, const double* q1, const double* q2, double* out) {
+  if (rows < 1 || w < 1 || !q1 || !q2 || !out) {
+    set_error(w < 1 ? "subspaces must have at least one column" : "bad argument");
+    return ISVD_EINVAL;
+  }
+  if (w > kCoreMaxS) { set_error("principal angle: too many columns for the core kernel"); return ISVD_EINVAL; }
+  double d1 = 0.0, d2 = 0.0;
+  ISVD_TRY(isvd_ortho_defect(1, rows, w, q1, &d1));
+  if (d1 > 1e-6) { set_error("q1 is not orthonormal (defect > 1e-6)"); return ISVD_EINVAL; }
+  ISVD_TRY(isvd_ortho_defect(1, rows, w, q2, &d2));
+  if (d2 > 1e-6) { set_error("q2 is not orthonormal (defect > 1e-6)"); return ISVD_EINVAL; }
+  double *a = nullptr, *b = nullptr, *part = nullptr, *c = nullptr, *uk = nullptr, *vk = nullptr,
+         *sv = nullptr, *vscr = nullptr;
+  int rc = dalloc(&a, (size_t)rows * w);
+  if (rc == ISVD_OK) rc = dalloc(&b, (size_t)rows * w);
+  if (rc == ISVD_OK) rc = dalloc(&part, (size_t)std::max<int64_t>(1, gram_part_elems(1, rows, w, w)));
+  if (rc == ISVD_OK) rc = dalloc(&c, (size_t)w * w);
+  if (rc == ISVD_OK) rc = dalloc(&uk, (size_t)w * w);
+  if (rc == ISVD_OK) rc = dalloc(&vk, (size_t)w * w);
+  if (rc == ISVD_OK) rc = dalloc(&sv, (size_t)w);
+  if (rc == ISVD_OK && w > kSmemMaxS) rc = dalloc(&vscr, (size_t)w * (w | 1));
+  if (rc == ISVD_OK && (cudaMemcpy(a, q1, sizeof(double) * rows * w, cudaMemcpyHostToDevice) != cudaSuccess ||
+                        cudaMemcpy(b, q2, sizeof(double) * rows * w, cudaMemcpyHostToDevice) != cudaSuccess))
+    rc = ISVD_ENODEV;
+  if (rc == ISVD_OK) rc = launch_gram(1, rows, w, w, Mat{a, 0, w}, Mat{b, 0, w}, part, c, 0);
+  if (rc == ISVD_OK)
+    rc = launch_core_svd(1, w, c, (int64_t)w * w, w, uk, vk, (int64_t)w * w, w, sv, w, vscr, nullptr, 0);
+  double smin = 0.0;
+  if (rc == ISVD_OK && cudaMemcpy(&smin, sv + (w - 1), sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+    rc = ISVD_ENODEV;
+  if (rc == ISVD_OK) *out = std::acos(std::min(1.0, std::max(0.0, smin)));
+  dfree(a); dfree(b); dfree(part); dfree(c); dfree(uk); dfree(vk); dfree(sv); dfree(vscr);
+  return rc;
+}
+
 // --------------------------------------------------------- functional kernels
 
 int isvd_gram(int rows, int wa, int wb, const double* xa, int lda, const double* xb, int ldb,

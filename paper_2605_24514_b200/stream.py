@@ -1,9 +1,9 @@
 """Event types and the Algorithm-1 simulation loop (mirror of svdstream/stream.py).
 
 ``run_stream`` is ``run_simulation`` (stream.py:257-333) with the initial
-matrix and the event list passed in explicitly -- the reference's own loop
-builds its events from generators that are out of scope here;
-BASELINE's synthetic inputs come from ``workloads``.
+matrix and the event list passed in explicitly; ``workloads.run_simulation``
+drives it from a ``StreamSpec`` with the reference's own generators, and
+BASELINE's seeded inputs come from ``workloads.cfg1..cfg5a``.
 """
 
 from __future__ import annotations
@@ -100,6 +100,7 @@ def run_stream(initial, events, k: int, policy: PolicyConfig | None = None,
             apply_event(engine, event)
         except ValueError as exc:
             raise ValueError(f"event at step {t} failed: {exc}") from exc
+        engine.synchronize()  # the update is complete when its kernels are (stream.py:284-289)
         update_time = time.perf_counter() - start
 
         if adaptive and isinstance(event, (RowAppend, ColAppend)):

@@ -10,6 +10,8 @@ Events are tuples: ("row", x) | ("col", y) | ("rank1", i, j, delta).
 
 from __future__ import annotations
 
+from dataclasses import dataclass
+
 import numpy as np
 
 
@@ -145,3 +147,142 @@ def to_stream_events(events):
         else:
             out.append(RankOneUpdate(ev[1], ev[2], ev[3]))
     return out
+
+
+# ---------------------------------------------------------------------------
+# The reference's own synthetic streams (svdstream/stream.py:73-200 and
+# rng.py), restated so its CLI scenarios and acceptance streams (which are
+# calibrated on STREAM_SEED = 7, acceptance.py:35-37) can be replayed on the
+# device engine.  Substream tags as rng.py:12-17.
+INIT, EVENTS, STRUCTURAL, MIXED, PANEL, PORTFOLIO = 0, 1, 2, 3, 4, 5
+
+
+def substream(seed: int, tag: int) -> np.random.Generator:
+    """rng.py:20-25."""
+    seed = int(seed)
+    if seed < 0:
+        raise ValueError(f"seed must be nonnegative, got {seed}")
+    return np.random.default_rng([seed, int(tag)])
+
+
+def gen_low_rank(m: int, n: int, rank: int, noise_scale: float, seed: int) -> np.ndarray:
+    """stream.py:73-83: Gaussian factors of the given rank plus dense noise."""
+    if not 1 <= rank <= min(m, n):
+        raise ValueError(f"rank must be in [1, min(m, n)], got {rank} for {m}x{n}")
+    if noise_scale < 0.0:
+        raise ValueError(f"noise_scale must be >= 0, got {noise_scale}")
+    gen = substream(seed, INIT)
+    left = gen.standard_normal((m, rank))
+    right = gen.standard_normal((n, rank))
+    return left @ right.T + noise_scale * gen.standard_normal((m, n))
+
+
+def gen_rank_one_events(count: int, delta_sd: float, rows: int, cols: int, seed: int):
+    """stream.py:86-100: uniform in-bounds (i, j), normal deltas."""
+    if count < 0:
+        raise ValueError(f"count must be >= 0, got {count}")
+    gen = substream(seed, EVENTS)
+    i_idx = gen.integers(0, rows, size=count)
+    j_idx = gen.integers(0, cols, size=count)
+    deltas = gen.normal(0.0, delta_sd, size=count)
+    return [("rank1", int(i), int(j), float(d)) for i, j, d in zip(i_idx, j_idx, deltas)]
+
+
+def gen_structural_events(kind: str, count: int, factor_rank: int, noise_scale: float,
+                          width: int, seed: int):
+    """stream.py:103-127: appends from a fixed latent factor model."""
+    if kind not in ("row", "col"):
+        raise ValueError(f"kind must be 'row' or 'col', got {kind!r}")
+    if count < 0:
+        raise ValueError(f"count must be >= 0, got {count}")
+    gen = substream(seed, STRUCTURAL)
+    directions = gen.standard_normal((factor_rank, width))
+    events = []
+    for _ in range(count):
+        loading = gen.standard_normal(factor_rank)
+        events.append((kind, loading @ directions + noise_scale * gen.standard_normal(width)))
+    return events
+
+
+def gen_mixed_stream(count: int, mix_weights, base_m: int, base_n: int, factor_rank: int,
+                     noise_scale: float, delta_sd: float, seed: int):
+    """stream.py:130-165: weighted interleaving with coherent loadings."""
+    weights = np.asarray(mix_weights, dtype=np.float64)
+    if weights.shape != (3,) or np.any(weights < 0) or weights.sum() <= 0:
+        raise ValueError("mix_weights must be 3 nonnegative values, not all zero")
+    gen = substream(seed, MIXED)
+    kinds = gen.choice(3, size=count, p=weights / weights.sum())
+    left = gen.standard_normal((base_m, factor_rank))
+    right = gen.standard_normal((base_n, factor_rank))
+    events = []
+    for kind in kinds:
+        if kind == 0:
+            loading = gen.standard_normal(factor_rank)
+            events.append(("row", loading @ right.T + noise_scale * gen.standard_normal(len(right))))
+            left = np.vstack([left, loading[None, :]])
+        elif kind == 1:
+            loading = gen.standard_normal(factor_rank)
+            events.append(("col", left @ loading + noise_scale * gen.standard_normal(len(left))))
+            right = np.vstack([right, loading[None, :]])
+        else:
+            i = int(gen.integers(0, len(left)))
+            j = int(gen.integers(0, len(right)))
+            events.append(("rank1", i, j, float(gen.normal(0.0, delta_sd))))
+    return events
+
+
+@dataclass
+class StreamSpec:
+    """stream.py:171-197: one synthetic run (matrix, events, policy, logging)."""
+
+    m: int = 50
+    n: int = 40
+    true_rank: int = 5
+    noise_scale: float = 0.05
+    k: int = 5
+    seed: int = 0
+    scenario: str = "rank1"  # rank1 | rows | cols | mixed
+    events: int = 10_000
+    delta_sd: float = 0.05
+    mix_weights: tuple = (0.05, 0.05, 0.90)
+    policy: object = None
+    log_every: int = 50
+    tol: float = 1e-10
+    reortho_guard: bool = False
+
+    def __post_init__(self):
+        if self.scenario not in ("rank1", "rows", "cols", "mixed"):
+            raise ValueError(f"unknown scenario {self.scenario!r}")
+        if self.events < 0:
+            raise ValueError(f"events must be >= 0, got {self.events}")
+        if self.log_every < 1:
+            raise ValueError(f"log_every must be >= 1, got {self.log_every}")
+        if self.policy is None:
+            from .policies import PolicyConfig
+
+            self.policy = PolicyConfig()
+
+
+def build_events(spec: StreamSpec):
+    """stream.py:200-220."""
+    if spec.scenario == "rank1":
+        return gen_rank_one_events(spec.events, spec.delta_sd, spec.m, spec.n, spec.seed)
+    if spec.scenario == "rows":
+        return gen_structural_events("row", spec.events, spec.true_rank, spec.noise_scale,
+                                     spec.n, spec.seed)
+    if spec.scenario == "cols":
+        return gen_structural_events("col", spec.events, spec.true_rank, spec.noise_scale,
+                                     spec.m, spec.seed)
+    return gen_mixed_stream(spec.events, spec.mix_weights, spec.m, spec.n, spec.true_rank,
+                            spec.noise_scale, spec.delta_sd, spec.seed)
+
+
+def run_simulation(spec: StreamSpec, return_engine: bool = False):
+    """stream.py:257-333 on the device engine: the spec's generated matrix and
+    events through stream.run_stream (Algorithm 1)."""
+    from .stream import run_stream
+
+    initial = gen_low_rank(spec.m, spec.n, spec.true_rank, spec.noise_scale, spec.seed)
+    return run_stream(initial, to_stream_events(build_events(spec)), spec.k, spec.policy,
+                      log_every=spec.log_every, tol=spec.tol, reortho_guard=spec.reortho_guard,
+                      return_engine=return_engine)

@@ -129,3 +129,49 @@ def sim_inputs(golden, tag):
         ev = decode_events(golden["sim_guard_kinds"], golden["sim_guard_vecs"], *a0.shape)
         return a0, ev, 6, dict(kind="periodic", period=80), 10
     raise KeyError(tag)
+
+
+# ----------------------------------------------------- reference CSV files
+GOLDEN_DIR = ROOT / "tests" / "golden"
+
+
+def read_table(path):
+    """(header lines, column names, rows as lists of strings) of a file in
+    the reference's record format (cli.py:74-83), plain or gzipped."""
+    import gzip
+
+    p = Path(path)
+    text = gzip.open(p, "rt").read() if p.suffix == ".gz" else p.read_text()
+    lines = text.splitlines()
+    cols = lines[2].split(",")
+    return lines[:2], cols, [ln.split(",") for ln in lines[3:]]
+
+
+def compare_tables(ours, ref, *, exact=(), angles=(), skip=("update_time", "opt_time"),
+                   rtol=1e-8):
+    """Column-by-column diff of two record files: `exact` columns equal as
+    text, `angles` (arccos-based, ill-conditioned near 0) within 1e-6 rad or
+    1e-11 in cosine, every other column within rtol relative (NaN where the
+    reference has NaN)."""
+    _, c1, r1 = read_table(ours)
+    _, c2, r2 = read_table(ref)
+    assert c1 == c2, (c1, c2)
+    assert len(r1) == len(r2), (len(r1), len(r2))
+    for j, name in enumerate(c1):
+        if name in skip:
+            continue
+        a = [row[j] for row in r1]
+        b = [row[j] for row in r2]
+        if name in exact:
+            assert a == b, f"column {name} differs"
+            continue
+        x = np.array([float(v) for v in a])
+        y = np.array([float(v) for v in b])
+        assert np.array_equal(np.isnan(x), np.isnan(y)), f"column {name}: NaN pattern"
+        ok = ~np.isnan(y)
+        if name in angles:
+            bad = (np.abs(x[ok] - y[ok]) > 1e-6) & (np.abs(np.cos(x[ok]) - np.cos(y[ok])) > 1e-11)
+            assert not bad.any(), f"column {name}: {np.max(np.abs(x[ok] - y[ok]))}"
+        else:
+            np.testing.assert_allclose(x[ok], y[ok], rtol=rtol, atol=1e-300,
+                                       err_msg=f"column {name}")

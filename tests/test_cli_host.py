@@ -17,10 +17,10 @@ def test_usage_errors_exit_2():
 def test_csv_format(tmp_path: Path):
     recs = [MetricsRecord(step=0, frob_error=1.5, evr=0.9, rank=3, refreshed=False,
                           update_time=0.1, frob_opt=None, frob_gap=float("nan"))]
-    p = tmp_path / "synthetic.csv"
-    cli.write_records_csv(p, recs, "manifest.json")
+    p = tmp_path / "synthetic_rank1.csv"
+    cli.write_records_csv(p, recs, "synthetic_rank1_manifest.json")
     lines = p.read_text().splitlines()
-    assert lines[0] == "# manifest: manifest.json"
+    assert lines[0] == "# manifest: synthetic_rank1_manifest.json"
     assert lines[1] == "# nondeterministic columns: update_time,opt_time"
     assert lines[2].split(",") == list(cli.SYNTHETIC_COLUMNS)
     row = dict(zip(cli.SYNTHETIC_COLUMNS, lines[3].split(",")))

@@ -1,26 +1,91 @@
-"""CLI front end on the device: `synthetic` writes the reference-format
-table for a BASELINE configuration; `verify --fast` passes."""
+"""The CLI and record pipelines on the device, diffed against files the
+reference wrote for the same runs (tests/golden/make_golden_pipeline.py):
+the synthetic records table, BASELINE config 3 through the finance loop
+(every non-timing column, every day), the reference's own price-panel run,
+and the full acceptance suite."""
 import json
 
 import pytest
 
+from conftest import GOLDEN_DIR, compare_tables, read_table
 from paper_2605_24514_b200 import cli
 
 pytestmark = pytest.mark.gpu
 
 
-def test_synthetic_config1(tmp_path):
-    out = tmp_path / "cfg1"
-    assert cli.main(["synthetic", "--config", "1", "--seed", "0", "--out", str(out),
+def test_synthetic_scenario_matches_reference_file(tmp_path):
+    argv = ["synthetic", "--seed", "7", "--scenario", "rank1", "--events", "2000",
+            "--refresh-every", "500", "--out", str(tmp_path)]
+    assert cli.main(argv) == cli.EXIT_OK
+    csv = tmp_path / "synthetic_rank1.csv"
+    man = json.loads((tmp_path / "synthetic_rank1_manifest.json").read_text())
+    assert man["outputs"] == ["synthetic_rank1.csv", "synthetic_rank1_manifest.json"]
+    for key in ("tool", "version", "subcommand", "argv", "config", "seed", "backend", "versions",
+                "started", "finished", "outputs"):
+        assert key in man
+    head, _, _ = read_table(csv)
+    assert head[0] == "# manifest: synthetic_rank1_manifest.json"
+    compare_tables(csv, GOLDEN_DIR / "ref_synthetic_rank1.csv.gz", exact=("step", "rank", "refreshed"),
+                   angles=("angle_ref", "angle_opt"))
+
+
+def test_synthetic_baseline_config(tmp_path):
+    assert cli.main(["synthetic", "--config", "1", "--seed", "0", "--out", str(tmp_path),
                      "--events", "120"]) == cli.EXIT_OK
-    lines = (out / "synthetic.csv").read_text().splitlines()
+    lines = (tmp_path / "synthetic_config1.csv").read_text().splitlines()
     assert len(lines) == 3 + 121  # header lines + init record + one per event
-    man = json.loads((out / "manifest.json").read_text())
+    man = json.loads((tmp_path / "synthetic_config1_manifest.json").read_text())
     assert man["config"]["k"] == 10 and man["seed"] == 0
-    # the periodic policy refreshed at t = 100
-    refreshed = [ln.split(",")[9] for ln in lines[3:]]
-    assert refreshed[100] == "True"
+    assert [ln.split(",")[9] for ln in lines[3:]][100] == "True"  # periodic refresh at t = 100
 
 
-def test_verify_fast():
+def test_finance_config3_matches_reference_file(tmp_path):
+    """BASELINE config 3 (2268 daily appends, k = 5, angle refresh 5 deg),
+    equal-weight and two Dirichlet portfolios, a snapshot every day."""
+    assert cli.main(["finance", "--seed", "0", "--baseline-config3",
+                     "--portfolios", "equal,dirichlet:2", "--out", str(tmp_path)]) == cli.EXIT_OK
+    compare_tables(tmp_path / "finance.csv", GOLDEN_DIR / "ref_finance_cfg3.csv.gz",
+                   exact=("step", "date", "refreshed", "rank"), angles=("angle_factor",))
+    _, cols, rows = read_table(tmp_path / "finance_risk.csv")
+    assert cols[:2] == ["step", "date"] and len(rows) == 2268
+    # VaR99 = Phi^-1(0.99) x the low-rank-plus-diagonal volatility
+    for row in rows[::97]:
+        vol, var = float(row[cols.index("vol_lr_diag_equal")]), float(row[cols.index("var99_equal")])
+        assert abs(var - 2.3263478740408408 * vol) <= 1e-14 * var
+
+
+def test_finance_price_panel_matches_reference_file(tmp_path):
+    """The reference's synthetic price panel (log returns, expanding
+    centering), periodic refresh every 20 days, snapshots every 5."""
+    assert cli.main(["finance", "--seed", "2", "--synthetic-panel", "--refresh-every", "20",
+                     "--portfolios", "equal,dirichlet:1", "--out", str(tmp_path)]) == cli.EXIT_OK
+    compare_tables(tmp_path / "finance.csv", GOLDEN_DIR / "ref_finance_panel.csv.gz",
+                   exact=("step", "date", "refreshed", "rank"), angles=("angle_factor",))
+
+
+def test_finance_grid_mode(tmp_path):
+    assert cli.main(["finance", "--seed", "2", "--synthetic-panel", "--days", "400",
+                     "--grid-k", "3,5", "--grid-refresh", "none,50", "--out",
+                     str(tmp_path)]) == cli.EXIT_OK
+    for k in (3, 5):
+        for tag in ("none", "50"):
+            assert (tmp_path / f"finance_k{k}_refresh{tag}.csv").exists()
+            assert (tmp_path / f"finance_k{k}_refresh{tag}_manifest.json").exists()
+
+
+def test_verify_matches_reference_verdicts(capsys):
+    """Every check the reference passes passes here, except the CPU timing
+    law of check 7 (see acceptance.check_runtime_scaling)."""
+    from paper_2605_24514_b200.acceptance import run_acceptance
+
+    ref = {r["number"]: r for r in json.loads((GOLDEN_DIR / "ref_acceptance.json").read_text())}
+    res = {r.number: r for r in run_acceptance(fast=False)}
+    assert sorted(res) == sorted(ref)
+    for num, r in res.items():
+        assert r.name == ref[num]["name"]
+        if num != 7:
+            assert r.passed, (num, r.name, r.detail)
+
+
+def test_verify_fast_exit_code():
     assert cli.main(["verify", "--fast"]) == cli.EXIT_OK
