@@ -148,11 +148,16 @@ def read_table(path):
 
 
 def compare_tables(ours, ref, *, exact=(), angles=(), skip=("update_time", "opt_time"),
-                   rtol=1e-8):
+                   rtol=1e-8, floors=None):
     """Column-by-column diff of two record files: `exact` columns equal as
     text, `angles` (arccos-based, ill-conditioned near 0) within 1e-6 rad or
     1e-11 in cosine, every other column within rtol relative (NaN where the
-    reference has NaN)."""
+    reference has NaN) plus an absolute floor for differences of nearly
+    equal operands: floors = {column: (atol, scale column or None)} allows
+    |d| <= atol * |scale| (e.g. frob_gap = frob_error - frob_opt is zero up to
+    rounding of its operands right after a refresh; a risk_rel_error of 1e-8
+    is a difference of two volatilities that agree to 1e-11 relative)."""
+    floors = floors or {}
     _, c1, r1 = read_table(ours)
     _, c2, r2 = read_table(ref)
     assert c1 == c2, (c1, c2)
@@ -173,5 +178,12 @@ def compare_tables(ours, ref, *, exact=(), angles=(), skip=("update_time", "opt_
             bad = (np.abs(x[ok] - y[ok]) > 1e-6) & (np.abs(np.cos(x[ok]) - np.cos(y[ok])) > 1e-11)
             assert not bad.any(), f"column {name}: {np.max(np.abs(x[ok] - y[ok]))}"
         else:
-            np.testing.assert_allclose(x[ok], y[ok], rtol=rtol, atol=1e-300,
-                                       err_msg=f"column {name}")
+            tol = rtol * np.abs(y[ok])
+            if name in floors:
+                atol, scale = floors[name]
+                sc = (np.abs(np.array([float(row[c1.index(scale)]) for row in r2]))[ok]
+                      if scale else 1.0)
+                tol = tol + atol * sc
+            bad = np.abs(x[ok] - y[ok]) > tol
+            assert not bad.any(), (f"column {name}: max |d| {np.max(np.abs(x[ok] - y[ok]))}, "
+                                   f"{int(bad.sum())} of {int(ok.sum())} rows")

@@ -12,6 +12,12 @@ from paper_2605_24514_b200 import cli
 
 pytestmark = pytest.mark.gpu
 
+# risk_rel_error = |vol_inc - vol_batch| / vol_batch is ~1e-8 .. 1e-5 here: its
+# rows agree when both volatilities agree with the reference's to 1e-11
+# relative; cov_rel_error likewise to 1e-11 of the covariance norm
+RISK_FLOORS = {"risk_rel_error_equal": (1e-11, None), "risk_rel_error_dirichlet1": (1e-11, None),
+               "risk_rel_error_dirichlet2": (1e-11, None), "cov_rel_error": (1e-11, None)}
+
 
 def test_synthetic_scenario_matches_reference_file(tmp_path):
     argv = ["synthetic", "--seed", "7", "--scenario", "rank1", "--events", "2000",
@@ -26,7 +32,7 @@ def test_synthetic_scenario_matches_reference_file(tmp_path):
     head, _, _ = read_table(csv)
     assert head[0] == "# manifest: synthetic_rank1_manifest.json"
     compare_tables(csv, GOLDEN_DIR / "ref_synthetic_rank1.csv.gz", exact=("step", "rank", "refreshed"),
-                   angles=("angle_ref", "angle_opt"))
+                   angles=("angle_ref", "angle_opt"), floors={"frob_gap": (1e-12, "frob_error")})
 
 
 def test_synthetic_baseline_config(tmp_path):
@@ -45,7 +51,8 @@ def test_finance_config3_matches_reference_file(tmp_path):
     assert cli.main(["finance", "--seed", "0", "--baseline-config3",
                      "--portfolios", "equal,dirichlet:2", "--out", str(tmp_path)]) == cli.EXIT_OK
     compare_tables(tmp_path / "finance.csv", GOLDEN_DIR / "ref_finance_cfg3.csv.gz",
-                   exact=("step", "date", "refreshed", "rank"), angles=("angle_factor",))
+                   exact=("step", "date", "refreshed", "rank"), angles=("angle_factor",),
+                   floors=RISK_FLOORS)
     _, cols, rows = read_table(tmp_path / "finance_risk.csv")
     assert cols[:2] == ["step", "date"] and len(rows) == 2268
     # VaR99 = Phi^-1(0.99) x the low-rank-plus-diagonal volatility
@@ -60,7 +67,8 @@ def test_finance_price_panel_matches_reference_file(tmp_path):
     assert cli.main(["finance", "--seed", "2", "--synthetic-panel", "--refresh-every", "20",
                      "--portfolios", "equal,dirichlet:1", "--out", str(tmp_path)]) == cli.EXIT_OK
     compare_tables(tmp_path / "finance.csv", GOLDEN_DIR / "ref_finance_panel.csv.gz",
-                   exact=("step", "date", "refreshed", "rank"), angles=("angle_factor",))
+                   exact=("step", "date", "refreshed", "rank"), angles=("angle_factor",),
+                   floors=RISK_FLOORS)
 
 
 def test_finance_grid_mode(tmp_path):
