@@ -22,6 +22,7 @@
 //   5. the reference's output conventions (_kernels.pyx:94-109): descending
 //      sort, snap below 1e-12 sigma_0, dead left columns completed over
 //      e_0, e_1, ... in order.
+#include <algorithm>
 #include <cooperative_groups.h>
 #include "common.cuh"
 #include "core_svd.cuh"
@@ -98,22 +99,15 @@ __device__ __forceinline__ void apply_rots(double* col, int64_t stride, const SM
 // every CTA's shared memory over DSMEM, and cluster barriers separate the
 // phases.  At B = 1 this spreads the 129-root core over CL SMs.
 template <int kN, bool WIDE, int CL>
-__global__ void __launch_bounds__(WIDE ? 512 : 32) arrow_svd_kernel(int n, const double* __restrict__ core,
-                                                       int64_t core_stride, int ldcore,
-                                                       double* __restrict__ uk,
-                                                       double* __restrict__ vk, int64_t out_stride,
-                                                       int ldo, double* __restrict__ sv,
-                                                       int64_t sv_stride, double* __restrict__ s_out,
-                                                       int64_t s_out_stride, int nkeep,
-                                                       const int* __restrict__ gate,
-                                                       ArrowFuse af) {
-  griddep_launch_dependents();
-  griddep_wait();
-  if (gate && *gate) return;
+__device__ __forceinline__ void arrow_body(int b, int n, const double* __restrict__ core,
+                                           int64_t core_stride, int ldcore,
+                                           double* __restrict__ uk, double* __restrict__ vk,
+                                           int64_t out_stride, int ldo, double* __restrict__ sv,
+                                           int64_t sv_stride, double* __restrict__ s_out,
+                                           int64_t s_out_stride, int nkeep, const ArrowFuse& af) {
   __shared__ ArrowSmem<kN> S;
   namespace cg = cooperative_groups;
   const int crank = CL > 1 ? (int)cg::this_cluster().block_rank() : 0;
-  const int b = blockIdx.x / CL;
   // cluster-wide barrier (release/acquire at cluster scope) or a CTA barrier
   auto csync = [&]() {
     if constexpr (CL > 1) cg::this_cluster().sync(); else __syncthreads();
@@ -709,6 +703,374 @@ __global__ void __launch_bounds__(WIDE ? 512 : 32) arrow_svd_kernel(int n, const
   }
 }
 
+// One CTA (CL > 1: one cluster) per core.  List mode (!WIDE, af.fb_list):
+// the cores arrow_cta_kernel handed back, *af.fb_count of them; the last
+// CTA to finish resets the list for the next tick.
+template <int kN, bool WIDE, int CL>
+__global__ void __launch_bounds__(WIDE ? 512 : 32, 1) arrow_svd_kernel(int n, const double* __restrict__ core,
+                                                       int64_t core_stride, int ldcore,
+                                                       double* __restrict__ uk,
+                                                       double* __restrict__ vk, int64_t out_stride,
+                                                       int ldo, double* __restrict__ sv,
+                                                       int64_t sv_stride, double* __restrict__ s_out,
+                                                       int64_t s_out_stride, int nkeep,
+                                                       const int* __restrict__ gate,
+                                                       ArrowFuse af) {
+  griddep_launch_dependents();
+  griddep_wait();
+  if (gate && *gate) return;
+  const bool list = !WIDE && CL == 1 && af.fb_list;
+  const int cnt = list ? *reinterpret_cast<volatile int*>(af.fb_count) : (int)(gridDim.x / CL);
+  const int step = list ? (int)gridDim.x : cnt;
+  // one call site (the body is inlined once)
+  for (int idx = blockIdx.x / CL; idx < cnt; idx += step)
+    arrow_body<kN, WIDE, CL>(list ? af.fb_list[idx] : idx, n, core, core_stride, ldcore, uk, vk,
+                             out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep, af);
+  if (list) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(af.fb_done, 1) == (int)gridDim.x - 1) {
+        *af.fb_count = 0;
+        *af.fb_done = 0;
+        __threadfence();
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Append core of a batched k <= 32 stream (s = r + 1 <= 33) on one CTA of
+// five warps: the same secular-equation solution as arrow_body (roots by the
+// two-pole rational iteration with bisection safeguard, Loewner zhat,
+// vectors from zhat, the reference's sort and snap), with four threads per
+// root / Loewner product / vector (the lanes of a quad split the poles and
+// combine their partial sums with an xor butterfly, so the quad's branch
+// decisions agree bit for bit) instead of one thread, Uk / Vk kept in shared
+// memory, and the fused epilogue (W <- [W 0; 0 1] Uk, Gv <- [Gv 0; 0 1/rho]
+// Vk on DMMA) spread over the five warps' row groups.  Cores that need
+// deflation (a tiny z entry, coincident poles), or with a dead singular
+// value, are handed to the one-warp kernel (list mode) untouched.
+constexpr int kACThreads = 160;
+constexpr int kACN = 40;   // root capacity (one quad each)
+constexpr int kACLd = 36;  // Uk / Vk tile pitch
+
+struct ArrowCtaSmem {
+  double Uk[33 * kACLd];
+  double Vk[33 * kACLd];
+  double d[kACN], z[kACN], kd[kACN], kz[kACN], mu[kACN], sig[kACN], zhat[kACN];
+  int kcol[kACN], order[kACN], org[kACN], pos[kACN];
+  double wmax[8];
+  double scale;
+};
+
+__global__ void __launch_bounds__(kACThreads, 6) arrow_cta_kernel(
+    int n, const double* __restrict__ core, int64_t core_stride, int ldcore,
+    double* __restrict__ sv, int64_t sv_stride, double* __restrict__ s_out, int64_t s_out_stride,
+    int nkeep, const int* __restrict__ gate, ArrowFuse af) {
+  if (gate && *gate) return;
+  extern __shared__ __align__(16) unsigned char ac_raw[];
+  ArrowCtaSmem& S = *reinterpret_cast<ArrowCtaSmem*>(ac_raw);
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int quad = tid >> 2, ql = tid & 3;
+  const unsigned qmask = 0xFu << (lane & 28);
+  const int r = n - 1;
+  const double eps = 2.220446049250313e-16;
+  const double* K = core + b * core_stride;
+  auto qsum = [&](double v) {
+    v += __shfl_xor_sync(qmask, v, 1);
+    return v + __shfl_xor_sync(qmask, v, 2);
+  };
+  // ---- zero the tiles (rows / columns beyond the core feed the DMMA epilogue)
+  for (int i = tid; i < 33 * kACLd; i += kACThreads) {
+    S.Uk[i] = 0.0;
+    S.Vk[i] = 0.0;
+  }
+  // ---- load and scale
+  double mx = 0.0;
+  if (tid < n) {
+    const double dc = tid < r ? fabs(K[tid * ldcore + tid]) : 0.0, zc = K[r * ldcore + tid];
+    S.d[tid] = dc;
+    S.z[tid] = zc;
+    mx = fmax(dc, fabs(zc));
+  }
+  mx = warp_max(mx);
+  if (lane == 0) S.wmax[warp] = mx;
+  __syncthreads();
+  if (tid == 0) {
+    double m2 = 0.0;
+    for (int w = 0; w < kACThreads / 32; ++w) m2 = fmax(m2, S.wmax[w]);
+    S.scale = m2 > 0.0 ? m2 : 1.0;
+  }
+  __syncthreads();
+  const double scale = S.scale;
+  if (tid < n) {
+    S.d[tid] /= scale;
+    S.z[tid] /= scale;
+  }
+  __syncthreads();
+  // ascending poles; ties: higher column first (the rho column r leads)
+  if (tid < n) {
+    const double dc = S.d[tid];
+    int rank = 0;
+    for (int e = 0; e < n; ++e) {
+      const double de = S.d[e];
+      rank += (de < dc) || (de == dc && e > tid);
+    }
+    S.order[rank] = tid;
+  }
+  __syncthreads();
+  // ---- deflation check (as arrow_body); none needed: every pole kept in order
+  {
+    const double tol = 8.0 * eps;
+    bool need = false;
+    if (tid < n) {
+      const int c = S.order[tid];
+      const double dc = S.d[c];
+      need = fabs(S.z[c]) <= tol;
+      if (tid > 0) need |= dc <= tol || dc - S.d[S.order[tid - 1]] <= tol;
+      S.kcol[tid] = c;
+      S.kd[tid] = tid == 0 ? 0.0 : dc;
+      S.kz[tid] = S.z[c];
+    }
+    if (__syncthreads_or(need)) {
+      if (tid == 0) af.fb_list[atomicAdd(af.fb_count, 1)] = b;
+      return;
+    }
+  }
+  const int N = n;
+  // ---- roots: quad i solves for sigma_i in (kd[i], kd[i+1]) (the last beyond kd[N-1])
+  if (quad < N) {
+    const int i = quad;
+    int o;
+    double lo, hi;
+    const double di = S.kd[i];
+    if (i < N - 1) {
+      const double dn = S.kd[i + 1];
+      const double sm = 0.5 * (di + dn);
+      const double mum = (sm - di) * (sm + di);
+      double f = 0.0;
+      for (int j = ql; j < N; j += 4) {
+        const double dj = S.kd[j];
+        f += S.kz[j] * S.kz[j] * frcp((dj - di) * (dj + di) - mum);
+      }
+      f = 1.0 + qsum(f);
+      if (f > 0.0) {
+        o = i; lo = 0.0; hi = mum;
+      } else {
+        o = i + 1; lo = (sm - dn) * (sm + dn); hi = 0.0;
+      }
+    } else {
+      o = i;
+      double zz = 0.0;
+      for (int j = ql; j < N; j += 4) zz += S.kz[j] * S.kz[j];
+      lo = 0.0;
+      hi = qsum(zz);
+    }
+    const double dorg = S.kd[o];
+    const double Di = (di - dorg) * (di + dorg);
+    const double Dn = (i < N - 1) ? (S.kd[i + 1] - dorg) * (S.kd[i + 1] + dorg) : 0.0;
+    double x = 0.5 * (lo + hi);
+    for (int it = 0; it < 80; ++it) {
+      double psi = 0.0, dpsi = 0.0, phi = 0.0, dphi = 0.0, aps = 0.0;
+      for (int j = ql; j < N; j += 4) {
+        const double dj = S.kd[j];
+        const double t = frcp((dj - dorg) * (dj + dorg) - x);
+        const double w = S.kz[j] * S.kz[j] * t;
+        if (j <= i) {
+          psi += w;
+          dpsi += w * t;
+        } else {
+          phi += w;
+          dphi += w * t;
+        }
+        aps += fabs(w);
+      }
+      psi = qsum(psi);
+      dpsi = qsum(dpsi);
+      phi = qsum(phi);
+      dphi = qsum(dphi);
+      aps = qsum(aps);
+      // identical in the four lanes from here on (xor-reduced inputs)
+      const double g = 1.0 + psi + phi;
+      if (g < 0.0) lo = x; else hi = x;
+      if (fabs(g) <= 4.0 * eps * (1.0 + aps) * N || !(g == g)) break;
+      const double pi_ = Di - x;
+      const double b1 = dpsi * pi_ * pi_;
+      const double a1 = psi - b1 / pi_;
+      double xn;
+      if (i < N - 1) {
+        const double qn = Dn - x;
+        const double b2 = dphi * qn * qn;
+        const double a2 = phi - b2 / qn;
+        const double A = 1.0 + a1 + a2;
+        const double Dl = Dn - Di;
+        const double B = A * Dl + b1 + b2, C = b1 * Dl;
+        const double disc = B * B - 4.0 * A * C;
+        xn = 0.5 * (lo + hi);
+        if (disc >= 0.0) {
+          const double qv = -0.5 * (B + copysign(sqrt(disc), B));
+          const double p1 = (A != 0.0) ? qv / A : -1e300;
+          const double p2 = (qv != 0.0) ? C / qv : -1e300;
+          const double x1 = Di - p1, x2 = Di - p2;
+          if (x1 > lo && x1 < hi) xn = x1;
+          else if (x2 > lo && x2 < hi) xn = x2;
+        }
+      } else {
+        const double A = 1.0 + a1 + phi;
+        xn = (A > 0.0) ? Di + b1 / A : 0.5 * (lo + hi);
+        if (!(xn > lo && xn < hi)) xn = 0.5 * (lo + hi);
+      }
+      if (fabs(xn - x) <= 2.0 * eps * fmax(fabs(xn), 1e-300) ||
+          hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi))) {
+        x = xn;
+        break;
+      }
+      x = xn;
+    }
+    if (ql == 0) {
+      S.org[i] = o;
+      S.mu[i] = x;
+      S.sig[i] = sqrt(dorg * dorg + x);
+    }
+  }
+  __syncthreads();
+  // ---- Loewner: zhat_j^2 = prod_k (sigma_k^2 - d_j^2) / prod_{k != j} (d_k^2 - d_j^2)
+  if (quad < N) {
+    const int j = quad;
+    const double dj = S.kd[j];
+    auto sdiff = [&](int k) {
+      const double dk = S.kd[S.org[k]];
+      return S.mu[k] - (dj - dk) * (dj + dk);
+    };
+    double acc = 1.0;
+    for (int k = ql; k < N - 1; k += 4) {
+      const double dk = k < j ? S.kd[k] : S.kd[k + 1];
+      acc *= sdiff(k) * frcp((dk - dj) * (dk + dj));
+    }
+    acc *= __shfl_xor_sync(qmask, acc, 1);
+    acc *= __shfl_xor_sync(qmask, acc, 2);
+    acc *= sdiff(N - 1);
+    if (ql == 0) S.zhat[j] = copysign(sqrt(fmax(acc, 0.0)), S.kz[j]);
+  }
+  // ---- sorted output positions: descending sigma, ties by index; sigma_max
+  double m1 = 0.0;
+  if (tid < n) {
+    const double st = S.sig[tid];
+    int rank = 0;
+    for (int e = 0; e < n; ++e) {
+      const double se = S.sig[e];
+      rank += (se > st) || (se == st && e < tid);
+    }
+    S.pos[tid] = rank;
+    m1 = st;
+  }
+  m1 = warp_max(m1);
+  if (lane == 0) S.wmax[warp] = m1;
+  __syncthreads();
+  double smax = 0.0;
+  for (int w = 0; w < kACThreads / 32; ++w) smax = fmax(smax, S.wmax[w]);
+  // ---- vectors into the shared tiles (quad per root)
+  bool dead = false;
+  if (quad < N) {
+    const int t = quad;
+    const int pc = S.pos[t];
+    const double dorg = S.kd[S.org[t]];
+    const double mu = S.mu[t];
+    double nv = 0.0, nu = 0.0;
+    for (int j = ql; j < N; j += 4) {
+      const double dj = S.kd[j];
+      const double vj = S.zhat[j] * frcp((dj - dorg) * (dj + dorg) - mu);
+      nv = fma(vj, vj, nv);
+      nu = fma(dj * vj, dj * vj, nu);
+    }
+    nv = qsum(nv);
+    nu = 1.0 + qsum(nu);  // the z-row entry of u is -1
+    const double iv = rsqrt(nv), iu = rsqrt(nu);
+    const double sg = S.sig[t];
+    dead = !(sg > 0.0) || sg < kZeroSvRtol * smax;
+    for (int j = ql; j < N; j += 4) {
+      const double dj = S.kd[j];
+      const double vj = S.zhat[j] * frcp((dj - dorg) * (dj + dorg) - mu);
+      const int row = S.kcol[j];
+      S.Vk[row * kACLd + pc] = vj * iv;
+      if (row != r) S.Uk[row * kACLd + pc] = dj * vj * iu;
+    }
+    if (ql == 0) S.Uk[r * kACLd + pc] = -iu;
+  }
+  if (__syncthreads_or(dead)) {
+    if (tid == 0) af.fb_list[atomicAdd(af.fb_count, 1)] = b;
+    return;
+  }
+  // install sigma; columns >= keep of the tiles out of the rotation
+  const int keep = nkeep;
+  if (tid < n) {
+    const int pc = S.pos[tid];
+    const double v = S.sig[tid] * scale;
+    sv[b * sv_stride + pc] = v;
+    if (s_out && pc < keep) s_out[b * s_out_stride + pc] = v;
+  }
+  for (int idx = tid; idx < n * 32; idx += kACThreads) {
+    const int i = idx >> 5, cc = idx & 31;
+    if (cc >= keep) {
+      S.Uk[i * kACLd + cc] = 0.0;
+      S.Vk[i * kACLd + cc] = 0.0;
+    }
+  }
+  __syncthreads();
+  // ---- fused epilogue: W <- [W 0; 0 1] Uk[:, :keep], Gv <- [Gv 0; 0 1/rho] Vk[:, :keep]
+  double* uwb = af.uw.p + b * af.uw.stride;
+  double* gwb = af.gw.p + b * af.gw.stride;
+  const int nwg = af.uw_mode == 2 ? (af.uw_rows + 7) / 8 : 0;
+  const int ngg = (af.gw_rows + 7) / 8;
+  const int g = lane >> 2, q = lane & 3;
+  for (int item = warp; item < nwg + ngg; item += kACThreads / 32) {
+    const bool isw = item < nwg;
+    double* X = isw ? uwb : gwb;
+    const int ld = isw ? af.uw.ld : af.gw.ld;
+    const int rows = isw ? af.uw_rows : af.gw_rows;
+    const double* Q = isw ? S.Uk : S.Vk;
+    const int row0 = 8 * (isw ? item : item - nwg);
+    const int row = row0 + g;
+    double a[8];
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const int k = kk * 4 + q;
+      a[kk] = (row < rows && k < r) ? X[(int64_t)row * ld + k] : 0.0;
+    }
+    double d[4][2];
+#pragma unroll
+    for (int nn = 0; nn < 4; ++nn) d[nn][0] = d[nn][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk)
+#pragma unroll
+      for (int nn = 0; nn < 4; ++nn)
+        dmma_8x8x4(d[nn][0], d[nn][1], a[kk], Q[(kk * 4 + q) * kACLd + nn * 8 + g]);
+    if (row < rows) {
+#pragma unroll
+      for (int nn = 0; nn < 4; ++nn) {
+        const int c0 = nn * 8 + 2 * q;
+        if (c0 < ld) *reinterpret_cast<double2*>(X + (int64_t)row * ld + c0) = make_double2(d[nn][0], d[nn][1]);
+      }
+    }
+  }
+  // new rows: W[uw_rows] = Uk[r, :keep] (mode 2) or W = Uk[:, :keep] (mode 1);
+  // Gv[gw_rows] = (1/rho) Vk[r, :keep]
+  if (af.uw_mode == 1) {
+    for (int idx = tid; idx < n * af.uw.ld; idx += kACThreads) {
+      const int i = idx / af.uw.ld, cc = idx % af.uw.ld;
+      uwb[(int64_t)i * af.uw.ld + cc] = cc < 32 ? S.Uk[i * kACLd + cc] : 0.0;
+    }
+  } else if (tid < af.uw.ld) {
+    uwb[(int64_t)af.uw_rows * af.uw.ld + tid] = tid < 32 ? S.Uk[r * kACLd + tid] : 0.0;
+  }
+  if (tid >= 64 && tid - 64 < af.gw.ld) {
+    const int cc = tid - 64;
+    gwb[(int64_t)af.gw_rows * af.gw.ld + cc] = cc < 32 ? af.inj[b] * S.Vk[r * kACLd + cc] : 0.0;
+  }
+}
+
 }  // namespace
 
 int read_arrow_counters(int64_t* out4, int reset) {
@@ -731,12 +1093,24 @@ int launch_arrow_svd(int batch, int s, const double* core, int64_t core_stride, 
     return ISVD_EINVAL;
   }
   if (batch == 0) return ISVD_OK;
-  if (s <= 40) {
+  if (s <= 33 && af && af->uw_mode && af->fb_list) {
+    // steady state of a batched k <= 32 stream: CTA per core, then the
+    // one-warp kernel on the cores it handed back (deflation, dead sigma)
+    arrow_cta_kernel<<<batch, kACThreads, sizeof(ArrowCtaSmem), st>>>(
+        s, core, core_stride, ldcore, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate, *af);
+    ISVD_LAUNCHED();
+    const int grid = std::min(batch, 4 * 148);
+    arrow_svd_kernel<40, false, 1><<<grid, 32, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
+                                                        out_stride, ldo, sv, sv_stride, s_out,
+                                                        s_out_stride, nkeep, g_gate, *af);
+  } else if (s <= 40) {
     // one warp per core: roots 32..39 (s = 33 is the k = 32 append core) are
     // solved warp-cooperatively after the one-root-per-lane pass
+    ArrowFuse a1 = af ? *af : ArrowFuse{};
+    a1.fb_list = nullptr;
     arrow_svd_kernel<40, false, 1><<<batch, 32, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
                                                          out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate,
-                                                         af ? *af : ArrowFuse{});
+                                                         a1);
   } else if (batch <= kClusterMaxBatch) {
     // few wide cores (config 5b: one 129 core per tick): a cluster per core
     cudaLaunchConfig_t cfg = {};

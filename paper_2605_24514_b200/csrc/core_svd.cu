@@ -17,6 +17,8 @@
 // an odd pitch (bank-conflict-free column walks).  Each warp owns a pair per
 // round; lanes stride over rows; three warp-shuffle reductions give
 // a_pp, a_qq, a_pq.  For s > kSmemMaxS, V is kept in a global scratch.
+#include <algorithm>
+#include <cstdlib>
 #include "common.cuh"
 #include "core_svd.cuh"
 #include "tick.cuh"
@@ -505,14 +507,13 @@ __device__ __forceinline__ void j32c_round(double (&x)[32], int lane, double2* c
 }
 
 template <bool BUILD>
-__global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32c_kernel(
-    int s, const double* __restrict__ core, int64_t core_stride, int ldcore, double* __restrict__ uk,
-    double* __restrict__ vk, int64_t out_stride, int ldo, double* __restrict__ sv,
-    int64_t sv_stride, int batch, Rank1Core rc, double* __restrict__ s_out, int64_t s_out_stride) {
+__device__ __forceinline__ void j32c_body(
+    int b, int s, const double* __restrict__ core, int64_t core_stride, int ldcore,
+    double* __restrict__ uk, double* __restrict__ vk, int64_t out_stride, int ldo,
+    double* __restrict__ sv, int64_t sv_stride, const Rank1Core& rc, double* __restrict__ s_out,
+    int64_t s_out_stride) {
   extern __shared__ __align__(16) unsigned char j32_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int b = blockIdx.x * kJ32Warps + warp;
-  if (b >= batch) return;
   J32Smem& W = reinterpret_cast<J32Smem*>(j32_raw)[warp];
   double* nrmv = W.nrm;
   int* pos = W.pos;
@@ -879,6 +880,675 @@ __global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32c_kernel(
   }
 }
 
+
+// One warp per core.  List mode (rc.fb_list, BUILD): the cores that
+// rank1_fast_kernel handed back, *fb_count of them; the last CTA to finish
+// resets the list for the next tick.
+template <bool BUILD>
+__global__ void __launch_bounds__(kJ32Warps * 32, 3) jacobi32c_kernel(
+    int s, const double* __restrict__ core, int64_t core_stride, int ldcore, double* __restrict__ uk,
+    double* __restrict__ vk, int64_t out_stride, int ldo, double* __restrict__ sv,
+    int64_t sv_stride, int batch, Rank1Core rc, double* __restrict__ s_out, int64_t s_out_stride) {
+  const int warp = threadIdx.x >> 5;
+  if constexpr (!BUILD) {
+    const int b = blockIdx.x * kJ32Warps + warp;
+    if (b >= batch) return;
+    j32c_body<false>(b, s, core, core_stride, ldcore, uk, vk, out_stride, ldo, sv, sv_stride, rc,
+                     s_out, s_out_stride);
+    return;
+  }
+  const bool list = BUILD && rc.fb_list;
+  const int cnt = list ? *reinterpret_cast<volatile int*>(rc.fb_count) : batch;
+  const int step = list ? gridDim.x * kJ32Warps : cnt;
+  // one call site (the body is inlined once)
+  for (int idx = blockIdx.x * kJ32Warps + warp; idx < cnt; idx += step)
+    j32c_body<BUILD>(list ? rc.fb_list[idx] : idx, s, core, core_stride, ldcore, uk, vk, out_stride,
+                     ldo, sv, sv_stride, rc, s_out, s_out_stride);
+  if (list) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(rc.fb_done, 1) == (int)gridDim.x - 1) {
+        *rc.fb_count = 0;
+        *rc.fb_done = 0;
+        __threadfence();
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Rank-1 Brand core on one CTA (4 warps) from the structure of
+// K = diag(s) + delta a b^T (_kernels.pyx:190-237: the core of the
+// projection rule, engine.py:149-167).  For a well-conditioned core (every
+// s live and within a factor of 100, the steady state of a rank-1 stream)
+// two simultaneous Jacobi steps reach the reference's stop (|M_pq| <=
+// 1e-14 sqrt(M_pp M_qq), _kernels.pyx:38-59), as j32_step does, but
+//   * the first Gram M1 = K^T K = diag(s^2) + delta (s o a) b^T + delta
+//     b (s o a)^T + delta^2 |a|^2 b b^T is formed from the structure
+//     (O(s^2) scalar work, no DMMA),
+//   * the first rotation G1 = K J1 = K + diag(s)(J1 - I) + delta a
+//     (b^T (J1 - I)) also from the structure (J1 = I + Theta1 +
+//     Theta1^2 / 2, Theta1^2 on DMMA, symmetric: upper tiles only),
+//   * only the second step (Gram of G1, first-order rotation G2 = G1 (I +
+//     Theta2)) runs on dense 32 x 32 products -- 80 + 128 DMMA.8x8x4
+//     instead of 544 for two dense steps;
+// the work of one core is split over four warps (tiles and row groups), so
+// the per-core dependent chain is ~4x shorter than the one-warp kernel's.
+// V follows from the structure (v = K^T g / sigma^2, as formula_v), and the
+// epilogue rotates the deferred bases (W rows by warps 0-1, Gv rows by
+// warps 2-3) straight from the shared-memory Uk / Vk.
+// Cores outside the fast path (close or dead singular values, a third
+// step, delta == 0) are appended to a list and finished by the one-warp
+// kernel (jacobi32c_kernel, list mode) with the engine state untouched;
+// the tracked entry / N / read-back ring are updated here for every core.
+constexpr int kR1Threads = 128;
+constexpr int kLdT = 36;  // row pitch: conflict-free A (row g) / B (row q) fragment reads and row stores
+
+struct R1Smem {
+  double T0[32 * kLdT];  // Theta1 -> J1 - I -> Theta2 -> Uk
+  double T1[32 * kLdT];  // G1 -> G2 -> Vk
+  double a[32], bv[32], sv[32], d[32], beta[32], inv[32], nrm2[32];
+  double red[2][4][32];
+  double wt[4];
+  int wv[4];
+  int pos[32], ipos[32];
+  int status;
+};
+
+__device__ __forceinline__ void r1_tile(int idx, int& mi, int& ni) {
+  // upper-triangular 4 x 4 tile enumeration (10 tiles)
+  mi = idx < 4 ? 0 : (idx < 7 ? 1 : (idx < 9 ? 2 : 3));
+  ni = idx < 4 ? idx : (idx < 7 ? idx - 3 : (idx < 9 ? idx - 5 : 3));
+}
+
+// X[0:rows, :] <- X[0:rows, 0:r] Q (Q: 32 x 32 in shared memory, pitch kLdT,
+// zero beyond r rows / keep columns), row groups rg0, rg0 + step, ... of one
+// warp; the next group's operands are loaded before this group's stores.
+__device__ __forceinline__ void r1_rotate(double* X, int ld, int rows, int r, const double* Q,
+                                          int rg0, int step) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  auto load_a = [&](double (&a)[8], int row0) {
+    const int row = row0 + g;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const int k = kk * 4 + q;
+      a[kk] = (row < rows && k < r) ? X[(int64_t)row * ld + k] : 0.0;
+    }
+  };
+  double a[8];
+  if (8 * rg0 < rows) load_a(a, 8 * rg0);
+  for (int row0 = 8 * rg0; row0 < rows; row0 += 8 * step) {
+    double an[8];
+    if (row0 + 8 * step < rows) load_a(an, row0 + 8 * step);
+    double d[4][2];
+#pragma unroll
+    for (int nn = 0; nn < 4; ++nn) d[nn][0] = d[nn][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk)
+#pragma unroll
+      for (int nn = 0; nn < 4; ++nn)
+        dmma_8x8x4(d[nn][0], d[nn][1], a[kk], Q[(kk * 4 + q) * kLdT + nn * 8 + g]);
+    const int row = row0 + g;
+    if (row < rows) {
+#pragma unroll
+      for (int nn = 0; nn < 4; ++nn) {
+        const int c0 = nn * 8 + 2 * q;
+        if (c0 < ld) *reinterpret_cast<double2*>(X + (int64_t)row * ld + c0) = make_double2(d[nn][0], d[nn][1]);
+      }
+    }
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) a[kk] = an[kk];
+  }
+}
+
+__global__ void __launch_bounds__(kR1Threads, 8) rank1_fast_kernel(
+    int s, int batch, Rank1Core rc, double* __restrict__ uk, double* __restrict__ vk,
+    int64_t out_stride, int ldo, double* __restrict__ sv_out, int64_t sv_stride,
+    double* __restrict__ s_out, int64_t s_out_stride, int* __restrict__ fb_list,
+    int* __restrict__ fb_count) {
+  extern __shared__ __align__(16) unsigned char r1_raw[];
+  R1Smem& S = *reinterpret_cast<R1Smem*>(r1_raw);
+  const int b = blockIdx.x;
+  if (b >= batch) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int c = lane;          // column handled in the scalar phases
+  const int r0 = 8 * warp;     // and its rows r0 .. r0 + 7
+  double* T0 = S.T0;
+  double* T1 = S.T1;
+  const int64_t ii = rc.ii[b], jj = rc.jj[b];
+  const double del = rc.delta[b];
+  // ---- gathers (K6, _kernels.pyx:209-213) through the deferred bases:
+  // a = U[i, :] = [U_base 0; 0 I] W, b = V_eff[j, :] = [V | Z^T] G; thread
+  // (c, warp) forms the partial over a quarter of the contraction
+  {
+    const LazyBasis& lz = rc.lz;
+    double pa = 0.0, pb = 0.0;
+    if (c < s) {
+      if (!lz.active) {
+        if (warp == 0) pa = rc.U.p[b * rc.U.stride + ii * rc.U.ld + c];
+      } else if (ii >= lz.m_base) {
+        if (warp == 0) pa = lz.W.p[b * lz.W.stride + (lz.r_base + (ii - lz.m_base)) * lz.W.ld + c];
+      } else {
+        const double* ur = rc.U.p + b * rc.U.stride + ii * rc.U.ld;
+        const double* Wb = lz.W.p + b * lz.W.stride;
+        double uv[8], wv[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const int k = r0 + t;
+          const bool ok = k < lz.r_base;
+          uv[t] = ok ? ur[k] : 0.0;
+          wv[t] = ok ? Wb[k * lz.W.ld + c] : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < 8; ++t) pa = fma(uv[t], wv[t], pa);
+      }
+      const VDefer& vd = rc.vd;
+      const double* vr = rc.V.p + b * rc.V.stride + jj * rc.V.ld;
+      if (!vd.G) {
+        if (warp == 0) pb = vr[c];
+      } else {
+        const double* Gb = vd.G + b * vd.g_stride;
+        const double* Zb = vd.Z ? vd.Z + b * vd.z_stride + jj : nullptr;
+        double vv[10], gv[10];
+#pragma unroll
+        for (int t = 0; t < 10; ++t) {
+          const int k = 10 * warp + t;
+          double x = 0.0, y = 0.0;
+          if (k < vd.fw) {
+            x = vr[k];
+            y = Gb[k * vd.ldg + c];
+          } else if (k - vd.fw < vd.nz) {
+            x = Zb[(int64_t)(k - vd.fw) * vd.ldz];
+            y = Gb[k * vd.ldg + c];
+          }
+          vv[t] = x;
+          gv[t] = y;
+        }
+#pragma unroll
+        for (int t = 0; t < 10; ++t) pb = fma(vv[t], gv[t], pb);
+      }
+    }
+    S.red[0][warp][c] = pa;
+    S.red[1][warp][c] = pb;
+    if (tid < 32) S.sv[c] = c < s ? rc.s[(int64_t)b * rc.lds + c] : 0.0;
+    if (tid == 0 && rc.A) {
+      double* e = rc.A + b * rc.a_stride + ii * rc.lda + jj;
+      const double old = *e;
+      *e = old + del;
+      const double nn = rc.N[b] + (2.0 * del * old + del * del);
+      rc.N[b] = nn;
+      if (rc.ring) {
+        rc.ring[b] = nn;
+        rc.ring[rc.ring_stride + b] = rc.rho[b];
+        rc.ring[2 * rc.ring_stride + b] = rc.xnorm[b];
+      }
+    }
+  }
+  __syncthreads();
+  if (tid < 32) {
+    S.a[c] = ((S.red[0][0][c] + S.red[0][1][c]) + S.red[0][2][c]) + S.red[0][3][c];
+    S.bv[c] = ((S.red[1][0][c] + S.red[1][1][c]) + S.red[1][2][c]) + S.red[1][3][c];
+  }
+  __syncthreads();
+  // ---- column norms of K (K_rc = (delta a_r) b_c + [r == c] s_c) and the gate
+  const double bc = S.bv[c], sc = S.sv[c];
+  {
+    double p = 0.0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int r = r0 + t;
+      double k = (del * S.a[r]) * bc;
+      if (r == c) k += sc;
+      p = fma(k, k, p);
+    }
+    S.red[0][warp][c] = p;
+  }
+  __syncthreads();
+  if (tid < 32) {
+    const double dc = ((S.red[0][0][c] + S.red[0][1][c]) + S.red[0][2][c]) + S.red[0][3][c];
+    S.d[c] = dc;
+    const double smax = warp_max(c < s ? sc : 0.0);
+    const double smin = -warp_max(c < s ? -sc : -1e300);
+    const double a2 = warp_sum(S.a[c] * S.a[c]);
+    const double dmax = warp_max(dc);
+    if (c == 0) {
+      S.beta[0] = a2;
+      S.beta[1] = fmax(1e-30 * dmax, 1e-290);  // null2
+      // delta == 0 (a rejected device payload is staged as (0, 0, 0.0)) must
+      // leave the factors unchanged bit for bit: the one-warp kernel's exact
+      // path.  Outside the structure gate (a dead or a >100x smaller s): sweeps.
+      S.status = del == 0.0 ? -1 : ((smin > 0.0 && smin >= 1e-2 * smax) ? 1 : 2);
+    }
+  }
+  __syncthreads();
+  if (S.status < 0) {
+    if (tid == 0) fb_list[atomicAdd(fb_count, 1)] = b;
+    return;
+  }
+  const double a2 = S.beta[0], null2 = S.beta[1];
+  bool sweep = S.status == 2;
+  int steps = 0, nsw = 0;
+  // warp-level reduction of (violation, max |theta|) -> block verdict:
+  // 0 converged, 1 second-order step, 2 first-order step, -1 over the cap
+  auto verdict = [&](bool viol, double tmax) {
+    const bool wv = __any_sync(0xffffffffu, viol);
+    const double wt = warp_max(tmax);
+    if (lane == 0) {
+      S.wv[warp] = wv;
+      S.wt[warp] = wt;
+    }
+    __syncthreads();
+    const bool v = S.wv[0] | S.wv[1] | S.wv[2] | S.wv[3];
+    const double tm = fmax(fmax(S.wt[0], S.wt[1]), fmax(S.wt[2], S.wt[3]));
+    __syncthreads();  // S.wv / S.wt reusable
+    return !v ? 0 : (tm > 1e-4 ? -1 : (tm > 1e-8 ? 1 : 2));
+  };
+  // T0 <- J - I = Theta + Theta^2 / 2 (Theta skew in T0; Theta^2 symmetric:
+  // upper tiles on DMMA, mirrored)
+  auto second_order = [&]() {
+    double acc[3][2], th[3][2];
+#pragma unroll
+    for (int nt = 0; nt < 3; ++nt) {
+      const int idx = warp + 4 * nt;
+      if (idx >= 10) break;
+      int mi, ni;
+      r1_tile(idx, mi, ni);
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        dmma_8x8x4(d0, d1, T0[(8 * mi + g) * kLdT + 4 * kk + q], T0[(4 * kk + q) * kLdT + 8 * ni + g]);
+      acc[nt][0] = d0;
+      acc[nt][1] = d1;
+      const double2 tv = *reinterpret_cast<const double2*>(&T0[(8 * mi + g) * kLdT + 8 * ni + 2 * q]);
+      th[nt][0] = tv.x;
+      th[nt][1] = tv.y;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int nt = 0; nt < 3; ++nt) {
+      const int idx = warp + 4 * nt;
+      if (idx >= 10) break;
+      int mi, ni;
+      r1_tile(idx, mi, ni);
+      const int r = 8 * mi + g, cc = 8 * ni + 2 * q;
+      *reinterpret_cast<double2*>(&T0[r * kLdT + cc]) =
+          make_double2(fma(0.5, acc[nt][0], th[nt][0]), fma(0.5, acc[nt][1], th[nt][1]));
+      if (mi != ni) {
+        T0[cc * kLdT + r] = fma(0.5, acc[nt][0], -th[nt][0]);
+        T0[(cc + 1) * kLdT + r] = fma(0.5, acc[nt][1], -th[nt][1]);
+      }
+    }
+    __syncthreads();
+  };
+  // K (K_rc = (delta a_r) b_c + [r == c] s_c) into T1
+  auto build_k = [&]() {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int r = r0 + t;
+      double k = (del * S.a[r]) * bc;
+      if (r == c) k += sc;
+      T1[r * kLdT + c] = k;
+    }
+  };
+  // ---- simultaneous steps (as j32_step) on G in T1: Gram on DMMA (upper
+  // tiles), rotation G <- G + G (J - I); true once G meets the reference's
+  // stop (|theta| <= 1e-8 for the last step: O(1e-16) off-diagonals left)
+  auto dense_steps = [&](int maxit) -> bool {
+    bool done = false;
+  for (int it = 0; it < maxit && !done; ++it) {
+    double th[3][2];
+    bool viol = false;
+    double tmax = 0.0;
+#pragma unroll
+    for (int nt = 0; nt < 3; ++nt) {
+      const int idx = warp + 4 * nt;
+      if (idx >= 10) break;
+      int mi, ni;
+      r1_tile(idx, mi, ni);
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        dmma_8x8x4(d0, d1, T1[(4 * kk + q) * kLdT + 8 * mi + g], T1[(4 * kk + q) * kLdT + 8 * ni + g]);
+      th[nt][0] = d0;
+      th[nt][1] = d1;
+      if (mi == ni) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          if (g == 2 * q + e) S.d[8 * mi + g] = e ? d1 : d0;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int nt = 0; nt < 3; ++nt) {
+      const int idx = warp + 4 * nt;
+      if (idx >= 10) break;
+      int mi, ni;
+      r1_tile(idx, mi, ni);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = 8 * mi + g, cc = 8 * ni + 2 * q + e;
+        const double dr = S.d[r], dc = S.d[cc], m = th[nt][e];
+        const bool live = r != cc && dr > null2 && dc > null2;
+        viol |= live && m * m > (kOrthoEps * kOrthoEps) * (dr * dc);
+        const double t = live ? m * j32_rcp1(dc - dr) : 0.0;
+        tmax = fmax(tmax, (t - t == 0.0) ? fabs(t) : 1e300);
+        th[nt][e] = t;
+      }
+    }
+    const int stv = verdict(viol, tmax);
+    if (stv == 0) {
+      done = true;
+      break;
+    }
+    if (stv < 0) break;
+#pragma unroll
+    for (int nt = 0; nt < 3; ++nt) {
+      const int idx = warp + 4 * nt;
+      if (idx >= 10) break;
+      int mi, ni;
+      r1_tile(idx, mi, ni);
+      const int r = 8 * mi + g, cc = 8 * ni + 2 * q;
+      *reinterpret_cast<double2*>(&T0[r * kLdT + cc]) = make_double2(th[nt][0], th[nt][1]);
+      if (mi != ni) {
+        T0[cc * kLdT + r] = -th[nt][0];
+        T0[(cc + 1) * kLdT + r] = -th[nt][1];
+      }
+    }
+    __syncthreads();
+    if (stv == 1) second_order();
+    // G <- G + G (J - I): warp w owns row tile w
+    double d[4][2];
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) d[ni][0] = d[ni][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const double av = T1[(8 * warp + g) * kLdT + 4 * kk + q];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+        dmma_8x8x4(d[ni][0], d[ni][1], av, T0[(4 * kk + q) * kLdT + 8 * ni + g]);
+    }
+    double2 gn[4];
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const double2 gv = *reinterpret_cast<const double2*>(&T1[(8 * warp + g) * kLdT + 8 * ni + 2 * q]);
+      gn[ni] = make_double2(gv.x + d[ni][0], gv.y + d[ni][1]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+      *reinterpret_cast<double2*>(&T1[(8 * warp + g) * kLdT + 8 * ni + 2 * q]) = gn[ni];
+    __syncthreads();
+    ++steps;
+    if (stv == 2) done = true;  // |theta| <= 1e-8: O(1e-16) off-diagonals left
+  }
+    return done;
+  };
+  if (!sweep) {
+    // ---- step 1: Theta1 from the structured Gram (theta_rc = M_rc / (d_c - d_r))
+    int st1;
+    {
+      bool viol = false;
+      double tmax = 0.0;
+      const double dc = S.d[c];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int r = r0 + t;
+        const double dr = S.d[r];
+        const bool live = r != c && dr > null2 && dc > null2;
+        double th = 0.0;
+        if (live) {
+          // symmetric in (r, c) bit for bit: operands in (min, max) order
+          const int p = min(r, c), qx = max(r, c);
+          const double m = del * fma(S.sv[p] * S.a[p], S.bv[qx], (S.sv[qx] * S.a[qx]) * S.bv[p]) +
+                           ((del * del) * a2) * (S.bv[r] * bc);
+          viol |= m * m > (kOrthoEps * kOrthoEps) * (dr * dc);
+          th = m * j32_rcp1(dc - dr);
+          tmax = fmax(tmax, (th - th == 0.0) ? fabs(th) : 1e300);
+        }
+        T0[r * kLdT + c] = th;
+      }
+      st1 = verdict(viol, tmax);
+    }
+    if (st1 < 0) {
+      sweep = true;
+    } else {
+      if (st1 == 1) second_order();
+      if (st1 > 0) {
+        ++steps;
+        // beta = b^T (J1 - I)
+        double p = 0.0;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) p = fma(S.bv[r0 + t], T0[(r0 + t) * kLdT + c], p);
+        S.red[0][warp][c] = p;
+        __syncthreads();
+        if (tid < 32) S.beta[c] = ((S.red[0][0][c] + S.red[0][1][c]) + S.red[0][2][c]) + S.red[0][3][c];
+        __syncthreads();
+      }
+      // G1 = K + K (J1 - I) = K + diag(s) (J1 - I) + (delta a) beta^T   (G1 = K when st1 == 0)
+      {
+        const double betac = st1 > 0 ? S.beta[c] : 0.0;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const int r = r0 + t;
+          const double da = del * S.a[r];
+          double k = da * bc;
+          if (r == c) k += sc;
+          double gv = k;
+          if (st1 > 0) gv = k + fma(S.sv[r], T0[r * kLdT + c], da * betac);
+          T1[r * kLdT + c] = gv;
+        }
+      }
+      __syncthreads();
+      // ---- steps 2..4 (dense): G meets the stop, or the sweeps take over
+      if (st1 == 1 && !dense_steps(3)) sweep = true;
+    }
+  }
+  if (sweep) {
+    // ---- close or graded singular values: one-sided Jacobi sweeps from K
+    // with the reference's rotation and stop (_kernels.pyx:38-59), V
+    // accumulated in T0.  Circle-method pairing, 16 pairs per round, 8
+    // threads per pair (rows sub, sub + 8, ...); the pair's Gram entries
+    // are reduced by an xor butterfly, so all 8 threads agree bit for bit.
+    // Inside the structure gate, a first sweep whose rotations were all
+    // below kConvRel leaves O(1e-12) off-diagonals (quadratic convergence):
+    // the simultaneous steps finish G and V follows from the structure (as
+    // the one-warp kernel's one-sweep exit).
+    const bool gate_ok = S.status == 1;
+    build_k();
+#pragma unroll
+    for (int t = 0; t < 8; ++t) T0[(r0 + t) * kLdT + c] = (r0 + t == c && c < s) ? 1.0 : 0.0;
+    __syncthreads();
+    const int pr = tid >> 3, sub = tid & 7;
+    bool conv = false;
+    for (int sw = 0; sw < kMaxSweeps && !conv; ++sw) {
+      ++nsw;
+      bool rot = false;
+      float relmax = 0.0f;
+      for (int rr = 0; rr < 31; ++rr) {
+        const int x0 = tour_slot(pr, rr, 32), x1 = tour_slot(31 - pr, rr, 32);
+        const int p = min(x0, x1), qq = max(x0, x1);
+        double gp[4], gq[4], app = 0.0, aqq = 0.0, apq = 0.0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int i = sub + 8 * k;
+          gp[k] = T1[i * kLdT + p];
+          gq[k] = T1[i * kLdT + qq];
+          app = fma(gp[k], gp[k], app);
+          aqq = fma(gq[k], gq[k], aqq);
+          apq = fma(gp[k], gq[k], apq);
+        }
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+          app += __shfl_xor_sync(0xffffffffu, app, o);
+          aqq += __shfl_xor_sync(0xffffffffu, aqq, o);
+          apq += __shfl_xor_sync(0xffffffffu, apq, o);
+        }
+        const double pq = app * aqq;
+        if (qq < s && apq * apq > (kOrthoEps * kOrthoEps) * pq) {
+          relmax = fmaxf(relmax, __fdividef((float)(apq * apq), (float)pq));
+          // zeta = (aqq - app) / (2 apq), t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)),
+          // c = 1 / sqrt(1 + t^2), s = c t, in the overflow-safe form
+          // u = |d| + sqrt(d^2 + h^2) (d = aqq - app, h = 2 apq): c = u / sqrt(u^2 + h^2)
+          const double d = aqq - app, h = 2.0 * apq;
+          const double big = fmax(fabs(d), fabs(h));
+          double cs, sn;
+          if (big < 1e150 && big > 1e-140) {
+            const double x2 = fma(d, d, h * h);
+            const double u = fabs(d) + x2 * j32_rsqrt(x2);
+            const double qv = j32_rsqrt(fma(u, u, h * h));
+            cs = u * qv;
+            sn = (d < 0.0 ? -h : h) * qv;
+          } else {
+            const double zeta = d / h;
+            const double t = zeta >= 0.0 ? 1.0 / (zeta + sqrt(1.0 + zeta * zeta))
+                                         : -1.0 / (-zeta + sqrt(1.0 + zeta * zeta));
+            cs = 1.0 / sqrt(1.0 + t * t);
+            sn = t * cs;
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int i = sub + 8 * k;
+            T1[i * kLdT + p] = cs * gp[k] - sn * gq[k];
+            T1[i * kLdT + qq] = sn * gp[k] + cs * gq[k];
+            const double vp = T0[i * kLdT + p], vq = T0[i * kLdT + qq];
+            T0[i * kLdT + p] = cs * vp - sn * vq;
+            T0[i * kLdT + qq] = sn * vp + cs * vq;
+          }
+          rot = true;
+        }
+        __syncthreads();
+      }
+      const bool wr = __any_sync(0xffffffffu, rot);
+      const float wm = (float)warp_max((double)relmax);
+      if (lane == 0) {
+        S.wv[warp] = wr;
+        S.wt[warp] = wm;
+      }
+      __syncthreads();
+      const bool any = S.wv[0] | S.wv[1] | S.wv[2] | S.wv[3];
+      const double rm = fmax(fmax(S.wt[0], S.wt[1]), fmax(S.wt[2], S.wt[3]));
+      __syncthreads();
+      conv = !any;
+      if (!conv && sw == 0 && gate_ok && rm <= kConvRel * kConvRel) {
+        if (dense_steps(3)) {
+          sweep = false;  // V from the structure below
+          conv = true;
+        }
+        break;
+      }
+    }
+    if (!conv) {
+      if (tid == 0) fb_list[atomicAdd(fb_count, 1)] = b;
+      return;
+    }
+  }
+  // ---- sigma = column norms of G, stable descending order (_kernels.pyx:94-101)
+  {
+    double p = 0.0, pd = 0.0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const double gv = T1[(r0 + t) * kLdT + c];
+      p = fma(gv, gv, p);
+      pd = fma(S.a[r0 + t], gv, pd);
+    }
+    S.red[0][warp][c] = p;
+    S.red[1][warp][c] = pd;
+  }
+  __syncthreads();
+  if (tid < 32) {
+    const double n2 = ((S.red[0][0][c] + S.red[0][1][c]) + S.red[0][2][c]) + S.red[0][3][c];
+    const double ad = ((S.red[1][0][c] + S.red[1][1][c]) + S.red[1][2][c]) + S.red[1][3][c];
+    const double myn = sqrt(n2);
+    S.nrm2[c] = myn;
+    __syncwarp();
+    int rank = 0;
+    for (int p2 = 0; p2 < 32; ++p2) {
+      const double o = S.nrm2[p2];
+      rank += (o > myn) || (o == myn && p2 < c);
+    }
+    const double s0 = warp_max(myn);
+    const bool live = myn > 0.0 && !(myn < kZeroSvRtol * s0);
+    const bool dead = __any_sync(0xffffffffu, c < s && !live);
+    __syncwarp();
+    S.pos[c] = rank;
+    S.ipos[rank] = c;
+    S.inv[c] = (c < s && live) ? 1.0 / myn : 0.0;
+    S.d[c] = (c < s && live) ? 1.0 / n2 : 0.0;
+    S.beta[c] = del * ad;  // delta (a . g_c)
+    if (c == 0) S.status = dead ? -1 : 0;
+    if (!dead && c < s) {
+      sv_out[b * sv_stride + rank] = myn;
+      if (s_out) s_out[b * s_out_stride + rank] = myn;
+    }
+  }
+  __syncthreads();
+  if (S.status < 0) {
+    if (tid == 0) fb_list[atomicAdd(fb_count, 1)] = b;
+    return;
+  }
+  if (tid == 0) {
+    atomicAdd(&g_debug_counters[1], 1ull);
+    if (sweep) {
+      atomicAdd(&g_debug_counters[0], (unsigned long long)nsw);
+    } else {
+      atomicAdd(&g_debug_counters[2], (unsigned long long)steps);
+      atomicAdd(&g_debug_counters[3], 1ull);
+    }
+  }
+  // ---- Uk = G / sigma (sorted columns) -> T0; Vk = K^T g / sigma^2 -> T1
+  {
+    const int pc = S.pos[c];
+    const double iv = S.inv[c], in2 = S.d[c], dt = S.beta[c];
+    double vv[8], uu[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int k = r0 + t;
+      const double gv = T1[k * kLdT + c];
+      uu[t] = gv * iv;  // 0 for columns >= s (iv = 0); rows >= s of G are 0
+      // sweeps: the accumulated rotations; steps: the structure (v = K^T g / sigma^2)
+      vv[t] = sweep ? (c < s ? T0[k * kLdT + c] : 0.0) : fma(S.sv[k], gv, S.bv[k] * dt) * in2;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      T0[(r0 + t) * kLdT + pc] = uu[t];
+      T1[(r0 + t) * kLdT + pc] = vv[t];
+    }
+  }
+  __syncthreads();
+  // ---- outputs: deferred window W (warps 0-1), deferred right basis Gv (warps 2-3)
+  if (warp < 2) {
+    if (rc.uw_mode == 2) {
+      r1_rotate(rc.uw.p + b * rc.uw.stride, rc.uw.ld, rc.uw_rows, s, T0, warp, 2);
+    } else if (rc.uw_mode == 1) {
+      double* uwb = rc.uw.p + b * rc.uw.stride;
+      for (int idx = tid; idx < s * rc.uw.ld; idx += 64) {
+        const int i = idx / rc.uw.ld, cc = idx % rc.uw.ld;
+        uwb[(int64_t)i * rc.uw.ld + cc] = cc < s ? T0[i * kLdT + cc] : 0.0;
+      }
+    } else {
+      double* U = uk + b * out_stride;
+      for (int idx = tid; idx < s * s; idx += 64) {
+        const int i = idx / s, cc = idx % s;
+        U[i * ldo + cc] = T0[i * kLdT + cc];
+      }
+    }
+  } else {
+    if (rc.gw_rows > 0) {
+      r1_rotate(rc.gw.p + b * rc.gw.stride, rc.gw.ld, rc.gw_rows, s, T1, warp - 2, 2);
+    } else {
+      double* Vo = rc.vk_out ? rc.vk_out + b * rc.vk_stride : vk + b * out_stride;
+      const int ldv = rc.vk_out ? rc.ldvk : ldo;
+      for (int idx = tid - 64; idx < s * s; idx += 64) {
+        const int i = idx / s, cc = idx % s;
+        Vo[i * ldv + cc] = T1[i * kLdT + cc];
+      }
+    }
+  }
+}
+
 }  // namespace
 
 int read_debug_counters(int64_t* out, int reset) {
@@ -914,8 +1584,30 @@ int launch_rank1_core_svd32(int batch, int s, const Rank1Core& rc, double* uk, d
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  jacobi32c_kernel<true><<<ceil_div(batch, kJ32Warps), kJ32Warps * 32, smem, st>>>(
-      s, nullptr, 0, 0, uk, vk, out_stride, ldo, sv, sv_stride, batch, rc, s_out, s_out_stride);
+  // ISVD_RANK1_WARP=1 (A/B experiments): the one-warp kernel for every core
+  static const bool warp_only = [] {
+    const char* v = getenv("ISVD_RANK1_WARP");
+    return v && v[0] == '1';
+  }();
+  if (!rc.fb_list || warp_only) {
+    Rank1Core direct = rc;
+    direct.fb_list = nullptr;
+    jacobi32c_kernel<true><<<ceil_div(batch, kJ32Warps), kJ32Warps * 32, smem, st>>>(
+        s, nullptr, 0, 0, uk, vk, out_stride, ldo, sv, sv_stride, batch, direct, s_out, s_out_stride);
+    ISVD_LAUNCHED();
+    return ISVD_OK;
+  }
+  // CTA-per-core structured fast path, then the one-warp kernel on the cores
+  // it handed back (tracked entry / N / ring already updated: A = nullptr)
+  rank1_fast_kernel<<<batch, kR1Threads, sizeof(R1Smem), st>>>(
+      s, batch, rc, uk, vk, out_stride, ldo, sv, sv_stride, s_out, s_out_stride, rc.fb_list,
+      rc.fb_count);
+  ISVD_LAUNCHED();
+  Rank1Core fb = rc;
+  fb.A = nullptr;
+  const int grid = std::min(ceil_div(batch, kJ32Warps), 2 * 148);
+  jacobi32c_kernel<true><<<grid, kJ32Warps * 32, smem, st>>>(
+      s, nullptr, 0, 0, uk, vk, out_stride, ldo, sv, sv_stride, batch, fb, s_out, s_out_stride);
   ISVD_LAUNCHED();
   return ISVD_OK;
 }

@@ -67,6 +67,12 @@ struct Rank1Core {
   double* vk_out = nullptr;
   int64_t vk_stride = 0;
   int ldvk = 0;
+  // Fallback list (batch ints) and its count / completion counters (one int
+  // each, zero between ticks): with fb_list set, a CTA-per-core structured
+  // kernel factors the well-conditioned cores and the one-warp Jacobi the rest
+  int* fb_list = nullptr;
+  int* fb_count = nullptr;
+  int* fb_done = nullptr;
 };
 // K = diag(s) + delta U[i,:]^T Vt[:,j]^T built in registers and factored by
 // the warp Jacobi (s <= 32); also applies A[i,j] += delta and the N update.
@@ -95,6 +101,11 @@ struct ArrowFuse {
   Mat zU{}, zV{};
   int zm = 0, zn = 0;
   VDefer zvd{};
+  // fallback list (as Rank1Core): with fb_list set and s <= 33, a CTA-per-core
+  // secular kernel takes the cores without deflation, the one-warp kernel the rest
+  int* fb_list = nullptr;
+  int* fb_count = nullptr;
+  int* fb_done = nullptr;
 };
 int launch_arrow_svd(int batch, int s, const double* core, int64_t core_stride, int ldcore,
                      double* uk, double* vk, int64_t out_stride, int ldo, double* sv,

@@ -239,6 +239,7 @@ struct isvd_engine {
   double* ed = nullptr;
   int* dflag = nullptr;
   unsigned* zf_cnt = nullptr;  // per-stream CTA arrival counts (fused zero-sigma completion)
+  int* fbbuf = nullptr;        // rank-1 fallback list [0, B), counts [B, 2B), done counts [2B, 3B)
   double* ref = nullptr;
   int ref_m = 0, ref_r = 0, ref_cap = 0;
   bool has_ref = false;
@@ -672,7 +673,9 @@ struct isvd_engine {
     dfree(core); dfree(uk); dfree(vk); dfree(sv); dfree(vscr);
     dfree(z); dfree(inj); dfree(rho); dfree(xnorm); dfree(ev);
     dfree(ei); dfree(ej); dfree(ed); dfree(dflag);
-    if (zf_cnt) cudaFree(zf_cnt); dfree(ref); dfree(W); dfree(Gv); dfree(Zv);
+    if (zf_cnt) cudaFree(zf_cnt);
+    if (fbbuf) cudaFree(fbbuf);
+    dfree(ref); dfree(W); dfree(Gv); dfree(Zv);
     dfree(wx); dfree(wj); dfree(wpart); dfree(wout); dfree(wflags);
     dfree(snap.U); dfree(snap.V); dfree(snap.A); dfree(snap.s); dfree(snap.N); dfree(snap.ref);
     dfree(shv);
@@ -762,7 +765,9 @@ int isvd_engine_create(isvd_engine** out, int batch, int m, int n, int k, double
   A(dalloc(&e->sring, (size_t)isvd_engine::kRing * 3 * batch));
   if (rc == ISVD_OK) {
     if (cudaMalloc((void**)&e->zf_cnt, sizeof(unsigned) * batch) != cudaSuccess ||
-        cudaMemset(e->zf_cnt, 0, sizeof(unsigned) * batch) != cudaSuccess) {
+        cudaMemset(e->zf_cnt, 0, sizeof(unsigned) * batch) != cudaSuccess ||
+        cudaMalloc((void**)&e->fbbuf, sizeof(int) * 3 * batch) != cudaSuccess ||
+        cudaMemset(e->fbbuf, 0, sizeof(int) * 3 * batch) != cudaSuccess) {
       set_error("out of device memory");
       rc = ISVD_ENOMEM;
     }
@@ -946,6 +951,9 @@ static int issue_append(isvd_engine* e, const Slice& sl, const double* xd, int l
     af.zV = mat_at(e->Vm(), b0);
     af.zn = e->n;
     af.zvd = e->vdesc(b0, e->vnz + 1);
+    af.fb_list = e->fbbuf + b0;
+    af.fb_count = e->fbbuf + e->B + b0;
+    af.fb_done = e->fbbuf + 2 * e->B + b0;
   }
   if (e->append_jacobi)
     ISVD_TRY(launch_core_svd(nb, r + 1, core, cs, S, uk, vk, cs, S, sv, S,
@@ -1058,6 +1066,9 @@ static int issue_rank_one(isvd_engine* e, const Slice& sl, const int64_t* di, co
     rc.ring_stride = e->B;
     rc.rho = e->rho + b0;
     rc.xnorm = e->xnorm + b0;
+    rc.fb_list = e->fbbuf + b0;
+    rc.fb_count = e->fbbuf + e->B + b0;
+    rc.fb_done = e->fbbuf + 2 * e->B + b0;
     if (vp) {
       rc.vd = e->vdesc(b0, e->vnz);
     } else if (defer) {
@@ -1852,7 +1863,7 @@ int isvd_engine_frob_error(isvd_engine* e, double* out) {
   if (e) e->join();
   if (!e || !e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
   ISVD_TRY(e->flush());
-  ISVD_TRY(e->ensure_work(0, 0, (int64_t)e->B * frob_nblk(e->m), e->B));
+  ISVD_TRY(e->ensure_work(0, 0, (int64_t)e->B * frob_nblk(e->m, e->n), e->B));
   ISVD_TRY(launch_frob_error_sq(e->B, e->m, e->n, e->r, e->A, e->astride(), e->n_cap, e->Um(), e->s,
                                 e->ld, e->Vm(), e->wpart, e->wout, e->st));
   ISVD_TRY(e->allreduce(e->wout, e->B));  // row shards: sum of the per-shard squares

@@ -10,53 +10,99 @@ namespace isvd {
 
 namespace {
 
-constexpr int kFrobRows = 32;   // rows per CTA
-constexpr int kFrobCols = 64;   // V rows staged per chunk
+constexpr int kFT = 64;        // output tile edge (rows of A x columns of A)
+constexpr int kFC = 32;        // contraction chunk (singular triplets)
+constexpr int kFLd = kFC + 4;  // [kFT][kFLd] staging: conflict-free fragment loads and row stores
 constexpr int kWMax = 160;
 
-// ||A - U diag(s) V^T||_F^2 partial sums over a 32-row slab.
-__global__ void __launch_bounds__(256) frob_partial_kernel(int m, int n, int w, const double* A,
-                                                          int64_t a_stride, int lda, Mat U,
-                                                          const double* s, int lds, Mat V,
-                                                          double* partial, int nblk) {
-  extern __shared__ double sm[];
-  double* us = sm;                          // [kFrobRows][w+1]
-  double* vs = sm + kFrobRows * (w + 1);    // [kFrobCols][w+1]
+// ||A - U diag(s) V^T||_F^2 over one 64 x 64 tile of A (metrics.py:74-76):
+// the reconstruction tile (U diag s) V^T is contracted on the FP64 tensor
+// path (DMMA.8x8x4, 8 warps x (16 x 32) sub-tiles, 32-triplet chunks staged
+// in shared memory with a register prefetch of the next chunk), the tile of
+// A is loaded into registers before the contraction, and the epilogue
+// squares the residual in the accumulator layout.  One partial per tile,
+// summed in a fixed order by reduce_partials_kernel (deterministic).
+__global__ void __launch_bounds__(256) frob_tile_kernel(int m, int n, int w, const double* A,
+                                                       int64_t a_stride, int lda, Mat U,
+                                                       const double* s, int lds, Mat V,
+                                                       double* partial, int nblk) {
+  __shared__ __align__(16) double Xs[kFT][kFLd];  // (U diag s) rows
+  __shared__ __align__(16) double Vs[kFT][kFLd];  // V rows
   __shared__ double red[32];
-  const int b = blockIdx.y, blk = blockIdx.x;
-  const int row0 = blk * kFrobRows;
-  const double* Ab = A ? A + b * a_stride : nullptr;
+  const int b = blockIdx.z;
+  const int row0 = blockIdx.x * kFT, col0 = blockIdx.y * kFT;
+  const double* Ab = A + b * a_stride;
   const double* Ub = U.p + b * U.stride;
   const double* Vb = V.p + b * V.stride;
   const double* sb = s + (int64_t)b * lds;
-  const int W1 = w + 1;
-  for (int idx = threadIdx.x; idx < kFrobRows * w; idx += blockDim.x) {
-    int i = idx / w, t = idx % w;
-    int row = row0 + i;
-    us[i * W1 + t] = row < m ? Ub[(int64_t)row * U.ld + t] * sb[t] : 0.0;
-  }
-  double acc = 0.0;
-  for (int c0 = 0; c0 < n; c0 += kFrobCols) {
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < kFrobCols * w; idx += blockDim.x) {
-      int j = idx / w, t = idx % w;
-      int col = c0 + j;
-      vs[j * W1 + t] = col < n ? Vb[(int64_t)col * V.ld + t] : 0.0;
-    }
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < kFrobRows * kFrobCols; idx += blockDim.x) {
-      int i = idx / kFrobCols, j = idx % kFrobCols;
-      int row = row0 + i, col = c0 + j;
-      if (row < m && col < n) {
-        double rec = 0.0;
-        for (int t = 0; t < w; ++t) rec = fma(us[i * W1 + t], vs[j * W1 + t], rec);
-        double d = Ab[(int64_t)row * lda + col] - rec;
-        acc = fma(d, d, acc);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int mt0 = (warp >> 1) * 2, nt0 = (warp & 1) * 4;
+  // the A entries this thread's accumulators cover, loaded up front
+  double av[2][4][2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t)
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = row0 + (mt0 + t) * 8 + g, j = col0 + (nt0 + u) * 8 + 2 * q + e;
+        av[t][u][e] = (i < m && j < n) ? Ab[(int64_t)i * lda + j] : 0.0;
       }
+  // loader: element k of thread tid -> (row = idx / 32, triplet = idx % 32)
+  double vx[8], vv[8];
+  auto fetch = [&](int c0) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int idx = tid + k * 256;
+      const int rr = idx >> 5, cc = idx & 31, t = c0 + cc;
+      const bool tin = t < w;
+      vx[k] = (tin && row0 + rr < m) ? Ub[(int64_t)(row0 + rr) * U.ld + t] * sb[t] : 0.0;
+      vv[k] = (tin && col0 + rr < n) ? Vb[(int64_t)(col0 + rr) * V.ld + t] : 0.0;
+    }
+  };
+  double acc[2][4][2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
+  fetch(0);
+  for (int c0 = 0; c0 < w; c0 += kFC) {
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int idx = tid + k * 256;
+      Xs[idx >> 5][idx & 31] = vx[k];
+      Vs[idx >> 5][idx & 31] = vv[k];
+    }
+    __syncthreads();
+    if (c0 + kFC < w) fetch(c0 + kFC);
+#pragma unroll
+    for (int kk = 0; kk < kFC / 4; ++kk) {
+      const int kc = kk * 4 + q;
+      double a[2], bf[4];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) a[t] = Xs[(mt0 + t) * 8 + g][kc];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) bf[u] = Vs[(nt0 + u) * 8 + g][kc];
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) dmma_8x8x4(acc[t][u][0], acc[t][u][1], a[t], bf[u]);
     }
   }
-  double tot = block_sum(acc, red);
-  if (threadIdx.x == 0) partial[(int64_t)b * nblk + blk] = tot;
+  double sq = 0.0;
+#pragma unroll
+  for (int t = 0; t < 2; ++t)
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double d = av[t][u][e] - acc[t][u][e];  // out-of-range entries: 0 - 0
+        sq = fma(d, d, sq);
+      }
+  const double tot = block_sum(sq, red);
+  if (tid == 0) partial[(int64_t)b * nblk + (int64_t)blockIdx.y * gridDim.x + blockIdx.x] = tot;
 }
 
 // out[b] = sum_k partial[b][k] (fixed order: per-thread strided then tree)
@@ -86,7 +132,7 @@ __global__ void defect_kernel(int w, const double* G, double* out) {
 
 }  // namespace
 
-int frob_nblk(int m) { return ceil_div(m, kFrobRows); }
+int frob_nblk(int m, int n) { return ceil_div(m, kFT) * ceil_div(n, kFT); }
 
 int launch_frob_error_sq(int batch, int m, int n, int w, const double* A, int64_t a_stride, int lda,
                          Mat U, const double* s, int lds, Mat V, double* partial, double* out,
@@ -95,18 +141,17 @@ int launch_frob_error_sq(int batch, int m, int n, int w, const double* A, int64_
     set_error("frob_error: width too large");
     return ISVD_EINVAL;
   }
-  int nblk = frob_nblk(m);
-  size_t smem = sizeof(double) * (kFrobRows + kFrobCols) * (w + 1);
-  static bool attr = false;
-  if (!attr) {
-    ISVD_CUDA(cudaFuncSetAttribute(frob_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   200 * 1024));
-    attr = true;
+  if (batch == 0) return ISVD_OK;
+  const int gx = ceil_div(m, kFT), gy = ceil_div(n, kFT);
+  if (gy > 65535 || batch > 65535) {
+    set_error("frob_error: matrix too wide");
+    return ISVD_EINVAL;
   }
-  frob_partial_kernel<<<dim3(nblk, batch), 256, smem, st>>>(m, n, w, A, a_stride, lda, U, s, lds, V,
-                                                            partial, nblk);
+  const int nblk = gx * gy;
+  frob_tile_kernel<<<dim3(gx, gy, batch), 256, 0, st>>>(m, n, w, A, a_stride, lda, U, s, lds, V,
+                                                        partial, nblk);
   ISVD_LAUNCHED();
-  reduce_partials_kernel<<<dim3(1, batch), 256, 0, st>>>(partial, nblk, 1, out);
+  reduce_partials_kernel<<<dim3(1, batch), 1024, 0, st>>>(partial, nblk, 1, out);
   ISVD_LAUNCHED();
   return ISVD_OK;
 }

@@ -6,8 +6,8 @@
 
 namespace isvd {
 
-int frob_nblk(int m);
-// out[b] = ||A[b] - U[b] diag(s[b]) V[b]^T||_F^2 ; partial: batch * frob_nblk(m)
+int frob_nblk(int m, int n);
+// out[b] = ||A[b] - U[b] diag(s[b]) V[b]^T||_F^2 ; partial: batch * frob_nblk(m, n)
 int launch_frob_error_sq(int batch, int m, int n, int w, const double* A, int64_t a_stride, int lda,
                          Mat U, const double* s, int lds, Mat V, double* partial, double* out,
                          cudaStream_t st);

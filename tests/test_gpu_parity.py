@@ -507,3 +507,88 @@ def test_rank_one_orthogonality_near_the_structure_gate(kappa):
     assert rel_err(f.s, oe.factors.s) < SIGMA_RTOL
     assert sine_angle(f.u, oe.factors.u) < ANGLE_TOL
     assert sine_angle(f.vt.T, oe.factors.vt.T) < ANGLE_TOL
+
+
+def test_rank_one_fast_and_fallback_cores_in_one_launch():
+    """One batched rank-1 launch holding every kind of core: streams with a
+    well-separated spectrum take the structured simultaneous steps, streams
+    with a repeated singular value (first-order angle above its cap) or
+    sigma_max / sigma_min > 100 the in-CTA Jacobi sweeps, and delta == 0
+    entries the one-warp kernel's exact path (list mode).  Every stream
+    matches its own oracle, and both the step and the sweep paths ran."""
+    rng = np.random.default_rng(11)
+    m, n, k, T, B = 72, 48, 12, 40, 48
+    a0s = []
+    for b in range(B):
+        qu = np.linalg.qr(rng.standard_normal((m, k)))[0]
+        qv = np.linalg.qr(rng.standard_normal((n, k)))[0]
+        kind = b % 3
+        if kind == 0:
+            sig = np.linspace(10.0, 2.0, k)            # fast path
+        elif kind == 1:
+            sig = np.linspace(10.0, 2.0, k)
+            sig[4] = sig[3]                             # repeated value: fallback
+        else:
+            sig = np.geomspace(10.0, 10.0 / 500.0, k)   # outside the kappa gate: fallback
+        a0s.append((qu * sig) @ qv.T)
+    a0 = np.stack(a0s)
+    eng = BatchedSvdEngine(a0, k)
+    oes = [OracleEngine(a0[b], k) for b in range(B)]
+    lib = _lib.load()
+    cnt = (C.c_int64 * 8)()
+    lib.isvd_debug_counters(cnt, 1)
+    for t in range(T):
+        ii, jj = rng.integers(0, m, B), rng.integers(0, n, B)
+        dd = rng.normal(0.0, 1e-2, B)
+        if t % 4 == 0:
+            dd[::5] = 0.0
+        eng.rank_one_update(ii, jj, dd)
+        for b in range(B):
+            oes[b].rank_one_update(int(ii[b]), int(jj[b]), float(dd[b]))
+    eng.synchronize()
+    lib.isvd_debug_counters(cnt, 1)
+    cores, fast = cnt[1], cnt[7]
+    assert cores == B * T and 0 < fast < cores, (cores, fast)
+    du, dv = eng.ortho_defect()
+    assert np.max(du) <= 1e-12 and np.max(dv) <= 1e-12
+    for b in range(B):
+        f, fo = eng.factors(b), oes[b].factors
+        assert rel_err(f.s, fo.s) < SIGMA_RTOL, b
+        assert sine_angle(f.u, fo.u) < ANGLE_TOL, b
+        assert sine_angle(f.vt.T, fo.vt.T) < ANGLE_TOL, b
+        assert np.array_equal(eng.tracked(b), oes[b].tracked), b
+
+
+def test_row_append_cta_and_fallback_cores_in_one_launch():
+    """Batched row appends (deferred bases, fused epilogue) whose cores go
+    both ways in one launch: ordinary rows take the CTA-per-core secular
+    kernel; in-span rows of exactly low-rank streams (rho below tol, a zero
+    z entry) and zero rows need deflation and are handed to the one-warp
+    kernel (list mode).  Every stream matches its own oracle."""
+    rng = np.random.default_rng(12)
+    B, m, n, k, T = 64, 60, 40, 12, 36
+    ys = [rng.standard_normal((n, k)) for _ in range(B)]
+    a0 = np.stack([rng.standard_normal((m, k)) @ ys[b].T +
+                   (0.0 if b % 3 == 0 else 0.05) * rng.standard_normal((m, n)) for b in range(B)])
+    eng = BatchedSvdEngine(a0, k)
+    oes = [OracleEngine(a0[b], k) for b in range(B)]
+    for t in range(T):
+        x = np.empty((B, n))
+        for b in range(B):
+            if b % 3 == 0:
+                x[b] = ys[b] @ rng.standard_normal(k)  # in the row space: rho ~ 0
+            elif b % 3 == 1 and t % 5 == 0:
+                x[b] = 0.0
+            else:
+                x[b] = ys[b] @ rng.standard_normal(k) + 0.05 * rng.standard_normal(n)
+        eng.row_append(x)
+        for b in range(B):
+            oes[b].row_append(x[b])
+    du, dv = eng.ortho_defect()
+    assert np.max(du) <= 1e-12 and np.max(dv) <= 1e-12
+    for b in range(B):
+        f, fo = eng.factors(b), oes[b].factors
+        assert rel_err(f.s, fo.s) < SIGMA_RTOL, b
+        assert sine_angle(f.u, fo.u) < ANGLE_TOL, b
+        assert sine_angle(f.vt.T, fo.vt.T) < ANGLE_TOL, b
+        assert np.array_equal(eng.tracked(b), oes[b].tracked), b
