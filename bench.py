@@ -57,7 +57,7 @@ DMMA_PEAK_TFS = 37.06  # measured FP64 DMMA.8x8x4 peak, profiles/r01_fp64_peaks.
 def _ncu_summary():
     """Per-kernel ncu --set full figures committed under profiles/ (for the
     roofline `traffic` field); {} when absent."""
-    for p in sorted((ROOT / "profiles").glob("r*_ncu_summary.json"), reverse=True):
+    for p in sorted((ROOT / "profiles").glob("r*_tick_ncu_summary.json"), reverse=True):
         try:
             return json.loads(p.read_text()), p.name
         except Exception:
@@ -325,11 +325,12 @@ def _simulate_bytes(B, steps, window=32, vwin=8):
 def _simulate_flops(B, steps, window=32, vwin=8, rank1_steps=2.0):
     """Algorithmic FP64 flops of the two core kernels over `steps` ticks,
     following the same data flow as _simulate_bytes:
-    * rank-1 tick (jacobi32c): the core factorisation as the simultaneous
-      Jacobi steps run it -- per step the 32 x 32 Gram (2 k^3, symmetric half
-      counted in full as DMMA computes it), Theta^2 on the first step, and
-      G (J - I) (2 k^3 each) -- plus the fused rotations of the deferred
-      bases: W (rows_W x k) . Uk and G (rows_G x k) . Vk (2 rows k^2 each);
+    * rank-1 tick (rank1_fast_kernel): the core factorisation as the
+      simultaneous Jacobi steps run it -- the first step from the structure
+      of K (Gram and rotation O(k^2), Theta^2 2 k^3), each further step the
+      32 x 32 Gram (2 k^3) and G (J - I) (2 k^3) -- plus the fused rotations
+      of the deferred bases: W (rows_W x k) . Uk and G (rows_G x k) . Vk
+      (2 rows k^2 each);
     * row tick (arrow): the secular solve is O(k^2) (counted as 40 (k+1)^2)
       plus the fused rotations [W 0; 0 1] . Q and [G 0; 0 1] . Vk (2 rows (k+1) k).
     Returns (rank-1 flops, row flops)."""
@@ -337,7 +338,7 @@ def _simulate_flops(B, steps, window=32, vwin=8, rank1_steps=2.0):
     f_r1 = f_row = 0.0
     b_rows, active = 0, False
     vpend, nz = False, 0
-    core = 2.0 * k ** 3 * (3.0 + 2.0 * max(0.0, rank1_steps - 1.0))
+    core = 2.0 * k ** 3 * (1.0 + 2.0 * max(0.0, rank1_steps - 1.0))
     for t in range(steps):
         row = t % 2 == 0
         g_rows = (k + nz) if vpend else 0
@@ -666,9 +667,9 @@ def run_gpu(args):
         # epilogues), so their bytes are accounted with them
         kernels = {
             "project_append (K1, row ticks)": {"ms": float(ph[0]), "bytes": proj_bytes},
-            "arrow_svd + fused W/G rotation (K2a, row ticks)": {
+            "append core + fused W/G rotation (K2a, row ticks)": {
                 "ms": float(ph[1] + ph[2]), "bytes": rot_row},
-            "jacobi32c + fused W/G rotation (K2b, rank-1 ticks)": {
+            "rank-1 core + fused W/G rotation (K2b, rank-1 ticks)": {
                 "ms": float(ph[4] + ph[5] + ph[6]), "bytes": rot_r1},
             "rotate U flush (K3, deferred)": {"ms": flush_ms, "bytes": flush_bytes},
             "V materialisation (K3, every 8 row appends)": {"ms": max(0.0, tot(3) - flush_ms),
@@ -682,8 +683,8 @@ def run_gpu(args):
         # algorithmic flops of the two FP64-latency-bound core kernels
         r1_steps = float(dbg[6]) / max(1, int(dbg[7])) if dbg[7] else 2.0
         f_r1, f_row = _simulate_flops(B, diag_steps, window, rank1_steps=r1_steps)
-        kernels["jacobi32c + fused W/G rotation (K2b, rank-1 ticks)"]["flops"] = f_r1
-        kernels["arrow_svd + fused W/G rotation (K2a, row ticks)"]["flops"] = f_row
+        kernels["rank-1 core + fused W/G rotation (K2b, rank-1 ticks)"]["flops"] = f_r1
+        kernels["append core + fused W/G rotation (K2a, row ticks)"]["flops"] = f_row
         for v in kernels.values():
             v["tflops"] = (v["flops"] / (v["ms"] / 1e3) / 1e12) if (v.get("flops") and v["ms"]) \
                 else None
@@ -705,8 +706,8 @@ def run_gpu(args):
         dom = kernels[dom_name]
         n_launch = max(1, (diag_steps + 1) // 2 if "row ticks" in dom_name else diag_steps // 2)
         ncu_key = {"project_append (K1, row ticks)": "proj5a",
-                   "arrow_svd + fused W/G rotation (K2a, row ticks)": "arrow5a",
-                   "jacobi32c + fused W/G rotation (K2b, rank-1 ticks)": "jacobi5a"}.get(dom_name)
+                   "append core + fused W/G rotation (K2a, row ticks)": "arrowcta",
+                   "rank-1 core + fused W/G rotation (K2b, rank-1 ticks)": "r1fast"}.get(dom_name)
         traffic = ncu_traffic(ncu_key) if ncu_key else None
         measured = (f"first {diag_steps} ticks in timing mode (one launch per kernel over all "
                     "streams, CUDA events around each phase on the engine stream)")

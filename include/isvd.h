@@ -54,6 +54,10 @@ int64_t isvd_launch_count(void);
  * solver counters, out8[6] = simultaneous steps on the rank-1 fast path,
  * out8[7] = rank-1 cores finished on it); reset if nonzero. */
 int isvd_debug_counters(int64_t* out8, int reset);
+/* Diagnostics: per-core phase timestamps (SM clock) of the last rank-1 core
+ * launch, recorded only by a library built with -DISVD_R1_TRACE (else all
+ * zero): out[b * 10 + k], k = 0..9, for b < n (n <= 4096). */
+int isvd_debug_trace(int64_t* out, int n);
 
 /* 1. Functional kernels (backend.py:54-63) ---------------------------------- */
 

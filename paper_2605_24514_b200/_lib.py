@@ -31,6 +31,7 @@ SIGNATURES = {
     "isvd_version": (C.c_int, []),
     "isvd_launch_count": (C.c_int64, []),
     "isvd_debug_counters": (C.c_int, [_ip64, C.c_int]),
+    "isvd_debug_trace": (C.c_int, [_ip64, C.c_int]),
     "isvd_core_svd": (C.c_int, [C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp]),
     "isvd_row_append": (C.c_int, [C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, _dp, C.c_double,
                                   C.c_int, _dp, _dp, _dp, _dp]),

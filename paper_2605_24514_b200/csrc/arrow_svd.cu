@@ -764,10 +764,10 @@ struct ArrowCtaSmem {
   double scale;
 };
 
-__global__ void __launch_bounds__(kACThreads, 6) arrow_cta_kernel(
+__device__ __forceinline__ void arrow_cta_body(
     int n, const double* __restrict__ core, int64_t core_stride, int ldcore,
     double* __restrict__ sv, int64_t sv_stride, double* __restrict__ s_out, int64_t s_out_stride,
-    int nkeep, const int* __restrict__ gate, ArrowFuse af) {
+    int nkeep, const int* __restrict__ gate, const ArrowFuse& af) {
   if (gate && *gate) return;
   extern __shared__ __align__(16) unsigned char ac_raw[];
   ArrowCtaSmem& S = *reinterpret_cast<ArrowCtaSmem*>(ac_raw);
@@ -782,6 +782,11 @@ __global__ void __launch_bounds__(kACThreads, 6) arrow_cta_kernel(
     v += __shfl_xor_sync(qmask, v, 1);
     return v + __shfl_xor_sync(qmask, v, 2);
   };
+  // the epilogue's operands (W, Gv) start moving into L2 while the core is solved
+  if (tid == 0 && af.uw_mode == 2 && af.uw_rows > 0)
+    bulk_prefetch_l2(af.uw.p + b * af.uw.stride, (uint32_t)(af.uw_rows * af.uw.ld * sizeof(double)));
+  if (tid == 32 && af.gw_rows > 0)
+    bulk_prefetch_l2(af.gw.p + b * af.gw.stride, (uint32_t)(af.gw_rows * af.gw.ld * sizeof(double)));
   // ---- zero the tiles (rows / columns beyond the core feed the DMMA epilogue)
   for (int i = tid; i < 33 * kACLd; i += kACThreads) {
     S.Uk[i] = 0.0;
@@ -1071,6 +1076,28 @@ __global__ void __launch_bounds__(kACThreads, 6) arrow_cta_kernel(
   }
 }
 
+// The last CTA to finish hands the cores on the fallback list (if any) to
+// the one-warp kernel by a device-side tail launch (no host launch per tick).
+__global__ void __launch_bounds__(kACThreads, 6) arrow_cta_kernel(
+    int n, const double* __restrict__ core, int64_t core_stride, int ldcore,
+    double* __restrict__ uk, double* __restrict__ vk, int64_t out_stride, int ldo,
+    double* __restrict__ sv, int64_t sv_stride, double* __restrict__ s_out, int64_t s_out_stride,
+    int nkeep, const int* __restrict__ gate, ArrowFuse af) {
+  arrow_cta_body(n, core, core_stride, ldcore, sv, sv_stride, s_out, s_out_stride, nkeep, gate, af);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(af.fb_fast_done, 1) == (int)gridDim.x - 1) {
+      *af.fb_fast_done = 0;
+      const int cnt = *reinterpret_cast<volatile int*>(af.fb_count);
+      if (cnt > 0)
+        arrow_svd_kernel<40, false, 1><<<min(cnt, 4 * 148), 32, 0, cudaStreamTailLaunch>>>(
+            n, core, core_stride, ldcore, uk, vk, out_stride, ldo, sv, sv_stride, s_out,
+            s_out_stride, nkeep, gate, af);
+    }
+  }
+}
+
 }  // namespace
 
 int read_arrow_counters(int64_t* out4, int reset) {
@@ -1097,12 +1124,8 @@ int launch_arrow_svd(int batch, int s, const double* core, int64_t core_stride, 
     // steady state of a batched k <= 32 stream: CTA per core, then the
     // one-warp kernel on the cores it handed back (deflation, dead sigma)
     arrow_cta_kernel<<<batch, kACThreads, sizeof(ArrowCtaSmem), st>>>(
-        s, core, core_stride, ldcore, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate, *af);
-    ISVD_LAUNCHED();
-    const int grid = std::min(batch, 4 * 148);
-    arrow_svd_kernel<40, false, 1><<<grid, 32, 0, st>>>(s, core, core_stride, ldcore, uk, vk,
-                                                        out_stride, ldo, sv, sv_stride, s_out,
-                                                        s_out_stride, nkeep, g_gate, *af);
+        s, core, core_stride, ldcore, uk, vk, out_stride, ldo, sv, sv_stride, s_out, s_out_stride,
+        nkeep, g_gate, *af);
   } else if (s <= 40) {
     // one warp per core: roots 32..39 (s = 33 is the k = 32 append core) are
     // solved warp-cooperatively after the one-root-per-lane pass

@@ -18,6 +18,7 @@
 // round; lanes stride over rows; three warp-shuffle reductions give
 // a_pp, a_qq, a_pq.  For s > kSmemMaxS, V is kept in a global scratch.
 #include <algorithm>
+#include <vector>
 #include <cstdlib>
 #include "common.cuh"
 #include "core_svd.cuh"
@@ -29,6 +30,18 @@ namespace isvd {
 
 // profiling counters: [0] jacobi32 sweeps, [1] jacobi32 cores (isvd_debug_counters)
 __device__ unsigned long long g_debug_counters[8];
+// rank-1 core phase timestamps (ISVD_R1_TRACE builds): [core][phase]
+__device__ long long g_r1_trace[4096][10];
+#ifdef ISVD_R1_TRACE
+#define R1_MARK(k)                                                   \
+  do {                                                               \
+    if (threadIdx.x == 0 && b < 4096) g_r1_trace[b][k] = clock64();  \
+  } while (0)
+#else
+#define R1_MARK(k) \
+  do {             \
+  } while (0)
+#endif
 
 namespace {
 
@@ -949,6 +962,7 @@ struct R1Smem {
   double T0[32 * kLdT];  // Theta1 -> J1 - I -> Theta2 -> Uk
   double T1[32 * kLdT];  // G1 -> G2 -> Vk
   double a[32], bv[32], sv[32], d[32], beta[32], inv[32], nrm2[32];
+  double acc[4];         // A[i, j], N, rho, |x| of this stream
   double red[2][4][32];
   double wt[4];
   int wv[4];
@@ -1002,8 +1016,8 @@ __device__ __forceinline__ void r1_rotate(double* X, int ld, int rows, int r, co
   }
 }
 
-__global__ void __launch_bounds__(kR1Threads, 8) rank1_fast_kernel(
-    int s, int batch, Rank1Core rc, double* __restrict__ uk, double* __restrict__ vk,
+__device__ __forceinline__ void rank1_fast_body(
+    int s, int batch, const Rank1Core& rc, double* __restrict__ uk, double* __restrict__ vk,
     int64_t out_stride, int ldo, double* __restrict__ sv_out, int64_t sv_stride,
     double* __restrict__ s_out, int64_t s_out_stride, int* __restrict__ fb_list,
     int* __restrict__ fb_count) {
@@ -1011,12 +1025,19 @@ __global__ void __launch_bounds__(kR1Threads, 8) rank1_fast_kernel(
   R1Smem& S = *reinterpret_cast<R1Smem*>(r1_raw);
   const int b = blockIdx.x;
   if (b >= batch) return;
+  R1_MARK(0);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, q = lane & 3;
   const int c = lane;          // column handled in the scalar phases
   const int r0 = 8 * warp;     // and its rows r0 .. r0 + 7
   double* T0 = S.T0;
   double* T1 = S.T1;
+  // the epilogue's operands (deferred window W, right basis Gv) start
+  // moving into L2 while the core is factored
+  if (tid == 0 && rc.uw_mode == 2 && rc.uw_rows > 0)
+    bulk_prefetch_l2(rc.uw.p + b * rc.uw.stride, (uint32_t)(rc.uw_rows * rc.uw.ld * sizeof(double)));
+  if (tid == 32 && rc.gw_rows > 0)
+    bulk_prefetch_l2(rc.gw.p + b * rc.gw.stride, (uint32_t)(rc.gw_rows * rc.gw.ld * sizeof(double)));
   const int64_t ii = rc.ii[b], jj = rc.jj[b];
   const double del = rc.delta[b];
   // ---- gathers (K6, _kernels.pyx:209-213) through the deferred bases:
@@ -1073,20 +1094,34 @@ __global__ void __launch_bounds__(kR1Threads, 8) rank1_fast_kernel(
     S.red[0][warp][c] = pa;
     S.red[1][warp][c] = pb;
     if (tid < 32) S.sv[c] = c < s ? rc.s[(int64_t)b * rc.lds + c] : 0.0;
-    if (tid == 0 && rc.A) {
-      double* e = rc.A + b * rc.a_stride + ii * rc.lda + jj;
-      const double old = *e;
-      *e = old + del;
-      const double nn = rc.N[b] + (2.0 * del * old + del * del);
-      rc.N[b] = nn;
+    // tracked entry, N and read-back ring (engine.py:162-166): the loads
+    // are issued with the gathers, the stores after the epilogue
+    if (tid == 96 && rc.A) {
+      S.acc[0] = rc.A[b * rc.a_stride + ii * rc.lda + jj];
+      S.acc[1] = rc.N[b];
       if (rc.ring) {
-        rc.ring[b] = nn;
-        rc.ring[rc.ring_stride + b] = rc.rho[b];
-        rc.ring[2 * rc.ring_stride + b] = rc.xnorm[b];
+        S.acc[2] = rc.rho[b];
+        S.acc[3] = rc.xnorm[b];
       }
     }
   }
   __syncthreads();
+  R1_MARK(1);
+  // the stores of the tracked-entry update (every core, fast or handed back)
+  auto finish_acc = [&]() {
+    if (tid == 96 && rc.A) {
+      const double aij = S.acc[0];
+      rc.A[b * rc.a_stride + ii * rc.lda + jj] = aij + del;
+      const double nn = S.acc[1] + (2.0 * del * aij + del * del);
+      rc.N[b] = nn;
+      if (rc.ring) {
+        rc.ring[b] = nn;
+        rc.ring[rc.ring_stride + b] = S.acc[2];
+        rc.ring[2 * rc.ring_stride + b] = S.acc[3];
+      }
+    }
+  };
+
   if (tid < 32) {
     S.a[c] = ((S.red[0][0][c] + S.red[0][1][c]) + S.red[0][2][c]) + S.red[0][3][c];
     S.bv[c] = ((S.red[1][0][c] + S.red[1][1][c]) + S.red[1][2][c]) + S.red[1][3][c];
@@ -1125,9 +1160,11 @@ __global__ void __launch_bounds__(kR1Threads, 8) rank1_fast_kernel(
   __syncthreads();
   if (S.status < 0) {
     if (tid == 0) fb_list[atomicAdd(fb_count, 1)] = b;
+    finish_acc();
     return;
   }
   const double a2 = S.beta[0], null2 = S.beta[1];
+  R1_MARK(2);
   bool sweep = S.status == 2;
   int steps = 0, nsw = 0;
   // warp-level reduction of (violation, max |theta|) -> block verdict:
@@ -1311,6 +1348,7 @@ __global__ void __launch_bounds__(kR1Threads, 8) rank1_fast_kernel(
       }
       st1 = verdict(viol, tmax);
     }
+  R1_MARK(3);
     if (st1 < 0) {
       sweep = true;
     } else {
@@ -1342,9 +1380,11 @@ __global__ void __launch_bounds__(kR1Threads, 8) rank1_fast_kernel(
       }
       __syncthreads();
       // ---- steps 2..4 (dense): G meets the stop, or the sweeps take over
+  R1_MARK(4);
       if (st1 == 1 && !dense_steps(3)) sweep = true;
     }
   }
+  R1_MARK(5);
   if (sweep) {
     // ---- close or graded singular values: one-sided Jacobi sweeps from K
     // with the reference's rotation and stop (_kernels.pyx:38-59), V
@@ -1441,9 +1481,11 @@ __global__ void __launch_bounds__(kR1Threads, 8) rank1_fast_kernel(
     }
     if (!conv) {
       if (tid == 0) fb_list[atomicAdd(fb_count, 1)] = b;
+    finish_acc();
       return;
     }
   }
+  R1_MARK(6);
   // ---- sigma = column norms of G, stable descending order (_kernels.pyx:94-101)
   {
     double p = 0.0, pd = 0.0;
@@ -1486,6 +1528,7 @@ __global__ void __launch_bounds__(kR1Threads, 8) rank1_fast_kernel(
   __syncthreads();
   if (S.status < 0) {
     if (tid == 0) fb_list[atomicAdd(fb_count, 1)] = b;
+    finish_acc();
     return;
   }
   if (tid == 0) {
@@ -1497,6 +1540,7 @@ __global__ void __launch_bounds__(kR1Threads, 8) rank1_fast_kernel(
       atomicAdd(&g_debug_counters[3], 1ull);
     }
   }
+  R1_MARK(7);
   // ---- Uk = G / sigma (sorted columns) -> T0; Vk = K^T g / sigma^2 -> T1
   {
     const int pc = S.pos[c];
@@ -1518,8 +1562,57 @@ __global__ void __launch_bounds__(kR1Threads, 8) rank1_fast_kernel(
     }
   }
   __syncthreads();
-  // ---- outputs: deferred window W (warps 0-1), deferred right basis Gv (warps 2-3)
-  if (warp < 2) {
+  R1_MARK(8);
+  // ---- outputs: deferred window W and deferred right basis Gv (their 8-row
+  // groups dealt round-robin to the four warps); other modes: W / U by
+  // warps 0-1, Gv / V by warps 2-3
+  if (rc.uw_mode == 2 && rc.gw_rows > 0) {
+    double* uwb = rc.uw.p + b * rc.uw.stride;
+    double* gwb = rc.gw.p + b * rc.gw.stride;
+    const int nwg = (rc.uw_rows + 7) / 8, ngg = (rc.gw_rows + 7) / 8;
+    // the next item's operands are loaded before this item's stores
+    auto load_item = [&](int item, double (&a)[8]) {
+      const bool isw = item < nwg;
+      const double* X = isw ? uwb : gwb;
+      const int ld = isw ? rc.uw.ld : rc.gw.ld;
+      const int rows = isw ? rc.uw_rows : rc.gw_rows;
+      const int row = 8 * (isw ? item : item - nwg) + g;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const int k = kk * 4 + q;
+        a[kk] = (row < rows && k < s) ? X[(int64_t)row * ld + k] : 0.0;
+      }
+    };
+    double a[8];
+    if (warp < nwg + ngg) load_item(warp, a);
+    for (int item = warp; item < nwg + ngg; item += 4) {
+      double an[8];
+      if (item + 4 < nwg + ngg) load_item(item + 4, an);
+      const bool isw = item < nwg;
+      double* X = isw ? uwb : gwb;
+      const int ld = isw ? rc.uw.ld : rc.gw.ld;
+      const int rows = isw ? rc.uw_rows : rc.gw_rows;
+      const int row = 8 * (isw ? item : item - nwg) + g;
+      const double* Q = isw ? T0 : T1;
+      double d[4][2];
+#pragma unroll
+      for (int nn = 0; nn < 4; ++nn) d[nn][0] = d[nn][1] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+#pragma unroll
+        for (int nn = 0; nn < 4; ++nn)
+          dmma_8x8x4(d[nn][0], d[nn][1], a[kk], Q[(kk * 4 + q) * kLdT + nn * 8 + g]);
+      if (row < rows) {
+#pragma unroll
+        for (int nn = 0; nn < 4; ++nn) {
+          const int c0 = nn * 8 + 2 * q;
+          if (c0 < ld) *reinterpret_cast<double2*>(X + (int64_t)row * ld + c0) = make_double2(d[nn][0], d[nn][1]);
+        }
+      }
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) a[kk] = an[kk];
+    }
+  } else if (warp < 2) {
     if (rc.uw_mode == 2) {
       r1_rotate(rc.uw.p + b * rc.uw.stride, rc.uw.ld, rc.uw_rows, s, T0, warp, 2);
     } else if (rc.uw_mode == 1) {
@@ -1547,9 +1640,49 @@ __global__ void __launch_bounds__(kR1Threads, 8) rank1_fast_kernel(
       }
     }
   }
+  finish_acc();
+#ifdef ISVD_R1_TRACE
+  __syncthreads();
+#endif
+  R1_MARK(9);
+}
+
+// The last CTA to finish hands the cores on the fallback list (if any) to
+// the one-warp kernel by a device-side tail launch (it starts when this grid
+// has completed): no host launch per tick for the rare fallback.
+__global__ void __launch_bounds__(kR1Threads, 8) rank1_fast_kernel(
+    int s, int batch, Rank1Core rc, double* __restrict__ uk, double* __restrict__ vk,
+    int64_t out_stride, int ldo, double* __restrict__ sv_out, int64_t sv_stride,
+    double* __restrict__ s_out, int64_t s_out_stride) {
+  rank1_fast_body(s, batch, rc, uk, vk, out_stride, ldo, sv_out, sv_stride, s_out, s_out_stride,
+                  rc.fb_list, rc.fb_count);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(rc.fb_fast_done, 1) == (int)gridDim.x - 1) {
+      *rc.fb_fast_done = 0;
+      const int cnt = *reinterpret_cast<volatile int*>(rc.fb_count);
+      if (cnt > 0) {
+        Rank1Core fb = rc;
+        fb.A = nullptr;  // tracked entry / N / ring already updated
+        const int grid = min((cnt + kJ32Warps - 1) / kJ32Warps, 2 * 148);
+        jacobi32c_kernel<true><<<grid, kJ32Warps * 32, sizeof(J32Smem) * kJ32Warps,
+                                 cudaStreamTailLaunch>>>(s, nullptr, 0, 0, uk, vk, out_stride, ldo,
+                                                         sv_out, sv_stride, batch, fb, s_out,
+                                                         s_out_stride);
+      }
+    }
+  }
 }
 
 }  // namespace
+
+int read_r1_trace(int64_t* out, int n) {
+  std::vector<long long> h((size_t)4096 * 10);
+  ISVD_CUDA(cudaMemcpyFromSymbol(h.data(), g_r1_trace, sizeof(long long) * h.size()));
+  for (int i = 0; i < n * 10; ++i) out[i] = h[i];
+  return ISVD_OK;
+}
 
 int read_debug_counters(int64_t* out, int reset) {
   unsigned long long h[8];
@@ -1597,17 +1730,11 @@ int launch_rank1_core_svd32(int batch, int s, const Rank1Core& rc, double* uk, d
     ISVD_LAUNCHED();
     return ISVD_OK;
   }
-  // CTA-per-core structured fast path, then the one-warp kernel on the cores
-  // it handed back (tracked entry / N / ring already updated: A = nullptr)
+  // CTA-per-core structured fast path; the one-warp kernel on the cores it
+  // hands back is tail-launched from the device (tracked entry / N / ring
+  // already updated there)
   rank1_fast_kernel<<<batch, kR1Threads, sizeof(R1Smem), st>>>(
-      s, batch, rc, uk, vk, out_stride, ldo, sv, sv_stride, s_out, s_out_stride, rc.fb_list,
-      rc.fb_count);
-  ISVD_LAUNCHED();
-  Rank1Core fb = rc;
-  fb.A = nullptr;
-  const int grid = std::min(ceil_div(batch, kJ32Warps), 2 * 148);
-  jacobi32c_kernel<true><<<grid, kJ32Warps * 32, smem, st>>>(
-      s, nullptr, 0, 0, uk, vk, out_stride, ldo, sv, sv_stride, batch, fb, s_out, s_out_stride);
+      s, batch, rc, uk, vk, out_stride, ldo, sv, sv_stride, s_out, s_out_stride);
   ISVD_LAUNCHED();
   return ISVD_OK;
 }

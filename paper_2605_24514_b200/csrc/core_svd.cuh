@@ -9,6 +9,7 @@ constexpr int kSmemMaxS = 112;   // G and V both in shared memory up to here
 
 size_t core_svd_smem_bytes(int s, bool v_in_smem);
 int read_debug_counters(int64_t* out, int reset);
+int read_r1_trace(int64_t* out, int n);
 // [0] secular roots solved, [1] their iterations, [2] cores, [3] cores that
 // took the sequential deflation pass (arrow_svd.cu)
 int read_arrow_counters(int64_t* out4, int reset);
@@ -73,6 +74,7 @@ struct Rank1Core {
   int* fb_list = nullptr;
   int* fb_count = nullptr;
   int* fb_done = nullptr;
+  int* fb_fast_done = nullptr;  // CTA completion count of the fast kernel
 };
 // K = diag(s) + delta U[i,:]^T Vt[:,j]^T built in registers and factored by
 // the warp Jacobi (s <= 32); also applies A[i,j] += delta and the N update.
@@ -106,6 +108,7 @@ struct ArrowFuse {
   int* fb_list = nullptr;
   int* fb_count = nullptr;
   int* fb_done = nullptr;
+  int* fb_fast_done = nullptr;  // CTA completion count of the CTA kernel
 };
 int launch_arrow_svd(int batch, int s, const double* core, int64_t core_stride, int ldcore,
                      double* uk, double* vk, int64_t out_stride, int ldo, double* sv,

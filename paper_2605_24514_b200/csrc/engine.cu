@@ -239,7 +239,7 @@ struct isvd_engine {
   double* ed = nullptr;
   int* dflag = nullptr;
   unsigned* zf_cnt = nullptr;  // per-stream CTA arrival counts (fused zero-sigma completion)
-  int* fbbuf = nullptr;        // rank-1 fallback list [0, B), counts [B, 2B), done counts [2B, 3B)
+  int* fbbuf = nullptr;        // core fallback list [0, B), counts [B, 2B), done counts [2B, 3B) and [3B, 4B)
   double* ref = nullptr;
   int ref_m = 0, ref_r = 0, ref_cap = 0;
   bool has_ref = false;
@@ -709,6 +709,11 @@ int isvd_debug_counters(int64_t* out8, int reset) {
   ISVD_TRY(check_device());
   return read_debug_counters(out8, reset);
 }
+int isvd_debug_trace(int64_t* out, int n) {
+  if (!out || n < 0 || n > 4096) { set_error("bad argument"); return ISVD_EINVAL; }
+  ISVD_TRY(check_device());
+  return read_r1_trace(out, n);
+}
 int64_t isvd_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
 
 int isvd_engine_create(isvd_engine** out, int batch, int m, int n, int k, double tol,
@@ -766,8 +771,8 @@ int isvd_engine_create(isvd_engine** out, int batch, int m, int n, int k, double
   if (rc == ISVD_OK) {
     if (cudaMalloc((void**)&e->zf_cnt, sizeof(unsigned) * batch) != cudaSuccess ||
         cudaMemset(e->zf_cnt, 0, sizeof(unsigned) * batch) != cudaSuccess ||
-        cudaMalloc((void**)&e->fbbuf, sizeof(int) * 3 * batch) != cudaSuccess ||
-        cudaMemset(e->fbbuf, 0, sizeof(int) * 3 * batch) != cudaSuccess) {
+        cudaMalloc((void**)&e->fbbuf, sizeof(int) * 4 * batch) != cudaSuccess ||
+        cudaMemset(e->fbbuf, 0, sizeof(int) * 4 * batch) != cudaSuccess) {
       set_error("out of device memory");
       rc = ISVD_ENOMEM;
     }
@@ -954,6 +959,7 @@ static int issue_append(isvd_engine* e, const Slice& sl, const double* xd, int l
     af.fb_list = e->fbbuf + b0;
     af.fb_count = e->fbbuf + e->B + b0;
     af.fb_done = e->fbbuf + 2 * e->B + b0;
+    af.fb_fast_done = e->fbbuf + 3 * e->B + b0;
   }
   if (e->append_jacobi)
     ISVD_TRY(launch_core_svd(nb, r + 1, core, cs, S, uk, vk, cs, S, sv, S,
@@ -1069,6 +1075,7 @@ static int issue_rank_one(isvd_engine* e, const Slice& sl, const int64_t* di, co
     rc.fb_list = e->fbbuf + b0;
     rc.fb_count = e->fbbuf + e->B + b0;
     rc.fb_done = e->fbbuf + 2 * e->B + b0;
+    rc.fb_fast_done = e->fbbuf + 3 * e->B + b0;
     if (vp) {
       rc.vd = e->vdesc(b0, e->vnz);
     } else if (defer) {

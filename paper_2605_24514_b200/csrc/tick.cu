@@ -86,6 +86,11 @@ __global__ void __launch_bounds__(256) project_append_kernel(
     }
   }
   const double* Zb = (RT == 1 && G && nz > 0) ? vd.Z + b * vd.z_stride : nullptr;
+  // the appended residuals are read twice (pass 1 and pass 2): start them
+  // into L2 with the bulk copy of F
+  if (Zb && threadIdx.x < nz && (vd.ldz & 1) == 0 && (rows & 1) == 0 &&
+      (reinterpret_cast<uintptr_t>(Zb) & 15) == 0)
+    bulk_prefetch_l2(Zb + (int64_t)threadIdx.x * vd.ldz, (uint32_t)(rows * sizeof(double)));
   // x: norm, tracked-matrix write (and staging) overlap the bulk copy
   double xx = 0.0;
   for (int c = threadIdx.x; c < rows; c += blockDim.x) {

@@ -16,7 +16,8 @@ cubin = "/tmp/ncu_lines.cubin"
 subprocess.run(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
                 "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
                 f"-I{ROOT / 'include'}", f"-I{ROOT / 'paper_2605_24514_b200/csrc'}", "-cubin", "-o",
-                cubin, str(ROOT / "paper_2605_24514_b200/csrc" / src)], check=True)
+                cubin, str(ROOT / "paper_2605_24514_b200/csrc" / src)]
+               + (["-rdc=true"] if src in ("core_svd.cu", "arrow_svd.cu") else []), check=True)
 sass = subprocess.run(["nvdisasm", "-g", "-c", cubin], capture_output=True, text=True).stdout
 lines = sass.split("\n")
 start = next(i for i, l in enumerate(lines) if l.strip().startswith(".text.") and kname in l)
