@@ -31,6 +31,10 @@
 
 namespace isvd {
 
+#ifdef ISVD_R1_TRACE
+extern __device__ long long g_r1_trace[4096][10];  // core_svd.cu (relocatable device code)
+#endif
+
 namespace {
 
 constexpr int kN = kCoreMaxS;  // max core size
@@ -751,6 +755,16 @@ __global__ void __launch_bounds__(WIDE ? 512 : 32, 1) arrow_svd_kernel(int n, co
 // Vk on DMMA) spread over the five warps' row groups.  Cores that need
 // deflation (a tiny z entry, coincident poles), or with a dead singular
 // value, are handed to the one-warp kernel (list mode) untouched.
+#ifdef ISVD_R1_TRACE
+#define AC_MARK(k)                                                   \
+  do {                                                               \
+    if (threadIdx.x == 0 && b < 4096) g_r1_trace[b][k] = clock64();  \
+  } while (0)
+#else
+#define AC_MARK(k) \
+  do {             \
+  } while (0)
+#endif
 constexpr int kACThreads = 160;
 constexpr int kACN = 40;   // root capacity (one quad each)
 constexpr int kACLd = 36;  // Uk / Vk tile pitch
@@ -758,10 +772,9 @@ constexpr int kACLd = 36;  // Uk / Vk tile pitch
 struct ArrowCtaSmem {
   double Uk[33 * kACLd];
   double Vk[33 * kACLd];
-  double d[kACN], z[kACN], kd[kACN], kz[kACN], mu[kACN], sig[kACN], zhat[kACN];
-  int kcol[kACN], order[kACN], org[kACN], pos[kACN];
+  double d[kACN], kd[kACN], kz[kACN], mu[kACN], sig[kACN], zhat[kACN];
+  int kcol[kACN], org[kACN], pos[kACN];
   double wmax[8];
-  double scale;
 };
 
 __device__ __forceinline__ void arrow_cta_body(
@@ -787,97 +800,82 @@ __device__ __forceinline__ void arrow_cta_body(
     bulk_prefetch_l2(af.uw.p + b * af.uw.stride, (uint32_t)(af.uw_rows * af.uw.ld * sizeof(double)));
   if (tid == 32 && af.gw_rows > 0)
     bulk_prefetch_l2(af.gw.p + b * af.gw.stride, (uint32_t)(af.gw_rows * af.gw.ld * sizeof(double)));
+  AC_MARK(0);
   // ---- zero the tiles (rows / columns beyond the core feed the DMMA epilogue)
   for (int i = tid; i < 33 * kACLd; i += kACThreads) {
     S.Uk[i] = 0.0;
     S.Vk[i] = 0.0;
   }
   // ---- load and scale
-  double mx = 0.0;
+  double mx = 0.0, dv = 0.0, zv = 0.0;
   if (tid < n) {
-    const double dc = tid < r ? fabs(K[tid * ldcore + tid]) : 0.0, zc = K[r * ldcore + tid];
-    S.d[tid] = dc;
-    S.z[tid] = zc;
-    mx = fmax(dc, fabs(zc));
+    dv = tid < r ? fabs(K[tid * ldcore + tid]) : 0.0;
+    zv = K[r * ldcore + tid];
+    mx = fmax(dv, fabs(zv));
   }
   mx = warp_max(mx);
   if (lane == 0) S.wmax[warp] = mx;
   __syncthreads();
-  if (tid == 0) {
-    double m2 = 0.0;
-    for (int w = 0; w < kACThreads / 32; ++w) m2 = fmax(m2, S.wmax[w]);
-    S.scale = m2 > 0.0 ? m2 : 1.0;
-  }
-  __syncthreads();
-  const double scale = S.scale;
+  double scale = 0.0;
+  for (int w = 0; w < kACThreads / 32; ++w) scale = fmax(scale, S.wmax[w]);
+  scale = scale > 0.0 ? scale : 1.0;
   if (tid < n) {
-    S.d[tid] /= scale;
-    S.z[tid] /= scale;
+    dv /= scale;
+    zv /= scale;
+    S.d[tid] = dv;
   }
   __syncthreads();
-  // ascending poles; ties: higher column first (the rho column r leads)
-  if (tid < n) {
-    const double dc = S.d[tid];
-    int rank = 0;
-    for (int e = 0; e < n; ++e) {
-      const double de = S.d[e];
-      rank += (de < dc) || (de == dc && e > tid);
-    }
-    S.order[rank] = tid;
-  }
-  __syncthreads();
-  // ---- deflation check (as arrow_body); none needed: every pole kept in order
+  AC_MARK(1);
+  // ---- deflation check.  The poles are the installed singular values,
+  // sorted descending, plus the rho column's zero: without deflation (every
+  // |z| > tol, consecutive poles more than tol apart -- which also means
+  // strictly sorted) the ascending order is column r, then r - 1, ..., 0.
+  // Anything else (deflation, or unsorted poles) goes to the one-warp kernel.
   {
     const double tol = 8.0 * eps;
     bool need = false;
     if (tid < n) {
-      const int c = S.order[tid];
-      const double dc = S.d[c];
-      need = fabs(S.z[c]) <= tol;
-      if (tid > 0) need |= dc <= tol || dc - S.d[S.order[tid - 1]] <= tol;
-      S.kcol[tid] = c;
-      S.kd[tid] = tid == 0 ? 0.0 : dc;
-      S.kz[tid] = S.z[c];
+      need = fabs(zv) <= tol;
+      if (tid < r) need |= !(dv - S.d[tid + 1] > tol);  // S.d[r] = 0
+      const int pk = tid == r ? 0 : r - tid;
+      S.kcol[pk] = tid;
+      S.kd[pk] = dv;
+      S.kz[pk] = zv;
     }
     if (__syncthreads_or(need)) {
       if (tid == 0) af.fb_list[atomicAdd(af.fb_count, 1)] = b;
       return;
     }
   }
+  AC_MARK(2);
   const int N = n;
-  // ---- roots: quad i solves for sigma_i in (kd[i], kd[i+1]) (the last beyond kd[N-1])
+  // ---- roots: quad i solves for sigma_i in (kd[i], kd[i+1]) (the last beyond kd[N-1]).
+  // The first evaluation is at the interval midpoint (origin kd[i]); its sign
+  // picks the origin (the nearer pole) and the half-interval, and its terms
+  // already feed the first rational-model step (no separate bracketing pass).
   if (quad < N) {
     const int i = quad;
-    int o;
-    double lo, hi;
     const double di = S.kd[i];
-    if (i < N - 1) {
-      const double dn = S.kd[i + 1];
-      const double sm = 0.5 * (di + dn);
-      const double mum = (sm - di) * (sm + di);
-      double f = 0.0;
-      for (int j = ql; j < N; j += 4) {
-        const double dj = S.kd[j];
-        f += S.kz[j] * S.kz[j] * frcp((dj - di) * (dj + di) - mum);
-      }
-      f = 1.0 + qsum(f);
-      if (f > 0.0) {
-        o = i; lo = 0.0; hi = mum;
-      } else {
-        o = i + 1; lo = (sm - dn) * (sm + dn); hi = 0.0;
-      }
+    const double dn = i < N - 1 ? S.kd[i + 1] : 0.0;
+    const double sm = 0.5 * (di + dn);
+    const double mum = (sm - di) * (sm + di);
+    int o = i;
+    double dorg = di, lo, hi, x, Di = 0.0, Dn = 0.0;
+    bool first = i < N - 1;
+    if (first) {
+      lo = 0.0;
+      hi = mum;
+      x = mum;
     } else {
-      o = i;
       double zz = 0.0;
       for (int j = ql; j < N; j += 4) zz += S.kz[j] * S.kz[j];
       lo = 0.0;
       hi = qsum(zz);
+      x = 0.5 * (lo + hi);
     }
-    const double dorg = S.kd[o];
-    const double Di = (di - dorg) * (di + dorg);
-    const double Dn = (i < N - 1) ? (S.kd[i + 1] - dorg) * (S.kd[i + 1] + dorg) : 0.0;
-    double x = 0.5 * (lo + hi);
+    int iters = 0;
     for (int it = 0; it < 80; ++it) {
+      ++iters;
       double psi = 0.0, dpsi = 0.0, phi = 0.0, dphi = 0.0, aps = 0.0;
       for (int j = ql; j < N; j += 4) {
         const double dj = S.kd[j];
@@ -899,7 +897,22 @@ __device__ __forceinline__ void arrow_cta_body(
       aps = qsum(aps);
       // identical in the four lanes from here on (xor-reduced inputs)
       const double g = 1.0 + psi + phi;
-      if (g < 0.0) lo = x; else hi = x;
+      if (first) {
+        first = false;
+        if (!(g > 0.0)) {  // root above the midpoint: origin at kd[i+1]
+          o = i + 1;
+          dorg = dn;
+          lo = (sm - dn) * (sm + dn);
+          hi = 0.0;
+          x = lo;
+        }
+        Di = (di - dorg) * (di + dorg);
+        Dn = (dn - dorg) * (dn + dorg);
+      } else if (g < 0.0) {
+        lo = x;
+      } else {
+        hi = x;
+      }
       if (fabs(g) <= 4.0 * eps * (1.0 + aps) * N || !(g == g)) break;
       const double pi_ = Di - x;
       const double b1 = dpsi * pi_ * pi_;
@@ -934,6 +947,12 @@ __device__ __forceinline__ void arrow_cta_body(
       }
       x = xn;
     }
+#ifdef ISVD_ARROW_STATS
+    if (ql == 0) {
+      atomicAdd(&g_arrow_counters[0], 1ull);
+      atomicAdd(&g_arrow_counters[1], (unsigned long long)iters);
+    }
+#endif
     if (ql == 0) {
       S.org[i] = o;
       S.mu[i] = x;
@@ -941,6 +960,7 @@ __device__ __forceinline__ void arrow_cta_body(
     }
   }
   __syncthreads();
+  AC_MARK(3);
   // ---- Loewner: zhat_j^2 = prod_k (sigma_k^2 - d_j^2) / prod_{k != j} (d_k^2 - d_j^2)
   if (quad < N) {
     const int j = quad;
@@ -959,23 +979,34 @@ __device__ __forceinline__ void arrow_cta_body(
     acc *= sdiff(N - 1);
     if (ql == 0) S.zhat[j] = copysign(sqrt(fmax(acc, 0.0)), S.kz[j]);
   }
-  // ---- sorted output positions: descending sigma, ties by index; sigma_max
-  double m1 = 0.0;
-  if (tid < n) {
-    const double st = S.sig[tid];
-    int rank = 0;
-    for (int e = 0; e < n; ++e) {
-      const double se = S.sig[e];
-      rank += (se > st) || (se == st && e < tid);
+  // ---- sorted output positions: descending sigma, ties by index; sigma_max.
+  // Strict interlacing (kd_i < sigma_i < kd_{i+1}) makes the roots ascending,
+  // so position N - 1 - t unless rounding broke the order (then the ranks).
+  bool unsorted = false;
+  if (tid < n - 1) unsorted = !(S.sig[tid] < S.sig[tid + 1]);
+  if (__syncthreads_or(unsorted)) {
+    double m1 = 0.0;
+    if (tid < n) {
+      const double st = S.sig[tid];
+      int rank = 0;
+      for (int e = 0; e < n; ++e) {
+        const double se = S.sig[e];
+        rank += (se > st) || (se == st && e < tid);
+      }
+      S.pos[tid] = rank;
+      m1 = st;
     }
-    S.pos[tid] = rank;
-    m1 = st;
+    m1 = warp_max(m1);
+    if (lane == 0) S.wmax[warp] = m1;
+  } else if (tid < n) {
+    S.pos[tid] = n - 1 - tid;
+    if (tid == n - 1)
+      for (int w = 0; w < kACThreads / 32; ++w) S.wmax[w] = S.sig[n - 1];
   }
-  m1 = warp_max(m1);
-  if (lane == 0) S.wmax[warp] = m1;
   __syncthreads();
   double smax = 0.0;
   for (int w = 0; w < kACThreads / 32; ++w) smax = fmax(smax, S.wmax[w]);
+  AC_MARK(4);
   // ---- vectors into the shared tiles (quad per root)
   bool dead = false;
   if (quad < N) {
@@ -1008,6 +1039,7 @@ __device__ __forceinline__ void arrow_cta_body(
     if (tid == 0) af.fb_list[atomicAdd(af.fb_count, 1)] = b;
     return;
   }
+  AC_MARK(5);
   // install sigma; columns >= keep of the tiles out of the rotation
   const int keep = nkeep;
   if (tid < n) {
@@ -1024,6 +1056,7 @@ __device__ __forceinline__ void arrow_cta_body(
     }
   }
   __syncthreads();
+  AC_MARK(6);
   // ---- fused epilogue: W <- [W 0; 0 1] Uk[:, :keep], Gv <- [Gv 0; 0 1/rho] Vk[:, :keep]
   double* uwb = af.uw.p + b * af.uw.stride;
   double* gwb = af.gw.p + b * af.gw.stride;
@@ -1074,6 +1107,10 @@ __device__ __forceinline__ void arrow_cta_body(
     const int cc = tid - 64;
     gwb[(int64_t)af.gw_rows * af.gw.ld + cc] = cc < 32 ? af.inj[b] * S.Vk[r * kACLd + cc] : 0.0;
   }
+#ifdef ISVD_R1_TRACE
+  __syncthreads();
+#endif
+  AC_MARK(7);
 }
 
 // The last CTA to finish hands the cores on the fallback list (if any) to
