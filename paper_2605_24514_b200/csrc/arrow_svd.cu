@@ -23,6 +23,9 @@
 //      sort, snap below 1e-12 sigma_0, dead left columns completed over
 //      e_0, e_1, ... in order.
 #include <algorithm>
+#include <cstdlib>
+#include <cstdio>
+#include <chrono>
 #include <cooperative_groups.h>
 #include "common.cuh"
 #include "core_svd.cuh"
@@ -779,6 +782,7 @@ struct ArrowCtaSmem {
 
 __device__ __forceinline__ void arrow_cta_body(
     int n, const double* __restrict__ core, int64_t core_stride, int ldcore,
+    double* __restrict__ uk, double* __restrict__ vk, int64_t out_stride, int ldo,
     double* __restrict__ sv, int64_t sv_stride, double* __restrict__ s_out, int64_t s_out_stride,
     int nkeep, const int* __restrict__ gate, const ArrowFuse& af) {
   if (gate && *gate) return;
@@ -1057,6 +1061,19 @@ __device__ __forceinline__ void arrow_cta_body(
   }
   __syncthreads();
   AC_MARK(6);
+  if (!af.uw_mode) {
+    // unfused (single streams): the core's U / V to uk / vk for the
+    // rotation launch (every column; those >= keep are zero, as the
+    // rotation never reads them)
+    double* U = uk + b * out_stride;
+    double* V = vk + b * out_stride;
+    for (int idx = tid; idx < n * n; idx += kACThreads) {
+      const int i = idx / n, cc = idx % n;
+      U[i * ldo + cc] = S.Uk[i * kACLd + cc];
+      V[i * ldo + cc] = S.Vk[i * kACLd + cc];
+    }
+    return;
+  }
   // ---- fused epilogue: W <- [W 0; 0 1] Uk[:, :keep], Gv <- [Gv 0; 0 1/rho] Vk[:, :keep]
   double* uwb = af.uw.p + b * af.uw.stride;
   double* gwb = af.gw.p + b * af.gw.stride;
@@ -1120,7 +1137,8 @@ __global__ void __launch_bounds__(kACThreads, 6) arrow_cta_kernel(
     double* __restrict__ uk, double* __restrict__ vk, int64_t out_stride, int ldo,
     double* __restrict__ sv, int64_t sv_stride, double* __restrict__ s_out, int64_t s_out_stride,
     int nkeep, const int* __restrict__ gate, ArrowFuse af) {
-  arrow_cta_body(n, core, core_stride, ldcore, sv, sv_stride, s_out, s_out_stride, nkeep, gate, af);
+  arrow_cta_body(n, core, core_stride, ldcore, uk, vk, out_stride, ldo, sv, sv_stride, s_out,
+                 s_out_stride, nkeep, gate, af);
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -1157,9 +1175,10 @@ int launch_arrow_svd(int batch, int s, const double* core, int64_t core_stride, 
     return ISVD_EINVAL;
   }
   if (batch == 0) return ISVD_OK;
-  if (s <= 33 && af && af->uw_mode && af->fb_list) {
-    // steady state of a batched k <= 32 stream: CTA per core, then the
-    // one-warp kernel on the cores it handed back (deflation, dead sigma)
+  if (s <= 33 && af && af->fb_list) {
+    // k <= 32 streams: CTA per core (fused epilogue for the batched steady
+    // state, else Uk / Vk out for the rotation launch); the one-warp kernel
+    // takes the cores it hands back (deflation, dead sigma)
     arrow_cta_kernel<<<batch, kACThreads, sizeof(ArrowCtaSmem), st>>>(
         s, core, core_stride, ldcore, uk, vk, out_stride, ldo, sv, sv_stride, s_out, s_out_stride,
         nkeep, g_gate, *af);

@@ -17,9 +17,8 @@
 // same similarity, and the rotated factors come out bit-identical), so the
 // canonical form is produced whenever factors are read.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
-#include <cstdio>
-#include <cstdlib>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -38,6 +37,35 @@
 #include "../../include/isvd.h"
 
 namespace isvd {
+// Host-side section timer for the per-event path (ISVD_HOST_PROF=1: totals
+// printed to stderr at engine destruction; tools/b1_breakdown.py)
+struct HostProf {
+  bool on = false;
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long n[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  HostProf() {
+    const char* v = std::getenv("ISVD_HOST_PROF");
+    on = v && v[0] == '1';
+  }
+  static double now() {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  }
+  void add(int k, double t0) {
+    if (!on) return;
+    acc[k] += now() - t0;
+    n[k] += 1;
+  }
+  void report() {
+    if (!on) return;
+    static const char* names[8] = {"append:pre", "append:staging", "append:issue", "append:post",
+                                   "issue:K1", "issue:core", "issue:rotate", "rank1:total"};
+    for (int k = 0; k < 8; ++k)
+      if (n[k]) std::fprintf(stderr, "[isvd host] %-16s %8.2f us x %ld\n", names[k], acc[k] / n[k], n[k]);
+  }
+};
+static HostProf g_hprof;
+#define HP_T0(v) const double v = g_hprof.on ? HostProf::now() : 0.0
+
 
 static thread_local std::string g_err;
 thread_local const int* g_gate = nullptr;
@@ -239,6 +267,8 @@ struct isvd_engine {
   double* ed = nullptr;
   int* dflag = nullptr;
   unsigned* zf_cnt = nullptr;  // per-stream CTA arrival counts (fused zero-sigma completion)
+  int64_t* pack_dev = nullptr;          // small host rank-1 payloads: (i, j, delta) per slot
+  std::vector<int64_t> pack_host;
   int* fbbuf = nullptr;        // core fallback list [0, B), counts [B, 2B), done counts [2B, 3B) and [3B, 4B)
   double* ref = nullptr;
   int ref_m = 0, ref_r = 0, ref_cap = 0;
@@ -675,6 +705,7 @@ struct isvd_engine {
     dfree(ei); dfree(ej); dfree(ed); dfree(dflag);
     if (zf_cnt) cudaFree(zf_cnt);
     if (fbbuf) cudaFree(fbbuf);
+    dfree(pack_dev);
     dfree(ref); dfree(W); dfree(Gv); dfree(Zv);
     dfree(wx); dfree(wj); dfree(wpart); dfree(wout); dfree(wflags);
     dfree(snap.U); dfree(snap.V); dfree(snap.A); dfree(snap.s); dfree(snap.N); dfree(snap.ref);
@@ -801,6 +832,7 @@ int isvd_engine_create(isvd_engine** out, int batch, int m, int n, int k, double
 }
 
 int isvd_engine_destroy(isvd_engine* e) {
+  g_hprof.report();
   if (e) e->join();
   if (e) {
     if (e->st) cudaStreamSynchronize(e->st);
@@ -931,6 +963,7 @@ static int issue_append(isvd_engine* e, const Slice& sl, const double* xd, int l
     zdst = e->Zv + b0 * e->zvstride() + (int64_t)e->vnz * e->n_cap;
     zdst_stride = e->zvstride();
   }
+  HP_T0(hk1);
   ISVD_TRY(launch_project_append(nb, len, r, F, xd + (int64_t)b0 * len, len,
                                  e->s + (int64_t)b0 * e->ld, e->ld, e->tol, core, cs, S, zdst,
                                  zdst_stride, inj, e->rho + b0, e->xnorm + b0, Adst, e->astride(),
@@ -938,6 +971,8 @@ static int issue_append(isvd_engine* e, const Slice& sl, const double* xd, int l
                                  (e->sharded && !is_row) ? &e->ar : nullptr,
                                  e->append_jacobi ? 0 : 1, (vp || vrow) ? &vd : nullptr,
                                  e->ring_row(e->ring_slot, b0), e->B));
+  g_hprof.add(4, hk1);
+  HP_T0(hk2);
   if (one) e->mark();
   // steady state of a batched k <= 32 stream: the arrow kernel's warp also
   // rotates the deferred bases (no rotation launch, no Uk / Vk re-read)
@@ -956,21 +991,26 @@ static int issue_append(isvd_engine* e, const Slice& sl, const double* xd, int l
     af.zV = mat_at(e->Vm(), b0);
     af.zn = e->n;
     af.zvd = e->vdesc(b0, e->vnz + 1);
-    af.fb_list = e->fbbuf + b0;
-    af.fb_count = e->fbbuf + e->B + b0;
-    af.fb_done = e->fbbuf + 2 * e->B + b0;
-    af.fb_fast_done = e->fbbuf + 3 * e->B + b0;
   }
+  // CTA-per-core append cores (k <= 32): fused epilogue above, or Uk / Vk
+  // out for the rotation launch below; fallback list per slice
+  af.fb_list = e->fbbuf + b0;
+  af.fb_count = e->fbbuf + e->B + b0;
+  af.fb_done = e->fbbuf + 2 * e->B + b0;
+  af.fb_fast_done = e->fbbuf + 3 * e->B + b0;
   if (e->append_jacobi)
     ISVD_TRY(launch_core_svd(nb, r + 1, core, cs, S, uk, vk, cs, S, sv, S,
                              e->vscr ? e->vscr + (int64_t)b0 * S * (S | 1) : nullptr, nullptr, st));
   else
     ISVD_TRY(launch_arrow_svd(nb, r + 1, core, cs, S, uk, vk, cs, S, sv, S, st,
-                              e->s + (int64_t)b0 * e->ld, e->ld, keep, fuse_rot ? &af : nullptr));
+                              e->s + (int64_t)b0 * e->ld, e->ld, keep,
+                              (fuse_rot || !e->sharded) ? &af : nullptr));
+  g_hprof.add(5, hk2);
   if (fuse_rot) {
     if (one) { e->mark(); e->mark(); }
     return ISVD_OK;
   }
+  HP_T0(hk3);
   if (one) e->mark();
   // row: U <- [U 0; 0 1] Uk, V <- V Vk[:r] + z^ Vk[r] ; col: the same with U<->V
   RotJob grow{mat_at(is_row ? e->Um() : e->Vm(), b0), is_row ? e->m : e->n, uk, cs, S, nullptr, 0,
@@ -1031,6 +1071,7 @@ static int issue_append(isvd_engine* e, const Slice& sl, const double* xd, int l
   if (!fused)
     ISVD_TRY(launch_complete_zero(nb, keep, zf.s, zf.lds, zf.U, zf.m, zf.V, zf.n, st,
                                   vrow ? &zf.vd : nullptr));
+  g_hprof.add(6, hk3);
   return ISVD_OK;
 }
 
@@ -1178,12 +1219,25 @@ static int issue_rank_one(isvd_engine* e, const Slice& sl, const int64_t* di, co
 // Run `issue(slice)` over the batch: one slice on the engine stream, or
 // ngroups slices forked onto the group streams and joined back.
 }  // extern "C"
-template <class F>
-static int run_groups(isvd_engine* e, F&& issue) {
+// stream groups a tick of this engine is split into (1: everything on e->st)
+static int groups_for(const isvd_engine* e) {
   int G = e->timing ? 1 : e->ngroups;
   if (e->B < 2 * isvd_engine::kGroupMin) G = 1;
   G = std::min(G, e->B / isvd_engine::kGroupMin);
-  if (G < 1) G = 1;
+  return G < 1 ? 1 : G;
+}
+
+// Small host payloads of a single-group engine (single streams, configs
+// 1-4): one H2D on the engine stream itself.  The staging slot cannot be
+// overwritten early -- every reader is on the same stream -- so the copy
+// stream, its events and the slot tickets (five API calls) are skipped.
+static bool small_host_path(const isvd_engine* e, size_t bytes) {
+  return groups_for(e) == 1 && !e->pend && bytes <= (size_t(64) << 10);
+}
+
+template <class F>
+static int run_groups(isvd_engine* e, F&& issue) {
+  const int G = groups_for(e);
   e->ngroups_active = G;
   if (G == 1 || (e->pend && e->pend_G != G)) e->join();
   if (G == 1) return issue(Slice{0, e->B, e->st});
@@ -1205,6 +1259,7 @@ static int run_groups(isvd_engine* e, F&& issue) {
 extern "C" {
 
 static int append_common(isvd_engine* e, const double* x, int on_device, bool is_row) {
+  HP_T0(hp0);
   if (!e || !x) { set_error("null argument"); return ISVD_EINVAL; }
   if (!e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
   const int len = is_row ? e->n : e->m;
@@ -1259,9 +1314,17 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
   // slot, issued before this tick's kernels wait for the previous tick, so
   // the upload overlaps the previous tick's work; the slot is reused only
   // after the tick that last read it has finished.
+  g_hprof.add(0, hp0);
+  HP_T0(hp1);
   double* staged = nullptr;
   int slot = 0;
-  if (!on_device) {
+  const bool small = !on_device && !device_check && small_host_path(e, sizeof(double) * nelem);
+  if (small) {
+    slot = e->stage_slot;
+    e->stage_slot = (e->stage_slot + 1) % isvd_engine::kStageSlots;
+    staged = e->ev + (int64_t)slot * e->B * e->zlen();
+    ISVD_CUDA(cudaMemcpyAsync(staged, x, sizeof(double) * nelem, cudaMemcpyHostToDevice, e->st));
+  } else if (!on_device) {
     ISVD_TRY(e->ensure_copy_stream());
     slot = e->stage_slot;
     e->stage_slot = (e->stage_slot + 1) % isvd_engine::kStageSlots;
@@ -1285,6 +1348,8 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
     }
     ISVD_CUDA(cudaStreamWaitEvent(e->st, e->stage_ready, 0));
   }
+  g_hprof.add(1, hp1);
+  HP_T0(hp2);
   e->ring_slot = (int)(e->ring_cnt % isvd_engine::kRing);
   // Gated tick: the kernels are queued before the verdict is known and skip
   // themselves on the device if the payload was rejected, so the host's wait
@@ -1297,7 +1362,11 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
   });
   g_gate = nullptr;
   ISVD_TRY(rc_issue);
-  // the staging slot is free again once every group has run this tick
+  g_hprof.add(2, hp2);
+  HP_T0(hp3);
+  // the staging slot is free again once every group has run this tick (also
+  // after a small-path tick: a later large payload reuses the slot from the
+  // copy stream)
   if (!on_device) ISVD_TRY(e->ticket_record(e->stage_tk[slot]));
   if (gated) {
     ISVD_CUDA(cudaEventSynchronize(e->stage_ready));
@@ -1337,6 +1406,7 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
   e->ring_cnt += 1;
   e->canonical = false;
   e->step += 1;
+  g_hprof.add(3, hp3);
   return ISVD_OK;
 }
 
@@ -1350,6 +1420,11 @@ int isvd_engine_col_append(isvd_engine* e, const double* y, int on_device) {
 
 int isvd_engine_rank_one(isvd_engine* e, const int64_t* i, const int64_t* j, const double* delta,
                          int on_device) {
+  HP_T0(hr0);
+  struct HpEnd {
+    double t0;
+    ~HpEnd() { g_hprof.add(7, t0); }
+  } hp_end{hr0};
   if (!e || !i || !j || !delta) { set_error("null argument"); return ISVD_EINVAL; }
   if (!e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
   const int64_t *di = i, *dj = j;
@@ -1379,6 +1454,23 @@ int isvd_engine_rank_one(isvd_engine* e, const int64_t* i, const int64_t* j, con
       }
       if (!std::isfinite(delta[b])) { set_error("delta must be finite"); return ISVD_EINVAL; }
     }
+    if (small_host_path(e, 24 * (size_t)e->B)) {
+      // (i, j, delta) packed into one H2D on the engine stream
+      rslot = e->stage_slot;
+      e->stage_slot = (e->stage_slot + 1) % isvd_engine::kStageSlots;
+      if (!e->pack_dev) ISVD_TRY(dalloc(&e->pack_dev, (size_t)isvd_engine::kStageSlots * 3 * e->B));
+      e->pack_host.resize((size_t)3 * e->B);
+      int64_t* hp = e->pack_host.data();
+      std::memcpy(hp, i, sizeof(int64_t) * e->B);
+      std::memcpy(hp + e->B, j, sizeof(int64_t) * e->B);
+      std::memcpy(hp + 2 * e->B, delta, sizeof(double) * e->B);
+      int64_t* dp = e->pack_dev + (int64_t)rslot * 3 * e->B;
+      ISVD_CUDA(cudaMemcpyAsync(dp, hp, sizeof(int64_t) * 3 * e->B, cudaMemcpyHostToDevice, e->st));
+      di = dp;
+      dj = dp + e->B;
+      dd = reinterpret_cast<const double*>(dp + 2 * e->B);
+      rslot = -1;  // no copy-stream ticket
+    } else {
     // double-buffered staging on the copy stream, as for appended rows
     ISVD_TRY(e->ensure_copy_stream());
     rslot = e->stage_slot;
@@ -1393,6 +1485,7 @@ int isvd_engine_rank_one(isvd_engine* e, const int64_t* i, const int64_t* j, con
     ISVD_CUDA(cudaEventRecord(e->stage_ready, e->cp_st));
     ISVD_CUDA(cudaStreamWaitEvent(e->st, e->stage_ready, 0));
     di = si; dj = sj; dd = sd;
+    }
   } else if (!e->sharded) {
     // device payload: copied into a staging slot on the engine stream and
     // bounds/finiteness-checked there (the caller's buffer is then free
@@ -1423,7 +1516,7 @@ int isvd_engine_rank_one(isvd_engine* e, const int64_t* i, const int64_t* j, con
     return issue_rank_one(e, sl, di, dj, dd, lazy_state, defer, vp);
   }));
   if (defer) e->vpend = true;
-  if (!on_device || !e->sharded) ISVD_TRY(e->ticket_record(e->stage_tk[rslot]));
+  if (rslot >= 0 && (!on_device || !e->sharded)) ISVD_TRY(e->ticket_record(e->stage_tk[rslot]));
   if (lazy_state == 1) {
     e->lazy_active = true;
     e->m_base = e->m;

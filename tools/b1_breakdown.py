@@ -64,7 +64,38 @@ def main():
     out["cfg2_rank1"] = run("cfg2", a0, ev, meta["k"])
     a0, ev, meta = workloads.cfg3()
     out["cfg3_rows"] = run("cfg3", a0, ev, meta["k"])
+    out["cfg1_host_split"] = host_split()
     print(json.dumps(out, indent=1))
+
+
+
+def host_split(n=400):
+    """cfg1 row appends: the Python API vs a direct C-ABI call (pageable and
+    pinned payloads), enqueue cost per event without synchronisation."""
+    import torch
+
+    lib = _lib.load()
+    a0, ev, meta = workloads.cfg1()
+    xs = np.stack([e[1] for e in ev[:n]])
+    pinned = torch.empty(xs.shape, dtype=torch.float64, pin_memory=True)
+    pinned.copy_(torch.from_numpy(xs))
+    pn = pinned.numpy()
+    out = {}
+    for name, mode in (("python_api", 0), ("cabi_pageable", 1), ("cabi_pinned", 2)):
+        e = SvdEngine(a0, meta["k"])
+        e.synchronize()
+        h = e._h.h
+        t0 = time.perf_counter()
+        for t in range(n):
+            if mode == 0:
+                e.row_append(xs[t])
+            else:
+                src = xs[t] if mode == 1 else pn[t]
+                _lib.check(lib.isvd_engine_row_append(h, src.ctypes.data, 0))
+        t1 = time.perf_counter()
+        e.synchronize()
+        out[name + "_enqueue_us"] = 1e6 * (t1 - t0) / n
+    return out
 
 
 if __name__ == "__main__":
