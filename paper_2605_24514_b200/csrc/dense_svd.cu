@@ -88,7 +88,8 @@ __global__ void __launch_bounds__(kThreads) dsvd_round_kernel(int ldx, int ncp, 
   }
   __syncthreads();
 
-  // ---- Gram of the 32 selected columns (DMMA)
+  // ---- Gram of the 32 selected columns (DMMA); four 4-row chunks of loads
+  // in flight per warp before their DMMAs
   {
     double acc[10][2];
 #pragma unroll
@@ -96,18 +97,26 @@ __global__ void __launch_bounds__(kThreads) dsvd_round_kernel(int ldx, int ncp, 
     const double* cp[4];
 #pragma unroll
     for (int cg = 0; cg < 4; ++cg) cp[cg] = xb + (int64_t)col(cg * 8 + g) * ldx + q;
-    for (int k0 = warp * 4; k0 < ldx; k0 += nw * 4) {
-      double a[4];
+    constexpr int U = 4;
+    for (int k0 = warp * 4; k0 < ldx; k0 += nw * 4 * U) {
+      double a[U][4];
 #pragma unroll
-      for (int cg = 0; cg < 4; ++cg) a[cg] = cp[cg][k0];
-      int t = 0;
+      for (int u = 0; u < U; ++u) {
+        const int kk = k0 + u * nw * 4;
 #pragma unroll
-      for (int c1 = 0; c1 < 4; ++c1)
+        for (int cg = 0; cg < 4; ++cg) a[u][cg] = kk < ldx ? cp[cg][kk] : 0.0;
+      }
 #pragma unroll
-        for (int c2 = c1; c2 < 4; ++c2) {
-          dmma_8x8x4(acc[t][0], acc[t][1], a[c1], a[c2]);
-          ++t;
-        }
+      for (int u = 0; u < U; ++u) {
+        int t = 0;
+#pragma unroll
+        for (int c1 = 0; c1 < 4; ++c1)
+#pragma unroll
+          for (int c2 = c1; c2 < 4; ++c2) {
+            dmma_8x8x4(acc[t][0], acc[t][1], a[u][c1], a[u][c2]);
+            ++t;
+          }
+      }
     }
     // warps add their partial Grams in a fixed order (bit-reproducible runs)
     for (int w = 0; w < nw; ++w) {
@@ -165,29 +174,37 @@ __global__ void __launch_bounds__(kThreads) dsvd_round_kernel(int ldx, int ncp, 
         rs[tid] = s;
       }
       __syncthreads();
+      // M <- J^T M J and Q <- Q J in one pass: thread (pa, pb) owns the 2 x 2
+      // block of rows {p_a, q_a} and columns {p_b, q_b} (the column rotation,
+      // then the row rotation: the same arithmetic as two separate passes)
+      {
+        const int pa = tid >> 4, pb = tid & 15;
+        const double ca = rc[pa], sa = rs[pa], cb = rc[pb], sb = rs[pb];
+        if (sa != 0.0 || sb != 0.0) {
+          const int ra = rp[pa], qa = rq[pa], kb = rp[pb], qb = rq[pb];
+          double m00 = M[ra][kb], m01 = M[ra][qb], m10 = M[qa][kb], m11 = M[qa][qb];
+          if (sb != 0.0) {
+            const double n00 = cb * m00 - sb * m01, n01 = sb * m00 + cb * m01;
+            const double n10 = cb * m10 - sb * m11, n11 = sb * m10 + cb * m11;
+            m00 = n00; m01 = n01; m10 = n10; m11 = n11;
+          }
+          if (sa != 0.0) {
+            const double n00 = ca * m00 - sa * m10, n10 = sa * m00 + ca * m10;
+            const double n01 = ca * m01 - sa * m11, n11 = sa * m01 + ca * m11;
+            m00 = n00; m01 = n01; m10 = n10; m11 = n11;
+          }
+          M[ra][kb] = m00; M[ra][qb] = m01; M[qa][kb] = m10; M[qa][qb] = m11;
+        }
+      }
       for (int task = tid; task < (PW / 2) * PW; task += kThreads) {
         int pr = task / PW, i = task % PW;
         double s = rs[pr];
         if (s == 0.0) continue;
         double c = rc[pr];
         int p = rp[pr], qq = rq[pr];
-        double mp = M[i][p], mq = M[i][qq];
-        M[i][p] = c * mp - s * mq;
-        M[i][qq] = s * mp + c * mq;
         double qp = Q[i][p], qv = Q[i][qq];
         Q[i][p] = c * qp - s * qv;
         Q[i][qq] = s * qp + c * qv;
-      }
-      __syncthreads();
-      for (int task = tid; task < (PW / 2) * PW; task += kThreads) {
-        int pr = task / PW, i = task % PW;
-        double s = rs[pr];
-        if (s == 0.0) continue;
-        double c = rc[pr];
-        int p = rp[pr], qq = rq[pr];
-        double mp = M[p][i], mq = M[qq][i];
-        M[p][i] = c * mp - s * mq;
-        M[qq][i] = s * mp + c * mq;
       }
       __syncthreads();
     }
@@ -208,10 +225,16 @@ __global__ void __launch_bounds__(kThreads) dsvd_round_kernel(int ldx, int ncp, 
   for (int target = 0; target < 2; ++target) {
     double* T = target == 0 ? xb : jb;
     const int ld = target == 0 ? ldx : ncp;
-    for (int r0 = warp * 8; r0 < ld; r0 += nw * 8) {
-      double a[8];
+    // the next 8-row group's operands are loaded before this group's stores
+    auto load = [&](double (&a)[8], int r0) {
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) a[kk] = T[(int64_t)col(kk * 4 + q) * ld + r0 + g];
+    };
+    double a[8];
+    if (warp * 8 < ld) load(a, warp * 8);
+    for (int r0 = warp * 8; r0 < ld; r0 += nw * 8) {
+      double an[8];
+      if (r0 + nw * 8 < ld) load(an, r0 + nw * 8);
 #pragma unroll
       for (int nn = 0; nn < 4; ++nn) {
         double d0 = 0.0, d1 = 0.0;
@@ -220,6 +243,8 @@ __global__ void __launch_bounds__(kThreads) dsvd_round_kernel(int ldx, int ncp, 
         T[(int64_t)col(nn * 8 + 2 * q) * ld + r0 + g] = d0;
         T[(int64_t)col(nn * 8 + 2 * q + 1) * ld + r0 + g] = d1;
       }
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) a[kk] = an[kk];
     }
   }
 }
