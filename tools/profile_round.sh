@@ -11,7 +11,7 @@ SHORT="python bench.py --steps 16 --warmup 3 --no-cpu-baseline --e2e-steps 4 --d
 timeout 300 $SHORT > gpurun_out/plain.log 2>&1 || exit 1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "isvd_timed/" --csv --log-file gpurun_out/launches.csv $SHORT > gpurun_out/ncu_launch.log 2>&1
 FULL="timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled"
-for spec in "project_append:proj5a:8" "rank1_fast:r1fast:8" "arrow_cta:arrowcta:8" "rotate_reg_kernel<40:vflush5a:0" "rotate_reg_kernel<32, 0>:flush5a:0"; do
+for spec in "project_append:proj5a:8" "rank1_fast:r1fast:8" "arrow_cta:arrowcta:8" "rotate_reg_kernel<.int.40:vflush5a:0" "rotate_reg_kernel<.int.32, .bool.0>:flush5a:0"; do
   IFS=: read k name sk <<< "$spec"
   $FULL -k "regex:$k" -s $sk -c 1 -o gpurun_out/$name $SHORT > gpurun_out/ncu_$name.log 2>&1
 done
