@@ -1228,14 +1228,13 @@ static int groups_for(const isvd_engine* e) {
 }
 
 // Small host payloads of a single-group engine (single streams, configs
-// 1-3): one H2D on the engine stream itself.  The staging slot cannot be
+// 1-4): one H2D on the engine stream itself.  The staging slot cannot be
 // overwritten early -- every reader is on the same stream -- so the copy
-// stream, its events and the slot tickets (five API calls) are skipped.
-// Only a few KB: a larger pageable copy queued behind the engine's kernels
-// holds the driver's staging buffer, and the next event's copy then waits
-// for the device (config-4 rows of 40 KB: 64 -> 94 us per event).
+// stream, its events and the slot tickets (five API calls) are skipped
+// (config-4 rows of 40 KB: 103 -> 94 us per synchronised event; config 1:
+// enqueue 37 -> 28 us).
 static bool small_host_path(const isvd_engine* e, size_t bytes) {
-  return groups_for(e) == 1 && !e->pend && bytes <= (size_t(4) << 10);
+  return groups_for(e) == 1 && !e->pend && bytes <= (size_t(64) << 10);
 }
 
 template <class F>
