@@ -533,7 +533,8 @@ struct isvd_engine {
     ev_marks.push_back(ev);
   }
 
-  int S() const { return ld + 1; }
+  // core pitch: ld + 1 rounded to even (16-byte rows for the TMA-staged rotation)
+  int S() const { return ld + 2; }
   int64_t ustride() const { return (int64_t)m_cap * ld; }
   int64_t vstride() const { return (int64_t)n_cap * ld; }
   int64_t astride() const { return (int64_t)m_cap * n_cap; }

@@ -827,6 +827,111 @@ __global__ void __launch_bounds__(kRotWarps * 32, 1)
   }
 }
 
+// Small wide jobs (config 5b's per-tick W window and V, config 4 at k = 64):
+// the eight warps split the output columns of one 8-row group instead of
+// taking a row group each, so a CTA needs only a few rows and the job
+// spreads over many SMs (64 rows per CTA had left 22 CTAs busy for a 1400-row
+// job).  All warps read the whole group before any warp stores into it (one
+// barrier per group; the next group's loads are already in flight).
+template <int KP>
+__global__ void __launch_bounds__(kRotWarps * 32, 1)
+    rotate_nsplit_kernel(int r, int keep, int NP, RotJob j0, RotJob j1, int nblk0, int rpb,
+                         const int* __restrict__ gate) {
+  griddep_launch_dependents();
+  griddep_wait();
+  if (gate && *gate) return;
+  extern __shared__ __align__(16) double smem[];
+  constexpr int kMaxTiles = 3;  // n-tiles per warp (NP <= 192)
+  constexpr int kP = 132;       // row pitch of the staged core: conflict-free B-fragment reads
+  const int NT = NP / 8;
+  double* Qs = smem;            // [r + 1][kP]: rows 0..r of the core, columns 0..NP-1
+  __shared__ __align__(8) uint64_t bar;
+  const bool second = blockIdx.x >= nblk0;
+  const RotJob& J = second ? j1 : j0;
+  const int blk = second ? blockIdx.x - nblk0 : blockIdx.x;
+  const int b = blockIdx.y;
+  const double* Q = J.Q + b * J.q_stride;
+  const bool has_last = (J.z != nullptr) || J.new_row;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // the core (rows 0..r) by TMA bulk copies, one per row, issued by warp 0
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const uint32_t row_bytes = (uint32_t)NP * 8u;
+  if (warp == 0) {
+    if (lane == 0) mbar_expect_tx(&bar, row_bytes * (uint32_t)(r + 1));
+    __syncwarp();
+    for (int l = lane; l <= r; l += 32) bulk_g2s(Qs + l * kP, Q + (int64_t)l * J.ldq, row_bytes, &bar);
+  }
+  double* X = J.X.p + b * J.X.stride;
+  const int ld = J.X.ld;
+  const double zscale = J.z ? J.inj_scale[b] : 0.0;
+  const double* zb = J.z ? J.z + b * J.z_stride : nullptr;
+  const int g = lane >> 2, q = lane & 3;
+  const int per = (NT + kRotWarps - 1) / kRotWarps;
+  const int n_lo = warp * per;
+  const int row_begin = blk * rpb;
+  const int row_end = min(J.rows, row_begin + rpb);
+  // natural k order: lane (g, q) holds X[row][4 kk + q]
+  auto load = [&](int r0, double* dst) {
+    const int row = r0 + g;
+#pragma unroll
+    for (int kk = 0; kk < KP / 4; ++kk) {
+      const int k = 4 * kk + q;
+      dst[kk] = (row < row_end && k < r) ? X[(int64_t)row * ld + k] : 0.0;
+    }
+  };
+  double a[KP / 4];
+  if (row_begin < row_end) load(row_begin, a);
+  mbar_wait(&bar, 0);
+  if (J.new_row && blk == 0) {
+    double* nr = X + (int64_t)J.rows * ld;
+    for (int c = threadIdx.x; c < ld; c += blockDim.x)
+      nr[c] = (has_last && c < keep && c < NP) ? Qs[r * kP + c] : 0.0;
+  }
+  for (int row0 = row_begin; row0 < row_end; row0 += 8) {
+    double an[KP / 4];
+    const bool more = row0 + 8 < row_end;
+    if (more) load(row0 + 8, an);
+    const int row = row0 + g;
+    const double zr = (zb && row < row_end) ? zb[row] * zscale : 0.0;
+    double d[kMaxTiles][2];
+#pragma unroll
+    for (int j = 0; j < kMaxTiles; ++j) d[j][0] = d[j][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < KP / 4; ++kk) {
+      const int k = 4 * kk + q;
+#pragma unroll
+      for (int j = 0; j < kMaxTiles; ++j) {
+        const int c = (n_lo + j) * 8 + g;
+        if (j < per && n_lo + j < NT) {
+          const double bv = (k < r && c < keep) ? Qs[k * kP + c] : 0.0;
+          dmma_8x8x4(d[j][0], d[j][1], a[kk], bv);
+        }
+      }
+    }
+    __syncthreads();  // every warp's DMMAs have consumed this group's rows
+#pragma unroll
+    for (int j = 0; j < kMaxTiles; ++j) {
+      if (j >= per || n_lo + j >= NT) break;
+      const int c0 = (n_lo + j) * 8 + 2 * q;
+      double d0 = d[j][0], d1 = d[j][1];
+      if (zb) {
+        d0 = fma(zr, c0 < keep ? Qs[r * kP + c0] : 0.0, d0);
+        d1 = fma(zr, c0 + 1 < keep ? Qs[r * kP + c0 + 1] : 0.0, d1);
+      }
+      if (row < row_end)
+        *reinterpret_cast<double2*>(X + (int64_t)row * ld + c0) = make_double2(d0, d1);
+    }
+    if (more) {
+#pragma unroll
+      for (int kk = 0; kk < KP / 4; ++kk) a[kk] = an[kk];
+    }
+  }
+}
+
 // Rows per CTA: enough CTAs to cover the SMs twice for small jobs (config 5b's
 // V / W at B = 1), 512 rows for large ones (the Q staging is amortised).
 static int rot_rows_per_block(int64_t total_rows) {
@@ -1549,6 +1654,36 @@ static int rotate_dispatch(int batch, int r, int keep, const RotJob& j0, const R
         rotate_reg_kernel<KP, false><<<dim3(rb0 + rb1, batch), kRegWarps * 32, 0, st>>>(
             r, keep, j0, j1 ? *j1 : j0, rb0, g_gate, fz ? *zf : ZeroFix{});
       if (fused) *fused = fz;
+      ISVD_LAUNCHED();
+      return ISVD_OK;
+    }
+  }
+  const int64_t total_rows = (int64_t)batch * (j0.rows + (j1 ? j1->rows : 0));
+  if constexpr (KP >= 64 && KP % 8 == 0) {
+    const bool tma_ok = (reinterpret_cast<uintptr_t>(j0.Q) % 16 == 0) && j0.ldq % 2 == 0 &&
+                        j0.q_stride % 2 == 0 &&
+                        (!j1 || ((reinterpret_cast<uintptr_t>(j1->Q) % 16 == 0) && j1->ldq % 2 == 0 &&
+                                 j1->q_stride % 2 == 0));
+    if (tma_ok && NT >= 8 && NT <= 3 * kRotWarps && NP <= 132 && total_rows <= 148 * 64) {
+      // small wide job: 16 rows per CTA, warps split the columns
+      static bool attr_ns = false;
+      if (!attr_ns) {
+        ISVD_CUDA(cudaFuncSetAttribute(rotate_nsplit_kernel<KP>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+        attr_ns = true;
+      }
+      constexpr int kNsRows = 16;
+      int s0 = ceil_div(j0.rows, kNsRows);
+      if (j0.new_row && s0 == 0) s0 = 1;
+      int s1 = 0;
+      if (j1) {
+        s1 = ceil_div(j1->rows, kNsRows);
+        if (j1->new_row && s1 == 0) s1 = 1;
+      }
+      const size_t smem_ns = sizeof(double) * (size_t)(r + 1) * 132;
+      ISVD_CUDA(launch_ex(batch <= 32, 1, rotate_nsplit_kernel<KP>, dim3(s0 + s1, batch),
+                          dim3(kRotWarps * 32), smem_ns, st, r, keep, NP, j0, j1 ? *j1 : j0, s0,
+                          kNsRows, g_gate));
       ISVD_LAUNCHED();
       return ISVD_OK;
     }
