@@ -827,6 +827,10 @@ __global__ void __launch_bounds__(kRotWarps * 32, 1)
   }
 }
 
+__device__ void complete_zero_stream(int b, int w, const double* __restrict__ s, int lds, Mat U,
+                                     int m, Mat V, int n, double* coef, double* red,
+                                     const VDefer& vd);
+
 // Small wide jobs (config 5b's per-tick W window and V, config 4 at k = 64):
 // the eight warps split the output columns of one 8-row group instead of
 // taking a row group each, so a CTA needs only a few rows and the job
@@ -836,7 +840,7 @@ __global__ void __launch_bounds__(kRotWarps * 32, 1)
 template <int KP>
 __global__ void __launch_bounds__(kRotWarps * 32, 1)
     rotate_nsplit_kernel(int r, int keep, int NP, RotJob j0, RotJob j1, int nblk0, int rpb,
-                         const int* __restrict__ gate) {
+                         const int* __restrict__ gate, ZeroFix zf) {
   griddep_launch_dependents();
   griddep_wait();
   if (gate && *gate) return;
@@ -883,6 +887,12 @@ __global__ void __launch_bounds__(kRotWarps * 32, 1)
       dst[kk] = (row < row_end && k < r) ? X[(int64_t)row * ld + k] : 0.0;
     }
   };
+  // zero-sigma completion (engine.py:59-70) fused as in rotate_reg_kernel:
+  // every CTA of the stream sees the same final s; the common case skips it
+  bool zf_need = false;
+  if (zf.counter)
+    for (int t = threadIdx.x; t < zf.w; t += blockDim.x) zf_need |= zf.s[(int64_t)b * zf.lds + t] == 0.0;
+  zf_need = __syncthreads_or(zf_need);
   double a[KP / 4];
   if (row_begin < row_end) load(row_begin, a);
   mbar_wait(&bar, 0);
@@ -928,6 +938,23 @@ __global__ void __launch_bounds__(kRotWarps * 32, 1)
     if (more) {
 #pragma unroll
       for (int kk = 0; kk < KP / 4; ++kk) a[kk] = an[kk];
+    }
+  }
+  if (zf_need) {
+    // last CTA of this stream: every row of both sides is written
+    __shared__ int last;
+    __shared__ double zred[32];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned prev = atomicAdd(zf.counter + b, 1u);
+      last = prev == gridDim.x - 1;
+      if (last) zf.counter[b] = 0;
+    }
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      complete_zero_stream(b, zf.w, zf.s, zf.lds, zf.U, zf.m, zf.V, zf.n, smem, zred, zf.vd);
     }
   }
 }
@@ -1683,7 +1710,8 @@ static int rotate_dispatch(int batch, int r, int keep, const RotJob& j0, const R
       const size_t smem_ns = sizeof(double) * (size_t)(r + 1) * 132;
       ISVD_CUDA(launch_ex(batch <= 32, 1, rotate_nsplit_kernel<KP>, dim3(s0 + s1, batch),
                           dim3(kRotWarps * 32), smem_ns, st, r, keep, NP, j0, j1 ? *j1 : j0, s0,
-                          kNsRows, g_gate));
+                          kNsRows, g_gate, zf ? *zf : ZeroFix{}));
+      if (fused) *fused = zf != nullptr;
       ISVD_LAUNCHED();
       return ISVD_OK;
     }
