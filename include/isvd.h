@@ -56,7 +56,8 @@ int64_t isvd_launch_count(void);
 int isvd_debug_counters(int64_t* out8, int reset);
 /* Diagnostics: per-core phase timestamps (SM clock) of the last rank-1 core
  * launch, recorded only by a library built with -DISVD_R1_TRACE (else all
- * zero): out[b * 10 + k], k = 0..9, for b < n (n <= 4096). */
+ * zero): out[b * 10 + k], k = 0..9, for b < n (n <= 4096).  A negative n
+ * reads the marks of the last projection (K1) launch for -n streams. */
 int isvd_debug_trace(int64_t* out, int n);
 
 /* 1. Functional kernels (backend.py:54-63) ---------------------------------- */

@@ -742,8 +742,9 @@ int isvd_debug_counters(int64_t* out8, int reset) {
   return read_debug_counters(out8, reset);
 }
 int isvd_debug_trace(int64_t* out, int n) {
-  if (!out || n < 0 || n > 4096) { set_error("bad argument"); return ISVD_EINVAL; }
+  if (!out || n < -4096 || n > 4096) { set_error("bad argument"); return ISVD_EINVAL; }
   ISVD_TRY(check_device());
+  if (n < 0) return read_k1_trace(out, -n);  // the projection kernel's marks
   return read_r1_trace(out, n);
 }
 int64_t isvd_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }

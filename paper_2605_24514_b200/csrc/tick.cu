@@ -1,6 +1,7 @@
 // Per-tick kernels of the incremental update (kernels K1, K3-K6, K9).
 #include <algorithm>
 #include <type_traits>
+#include <vector>
 #include <cooperative_groups.h>
 #include <cstdlib>
 #include "common.cuh"
@@ -14,6 +15,19 @@ namespace isvd {
 namespace {
 
 constexpr int kRMax = kCoreMaxS;  // max factor width handled by the tick kernels
+
+// projection-kernel phase timestamps (ISVD_R1_TRACE builds): [stream][phase]
+#ifdef ISVD_R1_TRACE
+__device__ long long g_k1_trace[4096][10];
+#define K1_MARK(k)                                                            \
+  do {                                                                        \
+    if (threadIdx.x == 0 && blockIdx.x < 4096) g_k1_trace[blockIdx.x][k] = clock64(); \
+  } while (0)
+#else
+#define K1_MARK(k) \
+  do {             \
+  } while (0)
+#endif
 
 // ---------------------------------------------------------------- K1 + K9
 // One CTA per stream.  Pass 1: p = F^T x (lanes over factor columns, warps
@@ -35,6 +49,7 @@ __global__ void __launch_bounds__(256) project_append_kernel(
     double* __restrict__ N, int arrow_only, VDefer vd, const int* __restrict__ gate,
     double* __restrict__ ring, int64_t ring_stride) {
   if (gate && *gate) return;
+  K1_MARK(0);
   // sized by RT, not kRMax: with a 64 KB staged F the static arrays decide
   // whether 2 or 3 CTAs fit per SM
   constexpr int PN = (RT == 1) ? kGMaxRows : RT * 32;
@@ -99,8 +114,10 @@ __global__ void __launch_bounds__(256) project_append_kernel(
     if (Ab) Ab[(int64_t)c * a_step] = xc;
     if (STAGE) xs[c] = xc;
   }
+  K1_MARK(1);
   if (STAGE) mbar_wait(&bar, 0);
   __syncthreads();
+  K1_MARK(2);
 
   double acc[RT];  // RT = ceil(r / 32) column tiles per lane
 #pragma unroll
@@ -143,6 +160,7 @@ __global__ void __launch_bounds__(256) project_append_kernel(
     if (l < fw) part[warp][l] = acc[t];
   }
   __syncthreads();
+  K1_MARK(3);
   for (int l = threadIdx.x; l < fw; l += blockDim.x) {
     double v = 0.0;
     for (int w = 0; w < nw; ++w) v += part[w][l];
@@ -159,6 +177,7 @@ __global__ void __launch_bounds__(256) project_append_kernel(
     }
   }
   double xnorm2 = block_sum(xx, red);  // contains __syncthreads, p visible after
+  K1_MARK(4);
   // Deferred right basis (F_eff = F G, G r x r): the core takes G^T (F^T x)
   // and the residual subtracts F (G G^T F^T x); F_eff is never formed.
   const double* pc = p;  // projection coefficients of the core
@@ -192,6 +211,7 @@ __global__ void __launch_bounds__(256) project_append_kernel(
     pz = pg[1];
   }
 
+  K1_MARK(5);
   double zz = 0.0;
   double* zb = z + b * z_stride;
   if (STAGE) {
@@ -224,7 +244,9 @@ __global__ void __launch_bounds__(256) project_append_kernel(
       }
     }
   }
+  K1_MARK(6);
   double rho = sqrt(block_sum(zz, red));
+  K1_MARK(7);
   const bool fresh = rho > tol;
   const int P = r + 1;
   double* Kb = core + b * core_stride;
@@ -259,6 +281,236 @@ __global__ void __launch_bounds__(256) project_append_kernel(
       ring[2 * ring_stride + b] = sqrt(xnorm2);
     }
   }
+  K1_MARK(8);
+}
+
+// K1 for batched narrow streams (r <= 32 factor columns, rows <= 256: the
+// row append of config 5a and of the small single streams): the same
+// contract as project_append_kernel<true, 1>, organised so that the CTA's
+// time is the HBM latency of its operands plus a short on-chip part.
+//  * Every row of F is staged by its own TMA bulk copy into a padded row
+//    (pitch ld + 2 doubles, an odd number of 16-byte units): pass 1 (lane =
+//    column, warps over rows) and pass 2 (thread = row, 16-byte loads) are
+//    both bank-conflict free with the coefficients read as broadcasts, and
+//    x[c] sits in the padding of row c.
+//  * Everything that does not depend on F is done while the copy is in
+//    flight: x (norm, tracked-matrix row), the deferred basis G (registers),
+//    the appended residuals Z (each thread keeps its row's entries for both
+//    passes, their dot products with x are finished before the wait), s and N.
+//  * Four CTA barriers after the wait (partials, G^T p, G G^T p, rho).
+constexpr int kP32Rows = 256;
+__global__ void __launch_bounds__(256, 3) project_append32_kernel(
+    int rows, int r, Mat F, const double* __restrict__ x, int64_t x_stride,
+    const double* __restrict__ s, int lds, double tol, double* __restrict__ core,
+    int64_t core_stride, int ldcore, double* __restrict__ z, int64_t z_stride,
+    double* __restrict__ inj_scale, double* __restrict__ rho_out, double* __restrict__ xnorm_out,
+    double* __restrict__ A, int64_t a_stride, int64_t a_off, int64_t a_step,
+    double* __restrict__ N, int arrow_only, VDefer vd, const int* __restrict__ gate,
+    double* __restrict__ ring, int64_t ring_stride) {
+  if (gate && *gate) return;
+  K1_MARK(0);
+  constexpr int GI = (kGMaxRows + 7) / 8;
+  __shared__ double part[8][kGMaxRows];  // per-warp partials of [F | Z^T]^T x
+  __shared__ double part2[8][32];        // per-warp partials of G^T p
+  __shared__ __align__(16) double pcs[32];         // core coefficients
+  __shared__ __align__(16) double pzs[kGMaxRows];  // coefficients multiplying [F | Z^T] in z
+  __shared__ double redx[8], redz[8];
+  __shared__ __align__(8) uint64_t bar;
+  extern __shared__ __align__(128) double Fs[];  // [rows][ld + 2]: F row, x[c], pad
+  const double* __restrict__ G = vd.G;
+  const int fw = G ? vd.fw : r;
+  const int nz = G ? vd.nz : 0;
+  const int gr = fw + nz;
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ld = F.ld, pitch = ld + 2;
+  const double* Fb = F.p + b * F.stride;
+  const bool has = tid < rows;
+
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (tid == 0) mbar_expect_tx(&bar, (uint32_t)rows * ld * 8u);
+  if (has) bulk_g2s(Fs + (size_t)tid * pitch, Fb + (int64_t)tid * ld, (uint32_t)ld * 8u, &bar);
+  // operands that do not depend on F, all in flight together
+  double greg[GI];
+#pragma unroll
+  for (int i = 0; i < GI; ++i) greg[i] = 0.0;
+  if (G) {
+    const double* Gb = G + b * vd.g_stride;
+#pragma unroll
+    for (int i = 0; i < GI; ++i) {
+      const int c = warp + 8 * i;
+      if (c < gr && lane < r) greg[i] = Gb[c * vd.ldg + lane];
+    }
+  }
+  double zreg[kVWin];
+#pragma unroll
+  for (int t = 0; t < kVWin; ++t) zreg[t] = 0.0;
+  if (nz > 0 && has) {
+    const double* Zb = vd.Z + b * vd.z_stride + tid;
+#pragma unroll
+    for (int t = 0; t < kVWin; ++t)
+      if (t < nz) zreg[t] = Zb[(int64_t)t * vd.ldz];
+  }
+  const double xc = has ? x[b * x_stride + tid] : 0.0;
+  const double sj = tid < r ? s[(int64_t)b * lds + tid] : 0.0;
+  const double n0 = tid == 0 ? N[b] : 0.0;
+  if (has) {
+    if (A) A[b * a_stride + a_off + (int64_t)tid * a_step] = xc;
+    Fs[(size_t)tid * pitch + ld] = xc;
+  }
+  {
+    const double xx = warp_sum(xc * xc);
+    if (lane == 0) redx[warp] = xx;
+  }
+  // appended residual columns: <Z[t], x>, per-warp partials next to F's
+#pragma unroll
+  for (int t = 0; t < kVWin; ++t) {
+    if (t < nz) {
+      const double v = warp_sum(zreg[t] * xc);
+      if (lane == 0) part[warp][fw + t] = v;
+    }
+  }
+  K1_MARK(1);
+  mbar_wait(&bar, 0);
+  __syncthreads();
+  K1_MARK(2);
+
+  // ---- pass 1: partial p = F^T x over the warp's rows (lane = column)
+  {
+    const double* fc = Fs + (lane < fw ? lane : 0);
+    const double* xq = Fs + ld;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int c = warp;
+#pragma unroll 2
+    for (; c + 24 < rows; c += 32) {
+      a0 = fma(fc[(c)*pitch], xq[(c)*pitch], a0);
+      a1 = fma(fc[(c + 8) * pitch], xq[(c + 8) * pitch], a1);
+      a2 = fma(fc[(c + 16) * pitch], xq[(c + 16) * pitch], a2);
+      a3 = fma(fc[(c + 24) * pitch], xq[(c + 24) * pitch], a3);
+    }
+    for (; c < rows; c += 8) a0 = fma(fc[c * pitch], xq[c * pitch], a0);
+    if (lane < fw) part[warp][lane] = (a0 + a1) + (a2 + a3);
+  }
+  __syncthreads();
+  K1_MARK(3);
+  // ---- coefficients: core takes pc = G^T p (p over [F | Z^T]); z subtracts
+  // [F | Z^T] pz with pz = G pc.  Without a deferred basis pc = pz = p.
+  if (G) {
+    double v = 0.0;
+#pragma unroll
+    for (int i = 0; i < GI; ++i) {
+      const int c = warp + 8 * i;
+      if (c < gr) {
+        double pe = part[0][c];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) pe += part[w][c];
+        v = fma(greg[i], pe, v);
+      }
+    }
+    part2[warp][lane] = v;
+    __syncthreads();
+    K1_MARK(4);
+    double g0 = part2[0][lane];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) g0 += part2[w][lane];
+    if (warp == 0) pcs[lane] = g0;
+#pragma unroll
+    for (int i = 0; i < GI; ++i) {
+      const int c = warp + 8 * i;
+      const double t = warp_sum(greg[i] * g0);
+      if (lane == 0 && c < gr) pzs[c] = t;
+    }
+  } else {
+    K1_MARK(4);
+    if (tid < fw) {
+      double pe = part[0][tid];
+#pragma unroll
+      for (int w = 1; w < 8; ++w) pe += part[w][tid];
+      pcs[tid] = pe;
+      pzs[tid] = pe;
+    }
+  }
+  __syncthreads();
+  K1_MARK(5);
+
+  // ---- pass 2: z = x - [F | Z^T] pz (thread = row), rho = ||z||
+  double zz = 0.0;
+  if (has) {
+    const double* fr = Fs + (size_t)tid * pitch;
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+    int j = 0;
+#pragma unroll 4
+    for (; j + 3 < fw; j += 4) {
+      const double2 f01 = *reinterpret_cast<const double2*>(fr + j);
+      const double2 f23 = *reinterpret_cast<const double2*>(fr + j + 2);
+      const double2 p01 = *reinterpret_cast<const double2*>(pzs + j);
+      const double2 p23 = *reinterpret_cast<const double2*>(pzs + j + 2);
+      v0 = fma(f01.x, p01.x, v0);
+      v1 = fma(f01.y, p01.y, v1);
+      v2 = fma(f23.x, p23.x, v2);
+      v3 = fma(f23.y, p23.y, v3);
+    }
+    for (; j < fw; ++j) v0 = fma(fr[j], pzs[j], v0);
+#pragma unroll
+    for (int t = 0; t < kVWin; t += 2) {
+      if (t < nz) v2 = fma(zreg[t], pzs[fw + t], v2);
+      if (t + 1 < nz) v3 = fma(zreg[t + 1], pzs[fw + t + 1], v3);
+    }
+    const double zc = xc - ((v0 + v1) + (v2 + v3));
+    z[b * z_stride + tid] = zc;
+    zz = zc * zc;
+  }
+  zz = warp_sum(zz);
+  if (lane == 0) redz[warp] = zz;
+  K1_MARK(6);
+  __syncthreads();
+  double rho2 = redz[0];
+#pragma unroll
+  for (int w = 1; w < 8; ++w) rho2 += redz[w];
+  const double rho = sqrt(rho2);
+  K1_MARK(7);
+  const bool fresh = rho > tol;
+  const int P = r + 1;
+  double* Kb = core + b * core_stride;
+  if (arrow_only) {
+    // the secular solver reads only the diagonal and the last row
+    if (tid < P) {
+      if (tid < r) Kb[tid * ldcore + tid] = sj;
+      Kb[r * ldcore + tid] = (tid < r) ? pcs[tid] : (fresh ? rho : 0.0);
+    }
+  } else {
+    const double* sb = s + (int64_t)b * lds;
+    for (int idx = tid; idx < P * P; idx += 256) {
+      const int i = idx / P, jj = idx % P;
+      double v = 0.0;
+      if (i < r) {
+        if (i == jj) v = sb[i];
+      } else {
+        v = (jj < r) ? pcs[jj] : (fresh ? rho : 0.0);
+      }
+      Kb[i * ldcore + jj] = v;
+    }
+  }
+  if (tid == 0) {
+    double xnorm2 = redx[0];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) xnorm2 += redx[w];
+    inj_scale[b] = fresh ? 1.0 / rho : 0.0;
+    rho_out[b] = rho;
+    xnorm_out[b] = sqrt(xnorm2);
+    const double nn = n0 + xnorm2;
+    N[b] = nn;
+    if (ring) {  // this tick's result row for the host read-back (engine.cu)
+      ring[b] = nn;
+      ring[ring_stride + b] = rho;
+      ring[2 * ring_stride + b] = sqrt(xnorm2);
+    }
+  }
+  K1_MARK(8);
 }
 
 // K1 for a few streams with long factors (config 5b: B = 1, n = 1024,
@@ -1577,6 +1829,23 @@ int launch_project_append(int batch, int rows, int r, Mat F, const double* x, in
                        (F.ld % 2 == 0);
   const bool staged = stage <= 96 * 1024 && aligned;
   const int rt = (r + 31) / 32;
+  if (aligned && rt == 1 && rows <= kP32Rows && F.ld <= 32 && (F.ld % 8) == 0 &&
+      (!G || vd->fw + vd->nz <= kGMaxRows)) {
+    // batched narrow streams: padded per-row staging (see project_append32_kernel)
+    const size_t dyn = sizeof(double) * (size_t)rows * (F.ld + 2);
+    static bool attr32 = false;
+    if (!attr32) {
+      ISVD_CUDA(cudaFuncSetAttribute(project_append32_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+      attr32 = true;
+    }
+    project_append32_kernel<<<batch, 256, dyn, st>>>(
+        rows, r, F, x, x_stride, s, lds, tol, core, core_stride, ldcore, z, z_stride, inj_scale,
+        rho_out, xnorm_out, A, a_stride, a_off, a_step, N, arrow_only, vd ? *vd : VDefer{}, g_gate,
+        ring, ring_stride);
+    ISVD_LAUNCHED();
+    return ISVD_OK;
+  }
   auto go = [&](auto stage_tag, auto rt_tag) -> int {
     constexpr bool SG = decltype(stage_tag)::value;
     constexpr int RT = decltype(rt_tag)::value;
@@ -1925,6 +2194,18 @@ int launch_check_finite(size_t n, const double* p, int* flag, cudaStream_t st) {
   int g = (int)std::min<size_t>((n + 511) / 512, 296);
   check_finite_kernel<<<g, 256, 0, st>>>(n, p, flag);
   ISVD_LAUNCHED();
+  return ISVD_OK;
+}
+
+// Phase timestamps of the last projection launch (ISVD_R1_TRACE builds; zero otherwise).
+int read_k1_trace(int64_t* out, int n) {
+#ifdef ISVD_R1_TRACE
+  std::vector<long long> h((size_t)4096 * 10);
+  ISVD_CUDA(cudaMemcpyFromSymbol(h.data(), g_k1_trace, sizeof(long long) * h.size()));
+  for (int i = 0; i < n * 10; ++i) out[i] = h[i];
+#else
+  for (int i = 0; i < n * 10; ++i) out[i] = 0;
+#endif
   return ISVD_OK;
 }
 

@@ -159,5 +159,6 @@ int launch_sumsq(int batch, int rows, int cols, const double* a, int64_t a_strid
 int launch_check_finite(size_t n, const double* p, int* flag, cudaStream_t st);
 int launch_stage_rank1(int B, const int64_t* i, const int64_t* j, const double* d, int64_t* si,
                        int64_t* sj, double* sd, int64_t m, int64_t n, int* flag, cudaStream_t st);
+int read_k1_trace(int64_t* out, int n);
 
 }  // namespace isvd
