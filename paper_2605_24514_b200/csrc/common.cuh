@@ -57,6 +57,39 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
+// Eight warp sums at once (transposing butterfly: 9 shuffle pairs, depth 5,
+// instead of 40): returns sum over the warp of v[t] with
+// t = 4 * bit4(lane) + 2 * bit3(lane) + bit2(lane) (see warp_sum8_slot).
+__device__ __forceinline__ double warp_sum8(const double (&v)[8]) {
+  const int lane = threadIdx.x & 31;
+  double w4[4], w2[2];
+  {
+    const bool hi = lane & 16;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double keep = hi ? v[k + 4] : v[k], send = hi ? v[k] : v[k + 4];
+      w4[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+  }
+  {
+    const bool hi = lane & 8;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const double keep = hi ? w4[k + 2] : w4[k], send = hi ? w4[k] : w4[k + 2];
+      w2[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+  }
+  const bool hi = lane & 4;
+  const double keep = hi ? w2[1] : w2[0], send = hi ? w2[0] : w2[1];
+  double r = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  r += __shfl_xor_sync(0xffffffffu, r, 2);
+  r += __shfl_xor_sync(0xffffffffu, r, 1);
+  return r;
+}
+__device__ __forceinline__ int warp_sum8_slot(int lane) {
+  return ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+}
+
 // Block-wide sum; `red` must hold >= 32 doubles of shared memory.  Result is
 // returned to every thread.
 __device__ __forceinline__ double block_sum(double v, double* red) {

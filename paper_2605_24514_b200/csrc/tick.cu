@@ -287,18 +287,23 @@ __global__ void __launch_bounds__(256) project_append_kernel(
 // K1 for batched narrow streams (r <= 32 factor columns, rows <= 256: the
 // row append of config 5a and of the small single streams): the same
 // contract as project_append_kernel<true, 1>, organised so that the CTA's
-// time is the HBM latency of its operands plus a short on-chip part.
-//  * Every row of F is staged by its own TMA bulk copy into a padded row
-//    (pitch ld + 2 doubles, an odd number of 16-byte units): pass 1 (lane =
-//    column, warps over rows) and pass 2 (thread = row, 16-byte loads) are
-//    both bank-conflict free with the coefficients read as broadcasts, and
-//    x[c] sits in the padding of row c.
-//  * Everything that does not depend on F is done while the copy is in
-//    flight: x (norm, tracked-matrix row), the deferred basis G (registers),
-//    the appended residuals Z (each thread keeps its row's entries for both
-//    passes, their dot products with x are finished before the wait), s and N.
+// time is the HBM latency of its operands plus a short on-chip part (the
+// general kernel spent 17 K of its 20 K cycles per stream after the data had
+// arrived; tools/k1_trace.py).
+//  * F is staged by TMA bulk copies (32 KB pieces, one issuing thread).
+//    Everything that does not depend on F is loaded before the copy is
+//    issued and consumed while it is in flight: x (norm, tracked-matrix
+//    row), the deferred basis G (registers), the appended residuals Z (each
+//    thread keeps its row's entries for both passes; their dot products with
+//    x, one transposing butterfly, are done before the wait), s and N.
+//  * LD (the factor pitch) is a template parameter: every shared-memory
+//    offset of the two passes is an immediate.  Pass 1: lane = column, each
+//    warp 32 consecutive rows, x read as broadcast pairs.  Pass 2: thread =
+//    row, 16-byte loads walking the row from a skewed start (conflict-free
+//    without padding), coefficients zero-padded to LD.
 //  * Four CTA barriers after the wait (partials, G^T p, G G^T p, rho).
 constexpr int kP32Rows = 256;
+template <int LD>
 __global__ void __launch_bounds__(256, 3) project_append32_kernel(
     int rows, int r, Mat F, const double* __restrict__ x, int64_t x_stride,
     const double* __restrict__ s, int lds, double tol, double* __restrict__ core,
@@ -310,106 +315,128 @@ __global__ void __launch_bounds__(256, 3) project_append32_kernel(
   if (gate && *gate) return;
   K1_MARK(0);
   constexpr int GI = (kGMaxRows + 7) / 8;
-  __shared__ double part[8][kGMaxRows];  // per-warp partials of [F | Z^T]^T x
-  __shared__ double part2[8][32];        // per-warp partials of G^T p
-  __shared__ __align__(16) double pcs[32];         // core coefficients
-  __shared__ __align__(16) double pzs[kGMaxRows];  // coefficients multiplying [F | Z^T] in z
+  constexpr int S = LD / 2;  // 16-byte units per row
+  static_assert(LD % 8 == 0 && LD <= 32, "factor pitch");
+  static_assert(kVWin == 8 && GI <= 8, "warp_sum8 reduces eight values");
+  __shared__ __align__(16) double part[kGMaxRows][8];  // [column of [F | Z^T]][warp] partials of p
+  __shared__ double part2[8][32];                      // per-warp partials of G^T p
+  __shared__ double pcs[32];                           // core coefficients
+  __shared__ __align__(16) double pzf[32];             // coefficients multiplying F in z (zero beyond fw)
+  __shared__ double pzz[kVWin];                        // ... multiplying Z^T
   __shared__ double redx[8], redz[8];
   __shared__ __align__(8) uint64_t bar;
-  extern __shared__ __align__(128) double Fs[];  // [rows][ld + 2]: F row, x[c], pad
+  extern __shared__ __align__(128) double Fs[];  // [rows][LD], then x[rows]
   const double* __restrict__ G = vd.G;
   const int fw = G ? vd.fw : r;
   const int nz = G ? vd.nz : 0;
   const int gr = fw + nz;
   const int b = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int ld = F.ld, pitch = ld + 2;
-  const double* Fb = F.p + b * F.stride;
   const bool has = tid < rows;
+  double* xs = Fs + (size_t)rows * LD;
 
-  if (tid == 0) {
-    mbar_init(&bar, 1);
-    fence_barrier_init();
-  }
-  __syncthreads();
-  if (tid == 0) mbar_expect_tx(&bar, (uint32_t)rows * ld * 8u);
-  if (has) bulk_g2s(Fs + (size_t)tid * pitch, Fb + (int64_t)tid * ld, (uint32_t)ld * 8u, &bar);
-  // operands that do not depend on F, all in flight together
+  // operands that do not depend on F: all loads issued before anything waits
   double greg[GI];
 #pragma unroll
   for (int i = 0; i < GI; ++i) greg[i] = 0.0;
-  if (G) {
-    const double* Gb = G + b * vd.g_stride;
+  if (G && lane < r) {
+    const double* Gp = G + b * vd.g_stride + warp * vd.ldg + lane;
+    const int gstep = 8 * vd.ldg;
 #pragma unroll
-    for (int i = 0; i < GI; ++i) {
-      const int c = warp + 8 * i;
-      if (c < gr && lane < r) greg[i] = Gb[c * vd.ldg + lane];
-    }
+    for (int i = 0; i < GI; ++i)
+      if (warp + 8 * i < gr) greg[i] = Gp[i * gstep];
   }
   double zreg[kVWin];
 #pragma unroll
   for (int t = 0; t < kVWin; ++t) zreg[t] = 0.0;
   if (nz > 0 && has) {
-    const double* Zb = vd.Z + b * vd.z_stride + tid;
+    const double* Zp = vd.Z + b * vd.z_stride + tid;
 #pragma unroll
-    for (int t = 0; t < kVWin; ++t)
-      if (t < nz) zreg[t] = Zb[(int64_t)t * vd.ldz];
+    for (int t = 0; t < kVWin; ++t) {
+      if (t < nz) zreg[t] = *Zp;
+      Zp += vd.ldz;
+    }
   }
   const double xc = has ? x[b * x_stride + tid] : 0.0;
   const double sj = tid < r ? s[(int64_t)b * lds + tid] : 0.0;
   const double n0 = tid == 0 ? N[b] : 0.0;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+    const uint32_t total = (uint32_t)rows * LD * 8u;
+    mbar_expect_tx(&bar, total);
+    const char* src = reinterpret_cast<const char*>(F.p + b * F.stride);
+    const uint32_t kPiece = 32768;
+    for (uint32_t off = 0; off < total; off += kPiece)
+      bulk_g2s(reinterpret_cast<char*>(Fs) + off, src + off, min(kPiece, total - off), &bar);
+  }
+  if (tid < 32) pzf[tid] = 0.0;
   if (has) {
     if (A) A[b * a_stride + a_off + (int64_t)tid * a_step] = xc;
-    Fs[(size_t)tid * pitch + ld] = xc;
+    xs[tid] = xc;
   }
   {
     const double xx = warp_sum(xc * xc);
     if (lane == 0) redx[warp] = xx;
   }
   // appended residual columns: <Z[t], x>, per-warp partials next to F's
+  if (nz > 0) {
+    double zx[kVWin];
 #pragma unroll
-  for (int t = 0; t < kVWin; ++t) {
-    if (t < nz) {
-      const double v = warp_sum(zreg[t] * xc);
-      if (lane == 0) part[warp][fw + t] = v;
-    }
+    for (int t = 0; t < kVWin; ++t) zx[t] = zreg[t] * xc;
+    const double v = warp_sum8(zx);
+    const int t = warp_sum8_slot(lane);
+    if ((lane & 3) == 0 && t < nz) part[fw + t][warp] = v;
   }
   K1_MARK(1);
+  __syncthreads();  // barrier initialised (thread 0), xs / redx / part visible
   mbar_wait(&bar, 0);
-  __syncthreads();
   K1_MARK(2);
 
-  // ---- pass 1: partial p = F^T x over the warp's rows (lane = column)
+  // ---- pass 1: partial p = F^T x over the warp's 32 rows (lane = column)
   {
-    const double* fc = Fs + (lane < fw ? lane : 0);
-    const double* xq = Fs + ld;
+    const int r0 = warp * 32;
+    const int nr = min(32, rows - r0);
+    const double* fp = Fs + r0 * LD + (lane < LD ? lane : 0);
+    const double* xp = xs + r0;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int c = warp;
+    int i = 0;
 #pragma unroll 2
-    for (; c + 24 < rows; c += 32) {
-      a0 = fma(fc[(c)*pitch], xq[(c)*pitch], a0);
-      a1 = fma(fc[(c + 8) * pitch], xq[(c + 8) * pitch], a1);
-      a2 = fma(fc[(c + 16) * pitch], xq[(c + 16) * pitch], a2);
-      a3 = fma(fc[(c + 24) * pitch], xq[(c + 24) * pitch], a3);
+    for (; i + 8 <= nr; i += 8) {
+      const double2 x01 = *reinterpret_cast<const double2*>(xp + i);
+      const double2 x23 = *reinterpret_cast<const double2*>(xp + i + 2);
+      const double2 x45 = *reinterpret_cast<const double2*>(xp + i + 4);
+      const double2 x67 = *reinterpret_cast<const double2*>(xp + i + 6);
+      const double* f = fp + i * LD;
+      a0 = fma(f[0 * LD], x01.x, a0);
+      a1 = fma(f[1 * LD], x01.y, a1);
+      a2 = fma(f[2 * LD], x23.x, a2);
+      a3 = fma(f[3 * LD], x23.y, a3);
+      a0 = fma(f[4 * LD], x45.x, a0);
+      a1 = fma(f[5 * LD], x45.y, a1);
+      a2 = fma(f[6 * LD], x67.x, a2);
+      a3 = fma(f[7 * LD], x67.y, a3);
     }
-    for (; c < rows; c += 8) a0 = fma(fc[c * pitch], xq[c * pitch], a0);
-    if (lane < fw) part[warp][lane] = (a0 + a1) + (a2 + a3);
+    for (; i < nr; ++i) a0 = fma(fp[i * LD], xp[i], a0);
+    if (lane < fw) part[lane][warp] = (a0 + a1) + (a2 + a3);
   }
   __syncthreads();
   K1_MARK(3);
-  // ---- coefficients: core takes pc = G^T p (p over [F | Z^T]); z subtracts
-  // [F | Z^T] pz with pz = G pc.  Without a deferred basis pc = pz = p.
+  // ---- coefficients: the core takes pc = G^T p (p over [F | Z^T]); z
+  // subtracts [F | Z^T] pz with pz = G pc.  Without a deferred basis pc = pz = p.
+  auto psum = [&](int c) {
+    const double2 q0 = *reinterpret_cast<const double2*>(&part[c][0]);
+    const double2 q1 = *reinterpret_cast<const double2*>(&part[c][2]);
+    const double2 q2 = *reinterpret_cast<const double2*>(&part[c][4]);
+    const double2 q3 = *reinterpret_cast<const double2*>(&part[c][6]);
+    return ((((((q0.x + q0.y) + q1.x) + q1.y) + q2.x) + q2.y) + q3.x) + q3.y;
+  };
   if (G) {
     double v = 0.0;
 #pragma unroll
     for (int i = 0; i < GI; ++i) {
       const int c = warp + 8 * i;
-      if (c < gr) {
-        double pe = part[0][c];
-#pragma unroll
-        for (int w = 1; w < 8; ++w) pe += part[w][c];
-        v = fma(greg[i], pe, v);
-      }
+      if (c < gr) v = fma(greg[i], psum(c), v);
     }
     part2[warp][lane] = v;
     __syncthreads();
@@ -418,20 +445,21 @@ __global__ void __launch_bounds__(256, 3) project_append32_kernel(
 #pragma unroll
     for (int w = 1; w < 8; ++w) g0 += part2[w][lane];
     if (warp == 0) pcs[lane] = g0;
+    double gp[8];
 #pragma unroll
-    for (int i = 0; i < GI; ++i) {
-      const int c = warp + 8 * i;
-      const double t = warp_sum(greg[i] * g0);
-      if (lane == 0 && c < gr) pzs[c] = t;
+    for (int i = 0; i < 8; ++i) gp[i] = i < GI ? greg[i] * g0 : 0.0;
+    const double t = warp_sum8(gp);
+    const int c = warp + 8 * warp_sum8_slot(lane);
+    if ((lane & 3) == 0 && c < gr) {
+      if (c < fw) pzf[c] = t;
+      else pzz[c - fw] = t;
     }
   } else {
     K1_MARK(4);
     if (tid < fw) {
-      double pe = part[0][tid];
-#pragma unroll
-      for (int w = 1; w < 8; ++w) pe += part[w][tid];
+      const double pe = psum(tid);
       pcs[tid] = pe;
-      pzs[tid] = pe;
+      pzf[tid] = pe;
     }
   }
   __syncthreads();
@@ -440,25 +468,31 @@ __global__ void __launch_bounds__(256, 3) project_append32_kernel(
   // ---- pass 2: z = x - [F | Z^T] pz (thread = row), rho = ||z||
   double zz = 0.0;
   if (has) {
-    const double* fr = Fs + (size_t)tid * pitch;
+    const double* fr = Fs + tid * LD;
+    // skewed start: the eight rows of a quarter-warp hit eight different
+    // 16-byte bank groups (row pitch S units: S % 8 == 0 -> skew by row,
+    // else by row pair)
+    int u = (S % 8 == 0) ? (tid & 7) : ((tid >> 1) & 3);
     double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
-    int j = 0;
-#pragma unroll 4
-    for (; j + 3 < fw; j += 4) {
-      const double2 f01 = *reinterpret_cast<const double2*>(fr + j);
-      const double2 f23 = *reinterpret_cast<const double2*>(fr + j + 2);
-      const double2 p01 = *reinterpret_cast<const double2*>(pzs + j);
-      const double2 p23 = *reinterpret_cast<const double2*>(pzs + j + 2);
+#pragma unroll
+    for (int k = 0; k < S; k += 2) {
+      const int u1 = (u + 1 == S) ? 0 : u + 1;
+      const double2 f01 = *reinterpret_cast<const double2*>(fr + 2 * u);
+      const double2 p01 = *reinterpret_cast<const double2*>(pzf + 2 * u);
+      const double2 f23 = *reinterpret_cast<const double2*>(fr + 2 * u1);
+      const double2 p23 = *reinterpret_cast<const double2*>(pzf + 2 * u1);
       v0 = fma(f01.x, p01.x, v0);
       v1 = fma(f01.y, p01.y, v1);
       v2 = fma(f23.x, p23.x, v2);
       v3 = fma(f23.y, p23.y, v3);
+      u = (u1 + 1 == S) ? 0 : u1 + 1;
     }
-    for (; j < fw; ++j) v0 = fma(fr[j], pzs[j], v0);
+    if (nz > 0) {
 #pragma unroll
-    for (int t = 0; t < kVWin; t += 2) {
-      if (t < nz) v2 = fma(zreg[t], pzs[fw + t], v2);
-      if (t + 1 < nz) v3 = fma(zreg[t + 1], pzs[fw + t + 1], v3);
+      for (int t = 0; t < kVWin; t += 2) {
+        v2 = fma(zreg[t], t < nz ? pzz[t] : 0.0, v2);
+        v3 = fma(zreg[t + 1], t + 1 < nz ? pzz[t + 1] : 0.0, v3);
+      }
     }
     const double zc = xc - ((v0 + v1) + (v2 + v3));
     z[b * z_stride + tid] = zc;
@@ -1831,18 +1865,30 @@ int launch_project_append(int batch, int rows, int r, Mat F, const double* x, in
   const int rt = (r + 31) / 32;
   if (aligned && rt == 1 && rows <= kP32Rows && F.ld <= 32 && (F.ld % 8) == 0 &&
       (!G || vd->fw + vd->nz <= kGMaxRows)) {
-    // batched narrow streams: padded per-row staging (see project_append32_kernel)
-    const size_t dyn = sizeof(double) * (size_t)rows * (F.ld + 2);
-    static bool attr32 = false;
-    if (!attr32) {
-      ISVD_CUDA(cudaFuncSetAttribute(project_append32_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-      attr32 = true;
+    // batched narrow streams (see project_append32_kernel)
+    const size_t dyn = sizeof(double) * ((size_t)rows * F.ld + rows);
+    auto go32 = [&](auto ld_tag) -> int {
+      constexpr int LD = decltype(ld_tag)::value;
+      static bool attr32 = false;
+      if (!attr32) {
+        ISVD_CUDA(cudaFuncSetAttribute(project_append32_kernel<LD>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+        attr32 = true;
+      }
+      project_append32_kernel<LD><<<batch, 256, dyn, st>>>(
+          rows, r, F, x, x_stride, s, lds, tol, core, core_stride, ldcore, z, z_stride, inj_scale,
+          rho_out, xnorm_out, A, a_stride, a_off, a_step, N, arrow_only, vd ? *vd : VDefer{},
+          g_gate, ring, ring_stride);
+      return ISVD_OK;
+    };
+    int rc32 = ISVD_OK;
+    switch (F.ld) {
+      case 8: rc32 = go32(std::integral_constant<int, 8>{}); break;
+      case 16: rc32 = go32(std::integral_constant<int, 16>{}); break;
+      case 24: rc32 = go32(std::integral_constant<int, 24>{}); break;
+      default: rc32 = go32(std::integral_constant<int, 32>{}); break;
     }
-    project_append32_kernel<<<batch, 256, dyn, st>>>(
-        rows, r, F, x, x_stride, s, lds, tol, core, core_stride, ldcore, z, z_stride, inj_scale,
-        rho_out, xnorm_out, A, a_stride, a_off, a_step, N, arrow_only, vd ? *vd : VDefer{}, g_gate,
-        ring, ring_stride);
+    ISVD_TRY(rc32);
     ISVD_LAUNCHED();
     return ISVD_OK;
   }
