@@ -775,7 +775,7 @@ constexpr int kACLd = 36;  // Uk / Vk tile pitch
 struct ArrowCtaSmem {
   double Uk[33 * kACLd];
   double Vk[33 * kACLd];
-  double d[kACN], kd[kACN], kz[kACN], mu[kACN], sig[kACN], zhat[kACN];
+  double d[kACN], kd[kACN], kz[kACN], kz2[kACN], mu[kACN], sig[kACN], zhat[kACN];
   int kcol[kACN], org[kACN], pos[kACN];
   double wmax[8];
 };
@@ -824,8 +824,9 @@ __device__ __forceinline__ void arrow_cta_body(
   for (int w = 0; w < kACThreads / 32; ++w) scale = fmax(scale, S.wmax[w]);
   scale = scale > 0.0 ? scale : 1.0;
   if (tid < n) {
-    dv /= scale;
-    zv /= scale;
+    const double rs = 1.0 / scale;
+    dv *= rs;
+    zv *= rs;
     S.d[tid] = dv;
   }
   __syncthreads();
@@ -845,6 +846,7 @@ __device__ __forceinline__ void arrow_cta_body(
       S.kcol[pk] = tid;
       S.kd[pk] = dv;
       S.kz[pk] = zv;
+      S.kz2[pk] = zv * zv;
     }
     if (__syncthreads_or(need)) {
       if (tid == 0) af.fb_list[atomicAdd(af.fb_count, 1)] = b;
@@ -872,7 +874,7 @@ __device__ __forceinline__ void arrow_cta_body(
       x = mum;
     } else {
       double zz = 0.0;
-      for (int j = ql; j < N; j += 4) zz += S.kz[j] * S.kz[j];
+      for (int j = ql; j < N; j += 4) zz += S.kz2[j];
       lo = 0.0;
       hi = qsum(zz);
       x = 0.5 * (lo + hi);
@@ -880,25 +882,27 @@ __device__ __forceinline__ void arrow_cta_body(
     int iters = 0;
     for (int it = 0; it < 80; ++it) {
       ++iters;
-      double psi = 0.0, dpsi = 0.0, phi = 0.0, dphi = 0.0, aps = 0.0;
+      // x lies strictly between poles i and i + 1, so the terms of the
+      // poles below (j <= i) are negative and the others positive: the sign
+      // of w sorts them into psi / phi (selects instead of predicated pairs
+      // of FP64 instructions), and sum |w| = phi - psi
+      double psi = 0.0, dpsi = 0.0, phi = 0.0, dphi = 0.0;
       for (int j = ql; j < N; j += 4) {
         const double dj = S.kd[j];
         const double t = frcp((dj - dorg) * (dj + dorg) - x);
-        const double w = S.kz[j] * S.kz[j] * t;
-        if (j <= i) {
-          psi += w;
-          dpsi += w * t;
-        } else {
-          phi += w;
-          dphi += w * t;
-        }
-        aps += fabs(w);
+        const double w = S.kz2[j] * t;
+        const bool below = __double2hiint(w) < 0;
+        const double wl = below ? w : 0.0, wu = below ? 0.0 : w;
+        psi += wl;
+        dpsi = fma(wl, t, dpsi);
+        phi += wu;
+        dphi = fma(wu, t, dphi);
       }
       psi = qsum(psi);
       dpsi = qsum(dpsi);
       phi = qsum(phi);
       dphi = qsum(dphi);
-      aps = qsum(aps);
+      const double aps = phi - psi;
       // identical in the four lanes from here on (xor-reduced inputs)
       const double g = 1.0 + psi + phi;
       if (first) {
@@ -918,14 +922,22 @@ __device__ __forceinline__ void arrow_cta_body(
         hi = x;
       }
       if (fabs(g) <= 4.0 * eps * (1.0 + aps) * N || !(g == g)) break;
+      // rational model psi ~ a1 + b1 / (Di - x'), phi ~ a2 + b2 / (Dn - x')
+      // matched in value and slope at x: b1 = psi' (Di - x)^2, a1 = psi -
+      // psi' (Di - x) (no division); the model's root from the stable
+      // quadratic formula, with ~1 ulp reciprocals (frcp) for its two
+      // quotients -- the iterate only has to land inside the bracket, the
+      // stop tests are on g and on the bracket
       const double pi_ = Di - x;
-      const double b1 = dpsi * pi_ * pi_;
-      const double a1 = psi - b1 / pi_;
+      const double dp1 = dpsi * pi_;
+      const double b1 = dp1 * pi_;
+      const double a1 = psi - dp1;
       double xn;
       if (i < N - 1) {
         const double qn = Dn - x;
-        const double b2 = dphi * qn * qn;
-        const double a2 = phi - b2 / qn;
+        const double dp2 = dphi * qn;
+        const double b2 = dp2 * qn;
+        const double a2 = phi - dp2;
         const double A = 1.0 + a1 + a2;
         const double Dl = Dn - Di;
         const double B = A * Dl + b1 + b2, C = b1 * Dl;
@@ -933,15 +945,15 @@ __device__ __forceinline__ void arrow_cta_body(
         xn = 0.5 * (lo + hi);
         if (disc >= 0.0) {
           const double qv = -0.5 * (B + copysign(sqrt(disc), B));
-          const double p1 = (A != 0.0) ? qv / A : -1e300;
-          const double p2 = (qv != 0.0) ? C / qv : -1e300;
+          const double p1 = (A != 0.0) ? qv * frcp(A) : -1e300;
+          const double p2 = (qv != 0.0) ? C * frcp(qv) : -1e300;
           const double x1 = Di - p1, x2 = Di - p2;
           if (x1 > lo && x1 < hi) xn = x1;
           else if (x2 > lo && x2 < hi) xn = x2;
         }
       } else {
         const double A = 1.0 + a1 + phi;
-        xn = (A > 0.0) ? Di + b1 / A : 0.5 * (lo + hi);
+        xn = (A > 0.0) ? Di + b1 * frcp(A) : 0.5 * (lo + hi);
         if (!(xn > lo && xn < hi)) xn = 0.5 * (lo + hi);
       }
       if (fabs(xn - x) <= 2.0 * eps * fmax(fabs(xn), 1e-300) ||
@@ -1080,20 +1092,31 @@ __device__ __forceinline__ void arrow_cta_body(
   const int nwg = af.uw_mode == 2 ? (af.uw_rows + 7) / 8 : 0;
   const int ngg = (af.gw_rows + 7) / 8;
   const int g = lane >> 2, q = lane & 3;
+  // (the next row group's operand is loaded before the current group's DMMAs)
+  auto load_item = [&](int item, double (&a)[8]) {
+    const bool isw = item < nwg;
+    const double* X = isw ? uwb : gwb;
+    const int ld = isw ? af.uw.ld : af.gw.ld;
+    const int rows = isw ? af.uw_rows : af.gw_rows;
+    const int row = 8 * (isw ? item : item - nwg) + g;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const int k = kk * 4 + q;
+      a[kk] = (row < rows && k < r) ? X[(int64_t)row * ld + k] : 0.0;
+    }
+  };
+  double a[8];
+  if (warp < nwg + ngg) load_item(warp, a);
   for (int item = warp; item < nwg + ngg; item += kACThreads / 32) {
     const bool isw = item < nwg;
     double* X = isw ? uwb : gwb;
     const int ld = isw ? af.uw.ld : af.gw.ld;
     const int rows = isw ? af.uw_rows : af.gw_rows;
     const double* Q = isw ? S.Uk : S.Vk;
-    const int row0 = 8 * (isw ? item : item - nwg);
-    const int row = row0 + g;
-    double a[8];
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {
-      const int k = kk * 4 + q;
-      a[kk] = (row < rows && k < r) ? X[(int64_t)row * ld + k] : 0.0;
-    }
+    const int row = 8 * (isw ? item : item - nwg) + g;
+    double an[8];
+    const int nxt = item + kACThreads / 32;
+    if (nxt < nwg + ngg) load_item(nxt, an);
     double d[4][2];
 #pragma unroll
     for (int nn = 0; nn < 4; ++nn) d[nn][0] = d[nn][1] = 0.0;
@@ -1109,6 +1132,8 @@ __device__ __forceinline__ void arrow_cta_body(
         if (c0 < ld) *reinterpret_cast<double2*>(X + (int64_t)row * ld + c0) = make_double2(d[nn][0], d[nn][1]);
       }
     }
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) a[kk] = an[kk];
   }
   // new rows: W[uw_rows] = Uk[r, :keep] (mode 2) or W = Uk[:, :keep] (mode 1);
   // Gv[gw_rows] = (1/rho) Vk[r, :keep]
