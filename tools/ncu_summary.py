@@ -28,6 +28,9 @@ KEYS = {
     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_cycles_pct",
     "sm__warps_active.avg.pct_of_peak_sustained_active": "occupancy_pct",
     "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active": "dmma_pipe_pct",
+    "sm__ops_path_tensor_src_fp64.avg.pct_of_peak_sustained_elapsed": "tensor_fp64_ops_pct_peak",
+    "sm__ops_path_tensor_src_fp64.sum": "tensor_fp64_ops",
+    "TPC.TriageCompute.sm__pipe_fp64_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed": "fp64_cycles_realtime_pct",
     "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio": "stall_wait_per_issue",
     "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
     "launch__registers_per_thread": "regs",
