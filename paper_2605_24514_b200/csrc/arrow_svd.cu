@@ -80,6 +80,49 @@ __device__ __forceinline__ double frcp(double x) {
   return fma(r, e, r);
 }
 
+// One step of the two-pole rational iteration for the secular equation
+// g(x) = 1 + psi(x) + phi(x) (poles below / above the root, squared
+// distances Di, Dn from the origin): the model psi ~ a1 + b1 / (Di - x'),
+// phi ~ a2 + b2 / (Dn - x') matches value and slope at x (b1 = psi' (Di -
+// x)^2, a1 = psi - psi' (Di - x): no division), its root comes from the
+// stable quadratic formula with ~1 ulp reciprocals for the two quotients --
+// the iterate only has to land inside the bracket (lo, hi), the stop tests
+// are on g and on the bracket -- and falls back to bisection otherwise.
+// `last`: the root beyond the largest pole (phi is a plain constant there).
+__device__ __forceinline__ double secular_model_step(bool last, double x, double psi, double dpsi,
+                                                     double phi, double dphi, double Di, double Dn,
+                                                     double lo, double hi) {
+  const double pi_ = Di - x;
+  const double dp1 = dpsi * pi_;
+  const double b1 = dp1 * pi_;
+  const double a1 = psi - dp1;
+  double xn = 0.5 * (lo + hi);
+  if (!last) {
+    const double qn = Dn - x;
+    const double dp2 = dphi * qn;
+    const double b2 = dp2 * qn;
+    const double a2 = phi - dp2;
+    const double A = 1.0 + a1 + a2;
+    const double Dl = Dn - Di;
+    // A p^2 + (A Dl + b1 + b2) p + b1 Dl = 0 with p = Di - x'
+    const double B = A * Dl + b1 + b2, C = b1 * Dl;
+    const double disc = B * B - 4.0 * A * C;
+    if (disc >= 0.0) {
+      const double qv = -0.5 * (B + copysign(sqrt(disc), B));
+      const double p1 = (A != 0.0) ? qv * frcp(A) : -1e300;
+      const double p2 = (qv != 0.0) ? C * frcp(qv) : -1e300;
+      const double x1 = Di - p1, x2 = Di - p2;
+      if (x1 > lo && x1 < hi) xn = x1;
+      else if (x2 > lo && x2 < hi) xn = x2;
+    }
+  } else {
+    const double A = 1.0 + a1 + phi;
+    const double xc = (A > 0.0) ? Di + b1 * frcp(A) : xn;
+    if (xc > lo && xc < hi) xn = xc;
+  }
+  return xn;
+}
+
 template <class SM>
 __device__ __forceinline__ void apply_rots(double* col, int64_t stride, const SM& S,
                                            bool left) {
@@ -280,51 +323,44 @@ __device__ __forceinline__ void arrow_body(int b, int n, const double* __restric
   // over once every thread has one (n = 33 with one warp per core).
   auto warp_root = [&](int i) {
     const int lane = tid & 31;
-      int o;
-      double lo, hi;
+      // The first evaluation is at the interval midpoint (origin kd[i]); its
+      // sign picks the origin (the nearer pole) and the half-interval, and
+      // its terms already feed the first rational-model step (no separate
+      // bracketing pass).  x lies strictly between poles i and i + 1, so the
+      // terms of the poles below are negative and the others positive: the
+      // sign of w sorts them into psi / phi, and sum |w| = phi - psi.
       const double di = S.kd[i];
-      if (i < N - 1) {
-        const double dn = S.kd[i + 1];
-        const double sm = 0.5 * (di + dn);
-        const double mum = (sm - di) * (sm + di);
-        double f = 0.0;
-        for (int j = lane; j < N; j += 32) {
-          const double dj = S.kd[j];
-          f += S.kz[j] * S.kz[j] * frcp((dj - di) * (dj + di) - mum);
-        }
-        f = 1.0 + warp_sum(f);
-        if (f > 0.0) {
-          o = i; lo = 0.0; hi = mum;
-        } else {
-          o = i + 1; lo = (sm - dn) * (sm + dn); hi = 0.0;
-        }
+      const double dn = i < N - 1 ? S.kd[i + 1] : 0.0;
+      const double sm = 0.5 * (di + dn);
+      const double mum = (sm - di) * (sm + di);
+      int o = i;
+      double dorg = di, lo, hi, x, Di = 0.0, Dn = 0.0;
+      bool first = i < N - 1;
+      if (first) {
+        lo = 0.0;
+        hi = mum;
+        x = mum;
       } else {
-        o = i;
         double zz = 0.0;
         for (int j = lane; j < N; j += 32) zz += S.kz[j] * S.kz[j];
         lo = 0.0;
         hi = warp_sum(zz);
+        x = 0.5 * (lo + hi);
       }
-      const double dorg = S.kd[o];
-      const double Di = (di - dorg) * (di + dorg);
-      const double Dn = (i < N - 1) ? (S.kd[i + 1] - dorg) * (S.kd[i + 1] + dorg) : 0.0;
-      double x = 0.5 * (lo + hi);
       int iters = 0;
       for (int it = 0; it < 80; ++it) {
         ++iters;
-        double psi = 0.0, dpsi = 0.0, phi = 0.0, dphi = 0.0, aps = 0.0;
+        double psi = 0.0, dpsi = 0.0, phi = 0.0, dphi = 0.0;
         for (int j = lane; j < N; j += 32) {
           const double dj = S.kd[j];
           const double t = frcp((dj - dorg) * (dj + dorg) - x);
           const double w = S.kz[j] * S.kz[j] * t;
-          if (j <= i) {
-            psi += w;
-            dpsi += w * t;
-          } else {
-            phi += w;
-            dphi += w * t;
-          }
-          aps += fabs(w);
+          const bool below = __double2hiint(w) < 0;
+          const double wl = below ? w : 0.0, wu = below ? 0.0 : w;
+          psi += wl;
+          dpsi = fma(wl, t, dpsi);
+          phi += wu;
+          dphi = fma(wu, t, dphi);
         }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
@@ -332,38 +368,28 @@ __device__ __forceinline__ void arrow_body(int b, int n, const double* __restric
           dpsi += __shfl_xor_sync(0xffffffffu, dpsi, off);
           phi += __shfl_xor_sync(0xffffffffu, phi, off);
           dphi += __shfl_xor_sync(0xffffffffu, dphi, off);
-          aps += __shfl_xor_sync(0xffffffffu, aps, off);
         }
         // identical in every lane from here on (xor-reduced inputs)
+        const double aps = phi - psi;
         const double g = 1.0 + psi + phi;
-        if (g < 0.0) lo = x; else hi = x;
-        if (fabs(g) <= 4.0 * eps * (1.0 + aps) * N || !(g == g)) break;
-        const double pi_ = Di - x;
-        const double b1 = dpsi * pi_ * pi_;
-        const double a1 = psi - b1 / pi_;
-        double xn;
-        if (i < N - 1) {
-          const double qn = Dn - x;
-          const double b2 = dphi * qn * qn;
-          const double a2 = phi - b2 / qn;
-          const double A = 1.0 + a1 + a2;
-          const double Dl = Dn - Di;
-          const double B = A * Dl + b1 + b2, C = b1 * Dl;
-          const double disc = B * B - 4.0 * A * C;
-          xn = 0.5 * (lo + hi);
-          if (disc >= 0.0) {
-            const double q = -0.5 * (B + copysign(sqrt(disc), B));
-            const double p1 = (A != 0.0) ? q / A : -1e300;
-            const double p2 = (q != 0.0) ? C / q : -1e300;
-            const double x1 = Di - p1, x2 = Di - p2;
-            if (x1 > lo && x1 < hi) xn = x1;
-            else if (x2 > lo && x2 < hi) xn = x2;
+        if (first) {
+          first = false;
+          if (!(g > 0.0)) {  // root above the midpoint: origin at kd[i+1]
+            o = i + 1;
+            dorg = dn;
+            lo = (sm - dn) * (sm + dn);
+            hi = 0.0;
+            x = lo;
           }
+          Di = (di - dorg) * (di + dorg);
+          Dn = (dn - dorg) * (dn + dorg);
+        } else if (g < 0.0) {
+          lo = x;
         } else {
-          const double A = 1.0 + a1 + phi;
-          xn = (A > 0.0) ? Di + b1 / A : 0.5 * (lo + hi);
-          if (!(xn > lo && xn < hi)) xn = 0.5 * (lo + hi);
+          hi = x;
         }
+        if (fabs(g) <= 4.0 * eps * (1.0 + aps) * N || !(g == g)) break;
+        const double xn = secular_model_step(i == N - 1, x, psi, dpsi, phi, dphi, Di, Dn, lo, hi);
         if (fabs(xn - x) <= 2.0 * eps * fmax(fabs(xn), 1e-300) ||
             hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi))) {
           x = xn;
@@ -439,33 +465,7 @@ __device__ __forceinline__ void arrow_body(int b, int n, const double* __restric
       if (g < 0.0) lo = x; else hi = x;
       if (fabs(g) <= 4.0 * eps * (1.0 + aps) * N || !(g == g)) break;
       // two-pole rational model through (psi, dpsi) and (phi, dphi)
-      const double pi_ = Di - x;
-      const double b1 = dpsi * pi_ * pi_;
-      const double a1 = psi - b1 / pi_;
-      double xn;
-      if (i < N - 1) {
-        const double qn = Dn - x;
-        const double b2 = dphi * qn * qn;
-        const double a2 = phi - b2 / qn;
-        const double A = 1.0 + a1 + a2;
-        const double Dl = Dn - Di;
-        // A p^2 + (A Dl + b1 + b2) p + b1 Dl = 0 with p = Di - x'
-        const double B = A * Dl + b1 + b2, C = b1 * Dl;
-        const double disc = B * B - 4.0 * A * C;
-        xn = 0.5 * (lo + hi);
-        if (disc >= 0.0) {
-          const double q = -0.5 * (B + copysign(sqrt(disc), B));
-          const double p1 = (A != 0.0) ? q / A : -1e300;
-          const double p2 = (q != 0.0) ? C / q : -1e300;
-          const double x1 = Di - p1, x2 = Di - p2;
-          if (x1 > lo && x1 < hi) xn = x1;
-          else if (x2 > lo && x2 < hi) xn = x2;
-        }
-      } else {
-        const double A = 1.0 + a1 + phi;
-        xn = (A > 0.0) ? Di + b1 / A : 0.5 * (lo + hi);
-        if (!(xn > lo && xn < hi)) xn = 0.5 * (lo + hi);
-      }
+      const double xn = secular_model_step(i == N - 1, x, psi, dpsi, phi, dphi, Di, Dn, lo, hi);
       if (fabs(xn - x) <= 2.0 * eps * fmax(fabs(xn), 1e-300) || hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi))) {
         x = xn;
         break;
@@ -922,40 +922,7 @@ __device__ __forceinline__ void arrow_cta_body(
         hi = x;
       }
       if (fabs(g) <= 4.0 * eps * (1.0 + aps) * N || !(g == g)) break;
-      // rational model psi ~ a1 + b1 / (Di - x'), phi ~ a2 + b2 / (Dn - x')
-      // matched in value and slope at x: b1 = psi' (Di - x)^2, a1 = psi -
-      // psi' (Di - x) (no division); the model's root from the stable
-      // quadratic formula, with ~1 ulp reciprocals (frcp) for its two
-      // quotients -- the iterate only has to land inside the bracket, the
-      // stop tests are on g and on the bracket
-      const double pi_ = Di - x;
-      const double dp1 = dpsi * pi_;
-      const double b1 = dp1 * pi_;
-      const double a1 = psi - dp1;
-      double xn;
-      if (i < N - 1) {
-        const double qn = Dn - x;
-        const double dp2 = dphi * qn;
-        const double b2 = dp2 * qn;
-        const double a2 = phi - dp2;
-        const double A = 1.0 + a1 + a2;
-        const double Dl = Dn - Di;
-        const double B = A * Dl + b1 + b2, C = b1 * Dl;
-        const double disc = B * B - 4.0 * A * C;
-        xn = 0.5 * (lo + hi);
-        if (disc >= 0.0) {
-          const double qv = -0.5 * (B + copysign(sqrt(disc), B));
-          const double p1 = (A != 0.0) ? qv * frcp(A) : -1e300;
-          const double p2 = (qv != 0.0) ? C * frcp(qv) : -1e300;
-          const double x1 = Di - p1, x2 = Di - p2;
-          if (x1 > lo && x1 < hi) xn = x1;
-          else if (x2 > lo && x2 < hi) xn = x2;
-        }
-      } else {
-        const double A = 1.0 + a1 + phi;
-        xn = (A > 0.0) ? Di + b1 * frcp(A) : 0.5 * (lo + hi);
-        if (!(xn > lo && xn < hi)) xn = 0.5 * (lo + hi);
-      }
+      const double xn = secular_model_step(i == N - 1, x, psi, dpsi, phi, dphi, Di, Dn, lo, hi);
       if (fabs(xn - x) <= 2.0 * eps * fmax(fabs(xn), 1e-300) ||
           hi - lo <= 2.0 * eps * fmax(fabs(lo), fabs(hi))) {
         x = xn;
