@@ -784,7 +784,7 @@ __device__ __forceinline__ void arrow_cta_body(
     int n, const double* __restrict__ core, int64_t core_stride, int ldcore,
     double* __restrict__ uk, double* __restrict__ vk, int64_t out_stride, int ldo,
     double* __restrict__ sv, int64_t sv_stride, double* __restrict__ s_out, int64_t s_out_stride,
-    int nkeep, const int* __restrict__ gate, const ArrowFuse& af) {
+    int nkeep, const int* __restrict__ gate, const ArrowFuse& af, int& done_old) {
   if (gate && *gate) return;
   extern __shared__ __align__(16) unsigned char ac_raw[];
   ArrowCtaSmem& S = *reinterpret_cast<ArrowCtaSmem*>(ac_raw);
@@ -849,7 +849,10 @@ __device__ __forceinline__ void arrow_cta_body(
       S.kz2[pk] = zv * zv;
     }
     if (__syncthreads_or(need)) {
-      if (tid == 0) af.fb_list[atomicAdd(af.fb_count, 1)] = b;
+      if (tid == 0) {
+        af.fb_list[atomicAdd(af.fb_count, 1)] = b;
+        done_old = fb_arrive(af.fb_fast_done, true);
+      }
       return;
     }
   }
@@ -1019,9 +1022,13 @@ __device__ __forceinline__ void arrow_cta_body(
     if (ql == 0) S.Uk[r * kACLd + pc] = -iu;
   }
   if (__syncthreads_or(dead)) {
-    if (tid == 0) af.fb_list[atomicAdd(af.fb_count, 1)] = b;
+    if (tid == 0) {
+      af.fb_list[atomicAdd(af.fb_count, 1)] = b;
+      done_old = fb_arrive(af.fb_fast_done, true);
+    }
     return;
   }
+  if (tid == 0) done_old = fb_arrive(af.fb_fast_done, false);  // this core stays here
   AC_MARK(5);
   // install sigma; columns >= keep of the tiles out of the rotation
   const int keep = nkeep;
@@ -1122,26 +1129,25 @@ __device__ __forceinline__ void arrow_cta_body(
   AC_MARK(7);
 }
 
-// The last CTA to finish hands the cores on the fallback list (if any) to
-// the one-warp kernel by a device-side tail launch (no host launch per tick).
+// The CTA whose decision completes the count (fb_arrive) hands the cores on
+// the fallback list (if any) to the one-warp kernel by a device-side tail
+// launch, which starts when this grid has completed (no host launch per tick).
 __global__ void __launch_bounds__(kACThreads, 6) arrow_cta_kernel(
     int n, const double* __restrict__ core, int64_t core_stride, int ldcore,
     double* __restrict__ uk, double* __restrict__ vk, int64_t out_stride, int ldo,
     double* __restrict__ sv, int64_t sv_stride, double* __restrict__ s_out, int64_t s_out_stride,
     int nkeep, const int* __restrict__ gate, ArrowFuse af) {
+  int done_old = -1;
   arrow_cta_body(n, core, core_stride, ldcore, uk, vk, out_stride, ldo, sv, sv_stride, s_out,
-                 s_out_stride, nkeep, gate, af);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(af.fb_fast_done, 1) == (int)gridDim.x - 1) {
-      *af.fb_fast_done = 0;
-      const int cnt = *reinterpret_cast<volatile int*>(af.fb_count);
-      if (cnt > 0)
-        arrow_svd_kernel<40, false, 1><<<min(cnt, 4 * 148), 32, 0, cudaStreamTailLaunch>>>(
-            n, core, core_stride, ldcore, uk, vk, out_stride, ldo, sv, sv_stride, s_out,
-            s_out_stride, nkeep, gate, af);
-    }
+                 s_out_stride, nkeep, gate, af, done_old);
+  if (threadIdx.x == 0 && done_old == (int)gridDim.x - 1) {
+    __threadfence();  // the other CTAs' list entries (each ordered before its count)
+    *af.fb_fast_done = 0;
+    const int cnt = *reinterpret_cast<volatile int*>(af.fb_count);
+    if (cnt > 0)
+      arrow_svd_kernel<40, false, 1><<<min(cnt, 4 * 148), 32, 0, cudaStreamTailLaunch>>>(
+          n, core, core_stride, ldcore, uk, vk, out_stride, ldo, sv, sv_stride, s_out,
+          s_out_stride, nkeep, gate, af);
   }
 }
 

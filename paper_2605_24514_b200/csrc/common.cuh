@@ -108,6 +108,19 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return r;
 }
 
+// CTA-per-core kernels with a device-launched fallback: every CTA counts
+// itself once it has decided whether it keeps its core (`handed`: it appended
+// the core to the fallback list, which is ordered before the count); the CTA
+// whose arrival completes the count tail-launches the fallback kernel when it
+// finishes.  Counting at the decision instead of at the end keeps the fence
+// and the atomic's round trip (20-35 % of a CTA's lifetime in ncu's stall
+// samples) off the end of every CTA: the count is in flight during the
+// epilogue.  Returns the previous count (thread 0 only).
+__device__ __forceinline__ int fb_arrive(int* done, bool handed) {
+  if (handed) __threadfence();
+  return atomicAdd(done, 1);
+}
+
 // D(8x8) += A(8x4, row) * B(4x8, col), FP64 tensor path (DMMA.8x8x4).
 // Fragment layout (verified on B200, profiles/r01_fp64_peaks.txt):
 //   a = A[lane>>2][lane&3], b = B[lane&3][lane>>2],

@@ -1020,7 +1020,7 @@ __device__ __forceinline__ void rank1_fast_body(
     int s, int batch, const Rank1Core& rc, double* __restrict__ uk, double* __restrict__ vk,
     int64_t out_stride, int ldo, double* __restrict__ sv_out, int64_t sv_stride,
     double* __restrict__ s_out, int64_t s_out_stride, int* __restrict__ fb_list,
-    int* __restrict__ fb_count) {
+    int* __restrict__ fb_count, int& done_old) {
   extern __shared__ __align__(16) unsigned char r1_raw[];
   R1Smem& S = *reinterpret_cast<R1Smem*>(r1_raw);
   const int b = blockIdx.x;
@@ -1159,7 +1159,10 @@ __device__ __forceinline__ void rank1_fast_body(
   }
   __syncthreads();
   if (S.status < 0) {
-    if (tid == 0) fb_list[atomicAdd(fb_count, 1)] = b;
+    if (tid == 0) {
+      fb_list[atomicAdd(fb_count, 1)] = b;
+      done_old = fb_arrive(rc.fb_fast_done, true);
+    }
     finish_acc();
     return;
   }
@@ -1480,7 +1483,10 @@ __device__ __forceinline__ void rank1_fast_body(
       }
     }
     if (!conv) {
-      if (tid == 0) fb_list[atomicAdd(fb_count, 1)] = b;
+      if (tid == 0) {
+      fb_list[atomicAdd(fb_count, 1)] = b;
+      done_old = fb_arrive(rc.fb_fast_done, true);
+    }
     finish_acc();
       return;
     }
@@ -1527,11 +1533,15 @@ __device__ __forceinline__ void rank1_fast_body(
   }
   __syncthreads();
   if (S.status < 0) {
-    if (tid == 0) fb_list[atomicAdd(fb_count, 1)] = b;
+    if (tid == 0) {
+      fb_list[atomicAdd(fb_count, 1)] = b;
+      done_old = fb_arrive(rc.fb_fast_done, true);
+    }
     finish_acc();
     return;
   }
   if (tid == 0) {
+    done_old = fb_arrive(rc.fb_fast_done, false);  // this core stays here
     atomicAdd(&g_debug_counters[1], 1ull);
     if (sweep) {
       atomicAdd(&g_debug_counters[0], (unsigned long long)nsw);
@@ -1647,30 +1657,29 @@ __device__ __forceinline__ void rank1_fast_body(
   R1_MARK(9);
 }
 
-// The last CTA to finish hands the cores on the fallback list (if any) to
-// the one-warp kernel by a device-side tail launch (it starts when this grid
-// has completed): no host launch per tick for the rare fallback.
+// The CTA whose decision completes the count (fb_arrive) hands the cores on
+// the fallback list (if any) to the one-warp kernel by a device-side tail
+// launch (it starts when this grid has completed): no host launch per tick
+// for the rare fallback.
 __global__ void __launch_bounds__(kR1Threads, 8) rank1_fast_kernel(
     int s, int batch, Rank1Core rc, double* __restrict__ uk, double* __restrict__ vk,
     int64_t out_stride, int ldo, double* __restrict__ sv_out, int64_t sv_stride,
     double* __restrict__ s_out, int64_t s_out_stride) {
+  int done_old = -1;
   rank1_fast_body(s, batch, rc, uk, vk, out_stride, ldo, sv_out, sv_stride, s_out, s_out_stride,
-                  rc.fb_list, rc.fb_count);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(rc.fb_fast_done, 1) == (int)gridDim.x - 1) {
-      *rc.fb_fast_done = 0;
-      const int cnt = *reinterpret_cast<volatile int*>(rc.fb_count);
-      if (cnt > 0) {
-        Rank1Core fb = rc;
-        fb.A = nullptr;  // tracked entry / N / ring already updated
-        const int grid = min((cnt + kJ32Warps - 1) / kJ32Warps, 2 * 148);
-        jacobi32c_kernel<true><<<grid, kJ32Warps * 32, sizeof(J32Smem) * kJ32Warps,
-                                 cudaStreamTailLaunch>>>(s, nullptr, 0, 0, uk, vk, out_stride, ldo,
-                                                         sv_out, sv_stride, batch, fb, s_out,
-                                                         s_out_stride);
-      }
+                  rc.fb_list, rc.fb_count, done_old);
+  if (threadIdx.x == 0 && done_old == (int)gridDim.x - 1) {
+    __threadfence();  // the other CTAs' list entries (each ordered before its count)
+    *rc.fb_fast_done = 0;
+    const int cnt = *reinterpret_cast<volatile int*>(rc.fb_count);
+    if (cnt > 0) {
+      Rank1Core fb = rc;
+      fb.A = nullptr;  // tracked entry / N / ring already updated
+      const int grid = min((cnt + kJ32Warps - 1) / kJ32Warps, 2 * 148);
+      jacobi32c_kernel<true><<<grid, kJ32Warps * 32, sizeof(J32Smem) * kJ32Warps,
+                               cudaStreamTailLaunch>>>(s, nullptr, 0, 0, uk, vk, out_stride, ldo,
+                                                       sv_out, sv_stride, batch, fb, s_out,
+                                                       s_out_stride);
     }
   }
 }
