@@ -1425,10 +1425,22 @@ __global__ void __launch_bounds__(kRegWarps * 32, 8)
           a[kk + 1] = v.y;
         }
       } else {
+        // the lane whose k range crosses into Z^T: nx entries from X, then
+        // the appended residuals through a running pointer (one add per k)
+        const int k0 = q * KQ;
+        const int nx = min(max(J.zfw - k0, 0), KQ);
+        const int ne = min(max(r - k0, 0), KQ);  // entries below r
+        const double* zp = zsb + (int64_t)max(k0 - J.zfw, 0) * J.ldzs;
 #pragma unroll
         for (int kk = 0; kk < KQ; ++kk) {
-          const int k = q * KQ + kk;
-          a[kk] = k < J.zfw ? src[k] : (k < r ? zsb[(int64_t)(k - J.zfw) * J.ldzs] : 0.0);
+          double v = 0.0;
+          if (kk < nx) {
+            v = src[k0 + kk];
+          } else if (kk < ne) {
+            v = *zp;
+            zp += J.ldzs;
+          }
+          a[kk] = v;
         }
       }
     } else if (row < row_end) {
