@@ -732,7 +732,19 @@ def run_gpu(args):
         if ncu_key and ncu_key in summ:
             roof["ncu"] = {k2: summ[ncu_key].get(k2) for k2 in
                            ("fp64_pipe_pct", "dmma_pipe_pct", "occupancy_pct", "dram_pct_peak",
-                            "regs", "warp_instructions")}
+                            "regs", "warp_instructions", "tensor_fp64_ops")}
+            # executed (not algorithmic) FP64 tensor work: ncu's
+            # sm__ops_path_tensor_src_fp64.sum of one stream-group launch,
+            # scaled to all streams, over this run's measured launch time --
+            # the share of the DMMA roof the kernel actually occupies (symmetric
+            # products computed in full tiles, 8-row group padding and the
+            # convergence-check Grams are executed but not algorithmic flops)
+            t_ops = summ[ncu_key].get("tensor_fp64_ops")
+            if t_ops and dom["ms"]:
+                ex = t_ops * 4.0 * B / TOTAL_STREAMS * n_launch / (dom["ms"] / 1e3) / 1e12
+                roof["executed"] = {"tensor_tflops": ex, "frac_of_dmma_peak": ex / DMMA_PEAK_TFS,
+                                    "source": f"profiles/{summ_file}: {ncu_key} "
+                                              "sm__ops_path_tensor_src_fp64.sum x 4 groups"}
         # BASELINE's second metric: basis-rotation HBM GB/s -- the deferred U
         # flush and the V materialisation, the two launches that stream a
         # tall basis through HBM

@@ -118,6 +118,42 @@ class TestMetrics:
         o = compute_oracle(rng.standard_normal((10, 6)), 2)
         assert o.singular_values.shape == (6,) and o.basis.shape == (10, 2)
 
+    def test_oracle_after_refresh_reuses_the_refresh_svd(self):
+        """The observation that follows an init / refresh of the same tracked
+        matrix is served from that dense SVD (engine.cu: svdc_*): it must
+        equal a fresh factorisation of the tracked matrix bit for bit, and any
+        event must invalidate it (metrics.py:56-64, stream.py:291-333)."""
+        rng = np.random.default_rng(7)
+        a0 = rng.standard_normal((60, 9)) @ rng.standard_normal((9, 40)) + 0.01 * rng.standard_normal((60, 40))
+        eng = SvdEngine(a0, k=6)
+        for phase in range(3):
+            if phase == 1:
+                for _ in range(5):
+                    eng.row_append(rng.standard_normal(40))
+                eng.refresh()
+            cached = compute_oracle(eng, 6)           # right after init / refresh
+            host = compute_oracle(eng.tracked, 6)     # the same matrix through the functional entry
+            np.testing.assert_allclose(cached.singular_values, host.singular_values, rtol=1e-12, atol=1e-13)
+            np.testing.assert_allclose(cached.basis, host.basis, atol=1e-10)
+            eng.set_rank(6)                           # same rank: only drops the cached spectrum
+            fresh = compute_oracle(eng, 6)            # the resident matrix, factored again
+            assert np.array_equal(cached.singular_values, fresh.singular_values)
+            assert np.array_equal(cached.basis, fresh.basis)
+            assert cached.frob_opt == fresh.frob_opt
+            if phase == 2:
+                break
+            # an event invalidates: the next observation factors the new matrix
+            eng.rank_one_update(3, 4, 0.5)
+            after = compute_oracle(eng, 6)
+            fresh = compute_oracle(eng.tracked, 6)
+            assert np.array_equal(after.singular_values, fresh.singular_values)
+            assert not np.array_equal(after.singular_values, cached.singular_values)
+        # a different width is not served from the cache
+        eng.refresh()
+        assert compute_oracle(eng, 3).basis.shape == (eng.shape[0], 3)
+        np.testing.assert_array_equal(compute_oracle(eng, 3).singular_values,
+                                      compute_oracle(eng.tracked, 3).singular_values)
+
     def test_error_ratio(self):
         assert error_ratio(2.0, 2.0) == 1.0
         assert math.isnan(error_ratio(0.5, 0.0))
