@@ -175,6 +175,26 @@ static bool all_finite(const double* p, size_t n) { return finite_chunk(p, n); }
 
 using namespace isvd;
 
+// Leading triplets and spectrum of the tracked matrix kept from the last
+// oracle observation (device buffers, owned here): the refresh that the
+// policies fire right after observing the same matrix (stream.py:291-333:
+// observe, decide, refresh) installs them instead of factoring A a second
+// time.  Valid until an event changes the tracked matrix.
+struct OracleKeep {
+  double *U = nullptr, *V = nullptr, *sw = nullptr, *sa = nullptr;
+  int B = 0, m = 0, n = 0, w = 0, ldw = 0, nc = 0;
+  bool valid = false;
+  bool nozero = false;  // every kept sigma > 0 (no zero-sigma completion involved)
+  void drop() {
+    if (U) cudaFree(U);
+    if (V) cudaFree(V);
+    if (sw) cudaFree(sw);
+    if (sa) cudaFree(sa);
+    U = V = sw = sa = nullptr;
+    valid = false;
+  }
+};
+
 struct isvd_engine {
   int B = 0, m = 0, n = 0, r = 0, k = 0;
   // Row sharding (isvd_engine_set_shard): this rank holds global rows
@@ -284,6 +304,7 @@ struct isvd_engine {
   int64_t svdc_cap = 0;
   bool svdc_valid = false;
   int svdc_w = 0;
+  OracleKeep okeep;
   int64_t wx_n = 0, wj_n = 0, wpart_n = 0, wout_n = 0;
   int* wflags = nullptr;
   std::vector<int> hflags;
@@ -705,8 +726,20 @@ struct isvd_engine {
         ISVD_TRY(dalloc(&svdc_sall, (size_t)B * nc));
         svdc_cap = (int64_t)B * nc;
       }
-      ISVD_TRY(dense_svd_run(B, m, n, A, astride(), n_cap, w, Um(), Vm(), s, ld, svdc_sall, nc, wx,
-                             wj, wflags, hflags.data(), st, &sweeps));
+      if (okeep.valid && okeep.nozero && okeep.B == B && okeep.m == m && okeep.n == n &&
+          okeep.nc == nc && w <= okeep.w) {
+        // the matrix just observed: its leading w triplets and spectrum
+        ISVD_TRY(launch_copy_rows(B, m, w, okeep.U, (int64_t)m * okeep.ldw, okeep.ldw, U, ustride(),
+                                  ld, st));
+        ISVD_TRY(launch_copy_rows(B, n, w, okeep.V, (int64_t)n * okeep.ldw, okeep.ldw, V, vstride(),
+                                  ld, st));
+        ISVD_TRY(launch_copy_rows(B, 1, w, okeep.sw, okeep.ldw, okeep.ldw, s, ld, ld, st));
+        ISVD_CUDA(cudaMemcpyAsync(svdc_sall, okeep.sa, sizeof(double) * B * nc,
+                                  cudaMemcpyDeviceToDevice, st));
+      } else {
+        ISVD_TRY(dense_svd_run(B, m, n, A, astride(), n_cap, w, Um(), Vm(), s, ld, svdc_sall, nc, wx,
+                               wj, wflags, hflags.data(), st, &sweeps));
+      }
       svdc_w = w;
     }
     r = w;
@@ -721,6 +754,7 @@ struct isvd_engine {
 
   ~isvd_engine() {
     dfree(svdc_sall);
+    okeep.drop();
     dfree(U); dfree(V); dfree(s); dfree(A); dfree(N);
     dfree(core); dfree(uk); dfree(vk); dfree(sv); dfree(vscr);
     dfree(z); dfree(inj); dfree(rho); dfree(xnorm); dfree(ev);
@@ -909,6 +943,7 @@ int isvd_engine_init(isvd_engine* e, const double* a0, int on_device) {
   if (e) e->join();
   if (!e || !a0) { set_error("null argument"); return ISVD_EINVAL; }
   e->svdc_valid = false;
+  e->okeep.valid = false;
   const size_t cnt = (size_t)e->B * e->m * e->n;
   if (!on_device) {
     if (!all_finite(a0, cnt)) { set_error("initial matrix contains non-finite entries"); return ISVD_EINVAL; }
@@ -1289,6 +1324,7 @@ static int append_common(isvd_engine* e, const double* x, int on_device, bool is
   if (!e || !x) { set_error("null argument"); return ISVD_EINVAL; }
   if (!e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
   e->svdc_valid = false;
+  e->okeep.valid = false;
   const int len = is_row ? e->n : e->m;
   // Finiteness of a host payload (the reference's as_vector, linalg.py:31-40)
   // is checked before anything changes the engine's logical state: small
@@ -1455,6 +1491,7 @@ int isvd_engine_rank_one(isvd_engine* e, const int64_t* i, const int64_t* j, con
   if (!e || !i || !j || !delta) { set_error("null argument"); return ISVD_EINVAL; }
   if (!e->initialized) { set_error("engine not initialised"); return ISVD_ESTATE; }
   e->svdc_valid = false;
+  e->okeep.valid = false;
   const int64_t *di = i, *dj = j;
   const double* dd = delta;
   int rslot = 0;
@@ -1775,6 +1812,7 @@ int isvd_engine_device_views(isvd_engine* e, double** u, int64_t* u_stride, int*
   if (!e) { set_error("null engine"); return ISVD_EINVAL; }
   ISVD_TRY(e->flush());
   e->svdc_valid = false;  // the caller may write through the views
+  e->okeep.valid = false;
   if (u) *u = e->U;
   if (u_stride) *u_stride = e->ustride();
   if (ldu) *ldu = e->ld;
@@ -1833,6 +1871,7 @@ int isvd_engine_restore(isvd_engine* e) {
   if (e) e->join();
   if (!e || !e->snap.valid) { set_error("no snapshot to restore"); return ISVD_ESTATE; }
   e->svdc_valid = false;
+  e->okeep.valid = false;
   auto& S = e->snap;
   if (S.m_cap != e->m_cap || S.n_cap != e->n_cap || S.ld != e->ld) {
     set_error("capacities changed since the snapshot");
@@ -2164,7 +2203,7 @@ int isvd_engine_angle(isvd_engine* e, int which, const double* q, int q_cols, in
 
 static int oracle_common(int B, int m, int n, const double* a_dev, int64_t a_stride, int lda,
                          int w_keep, double* s_host, double* u_host, double* vt_host,
-                         cudaStream_t st) {
+                         cudaStream_t st, OracleKeep* keep = nullptr) {
   const int w = std::max(0, std::min(w_keep, std::min(m, n)));
   DenseSvdPlan P = dense_svd_plan(m, n, w);
   const int nc = P.nc;
@@ -2212,6 +2251,15 @@ static int oracle_common(int B, int m, int n, const double* a_dev, int64_t a_str
     if (cudaStreamSynchronize(st) != cudaSuccess) T(ISVD_ENODEV);
   }
   cudaError_t last = cudaStreamSynchronize(st);
+  if (keep) {
+    keep->drop();
+    if (rc == ISVD_OK && w > 0) {
+      keep->U = U; keep->V = V; keep->sw = sw; keep->sa = sa;
+      keep->B = B; keep->m = m; keep->n = n; keep->w = w; keep->ldw = ldw; keep->nc = nc;
+      keep->valid = true;
+      U = V = sw = sa = nullptr;
+    }
+  }
   dfree(x); dfree(jac); dfree(U); dfree(V); dfree(sa); dfree(sw); dfree(fl);
   if (rc == ISVD_ENODEV && g_err.empty())
     set_error(std::string("oracle: device failure: ") + cudaGetErrorString(last));
@@ -2254,7 +2302,20 @@ int isvd_engine_oracle(isvd_engine* e, int w_keep, double* s, double* u) {
     ISVD_CUDA(cudaStreamSynchronize(e->st));
     return ISVD_OK;
   }
-  return oracle_common(e->B, e->m, e->n, e->A, e->astride(), e->n_cap, w_keep, s, u, nullptr, e->st);
+  std::vector<double> s_tmp;
+  double* s_out = s;
+  if (!s_out) {
+    s_tmp.resize((size_t)e->B * nc);
+    s_out = s_tmp.data();
+  }
+  ISVD_TRY(oracle_common(e->B, e->m, e->n, e->A, e->astride(), e->n_cap, w_keep, s_out, u, nullptr,
+                         e->st, &e->okeep));
+  if (e->okeep.valid) {
+    bool nz = true;
+    for (int b = 0; b < e->B; ++b) nz = nz && s_out[(size_t)b * nc + e->okeep.w - 1] > 0.0;
+    e->okeep.nozero = nz;
+  }
+  return ISVD_OK;
 }
 
 // ------------------------------------------- functional metrics (host bases)

@@ -154,6 +154,56 @@ class TestMetrics:
         np.testing.assert_array_equal(compute_oracle(eng, 3).singular_values,
                                       compute_oracle(eng.tracked, 3).singular_values)
 
+    def test_refresh_after_oracle_reuses_the_observed_svd(self):
+        """The policies observe (oracle) and then refresh the same tracked
+        matrix (stream.py:291-333); the refresh installs the observed leading
+        triplets instead of factoring A again (engine.cu: OracleKeep).  Same
+        factors as a refresh without the observation, also at a smaller armed
+        rank, and an event in between drops the kept factorisation."""
+        rng = np.random.default_rng(11)
+        a0 = rng.standard_normal((80, 12)) @ rng.standard_normal((12, 30)) + 0.02 * rng.standard_normal((80, 30))
+        rows = [rng.standard_normal(30) for _ in range(6)]
+
+        def fresh(k_new, extra=False):
+            e = SvdEngine(a0, k=8)
+            for r in rows:
+                e.row_append(r)
+            if extra:
+                e.rank_one_update(5, 7, 0.3)
+            e.set_rank(k_new)
+            e.refresh()
+            return e.factors
+
+        for k_new in (8, 5):
+            e = SvdEngine(a0, k=8)
+            for r in rows:
+                e.row_append(r)
+            o = compute_oracle(e, 8)
+            e.set_rank(k_new)       # the armed rank of the adaptive policy
+            e.refresh()
+            f, g = e.factors, fresh(k_new)
+            np.testing.assert_allclose(f.s, g.s, rtol=1e-13)
+            np.testing.assert_allclose(f.u, g.u, atol=1e-11)
+            np.testing.assert_allclose(f.vt, g.vt, atol=1e-11)
+            np.testing.assert_allclose(f.s, o.singular_values[:k_new], rtol=1e-13)
+            assert abs(frob_error(e) - math.sqrt(float(np.sum(o.singular_values[k_new:] ** 2)))) <= 1e-9
+        e = SvdEngine(a0, k=8)
+        for r in rows:
+            e.row_append(r)
+        compute_oracle(e, 8)
+        e.rank_one_update(5, 7, 0.3)   # the tracked matrix changed: factor again
+        e.refresh()
+        g = fresh(8, extra=True)
+        np.testing.assert_allclose(e.factors.s, g.s, rtol=1e-13)
+        np.testing.assert_allclose(e.factors.u, g.u, atol=1e-11)
+        # a larger rank than observed is factored again
+        e = SvdEngine(a0, k=4)
+        compute_oracle(e, 4)
+        e.set_rank(7)
+        e.refresh()
+        assert e.factors.s.shape == (7,)
+        np.testing.assert_allclose(e.factors.s, np.linalg.svd(a0, compute_uv=False)[:7], rtol=1e-10)
+
     def test_error_ratio(self):
         assert error_ratio(2.0, 2.0) == 1.0
         assert math.isnan(error_ratio(0.5, 0.0))
