@@ -818,6 +818,162 @@ __global__ void __launch_bounds__(256) proj_cluster_kernel(
   cl.sync();  // no CTA leaves while its partials may still be read
 }
 
+// proj_cluster_kernel for slices of at most 64 rows per CTA (config 5b's V:
+// 1024 x 128 over 16 CTAs): each warp loads its eight rows of F once, all
+// loads in flight together, and keeps them in registers for both passes
+// (the general kernel walks the slice twice with dependent row-by-row loads:
+// 4 + 8 load latencies per warp); the eight residual entries of a warp come
+// out of one transposing butterfly.  Same contract, same fixed summation
+// orders across the cluster.
+template <int RT>
+__global__ void __launch_bounds__(256) proj_cluster_reg_kernel(
+    int rows, int r, Mat F, const double* __restrict__ x, int64_t x_stride,
+    const double* __restrict__ s, int lds, double tol, double* __restrict__ core,
+    int64_t core_stride, int ldcore, double* __restrict__ z, int64_t z_stride,
+    double* __restrict__ inj_scale, double* __restrict__ rho_out, double* __restrict__ xnorm_out,
+    double* __restrict__ A, int64_t a_stride, int64_t a_off, int64_t a_step,
+    double* __restrict__ N, int arrow_only) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  griddep_launch_dependents();
+  griddep_wait();
+  __shared__ double pw[8][kRMax];
+  __shared__ double ppart[kRMax + 1];  // this CTA's partial F^T x (and ||x||^2 at [r])
+  __shared__ double p[kRMax];
+  __shared__ double xw[8], zw[8];
+  __shared__ double zpart, xn2;
+  const int crank = (int)cl.block_rank();
+  const int b = blockIdx.x / kProjCluster;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rps = (rows + kProjCluster - 1) / kProjCluster;  // <= 64 (launcher)
+  const int c0 = min(rows, crank * rps), c1 = min(rows, c0 + rps);
+  const double* Fb = F.p + b * F.stride;
+  const double* xb = x + b * x_stride;
+  const int row0 = c0 + warp * 8;
+  // ---- this warp's eight rows of F and their x entries, all loads in flight
+  double f[8][RT], xr[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int row = row0 + i;
+    const bool ok = row < c1;
+    const double* fr = Fb + (int64_t)row * F.ld + lane;
+#pragma unroll
+    for (int t = 0; t < RT; ++t) f[i][t] = (ok && lane + 32 * t < r) ? fr[32 * t] : 0.0;
+    xr[i] = ok ? xb[row] : 0.0;
+  }
+  // lane i < 8 owns row i of the warp: tracked-matrix entry and ||x||^2
+  double xl = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (lane == i) xl = xr[i];
+  if (A && lane < 8 && row0 + lane < c1)
+    A[b * a_stride + a_off + (int64_t)(row0 + lane) * a_step] = xl;
+  {
+    const double xx = warp_sum(xl * xl);
+    if (lane == 0) xw[warp] = xx;
+  }
+  // ---- pass 1: partial p over the warp's rows, then the CTA, then the cluster
+#pragma unroll
+  for (int t = 0; t < RT; ++t) {
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) {
+      a0 = fma(f[i][t], xr[i], a0);
+      a1 = fma(f[i + 1][t], xr[i + 1], a1);
+    }
+    const int l = lane + 32 * t;
+    if (l < r) pw[warp][l] = a0 + a1;
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < r) {
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) v += pw[w][threadIdx.x];
+    ppart[threadIdx.x] = v;
+  } else if ((int)threadIdx.x == r) {
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) v += xw[w];
+    ppart[r] = v;
+  }
+  cl.sync();
+  if ((int)threadIdx.x <= r) {
+    const int l = threadIdx.x;
+    double v = 0.0;
+#pragma unroll
+    for (int k = 0; k < kProjCluster; ++k) v += cl.map_shared_rank(ppart, k)[l];
+    if (l < r) p[l] = v; else xn2 = v;
+  }
+  __syncthreads();
+  const double xnorm2 = xn2;
+  // ---- pass 2 from the registers: z = x - F p on the warp's rows
+  double zz = 0.0;
+  {
+    double pt[RT];
+#pragma unroll
+    for (int t = 0; t < RT; ++t) pt[t] = lane + 32 * t < r ? p[lane + 32 * t] : 0.0;
+    double v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      double a0 = 0.0;
+#pragma unroll
+      for (int t = 0; t < RT; ++t) a0 = fma(f[i][t], pt[t], a0);
+      v[i] = a0;
+    }
+    const double fp = warp_sum8(v);
+    const int slot = warp_sum8_slot(lane);
+    const double xs = __shfl_sync(0xffffffffu, xl, slot);
+    const int row = row0 + slot;
+    if ((lane & 3) == 0 && row < c1) {
+      const double zc = xs - fp;
+      z[b * z_stride + row] = zc;
+      zz = zc * zc;
+    }
+  }
+  zz = warp_sum(zz);
+  if (lane == 0) zw[warp] = zz;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) v += zw[w];
+    zpart = v;
+  }
+  cl.sync();
+  double zsum = 0.0;
+#pragma unroll
+  for (int k = 0; k < kProjCluster; ++k) zsum += *cl.map_shared_rank(&zpart, k);
+  const double rho = sqrt(zsum);
+  const bool fresh = rho > tol;
+  const int P = r + 1;
+  double* Kb = core + b * core_stride;
+  const double* sb = s + (int64_t)b * lds;
+  if (arrow_only) {
+    for (int j = crank * blockDim.x + threadIdx.x; j < P; j += kProjCluster * blockDim.x) {
+      if (j < r) Kb[j * ldcore + j] = sb[j];
+      Kb[r * ldcore + j] = (j < r) ? p[j] : (fresh ? rho : 0.0);
+    }
+  } else {
+    for (int i = crank; i < P; i += kProjCluster)
+      for (int j = threadIdx.x; j < P; j += blockDim.x) {
+        double v = 0.0;
+        if (i < r) {
+          if (i == j) v = sb[i];
+        } else {
+          v = (j < r) ? p[j] : (fresh ? rho : 0.0);
+        }
+        Kb[i * ldcore + j] = v;
+      }
+  }
+  if (crank == 0 && threadIdx.x == 0) {
+    inj_scale[b] = fresh ? 1.0 / rho : 0.0;
+    rho_out[b] = rho;
+    xnorm_out[b] = sqrt(xnorm2);
+    N[b] += xnorm2;
+  }
+  cl.sync();  // no CTA leaves while its partials may still be read
+}
+
 // out[l] = sum_t part[t * cnt + l], fixed order (row-sharded reductions, B = 1)
 __global__ void split_reduce_kernel(int cnt, int np, const double* __restrict__ part,
                                     double* __restrict__ out) {
@@ -1830,6 +1986,19 @@ int launch_project_append(int batch, int rows, int r, Mat F, const double* x, in
                                        cudaFuncAttributeNonPortableClusterSizeAllowed, 1));    \
         attr = true;                                                                           \
       }                                                                                        \
+    }                                                                                          \
+    if (K <= 4 && rows <= 64 * kProjCluster) {                                                 \
+      static bool attr2 = false;                                                               \
+      if (!attr2) {                                                                            \
+        ISVD_CUDA(cudaFuncSetAttribute(proj_cluster_reg_kernel<(K <= 4 ? K : 4)>,              \
+                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1));    \
+        attr2 = true;                                                                          \
+      }                                                                                        \
+      e = cudaLaunchKernelEx(&cfg, proj_cluster_reg_kernel<(K <= 4 ? K : 4)>, rows, r, F, x,   \
+                             x_stride, s, lds, tol, core, core_stride, ldcore, z, z_stride,    \
+                             inj_scale, rho_out, xnorm_out, A, a_stride, a_off, a_step, N,     \
+                             arrow_only);                                                      \
+      break;                                                                                   \
     }                                                                                          \
     e = cudaLaunchKernelEx(&cfg, proj_cluster_kernel<K>, rows, r, F, x, x_stride, s, lds, tol, \
                            core, core_stride, ldcore, z, z_stride, inj_scale, rho_out,         \
