@@ -42,6 +42,12 @@ namespace {
 
 constexpr int kN = kCoreMaxS;  // max core size
 constexpr int kArrowCluster = 8;      // CTAs per wide core when the batch is small
+// A core of more than 128 roots on very few streams (config 5b: one 129 core
+// per tick): 16 CTAs x 16 warps give every root / Loewner product / vector
+// its own warp in ONE round -- with 8 CTAs the 129th item made one warp run a
+// second round, which was half of each phase (tools/trace_5b.py).
+constexpr int kArrowClusterWide = 16;  // non-portable cluster size
+constexpr int kClusterWideMaxBatch = 4;
 constexpr int kClusterMaxBatch = 32;  // up to 256 CTAs
 __device__ unsigned long long g_arrow_counters[4];
 
@@ -148,6 +154,17 @@ __device__ __forceinline__ void apply_rots(double* col, int64_t stride, const SM
 // vectors are split over the CL * 16 warps, each result is stored into
 // every CTA's shared memory over DSMEM, and cluster barriers separate the
 // phases.  At B = 1 this spreads the 129-root core over CL SMs.
+// phase marks of the wide (cluster) solver in trace builds: rank-0 CTA, thread 0
+#ifdef ISVD_R1_TRACE
+#define AB_MARK(k)                                                                     \
+  do {                                                                                 \
+    if (WIDE && crank == 0 && threadIdx.x == 0 && b < 4096) g_r1_trace[b][k] = clock64(); \
+  } while (0)
+#else
+#define AB_MARK(k) \
+  do {             \
+  } while (0)
+#endif
 template <int kN, bool WIDE, int CL>
 __device__ __forceinline__ void arrow_body(int b, int n, const double* __restrict__ core,
                                            int64_t core_stride, int ldcore,
@@ -180,6 +197,7 @@ __device__ __forceinline__ void arrow_body(int b, int n, const double* __restric
     if (SO && pc < nkeep) SO[pc] = v;
   };
   const double eps = 2.220446049250313e-16;
+  AB_MARK(0);
 
   // ---- load, scale (max over the block: warp maxima, then one smem pass)
   __shared__ double wmax[16];
@@ -206,15 +224,26 @@ __device__ __forceinline__ void arrow_body(int b, int n, const double* __restric
   }
   __syncthreads();
   // ascending order of poles; ties: higher column first (the rho column r
-  // leads the zero group)
-  for (int c = tid; c < n; c += blockDim.x) {
-    double dc = S.delta[c];
-    int rank = 0;
-    for (int e = 0; e < n; ++e) {
-      double de = S.delta[e];
-      rank += (de < dc) || (de == dc && e > c);
+  // leads the zero group).  The poles are the installed singular values:
+  // normally strictly descending and positive, so the order is r, r - 1,
+  // ..., 0 (one parallel check instead of the O(n^2) rank pass).
+  {
+    bool unsorted = false;
+    for (int c = tid; c < r; c += blockDim.x)
+      unsorted |= !(S.delta[c] > (c + 1 < r ? S.delta[c + 1] : 0.0));
+    if (!__syncthreads_or(unsorted)) {
+      for (int p = tid; p < n; p += blockDim.x) S.order[p] = r - p;
+    } else {
+      for (int c = tid; c < n; c += blockDim.x) {
+        double dc = S.delta[c];
+        int rank = 0;
+        for (int e = 0; e < n; ++e) {
+          double de = S.delta[e];
+          rank += (de < dc) || (de == dc && e > c);
+        }
+        S.order[rank] = c;
+      }
     }
-    S.order[rank] = c;
   }
   __syncthreads();
 
@@ -314,7 +343,9 @@ __device__ __forceinline__ void arrow_body(int b, int n, const double* __restric
     S.ndefl = nd;
     S.nrot = nr;
   }
+  AB_MARK(1);
   csync();  // CL > 1: also guarantees every CTA of the cluster is resident before DSMEM use
+  AB_MARK(2);
   const int N = S.nkept, ND = S.ndefl;
 
   // ---- roots: thread (WIDE: warp) i solves for sigma_i in (kd[i], kd[i+1]).
@@ -478,7 +509,9 @@ __device__ __forceinline__ void arrow_body(int b, int n, const double* __restric
   }
   // deflated singular values (unscaled positions 0..ND-1)
   for (int k = tid; k < ND; k += blockDim.x) S.sig[k] = S.dzero[k] ? 0.0 : S.delta[S.dcol[k]];
+  AB_MARK(3);
   csync();
+  AB_MARK(4);
 
   // ---- Loewner: zhat_j^2 = prod_k (sigma_k^2 - d_j^2) / prod_{k != j} (d_k^2 - d_j^2)
   if (WIDE) {
@@ -511,15 +544,26 @@ __device__ __forceinline__ void arrow_body(int b, int n, const double* __restric
     for (int k = j; k < N - 1; ++k) acc *= sdiff(k) * frcp((S.kd[k + 1] - dj) * (S.kd[k + 1] + dj));
     S.zhat[j] = copysign(sqrt(fmax(acc, 0.0)), S.kz[j]);
   }
-  // ---- sorted output positions: descending sigma, ties by triple index
-  for (int t = tid; t < n; t += blockDim.x) {
-    const double st = S.sig[t];
-    int rank = 0;
-    for (int e = 0; e < n; ++e) {
-      const double se = S.sig[e];
-      rank += (se > st) || (se == st && e < t);
+  // ---- sorted output positions: descending sigma, ties by triple index.
+  // Without deflation the interlacing kd_i < sigma_i < kd_{i+1} makes the
+  // roots strictly ascending: position n - 1 - t unless rounding broke the
+  // order (then, or with deflated values in front, the rank pass).
+  {
+    bool unsorted = false;
+    for (int t = tid; t + 1 < n; t += blockDim.x) unsorted |= !(S.sig[t] < S.sig[t + 1]);
+    if (!__syncthreads_or(unsorted)) {
+      for (int t = tid; t < n; t += blockDim.x) S.pos[t] = n - 1 - t;
+    } else {
+      for (int t = tid; t < n; t += blockDim.x) {
+        const double st = S.sig[t];
+        int rank = 0;
+        for (int e = 0; e < n; ++e) {
+          const double se = S.sig[e];
+          rank += (se > st) || (se == st && e < t);
+        }
+        S.pos[t] = rank;
+      }
     }
-    S.pos[t] = rank;
   }
   // largest singular value: block max (the previous sync made sig visible)
   {
@@ -528,7 +572,9 @@ __device__ __forceinline__ void arrow_body(int b, int n, const double* __restric
     m1 = warp_max(m1);
     if ((tid & 31) == 0) wmax[tid >> 5] = m1;
   }
+  AB_MARK(5);
   csync();
+  AB_MARK(6);
   double smax = 0.0;
   for (int w = 0; w < (int)(blockDim.x >> 5); ++w) smax = fmax(smax, wmax[w]);
 
@@ -636,7 +682,9 @@ __device__ __forceinline__ void arrow_body(int b, int n, const double* __restric
     }
     put_sv(pc, dead ? 0.0 : sg * scale);
   }
+  AB_MARK(7);
   csync();  // every column of U / V / SV written (global, cluster scope)
+  AB_MARK(8);
   if (crank != 0) return;
 
   // ---- dead-column completion over e_0, e_1, ... (_kernels.pyx:62-79)
@@ -1191,13 +1239,15 @@ int launch_arrow_svd(int batch, int s, const double* core, int64_t core_stride, 
   } else if (batch <= kClusterMaxBatch) {
     // few wide cores (config 5b: one 129 core per tick): a cluster per core
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(batch * kArrowCluster);
+    const bool wide16 = s > 128 && batch <= kClusterWideMaxBatch;
+    const int clsz = wide16 ? kArrowClusterWide : kArrowCluster;
+    cfg.gridDim = dim3(batch * clsz);
     cfg.blockDim = dim3(512);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = st;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = kArrowCluster;
+    at[0].val.clusterDim.x = clsz;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1205,6 +1255,22 @@ int launch_arrow_svd(int batch, int s, const double* core, int64_t core_stride, 
     cfg.attrs = at;
     cfg.numAttrs = 2;
     cudaError_t e;
+    if (wide16) {
+      static bool attr16 = false;
+      if (!attr16) {
+        ISVD_CUDA(cudaFuncSetAttribute(arrow_svd_kernel<136, true, kArrowClusterWide>,
+                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        ISVD_CUDA(cudaFuncSetAttribute(arrow_svd_kernel<kN, true, kArrowClusterWide>,
+                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        attr16 = true;
+      }
+      if (s <= 136)
+        e = cudaLaunchKernelEx(&cfg, arrow_svd_kernel<136, true, kArrowClusterWide>, s, core,
+                               core_stride, ldcore, uk, vk, out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate, ArrowFuse{});
+      else
+        e = cudaLaunchKernelEx(&cfg, arrow_svd_kernel<kN, true, kArrowClusterWide>, s, core,
+                               core_stride, ldcore, uk, vk, out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate, ArrowFuse{});
+    } else
     if (s <= 72)
       e = cudaLaunchKernelEx(&cfg, arrow_svd_kernel<72, true, kArrowCluster>, s, core, core_stride,
                              ldcore, uk, vk, out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate, ArrowFuse{});
