@@ -1286,6 +1286,7 @@ __global__ void __launch_bounds__(kRotWarps * 32, 1)
   griddep_launch_dependents();
   griddep_wait();
   if (gate && *gate) return;
+  K1_MARK(0);
   extern __shared__ __align__(16) double smem[];
   constexpr int kMaxTiles = 3;  // n-tiles per warp (NP <= 192)
   constexpr int kP = 132;       // row pitch of the staged core: conflict-free B-fragment reads
@@ -1305,12 +1306,12 @@ __global__ void __launch_bounds__(kRotWarps * 32, 1)
     fence_barrier_init();
   }
   __syncthreads();
+  // (row w + 8 i by lane i of warp w: a warp serialises its lanes' copy
+  // issues, so one warp issuing all r + 1 of them held the CTA for 8 K cycles)
   const uint32_t row_bytes = (uint32_t)NP * 8u;
-  if (warp == 0) {
-    if (lane == 0) mbar_expect_tx(&bar, row_bytes * (uint32_t)(r + 1));
-    __syncwarp();
-    for (int l = lane; l <= r; l += 32) bulk_g2s(Qs + l * kP, Q + (int64_t)l * J.ldq, row_bytes, &bar);
-  }
+  if (threadIdx.x == 0) mbar_expect_tx(&bar, row_bytes * (uint32_t)(r + 1));
+  for (int l = warp + kRotWarps * lane; l <= r; l += kRotWarps * 32)
+    bulk_g2s(Qs + l * kP, Q + (int64_t)l * J.ldq, row_bytes, &bar);
   double* X = J.X.p + b * J.X.stride;
   const int ld = J.X.ld;
   const double zscale = J.z ? J.inj_scale[b] : 0.0;
@@ -1335,53 +1336,75 @@ __global__ void __launch_bounds__(kRotWarps * 32, 1)
   if (zf.counter)
     for (int t = threadIdx.x; t < zf.w; t += blockDim.x) zf_need |= zf.s[(int64_t)b * zf.lds + t] == 0.0;
   zf_need = __syncthreads_or(zf_need);
-  double a[KP / 4];
-  if (row_begin < row_end) load(row_begin, a);
+  K1_MARK(1);
+  // Two 8-row groups per pass and the k range split over two accumulator
+  // sets: 2 groups x 2 tiles x 2 = 8 independent DMMA chains per warp (a
+  // dependent DMMA issues only every ~200 cycles: with one group and two
+  // chains per warp a group took 6.7 K cycles, tools/trace_rot5b.py), and
+  // each B fragment feeds both groups.
+  double a0[KP / 4], a1[KP / 4];
+  if (row_begin < row_end) {
+    load(row_begin, a0);
+    load(row_begin + 8, a1);
+  }
+  K1_MARK(2);
   mbar_wait(&bar, 0);
+  K1_MARK(3);
   if (J.new_row && blk == 0) {
     double* nr = X + (int64_t)J.rows * ld;
     for (int c = threadIdx.x; c < ld; c += blockDim.x)
       nr[c] = (has_last && c < keep && c < NP) ? Qs[r * kP + c] : 0.0;
   }
-  for (int row0 = row_begin; row0 < row_end; row0 += 8) {
-    double an[KP / 4];
-    const bool more = row0 + 8 < row_end;
-    if (more) load(row0 + 8, an);
-    const int row = row0 + g;
-    const double zr = (zb && row < row_end) ? zb[row] * zscale : 0.0;
-    double d[kMaxTiles][2];
+  for (int row0 = row_begin; row0 < row_end; row0 += 16) {
+    if (row0 != row_begin) {
+      load(row0, a0);
+      load(row0 + 8, a1);
+    }
+    const int rowA = row0 + g, rowB = row0 + 8 + g;
+    const double zrA = (zb && rowA < row_end) ? zb[rowA] * zscale : 0.0;
+    const double zrB = (zb && rowB < row_end) ? zb[rowB] * zscale : 0.0;
+    double d[2][kMaxTiles][2][2];
 #pragma unroll
-    for (int j = 0; j < kMaxTiles; ++j) d[j][0] = d[j][1] = 0.0;
+    for (int gi = 0; gi < 2; ++gi)
 #pragma unroll
-    for (int kk = 0; kk < KP / 4; ++kk) {
-      const int k = 4 * kk + q;
+      for (int j = 0; j < kMaxTiles; ++j)
 #pragma unroll
-      for (int j = 0; j < kMaxTiles; ++j) {
-        const int c = (n_lo + j) * 8 + g;
-        if (j < per && n_lo + j < NT) {
-          const double bv = (k < r && c < keep) ? Qs[k * kP + c] : 0.0;
-          dmma_8x8x4(d[j][0], d[j][1], a[kk], bv);
+        for (int par = 0; par < 2; ++par) d[gi][j][par][0] = d[gi][j][par][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < KP / 4; kk += 2) {
+#pragma unroll
+      for (int par = 0; par < 2; ++par) {
+        const int kq = kk + par;
+        const int kx = 4 * kq + q;
+#pragma unroll
+        for (int j = 0; j < kMaxTiles; ++j) {
+          const int c = (n_lo + j) * 8 + g;
+          if (j < per && n_lo + j < NT) {
+            const double bv = (kx < r && c < keep) ? Qs[kx * kP + c] : 0.0;
+            dmma_8x8x4(d[0][j][par][0], d[0][j][par][1], a0[kq], bv);
+            dmma_8x8x4(d[1][j][par][0], d[1][j][par][1], a1[kq], bv);
+          }
         }
       }
     }
-    __syncthreads();  // every warp's DMMAs have consumed this group's rows
+    __syncthreads();  // every warp's DMMAs have consumed these rows
 #pragma unroll
     for (int j = 0; j < kMaxTiles; ++j) {
       if (j >= per || n_lo + j >= NT) break;
       const int c0 = (n_lo + j) * 8 + 2 * q;
-      double d0 = d[j][0], d1 = d[j][1];
-      if (zb) {
-        d0 = fma(zr, c0 < keep ? Qs[r * kP + c0] : 0.0, d0);
-        d1 = fma(zr, c0 + 1 < keep ? Qs[r * kP + c0 + 1] : 0.0, d1);
-      }
-      if (row < row_end)
-        *reinterpret_cast<double2*>(X + (int64_t)row * ld + c0) = make_double2(d0, d1);
-    }
-    if (more) {
-#pragma unroll
-      for (int kk = 0; kk < KP / 4; ++kk) a[kk] = an[kk];
+      const double q0 = (zb && c0 < keep) ? Qs[r * kP + c0] : 0.0;
+      const double q1 = (zb && c0 + 1 < keep) ? Qs[r * kP + c0 + 1] : 0.0;
+      if (rowA < row_end)
+        *reinterpret_cast<double2*>(X + (int64_t)rowA * ld + c0) =
+            make_double2(fma(zrA, q0, d[0][j][0][0] + d[0][j][1][0]),
+                         fma(zrA, q1, d[0][j][0][1] + d[0][j][1][1]));
+      if (rowB < row_end)
+        *reinterpret_cast<double2*>(X + (int64_t)rowB * ld + c0) =
+            make_double2(fma(zrB, q0, d[1][j][0][0] + d[1][j][1][0]),
+                         fma(zrB, q1, d[1][j][0][1] + d[1][j][1][1]));
     }
   }
+  K1_MARK(4);
   if (zf_need) {
     // last CTA of this stream: every row of both sides is written
     __shared__ int last;
