@@ -197,6 +197,7 @@ __device__ __forceinline__ void arrow_body(int b, int n, const double* __restric
     if (SO && pc < nkeep) SO[pc] = v;
   };
   const double eps = 2.220446049250313e-16;
+  constexpr int kPL = (kN + 31) / 32;  // poles per lane when a warp shares one root / vector
   AB_MARK(0);
 
   // ---- load, scale (max over the block: warp maxima, then one smem pass)
@@ -382,16 +383,23 @@ __device__ __forceinline__ void arrow_body(int b, int n, const double* __restric
       for (int it = 0; it < 80; ++it) {
         ++iters;
         double psi = 0.0, dpsi = 0.0, phi = 0.0, dphi = 0.0;
-        for (int j = lane; j < N; j += 32) {
-          const double dj = S.kd[j];
-          const double t = frcp((dj - dorg) * (dj + dorg) - x);
-          const double w = S.kz[j] * S.kz[j] * t;
-          const bool below = __double2hiint(w) < 0;
-          const double wl = below ? w : 0.0, wu = below ? 0.0 : w;
-          psi += wl;
-          dpsi = fma(wl, t, dpsi);
-          phi += wu;
-          dphi = fma(wu, t, dphi);
+        // a lane's poles fully unrolled (at most kPL): their reciprocal
+        // chains are independent and a dependent FP64 instruction issues
+        // only every ~40 cycles, so the rolled loop ran them back to back
+#pragma unroll
+        for (int ip = 0; ip < kPL; ++ip) {
+          const int j = lane + 32 * ip;
+          if (j < N) {
+            const double dj = S.kd[j];
+            const double t = frcp((dj - dorg) * (dj + dorg) - x);
+            const double w = S.kz[j] * S.kz[j] * t;
+            const bool below = __double2hiint(w) < 0;
+            const double wl = below ? w : 0.0, wu = below ? 0.0 : w;
+            psi += wl;
+            dpsi = fma(wl, t, dpsi);
+            phi += wu;
+            dphi = fma(wu, t, dphi);
+          }
         }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
@@ -523,9 +531,13 @@ __device__ __forceinline__ void arrow_body(int b, int n, const double* __restric
         return S.mu[k] - (dj - dk) * (dj + dk);
       };
       double acc = 1.0;
-      for (int k = lane; k < N - 1; k += 32) {
-        const double dk = k < j ? S.kd[k] : S.kd[k + 1];
-        acc *= sdiff(k) * frcp((dk - dj) * (dk + dj));
+#pragma unroll
+      for (int ip = 0; ip < kPL; ++ip) {  // independent quotients, then the lane's product
+        const int k = lane + 32 * ip;
+        if (k < N - 1) {
+          const double dk = k < j ? S.kd[k] : S.kd[k + 1];
+          acc *= sdiff(k) * frcp((dk - dj) * (dk + dj));
+        }
       }
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) acc *= __shfl_xor_sync(0xffffffffu, acc, off);
@@ -586,9 +598,17 @@ __device__ __forceinline__ void arrow_body(int b, int n, const double* __restric
       const double dorg = S.kd[S.org[t]];
       const double mu = S.mu[t];
       double nv = 0.0, nu = 0.0;
-      for (int j = lane; j < N; j += 32) {
-        const double dj = S.kd[j];
-        const double vj = S.zhat[j] * frcp((dj - dorg) * (dj + dorg) - mu);
+      double vjs[kPL], djs[kPL];  // the lane's entries, kept for the write pass
+#pragma unroll
+      for (int ip = 0; ip < kPL; ++ip) {
+        const int j = lane + 32 * ip;
+        double vj = 0.0, dj = 0.0;
+        if (j < N) {
+          dj = S.kd[j];
+          vj = S.zhat[j] * frcp((dj - dorg) * (dj + dorg) - mu);
+        }
+        vjs[ip] = vj;
+        djs[ip] = dj;
         nv = fma(vj, vj, nv);
         nu = fma(dj * vj, dj * vj, nu);
       }
@@ -597,12 +617,14 @@ __device__ __forceinline__ void arrow_body(int b, int n, const double* __restric
       const double iv = rsqrt(nv), iu = rsqrt(nu);
       const double sg = S.sig[t];
       const bool dead = !(sg > 0.0) || sg < kZeroSvRtol * smax;
-      for (int j = lane; j < N; j += 32) {
-        const double dj = S.kd[j];
-        const double vj = S.zhat[j] * frcp((dj - dorg) * (dj + dorg) - mu);
-        const int row = S.kcol[j];
-        V[row * ldo + pc] = vj * iv;
-        if (row != r) U[row * ldo + pc] = dead ? 0.0 : dj * vj * iu;
+#pragma unroll
+      for (int ip = 0; ip < kPL; ++ip) {
+        const int j = lane + 32 * ip;
+        if (j < N) {
+          const int row = S.kcol[j];
+          V[row * ldo + pc] = vjs[ip] * iv;
+          if (row != r) U[row * ldo + pc] = dead ? 0.0 : djs[ip] * vjs[ip] * iu;
+        }
       }
       if (lane == 0) {
         U[r * ldo + pc] = dead ? 0.0 : -iu;
