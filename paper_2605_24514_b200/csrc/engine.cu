@@ -1669,7 +1669,9 @@ int isvd_engine_has_reference(const isvd_engine* e, int* has_ref, int* ref_m, in
 int isvd_engine_get_factors(isvd_engine* e, int b, double* u, double* sv, double* v) {
   if (e) e->join();
   if (!e || b < 0 || b >= e->B) { set_error("bad stream index"); return ISVD_EINVAL; }
-  ISVD_TRY(e->canonicalize());
+  // the singular values alone need neither the deferred bases materialised
+  // nor the sign convention applied (metrics read them every tick)
+  if (u || v) ISVD_TRY(e->canonicalize());
   const int r = e->r;
   if (r > 0) {
     if (u)

@@ -424,6 +424,25 @@ class SvdEngine:
         return self._scalars()[2]
 
     @property
+    def rank(self) -> int:
+        """Current factor width (no transfer)."""
+        return self._shape_all()[3]
+
+    @property
+    def singular_values(self) -> np.ndarray:
+        """The installed singular values alone: r doubles, no basis download
+        and no materialisation of the deferred bases (the per-tick metrics,
+        metrics.py:86-93 / 122-145, need only these and the rank)."""
+        if "factors" in self._cache:
+            return self._cache["factors"].s
+        if "s" not in self._cache:
+            r = self._shape_all()[3]
+            s = np.empty(r)
+            _lib.check(self._h.lib.isvd_engine_get_factors(self._h.h, 0, None, _lib.dptr(s), None))
+            self._cache["s"] = s
+        return self._cache["s"]
+
+    @property
     def factors(self) -> SvdFactors:
         if "factors" not in self._cache:
             _, m, n, r, _, _ = self._shape_all()

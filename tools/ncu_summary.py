@@ -90,7 +90,8 @@ def rep(path):
 
 
 def main():
-    prof = ROOT / "profiles"
+    import os
+    prof = Path(os.environ.get("ISVD_SUMMARY_OUT", str(ROOT / "profiles")))
     txt = launches()
     if txt:
         (prof / f"{tag}_launches.txt").write_text(txt)
