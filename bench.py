@@ -327,10 +327,12 @@ def _simulate_flops(B, steps, window=32, vwin=8, rank1_steps=2.0):
     following the same data flow as _simulate_bytes:
     * rank-1 tick (rank1_fast_kernel): the core factorisation as the
       simultaneous Jacobi steps run it -- the first step from the structure
-      of K (Gram and rotation O(k^2), Theta^2 2 k^3), each further step the
-      32 x 32 Gram (2 k^3) and G (J - I) (2 k^3) -- plus the fused rotations
-      of the deferred bases: W (rows_W x k) . Uk and G (rows_G x k) . Vk
-      (2 rows k^2 each);
+      of K (Gram and rotation O(k^2); Theta^2 is symmetric: k^3), each
+      further step the symmetric 32 x 32 Gram (k^3) and G (J - I) (2 k^3) --
+      plus the fused rotations of the deferred bases: W (rows_W x k) . Uk and
+      G (rows_G x k) . Vk (2 rows k^2 each).  (Symmetric products are counted
+      once: the model stays at or below what ncu counts as executed tensor
+      flops, profiles/r*_tick_ncu_summary.json r1fast.tensor_fp64_ops.)
     * row tick (arrow): the secular solve is O(k^2) (counted as 40 (k+1)^2)
       plus the fused rotations [W 0; 0 1] . Q and [G 0; 0 1] . Vk (2 rows (k+1) k).
     Returns (rank-1 flops, row flops)."""
@@ -338,7 +340,7 @@ def _simulate_flops(B, steps, window=32, vwin=8, rank1_steps=2.0):
     f_r1 = f_row = 0.0
     b_rows, active = 0, False
     vpend, nz = False, 0
-    core = 2.0 * k ** 3 * (1.0 + 2.0 * max(0.0, rank1_steps - 1.0))
+    core = 1.0 * k ** 3 + 3.0 * k ** 3 * max(0.0, rank1_steps - 1.0)
     for t in range(steps):
         row = t % 2 == 0
         g_rows = (k + nz) if vpend else 0
