@@ -1261,7 +1261,36 @@ int launch_arrow_svd(int batch, int s, const double* core, int64_t core_stride, 
   } else if (batch <= kClusterMaxBatch) {
     // few wide cores (config 5b: one 129 core per tick): a cluster per core
     cudaLaunchConfig_t cfg = {};
-    const bool wide16 = s > 128 && batch <= kClusterWideMaxBatch;
+    bool wide16 = s > 128 && batch <= kClusterWideMaxBatch;
+    if (wide16) {
+      // a 16-CTA cluster of 512-thread CTAs must fit one GPC: checked once,
+      // the portable 8-CTA cluster otherwise
+      static int wide_ok = -1;
+      if (wide_ok < 0) {
+        wide_ok = 0;
+        cudaLaunchConfig_t qc = {};
+        qc.gridDim = dim3(kArrowClusterWide);
+        qc.blockDim = dim3(512);
+        cudaLaunchAttribute qa[1];
+        qa[0].id = cudaLaunchAttributeClusterDimension;
+        qa[0].val.clusterDim.x = kArrowClusterWide;
+        qa[0].val.clusterDim.y = 1;
+        qa[0].val.clusterDim.z = 1;
+        qc.attrs = qa;
+        qc.numAttrs = 1;
+        int nclusters = 0;
+        if (cudaFuncSetAttribute(arrow_svd_kernel<136, true, kArrowClusterWide>,
+                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+            cudaFuncSetAttribute(arrow_svd_kernel<kN, true, kArrowClusterWide>,
+                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+            cudaOccupancyMaxActiveClusters(&nclusters, arrow_svd_kernel<kN, true, kArrowClusterWide>,
+                                           &qc) == cudaSuccess &&
+            nclusters >= 1)
+          wide_ok = 1;
+        cudaGetLastError();
+      }
+      wide16 = wide_ok == 1;
+    }
     const int clsz = wide16 ? kArrowClusterWide : kArrowCluster;
     cfg.gridDim = dim3(batch * clsz);
     cfg.blockDim = dim3(512);
@@ -1278,14 +1307,6 @@ int launch_arrow_svd(int batch, int s, const double* core, int64_t core_stride, 
     cfg.numAttrs = 2;
     cudaError_t e;
     if (wide16) {
-      static bool attr16 = false;
-      if (!attr16) {
-        ISVD_CUDA(cudaFuncSetAttribute(arrow_svd_kernel<136, true, kArrowClusterWide>,
-                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        ISVD_CUDA(cudaFuncSetAttribute(arrow_svd_kernel<kN, true, kArrowClusterWide>,
-                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        attr16 = true;
-      }
       if (s <= 136)
         e = cudaLaunchKernelEx(&cfg, arrow_svd_kernel<136, true, kArrowClusterWide>, s, core,
                                core_stride, ldcore, uk, vk, out_stride, ldo, sv, sv_stride, s_out, s_out_stride, nkeep, g_gate, ArrowFuse{});
