@@ -232,6 +232,75 @@ def _run_batched(eng, ticks):
             eng.rank_one_update(tk[1], tk[2], tk[3])
 
 
+@pytest.mark.parametrize("n,k,B", [(7, 3, 1), (33, 8, 1), (100, 12, 1), (255, 20, 1), (256, 24, 1),
+                                    (64, 31, 1), (50, 5, 70), (200, 17, 70), (256, 32, 66)])
+def test_row_append_projection_shapes(n, k, B):
+    """The narrow-stream projection kernel (project_append32_kernel<LD>, every
+    factor pitch 8 / 16 / 24 / 32; B >= 64 turns the deferred right basis on:
+    appended residuals Z and the small G) over ragged widths, mixed with
+    rank-1 updates so G is not the identity: factors, tracked matrix and N
+    against the oracle engine of each stream (_kernels.pyx:135-157)."""
+    rng = np.random.default_rng(1000 * n + k)
+    m0, T = max(k + 3, 24), 21
+    x0 = rng.standard_normal((B, m0, min(k, n))) @ rng.standard_normal((B, min(k, n), n))
+    a0 = x0 + 0.05 * rng.standard_normal((B, m0, n))
+    eng = BatchedSvdEngine(a0, k, m_cap=m0 + T)
+    streams = [[] for _ in range(B)]
+    for t in range(T):
+        if t % 3 == 2:
+            i = rng.integers(0, eng.shape[0], B)
+            j = rng.integers(0, n, B)
+            d = 0.1 * rng.standard_normal(B)
+            eng.rank_one_update(i, j, d)
+            for b in range(B):
+                streams[b].append(("r1", int(i[b]), int(j[b]), float(d[b])))
+        else:
+            rows = rng.standard_normal((B, n))
+            if t == 7:
+                rows[0] = 0.0  # a zero row: rho <= tol branch
+            eng.row_append(rows)
+            for b in range(B):
+                streams[b].append(("row", rows[b].copy()))
+    sq, _, _ = eng.scalars()
+    for b in sorted({0, B // 2, B - 1}):
+        oe = _oracle_stream(a0[b], streams[b], k)
+        f = eng.factors(b)
+        assert rel_err(f.s, oe.factors.s) < SIGMA_RTOL, (b, f.s, oe.factors.s)
+        live = oe.factors.s > 1e-9 * oe.factors.s[0]
+        assert sine_angle(f.u[:, live], oe.factors.u[:, live]) < ANGLE_TOL, b
+        assert sine_angle(f.vt.T[:, live], oe.factors.vt.T[:, live]) < ANGLE_TOL, b
+        assert np.array_equal(eng.tracked(b), oe.tracked), b
+        assert abs(sq[b] - oe.sq_norm) <= 1e-12 * oe.sq_norm, b
+
+
+@pytest.mark.parametrize("n,k", [(130, 128), (520, 40), (1000, 100), (1024, 128), (700, 130)])
+def test_wide_single_stream_row_appends(n, k):
+    """Few streams with wide factors (config 5b's shape class): the cluster
+    projection (register-resident slices of <= 64 rows per CTA for k <= 128,
+    the general cluster kernel above), the 16-CTA / 8-CTA cluster secular
+    solver and the column-split rotation, against the oracle engine."""
+    rng = np.random.default_rng(n + k)
+    m0 = k + 12
+    a0 = rng.standard_normal((m0, k)) @ rng.standard_normal((k, n)) + 1e-3 * rng.standard_normal((m0, n))
+    eng, oe = SvdEngine(a0, k), OracleEngine(a0, k)
+    for t in range(7):
+        if t == 3:
+            i, j, d = int(rng.integers(m0)), int(rng.integers(n)), float(rng.normal(0, 0.1))
+            eng.rank_one_update(i, j, d)
+            oe.rank_one_update(i, j, d)
+        else:
+            x = rng.standard_normal(k) @ a0[:k] + 1e-3 * rng.standard_normal(n)
+            eng.row_append(x)
+            oe.row_append(x)
+    f, g = eng.factors, oe.factors
+    assert rel_err(f.s, g.s) < SIGMA_RTOL
+    live = g.s > 1e-6 * g.s[0]
+    assert sine_angle(f.u[:, live], g.u[:, live]) < ANGLE_TOL
+    assert sine_angle(f.vt.T[:, live], g.vt.T[:, live]) < ANGLE_TOL
+    assert np.array_equal(eng.tracked, oe.tracked)
+    assert abs(eng.sq_norm - oe.sq_norm) <= 1e-12 * oe.sq_norm
+
+
 def test_cfg5a_batched_matches_oracle():
     """8 streams, 64 interleaved events each, through the batched engine vs
     one oracle engine per stream."""
