@@ -591,46 +591,82 @@ __device__ __forceinline__ void arrow_body(int b, int n, const double* __restric
   for (int w = 0; w < (int)(blockDim.x >> 5); ++w) smax = fmax(smax, wmax[w]);
 
   // ---- vectors, written straight into their sorted columns
-  if (WIDE && ND == 0 && S.nrot == 0) {
-    const int lane = tid & 31, nwarp = (blockDim.x >> 5) * CL;
-    for (int t = crank * (blockDim.x >> 5) + (tid >> 5); t < n; t += nwarp) {
-      const int pc = S.pos[t];
-      const double dorg = S.kd[S.org[t]];
-      const double mu = S.mu[t];
-      double nv = 0.0, nu = 0.0;
-      double vjs[kPL], djs[kPL];  // the lane's entries, kept for the write pass
+  bool wide_done = false;
+  if constexpr (WIDE) {
+    if (ND == 0 && S.nrot == 0) {
+      // One warp per vector.  A warp's column goes through shared memory so
+      // that the CTA's (up to) 16 columns -- contiguous output columns when the
+      // roots are in order -- leave as 128-byte row segments: written lane by
+      // lane, every store instruction touched 32 different rows and the
+      // uncoalesced stores were two thirds of this phase (4.5 K of 7 K cycles).
+      wide_done = true;
+      constexpr int kVW = 16;                 // warps per CTA (512 threads)
+      __shared__ double vst[kN][kVW + 1];     // [row][warp]: V's columns, then U's
+      __shared__ int vpc[kVW];                // output column per warp, -1: none
+      const int lane = tid & 31, warp = tid >> 5, nwarp = kVW * CL;
+      for (int base = crank * kVW; base < n; base += nwarp) {
+        const int t = base + warp;
+        const bool have = t < n;
+        double vjs[kPL], djs[kPL];  // the lane's entries, kept for the write passes
+        double iv = 0.0, iu = 0.0;
+        bool dead = true;
+        if (have) {
+          const double dorg = S.kd[S.org[t]];
+          const double mu = S.mu[t];
+          double nv = 0.0, nu = 0.0;
 #pragma unroll
-      for (int ip = 0; ip < kPL; ++ip) {
-        const int j = lane + 32 * ip;
-        double vj = 0.0, dj = 0.0;
-        if (j < N) {
-          dj = S.kd[j];
-          vj = S.zhat[j] * frcp((dj - dorg) * (dj + dorg) - mu);
+          for (int ip = 0; ip < kPL; ++ip) {
+            const int j = lane + 32 * ip;
+            double vj = 0.0, dj = 0.0;
+            if (j < N) {
+              dj = S.kd[j];
+              vj = S.zhat[j] * frcp((dj - dorg) * (dj + dorg) - mu);
+            }
+            vjs[ip] = vj;
+            djs[ip] = dj;
+            nv = fma(vj, vj, nv);
+            nu = fma(dj * vj, dj * vj, nu);
+          }
+          nv = warp_sum(nv);
+          nu = 1.0 + warp_sum(nu);  // the z-row entry of u is -1
+          iv = rsqrt(nv);
+          iu = rsqrt(nu);
+          const double sg = S.sig[t];
+          dead = !(sg > 0.0) || sg < kZeroSvRtol * smax;
+          if (lane == 0) {
+            vpc[warp] = S.pos[t];
+            put_sv(S.pos[t], dead ? 0.0 : sg * scale);
+          }
+        } else if (lane == 0) {
+          vpc[warp] = -1;
         }
-        vjs[ip] = vj;
-        djs[ip] = dj;
-        nv = fma(vj, vj, nv);
-        nu = fma(dj * vj, dj * vj, nu);
-      }
-      nv = warp_sum(nv);
-      nu = 1.0 + warp_sum(nu);  // the z-row entry of u is -1
-      const double iv = rsqrt(nv), iu = rsqrt(nu);
-      const double sg = S.sig[t];
-      const bool dead = !(sg > 0.0) || sg < kZeroSvRtol * smax;
+        // (every row 0 .. n-1 is some pole's row: no deflation here)
+        for (int pass = 0; pass < 2; ++pass) {
+          if (have) {
 #pragma unroll
-      for (int ip = 0; ip < kPL; ++ip) {
-        const int j = lane + 32 * ip;
-        if (j < N) {
-          const int row = S.kcol[j];
-          V[row * ldo + pc] = vjs[ip] * iv;
-          if (row != r) U[row * ldo + pc] = dead ? 0.0 : djs[ip] * vjs[ip] * iu;
+            for (int ip = 0; ip < kPL; ++ip) {
+              const int j = lane + 32 * ip;
+              if (j < N) {
+                const int row = S.kcol[j];
+                if (pass == 0) vst[row][warp] = vjs[ip] * iv;
+                else if (row != r) vst[row][warp] = dead ? 0.0 : djs[ip] * vjs[ip] * iu;
+              }
+            }
+            if (pass == 1 && lane == 0) vst[r][warp] = dead ? 0.0 : -iu;
+          }
+          __syncthreads();
+          double* X = pass == 0 ? V : U;
+          for (int idx = tid; idx < n * kVW; idx += blockDim.x) {
+            const int row = idx / kVW, w = idx % kVW;
+            const int pc = vpc[w];
+            if (pc >= 0) X[row * ldo + pc] = vst[row][w];
+          }
+          __syncthreads();
         }
-      }
-      if (lane == 0) {
-        U[r * ldo + pc] = dead ? 0.0 : -iu;
-        put_sv(pc, dead ? 0.0 : sg * scale);
       }
     }
+  }
+  if (wide_done) {
   } else if (ND == 0 && S.nrot == 0) {
     // common case (no deflation): every row of both columns is written once
     for (int t = tid; t < n; t += blockDim.x) {
