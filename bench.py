@@ -455,16 +455,19 @@ def run_cfg5b(torch, dev, lib, warm, world=1, rank=0):
     h_rows = torch.empty((T5B, N5B), dtype=torch.float64, pin_memory=True)
     h_rows.copy_(rows)
     hr = h_rows.numpy()
-    res = torch.empty((2, 3), dtype=torch.float64, pin_memory=True)
+    res = torch.empty((RES_SLOTS, 3), dtype=torch.float64, pin_memory=True)
     eng.restore()
     barrier()
     t0 = time.perf_counter()
     for t in range(warm, T5B):
         eng.row_append(hr[t:t + 1])
-        eng.scalars_async(res[t % 2].numpy(), t % 2)  # step result, read with one step of lag
-        if t > warm:
-            eng.scalars_wait((t - 1) % 2)
-    eng.scalars_wait((T5B - 1) % 2)
+        # step result, read E2E_LAG steps behind its issue (as the 5a leg); every
+        # result is read inside the timed region
+        eng.scalars_async(res[t % RES_SLOTS].numpy(), t % RES_SLOTS)
+        if t - warm >= E2E_LAG:
+            eng.scalars_wait((t - E2E_LAG) % RES_SLOTS)
+    for t in range(max(warm, T5B - E2E_LAG), T5B):
+        eng.scalars_wait(t % RES_SLOTS)
     eng.flush()
     eng.synchronize()
     e2e_s = max_over_ranks(time.perf_counter() - t0, device=dev)
@@ -489,7 +492,8 @@ def run_cfg5b(torch, dev, lib, warm, world=1, rank=0):
                    "rows_per_gpu": ml, "deferred_u_rows": window},
         "gpu_launches": int(launches),
         "e2e": {"value": steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": N5B * 8,
-                "d2h_bytes_per_step": 3 * 8, "steps": steps},
+                "d2h_bytes_per_step": 3 * 8, "steps": steps,
+                "result_readback_lag_steps": E2E_LAG},
         "roofline": {"kernel": "rotate U flush (K3, deferred, DMMA)", "bound": "tensor",
                      "achieved": flush_flops / (flush_ms / 1e3) / 1e12 if flush_ms else None,
                      "peak": DMMA_PEAK_TFS, "unit": "TFLOP/s",
