@@ -828,7 +828,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=512)
     ap.add_argument("--diag-steps", type=int, default=256)
     ap.add_argument("--cpu-streams", type=int, default=64)
-    ap.add_argument("--cpu-events", type=int, default=128)
+    ap.add_argument("--cpu-events", type=int, default=EVENTS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-k128", action="store_true", help="skip the config-5b (k=128) leg")
     ap.add_argument("--window", type=int, default=0,
