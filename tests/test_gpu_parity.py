@@ -549,6 +549,54 @@ def test_snapshot_restore_and_groups_reproduce():
         assert sine_angle(outs[0][idx].u, oe.factors.u) < ANGLE_TOL
 
 
+def test_benchmark_shape_ticks_are_bitwise_reproducible():
+    """Config-5a-shaped ticks (1024 x 256, k = 32: the narrow-stream
+    projection, the CTA-per-core kernels with their fused rotations, V
+    materialisations and a U flush) replayed from a snapshot: every stream's
+    factors, tracked norm and residuals must come out bit for bit the same
+    (a race in any of the tick kernels shows up as a differing bit; the pool
+    does not allow compute-sanitizer)."""
+    B, T = 128, 100
+    a0, ticks, _ = workloads.cfg5a_batch(9, B, n_events=T)
+    eng = BatchedSvdEngine(a0, 32, m_cap=1024 + T // 2 + 1, k_cap=32)
+    del a0
+    eng.snapshot()
+    outs = []
+    for rep in range(2):
+        if rep:
+            eng.restore()
+        _run_batched(eng, ticks)
+        eng.flush()
+        outs.append(([eng.factors(b) for b in range(0, B, 7)], [np.array(v) for v in eng.scalars()]))
+    for fa, fb in zip(outs[0][0], outs[1][0]):
+        assert np.array_equal(fa.s, fb.s) and np.array_equal(fa.u, fb.u) and np.array_equal(fa.vt, fb.vt)
+    for va, vb in zip(outs[0][1], outs[1][1]):
+        assert np.array_equal(va, vb)
+
+
+def test_wide_stream_ticks_are_bitwise_reproducible():
+    """The same check on a config-5b-shaped stream (1024 columns, k = 128):
+    cluster projection, cluster secular solver with staged vector stores,
+    column-split rotation."""
+    rng = np.random.default_rng(5)
+    m0, n, k, T = 4096, 1024, 128, 12
+    y = rng.standard_normal((n, k))
+    a0 = rng.standard_normal((m0, k)) @ y.T + 1e-3 * rng.standard_normal((m0, n))
+    rows = rng.standard_normal((T, k)) @ y.T
+    eng = BatchedSvdEngine(a0[None], k, m_cap=m0 + T + 1, k_cap=k)
+    eng.snapshot()
+    outs = []
+    for rep in range(2):
+        if rep:
+            eng.restore()
+        for t in range(T):
+            eng.row_append(rows[t:t + 1])
+        eng.flush()
+        outs.append(eng.factors(0))
+    fa, fb = outs
+    assert np.array_equal(fa.s, fb.s) and np.array_equal(fa.u, fb.u) and np.array_equal(fa.vt, fb.vt)
+
+
 @pytest.mark.parametrize("kappa", [99.0, 101.0, 5e3])
 def test_rank_one_orthogonality_near_the_structure_gate(kappa):
     """Long rank-1 streams whose spectrum sits just inside (99) and just
